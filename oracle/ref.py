@@ -1,0 +1,221 @@
+"""ctypes binding of oracle/_ref/libfcsref.so -- TEST INFRASTRUCTURE ONLY.
+
+The library is the UNMODIFIED reference (/root/reference/proj/src) compiled by
+oracle/Makefile against the shims in oracle/shims, plus oracle/ref_export.cpp.
+It is built in this container (where /root/reference exists) and travels to
+the GPU box inside the gpurun snapshot; nothing here reads /root/reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_ref", "libfcsref.so")
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(LIB_PATH)
+        dp = C.POINTER(C.c_double)
+        ip = C.POINTER(C.c_int)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_last_error.argtypes = [ip]
+        L.ref_blend_matrix.argtypes = [C.c_int, dp]
+        L.ref_fc_info.argtypes = [C.c_int, C.c_int, ip, dp, dp, dp]
+        L.ref_fc_apply.argtypes = [C.c_int, C.c_int, C.c_int, dp, C.c_long, C.c_int, C.c_int, dp, C.c_int]
+        L.ref_fc_evaluate.argtypes = [C.c_int, C.c_int, dp, C.c_int, dp, dp]
+        L.ref_train_classifier.argtypes = [C.c_char_p, dp]
+        L.ref_mlp_forward.argtypes = [C.c_char_p, C.c_int, dp, dp, ip]
+        L.ref_classify_line.argtypes = [C.c_char_p, C.c_int, dp, ip]
+        L.ref_engine_rect.restype = C.c_void_p
+        L.ref_engine_rect.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                                      C.c_int, C.c_int, ip, dp, dp, C.c_double, C.c_double, C.c_int,
+                                      C.c_char_p, C.c_long]
+        L.ref_engine_destroy.argtypes = [C.c_void_p]
+        L.ref_engine_nsubs.argtypes = [C.c_void_p]
+        L.ref_engine_dims.argtypes = [C.c_void_p, C.c_int, ip, ip]
+        L.ref_engine_get.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int, dp]
+        L.ref_engine_set.argtypes = [C.c_void_p, C.c_int, C.c_char_p, C.c_int, dp]
+        L.ref_engine_finish_ic.argtypes = [C.c_void_p]
+        L.ref_engine_phase.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.ref_engine_dt.argtypes = [C.c_void_p, dp]
+        L.ref_engine_set_dt.argtypes = [C.c_void_p, C.c_double]
+        L.ref_engine_advance.argtypes = [C.c_void_p]
+        L.ref_engine_time.argtypes = [C.c_void_p, dp, C.POINTER(C.c_long)]
+        L.ref_engine_run.argtypes = [C.c_void_p, dp, C.POINTER(C.c_long), dp]
+        L.ref_engine_set_max_steps.argtypes = [C.c_void_p, C.c_long]
+        _lib = L
+    return _lib
+
+
+class RefError(RuntimeError):
+    def __init__(self, kind, msg):
+        super().__init__(msg)
+        self.kind = kind
+
+
+def _check(rc):
+    if rc != 0:
+        k = C.c_int()
+        msg = lib().ref_last_error(C.byref(k)).decode()
+        raise RefError(k.value, msg)
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def blend_matrix(n_cont=25):
+    out = np.zeros((n_cont - 1) * 3)
+    _check(lib().ref_blend_matrix(n_cont, _dp(out)))
+    return out.reshape(n_cont - 1, 3)
+
+
+def fc_info(n, n_cont=25):
+    ne = C.c_int()
+    per = C.c_double()
+    nm = (n + n_cont - 1) // 2 + 1
+    fp = np.zeros(nm)
+    sp = np.zeros(nm)
+    _check(lib().ref_fc_info(n, n_cont, C.byref(ne), C.byref(per), _dp(fp), _dp(sp)))
+    return ne.value, per.value, fp, sp
+
+
+MODE = {"d1": 1, "d2": 2, "filter": 3, "smear": 4, "cont": 5}
+
+
+def fc_apply(lines, mode="d1", n_cont=25, threads=1):
+    """lines: (L, n) C-contiguous; unit-span operator per line."""
+    lines = np.ascontiguousarray(lines, dtype=np.float64)
+    L, n = lines.shape
+    if mode == "cont":
+        out = np.zeros((L, n_cont - 1))
+    else:
+        out = np.zeros_like(lines)
+    _check(lib().ref_fc_apply(n, n_cont, MODE[mode], _dp(lines), n, 1, L, _dp(out), threads))
+    return out
+
+
+def fc_evaluate(values, xs, n_cont=25):
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    out = np.zeros_like(xs)
+    _check(lib().ref_fc_evaluate(len(values), n_cont, _dp(values), len(xs), _dp(xs), _dp(out)))
+    return out
+
+
+def train_classifier(path):
+    acc = C.c_double()
+    _check(lib().ref_train_classifier(path.encode(), C.byref(acc)))
+    return acc.value
+
+
+def mlp_forward(path, x7):
+    x7 = np.ascontiguousarray(x7, dtype=np.float64).reshape(-1, 7)
+    n = x7.shape[0]
+    logits = np.zeros((n, 4))
+    cls = np.zeros(n, dtype=np.int32)
+    _check(lib().ref_mlp_forward(path.encode(), n, _dp(x7), _dp(logits),
+                                 cls.ctypes.data_as(C.POINTER(C.c_int))))
+    return logits, cls
+
+
+def classify_line(path, values):
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    tau = np.zeros(len(values), dtype=np.int32)
+    _check(lib().ref_classify_line(path.encode(), len(values), _dp(values),
+                                   tau.ctypes.data_as(C.POINTER(C.c_int))))
+    return tau
+
+
+class RefEngine:
+    """Engine over one rectangular I patch (ref_engine_rect)."""
+
+    def __init__(self, x0, y0, lx, ly, r, s, n0, nv, side_kinds, side_states=None,
+                 side_pressure=None, cfl=0.5, T=1e300, workers=1, weight_path="", max_steps=10**9):
+        kinds = np.ascontiguousarray(side_kinds, dtype=np.int32)
+        states = np.zeros(16) if side_states is None else np.ascontiguousarray(side_states, dtype=np.float64).ravel()
+        press = np.ones(4) if side_pressure is None else np.ascontiguousarray(side_pressure, dtype=np.float64)
+        h = lib().ref_engine_rect(x0, y0, lx, ly, r, s, n0, nv,
+                                  kinds.ctypes.data_as(C.POINTER(C.c_int)), _dp(states), _dp(press),
+                                  cfl, T, workers, weight_path.encode(), max_steps)
+        if not h:
+            _check(9)
+        self.h = h
+        self.nsubs = lib().ref_engine_nsubs(h)
+        self.dims = []
+        for k in range(self.nsubs):
+            a, b = C.c_int(), C.c_int()
+            _check(lib().ref_engine_dims(h, k, C.byref(a), C.byref(b)))
+            self.dims.append((a.value, b.value))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().ref_engine_destroy(self.h)
+            self.h = None
+
+    def get(self, sub, what, comp=0):
+        ni, nj = self.dims[sub]
+        out = np.zeros((nj, ni))
+        _check(lib().ref_engine_get(self.h, sub, what.encode(), comp, _dp(out)))
+        return out
+
+    def get_state(self, sub, what="e"):
+        return np.stack([self.get(sub, what, c) for c in range(4)])
+
+    def set(self, sub, what, arr, comp=0):
+        arr = np.ascontiguousarray(arr, dtype=np.float64)
+        _check(lib().ref_engine_set(self.h, sub, what.encode(), comp, _dp(arr)))
+
+    def set_state(self, sub, e):
+        for c in range(4):
+            self.set(sub, "e", e[c], c)
+
+    def finish_ic(self):
+        _check(lib().ref_engine_finish_ic(self.h))
+
+    def phase(self, phase, stage=0):
+        _check(lib().ref_engine_phase(self.h, phase, stage))
+
+    def reduce_dt(self):
+        dt = C.c_double()
+        _check(lib().ref_engine_dt(self.h, C.byref(dt)))
+        return dt.value
+
+    def advance(self):
+        _check(lib().ref_engine_advance(self.h))
+
+    def step(self):
+        """One superstep in the order of Engine::run (src/runtime.cpp:486-511)."""
+        self.phase(0)
+        self.phase(1)
+        self.phase(2)
+        self.reduce_dt()
+        for s in range(5):
+            self.phase(3, s)
+            self.phase(6)
+        self.advance()
+
+    def time(self):
+        t = C.c_double()
+        st = C.c_long()
+        lib().ref_engine_time(self.h, C.byref(t), C.byref(st))
+        return t.value, st.value
+
+    def run(self, steps):
+        lib().ref_engine_set_max_steps(self.h, steps)
+        w = C.c_double()
+        n = C.c_long()
+        t = C.c_double()
+        _check(lib().ref_engine_run(self.h, C.byref(w), C.byref(n), C.byref(t)))
+        return w.value, n.value, t.value
