@@ -1,0 +1,182 @@
+/*
+ * fcsg -- B200-native FC-SDNN time step, C ABI.
+ *
+ * Plain C: pointers, sizes and int status codes; no exception crosses this
+ * boundary and no torch or CUDA type appears in a signature (streams are
+ * passed as void*). A context is bound to one CUDA device and is used from
+ * one host thread. Every call returns FCSG_OK or one of the error kinds
+ * below; fcsg_last_error() describes the last failure of that context. The
+ * kinds map one-to-one onto the reference's exception types
+ * (include/fcs/errors.hpp:10-43) so a C++ or Python wrapper can rethrow
+ * ConfigError / UsageError / DecompositionError / InvalidStateError.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to the reference's proj/ directory).
+ */
+#ifndef FCSG_H
+#define FCSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    FCSG_OK = 0,
+    FCSG_CONFIG = 1,          /* fcs::ConfigError        */
+    FCSG_USAGE = 2,           /* fcs::UsageError         */
+    FCSG_GEOMETRY = 3,        /* fcs::GeometryError      */
+    FCSG_DECOMPOSITION = 4,   /* fcs::DecompositionError */
+    FCSG_INVALID_STATE = 5,   /* fcs::InvalidStateError  */
+    FCSG_CUDA_ERROR = 8,
+    FCSG_OTHER = 9
+};
+
+/* line-operator modes: FcOperator::derivative(order 1|2), filter, strong_filter */
+enum { FCSG_D1 = 1, FCSG_D2 = 2, FCSG_FILTER = 3, FCSG_SMEAR = 4 };
+
+typedef struct fcsg_ctx fcsg_ctx;
+
+/* ---- context ----------------------------------------------------------- */
+int fcsg_create(int device, fcsg_ctx** out);
+int fcsg_destroy(fcsg_ctx* ctx);
+/* Last error of this context. i/j are global lattice indices, as
+ * InvalidStateError{patch, subpatch, i, j, t} (include/fcs/errors.hpp:32-39). */
+int fcsg_last_error(fcsg_ctx* ctx, char* msg, int msg_len, int* kind, int* patch, int* subpatch,
+                    int* i, int* j, double* t);
+/* 1 if this build runs on a CUDA device, 0 for the CPU emulation harness. */
+int fcsg_is_cuda_build(void);
+int fcsg_synchronize(fcsg_ctx* ctx);
+
+/* device memory helpers for callers that do not own an allocator */
+int fcsg_device_alloc(fcsg_ctx* ctx, size_t bytes, void** ptr);
+int fcsg_device_free(fcsg_ctx* ctx, void* ptr);
+int fcsg_memcpy_h2d(fcsg_ctx* ctx, void* dst, const void* src, size_t bytes);
+int fcsg_memcpy_d2h(fcsg_ctx* ctx, void* dst, const void* src, size_t bytes);
+
+/* ---- FC operator --------------------------------------------------------
+ * Replaces fcs::fc::OperatorCache::get(n_points, n_cont, FilterSpec)
+ * (include/fcs/fc_core.hpp:96-105, src/fc_core.cpp:391-402) and the
+ * FcOperator constructor (src/fc_core.cpp:190-217). degree = 2 is the
+ * reference operator (FcOperator::degree, include/fcs/fc_core.hpp:35); other
+ * degrees are the generalised Gram basis. Same key -> same op_id.
+ * Errors: FCSG_CONFIG for n_points < 10, n_cont < 4, a failed blend fit. */
+int fcsg_operator(fcsg_ctx* ctx, int n_points, int n_cont, int degree, double alpha, int p,
+                  int p_smear, int* op_id);
+/* Sizes and tables of an operator: FcOperator::n_ext/n_modes/period/
+ * filter_profile/smear_profile/blend_matrix (include/fcs/fc_core.hpp:42-74).
+ * Output arrays may be NULL; blend is (n_cont-1) x (degree+1) row-major,
+ * profiles have n_modes entries. */
+int fcsg_operator_info(fcsg_ctx* ctx, int op_id, int* n_ext, int* n_modes, double* period,
+                       double* blend, double* filter_profile, double* smear_profile);
+
+/* Batched line operator on DEVICE buffers. Line l, element i is read at
+ * in[l*in_line_stride + i*in_stride] and written, times `scale`, at
+ * out[l*out_line_stride + i*out_stride]; in == out is allowed when the two
+ * layouts coincide. Replaces a loop of FcOperator::derivative(in, in_stride,
+ * out, out_stride, order) / filter / strong_filter (src/fc_core.cpp:257-306)
+ * and, with scale = inv_len, SubpatchData::deriv_q1/deriv_q2
+ * (src/subpatch_data.cpp:9-28). Errors: FCSG_USAGE for a bad mode (the
+ * reference's "order must be 1 or 2"). `stream` is a cudaStream_t; NULL is the
+ * default (legacy) stream, so torch's default stream orders correctly. */
+int fcsg_fc_lines(fcsg_ctx* ctx, int op_id, int mode, const double* d_in, long in_line_stride,
+                  long in_stride, double* d_out, long out_line_stride, long out_stride, long n_lines,
+                  double scale, void* stream);
+/* Same on HOST buffers (copies in and out, synchronous). */
+int fcsg_fc_lines_host(fcsg_ctx* ctx, int op_id, int mode, const double* h_in, long in_line_stride,
+                       long in_stride, double* h_out, long out_line_stride, long out_stride,
+                       long n_lines, double scale);
+
+/* ---- Engine (the FC-SDNN superstep) ---------------------------------------
+ * Replaces fcs::run::Engine's step loop (include/fcs/runtime.hpp:79-127,
+ * src/runtime.cpp:316-530) for subpatches whose init-time data
+ * (SubpatchData geometry/masks/metrics/line BCs, init_subpatch_data,
+ * src/subpatch_data.cpp:69-154; CommPlan, build_plan, src/runtime.cpp:89-274)
+ * is built by the caller and uploaded once. All subpatches of one engine
+ * share one rectangular shape ni x nj. */
+typedef struct fcsg_engine fcsg_engine;
+
+/* EngineConfig (include/fcs/runtime.hpp:59-73) fields used by the step */
+typedef struct {
+    double cfl;
+    double T;
+    int n_cont;              /* 25 */
+    double filter_alpha;     /* FilterSpec (include/fcs/fc_core.hpp:11-15) */
+    int filter_p;
+    int filter_p_smear;
+    double visc_c[4];        /* ViscosityWeights {1.5, 1, 0.25, 0} */
+    double abs_floor;        /* ClassifierConfig::abs_floor, 1e-4 */
+    int smear_radius;        /* 10 */
+    int debug_rhs;           /* keep the last stage's rhs readable (parity hooks) */
+} fcsg_engine_config;
+
+/* BcKind codes (include/fcs/bc.hpp:10-17); -1 = no boundary condition */
+enum {
+    FCSG_BC_NONE = -1,
+    FCSG_BC_INFLOW = 0,
+    FCSG_BC_OUTFLOW_PRESSURE = 1,
+    FCSG_BC_SLIP_WALL = 2,
+    FCSG_BC_NOSLIP_ADIABATIC = 3,
+    FCSG_BC_SUPERSONIC_OUTFLOW = 4,
+    FCSG_BC_ZERO_NORMAL_ALL = 5
+};
+
+int fcsg_engine_create(fcsg_ctx* ctx, const fcsg_engine_config* cfg, fcsg_engine** out);
+int fcsg_engine_destroy(fcsg_engine* eng);
+
+/* One SubpatchData: lattice origin (i0, j0) of patch `patch` (for error
+ * reports), shape, parameter spacings h1/h2 (LineInfo::inv_len =
+ * 1/((n-1) h)), per-point mask (1 interior, 2 fringe), metrics iq1x, iq2x,
+ * iq1y, iq2y, h_min, h_max, w_norm ([nj][ni] row-major), and the resolved
+ * line-end BCs: bc_kind / bc_state[4] / bc_pressure for rows' low ends (nj),
+ * rows' high ends (nj), columns' low ends (ni), columns' high ends (ni), in
+ * that order. */
+int fcsg_engine_add_subpatch(fcsg_engine* eng, int patch, int i0, int j0, int ni, int nj, double h1, double h2,
+                             const uint8_t* mask, const double* iq1x, const double* iq2x, const double* iq1y,
+                             const double* iq2y, const double* h_min, const double* h_max, const double* w_norm,
+                             const int* bc_kind, const double* bc_state, const double* bc_pressure, int* sub_id);
+/* CommPlan copies (include/fcs/runtime.hpp:17-22): solution copies
+ * (recipient subpatch, local index) <- (donor subpatch, local index), and
+ * viscosity-blend copies with weights, applied per recipient in the given
+ * order. */
+int fcsg_engine_set_plan(fcsg_engine* eng, long n_sol, const int* sol_dst_sub, const int* sol_dst,
+                         const int* sol_src_sub, const int* sol_src, long n_visc, const int* v_dst_sub,
+                         const int* v_dst, const int* v_src_sub, const int* v_src, const double* v_w);
+/* MlpClassifier::load (src/viscosity.cpp:63-89): FCNN v1 file, 7-16-16-16-16-4 tanh */
+int fcsg_engine_load_mlp(fcsg_engine* eng, const char* path);
+int fcsg_engine_finalize(fcsg_engine* eng);
+
+/* state e = (rho, rho u, rho v, E), [4][nj][ni] (State, include/fcs/subpatch_data.hpp:15) */
+int fcsg_engine_set_state(fcsg_engine* eng, int sub, const double* e4);
+/* fields: "e","e0","e2","e3","rhs3","rhs" (comp 0..3), "mu_hat","mu","tau",
+ * "speed","proxy","m01","iq1x","iq2x","iq1y","iq2y","h_min","h_max","w_norm" */
+int fcsg_engine_get_field(fcsg_engine* eng, int sub, const char* name, int comp, double* out);
+int fcsg_engine_set_field(fcsg_engine* eng, int sub, const char* name, int comp, const double* in);
+/* apply_ic tail: enforce_bc on every subpatch, then one fringe exchange (src/runtime.cpp:284-286) */
+int fcsg_engine_finish_ic(fcsg_engine* eng);
+/* Engine::step_phase(phase, stage) for phase 0 (viscosity), 1 (blend),
+ * 2 (filter/smear + E + BC), 3 (RHS + SSPRK stage + BC), 6 (exchange) */
+int fcsg_engine_phase(fcsg_engine* eng, int phase, int stage);
+/* dt = cfl min dt_local, clipped at T (src/runtime.cpp:492-497) */
+int fcsg_engine_reduce_dt(fcsg_engine* eng, double* dt);
+/* t += dt, step += 1 (src/runtime.cpp:505-507) */
+int fcsg_engine_advance(fcsg_engine* eng);
+/* n complete supersteps (Engine::run body, src/runtime.cpp:482-511); steady
+ * steps replay one CUDA graph. Stops when t >= T - 1e-15. *done = steps run.
+ * Errors: FCSG_INVALID_STATE with fcsg_last_error's patch/subpatch/i/j/t. */
+int fcsg_engine_run(fcsg_engine* eng, long n, int use_graph, long* done);
+/* enqueue n supersteps on `stream`-ordered engine work without any host
+ * synchronisation (benchmark path; errors surface at the next sync). */
+int fcsg_engine_enqueue(fcsg_engine* eng, long n);
+int fcsg_engine_time(fcsg_engine* eng, double* t, long* steps);
+int fcsg_engine_total_points(fcsg_engine* eng, long* n);
+/* the engine's CUDA stream (cudaStream_t), for event timing by the caller */
+int fcsg_engine_stream(fcsg_engine* eng, void** stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,96 @@
+#include "dev.h"
+
+#include <cstdlib>
+#include <cstring>
+
+#include "fc_tables.h"
+#include "fcsg_common.h"
+
+namespace fcsg {
+namespace dev {
+
+#if FCSG_CUDA
+
+namespace {
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(kCuda, std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+bool is_cuda() { return true; }
+void set_device(int device) { ck(cudaSetDevice(device), "cudaSetDevice"); }
+void* create_stream() {
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    return s;
+}
+void destroy_stream(void* s) { cudaStreamDestroy(static_cast<cudaStream_t>(s)); }
+void* alloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    ck(cudaMalloc(&p, bytes), "cudaMalloc");
+    return p;
+}
+void free(void* p) {
+    if (p) cudaFree(p);
+}
+void h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)), "h2d");
+    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "h2d sync");
+}
+void d2h(void* dst, const void* src, size_t bytes, void* stream) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)), "d2h");
+    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "d2h sync");
+}
+void d2d(void* dst, const void* src, size_t bytes, void* stream) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)), "d2d");
+}
+void memset0(void* p, size_t bytes, void* stream) {
+    ck(cudaMemsetAsync(p, 0, bytes, static_cast<cudaStream_t>(stream)), "memset");
+}
+void sync(void* stream) { ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "stream sync"); }
+void sync_device() { ck(cudaDeviceSynchronize(), "device sync"); }
+void check(const char* what) { ck(cudaGetLastError(), what); }
+void graph_begin(void* stream) {
+    ck(cudaStreamBeginCapture(static_cast<cudaStream_t>(stream), cudaStreamCaptureModeThreadLocal), "capture");
+}
+void graph_end(void* stream, void** graph, void** exec) {
+    cudaGraph_t g;
+    ck(cudaStreamEndCapture(static_cast<cudaStream_t>(stream), &g), "end capture");
+    cudaGraphExec_t x;
+    ck(cudaGraphInstantiate(&x, g, 0), "graph instantiate");
+    *graph = g;
+    *exec = x;
+}
+void graph_launch(void* exec, void* stream) {
+    ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(exec), static_cast<cudaStream_t>(stream)), "graph launch");
+}
+void graph_destroy(void* exec, void* graph) {
+    if (exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec));
+    if (graph) cudaGraphDestroy(static_cast<cudaGraph_t>(graph));
+}
+
+#else
+
+bool is_cuda() { return false; }
+void set_device(int) {}
+void* create_stream() { return nullptr; }
+void destroy_stream(void*) {}
+void* alloc(size_t bytes) { return std::calloc(bytes ? bytes : 16, 1); }
+void free(void* p) { std::free(p); }
+void h2d(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }
+void d2h(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }
+void d2d(void* dst, const void* src, size_t bytes, void*) { std::memmove(dst, src, bytes); }
+void memset0(void* p, size_t bytes, void*) { std::memset(p, 0, bytes); }
+void sync(void*) {}
+void sync_device() {}
+void check(const char*) {}
+void graph_begin(void*) {}
+void graph_end(void*, void**, void**) {}
+void graph_launch(void*, void*) {}
+void graph_destroy(void*, void*) {}
+
+#endif
+
+}  // namespace dev
+}  // namespace fcsg

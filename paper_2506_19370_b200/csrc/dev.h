@@ -1,0 +1,38 @@
+// Thin device-memory layer. The nvcc build (libfcsg.so) uses the CUDA
+// runtime; the FCSG_EMULATE build used only by the CPU unit tests maps the
+// same calls onto host memory.
+#pragma once
+
+#include <cstddef>
+#include <string>
+
+namespace fcsg {
+namespace dev {
+
+void set_device(int device);
+void* create_stream();
+void destroy_stream(void* s);
+void* alloc(size_t bytes);
+void free(void* p);
+void h2d(void* dst, const void* src, size_t bytes, void* stream);
+void d2h(void* dst, const void* src, size_t bytes, void* stream);
+void d2d(void* dst, const void* src, size_t bytes, void* stream);
+void memset0(void* p, size_t bytes, void* stream);
+void sync(void* stream);
+void sync_device();
+// throws Error(kCuda) if the last launch failed
+void check(const char* what);
+bool is_cuda();
+// CUDA graph capture of everything enqueued on `stream` between begin and end
+void graph_begin(void* stream);
+void graph_end(void* stream, void** graph, void** exec);
+void graph_launch(void* exec, void* stream);
+void graph_destroy(void* exec, void* graph);
+
+template <class T>
+T* alloc_n(size_t n) {
+    return static_cast<T*>(alloc(n * sizeof(T)));
+}
+
+}  // namespace dev
+}  // namespace fcsg

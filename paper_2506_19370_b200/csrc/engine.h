@@ -1,0 +1,107 @@
+// Host Engine: the drop-in for fcs::run::Engine's step loop
+// (include/fcs/runtime.hpp:79-127, src/runtime.cpp:316-530) over device-
+// resident subpatch data. Geometry, masks, metrics, windows and the exchange
+// plan are built at init time by the caller (the reference's
+// init_subpatch_data / build_plan equivalents) and uploaded once.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "context.h"
+#include "fc_tables.h"
+#include "step_kernels.h"
+
+namespace fcsg {
+
+// InvalidStateError{patch, subpatch, i, j, t} (include/fcs/errors.hpp:32-39)
+struct StateError : Error {
+    int patch, sub, i, j;
+    double t;
+    StateError(const std::string& m, int patch_, int sub_, int i_, int j_, double t_)
+        : Error(kInvalidState, m), patch(patch_), sub(sub_), i(i_), j(j_), t(t_) {}
+};
+
+// EngineConfig (include/fcs/runtime.hpp:59-73), the fields the step uses
+struct EngineConfig {
+    double cfl = 0.5;
+    double T = 1.0;
+    int n_cont = 25;
+    FilterSpec filter;
+    double visc_c[4] = {1.5, 1.0, 0.25, 0.0};  // ViscosityWeights (include/fcs/viscosity.hpp:72-74)
+    double abs_floor = 1e-4;                   // ClassifierConfig::abs_floor
+    int smear_radius = 10;
+    bool debug_rhs = false;                    // keep the last stage's rhs for parity hooks
+};
+
+struct SubSpec {
+    int patch = 0, i0 = 0, j0 = 0;
+    int ni = 0, nj = 0;
+    double h1 = 0, h2 = 0;
+    std::vector<uint8_t> mask;
+    std::vector<double> iq1x, iq2x, iq1y, iq2y, h_min, h_max, w_norm;
+    std::vector<BcDev> row_lo, row_hi, col_lo, col_hi;
+};
+
+class Engine {
+  public:
+    Engine(Ctx& ctx, const EngineConfig& cfg);
+    ~Engine();
+
+    int add_subpatch(SubSpec s);
+    // CommPlan (include/fcs/runtime.hpp:16-49), copies only: solution copies
+    // (dst_sub, dst, src_sub, src) and viscosity copies with weights.
+    void set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, std::vector<int> sol_src_sub,
+                  std::vector<int> sol_src, std::vector<int> v_dst_sub, std::vector<int> v_dst,
+                  std::vector<int> v_src_sub, std::vector<int> v_src, std::vector<double> v_w);
+    void set_mlp_packed(const std::vector<double>& w);  // kMlpWeights, per layer W then b
+    void load_mlp_file(const std::string& path);        // FCNN v1 (src/viscosity.cpp:63-89)
+    void finalize();
+
+    void set_state(int sub, const double* e4);
+    void get_field(int sub, const std::string& name, int comp, double* out);
+    void set_field(int sub, const std::string& name, int comp, const double* in);
+
+    void finish_ic();                  // enforce_bc + exchange (src/runtime.cpp:284-286)
+    void phase(int ph, int stage);     // Engine::step_phase bodies 0,1,2,3,6
+    double reduce_dt();                // worker-0 dt block (src/runtime.cpp:492-497)
+    void advance();                    // t += dt, step++ (src/runtime.cpp:505-507)
+    // n full supersteps; the steady-state step is replayed from a CUDA graph.
+    // Stops early when t >= T - 1e-15 (checked every step only if T is finite).
+    long run_steps(long n, bool use_graph);
+    void enqueue_step(bool step0);
+    // n supersteps enqueued without host synchronisation (graph replay after step 0)
+    void enqueue_steps(long n);
+    double time();
+    long steps() const { return host_step_; }
+    long total_points() const { return npts_; }
+    void check_error();
+    void* stream() const { return ctx_.stream; }
+
+  private:
+    double* field_ptr(const std::string& name, int comp);
+    Ctx& ctx_;
+    EngineConfig cfg_;
+    std::vector<SubSpec> subs_;
+    bool finalized_ = false;
+    int ni_ = 0, nj_ = 0;
+    long npts_ = 0;
+    int op_row_ = -1, op_col_ = -1;
+    LinePlans plans_{};
+    EngineDev E_{};
+    std::vector<void*> allocs_;
+    double* pool_ = nullptr;
+    std::vector<double> mlp_;
+    // plan (host staging until finalize)
+    std::vector<long> x_dst_, x_src_;
+    std::vector<int> visc_off_;
+    std::vector<long> visc_src_;
+    std::vector<double> visc_w_;
+    bool have_plan_ = false;
+    long host_step_ = 0;
+    void* graph_exec_ = nullptr;
+    void* graph_ = nullptr;
+};
+
+}  // namespace fcsg

@@ -1,0 +1,106 @@
+// Batched FC line operator: the drop-in for FcOperator::derivative / filter /
+// strong_filter (src/fc_core.cpp:257-306) applied over many lines at once.
+// One CTA owns LB complex lines = 2*LB real lines; real lines (2a, 2a+1) are
+// packed as one complex line, transformed with fc_transform (fft_line.h), and
+// unpacked. Loads/stores are coalesced along whichever axis is contiguous:
+// along the line for stride==1 (rows), across lines (one 16-byte load per
+// adjacent pair) when line_stride==1 (columns of a row-major field).
+#include "fc_lines.h"
+#include "fft_line.h"
+
+namespace fcsg {
+
+template <int LB>
+FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a) {
+    const FcPlanDev& pl = a.pl;
+    const int pitch = LB + 1;
+    double2* buf = smem;
+    double2* scr = smem + pl.n_ext * pitch;
+    const int N = pl.n;
+    const long l0 = static_cast<long>(block) * 2 * LB;
+    const long ls = a.line_stride, st = a.stride;
+    const long ols = a.out_line_stride, ost = a.out_stride;
+    const int total = N * LB;
+    const bool rows = (st == 1);
+    const bool orows = (ost == 1);
+    for (int w = t.tid; w < total; w += t.nthr) {
+        int i, c;
+        if (rows) { i = w % N; c = w / N; }
+        else { c = w % LB; i = w / LB; }
+        const long l = l0 + 2 * c;
+        double v0 = 0.0, v1 = 0.0;
+        if (l < a.n_lines) v0 = a.in[l * ls + i * st];
+        if (l + 1 < a.n_lines) v1 = a.in[(l + 1) * ls + i * st];
+        buf[i * pitch + c] = mk2(v0, v1);
+    }
+    FCSG_SYNC();
+    fc_transform(t, buf, pitch, LB, pl, a.mode, scr, a.scr_cap);
+    for (int w = t.tid; w < total; w += t.nthr) {
+        int i, c;
+        if (orows) { i = w % N; c = w / N; }
+        else { c = w % LB; i = w / LB; }
+        const long l = l0 + 2 * c;
+        const double2 v = buf[i * pitch + c];
+        if (l < a.n_lines) a.out[l * ols + i * ost] = v.x * a.scale;
+        if (l + 1 < a.n_lines) a.out[(l + 1) * ols + i * ost] = v.y * a.scale;
+    }
+}
+
+#if FCSG_CUDA
+template <int LB>
+__global__ void __launch_bounds__(256) fc_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+    extern __shared__ double2 smem[];
+    fc_lines_body<LB>(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, smem, a);
+}
+#endif
+
+size_t fc_lines_smem_bytes(const FcPlanDev& pl, int LB, int scr_cap) {
+    return (static_cast<size_t>(pl.n_ext) * (LB + 1) + scr_cap) * sizeof(double2);
+}
+
+int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {
+    int cap = 0;
+    for (int s = 0; s < pl.nstages; ++s) {
+        const int p = pl.radix[s];
+        const bool reg = p == 2 || p == 3 || p == 4 || p == 5 || p == 7 || p == 8 || p == 9 || p == 11 || p == 13;
+        if (!reg) cap = std::max(cap, p * LB * std::max(1, 256 / (p * LB)));
+    }
+    return cap;
+}
+
+void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
+    const int lines_per_block = 2 * LB;
+    const int nblk = static_cast<int>((a.n_lines + lines_per_block - 1) / lines_per_block);
+    if (nblk == 0) return;
+    a.scr_cap = fc_lines_scr_cap(a.pl, LB);
+    const size_t smem = fc_lines_smem_bytes(a.pl, LB, a.scr_cap);
+#if FCSG_CUDA
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (LB) {
+        case 4:
+            { static bool once = (cudaFuncSetAttribute(fc_lines_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true); (void)once; }
+            fc_lines_kernel<4><<<nblk, 256, smem, s>>>(a);
+            break;
+        case 8:
+            { static bool once = (cudaFuncSetAttribute(fc_lines_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true); (void)once; }
+            fc_lines_kernel<8><<<nblk, 256, smem, s>>>(a);
+            break;
+        default:
+            { static bool once = (cudaFuncSetAttribute(fc_lines_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true); (void)once; }
+            fc_lines_kernel<16><<<nblk, 256, smem, s>>>(a);
+            break;
+    }
+#else
+    (void)stream;
+    std::vector<double2> sm(smem / sizeof(double2));
+    for (int b = 0; b < nblk; ++b) {
+        switch (LB) {
+            case 4: fc_lines_body<4>(Thr{0, 1}, b, sm.data(), a); break;
+            case 8: fc_lines_body<8>(Thr{0, 1}, b, sm.data(), a); break;
+            default: fc_lines_body<16>(Thr{0, 1}, b, sm.data(), a); break;
+        }
+    }
+#endif
+}
+
+}  // namespace fcsg

@@ -1,0 +1,29 @@
+#pragma once
+
+#include <algorithm>
+#include <cstddef>
+#include <vector>
+
+#include "fcsg_common.h"
+
+namespace fcsg {
+
+struct FcLinesArgs {
+    FcPlanDev pl;
+    int mode;          // 1 d/dq, 2 d2/dq2, 3 filter, 4 smear filter
+    const double* in;  // line l, element i at in[l*line_stride + i*stride]
+    double* out;       // line l, element i at out[l*out_line_stride + i*out_stride]; in == out allowed
+    long line_stride;
+    long stride;
+    long out_line_stride;
+    long out_stride;
+    long n_lines;
+    double scale;      // multiplies every output (inv_len^order for derivatives)
+    int scr_cap;       // complex scratch slots for generic-radix stages (set by the launcher)
+};
+
+size_t fc_lines_smem_bytes(const FcPlanDev& pl, int LB, int scr_cap);
+int fc_lines_scr_cap(const FcPlanDev& pl, int LB);
+void launch_fc_lines(FcLinesArgs a, int LB, void* stream);
+
+}  // namespace fcsg

@@ -1,0 +1,98 @@
+// Common definitions shared by the sm_100a kernels and their host launchers.
+//
+// Every kernel body in this directory is written as an FCSG_HD function that
+// takes an explicit (tid, nthr) thread context and a shared-memory pointer, so
+// the identical source also compiles as plain C++ (FCSG_EMULATE) for the
+// CPU unit-test harness (tests/, libfcsg_emu.so). The product library
+// libfcsg.so is always the nvcc build; nothing in the package loads the
+// emulation build.
+#pragma once
+
+#include <cstdint>
+
+#if defined(__CUDACC__) && !defined(FCSG_EMULATE)
+// device compile of the product: kernel bodies are device code
+#include <cuda_runtime.h>
+#define FCSG_HD __device__ __forceinline__
+#define FCSG_DEV __device__ __forceinline__
+#define FCSG_SYNC() __syncthreads()
+#define FCSG_CUDA 1
+#else
+#include <cmath>
+#include <cstring>
+#define FCSG_HD inline
+#define FCSG_DEV inline
+#define FCSG_SYNC() ((void)0)
+#define FCSG_CUDA 0
+#if !defined(FCSG_EMULATE)
+#include <vector_types.h>  // host TU of the product: CUDA's double2
+#elif !defined(__CUDACC__)
+struct double2 {
+    double x, y;
+};
+#endif
+#endif
+
+namespace fcsg {
+
+// error kinds, shared with include/fcsg.h and the reference's exception types
+// (include/fcs/errors.hpp:10-43)
+enum ErrKind : int {
+    kOk = 0,
+    kConfig = 1,
+    kUsage = 2,
+    kGeometry = 3,
+    kDecomposition = 4,
+    kInvalidState = 5,
+    kCuda = 8,
+    kOther = 9,
+};
+
+// device error word: code, subpatch, i, j (first failure wins)
+struct DevError {
+    int code;  // 0 = none; 1 = nonpositive density or pressure (rhs), 2 = proxy/MWSB, 3 = nonfinite wave speed
+    int sub;
+    int i;
+    int j;
+};
+
+struct Thr {
+    int tid;
+    int nthr;
+};
+
+FCSG_HD double2 mk2(double a, double b) {
+    double2 r;
+    r.x = a;
+    r.y = b;
+    return r;
+}
+FCSG_HD double2 cadd(double2 a, double2 b) { return mk2(a.x + b.x, a.y + b.y); }
+FCSG_HD double2 csub(double2 a, double2 b) { return mk2(a.x - b.x, a.y - b.y); }
+FCSG_HD double2 cmul(double2 a, double2 b) { return mk2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+// a * conj(b)
+FCSG_HD double2 cmulc(double2 a, double2 b) { return mk2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y); }
+FCSG_HD double2 cscale(double2 a, double s) { return mk2(a.x * s, a.y * s); }
+
+constexpr int kMaxStages = 12;
+constexpr int kMaxGap = 64;     // n_cont - 1
+constexpr int kMaxDeg = 6;      // degree + 1 <= 7
+
+// Device-side description of one FC operator (n points, n_cont, degree):
+// FFT plan over n_ext = n + n_cont - 1 plus the continuation and spectral
+// multiplier tables (see fc_tables.cpp for how each table restates
+// src/fc_core.cpp).
+struct FcPlanDev {
+    int n;        // points per line (N)
+    int n_ext;    // FFT length
+    int n_gap;    // n_cont - 1
+    int dp1;      // degree + 1 boundary points used by the continuation
+    int nstages;
+    int radix[kMaxStages];
+    int span[kMaxStages];
+    const double2* tw;      // exp(-2 pi i k / n_ext), k < n_ext
+    const double* blend;    // n_gap x dp1, row-major (FcOperator::blend_matrix)
+    const double2* mult;    // 4 x n_ext multipliers in DIF output order: d1, d2, filter, smear
+};
+
+}  // namespace fcsg

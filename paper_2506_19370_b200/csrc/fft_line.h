@@ -1,0 +1,313 @@
+// Shared-memory FC line transform: continuation -> mixed-radix FFT -> spectral
+// multiplier -> inverse FFT, for a batch of LB complex lines held in shared
+// memory as buf[pos * pitch + line] (line index fastest, so the 32 lanes of a
+// warp touch consecutive 16-byte slots: conflict-free, and one twiddle per
+// butterfly is a broadcast).
+//
+// Restates FcOperator::derivative / apply_profile (src/fc_core.cpp:221-238,
+// 257-297) for TWO real lines at once: the complex line z = a + i b is
+// transformed with a full complex DFT of length n_ext; because every
+// multiplier used by the reference is Hermitian-consistent (i*w*k_signed with
+// the even-n Nyquist bin zeroed for odd derivatives; real-even for the second
+// derivative and both filter profiles), Re/Im of the result are exactly the
+// reference's c2r outputs for a and b.
+//
+// Forward: in-place decimation-in-frequency (natural order in, digit-reversed
+// out); the multiplier table is stored in that digit-reversed order; inverse:
+// in-place decimation-in-time (digit-reversed in, natural out, unnormalised,
+// as FFTW's c2r). No permutation pass is needed.
+#pragma once
+
+#include "fcsg_common.h"
+
+namespace fcsg {
+
+FCSG_HD double2 ld2(const double2* p) {
+#if FCSG_CUDA && defined(__CUDA_ARCH__)
+    return __ldg(p);
+#else
+    return *p;
+#endif
+}
+FCSG_HD double ld1(const double* p) {
+#if FCSG_CUDA && defined(__CUDA_ARCH__)
+    return __ldg(p);
+#else
+    return *p;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// small DFTs in registers: y_q = sum_r x_r exp(-+ 2 pi i r q / P)
+
+template <bool INV>
+FCSG_HD void dft2(double2* x) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+}
+
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+FCSG_HD double2 mul_mi(double2 v) {
+    return INV ? mk2(-v.y, v.x) : mk2(v.y, -v.x);
+}
+
+template <bool INV>
+FCSG_HD void dft4v(double2& x0, double2& x1, double2& x2, double2& x3) {
+    const double2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_mi<INV>(csub(x1, x3));
+    x0 = cadd(t0, t2);
+    x2 = csub(t0, t2);
+    x1 = cadd(t1, t3);
+    x3 = csub(t1, t3);
+}
+
+template <bool INV>
+FCSG_HD void dft4(double2* x) {
+    dft4v<INV>(x[0], x[1], x[2], x[3]);
+}
+
+template <bool INV>
+FCSG_HD void dft8(double2* x) {
+    double2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
+    double2 o0 = x[1], o1 = x[3], o2 = x[5], o3 = x[7];
+    dft4v<INV>(e0, e1, e2, e3);
+    dft4v<INV>(o0, o1, o2, o3);
+    const double h = 0.70710678118654752440;
+    // w8^q = exp(-+ i pi q / 4)
+    const double2 w1o = INV ? mk2(h * (o1.x - o1.y), h * (o1.x + o1.y)) : mk2(h * (o1.x + o1.y), h * (o1.y - o1.x));
+    const double2 w2o = mul_mi<INV>(o2);
+    const double2 w3o = INV ? mk2(-h * (o3.x + o3.y), h * (o3.x - o3.y)) : mk2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+    x[0] = cadd(e0, o0);
+    x[4] = csub(e0, o0);
+    x[1] = cadd(e1, w1o);
+    x[5] = csub(e1, w1o);
+    x[2] = cadd(e2, w2o);
+    x[6] = csub(e2, w2o);
+    x[3] = cadd(e3, w3o);
+    x[7] = csub(e3, w3o);
+}
+
+// odd P: symmetric-pair form. cos/sin(2 pi k / P) come from the n-point
+// twiddle table (P divides n): tw[k n / P] = (cos, -sin).
+template <int P, bool INV>
+FCSG_HD void dft_odd(double2* x, const double2* tw, int n) {
+    constexpr int H = (P - 1) / 2;
+    double2 a[H], b[H];
+    double2 y0 = x[0];
+    for (int k = 1; k <= H; ++k) {
+        a[k - 1] = cadd(x[k], x[P - k]);
+        b[k - 1] = csub(x[k], x[P - k]);
+        y0 = cadd(y0, a[k - 1]);
+    }
+    const int st = n / P;
+    double2 y[P];
+    y[0] = y0;
+    for (int q = 1; q <= H; ++q) {
+        double2 re = x[0];
+        double2 im = mk2(0.0, 0.0);
+        int idx = 0;
+        for (int k = 1; k <= H; ++k) {
+            idx += q;
+            if (idx >= P) idx -= P;
+            const double2 w = ld2(tw + idx * st);
+            re = mk2(re.x + a[k - 1].x * w.x, re.y + a[k - 1].y * w.x);
+            im = mk2(im.x - b[k - 1].x * w.y, im.y - b[k - 1].y * w.y);
+        }
+        // forward: y_q = re - i im, y_{P-q} = re + i im
+        const double2 mi = mul_mi<INV>(im);
+        y[q] = cadd(re, mi);
+        y[P - q] = csub(re, mi);
+    }
+    for (int q = 0; q < P; ++q) x[q] = y[q];
+}
+
+template <int P, bool INV>
+FCSG_HD void dft_reg(double2* x, const double2* tw, int n) {
+    if constexpr (P == 2) dft2<INV>(x);
+    else if constexpr (P == 4) dft4<INV>(x);
+    else if constexpr (P == 8) dft8<INV>(x);
+    else dft_odd<P, INV>(x, tw, n);
+}
+
+// ---------------------------------------------------------------------------
+// one radix-P stage over all LB lines. Stage span L, m = L / P; butterfly
+// (block, j) works on positions block*L + j + q*m, q < P.
+
+template <int P>
+FCSG_HD void stage_reg(Thr t, double2* buf, int pitch, int LB, int n, int L, const double2* tw, bool inv) {
+    const int m = L / P;
+    const int total = (n / P) * LB;
+    const int tstep = n / L;
+    for (int w = t.tid; w < total; w += t.nthr) {
+        const int line = w % LB;
+        const int b = w / LB;
+        const int blk = b / m;
+        const int j = b - blk * m;
+        double2* p = buf + (blk * L + j) * pitch + line;
+        const int ms = m * pitch;
+        double2 x[P];
+        for (int q = 0; q < P; ++q) x[q] = p[q * ms];
+        if (!inv) {
+            dft_reg<P, false>(x, tw, n);
+            if (j)
+                for (int q = 1; q < P; ++q) x[q] = cmul(x[q], ld2(tw + j * q * tstep));
+        } else {
+            if (j)
+                for (int q = 1; q < P; ++q) x[q] = cmulc(x[q], ld2(tw + j * q * tstep));
+            dft_reg<P, true>(x, tw, n);
+        }
+        for (int q = 0; q < P; ++q) p[q * ms] = x[q];
+    }
+}
+
+// generic radix (large primes): direct DFT with outputs staged in scr
+// (scr_cap complex slots) so the stage stays in place. Contains syncs.
+FCSG_HD void stage_generic(Thr t, double2* buf, int pitch, int LB, int n, int L, int P,
+                           const double2* tw, bool inv, double2* scr, int scr_cap) {
+    const int m = L / P;
+    const int nb = n / P;
+    const int tstep = n / L;
+    const int pstep = n / P;
+    const int ms = m * pitch;
+    if (inv) {  // DIT: twiddle the inputs once, in place
+        const int total = n * LB;
+        for (int w = t.tid; w < total; w += t.nthr) {
+            const int line = w % LB;
+            const int pos = w / LB;
+            const int blk = pos / L;
+            const int rem = pos - blk * L;
+            const int q = rem / m;
+            const int j = rem - q * m;
+            if (j && q) {
+                double2* p = buf + pos * pitch + line;
+                *p = cmulc(*p, ld2(tw + j * q * tstep));
+            }
+        }
+        FCSG_SYNC();
+    }
+    const int per_b = P * LB;
+    int K = scr_cap / per_b;
+    if (K < 1) K = 1;
+    for (int b0 = 0; b0 < nb; b0 += K) {
+        const int kk = (nb - b0 < K) ? nb - b0 : K;
+        const int total = kk * per_b;
+        for (int w = t.tid; w < total; w += t.nthr) {
+            const int line = w % LB;
+            const int rest = w / LB;
+            const int q = rest % P;
+            const int bb = b0 + rest / P;
+            const int blk = bb / m;
+            const int j = bb - blk * m;
+            const double2* p = buf + (blk * L + j) * pitch + line;
+            double2 step = ld2(tw + q * pstep);
+            if (inv) step.y = -step.y;
+            double2 cur = mk2(1.0, 0.0);
+            double2 acc = mk2(0.0, 0.0);
+            int idx = 0;
+            for (int r = 0; r < P; ++r) {
+                const double2 xr = p[r * ms];
+                acc = cadd(acc, cmul(xr, cur));
+                idx += q;
+                if (idx >= P) idx -= P;
+                if ((r & 7) == 7) {  // refresh the rotation from the table
+                    cur = ld2(tw + idx * pstep);
+                    if (inv) cur.y = -cur.y;
+                } else {
+                    cur = cmul(cur, step);
+                }
+            }
+            if (!inv && j && q) acc = cmul(acc, ld2(tw + j * q * tstep));
+            scr[w] = acc;
+        }
+        FCSG_SYNC();
+        for (int w = t.tid; w < total; w += t.nthr) {
+            const int line = w % LB;
+            const int rest = w / LB;
+            const int q = rest % P;
+            const int bb = b0 + rest / P;
+            const int blk = bb / m;
+            const int j = bb - blk * m;
+            buf[(blk * L + j) * pitch + line + q * ms] = scr[w];
+        }
+        FCSG_SYNC();
+    }
+}
+
+#if FCSG_CUDA
+__host__ __device__
+#endif
+inline bool radix_in_registers(int p) {
+    return p == 2 || p == 3 || p == 4 || p == 5 || p == 7 || p == 8 || p == 9 || p == 11 || p == 13;
+}
+
+FCSG_HD void run_stage(Thr t, double2* buf, int pitch, int LB, int n, int L, int P, const double2* tw,
+                       bool inv, double2* scr, int scr_cap) {
+    switch (P) {
+        case 2: stage_reg<2>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 3: stage_reg<3>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 4: stage_reg<4>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 5: stage_reg<5>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 7: stage_reg<7>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 8: stage_reg<8>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 9: stage_reg<9>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 11: stage_reg<11>(t, buf, pitch, LB, n, L, tw, inv); break;
+        case 13: stage_reg<13>(t, buf, pitch, LB, n, L, tw, inv); break;
+        default: stage_generic(t, buf, pitch, LB, n, L, P, tw, inv, scr, scr_cap); break;
+    }
+}
+
+// FcOperator::continuation (src/fc_core.cpp:221-238) for LB complex lines:
+// gap[j] = sum_i A[j,i] f[N-dp1+i]  +  sum_i A[g-1-j,i] f[dp1-1-i], written
+// at positions N..N+g-1.
+FCSG_HD void continuation(Thr t, double2* buf, int pitch, int LB, const FcPlanDev& pl) {
+    const int N = pl.n, g = pl.n_gap, d1 = pl.dp1;
+    const int total = g * LB;
+    for (int w = t.tid; w < total; w += t.nthr) {
+        const int line = w % LB;
+        const int jj = w / LB;
+        double2 a = mk2(0.0, 0.0), b = mk2(0.0, 0.0);
+        const double* Ar = pl.blend + jj * d1;
+        const double* Al = pl.blend + (g - 1 - jj) * d1;
+        for (int i = 0; i < d1; ++i) {
+            const double2 fr = buf[(N - d1 + i) * pitch + line];
+            const double2 fl = buf[(d1 - 1 - i) * pitch + line];
+            const double cr = ld1(Ar + i), cl = ld1(Al + i);
+            a = mk2(a.x + cr * fr.x, a.y + cr * fr.y);
+            b = mk2(b.x + cl * fl.x, b.y + cl * fl.y);
+        }
+        buf[(N + jj) * pitch + line] = cadd(a, b);
+    }
+}
+
+// modes (match include/fcsg.h): 1 = d/dq, 2 = d2/dq2, 3 = filter, 4 = smear filter
+FCSG_HD void spec_mult(Thr t, double2* buf, int pitch, int LB, int n, const double2* mult) {
+    const int total = n * LB;
+    for (int w = t.tid; w < total; w += t.nthr) {
+        const int line = w % LB;
+        const int pos = w / LB;
+        double2* p = buf + pos * pitch + line;
+        *p = cmul(*p, ld2(mult + pos));
+    }
+}
+
+// Full unit-span operator on the LB complex lines already loaded at
+// positions 0..N-1. Ends with a sync; result at positions 0..N-1.
+FCSG_HD void fc_transform(Thr t, double2* buf, int pitch, int LB, const FcPlanDev& pl, int mode,
+                          double2* scr, int scr_cap) {
+    continuation(t, buf, pitch, LB, pl);
+    FCSG_SYNC();
+    const int n = pl.n_ext;
+    for (int s = 0; s < pl.nstages; ++s) {
+        run_stage(t, buf, pitch, LB, n, pl.span[s], pl.radix[s], pl.tw, false, scr, scr_cap);
+        FCSG_SYNC();
+    }
+    spec_mult(t, buf, pitch, LB, n, pl.mult + (mode - 1) * n);
+    FCSG_SYNC();
+    for (int s = pl.nstages - 1; s >= 0; --s) {
+        run_stage(t, buf, pitch, LB, n, pl.span[s], pl.radix[s], pl.tw, true, scr, scr_cap);
+        FCSG_SYNC();
+    }
+}
+
+}  // namespace fcsg

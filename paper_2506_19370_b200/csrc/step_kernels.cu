@@ -1,0 +1,788 @@
+// Kernels of one FC-SDNN superstep (Engine::run body, src/runtime.cpp:482-511).
+//
+//  phase 0  proxy_kernel     proxy_value / mwsb_value per point   (src/viscosity.cpp:13-29, runtime.cpp:327-346)
+//           classify_kernel  row + column 7-point stencils -> MLP -> min -> mu_hat
+//                            (src/viscosity.cpp:48-59,108-160,211-251)
+//  phase 1  blend_kernel     mu = max(w_norm mu_hat + sum w mu_hat_src, 0) and the
+//                            dt_bound_local min (src/runtime.cpp:352-371, euler.cpp:223-236)
+//  phase 2  filter rows/cols + E rebuild (or the t=0 smear)   (src/runtime.cpp:373-424,
+//                            subpatch_data.cpp:30-67), dilation at t=0
+//  stage    pass A (rows)    D1 of F, G, w  ->  iq1x D1F + iq1y D1G, D1w
+//           pass B (cols)    D2 of F, G, w  ->  inviscid rhs, mu grad w; D2 of mu grad w
+//           pass C (rows)    D1 of mu grad w -> rhs -> SSPRK(5,4) update
+//                            (euler_rhs src/euler.cpp:25-101, ssprk_stage_update :182-221)
+//           bc_kernel        enforce_bc, row ends then column ends (src/euler.cpp:105-180)
+//           exchange_kernel  phase 6 fringe copies (src/runtime.cpp:433-454)
+//
+// The 40 line derivatives of euler_rhs are therefore done as 3 line passes;
+// each pass keeps two real quantities per complex FFT line (fft_line.h).
+#include "fft_line.h"
+#include "step_kernels.h"
+
+#include <cmath>
+#include <vector>
+
+namespace fcsg {
+
+namespace {
+constexpr double kG = 1.4;
+constexpr double kGm1 = kG - 1.0;
+// include/fcs/euler.hpp:20-29
+constexpr double SB0 = 0.391752226571890;
+constexpr double SA20 = 0.444370493651235, SA21 = 0.555629506348765, SB1 = 0.368410593050371;
+constexpr double SA30 = 0.620101851488403, SA32 = 0.379898148511597, SB2 = 0.251891774271694;
+constexpr double SA40 = 0.178079954393132, SA43 = 0.821920045606868, SB3 = 0.544974750228521;
+constexpr double SC2 = 0.517231671970585, SC3 = 0.096059710526147, SD3 = 0.063692468666290,
+                 SC4 = 0.386708617503269, SD4 = 0.226007483236906;
+constexpr int kThreads = 256;
+}  // namespace
+
+FCSG_HD void raise_error(StepScalars* sc, int code, int sub, int i, int j) {
+#if FCSG_CUDA
+    if (atomicCAS(&sc->err.code, 0, code) == 0) {
+        sc->err.sub = sub;
+        sc->err.i = i;
+        sc->err.j = j;
+    }
+#else
+    if (sc->err.code == 0) {
+        sc->err.code = code;
+        sc->err.sub = sub;
+        sc->err.i = i;
+        sc->err.j = j;
+    }
+#endif
+}
+
+FCSG_HD unsigned long long dbits(double v) {
+#if FCSG_CUDA
+    return static_cast<unsigned long long>(__double_as_longlong(v));
+#else
+    unsigned long long u;
+    std::memcpy(&u, &v, 8);
+    return u;
+#endif
+}
+
+FCSG_HD bool finite_d(double v) {
+#if FCSG_CUDA
+    return isfinite(v);
+#else
+    return std::isfinite(v);
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// generic line pass
+
+struct LineCtx {
+    int sub;
+    int line0;
+    int nl_valid;
+    long base;
+    int ni;
+    bool rows;
+};
+
+FCSG_HD long pidx(const LineCtx& c, int l, int i) {
+    return c.rows ? c.base + static_cast<long>(c.line0 + l) * c.ni + i : c.base + static_cast<long>(i) * c.ni + c.line0 + l;
+}
+
+template <int LB, class Pass>
+FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const EngineDev& E, const FcPlanDev& pl,
+                       int scr_cap) {
+    constexpr bool rows = Pass::kRows;
+    const int ni = E.ni, nj = E.nj;
+    const int N = rows ? ni : nj;
+    const int nlines = rows ? nj : ni;
+    const int bps = (nlines + LB - 1) / LB;
+    LineCtx c;
+    c.sub = block / bps;
+    c.line0 = (block % bps) * LB;
+    c.nl_valid = (nlines - c.line0 < LB) ? nlines - c.line0 : LB;
+    c.base = static_cast<long>(c.sub) * ni * nj;
+    c.ni = ni;
+    c.rows = rows;
+    const int pitch = LB + 1;
+    double2* buf = smem;
+    double2* scr = smem + pl.n_ext * pitch;
+    const double inv_len = P.kScaled ? (rows ? E.inv_len1[c.sub] : E.inv_len2[c.sub]) : 1.0;
+    const int total = N * LB;
+    for (int r = 0; r < Pass::kRounds; ++r) {
+        for (int w = t.tid; w < total; w += t.nthr) {
+            int i, l;
+            if (rows) {
+                i = w % N;
+                l = w / N;
+            } else {
+                l = w % LB;
+                i = w / LB;
+            }
+            double2 v = mk2(0.0, 0.0);
+            if (l < c.nl_valid) v = P.load(r, pidx(c, l, i), c, l, i);
+            buf[i * pitch + l] = v;
+        }
+        FCSG_SYNC();
+        fc_transform(t, buf, pitch, LB, pl, P.mode(r), scr, scr_cap);
+        for (int w = t.tid; w < total; w += t.nthr) {
+            int i, l;
+            if (rows) {
+                i = w % N;
+                l = w / N;
+            } else {
+                l = w % LB;
+                i = w / LB;
+            }
+            if (l < c.nl_valid) {
+                const double2 v = buf[i * pitch + l];
+                P.store(r, pidx(c, l, i), mk2(v.x * inv_len, v.y * inv_len), c, l, i);
+            }
+        }
+        FCSG_SYNC();
+    }
+    P.finish(t, c, N);
+}
+
+// conservative -> (theta, u, v, p) exactly as euler_rhs (src/euler.cpp:29-41,44-55)
+struct Prim {
+    double rho, mx, my, E, theta, p;
+};
+FCSG_HD Prim prim_rhs(const EngineDev& E, long p) {
+    Prim q;
+    q.rho = E.e[0][p];
+    q.mx = E.e[1][p];
+    q.my = E.e[2][p];
+    q.E = E.e[3][p];
+    const double rs = (q.rho != 0.0) ? q.rho : 1e-300;
+    const double pr = kGm1 * (q.E - 0.5 * (q.mx * q.mx + q.my * q.my) / rs);
+    q.theta = pr / rs;
+    q.p = q.rho * q.theta;
+    return q;
+}
+
+// flux pair (F_c, G_c) (src/euler.cpp:44-55, 64-75)
+FCSG_HD double2 flux_pair(const Prim& q, int c) {
+    const double u = q.mx / q.rho, v = q.my / q.rho;
+    switch (c) {
+        case 0: return mk2(q.mx, q.my);
+        case 1: return mk2(q.mx * u + q.p, q.mx * v);
+        case 2: return mk2(q.my * u, q.my * v + q.p);
+        default: return mk2(u * (q.E + q.p), v * (q.E + q.p));
+    }
+}
+
+// Pass A (rows): D1 of F_c, G_c (rounds 0..3) and of w = (rho, rho u, rho v, theta) (4, 5)
+struct PassA {
+    static constexpr bool kRows = true;
+    static constexpr int kRounds = 6;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    FCSG_HD PassA(const EngineDev& e, int) : E(e) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, int l, int i) const {
+        const Prim q = prim_rhs(E, p);
+        if (r == 0 && E.mask[p] == 1) {
+            // interior positivity diagnostic (src/euler.cpp:37-39)
+            const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
+            if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) {
+                const int il = c.rows ? i : c.line0 + l, jl = c.rows ? c.line0 + l : i;
+                raise_error(E.sc, 1, c.sub, il, jl);
+            }
+        }
+        if (r < 4) return flux_pair(q, r);
+        if (r == 4) return mk2(q.rho, q.mx);
+        return mk2(q.my, q.theta);
+    }
+    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+        if (r < 4) {
+            E.tA[r][p] = E.iq1x[p] * v.x + E.iq1y[p] * v.y;
+        } else {
+            const int c0 = 2 * (r - 4);
+            E.tW[c0][p] = v.x;
+            E.tW[c0 + 1][p] = v.y;
+        }
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// Pass B (cols): D2 of F, G, w; inviscid rhs and mu grad w; then D2 of mu grad w
+struct PassB {
+    static constexpr bool kRows = false;
+    static constexpr int kRounds = 10;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    FCSG_HD PassB(const EngineDev& e, int) : E(e) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
+        if (r >= 6) return mk2(E.tS4[r - 6][p], E.tS5[r - 6][p]);
+        const Prim q = prim_rhs(E, p);
+        if (r < 4) return flux_pair(q, r);
+        if (r == 4) return mk2(q.rho, q.mx);
+        return mk2(q.my, q.theta);
+    }
+    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+        if (r < 4) {
+            E.tA[r][p] = -(E.tA[r][p] + (E.iq2x[p] * v.x + E.iq2y[p] * v.y));
+        } else if (r < 6) {
+            const int c0 = 2 * (r - 4);
+            const double mu = E.mu[p];
+            const double a = E.iq1x[p], b = E.iq2x[p], cc = E.iq1y[p], d = E.iq2y[p];
+            for (int k = 0; k < 2; ++k) {
+                const double d1 = E.tW[c0 + k][p];
+                const double d2 = k == 0 ? v.x : v.y;
+                const double gx = a * d1 + b * d2;
+                const double gy = cc * d1 + d * d2;
+                E.tS4[c0 + k][p] = mu * gx;
+                E.tS5[c0 + k][p] = mu * gy;
+            }
+        } else {
+            const int c = r - 6;
+            E.tA[c][p] += E.iq2x[p] * v.x + E.iq2y[p] * v.y;
+        }
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// Pass C (rows): D1 of mu grad w, rhs, SSPRK(5,4) stage update (src/euler.cpp:182-221)
+struct PassC {
+    static constexpr bool kRows = true;
+    static constexpr int kRounds = 4;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    int stage;
+    FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const { return mk2(E.tS4[r][p], E.tS5[r][p]); }
+    FCSG_HD void store(int c, long p, double2 v, const LineCtx&, int, int) const {
+        const double dt = E.sc->dt;  // device-resident step size (finalize_dt_kernel)
+        const double r = E.tA[c][p] + (E.iq1x[p] * v.x + E.iq1y[p] * v.y);
+        if (E.rhs[0]) E.rhs[c][p] = r;
+        double* u = E.e[c];
+        switch (stage) {
+            case 0: {
+                const double u0 = u[p];  // e0 == e at stage 0 (set in phase 2)
+                E.e0[c][p] = u0;
+                u[p] = u0 + dt * SB0 * r;
+                break;
+            }
+            case 1: {
+                const double nu = SA20 * E.e0[c][p] + SA21 * u[p] + dt * SB1 * r;
+                u[p] = nu;
+                E.e2[c][p] = nu;
+                break;
+            }
+            case 2: {
+                const double nu = SA30 * E.e0[c][p] + SA32 * u[p] + dt * SB2 * r;
+                u[p] = nu;
+                E.e3[c][p] = nu;
+                break;
+            }
+            case 3:
+                E.rhs3[c][p] = r;
+                u[p] = SA40 * E.e0[c][p] + SA43 * u[p] + dt * SB3 * r;
+                break;
+            default:
+                u[p] = SC2 * E.e2[c][p] + SC3 * E.e3[c][p] + dt * SD3 * E.rhs3[c][p] + SC4 * u[p] + dt * SD4 * r;
+                break;
+        }
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// Phase 2 rows: filter (or, at t=0, smear) rho, rho u, rho v, theta
+// (src/runtime.cpp:375-411, subpatch_data.cpp:30-67)
+struct PassFR {
+    static constexpr bool kRows = true;
+    static constexpr int kRounds = 2;
+    static constexpr bool kScaled = false;
+    const EngineDev& E;
+    bool smear;
+    FCSG_HD PassFR(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
+    FCSG_HD int mode(int) const { return smear ? 4 : 3; }
+    FCSG_HD static double2 orig(const EngineDev& E, int r, long p) {
+        const double rho = E.e[0][p], mx = E.e[1][p];
+        if (r == 0) return mk2(rho, mx);
+        const double my = E.e[2][p], En = E.e[3][p];
+        const double th = kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho;
+        return mk2(my, th);
+    }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const { return orig(E, r, p); }
+    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+        if (smear) {
+            const double m = E.m01[p];
+            const double2 f = orig(E, r, p);
+            v = mk2(m * v.x + (1.0 - m) * f.x, m * v.y + (1.0 - m) * f.y);
+        }
+        E.tF[2 * r][p] = v.x;
+        E.tF[2 * r + 1][p] = v.y;
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// Phase 2 cols: filter/smear columns of the row results, then E rebuild
+struct PassFC {
+    static constexpr bool kRows = false;
+    static constexpr int kRounds = 2;
+    static constexpr bool kScaled = false;
+    const EngineDev& E;
+    bool smear;
+    FCSG_HD PassFC(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
+    FCSG_HD int mode(int) const { return smear ? 4 : 3; }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
+        return mk2(E.tF[2 * r][p], E.tF[2 * r + 1][p]);
+    }
+    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+        if (smear) {
+            const double m = E.m01[p];
+            const double fa = E.tF[2 * r][p], fb = E.tF[2 * r + 1][p];
+            v = mk2(m * v.x + (1.0 - m) * fa, m * v.y + (1.0 - m) * fb);
+        }
+        if (r == 0) {
+            E.e[0][p] = v.x;
+            E.e[1][p] = v.y;
+        } else {
+            E.e[2][p] = v.x;
+            E.tF[3][p] = v.y;  // theta, consumed by finish()
+        }
+    }
+    FCSG_HD void finish(Thr t, const LineCtx& c, int N) const {
+        // E = rho theta/(gamma-1) + |m|^2 / (2 rho)   (src/runtime.cpp:413-420)
+        const int total = N * c.nl_valid;
+        for (int w = t.tid; w < total; w += t.nthr) {
+            const int l = w % c.nl_valid, i = w / c.nl_valid;
+            const long p = pidx(c, l, i);
+            const double rho = E.e[0][p], mx = E.e[1][p], my = E.e[2][p];
+            E.e[3][p] = rho * E.tF[3][p] / kGm1 + 0.5 * (mx * mx + my * my) / rho;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// pointwise kernels
+
+// phase 0, part 1: Mach proxy and wave-speed bound (src/viscosity.cpp:13-29)
+FCSG_HD void proxy_body(Thr t, int block, int nblocks, const EngineDev& E) {
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
+        if (!E.mask[p]) {
+            E.proxy[p] = 0.0;
+            E.speed[p] = 1.0;
+            continue;
+        }
+        const double rho = E.e[0][p], ru = E.e[1][p], rv = E.e[2][p], En = E.e[3][p];
+        const double u = ru / rho, v = rv / rho;
+        const double ke = 0.5 * rho * (u * u + v * v);
+        const double pr = kGm1 * (En - ke);
+        if (!(rho > 0.0) || !(pr > 0.0)) {
+            const long loc = p % (static_cast<long>(E.ni) * E.nj);
+            raise_error(E.sc, 2, static_cast<int>(p / (static_cast<long>(E.ni) * E.nj)), static_cast<int>(loc % E.ni),
+                        static_cast<int>(loc / E.ni));
+            E.proxy[p] = 0.0;
+            E.speed[p] = 1.0;
+            continue;
+        }
+        const double um = sqrt(u * u + v * v);
+        E.proxy[p] = um * sqrt(rho / (kG * pr));
+        E.speed[p] = um + sqrt(kG * pr / rho);
+    }
+}
+
+// MlpClassifier::forward + classify_stencil (src/viscosity.cpp:108-133) on a
+// raw 7-point stencil, with normalize_stencil's guard (src/viscosity.cpp:48-59)
+FCSG_HD int classify_stencil(const double* W, const double* s, double abs_floor) {
+    double lo = s[0], hi = s[0];
+    for (int k = 1; k < kMlpIn; ++k) {
+        lo = s[k] < lo ? s[k] : lo;
+        hi = s[k] > hi ? s[k] : hi;
+    }
+    const double span = hi - lo;
+    double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+    scale = scale > 1e-100 ? scale : 1e-100;
+    if (span <= 1e-13 * scale || span <= abs_floor) return 4;
+    double x[kMlpIn];
+    for (int k = 0; k < kMlpIn; ++k) x[k] = 2.0 * (s[k] - lo) / span - 1.0;
+    double h[kMlpHidden], g[kMlpHidden];
+    const double* w = W;
+    for (int i = 0; i < kMlpHidden; ++i) {
+        double acc = w[kMlpHidden * kMlpIn + i];
+        for (int j = 0; j < kMlpIn; ++j) acc += w[i * kMlpIn + j] * x[j];
+        h[i] = tanh(acc);
+    }
+    w += kMlpHidden * kMlpIn + kMlpHidden;
+    for (int layer = 0; layer < 3; ++layer) {
+        for (int i = 0; i < kMlpHidden; ++i) {
+            double acc = w[kMlpHidden * kMlpHidden + i];
+            for (int j = 0; j < kMlpHidden; ++j) acc += w[i * kMlpHidden + j] * h[j];
+            g[i] = tanh(acc);
+        }
+        for (int i = 0; i < kMlpHidden; ++i) h[i] = g[i];
+        w += kMlpHidden * kMlpHidden + kMlpHidden;
+    }
+    double lg[kMlpOut];
+    for (int i = 0; i < kMlpOut; ++i) {
+        double acc = w[kMlpOut * kMlpHidden + i];
+        for (int j = 0; j < kMlpHidden; ++j) acc += w[i * kMlpHidden + j] * h[j];
+        lg[i] = acc;
+    }
+    int best = 0;
+    for (int k = 1; k < kMlpOut; ++k)
+        if (lg[k] > lg[best]) best = k;
+    return best + 1;
+}
+
+// Classifier::classify (src/viscosity.cpp:211-238) for one point of a
+// rectangular subpatch: min of the row-window and column-window classes.
+FCSG_HD int classify_point(const double* W, const double* f, long base, int ni, int nj, int i, int j, double abs_floor) {
+    double s[kMlpIn];
+    int cr = 4, cc = 4;
+    if (ni >= kMlpIn) {
+        int st = i - kMlpIn / 2;
+        st = st < 0 ? 0 : (st > ni - kMlpIn ? ni - kMlpIn : st);
+        for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(j) * ni + st + k];
+        cr = classify_stencil(W, s, abs_floor);
+    }
+    if (nj >= kMlpIn) {
+        int st = j - kMlpIn / 2;
+        st = st < 0 ? 0 : (st > nj - kMlpIn ? nj - kMlpIn : st);
+        for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(st + k) * ni + i];
+        cc = classify_stencil(W, s, abs_floor);
+    }
+    return cr < cc ? cr : cc;
+}
+
+// phase 0, part 2: tau, mu_hat = c(tau) h_max S on interior points
+// (src/viscosity.cpp:240-251); at t=0 also the density class for the smear seed
+FCSG_HD void classify_body(Thr t, int block, int nblocks, double* Wsm, const EngineDev& E, bool step0) {
+    for (int k = t.tid; k < kMlpWeights; k += t.nthr) Wsm[k] = E.mlp[k];
+    FCSG_SYNC();
+    const long sz = static_cast<long>(E.ni) * E.nj;
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
+        const long base = (p / sz) * sz;
+        const long loc = p - base;
+        const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
+        const int tau = classify_point(Wsm, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
+        E.tau[p] = tau;
+        E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
+        if (step0) {
+            const int tr = classify_point(Wsm, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
+            E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
+        }
+    }
+}
+
+// t=0 smear mask: box dilation of radius smear_radius (src/runtime.cpp:393-402)
+FCSG_HD void dilate_body(Thr t, int block, int nblocks, const EngineDev& E) {
+    const long sz = static_cast<long>(E.ni) * E.nj;
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    const int rad = E.smear_radius;
+    for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
+        const long base = (p / sz) * sz;
+        const long loc = p - base;
+        const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
+        double m = 0.0;
+        for (int b = (j - rad < 0 ? 0 : j - rad); b <= (j + rad > E.nj - 1 ? E.nj - 1 : j + rad) && m == 0.0; ++b)
+            for (int a = (i - rad < 0 ? 0 : i - rad); a <= (i + rad > E.ni - 1 ? E.ni - 1 : i + rad); ++a)
+                if (E.seed[base + static_cast<long>(b) * E.ni + a] != 0.0) {
+                    m = 1.0;
+                    break;
+                }
+        E.m01[p] = m;
+    }
+}
+
+// phase 1: viscosity blend + clamp, and the dt_bound_local minimum
+FCSG_HD void blend_body(Thr t, int block, int nblocks, const EngineDev& E) {
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    double best = INFINITY;
+    const long sz = static_cast<long>(E.ni) * E.nj;
+    for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
+        double m = E.w_norm[p] * E.mu_hat[p];
+        if (E.visc_off) {
+            const int e0 = E.visc_off[p], e1 = E.visc_off[p + 1];
+            for (int k = e0; k < e1; ++k) m += E.visc_w[k] * E.mu_hat[E.visc_src[k]];
+        }
+        m = m > 0.0 ? m : 0.0;
+        E.mu[p] = m;
+        if (E.mask[p] == 1) {
+            const double h = E.h_min[p];
+            const double rate = E.speed[p] / h + m / (h * h);
+            if (!(rate > 0.0) || !finite_d(rate)) {
+                const long loc = p % sz;
+                raise_error(E.sc, 3, static_cast<int>(p / sz), static_cast<int>(loc % E.ni), static_cast<int>(loc / E.ni));
+            } else {
+                const double v = 1.0 / rate;
+                best = v < best ? v : best;
+            }
+        }
+    }
+#if FCSG_CUDA
+    unsigned long long b = dbits(best);
+    for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_down_sync(0xffffffffu, b, off);
+        b = o < b ? o : b;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(&E.sc->dtmin_bits, b);
+#else
+    const unsigned long long b = dbits(best);
+    if (b < E.sc->dtmin_bits) E.sc->dtmin_bits = b;
+#endif
+}
+
+// dt = cfl * min dt_local, clipped at T (src/runtime.cpp:492-497)
+FCSG_HD void finalize_dt_body(const EngineDev& E) {
+    double m;
+#if FCSG_CUDA
+    m = __longlong_as_double(static_cast<long long>(E.sc->dtmin_bits));
+#else
+    std::memcpy(&m, &E.sc->dtmin_bits, 8);
+#endif
+    double dt = E.cfl * m;
+    if (E.sc->t + dt > E.T) dt = E.T - E.sc->t;
+    E.sc->dt = dt;
+}
+
+// t += dt; step += 1 (src/runtime.cpp:505-507); reset the dt minimum
+FCSG_HD void advance_body(const EngineDev& E) {
+    E.sc->t += E.sc->dt;
+    E.sc->step += 1;
+    E.sc->dtmin_bits = dbits(INFINITY);
+}
+
+// apply_bc_at (src/euler.cpp:105-165); p1/p2 are the first/second neighbours inward
+FCSG_HD void apply_bc_at(const EngineDev& E, const BcDev& bc, long p, long p1, long p2, int axis) {
+    double* const* e = E.e;
+    switch (bc.kind) {
+        case 0:
+            for (int c = 0; c < 4; ++c) e[c][p] = bc.state[c];
+            break;
+        case 1: {
+            const double rho = e[0][p], mx = e[1][p], my = e[2][p];
+            e[3][p] = bc.pressure / kGm1 + 0.5 * (mx * mx + my * my) / rho;
+            break;
+        }
+        case 2: {
+            double nx = axis == 0 ? E.iq1x[p] : E.iq2x[p];
+            double ny = axis == 0 ? E.iq1y[p] : E.iq2y[p];
+            const double nn = hypot(nx, ny);
+            nx /= nn;
+            ny /= nn;
+            const double rho = e[0][p], mx = e[1][p], my = e[2][p], En = e[3][p];
+            const double pr = kGm1 * (En - 0.5 * (mx * mx + my * my) / rho);
+            const double mn = mx * nx + my * ny;
+            const double tmx = mx - mn * nx, tmy = my - mn * ny;
+            e[1][p] = tmx;
+            e[2][p] = tmy;
+            e[3][p] = pr / kGm1 + 0.5 * (tmx * tmx + tmy * tmy) / rho;
+            break;
+        }
+        case 3: {
+            auto th = [&](long q) {
+                const double rho = e[0][q], mx = e[1][q], my = e[2][q], En = e[3][q];
+                return kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho;
+            };
+            const double tt = (4.0 * th(p1) - th(p2)) / 3.0;
+            const double rho = e[0][p];
+            e[1][p] = 0.0;
+            e[2][p] = 0.0;
+            e[3][p] = rho * tt / kGm1;
+            break;
+        }
+        case 5:
+            for (int c = 0; c < 4; ++c) e[c][p] = (4.0 * e[c][p1] - e[c][p2]) / 3.0;
+            break;
+        default:
+            break;
+    }
+}
+
+// enforce_bc (src/euler.cpp:167-180): one CTA per subpatch, all row ends, then all column ends
+FCSG_HD void bc_body(Thr t, int sub, const EngineDev& E) {
+    const int ni = E.ni, nj = E.nj;
+    const long base = static_cast<long>(sub) * ni * nj;
+    for (int j = t.tid; j < nj; j += t.nthr) {
+        const long r = base + static_cast<long>(j) * ni;
+        const BcDev& lo = E.bc_row_lo[static_cast<long>(sub) * nj + j];
+        const BcDev& hi = E.bc_row_hi[static_cast<long>(sub) * nj + j];
+        if (lo.kind >= 0) apply_bc_at(E, lo, r, r + 1, r + 2, 0);
+        if (hi.kind >= 0) apply_bc_at(E, hi, r + ni - 1, r + ni - 2, r + ni - 3, 0);
+    }
+    FCSG_SYNC();
+    for (int i = t.tid; i < ni; i += t.nthr) {
+        const long c0 = base + i, c1 = base + static_cast<long>(nj - 1) * ni + i;
+        const BcDev& lo = E.bc_col_lo[static_cast<long>(sub) * ni + i];
+        const BcDev& hi = E.bc_col_hi[static_cast<long>(sub) * ni + i];
+        if (lo.kind >= 0) apply_bc_at(E, lo, c0, c0 + ni, c0 + 2 * ni, 1);
+        if (hi.kind >= 0) apply_bc_at(E, hi, c1, c1 - ni, c1 - 2 * ni, 1);
+    }
+}
+
+// phase 6: fringe copies (src/runtime.cpp:436-439)
+FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    for (long k = static_cast<long>(block) * t.nthr + t.tid; k < E.n_x; k += step) {
+        const long d = E.x_dst[k], s = E.x_src[k];
+        for (int c = 0; c < 4; ++c) E.e[c][d] = E.e[c][s];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// kernels and launchers
+
+#if FCSG_CUDA
+template <int LB, class Pass>
+__global__ void __launch_bounds__(kThreads)
+    line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg) {
+    extern __shared__ double2 smem[];
+    const Pass P(E, arg);
+    line_pass<LB, Pass>(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, smem, P, E, pl,
+                        scr_cap);
+}
+__global__ void __launch_bounds__(kThreads) proxy_kernel(const __grid_constant__ EngineDev E) {
+    proxy_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
+}
+__global__ void __launch_bounds__(kThreads) classify_kernel(const __grid_constant__ EngineDev E, bool step0) {
+    __shared__ double W[kMlpWeights];
+    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, W, E, step0);
+}
+__global__ void __launch_bounds__(kThreads) dilate_kernel(const __grid_constant__ EngineDev E) {
+    dilate_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
+}
+__global__ void __launch_bounds__(kThreads) blend_kernel(const __grid_constant__ EngineDev E) {
+    blend_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
+}
+__global__ void finalize_dt_kernel(const __grid_constant__ EngineDev E) { finalize_dt_body(E); }
+__global__ void advance_kernel(const __grid_constant__ EngineDev E) { advance_body(E); }
+__global__ void __launch_bounds__(kThreads) bc_kernel(const __grid_constant__ EngineDev E) {
+    bc_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, E);
+}
+__global__ void __launch_bounds__(kThreads) exchange_kernel(const __grid_constant__ EngineDev E) {
+    exchange_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
+}
+#endif
+
+namespace {
+
+constexpr int kLB = 8;  // lines per CTA in the step passes
+
+int grid_for(long n) {
+    long g = (n + kThreads - 1) / kThreads;
+    if (g > 148 * 16) g = 148 * 16;
+    return static_cast<int>(g < 1 ? 1 : g);
+}
+
+template <class Pass>
+void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap, void* stream) {
+    const int nlines = Pass::kRows ? E.nj : E.ni;
+    const int bps = (nlines + kLB - 1) / kLB;
+    const int nblk = E.S * bps;
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2);
+#if FCSG_CUDA
+    auto k = line_pass_kernel<kLB, Pass>;
+    static bool attr_set = false;  // once per instantiation (not during graph capture)
+    if (!attr_set) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr_set = true;
+    }
+    k<<<nblk, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(E, pl, scr_cap, arg);
+#else
+    (void)stream;
+    const Pass P(E, arg);
+    std::vector<double2> sm(smem / sizeof(double2));
+    for (int b = 0; b < nblk; ++b) line_pass<kLB, Pass>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+#endif
+}
+
+}  // namespace
+
+int step_scr_cap(const FcPlanDev& pl) {
+    int cap = 0;
+    for (int s = 0; s < pl.nstages; ++s) {
+        const int p = pl.radix[s];
+        if (!radix_in_registers(p)) {
+            const int per = p * kLB;
+            const int k = kThreads / per > 1 ? kThreads / per : 1;
+            cap = cap > per * k ? cap : per * k;
+        }
+    }
+    return cap;
+}
+
+void launch_phase0(const EngineDev& E, bool step0, void* stream) {
+#if FCSG_CUDA
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    proxy_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E);
+    classify_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E, step0);
+#else
+    (void)stream;
+    proxy_body(Thr{0, 1}, 0, 1, E);
+    std::vector<double> W(kMlpWeights);
+    classify_body(Thr{0, 1}, 0, 1, W.data(), E, step0);
+#endif
+}
+
+void launch_phase1(const EngineDev& E, void* stream) {
+#if FCSG_CUDA
+    blend_kernel<<<grid_for(E.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+#else
+    (void)stream;
+    blend_body(Thr{0, 1}, 0, 1, E);
+#endif
+}
+
+void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* stream) {
+    if (step0) {
+#if FCSG_CUDA
+        dilate_kernel<<<grid_for(E.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+#else
+        dilate_body(Thr{0, 1}, 0, 1, E);
+#endif
+    }
+    run_line_pass<PassFR>(step0 ? 1 : 0, E, P.row, P.scr_row, stream);
+    run_line_pass<PassFC>(step0 ? 1 : 0, E, P.col, P.scr_col, stream);
+}
+
+void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
+    run_line_pass<PassA>(0, E, P.row, P.scr_row, stream);
+    run_line_pass<PassB>(0, E, P.col, P.scr_col, stream);
+    run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
+}
+
+void launch_bc(const EngineDev& E, void* stream) {
+#if FCSG_CUDA
+    bc_kernel<<<E.S, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+#else
+    (void)stream;
+    for (int s = 0; s < E.S; ++s) bc_body(Thr{0, 1}, s, E);
+#endif
+}
+
+void launch_exchange(const EngineDev& E, void* stream) {
+    if (E.n_x == 0) return;
+#if FCSG_CUDA
+    exchange_kernel<<<grid_for(E.n_x), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+#else
+    (void)stream;
+    exchange_body(Thr{0, 1}, 0, 1, E);
+#endif
+}
+
+void launch_finalize_dt(const EngineDev& E, void* stream) {
+#if FCSG_CUDA
+    finalize_dt_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(E);
+#else
+    (void)stream;
+    finalize_dt_body(E);
+#endif
+}
+
+void launch_advance(const EngineDev& E, void* stream) {
+#if FCSG_CUDA
+    advance_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(E);
+#else
+    (void)stream;
+    advance_body(E);
+#endif
+}
+
+}  // namespace fcsg

@@ -1,0 +1,98 @@
+// Device-side state of one engine and the kernel launchers of the FC-SDNN
+// superstep (see step_kernels.cu for what each kernel restates).
+#pragma once
+
+#include <cstdint>
+
+#include "fcsg_common.h"
+
+namespace fcsg {
+
+constexpr int kMlpIn = 7;
+constexpr int kMlpHidden = 16;
+constexpr int kMlpOut = 4;
+constexpr int kMlpLayers = 5;  // 7-16-16-16-16-4 (src/viscosity.cpp:366)
+// packed: per layer W (rows x cols, row-major) then b (rows)
+constexpr int kMlpWeights = (16 * 7 + 16) + 3 * (16 * 16 + 16) + (4 * 16 + 4);
+
+// device scalars of the running step (one per engine)
+struct StepScalars {
+    unsigned long long dtmin_bits;  // min over interior points of 1/(S/h + mu/h^2), as ordered bits
+    double dt;
+    double t;
+    long long step;
+    DevError err;
+};
+
+// BC table entry for one line end (BcSpec, include/fcs/bc.hpp:19-23)
+struct BcDev {
+    int kind;  // -1 none, else BcKind order: 0 inflow .. 5 zero_normal_all
+    int pad;
+    double state[4];
+    double pressure;
+};
+
+struct EngineDev {
+    int S, ni, nj;  // subpatches of one uniform rectangular shape
+    long npts;      // S * ni * nj
+    double cfl, T;
+    double visc_c[4];
+    double abs_floor;
+    int smear_radius;
+    // per-subpatch
+    const double* inv_len1;  // S
+    const double* inv_len2;  // S
+    const int* sub_i0;       // S: global lattice origin (error reports)
+    const int* sub_j0;
+    const int* sub_patch;
+    const BcDev* bc_row_lo;  // S * nj
+    const BcDev* bc_row_hi;
+    const BcDev* bc_col_lo;  // S * ni
+    const BcDev* bc_col_hi;
+    // per-point geometry
+    const uint8_t* mask;
+    const double *iq1x, *iq2x, *iq1y, *iq2y, *h_min, *h_max, *w_norm;
+    // state
+    double* e[4];
+    double* e0[4];
+    double* e2[4];
+    double* e3[4];
+    double* rhs3[4];
+    double* rhs[4];  // optional (nullptr unless debug_rhs): rhs of the last stage
+    double *mu_hat, *mu, *tau, *speed, *proxy, *seed, *m01;
+    // pass temporaries
+    double* tA[4];   // inviscid partials, then the partial rhs
+    double* tW[4];   // d/dq1 of w
+    double* tS4[4];  // mu * grad_x w
+    double* tS5[4];  // mu * grad_y w
+    double* tF[4];   // filter/smear row results
+    // viscosity blend plan, CSR by recipient point
+    const int* visc_off;     // npts + 1
+    const long* visc_src;    // global point index of donor
+    const double* visc_w;
+    // fringe exchange (copies): dst/src global point indices
+    const long* x_dst;
+    const long* x_src;
+    long n_x;
+    // classifier weights
+    const double* mlp;       // kMlpWeights
+    StepScalars* sc;
+};
+
+// FC plans for the two line orientations (rows: n = ni, cols: n = nj)
+struct LinePlans {
+    FcPlanDev row, col;
+    int scr_row, scr_col;
+};
+
+int step_scr_cap(const FcPlanDev& pl);
+void launch_phase0(const EngineDev& E, bool step0, void* stream);
+void launch_phase1(const EngineDev& E, void* stream);
+void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* stream);
+void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream);
+void launch_bc(const EngineDev& E, void* stream);
+void launch_exchange(const EngineDev& E, void* stream);
+void launch_finalize_dt(const EngineDev& E, void* stream);
+void launch_advance(const EngineDev& E, void* stream);
+
+}  // namespace fcsg

@@ -1,0 +1,175 @@
+"""Engine mirror over the C ABI (fcs::run::Engine, include/fcs/runtime.hpp:79-127).
+
+``Engine(dec, ic, cfg)`` uploads the init-time data of a decomposition (see
+geometry.py), evaluates the initial condition, applies the ``apply_ic`` tail
+(enforce_bc + one exchange) and then advances FC-SDNN supersteps on the GPU:
+``run(n)``/``step()`` for whole steps, ``step_phase(phase, stage)`` /
+``reduce_dt()`` / ``advance()`` for the reference's phase-level hooks, and
+``get``/``set`` for fields in the reference's [nj][ni] layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from . import geometry as G
+from . import problems as P
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+DEFAULT_WEIGHTS = os.path.join(HERE, "data", "fcnn_v1.bin")
+
+
+class fcsg_engine_config(C.Structure):
+    _fields_ = [("cfl", C.c_double), ("T", C.c_double), ("n_cont", C.c_int), ("filter_alpha", C.c_double),
+                ("filter_p", C.c_int), ("filter_p_smear", C.c_int), ("visc_c", C.c_double * 4),
+                ("abs_floor", C.c_double), ("smear_radius", C.c_int), ("debug_rhs", C.c_int)]
+
+
+@dataclass
+class EngineConfig:
+    """include/fcs/runtime.hpp:59-73 (fields used by the step)."""
+
+    cfl: float = 0.5
+    T: float = math.inf
+    n_cont: int = 25
+    filter_alpha: float = 23.025850929940457
+    filter_p: int = 7
+    filter_p_smear: int = 2
+    visc_c: tuple = (1.5, 1.0, 0.25, 0.0)
+    abs_floor: float = 1e-4
+    smear_radius: int = 10
+    max_steps: int = 10 ** 9
+    weights: str = DEFAULT_WEIGHTS
+    debug_rhs: bool = False
+
+
+def _bc_arrays(d: G.SubData):
+    ends = list(d.bc_row_lo) + list(d.bc_row_hi) + list(d.bc_col_lo) + list(d.bc_col_hi)
+    kind = np.array([-1 if e is None else e[0] for e in ends], dtype=np.int32)
+    state = np.zeros((len(ends), 4))
+    press = np.ones(len(ends))
+    for k, e in enumerate(ends):
+        if e is not None:
+            state[k] = e[1]
+            press[k] = e[2]
+    return kind, np.ascontiguousarray(state), press
+
+
+class Engine:
+    def __init__(self, ctx: N.Context, dec: G.Decomposition, ic=None, cfg: EngineConfig = EngineConfig(),
+                 initial_states=None):
+        self.ctx, self.dec, self.cfg = ctx, dec, cfg
+        L = ctx.lib
+        c = fcsg_engine_config(cfg.cfl, cfg.T, cfg.n_cont, cfg.filter_alpha, cfg.filter_p, cfg.filter_p_smear,
+                               (C.c_double * 4)(*cfg.visc_c), cfg.abs_floor, cfg.smear_radius, int(cfg.debug_rhs))
+        h = C.c_void_p()
+        ctx.check(L.fcsg_engine_create(ctx.h, C.byref(c), C.byref(h)))
+        self.h = h
+        self.shape = (dec.subs[0].nj, dec.subs[0].ni)
+        for d in dec.subs:
+            kind, state, press = _bc_arrays(d)
+            arr = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                   (d.iq1x, d.iq2x, d.iq1y, d.iq2y, d.h_min, d.h_max, d.w_norm)]
+            mask = np.ascontiguousarray(d.mask, dtype=np.uint8)
+            sid = C.c_int()
+            ctx.check(L.fcsg_engine_add_subpatch(
+                h, d.patch, d.sp.i0, d.sp.j0, d.ni, d.nj, d.h1, d.h2, mask.ctypes.data_as(C.POINTER(C.c_uint8)),
+                *[N.dptr(a) for a in arr], kind.ctypes.data_as(N.ip), N.dptr(state), N.dptr(press), C.byref(sid)))
+        pl = dec.plan
+        ptr = lambda a: np.ascontiguousarray(a, dtype=np.int32).ctypes.data_as(N.ip)
+        keep = [np.ascontiguousarray(a, dtype=np.int32) for a in
+                (pl.sol_dst_sub, pl.sol_dst, pl.sol_src_sub, pl.sol_src, pl.v_dst_sub, pl.v_dst, pl.v_src_sub,
+                 pl.v_src)]
+        vw = np.ascontiguousarray(pl.v_w, dtype=np.float64)
+        ctx.check(L.fcsg_engine_set_plan(h, len(keep[0]), *[k.ctypes.data_as(N.ip) for k in keep[:4]],
+                                         len(keep[4]), *[k.ctypes.data_as(N.ip) for k in keep[4:]], N.dptr(vw)))
+        ctx.check(L.fcsg_engine_load_mlp(h, cfg.weights.encode()))
+        ctx.check(L.fcsg_engine_finalize(h))
+        if initial_states is None and ic is not None:
+            initial_states = [P.initial_state(dec, ic, k) for k in range(len(dec.subs))]
+        if initial_states is not None:
+            for k, e in enumerate(initial_states):
+                self.set_state(k, e)
+            self.finish_ic()
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.fcsg_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state access --------------------------------------------------
+    def set_state(self, sub, e):
+        e = np.ascontiguousarray(e, dtype=np.float64)
+        self.ctx.check(self.ctx.lib.fcsg_engine_set_state(self.h, sub, N.dptr(e)))
+
+    def get(self, sub, name, comp=0):
+        out = np.empty(self.shape)
+        self.ctx.check(self.ctx.lib.fcsg_engine_get_field(self.h, sub, name.encode(), comp, N.dptr(out)))
+        return out
+
+    def get_state(self, sub, name="e"):
+        return np.stack([self.get(sub, name, c) for c in range(4)])
+
+    def set(self, sub, name, arr, comp=0):
+        a = np.ascontiguousarray(arr, dtype=np.float64)
+        self.ctx.check(self.ctx.lib.fcsg_engine_set_field(self.h, sub, name.encode(), comp, N.dptr(a)))
+
+    def finish_ic(self):
+        self.ctx.check(self.ctx.lib.fcsg_engine_finish_ic(self.h))
+
+    # ---- stepping --------------------------------------------------------
+    def step_phase(self, phase, stage=0):
+        self.ctx.check(self.ctx.lib.fcsg_engine_phase(self.h, phase, stage))
+
+    def reduce_dt(self):
+        dt = C.c_double()
+        self.ctx.check(self.ctx.lib.fcsg_engine_reduce_dt(self.h, C.byref(dt)))
+        return dt.value
+
+    def advance(self):
+        self.ctx.check(self.ctx.lib.fcsg_engine_advance(self.h))
+
+    def step_by_phases(self):
+        """One superstep through the phase hooks, in Engine::run order."""
+        self.step_phase(0)
+        self.step_phase(1)
+        self.step_phase(2)
+        self.reduce_dt()
+        for s in range(5):
+            self.step_phase(3, s)
+            self.step_phase(6)
+        self.advance()
+
+    def run(self, n_steps, use_graph=True):
+        done = C.c_long()
+        self.ctx.check(self.ctx.lib.fcsg_engine_run(self.h, n_steps, int(use_graph), C.byref(done)))
+        return done.value
+
+    def enqueue(self, n_steps):
+        self.ctx.check(self.ctx.lib.fcsg_engine_enqueue(self.h, n_steps))
+
+    def time(self):
+        t, st = C.c_double(), C.c_long()
+        self.ctx.check(self.ctx.lib.fcsg_engine_time(self.h, C.byref(t), C.byref(st)))
+        return t.value, st.value
+
+    def total_points(self):
+        n = C.c_long()
+        self.ctx.check(self.ctx.lib.fcsg_engine_total_points(self.h, C.byref(n)))
+        return n.value
+
+    def stream(self):
+        s = C.c_void_p()
+        self.ctx.check(self.ctx.lib.fcsg_engine_stream(self.h, C.byref(s)))
+        return s.value

@@ -1,0 +1,141 @@
+"""Synthetic BASELINE workloads (host side): decompositions + seeded initial data.
+
+No dataset is involved: BASELINE.json's configurations are synthetic, and the
+seeded generators here produce them with the stated shapes and value ranges.
+Random numbers use splitmix64 with uniform() = (next() >> 11) * 2^-53, the
+same generator as the reference's private Rng (src/viscosity.cpp:300-313).
+
+* ``fc_lines_config1``  config 1: 4096 lines of N=256 on [0,1],
+  f = sum_k a_k sin(w_k x + phi_k) + sum_j b_j x^j.
+* ``riemann_quadrants`` config 2: one 512x512 I patch on [0,1]^2, four-quadrant
+  Riemann data split at (0.5, 0.5), zero_normal_all sides (as riemann4,
+  src/problems.cpp:57-81), CFL 0.5.
+* ``vortex_tiles``      config 5: one I patch tiled by 256x256 subpatches
+  (subdivide_Q(r, s, 238, 9): 19-point intra-patch overlap), isentropic vortex
+  plus 1e-3 seeded noise on the primitives.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import geometry as G
+
+GAMMA = 1.4
+MASK64 = (1 << 64) - 1
+
+
+class SplitMix64:
+    """src/viscosity.cpp:300-313"""
+
+    def __init__(self, seed: int):
+        self.s = seed & MASK64 if seed else 0x9E3779B97F4A7C15
+
+    def next(self) -> int:
+        self.s = (self.s + 0x9E3779B97F4A7C15) & MASK64
+        z = self.s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & MASK64
+        return z ^ (z >> 31)
+
+    def uniform(self, a=0.0, b=1.0) -> float:
+        return a + (b - a) * ((self.next() >> 11) * 2.0 ** -53)
+
+
+def splitmix_uniform_array(seeds: np.ndarray, k: int) -> np.ndarray:
+    """k uniforms in [0,1) per seed (vectorised splitmix64, uint64 wraparound)."""
+    s = seeds.astype(np.uint64).copy()
+    out = np.empty(seeds.shape + (k,))
+    with np.errstate(over="ignore"):
+        for j in range(k):
+            s = s + np.uint64(0x9E3779B97F4A7C15)
+            z = s.copy()
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+            out[..., j] = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return out
+
+
+def conservative(rho, u, v, p):
+    """src/euler.cpp:10-12"""
+    return np.stack(np.broadcast_arrays(rho, rho * u, rho * v, p / (GAMMA - 1.0) + 0.5 * rho * (u * u + v * v)))
+
+
+def fc_lines_config1(n_lines=4096, n=256, seed=1):
+    rng = SplitMix64(seed)
+    x = np.arange(n) / (n - 1)
+    f = np.zeros((n_lines, n))
+    df = np.zeros((n_lines, n))
+    for l in range(n_lines):
+        for _ in range(4):
+            a, w, ph = rng.uniform(-1, 1), rng.uniform(1, 20), rng.uniform(0, 2 * math.pi)
+            f[l] += a * np.sin(w * x + ph)
+            df[l] += a * w * np.cos(w * x + ph)
+        b = [rng.uniform(-1, 1) for _ in range(4)]
+        for j in range(4):
+            f[l] += b[j] * x ** j
+            if j:
+                df[l] += j * b[j] * x ** (j - 1)
+    return x, f, df
+
+
+def riemann_quadrants(n=512, seed=2, nv=9):
+    """BASELINE config 2 (n=512) or a smaller n for parity tests."""
+    zero_normal = G.BcSpec(G.ZERO_NORMAL_ALL)
+    dec = G.rect_decomposition((0.0, 0.0), 1.0, 1.0, 1, 1, n - 2 * nv, nv, [zero_normal] * 4)
+    rng = SplitMix64(seed)
+    q = [(rng.uniform(0.1, 1.5), rng.uniform(-0.75, 0.75), rng.uniform(-0.75, 0.75), rng.uniform(0.03, 1.5))
+         for _ in range(4)]
+
+    def ic(x, y):
+        e = np.zeros((4,) + x.shape)
+        quads = [(x >= 0.5) & (y >= 0.5), (x < 0.5) & (y >= 0.5), (x < 0.5) & (y < 0.5), (x >= 0.5) & (y < 0.5)]
+        for k, m in enumerate(quads):
+            e[:, m] = np.asarray(conservative(*q[k]), dtype=np.float64).reshape(4, 1)
+        return e
+
+    return dec, ic, {"cfl": 0.5, "quadrant_states": q}
+
+
+def vortex_tiles(r=8, s=8, seed=5, n0=238, nv=9, noise=1e-3, beta=5.0):
+    """BASELINE config 5: an (r x s) tiling of 256x256 subpatches (n0=238)."""
+    zero_normal = G.BcSpec(G.ZERO_NORMAL_ALL)
+    h = 1.0 / (n0 - 1)  # fixed spacing: each preliminary cell is a unit square
+    lx = (r * (n0 - 1) + 2 * nv) * h
+    ly = (s * (n0 - 1) + 2 * nv) * h
+    dec = G.rect_decomposition((0.0, 0.0), lx, ly, r, s, n0, nv, [zero_normal] * 4)
+    p = dec.patches[0]
+    xc, yc = 0.5 * lx, 0.5 * ly
+    R = 0.25 * min(lx, ly) / 2.0  # vortex radius scale
+
+    def ic(x, y, I=None, J=None):
+        dx, dy = (x - xc) / R, (y - yc) / R
+        r2 = dx * dx + dy * dy
+        f = beta / (2 * math.pi) * np.exp(0.5 * (1 - r2))
+        u = -dy * f * 0.2
+        v = dx * f * 0.2
+        T = 1.0 - (GAMMA - 1.0) * (0.2 * beta) ** 2 / (8 * GAMMA * math.pi ** 2) * np.exp(1 - r2)
+        rho = T ** (1.0 / (GAMMA - 1.0))
+        pr = rho * T
+        if noise and I is not None:
+            lid = (I.astype(np.int64) * p.np2 + J.astype(np.int64)) + np.int64(seed) * np.int64(1 << 40)
+            un = splitmix_uniform_array(lid, 4) * 2.0 - 1.0
+            rho = rho * (1 + noise * un[..., 0])
+            u = u + noise * un[..., 1]
+            v = v + noise * un[..., 2]
+            pr = pr * (1 + noise * un[..., 3])
+        return conservative(rho, u, v, pr)
+
+    return dec, ic, {"cfl": 0.5}
+
+
+def initial_state(dec, ic, sub):
+    """Evaluate an IC on one subpatch (Engine::apply_ic, src/runtime.cpp:276-283)."""
+    d = dec.subs[sub]
+    try:
+        I, J = np.meshgrid(np.arange(d.sp.i0, d.sp.i1 + 1), np.arange(d.sp.j0, d.sp.j1 + 1))
+        return np.ascontiguousarray(ic(d.x, d.y, I, J))
+    except TypeError:
+        return np.ascontiguousarray(ic(d.x, d.y))
