@@ -1,0 +1,328 @@
+"""Benchmark: fp64 grid-point RK-stage updates/s of the FC-SDNN superstep.
+
+Workload (BASELINE config 5, weak scaling): per GPU one 8x8 tiling of 256x256
+subpatches (subdivide_Q(8, 8, 238, 9): 64 subpatches, 4,194,304 points,
+19-point intra-patch overlap), isentropic vortex + 1e-3 seeded noise, ANN
+(SDNN) classifier, CFL 0.5. A "step" is one full superstep (viscosity,
+blend, filter, 5 x (RHS + SSPRK stage + BC + exchange)); the metric counts
+5 x points per step (pt-stage), points counted with overlap multiplicity as
+the reference and the paper do (src/runtime.cpp:41-45).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fcsg|reference]
+
+--impl reference times the reference's own CPU Engine (the unmodified
+sources compiled into oracle/_ref) on the same workload and metric, with all
+host threads, on a bounded sample per step (see SAMPLE below).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "fp64 grid-point RK-stage updates/s"
+UNIT = "pt-stage/s"
+# paper Table 2, one 54-core Xeon node, weak/refinement N=550,854
+PAPER_1NODE = 6.74e7
+R_TILES, S_TILES = 8, 8
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device=0):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(rank_tiles=(R_TILES, S_TILES)):
+    from paper_2506_19370_b200 import problems as P
+
+    return P.vortex_tiles(r=rank_tiles[0], s=rank_tiles[1])
+
+
+# --------------------------------------------------------------------------
+# reference arm: the reference's own CPU Engine (oracle/_ref)
+
+SAMPLE_TILES = (4, 2)  # 8 subpatches of 256x256 (524,288 points) per timed step
+
+
+def reference_engine(tiles, threads):
+    from oracle import ref
+    from paper_2506_19370_b200 import engine as EN, problems as P
+
+    dec, ic, _ = P.vortex_tiles(r=tiles[0], s=tiles[1])
+    p = dec.patches[0]
+    R = ref.RefEngine(p.origin[0], p.origin[1], p.e1[0], p.e2[1], tiles[0], tiles[1], 238, p.nv, [5, 5, 5, 5],
+                      cfl=0.5, workers=threads, weight_path=EN.DEFAULT_WEIGHTS)
+    for k in range(len(dec.subs)):
+        R.set_state(k, P.initial_state(dec, ic, k))
+    R.finish_ic()
+    return R, dec.total_points()
+
+
+def cpu_rate(steps, warmup, threads):
+    R, npts = reference_engine(SAMPLE_TILES, threads)
+    if warmup:
+        R.run(warmup)
+    wall, n, _ = R.run(R.time()[1] + steps)
+    return 5.0 * npts * n / wall, wall / max(n, 1), npts
+
+
+def run_reference(args):
+    world, rank, _ = dist_init()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    rate, sps, npts = cpu_rate(args.steps, args.warmup, threads)
+    sample = (f"reference Engine::run (oracle/_ref: unmodified reference sources, FFTW replaced by the "
+              f"oracle/shims mixed-radix FFT), {SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} tiles of 256x256 "
+              f"({npts} points) of the config-5 workload per step, {threads} worker threads")
+    out = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": sps * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": rate / PAPER_1NODE, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": "config5-weak (sampled)", "tiles_per_step": list(SAMPLE_TILES)},
+           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+           "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# --------------------------------------------------------------------------
+# product arm
+
+
+ALG_BYTES = {  # algorithmic bytes per point per launch
+    "pass_a": 32 + 16 + 1 + 64,
+    "pass_b": 32 + 32 + 32 + 32 + 8 + 96,
+    "pass_c": 64 + 32 + 16 + 32 + 32 + 64,
+    "viscosity": 32 + 1 + 8 + 8 + 32,
+    "filter": 32 + 32 + 32 + 32 + 8,
+    "blend": 8 * 5 + 1 + 8,
+}
+LAUNCHES = {"pass_a": 5, "pass_b": 5, "pass_c": 5, "viscosity": 1, "filter": 1, "blend": 1, "bc": 6,
+            "exchange": 5}
+
+
+def fc_derivative_gbs(ctx):
+    """config 1 operator (4096 lines x N=256, reference operator n_cont=25)
+    from HBM to HBM, rotating buffers larger than L2 between launches."""
+    import torch
+
+    from paper_2506_19370_b200 import fc, problems as P
+
+    op = fc.FcOperator(ctx, 256)
+    _, f, _ = P.fc_lines_config1(n_lines=4096, n=256, seed=1)
+    src = torch.from_numpy(f).cuda()
+    nbuf = 16  # 16 x 2 x 8 MiB = 256 MiB > 126 MB L2
+    ins = [src.clone() for _ in range(nbuf)]
+    outs = [torch.empty_like(src) for _ in range(nbuf)]
+    for k in range(4):
+        op.apply(ins[k], 1, out=outs[k])
+    torch.cuda.synchronize()
+    reps = 64
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for k in range(reps):
+        op.apply(ins[k % nbuf], 1, out=outs[k % nbuf])
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    return 16.0 * f.size / (ms * 1e-3) / 1e9, ms
+
+
+def run_fcsg(args):
+    import torch
+
+    world, rank, local = dist_init()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    from paper_2506_19370_b200 import _native as N, engine as EN
+
+    ctx = N.Context(local)
+    dec, ic, _ = workload()
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+    npts = E.total_points()
+    stream = torch.cuda.ExternalStream(E.stream(), device=local)
+
+    # warm-up (includes the t=0 smear step and the CUDA-graph capture)
+    E.enqueue(max(args.warmup, 3))
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        E.enqueue(args.steps)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    t_now, steps_done = E.time()
+    E.run(0)  # surfaces a device-side InvalidStateError, if any
+    ms_step = ms_total / args.steps
+    value = 5.0 * npts * world * args.steps / (ms_total * 1e-3)
+
+    # e2e through the public API with HOST buffers: per step, H2D of the state
+    # from pinned memory, one superstep (fcsg_engine_run, which also checks the
+    # device error word), D2H of the resulting state
+    host_in = torch.empty((4, npts), dtype=torch.float64, pin_memory=True)
+    host_out = torch.empty((4, npts), dtype=torch.float64, pin_memory=True)
+    E.get_state_bulk(host_in)
+    e2e_steps = max(2, min(args.steps, 10))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        E.set_state_bulk(host_in)
+        E.run(1)
+        E.get_state_bulk(host_out)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = 5.0 * npts * world * e2e_steps / e2e_s
+    nbytes = 4 * npts * 8
+
+    # per-kernel-group device time (profiling hook, same engine and stream)
+    groups = {}
+    for g in ("viscosity", "blend", "filter", "pass_a", "pass_b", "pass_c", "bc", "exchange"):
+        groups[g] = E.time_group(g, reps=5)
+    share = {g: groups[g] * LAUNCHES[g] for g in groups}
+    dom = max(share, key=share.get)
+    hbm, peak_kind = peaks()
+    alg = ALG_BYTES.get(dom, 64) * npts
+    achieved = alg / (groups[dom] * 1e-3) / 1e9
+    fc_gbs, fc_ms = fc_derivative_gbs(ctx)
+
+    if rank != 0:
+        return
+    # CPU baseline: the reference on this box's host cores, bounded sample
+    cpu = None
+    if not args.no_cpu:
+        try:
+            threads = os.cpu_count() or 1
+            rate, sps, cnpts = cpu_rate(1, 0, threads)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"1 superstep of {SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} tiles of 256x256 ({cnpts} points) "
+                             f"of the same workload, reference Engine with {threads} worker threads "
+                             f"(oracle/_ref; FFTW replaced by the oracle/shims FFT)"}
+        except Exception as ex:  # the reference build is test infrastructure
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / PAPER_1NODE,
+        "vs_baseline_basis": "PAPER.md:1612 (BASELINE.md): 6.74e7 pt-stage/s, one 54-core Xeon 8273 node",
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config5-weak: {R_TILES}x{S_TILES} tiles of 256x256 per GPU "
+                               f"({npts} points/GPU, 19-point overlap), vortex + 1e-3 noise, ANN classifier, CFL 0.5",
+                   "points_per_gpu": npts, "l2": "working set ~1.7 GB/GPU >> 126 MB L2 (no flush needed)",
+                   "cuda_graph": True},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+                "steps": e2e_steps, "path": "fcsg_engine_set_state_bulk + fcsg_engine_run + fcsg_engine_get_state_bulk"},
+        "gpu_launches": E.launches_per_step() * args.steps,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "alg_bytes_per_point": ALG_BYTES.get(dom), "ms_per_launch": groups[dom]},
+        "kernel_groups_ms": groups,
+        "fc_derivative": {"config": "config1: 4096 lines x N=256, n_cont=25 (n_ext=280), d/dx, HBM->HBM",
+                          "gbs": fc_gbs, "us_per_call": fc_ms * 1e3, "frac_of_hbm": fc_gbs / hbm},
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "sim_time": t_now, "steps_run": steps_done,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fcsg", choices=["fcsg", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fcsg(args)
+
+
+if __name__ == "__main__":
+    main()

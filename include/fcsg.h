@@ -153,6 +153,10 @@ int fcsg_engine_set_state(fcsg_engine* eng, int sub, const double* e4);
 /* fields: "e","e0","e2","e3","rhs3","rhs" (comp 0..3), "mu_hat","mu","tau",
  * "speed","proxy","m01","iq1x","iq2x","iq1y","iq2y","h_min","h_max","w_norm" */
 int fcsg_engine_get_field(fcsg_engine* eng, int sub, const char* name, int comp, double* out);
+/* whole state of every subpatch in one call, component-major host layout
+ * [4][S][nj][ni] (pinned host memory gives full PCIe/C2C bandwidth) */
+int fcsg_engine_set_state_bulk(fcsg_engine* eng, const double* e);
+int fcsg_engine_get_state_bulk(fcsg_engine* eng, double* e);
 int fcsg_engine_set_field(fcsg_engine* eng, int sub, const char* name, int comp, const double* in);
 /* apply_ic tail: enforce_bc on every subpatch, then one fringe exchange (src/runtime.cpp:284-286) */
 int fcsg_engine_finish_ic(fcsg_engine* eng);
@@ -174,6 +178,12 @@ int fcsg_engine_time(fcsg_engine* eng, double* t, long* steps);
 int fcsg_engine_total_points(fcsg_engine* eng, long* n);
 /* the engine's CUDA stream (cudaStream_t), for event timing by the caller */
 int fcsg_engine_stream(fcsg_engine* eng, void** stream);
+/* profiling hooks: average device ms of one launch group over `reps`
+ * back-to-back launches (0 viscosity/classifier, 1 blend+dt, 2 filter,
+ * 3 pass A, 4 pass B, 5 pass C, 6 BC, 7 exchange), and the number of kernel
+ * launches one superstep issues */
+int fcsg_engine_time_group(fcsg_engine* eng, int which, int reps, double* ms);
+int fcsg_engine_launches_per_step(fcsg_engine* eng, int* n);
 
 #ifdef __cplusplus
 }

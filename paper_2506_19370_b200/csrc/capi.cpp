@@ -404,3 +404,31 @@ int fcsg_engine_stream(fcsg_engine* e, void** stream) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+int fcsg_engine_time_group(fcsg_engine* e, int which, int reps, double* ms) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { *ms = e->eng->time_pass(which, reps); });
+}
+
+int fcsg_engine_launches_per_step(fcsg_engine* e, int* n) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { *n = kLaunchesPerStep; });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int fcsg_engine_set_state_bulk(fcsg_engine* e, const double* e4s) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->set_state_bulk(e4s); });
+}
+
+int fcsg_engine_get_state_bulk(fcsg_engine* e, double* out) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->get_state_bulk(out); });
+}
+
+}  // extern "C"

@@ -42,6 +42,12 @@ void d2h(void* dst, const void* src, size_t bytes, void* stream) {
     ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)), "d2h");
     ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "d2h sync");
 }
+void h2d_async(void* dst, const void* src, size_t bytes, void* stream) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)), "h2d");
+}
+void d2h_async(void* dst, const void* src, size_t bytes, void* stream) {
+    ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)), "d2h");
+}
 void d2d(void* dst, const void* src, size_t bytes, void* stream) {
     ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)), "d2d");
 }
@@ -70,6 +76,22 @@ void graph_destroy(void* exec, void* graph) {
     if (graph) cudaGraphDestroy(static_cast<cudaGraph_t>(graph));
 }
 
+double time_on_stream(void* stream, void (*fn)(void*), void* arg) {
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ck(cudaEventRecord(a, s), "record");
+    fn(arg);
+    ck(cudaEventRecord(b, s), "record");
+    ck(cudaEventSynchronize(b), "event sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms;
+}
+
 #else
 
 bool is_cuda() { return false; }
@@ -81,6 +103,8 @@ void free(void* p) { std::free(p); }
 void h2d(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }
 void d2h(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }
 void d2d(void* dst, const void* src, size_t bytes, void*) { std::memmove(dst, src, bytes); }
+void h2d_async(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }
+void d2h_async(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }
 void memset0(void* p, size_t bytes, void*) { std::memset(p, 0, bytes); }
 void sync(void*) {}
 void sync_device() {}
@@ -89,6 +113,10 @@ void graph_begin(void*) {}
 void graph_end(void*, void**, void**) {}
 void graph_launch(void*, void*) {}
 void graph_destroy(void*, void*) {}
+double time_on_stream(void*, void (*fn)(void*), void* arg) {
+    fn(arg);
+    return 0.0;
+}
 
 #endif
 

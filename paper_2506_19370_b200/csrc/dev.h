@@ -16,6 +16,9 @@ void* alloc(size_t bytes);
 void free(void* p);
 void h2d(void* dst, const void* src, size_t bytes, void* stream);
 void d2h(void* dst, const void* src, size_t bytes, void* stream);
+// enqueue only (no stream sync)
+void h2d_async(void* dst, const void* src, size_t bytes, void* stream);
+void d2h_async(void* dst, const void* src, size_t bytes, void* stream);
 void d2d(void* dst, const void* src, size_t bytes, void* stream);
 void memset0(void* p, size_t bytes, void* stream);
 void sync(void* stream);
@@ -28,6 +31,8 @@ void graph_begin(void* stream);
 void graph_end(void* stream, void** graph, void** exec);
 void graph_launch(void* exec, void* stream);
 void graph_destroy(void* exec, void* graph);
+// elapsed milliseconds of work enqueued on `stream` by fn()
+double time_on_stream(void* stream, void (*fn)(void*), void* arg);
 
 template <class T>
 T* alloc_n(size_t n) {

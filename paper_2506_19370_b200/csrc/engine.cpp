@@ -280,6 +280,18 @@ void Engine::set_state(int sub, const double* e4) {
     for (int c = 0; c < 4; ++c) dev::h2d(E_.e[c] + sub * sz, e4 + c * sz, sz * sizeof(double), ctx_.stream);
 }
 
+void Engine::set_state_bulk(const double* e) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    for (int c = 0; c < 4; ++c) dev::h2d_async(E_.e[c], e + c * npts_, npts_ * sizeof(double), ctx_.stream);
+    dev::sync(ctx_.stream);
+}
+
+void Engine::get_state_bulk(double* e) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    for (int c = 0; c < 4; ++c) dev::d2h_async(e + c * npts_, E_.e[c], npts_ * sizeof(double), ctx_.stream);
+    dev::sync(ctx_.stream);
+}
+
 void Engine::get_field(int sub, const std::string& name, int comp, double* out) {
     if (sub < 0 || sub >= E_.S) throw Error(kUsage, "bad subpatch id");
     const long sz = static_cast<long>(ni_) * nj_;
@@ -370,6 +382,40 @@ void Engine::enqueue_step(bool step0) {
         launch_exchange(E_, s);
     }
     launch_advance(E_, s);
+}
+
+void Engine::launch_group(int which) {
+    void* s = ctx_.stream;
+    switch (which) {
+        case 0: launch_phase0(E_, false, s); break;
+        case 1: launch_phase1(E_, s); break;
+        case 2: launch_phase2(E_, plans_, false, s); break;
+        case 3: launch_pass_a(E_, plans_, s); break;
+        case 4: launch_pass_b(E_, plans_, s); break;
+        case 5: launch_pass_c(E_, plans_, 1, s); break;
+        case 6: launch_bc(E_, s); break;
+        case 7: launch_exchange(E_, s); break;
+        default: throw Error(kUsage, "bad launch group");
+    }
+}
+
+double Engine::time_pass(int which, int reps) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    if (reps < 1) reps = 1;
+    launch_group(which);  // warm
+    struct Arg {
+        Engine* e;
+        int which, reps;
+    } a{this, which, reps};
+    const double ms = dev::time_on_stream(
+        ctx_.stream,
+        [](void* p) {
+            auto* q = static_cast<Arg*>(p);
+            for (int r = 0; r < q->reps; ++r) q->e->launch_group(q->which);
+        },
+        &a);
+    dev::check("time_pass");
+    return ms / reps;
 }
 
 void Engine::enqueue_steps(long n) {

@@ -60,6 +60,9 @@ class Engine {
     void finalize();
 
     void set_state(int sub, const double* e4);
+    // all subpatches at once, component-major host layout [4][S][nj][ni]
+    void set_state_bulk(const double* e);
+    void get_state_bulk(double* e);
     void get_field(int sub, const std::string& name, int comp, double* out);
     void set_field(int sub, const std::string& name, int comp, const double* in);
 
@@ -77,6 +80,12 @@ class Engine {
     long steps() const { return host_step_; }
     long total_points() const { return npts_; }
     void check_error();
+    // average device milliseconds of one launch group (profiling hook):
+    // 0 phase 0 (proxy + classifier), 1 phase 1 (blend + dt), 2 phase 2
+    // (filter rows + cols), 3 pass A, 4 pass B, 5 pass C (stage 1), 6 BC,
+    // 7 exchange
+    double time_pass(int which, int reps);
+    void launch_group(int which);
     void* stream() const { return ctx_.stream; }
 
   private:

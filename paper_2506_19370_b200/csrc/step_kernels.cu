@@ -748,6 +748,16 @@ void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* strea
     run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
 }
 
+void launch_pass_a(const EngineDev& E, const LinePlans& P, void* stream) {
+    run_line_pass<PassA>(0, E, P.row, P.scr_row, stream);
+}
+void launch_pass_b(const EngineDev& E, const LinePlans& P, void* stream) {
+    run_line_pass<PassB>(0, E, P.col, P.scr_col, stream);
+}
+void launch_pass_c(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
+    run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
+}
+
 void launch_bc(const EngineDev& E, void* stream) {
 #if FCSG_CUDA
     bc_kernel<<<E.S, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);

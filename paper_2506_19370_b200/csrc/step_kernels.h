@@ -90,6 +90,12 @@ void launch_phase0(const EngineDev& E, bool step0, void* stream);
 void launch_phase1(const EngineDev& E, void* stream);
 void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* stream);
 void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream);
+// the three line passes of a stage, separately (profiling hooks)
+void launch_pass_a(const EngineDev& E, const LinePlans& P, void* stream);
+void launch_pass_b(const EngineDev& E, const LinePlans& P, void* stream);
+void launch_pass_c(const EngineDev& E, const LinePlans& P, int stage, void* stream);
+// kernel launches per superstep (excluding the t=0 dilation)
+constexpr int kLaunchesPerStep = 33;
 void launch_bc(const EngineDev& E, void* stream);
 void launch_exchange(const EngineDev& E, void* stream);
 void launch_finalize_dt(const EngineDev& E, void* stream);

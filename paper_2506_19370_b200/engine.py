@@ -113,6 +113,17 @@ class Engine:
         e = np.ascontiguousarray(e, dtype=np.float64)
         self.ctx.check(self.ctx.lib.fcsg_engine_set_state(self.h, sub, N.dptr(e)))
 
+    def set_state_bulk(self, e):
+        """all subpatches, [4][S][nj][ni]; ``e`` may be a numpy array or a
+        (pinned) CPU torch tensor"""
+        ptr = e.data_ptr() if hasattr(e, "data_ptr") else np.ascontiguousarray(e, dtype=np.float64).ctypes.data
+        self.ctx.check(self.ctx.lib.fcsg_engine_set_state_bulk(self.h, C.c_void_p(ptr)))
+
+    def get_state_bulk(self, out):
+        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        self.ctx.check(self.ctx.lib.fcsg_engine_get_state_bulk(self.h, C.c_void_p(ptr)))
+        return out
+
     def get(self, sub, name, comp=0):
         out = np.empty(self.shape)
         self.ctx.check(self.ctx.lib.fcsg_engine_get_field(self.h, sub, name.encode(), comp, N.dptr(out)))
@@ -167,6 +178,20 @@ class Engine:
     def total_points(self):
         n = C.c_long()
         self.ctx.check(self.ctx.lib.fcsg_engine_total_points(self.h, C.byref(n)))
+        return n.value
+
+    GROUPS = ("viscosity", "blend", "filter", "pass_a", "pass_b", "pass_c", "bc", "exchange")
+
+    def time_group(self, which, reps=10):
+        """average device ms of one launch of a kernel group (profiling hook)"""
+        idx = self.GROUPS.index(which) if isinstance(which, str) else which
+        ms = C.c_double()
+        self.ctx.check(self.ctx.lib.fcsg_engine_time_group(self.h, idx, reps, C.byref(ms)))
+        return ms.value
+
+    def launches_per_step(self):
+        n = C.c_int()
+        self.ctx.check(self.ctx.lib.fcsg_engine_launches_per_step(self.h, C.byref(n)))
         return n.value
 
     def stream(self):
