@@ -672,12 +672,17 @@ class Engine:
     def exchange(self):
         """phase 6 (src/runtime.cpp:433-454), copies only; every donor read
         happens after all stage updates (barrier)."""
-        src_e = [d.e.reshape(4, -1).copy() for d in self.subs]
+        src_e = [np.ascontiguousarray(d.e).reshape(4, -1).copy() for d in self.subs]
         for k, d in enumerate(self.subs):
             dst, src_sub, src = self.plan.sol[k]
-            ef = d.e.reshape(4, -1)
-            for n in range(len(dst)):
-                ef[:, dst[n]] = src_e[src_sub[n]][:, src[n]]
+            if len(dst) == 0:
+                continue
+            e = np.ascontiguousarray(d.e)  # reshape below must be a view
+            ef = e.reshape(4, -1)
+            for s in np.unique(src_sub):
+                m = src_sub == s
+                ef[:, dst[m]] = src_e[s][:, src[m]]
+            d.e = e
 
     def step(self):
         self.phase0()
