@@ -154,26 +154,7 @@ std::vector<double> build_blend_matrix(int n_cont, int d) {
     return A;
 }
 
-namespace {
 
-std::vector<int> factor_stages(int n) {
-    std::vector<int> f;
-    int m = n;
-    while (m % 8 == 0) { f.push_back(8); m /= 8; }
-    if (m % 4 == 0) { f.push_back(4); m /= 4; }
-    if (m % 2 == 0) { f.push_back(2); m /= 2; }
-    while (m % 9 == 0) { f.push_back(9); m /= 9; }
-    for (int p : {3, 5, 7, 11, 13})
-        while (m % p == 0) { f.push_back(p); m /= p; }
-    for (int p = 17; p * p <= m; p += 2)
-        while (m % p == 0) { f.push_back(p); m /= p; }
-    if (m > 1) f.push_back(m);
-    if (f.empty()) f.push_back(1);
-    if (static_cast<int>(f.size()) > kMaxStages) throw Error(kConfig, "FFT plan: too many stages");
-    return f;
-}
-
-}  // namespace
 
 FcTables build_fc_tables(int n_points, int n_cont, int degree, FilterSpec f) {
     // FcOperator ctor checks (src/fc_core.cpp:192-193)
@@ -199,11 +180,10 @@ FcTables build_fc_tables(int n_points, int n_cont, int degree, FilterSpec f) {
         t.smear_profile[k] = std::exp(-f.alpha * std::pow(r, 2.0 * f.p_smear));
     }
     // FFT plan: DIF stages, span L_0 = n, L_{s+1} = L_s / p_s
-    t.radix = factor_stages(n);
-    int L = n;
-    for (int p : t.radix) {
-        t.span.push_back(L);
-        L /= p;
+    const Factors fs = factor_stages(n);
+    for (int s = 0; s < fs.n; ++s) {
+        t.radix.push_back(fs.r[s]);
+        t.span.push_back(fs.span[s]);
     }
     t.tw.resize(n);
     for (int k = 0; k < n; ++k) {

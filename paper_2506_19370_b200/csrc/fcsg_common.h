@@ -75,6 +75,40 @@ FCSG_HD double2 cmulc(double2 a, double2 b) { return mk2(a.x * b.x + a.y * b.y, 
 FCSG_HD double2 cscale(double2 a, double s) { return mk2(a.x * s, a.y * s); }
 
 constexpr int kMaxStages = 12;
+
+// FFT stage radices of length n, largest-first among the register radices
+// (8, 4, 2, 9, 3, 5, 7, 11, 13), then the remaining primes (direct DFT).
+// Shared by the host tables (digit-reversal order of the multiplier table)
+// and the compile-time device plans, so both always agree.
+struct Factors {
+    int n = 0;
+    int r[kMaxStages] = {};
+    int span[kMaxStages] = {};
+};
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+constexpr Factors factor_stages(int len) {
+    Factors f{};
+    int m = len;
+    while (m % 8 == 0 && f.n < kMaxStages) { f.r[f.n++] = 8; m /= 8; }
+    if (m % 4 == 0) { f.r[f.n++] = 4; m /= 4; }
+    if (m % 2 == 0) { f.r[f.n++] = 2; m /= 2; }
+    while (m % 9 == 0 && f.n < kMaxStages) { f.r[f.n++] = 9; m /= 9; }
+    const int small[5] = {3, 5, 7, 11, 13};
+    for (int k = 0; k < 5; ++k)
+        while (m % small[k] == 0 && f.n < kMaxStages) { f.r[f.n++] = small[k]; m /= small[k]; }
+    for (int p = 17; p * p <= m; p += 2)
+        while (m % p == 0 && f.n < kMaxStages) { f.r[f.n++] = p; m /= p; }
+    if (m > 1 && f.n < kMaxStages) f.r[f.n++] = m;
+    if (f.n == 0) f.r[f.n++] = 1;
+    int L = len;
+    for (int s = 0; s < f.n; ++s) {
+        f.span[s] = L;
+        L /= f.r[s];
+    }
+    return f;
+}
 constexpr int kMaxGap = 64;     // n_cont - 1
 constexpr int kMaxDeg = 6;      // degree + 1 <= 7
 

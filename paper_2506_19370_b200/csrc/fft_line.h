@@ -237,7 +237,7 @@ FCSG_HD void stage_generic(Thr t, double2* buf, int pitch, int LB, int n, int L,
 #if FCSG_CUDA
 __host__ __device__
 #endif
-inline bool radix_in_registers(int p) {
+constexpr bool radix_in_registers(int p) {
     return p == 2 || p == 3 || p == 4 || p == 5 || p == 7 || p == 8 || p == 9 || p == 11 || p == 13;
 }
 
@@ -308,6 +308,129 @@ FCSG_HD void fc_transform(Thr t, double2* buf, int pitch, int LB, const FcPlanDe
         run_stage(t, buf, pitch, LB, n, pl.span[s], pl.radix[s], pl.tw, true, scr, scr_cap);
         FCSG_SYNC();
     }
+}
+
+// ---------------------------------------------------------------------------
+// compile-time plans for the hot lengths: every index computation below uses
+// constants (no runtime integer division), stages are unrolled at compile time
+
+template <int P, int L, int NE, int LB, int NTHR, bool INV>
+FCSG_HD void stage_reg_ct(int tid, double2* buf, const double2* tw) {
+    constexpr int m = L / P;
+    constexpr int total = (NE / P) * LB;
+    constexpr int tstep = NE / L;
+    constexpr int pitch = LB + 1;
+    constexpr int ms = m * pitch;
+    for (int w = tid; w < total; w += NTHR) {
+        const int line = w % LB;
+        const int b = w / LB;
+        const int blk = b / m;
+        const int j = b - blk * m;
+        double2* p = buf + (blk * L + j) * pitch + line;
+        double2 x[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) x[q] = p[q * ms];
+        if (!INV) {
+            dft_reg<P, false>(x, tw, NE);
+            if (m > 1 && j) {
+#pragma unroll
+                for (int q = 1; q < P; ++q) x[q] = cmul(x[q], ld2(tw + j * q * tstep));
+            }
+        } else {
+            if (m > 1 && j) {
+#pragma unroll
+                for (int q = 1; q < P; ++q) x[q] = cmulc(x[q], ld2(tw + j * q * tstep));
+            }
+            dft_reg<P, true>(x, tw, NE);
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) p[q * ms] = x[q];
+    }
+}
+
+template <int NE, int S, int LB, int NTHR, bool INV>
+FCSG_HD void stage_ct(int tid, double2* buf, const double2* tw, double2* scr, int scr_cap) {
+    constexpr Factors F = factor_stages(NE);
+    constexpr int P = F.r[S];
+    constexpr int L = F.span[S];
+    if constexpr (radix_in_registers(P)) {
+        stage_reg_ct<P, L, NE, LB, NTHR, INV>(tid, buf, tw);
+    } else {
+        stage_generic(Thr{tid, NTHR}, buf, LB + 1, LB, NE, L, P, tw, INV, scr, scr_cap);
+    }
+}
+
+template <int NE, int S, int LB, int NTHR>
+FCSG_HD void dif_stages_ct(int tid, double2* buf, const double2* tw, double2* scr, int scr_cap) {
+    constexpr Factors F = factor_stages(NE);
+    if constexpr (S < F.n) {
+        stage_ct<NE, S, LB, NTHR, false>(tid, buf, tw, scr, scr_cap);
+        FCSG_SYNC();
+        dif_stages_ct<NE, S + 1, LB, NTHR>(tid, buf, tw, scr, scr_cap);
+    }
+}
+
+template <int NE, int S, int LB, int NTHR>
+FCSG_HD void dit_stages_ct(int tid, double2* buf, const double2* tw, double2* scr, int scr_cap) {
+    if constexpr (S >= 0) {
+        stage_ct<NE, S, LB, NTHR, true>(tid, buf, tw, scr, scr_cap);
+        FCSG_SYNC();
+        dit_stages_ct<NE, S - 1, LB, NTHR>(tid, buf, tw, scr, scr_cap);
+    }
+}
+
+// compile-time continuation for the reference operator (n_cont = 25, d = 2)
+template <int N, int G, int D1, int LB, int NTHR>
+FCSG_HD void continuation_ct(int tid, double2* buf, const double* blend) {
+    constexpr int pitch = LB + 1;
+    for (int w = tid; w < G * LB; w += NTHR) {
+        const int line = w % LB;
+        const int jj = w / LB;
+        double2 a = mk2(0.0, 0.0), b = mk2(0.0, 0.0);
+        const double* Ar = blend + jj * D1;
+        const double* Al = blend + (G - 1 - jj) * D1;
+#pragma unroll
+        for (int i = 0; i < D1; ++i) {
+            const double2 fr = buf[(N - D1 + i) * pitch + line];
+            const double2 fl = buf[(D1 - 1 - i) * pitch + line];
+            const double cr = ld1(Ar + i), cl = ld1(Al + i);
+            a = mk2(a.x + cr * fr.x, a.y + cr * fr.y);
+            b = mk2(b.x + cl * fl.x, b.y + cl * fl.y);
+        }
+        buf[(N + jj) * pitch + line] = cadd(a, b);
+    }
+}
+
+template <int NE, int LB, int NTHR>
+FCSG_HD void spec_mult_ct(int tid, double2* buf, const double2* mult) {
+    constexpr int pitch = LB + 1;
+    for (int w = tid; w < NE * LB; w += NTHR) {
+        const int line = w % LB;
+        const int pos = w / LB;
+        double2* p = buf + pos * pitch + line;
+        *p = cmul(*p, ld2(mult + pos));
+    }
+}
+
+// fc_transform for n_ext = NE with the reference continuation (n_cont = 25,
+// degree 2): N = NE - 24.
+template <int NE, int LB, int NTHR>
+FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mode, double2* scr, int scr_cap) {
+    constexpr Factors F = factor_stages(NE);
+    continuation_ct<NE - 24, 24, 3, LB, NTHR>(tid, buf, pl.blend);
+    FCSG_SYNC();
+    dif_stages_ct<NE, 0, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+    spec_mult_ct<NE, LB, NTHR>(tid, buf, pl.mult + (mode - 1) * NE);
+    FCSG_SYNC();
+    dit_stages_ct<NE, F.n - 1, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+}
+
+// the lengths with a compile-time plan (reference operator, n_cont = 25)
+#if FCSG_CUDA
+__host__ __device__
+#endif
+constexpr bool has_ct_plan(int n_ext) {
+    return n_ext == 280 || n_ext == 536;
 }
 
 }  // namespace fcsg

@@ -88,43 +88,38 @@ FCSG_HD long pidx(const LineCtx& c, int l, int i) {
     return c.rows ? c.base + static_cast<long>(c.line0 + l) * c.ni + i : c.base + static_cast<long>(i) * c.ni + c.line0 + l;
 }
 
-template <int LB, class Pass>
+// One CTA owns LB lines of one subpatch (rows: stride-1 lines of length ni;
+// columns: stride-ni lines of length nj). For every round r of the pass it
+// loads two real quantities per point as one complex line, runs the FC
+// transform in shared memory and hands the scaled result to the pass's
+// epilogue. NE > 0 selects the compile-time plan for n_ext = NE (then
+// N = NE - 24); NE = 0 is the runtime-generic plan. NTHR is the CTA size
+// (1 in the CPU emulation harness). The epilogue of round r and the load of
+// round r+1 share one loop: each slot is read and rewritten by the same
+// thread, so no barrier is needed between them.
+template <int LB, class Pass, int NE, int NTHR>
 FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const EngineDev& E, const FcPlanDev& pl,
                        int scr_cap) {
     constexpr bool rows = Pass::kRows;
+    constexpr int pitch = LB + 1;
     const int ni = E.ni, nj = E.nj;
-    const int N = rows ? ni : nj;
+    const int N = NE > 0 ? NE - 24 : (rows ? ni : nj);
     const int nlines = rows ? nj : ni;
     const int bps = (nlines + LB - 1) / LB;
     LineCtx c;
     c.sub = block / bps;
-    c.line0 = (block % bps) * LB;
+    c.line0 = (block - c.sub * bps) * LB;
     c.nl_valid = (nlines - c.line0 < LB) ? nlines - c.line0 : LB;
     c.base = static_cast<long>(c.sub) * ni * nj;
     c.ni = ni;
     c.rows = rows;
-    const int pitch = LB + 1;
     double2* buf = smem;
-    double2* scr = smem + pl.n_ext * pitch;
+    double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
     const double inv_len = P.kScaled ? (rows ? E.inv_len1[c.sub] : E.inv_len2[c.sub]) : 1.0;
     const int total = N * LB;
-    for (int r = 0; r < Pass::kRounds; ++r) {
-        for (int w = t.tid; w < total; w += t.nthr) {
-            int i, l;
-            if (rows) {
-                i = w % N;
-                l = w / N;
-            } else {
-                l = w % LB;
-                i = w / LB;
-            }
-            double2 v = mk2(0.0, 0.0);
-            if (l < c.nl_valid) v = P.load(r, pidx(c, l, i), c, l, i);
-            buf[i * pitch + l] = v;
-        }
-        FCSG_SYNC();
-        fc_transform(t, buf, pitch, LB, pl, P.mode(r), scr, scr_cap);
-        for (int w = t.tid; w < total; w += t.nthr) {
+    const int tid = t.tid;
+    for (int r = 0; r <= Pass::kRounds; ++r) {
+        for (int w = tid; w < total; w += NTHR) {
             int i, l;
             if (rows) {
                 i = w % N;
@@ -134,13 +129,26 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
                 i = w / LB;
             }
             if (l < c.nl_valid) {
-                const double2 v = buf[i * pitch + l];
-                P.store(r, pidx(c, l, i), mk2(v.x * inv_len, v.y * inv_len), c, l, i);
+                const long p = pidx(c, l, i);
+                if (r > 0) {
+                    const double2 v = buf[i * pitch + l];
+                    P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), c, l, i);
+                }
+                if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c, l, i);
+            } else if (r < Pass::kRounds) {
+                buf[i * pitch + l] = mk2(0.0, 0.0);
             }
         }
+        if (r == Pass::kRounds) break;
         FCSG_SYNC();
+        if constexpr (NE > 0) {
+            fc_transform_ct<NE, LB, NTHR>(tid, buf, pl, P.mode(r), scr, scr_cap);
+        } else {
+            fc_transform(Thr{tid, NTHR}, buf, pitch, LB, pl, P.mode(r), scr, scr_cap);
+        }
     }
-    P.finish(t, c, N);
+    FCSG_SYNC();
+    P.finish(Thr{tid, NTHR}, c, N);
 }
 
 // conservative -> (theta, u, v, p) exactly as euler_rhs (src/euler.cpp:29-41,44-55)
@@ -387,10 +395,27 @@ FCSG_HD void proxy_body(Thr t, int block, int nblocks, const EngineDev& E) {
     }
 }
 
+// classifier weights: in the CUDA build they live in the constant bank (every
+// thread of a warp reads the same weight at the same time, so each DFMA takes
+// its weight straight from c[][]); refreshed from E.mlp before each launch
+#if FCSG_CUDA
+__constant__ double c_mlp[kMlpWeights];
+struct MlpW {
+    FCSG_HD double operator()(int k) const { return c_mlp[k]; }
+};
+#else
+struct MlpW {
+    const double* p;
+    double operator()(int k) const { return p[k]; }
+};
+#endif
+
 // MlpClassifier::forward + classify_stencil (src/viscosity.cpp:108-133) on a
 // raw 7-point stencil, with normalize_stencil's guard (src/viscosity.cpp:48-59)
-FCSG_HD int classify_stencil(const double* W, const double* s, double abs_floor) {
+template <class WA>
+FCSG_HD int classify_stencil(const WA& W, const double* s, double abs_floor) {
     double lo = s[0], hi = s[0];
+#pragma unroll
     for (int k = 1; k < kMlpIn; ++k) {
         lo = s[k] < lo ? s[k] : lo;
         hi = s[k] > hi ? s[k] : hi;
@@ -400,31 +425,42 @@ FCSG_HD int classify_stencil(const double* W, const double* s, double abs_floor)
     scale = scale > 1e-100 ? scale : 1e-100;
     if (span <= 1e-13 * scale || span <= abs_floor) return 4;
     double x[kMlpIn];
+#pragma unroll
     for (int k = 0; k < kMlpIn; ++k) x[k] = 2.0 * (s[k] - lo) / span - 1.0;
     double h[kMlpHidden], g[kMlpHidden];
-    const double* w = W;
+    constexpr int L0 = kMlpHidden * kMlpIn + kMlpHidden;     // layer 0 size (W then b)
+    constexpr int LH = kMlpHidden * kMlpHidden + kMlpHidden;  // hidden layer size
+#pragma unroll
     for (int i = 0; i < kMlpHidden; ++i) {
-        double acc = w[kMlpHidden * kMlpIn + i];
-        for (int j = 0; j < kMlpIn; ++j) acc += w[i * kMlpIn + j] * x[j];
+        double acc = W(kMlpHidden * kMlpIn + i);
+#pragma unroll
+        for (int j = 0; j < kMlpIn; ++j) acc += W(i * kMlpIn + j) * x[j];
         h[i] = tanh(acc);
     }
-    w += kMlpHidden * kMlpIn + kMlpHidden;
+#pragma unroll
     for (int layer = 0; layer < 3; ++layer) {
+        const int base = L0 + layer * LH;
+#pragma unroll
         for (int i = 0; i < kMlpHidden; ++i) {
-            double acc = w[kMlpHidden * kMlpHidden + i];
-            for (int j = 0; j < kMlpHidden; ++j) acc += w[i * kMlpHidden + j] * h[j];
+            double acc = W(base + kMlpHidden * kMlpHidden + i);
+#pragma unroll
+            for (int j = 0; j < kMlpHidden; ++j) acc += W(base + i * kMlpHidden + j) * h[j];
             g[i] = tanh(acc);
         }
+#pragma unroll
         for (int i = 0; i < kMlpHidden; ++i) h[i] = g[i];
-        w += kMlpHidden * kMlpHidden + kMlpHidden;
     }
+    constexpr int LO = L0 + 3 * LH;
     double lg[kMlpOut];
+#pragma unroll
     for (int i = 0; i < kMlpOut; ++i) {
-        double acc = w[kMlpOut * kMlpHidden + i];
-        for (int j = 0; j < kMlpHidden; ++j) acc += w[i * kMlpHidden + j] * h[j];
+        double acc = W(LO + kMlpOut * kMlpHidden + i);
+#pragma unroll
+        for (int j = 0; j < kMlpHidden; ++j) acc += W(LO + i * kMlpHidden + j) * h[j];
         lg[i] = acc;
     }
     int best = 0;
+#pragma unroll
     for (int k = 1; k < kMlpOut; ++k)
         if (lg[k] > lg[best]) best = k;
     return best + 1;
@@ -432,18 +468,21 @@ FCSG_HD int classify_stencil(const double* W, const double* s, double abs_floor)
 
 // Classifier::classify (src/viscosity.cpp:211-238) for one point of a
 // rectangular subpatch: min of the row-window and column-window classes.
-FCSG_HD int classify_point(const double* W, const double* f, long base, int ni, int nj, int i, int j, double abs_floor) {
+template <class WA>
+FCSG_HD int classify_point(const WA& W, const double* f, long base, int ni, int nj, int i, int j, double abs_floor) {
     double s[kMlpIn];
     int cr = 4, cc = 4;
     if (ni >= kMlpIn) {
         int st = i - kMlpIn / 2;
         st = st < 0 ? 0 : (st > ni - kMlpIn ? ni - kMlpIn : st);
+#pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(j) * ni + st + k];
         cr = classify_stencil(W, s, abs_floor);
     }
     if (nj >= kMlpIn) {
         int st = j - kMlpIn / 2;
         st = st < 0 ? 0 : (st > nj - kMlpIn ? nj - kMlpIn : st);
+#pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(st + k) * ni + i];
         cc = classify_stencil(W, s, abs_floor);
     }
@@ -452,20 +491,19 @@ FCSG_HD int classify_point(const double* W, const double* f, long base, int ni, 
 
 // phase 0, part 2: tau, mu_hat = c(tau) h_max S on interior points
 // (src/viscosity.cpp:240-251); at t=0 also the density class for the smear seed
-FCSG_HD void classify_body(Thr t, int block, int nblocks, double* Wsm, const EngineDev& E, bool step0) {
-    for (int k = t.tid; k < kMlpWeights; k += t.nthr) Wsm[k] = E.mlp[k];
-    FCSG_SYNC();
+template <class WA>
+FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, const EngineDev& E, bool step0) {
     const long sz = static_cast<long>(E.ni) * E.nj;
     const long step = static_cast<long>(nblocks) * t.nthr;
     for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
         const long base = (p / sz) * sz;
         const long loc = p - base;
         const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
-        const int tau = classify_point(Wsm, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
+        const int tau = classify_point(W, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
         E.tau[p] = tau;
         E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
         if (step0) {
-            const int tr = classify_point(Wsm, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
+            const int tr = classify_point(W, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
             E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
         }
     }
@@ -630,20 +668,20 @@ FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
 // kernels and launchers
 
 #if FCSG_CUDA
-template <int LB, class Pass>
-__global__ void __launch_bounds__(kThreads)
+template <int LB, class Pass, int NE>
+__global__ void __launch_bounds__(kThreads, 2)
     line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg) {
     extern __shared__ double2 smem[];
     const Pass P(E, arg);
-    line_pass<LB, Pass>(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, smem, P, E, pl,
-                        scr_cap);
+    line_pass<LB, Pass, NE, kThreads>(Thr{static_cast<int>(threadIdx.x), kThreads}, blockIdx.x, smem, P, E, pl,
+                                      scr_cap);
 }
 __global__ void __launch_bounds__(kThreads) proxy_kernel(const __grid_constant__ EngineDev E) {
     proxy_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
 }
 __global__ void __launch_bounds__(kThreads) classify_kernel(const __grid_constant__ EngineDev E, bool step0) {
-    __shared__ double W[kMlpWeights];
-    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, W, E, step0);
+    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, MlpW{}, E,
+                  step0);
 }
 __global__ void __launch_bounds__(kThreads) dilate_kernel(const __grid_constant__ EngineDev E) {
     dilate_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
@@ -671,25 +709,43 @@ int grid_for(long n) {
     return static_cast<int>(g < 1 ? 1 : g);
 }
 
+#if FCSG_CUDA
+template <class Pass, int NE>
+void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
+                      cudaStream_t s) {
+    auto k = line_pass_kernel<kLB, Pass, NE>;
+    static bool attr_set = false;  // once per instantiation (not during graph capture)
+    if (!attr_set) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        attr_set = true;
+    }
+    k<<<nblk, kThreads, smem, s>>>(E, pl, scr_cap, arg);
+}
+#endif
+
 template <class Pass>
 void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap, void* stream) {
     const int nlines = Pass::kRows ? E.nj : E.ni;
     const int bps = (nlines + kLB - 1) / kLB;
     const int nblk = E.S * bps;
     const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2);
+    // the compile-time plans assume the reference operator (n_cont 25, degree 2)
+    const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
 #if FCSG_CUDA
-    auto k = line_pass_kernel<kLB, Pass>;
-    static bool attr_set = false;  // once per instantiation (not during graph capture)
-    if (!attr_set) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr_set = true;
-    }
-    k<<<nblk, kThreads, smem, static_cast<cudaStream_t>(stream)>>>(E, pl, scr_cap, arg);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ref_op && pl.n_ext == 280) launch_line_pass<Pass, 280>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ref_op && pl.n_ext == 536) launch_line_pass<Pass, 536>(nblk, smem, arg, E, pl, scr_cap, s);
+    else launch_line_pass<Pass, 0>(nblk, smem, arg, E, pl, scr_cap, s);
 #else
     (void)stream;
     const Pass P(E, arg);
     std::vector<double2> sm(smem / sizeof(double2));
-    for (int b = 0; b < nblk; ++b) line_pass<kLB, Pass>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+    for (int b = 0; b < nblk; ++b) {
+        if (ref_op && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+        else if (ref_op && pl.n_ext == 536) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+        else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+    }
 #endif
 }
 
@@ -712,12 +768,12 @@ void launch_phase0(const EngineDev& E, bool step0, void* stream) {
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     proxy_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E);
+    cudaMemcpyToSymbolAsync(c_mlp, E.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
     classify_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E, step0);
 #else
     (void)stream;
     proxy_body(Thr{0, 1}, 0, 1, E);
-    std::vector<double> W(kMlpWeights);
-    classify_body(Thr{0, 1}, 0, 1, W.data(), E, step0);
+    classify_body(Thr{0, 1}, 0, 1, MlpW{E.mlp}, E, step0);
 #endif
 }
 
