@@ -110,6 +110,7 @@ typedef struct {
     double abs_floor;        /* ClassifierConfig::abs_floor, 1e-4 */
     int smear_radius;        /* 10 */
     int debug_rhs;           /* keep the last stage's rhs readable (parity hooks) */
+    int force_general;       /* 1: never use the Cartesian (zero metric term) passes */
 } fcsg_engine_config;
 
 /* BcKind codes (include/fcs/bc.hpp:10-17); -1 = no boundary condition */
@@ -176,6 +177,9 @@ int fcsg_engine_run(fcsg_engine* eng, long n, int use_graph, long* done);
 int fcsg_engine_enqueue(fcsg_engine* eng, long n);
 int fcsg_engine_time(fcsg_engine* eng, double* t, long* steps);
 int fcsg_engine_total_points(fcsg_engine* eng, long* n);
+/* 1 when every subpatch has iq2x == iq1y == 0 and the engine runs the
+ * 12-transform Cartesian stage passes, 0 for the general 20-transform passes */
+int fcsg_engine_is_cartesian(fcsg_engine* eng, int* yes);
 /* the engine's CUDA stream (cudaStream_t), for event timing by the caller */
 int fcsg_engine_stream(fcsg_engine* eng, void** stream);
 /* profiling hooks: average device ms of one launch group over `reps`

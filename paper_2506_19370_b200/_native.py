@@ -101,6 +101,7 @@ def _declare(L):
     L.fcsg_engine_time.argtypes = [vp, dp, C.POINTER(C.c_long)]
     L.fcsg_engine_total_points.argtypes = [vp, C.POINTER(C.c_long)]
     L.fcsg_engine_stream.argtypes = [vp, C.POINTER(vp)]
+    L.fcsg_engine_is_cartesian.argtypes = [vp, ip]
     L.fcsg_engine_set_state_bulk.argtypes = [vp, vp]
     L.fcsg_engine_get_state_bulk.argtypes = [vp, vp]
     L.fcsg_engine_time_group.argtypes = [vp, C.c_int, C.c_int, dp]

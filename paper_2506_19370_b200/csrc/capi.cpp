@@ -257,6 +257,7 @@ int fcsg_engine_create(fcsg_ctx* ctx, const fcsg_engine_config* cfg, fcsg_engine
         c.abs_floor = cfg->abs_floor;
         c.smear_radius = cfg->smear_radius;
         c.debug_rhs = cfg->debug_rhs != 0;
+        c.allow_cartesian = cfg->force_general == 0;
         auto* e = new fcsg_engine{ctx, std::make_unique<Engine>(*ctx, c)};
         *out = e;
     });
@@ -396,6 +397,11 @@ int fcsg_engine_time(fcsg_engine* e, double* t, long* steps) {
 int fcsg_engine_total_points(fcsg_engine* e, long* n) {
     if (!e) return FCSG_USAGE;
     return guard(e->ctx, [&] { *n = e->eng->total_points(); });
+}
+
+int fcsg_engine_is_cartesian(fcsg_engine* e, int* yes) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { *yes = e->eng->cartesian() ? 1 : 0; });
 }
 
 int fcsg_engine_stream(fcsg_engine* e, void** stream) {

@@ -152,6 +152,10 @@ void Engine::finalize() {
     for (int k = 0; k < 4; ++k) E.visc_c[k] = cfg_.visc_c[k];
     E.abs_floor = cfg_.abs_floor;
     E.smear_radius = cfg_.smear_radius;
+    E.cartesian = cfg_.allow_cartesian ? 1 : 0;
+    for (const auto& sp : subs_)
+        for (size_t k = 0; k < sp.iq2x.size(); ++k)
+            if (sp.iq2x[k] != 0.0 || sp.iq1y[k] != 0.0) E.cartesian = 0;
     std::vector<double> il1(S), il2(S);
     std::vector<int> i0(S), j0(S), pt(S);
     std::vector<BcDev> rlo, rhi, clo, chi;

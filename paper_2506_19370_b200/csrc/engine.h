@@ -33,6 +33,7 @@ struct EngineConfig {
     double abs_floor = 1e-4;                   // ClassifierConfig::abs_floor
     int smear_radius = 10;
     bool debug_rhs = false;                    // keep the last stage's rhs for parity hooks
+    bool allow_cartesian = true;               // use the zero-metric-term passes when they apply
 };
 
 struct SubSpec {
@@ -79,6 +80,7 @@ class Engine {
     double time();
     long steps() const { return host_step_; }
     long total_points() const { return npts_; }
+    bool cartesian() const { return E_.cartesian != 0; }
     void check_error();
     // average device milliseconds of one launch group (profiling hook):
     // 0 phase 0 (proxy + classifier), 1 phase 1 (blend + dt), 2 phase 2

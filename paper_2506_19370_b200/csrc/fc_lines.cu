@@ -10,20 +10,20 @@
 
 namespace fcsg {
 
-template <int LB>
+template <int LB, int NE, int NTHR>
 FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a) {
     const FcPlanDev& pl = a.pl;
-    const int pitch = LB + 1;
+    constexpr int pitch = LB + 1;
     double2* buf = smem;
-    double2* scr = smem + pl.n_ext * pitch;
-    const int N = pl.n;
+    double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
+    const int N = NE > 0 ? NE - 24 : pl.n;
     const long l0 = static_cast<long>(block) * 2 * LB;
     const long ls = a.line_stride, st = a.stride;
     const long ols = a.out_line_stride, ost = a.out_stride;
     const int total = N * LB;
     const bool rows = (st == 1);
     const bool orows = (ost == 1);
-    for (int w = t.tid; w < total; w += t.nthr) {
+    for (int w = t.tid; w < total; w += NTHR) {
         int i, c;
         if (rows) { i = w % N; c = w / N; }
         else { c = w % LB; i = w / LB; }
@@ -34,8 +34,9 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
         buf[i * pitch + c] = mk2(v0, v1);
     }
     FCSG_SYNC();
-    fc_transform(t, buf, pitch, LB, pl, a.mode, scr, a.scr_cap);
-    for (int w = t.tid; w < total; w += t.nthr) {
+    if constexpr (NE > 0) fc_transform_ct<NE, LB, NTHR>(t.tid, buf, pl, a.mode, scr, a.scr_cap);
+    else fc_transform(Thr{t.tid, NTHR}, buf, pitch, LB, pl, a.mode, scr, a.scr_cap);
+    for (int w = t.tid; w < total; w += NTHR) {
         int i, c;
         if (orows) { i = w % N; c = w / N; }
         else { c = w % LB; i = w / LB; }
@@ -47,10 +48,29 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
 }
 
 #if FCSG_CUDA
-template <int LB>
-__global__ void __launch_bounds__(256) fc_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+template <int LB, int NE>
+__global__ void __launch_bounds__(256, 2) fc_lines_kernel(const __grid_constant__ FcLinesArgs a) {
     extern __shared__ double2 smem[];
-    fc_lines_body<LB>(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, smem, a);
+    fc_lines_body<LB, NE, 256>(Thr{static_cast<int>(threadIdx.x), 256}, blockIdx.x, smem, a);
+}
+
+template <int LB, int NE>
+void launch_fc_lines_t(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_t s) {
+    static bool once = false;  // not during graph capture
+    if (!once) {
+        cudaFuncSetAttribute(fc_lines_kernel<LB, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(fc_lines_kernel<LB, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        once = true;
+    }
+    fc_lines_kernel<LB, NE><<<nblk, 256, smem, s>>>(a);
+}
+
+template <int LB>
+void launch_fc_lines_lb(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_t s) {
+    const bool ref_op = a.pl.n_gap == 24 && a.pl.dp1 == 3;
+    if (ref_op && a.pl.n_ext == 280) launch_fc_lines_t<LB, 280>(a, nblk, smem, s);
+    else if (ref_op && a.pl.n_ext == 536) launch_fc_lines_t<LB, 536>(a, nblk, smem, s);
+    else launch_fc_lines_t<LB, 0>(a, nblk, smem, s);
 }
 #endif
 
@@ -77,27 +97,18 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (LB) {
-        case 4:
-            { static bool once = (cudaFuncSetAttribute(fc_lines_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true); (void)once; }
-            fc_lines_kernel<4><<<nblk, 256, smem, s>>>(a);
-            break;
-        case 8:
-            { static bool once = (cudaFuncSetAttribute(fc_lines_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true); (void)once; }
-            fc_lines_kernel<8><<<nblk, 256, smem, s>>>(a);
-            break;
-        default:
-            { static bool once = (cudaFuncSetAttribute(fc_lines_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024), true); (void)once; }
-            fc_lines_kernel<16><<<nblk, 256, smem, s>>>(a);
-            break;
+        case 4: launch_fc_lines_lb<4>(a, nblk, smem, s); break;
+        case 8: launch_fc_lines_lb<8>(a, nblk, smem, s); break;
+        default: launch_fc_lines_lb<16>(a, nblk, smem, s); break;
     }
 #else
     (void)stream;
     std::vector<double2> sm(smem / sizeof(double2));
     for (int b = 0; b < nblk; ++b) {
         switch (LB) {
-            case 4: fc_lines_body<4>(Thr{0, 1}, b, sm.data(), a); break;
-            case 8: fc_lines_body<8>(Thr{0, 1}, b, sm.data(), a); break;
-            default: fc_lines_body<16>(Thr{0, 1}, b, sm.data(), a); break;
+            case 4: fc_lines_body<4, 0, 1>(Thr{0, 1}, b, sm.data(), a); break;
+            case 8: fc_lines_body<8, 0, 1>(Thr{0, 1}, b, sm.data(), a); break;
+            default: fc_lines_body<16, 0, 1>(Thr{0, 1}, b, sm.data(), a); break;
         }
     }
 #endif

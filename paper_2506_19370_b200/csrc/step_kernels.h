@@ -34,6 +34,7 @@ struct BcDev {
 
 struct EngineDev {
     int S, ni, nj;  // subpatches of one uniform rectangular shape
+    int cartesian;  // 1: iq2x == iq1y == 0 at every point (axis-aligned maps)
     long npts;      // S * ni * nj
     double cfl, T;
     double visc_c[4];

@@ -27,7 +27,8 @@ DEFAULT_WEIGHTS = os.path.join(HERE, "data", "fcnn_v1.bin")
 class fcsg_engine_config(C.Structure):
     _fields_ = [("cfl", C.c_double), ("T", C.c_double), ("n_cont", C.c_int), ("filter_alpha", C.c_double),
                 ("filter_p", C.c_int), ("filter_p_smear", C.c_int), ("visc_c", C.c_double * 4),
-                ("abs_floor", C.c_double), ("smear_radius", C.c_int), ("debug_rhs", C.c_int)]
+                ("abs_floor", C.c_double), ("smear_radius", C.c_int), ("debug_rhs", C.c_int),
+                ("force_general", C.c_int)]
 
 
 @dataclass
@@ -46,6 +47,7 @@ class EngineConfig:
     max_steps: int = 10 ** 9
     weights: str = DEFAULT_WEIGHTS
     debug_rhs: bool = False
+    force_general: bool = False  # never use the Cartesian (zero metric term) stage passes
 
 
 def _bc_arrays(d: G.SubData):
@@ -66,7 +68,8 @@ class Engine:
         self.ctx, self.dec, self.cfg = ctx, dec, cfg
         L = ctx.lib
         c = fcsg_engine_config(cfg.cfl, cfg.T, cfg.n_cont, cfg.filter_alpha, cfg.filter_p, cfg.filter_p_smear,
-                               (C.c_double * 4)(*cfg.visc_c), cfg.abs_floor, cfg.smear_radius, int(cfg.debug_rhs))
+                               (C.c_double * 4)(*cfg.visc_c), cfg.abs_floor, cfg.smear_radius, int(cfg.debug_rhs),
+                               int(cfg.force_general))
         h = C.c_void_p()
         ctx.check(L.fcsg_engine_create(ctx.h, C.byref(c), C.byref(h)))
         self.h = h
@@ -174,6 +177,11 @@ class Engine:
         t, st = C.c_double(), C.c_long()
         self.ctx.check(self.ctx.lib.fcsg_engine_time(self.h, C.byref(t), C.byref(st)))
         return t.value, st.value
+
+    def is_cartesian(self):
+        y = C.c_int()
+        self.ctx.check(self.ctx.lib.fcsg_engine_is_cartesian(self.h, C.byref(y)))
+        return bool(y.value)
 
     def total_points(self):
         n = C.c_long()

@@ -141,13 +141,17 @@ def _compare_engines(E, OE, nsub, atol_tau_margin=1e-9):
         assert np.array_equal(tau[sure], d.tau[sure])
 
 
-def test_superstep_phases_riemann(backend, engine_golden):
+@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
+def test_superstep_phases_riemann(backend, engine_golden, general):
     """Riemann quadrants on one 64x64 subpatch: every phase of two steps
-    against the oracle, and step 1 against the reference's own snapshots."""
+    against the oracle, and step 1 against the reference's own snapshots.
+    Run with the Cartesian stage passes (zero metric terms dropped) and with
+    the general 20-transform passes."""
     kind, ctx = backend
     g = engine_golden
     dec, ic, _ = P.riemann_quadrants(n=64, seed=2)
-    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5, debug_rhs=True))
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5, debug_rhs=True, force_general=general))
+    assert E.is_cartesian() == (not general)
     OE = oracle_engine(dec, ic)
     assert rel_err(E.get_state(0), g["r64_e_init"]) < 1e-15
     d = OE.subs[0]
@@ -178,15 +182,17 @@ def test_superstep_phases_riemann(backend, engine_golden):
     assert st == 2 and t == pytest.approx(OE.t, rel=1e-14)
 
 
-def test_superstep_tiles_exchange(backend, engine_golden):
+@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
+def test_superstep_tiles_exchange(backend, engine_golden, general):
     """2x2 overlapping 48x48 subpatches: fringe copies + viscosity blend; graph
     path equals the phase path bit for bit; state vs the reference run."""
     kind, ctx = backend
     g = engine_golden
     dec, ic, _ = P.vortex_tiles(r=2, s=2, n0=30)
     states = [g[f"v2_sub{k}_e_init"] for k in range(4)]
-    E = EN.Engine(ctx, dec, cfg=EN.EngineConfig(cfl=0.5), initial_states=states)
-    E2 = EN.Engine(ctx, dec, cfg=EN.EngineConfig(cfl=0.5), initial_states=states)
+    cfg = EN.EngineConfig(cfl=0.5, force_general=general)
+    E = EN.Engine(ctx, dec, cfg=cfg, initial_states=states)
+    E2 = EN.Engine(ctx, dec, cfg=cfg, initial_states=states)
     E.step_by_phases()
     E.step_by_phases()
     E2.run(2)
@@ -197,11 +203,12 @@ def test_superstep_tiles_exchange(backend, engine_golden):
 
 
 @pytest.mark.gpu
-def test_superstep_config2_full_size(gpu_ctx):
+@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
+def test_superstep_config2_full_size(gpu_ctx, general):
     """BASELINE config 2 at full size (one 512x512 subpatch, seeded quadrants,
     ANN classifier, CFL 0.5): 3 supersteps against the oracle."""
     dec, ic, _ = P.riemann_quadrants(n=512, seed=2)
-    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general))
     OE = oracle_engine(dec, ic)
     for _ in range(3):
         OE.step()
@@ -210,11 +217,12 @@ def test_superstep_config2_full_size(gpu_ctx):
 
 
 @pytest.mark.gpu
-def test_superstep_config5_subpatch_size(gpu_ctx):
+@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
+def test_superstep_config5_subpatch_size(gpu_ctx, general):
     """config 5 geometry (256x256 subpatches, 19-point overlap) on a 2x2 tiling,
     vortex + 1e-3 noise, 2 supersteps against the oracle."""
     dec, ic, _ = P.vortex_tiles(r=2, s=2)
-    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general))
     OE = oracle_engine(dec, ic)
     OE.step()
     OE.step()
