@@ -89,6 +89,9 @@ int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {
 }
 
 void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
+#if !FCSG_CUDA
+    LB = 4;  // the emulation runs one block shape
+#endif
     const int lines_per_block = 2 * LB;
     const int nblk = static_cast<int>((a.n_lines + lines_per_block - 1) / lines_per_block);
     if (nblk == 0) return;
@@ -104,12 +107,14 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
 #else
     (void)stream;
     std::vector<double2> sm(smem / sizeof(double2));
+    // same plan dispatch as the CUDA build, so the emulation covers the
+    // compile-time plans too
+    const bool ref_op = a.pl.n_gap == 24 && a.pl.dp1 == 3;
+    const int ne = ref_op && (a.pl.n_ext == 280 || a.pl.n_ext == 536) ? a.pl.n_ext : 0;
     for (int b = 0; b < nblk; ++b) {
-        switch (LB) {
-            case 4: fc_lines_body<4, 0, 1>(Thr{0, 1}, b, sm.data(), a); break;
-            case 8: fc_lines_body<8, 0, 1>(Thr{0, 1}, b, sm.data(), a); break;
-            default: fc_lines_body<16, 0, 1>(Thr{0, 1}, b, sm.data(), a); break;
-        }
+        if (ne == 280) fc_lines_body<4, 280, 1>(Thr{0, 1}, b, sm.data(), a);
+        else if (ne == 536) fc_lines_body<4, 536, 1>(Thr{0, 1}, b, sm.data(), a);
+        else fc_lines_body<4, 0, 1>(Thr{0, 1}, b, sm.data(), a);
     }
 #endif
 }

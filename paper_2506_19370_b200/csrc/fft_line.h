@@ -360,13 +360,13 @@ FCSG_HD void stage_ct(int tid, double2* buf, const double2* tw, double2* scr, in
     }
 }
 
-template <int NE, int S, int LB, int NTHR>
+// DIF stages S .. END-1
+template <int NE, int S, int LB, int NTHR, int END>
 FCSG_HD void dif_stages_ct(int tid, double2* buf, const double2* tw, double2* scr, int scr_cap) {
-    constexpr Factors F = factor_stages(NE);
-    if constexpr (S < F.n) {
+    if constexpr (S < END) {
         stage_ct<NE, S, LB, NTHR, false>(tid, buf, tw, scr, scr_cap);
         FCSG_SYNC();
-        dif_stages_ct<NE, S + 1, LB, NTHR>(tid, buf, tw, scr, scr_cap);
+        dif_stages_ct<NE, S + 1, LB, NTHR, END>(tid, buf, tw, scr, scr_cap);
     }
 }
 
@@ -412,6 +412,33 @@ FCSG_HD void spec_mult_ct(int tid, double2* buf, const double2* mult) {
     }
 }
 
+// Last DIF stage (span P, m = 1: butterflies on P contiguous positions, no
+// twiddles), the spectral multiplier and the first DIT stage touch the same P
+// positions, so one thread does all three in registers: two shared-memory
+// round trips and two barriers fewer per transform.
+template <int NE, int LB, int NTHR>
+FCSG_HD void middle_fused_ct(int tid, double2* buf, const double2* tw, const double2* mult) {
+    constexpr Factors F = factor_stages(NE);
+    constexpr int P = F.r[F.n - 1];
+    constexpr int total = (NE / P) * LB;
+    constexpr int pitch = LB + 1;
+    for (int w = tid; w < total; w += NTHR) {
+        const int line = w % LB;
+        const int blk = w / LB;
+        double2* p = buf + blk * P * pitch + line;
+        const double2* mm = mult + blk * P;
+        double2 x[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) x[q] = p[q * pitch];
+        dft_reg<P, false>(x, tw, NE);
+#pragma unroll
+        for (int q = 0; q < P; ++q) x[q] = cmul(x[q], ld2(mm + q));
+        dft_reg<P, true>(x, tw, NE);
+#pragma unroll
+        for (int q = 0; q < P; ++q) p[q * pitch] = x[q];
+    }
+}
+
 // fc_transform for n_ext = NE with the reference continuation (n_cont = 25,
 // degree 2): N = NE - 24.
 template <int NE, int LB, int NTHR>
@@ -419,10 +446,17 @@ FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mod
     constexpr Factors F = factor_stages(NE);
     continuation_ct<NE - 24, 24, 3, LB, NTHR>(tid, buf, pl.blend);
     FCSG_SYNC();
-    dif_stages_ct<NE, 0, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
-    spec_mult_ct<NE, LB, NTHR>(tid, buf, pl.mult + (mode - 1) * NE);
-    FCSG_SYNC();
-    dit_stages_ct<NE, F.n - 1, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+    if constexpr (radix_in_registers(F.r[F.n - 1])) {
+        dif_stages_ct<NE, 0, LB, NTHR, F.n - 1>(tid, buf, pl.tw, scr, scr_cap);
+        middle_fused_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE);
+        FCSG_SYNC();
+        dit_stages_ct<NE, F.n - 2, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+    } else {
+        dif_stages_ct<NE, 0, LB, NTHR, F.n>(tid, buf, pl.tw, scr, scr_cap);
+        spec_mult_ct<NE, LB, NTHR>(tid, buf, pl.mult + (mode - 1) * NE);
+        FCSG_SYNC();
+        dit_stages_ct<NE, F.n - 1, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+    }
 }
 
 // the lengths with a compile-time plan (reference operator, n_cont = 25)

@@ -20,6 +20,7 @@
 #include "step_kernels.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace fcsg {
@@ -781,13 +782,12 @@ FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
 // kernels and launchers
 
 #if FCSG_CUDA
-template <int LB, class Pass, int NE>
-__global__ void __launch_bounds__(kThreads, 2)
+template <int LB, class Pass, int NE, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
     line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg) {
     extern __shared__ double2 smem[];
     const Pass P(E, arg);
-    line_pass<LB, Pass, NE, kThreads>(Thr{static_cast<int>(threadIdx.x), kThreads}, blockIdx.x, smem, P, E, pl,
-                                      scr_cap);
+    line_pass<LB, Pass, NE, NT>(Thr{static_cast<int>(threadIdx.x), NT}, blockIdx.x, smem, P, E, pl, scr_cap);
 }
 __global__ void __launch_bounds__(kThreads) proxy_kernel(const __grid_constant__ EngineDev E) {
     proxy_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
@@ -823,17 +823,33 @@ int grid_for(long n) {
 }
 
 #if FCSG_CUDA
-template <class Pass, int NE>
-void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
-                      cudaStream_t s) {
-    auto k = line_pass_kernel<kLB, Pass, NE>;
+template <class Pass, int NE, int NT>
+void launch_line_pass_nt(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
+                         cudaStream_t s) {
+    auto k = line_pass_kernel<kLB, Pass, NE, NT>;
     static bool attr_set = false;  // once per instantiation (not during graph capture)
     if (!attr_set) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
-    k<<<nblk, kThreads, smem, s>>>(E, pl, scr_cap, arg);
+    k<<<nblk, NT, smem, s>>>(E, pl, scr_cap, arg);
+}
+
+// CTA size of the line passes (FCSG_LINE_THREADS=128|256, default 256)
+inline int line_threads() {
+    static const int nt = [] {
+        const char* v = std::getenv("FCSG_LINE_THREADS");
+        return (v && std::atoi(v) == 128) ? 128 : 256;
+    }();
+    return nt;
+}
+
+template <class Pass, int NE>
+void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
+                      cudaStream_t s) {
+    if (line_threads() == 128) launch_line_pass_nt<Pass, NE, 128>(nblk, smem, arg, E, pl, scr_cap, s);
+    else launch_line_pass_nt<Pass, NE, 256>(nblk, smem, arg, E, pl, scr_cap, s);
 }
 #endif
 
