@@ -321,6 +321,7 @@ FCSG_HD void stage_reg_ct(int tid, double2* buf, const double2* tw) {
     constexpr int tstep = NE / L;
     constexpr int pitch = LB + 1;
     constexpr int ms = m * pitch;
+#pragma unroll 2
     for (int w = tid; w < total; w += NTHR) {
         const int line = w % LB;
         const int b = w / LB;
@@ -422,6 +423,7 @@ FCSG_HD void middle_fused_ct(int tid, double2* buf, const double2* tw, const dou
     constexpr int P = F.r[F.n - 1];
     constexpr int total = (NE / P) * LB;
     constexpr int pitch = LB + 1;
+#pragma unroll 2
     for (int w = tid; w < total; w += NTHR) {
         const int line = w % LB;
         const int blk = w / LB;

@@ -823,10 +823,10 @@ int grid_for(long n) {
 }
 
 #if FCSG_CUDA
-template <class Pass, int NE, int NT>
+template <class Pass, int NE, int NT, int LB>
 void launch_line_pass_nt(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
                          cudaStream_t s) {
-    auto k = line_pass_kernel<kLB, Pass, NE, NT>;
+    auto k = line_pass_kernel<LB, Pass, NE, NT>;
     static bool attr_set = false;  // once per instantiation (not during graph capture)
     if (!attr_set) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -845,28 +845,41 @@ inline int line_threads() {
     return nt;
 }
 
-template <class Pass, int NE>
+template <class Pass, int NE, int LB>
 void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
                       cudaStream_t s) {
-    if (line_threads() == 128) launch_line_pass_nt<Pass, NE, 128>(nblk, smem, arg, E, pl, scr_cap, s);
-    else launch_line_pass_nt<Pass, NE, 256>(nblk, smem, arg, E, pl, scr_cap, s);
+    if (line_threads() == 128) launch_line_pass_nt<Pass, NE, 128, LB>(nblk, smem, arg, E, pl, scr_cap, s);
+    else launch_line_pass_nt<Pass, NE, 256, LB>(nblk, smem, arg, E, pl, scr_cap, s);
 }
 #endif
+
+// lines per CTA of the compile-time-plan passes (FCSG_LINE_LB=8|16, default 8)
+inline int line_lb() {
+    static const int lb = [] {
+        const char* v = std::getenv("FCSG_LINE_LB");
+        return (v && std::atoi(v) == 16) ? 16 : 8;
+    }();
+    return lb;
+}
 
 template <class Pass>
 void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap, void* stream) {
     const int nlines = Pass::kRows ? E.nj : E.ni;
-    const int bps = (nlines + kLB - 1) / kLB;
-    const int nblk = E.S * bps;
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2);
     // the compile-time plans assume the reference operator (n_cont 25, degree 2)
     const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
 #if FCSG_CUDA
+    const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? line_lb() : kLB;
+    const int nblk = E.S * ((nlines + lb - 1) / lb);
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap) * sizeof(double2);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (ref_op && pl.n_ext == 280) launch_line_pass<Pass, 280>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ref_op && pl.n_ext == 536) launch_line_pass<Pass, 536>(nblk, smem, arg, E, pl, scr_cap, s);
-    else launch_line_pass<Pass, 0>(nblk, smem, arg, E, pl, scr_cap, s);
+    if (ref_op && pl.n_ext == 280 && lb == 16) launch_line_pass<Pass, 280, 16>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ref_op && pl.n_ext == 280) launch_line_pass<Pass, 280, 8>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ref_op && pl.n_ext == 536 && lb == 16) launch_line_pass<Pass, 536, 16>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ref_op && pl.n_ext == 536) launch_line_pass<Pass, 536, 8>(nblk, smem, arg, E, pl, scr_cap, s);
+    else launch_line_pass<Pass, 0, 8>(nblk, smem, arg, E, pl, scr_cap, s);
 #else
+    const int nblk = E.S * ((nlines + kLB - 1) / kLB);
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2);
     (void)stream;
     const Pass P(E, arg);
     std::vector<double2> sm(smem / sizeof(double2));
@@ -885,7 +898,7 @@ int step_scr_cap(const FcPlanDev& pl) {
     for (int s = 0; s < pl.nstages; ++s) {
         const int p = pl.radix[s];
         if (!radix_in_registers(p)) {
-            const int per = p * kLB;
+            const int per = p * 16;  // largest LB of any instantiation
             const int k = kThreads / per > 1 ? kThreads / per : 1;
             cap = cap > per * k ? cap : per * k;
         }
