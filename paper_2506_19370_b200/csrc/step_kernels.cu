@@ -120,6 +120,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
     const int total = N * LB;
     const int tid = t.tid;
     for (int r = 0; r <= Pass::kRounds; ++r) {
+#pragma unroll 4
         for (int w = tid; w < total; w += NTHR) {
             int i, l;
             if (rows) {
@@ -158,10 +159,10 @@ struct Prim {
 };
 FCSG_HD Prim prim_rhs(const EngineDev& E, long p) {
     Prim q;
-    q.rho = E.e[0][p];
-    q.mx = E.e[1][p];
-    q.my = E.e[2][p];
-    q.E = E.e[3][p];
+    q.rho = ld1(E.e[0] + p);  // e is read-only in the passes that call this (A, B)
+    q.mx = ld1(E.e[1] + p);
+    q.my = ld1(E.e[2] + p);
+    q.E = ld1(E.e[3] + p);
     const double rs = (q.rho != 0.0) ? q.rho : 1e-300;
     const double pr = kGm1 * (q.E - 0.5 * (q.mx * q.mx + q.my * q.my) / rs);
     q.theta = pr / rs;
@@ -204,7 +205,7 @@ struct PassA {
     }
     FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
         if (r < 4) {
-            E.tA[r][p] = E.iq1x[p] * v.x + E.iq1y[p] * v.y;
+            E.tA[r][p] = ld1(E.iq1x + p) * v.x + ld1(E.iq1y + p) * v.y;
         } else {
             const int c0 = 2 * (r - 4);
             E.tW[c0][p] = v.x;
@@ -231,11 +232,11 @@ struct PassB {
     }
     FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
         if (r < 4) {
-            E.tA[r][p] = -(E.tA[r][p] + (E.iq2x[p] * v.x + E.iq2y[p] * v.y));
+            E.tA[r][p] = -(E.tA[r][p] + (ld1(E.iq2x + p) * v.x + ld1(E.iq2y + p) * v.y));
         } else if (r < 6) {
             const int c0 = 2 * (r - 4);
-            const double mu = E.mu[p];
-            const double a = E.iq1x[p], b = E.iq2x[p], cc = E.iq1y[p], d = E.iq2y[p];
+            const double mu = ld1(E.mu + p);
+            const double a = ld1(E.iq1x + p), b = ld1(E.iq2x + p), cc = ld1(E.iq1y + p), d = ld1(E.iq2y + p);
             for (int k = 0; k < 2; ++k) {
                 const double d1 = E.tW[c0 + k][p];
                 const double d2 = k == 0 ? v.x : v.y;
@@ -246,7 +247,7 @@ struct PassB {
             }
         } else {
             const int c = r - 6;
-            E.tA[c][p] += E.iq2x[p] * v.x + E.iq2y[p] * v.y;
+            E.tA[c][p] += ld1(E.iq2x + p) * v.x + ld1(E.iq2y + p) * v.y;
         }
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
@@ -297,9 +298,9 @@ struct PassC {
     int stage;
     FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const { return mk2(E.tS4[r][p], E.tS5[r][p]); }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const { return mk2(ld1(E.tS4[r] + p), ld1(E.tS5[r] + p)); }
     FCSG_HD void store(int c, long p, double2 v, const LineCtx&, int, int) const {
-        ssprk_update(E, stage, c, p, E.tA[c][p] + (E.iq1x[p] * v.x + E.iq1y[p] * v.y));
+        ssprk_update(E, stage, c, p, E.tA[c][p] + (ld1(E.iq1x + p) * v.x + ld1(E.iq1y + p) * v.y));
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -340,7 +341,7 @@ struct PassAc {
     }
     FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
         if (r < 2) {
-            const double a = E.iq1x[p];
+            const double a = ld1(E.iq1x + p);
             E.tA[2 * r][p] = a * v.x;
             E.tA[2 * r + 1][p] = a * v.y;
         } else {
@@ -371,13 +372,13 @@ struct PassBc {
         return mk2(q.my, q.theta);
     }
     FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
-        const double d = E.iq2y[p];
+        const double d = ld1(E.iq2y + p);
         if (r < 2) {
             E.tA[2 * r][p] = -(E.tA[2 * r][p] + d * v.x);
             E.tA[2 * r + 1][p] = -(E.tA[2 * r + 1][p] + d * v.y);
         } else if (r < 4) {
             const int c0 = 2 * (r - 2);
-            const double mu = E.mu[p], a = E.iq1x[p];
+            const double mu = ld1(E.mu + p), a = ld1(E.iq1x + p);
             E.tS4[c0][p] = mu * (a * E.tW[c0][p]);
             E.tS4[c0 + 1][p] = mu * (a * E.tW[c0 + 1][p]);
             E.tS5[c0][p] = mu * (d * v.x);
@@ -401,10 +402,10 @@ struct PassCc {
     FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
     FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
-        return mk2(E.tS4[2 * r][p], E.tS4[2 * r + 1][p]);
+        return mk2(ld1(E.tS4[2 * r] + p), ld1(E.tS4[2 * r + 1] + p));
     }
     FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
-        const double a = E.iq1x[p];
+        const double a = ld1(E.iq1x + p);
         ssprk_update(E, stage, 2 * r, p, E.tA[2 * r][p] + a * v.x);
         ssprk_update(E, stage, 2 * r + 1, p, E.tA[2 * r + 1][p] + a * v.y);
     }
@@ -714,8 +715,8 @@ FCSG_HD void apply_bc_at(const EngineDev& E, const BcDev& bc, long p, long p1, l
             break;
         }
         case 2: {
-            double nx = axis == 0 ? E.iq1x[p] : E.iq2x[p];
-            double ny = axis == 0 ? E.iq1y[p] : E.iq2y[p];
+            double nx = axis == 0 ? ld1(E.iq1x + p) : ld1(E.iq2x + p);
+            double ny = axis == 0 ? ld1(E.iq1y + p) : ld1(E.iq2y + p);
             const double nn = hypot(nx, ny);
             nx /= nn;
             ny /= nn;
