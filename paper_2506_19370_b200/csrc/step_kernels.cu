@@ -89,20 +89,48 @@ FCSG_HD long pidx(const LineCtx& c, int l, int i) {
     return c.rows ? c.base + static_cast<long>(c.line0 + l) * c.ni + i : c.base + static_cast<long>(i) * c.ni + c.line0 + l;
 }
 
+// asynchronous 8-byte global -> shared copies (cp.async), used to prefetch the
+// epilogue inputs of a round while its FFT runs
+FCSG_HD void stage_copy(double* dst, const double* src) {
+#if FCSG_CUDA
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+#else
+    *dst = *src;
+#endif
+}
+FCSG_HD void stage_commit() {
+#if FCSG_CUDA
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+#endif
+}
+FCSG_HD void stage_wait() {
+#if FCSG_CUDA
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+#endif
+}
+
 // One CTA owns LB lines of one subpatch (rows: stride-1 lines of length ni;
 // columns: stride-ni lines of length nj). For every round r of the pass it
 // loads two real quantities per point as one complex line, runs the FC
 // transform in shared memory and hands the scaled result to the pass's
 // epilogue. NE > 0 selects the compile-time plan for n_ext = NE (then
 // N = NE - 24); NE = 0 is the runtime-generic plan. NTHR is the CTA size
-// (1 in the CPU emulation harness). The epilogue of round r and the load of
-// round r+1 share one loop: each slot is read and rewritten by the same
-// thread, so no barrier is needed between them.
+// (1 in the CPU emulation harness).
+//
+// The epilogue of round r-1 and the load of round r share one loop (each
+// shared-memory slot is read and rewritten by the same thread, so no barrier
+// sits between them). The epilogue's global inputs (read-modify-write
+// partials, metrics, mu, RK registers) are prefetched into shared memory with
+// cp.async right before the round's FFT and waited for after it, so their
+// latency hides behind the transform. Each thread stages and consumes only its
+// own slots (stage[k * total + w]).
 template <int LB, class Pass, int NE, int NTHR>
 FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const EngineDev& E, const FcPlanDev& pl,
                        int scr_cap) {
     constexpr bool rows = Pass::kRows;
     constexpr int pitch = LB + 1;
+    constexpr int KS = Pass::kStage;
     const int ni = E.ni, nj = E.nj;
     const int N = NE > 0 ? NE - 24 : (rows ? ni : nj);
     const int nlines = rows ? nj : ni;
@@ -116,6 +144,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
     c.rows = rows;
     double2* buf = smem;
     double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
+    double* stg = reinterpret_cast<double*>(scr + scr_cap);
     const double inv_len = P.kScaled ? (rows ? E.inv_len1[c.sub] : E.inv_len2[c.sub]) : 1.0;
     const int total = N * LB;
     const int tid = t.tid;
@@ -134,26 +163,44 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
                 const long p = pidx(c, l, i);
                 if (r > 0) {
                     const double2 v = buf[i * pitch + l];
-                    P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), c, l, i);
+                    P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c);
                 }
-                if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c, l, i);
+                if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c);
             } else if (r < Pass::kRounds) {
                 buf[i * pitch + l] = mk2(0.0, 0.0);
             }
         }
         if (r == Pass::kRounds) break;
+        if constexpr (KS > 0) {
+            for (int w = tid; w < total; w += NTHR) {
+                int i, l;
+                if (rows) {
+                    i = w % N;
+                    l = w / N;
+                } else {
+                    l = w % LB;
+                    i = w / LB;
+                }
+                if (l >= c.nl_valid) continue;
+                const double* src[KS > 0 ? KS : 1];
+                const int n = P.stage_srcs(r, pidx(c, l, i), src);
+                for (int k = 0; k < n; ++k) stage_copy(stg + k * total + w, src[k]);
+            }
+            stage_commit();
+        }
         FCSG_SYNC();
         if constexpr (NE > 0) {
             fc_transform_ct<NE, LB, NTHR>(tid, buf, pl, P.mode(r), scr, scr_cap);
         } else {
             fc_transform(Thr{tid, NTHR}, buf, pitch, LB, pl, P.mode(r), scr, scr_cap);
         }
+        if constexpr (KS > 0) stage_wait();
     }
     FCSG_SYNC();
     P.finish(Thr{tid, NTHR}, c, N);
 }
 
-// conservative -> (theta, u, v, p) exactly as euler_rhs (src/euler.cpp:29-41,44-55)
+// conservative -> (theta, p) exactly as euler_rhs (src/euler.cpp:29-41,44-55)
 struct Prim {
     double rho, mx, my, E, theta, p;
 };
@@ -181,31 +228,42 @@ FCSG_HD double2 flux_pair(const Prim& q, int c) {
     }
 }
 
+// interior positivity diagnostic of euler_rhs (src/euler.cpp:37-39)
+FCSG_HD void check_positive(const EngineDev& E, const Prim& q, long p, const LineCtx& c) {
+    if (E.mask[p] != 1) return;
+    const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
+    if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) {
+        const long loc = p - c.base;
+        raise_error(E.sc, 1, c.sub, static_cast<int>(loc % c.ni), static_cast<int>(loc / c.ni));
+    }
+}
+
 // Pass A (rows): D1 of F_c, G_c (rounds 0..3) and of w = (rho, rho u, rho v, theta) (4, 5)
+// staged per store(r < 4): iq1x, iq1y
 struct PassA {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 6;
+    static constexpr int kStage = 2;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassA(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, int l, int i) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx& c) const {
         const Prim q = prim_rhs(E, p);
-        if (r == 0 && E.mask[p] == 1) {
-            // interior positivity diagnostic (src/euler.cpp:37-39)
-            const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
-            if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) {
-                const int il = c.rows ? i : c.line0 + l, jl = c.rows ? c.line0 + l : i;
-                raise_error(E.sc, 1, c.sub, il, jl);
-            }
-        }
+        if (r == 0) check_positive(E, q, p, c);
         if (r < 4) return flux_pair(q, r);
         if (r == 4) return mk2(q.rho, q.mx);
         return mk2(q.my, q.theta);
     }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        if (r >= 4) return 0;
+        s[0] = E.iq1x + p;
+        s[1] = E.iq1y + p;
+        return 2;
+    }
+    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
         if (r < 4) {
-            E.tA[r][p] = ld1(E.iq1x + p) * v.x + ld1(E.iq1y + p) * v.y;
+            E.tA[r][p] = st[0] * v.x + st[ss] * v.y;
         } else {
             const int c0 = 2 * (r - 4);
             E.tW[c0][p] = v.x;
@@ -215,92 +273,123 @@ struct PassA {
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
-// Pass B (cols): D2 of F, G, w; inviscid rhs and mu grad w; then D2 of mu grad w
+// Pass B (cols): D2 of F, G, w; inviscid rhs and mu grad w; then D2 of mu grad w.
+// load(r >= 6) reads tS4/tS5[r-6], written by store(4 or 5) in an earlier round.
 struct PassB {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 10;
+    static constexpr int kStage = 7;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassB(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const {
         if (r >= 6) return mk2(E.tS4[r - 6][p], E.tS5[r - 6][p]);
         const Prim q = prim_rhs(E, p);
         if (r < 4) return flux_pair(q, r);
         if (r == 4) return mk2(q.rho, q.mx);
         return mk2(q.my, q.theta);
     }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+    // r<4: tA[r], iq2x, iq2y; r=4,5: iq2x, iq2y, iq1x, iq1y, mu, tW x2; r>=6: tA[r-6], iq2x, iq2y
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        s[0] = E.iq2x + p;
+        s[1] = E.iq2y + p;
         if (r < 4) {
-            E.tA[r][p] = -(E.tA[r][p] + (ld1(E.iq2x + p) * v.x + ld1(E.iq2y + p) * v.y));
+            s[2] = E.tA[r] + p;
+            return 3;
+        }
+        if (r < 6) {
+            const int c0 = 2 * (r - 4);
+            s[2] = E.iq1x + p;
+            s[3] = E.iq1y + p;
+            s[4] = E.mu + p;
+            s[5] = E.tW[c0] + p;
+            s[6] = E.tW[c0 + 1] + p;
+            return 7;
+        }
+        s[2] = E.tA[r - 6] + p;
+        return 3;
+    }
+    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        const double b = st[0], d = st[ss];
+        if (r < 4) {
+            E.tA[r][p] = -(st[2 * ss] + (b * v.x + d * v.y));
         } else if (r < 6) {
             const int c0 = 2 * (r - 4);
-            const double mu = ld1(E.mu + p);
-            const double a = ld1(E.iq1x + p), b = ld1(E.iq2x + p), cc = ld1(E.iq1y + p), d = ld1(E.iq2y + p);
+            const double a = st[2 * ss], cc = st[3 * ss], mu = st[4 * ss];
+            const double d1[2] = {st[5 * ss], st[6 * ss]};
+            const double d2[2] = {v.x, v.y};
             for (int k = 0; k < 2; ++k) {
-                const double d1 = E.tW[c0 + k][p];
-                const double d2 = k == 0 ? v.x : v.y;
-                const double gx = a * d1 + b * d2;
-                const double gy = cc * d1 + d * d2;
+                const double gx = a * d1[k] + b * d2[k];
+                const double gy = cc * d1[k] + d * d2[k];
                 E.tS4[c0 + k][p] = mu * gx;
                 E.tS5[c0 + k][p] = mu * gy;
             }
         } else {
-            const int c = r - 6;
-            E.tA[c][p] += ld1(E.iq2x + p) * v.x + ld1(E.iq2y + p) * v.y;
+            E.tA[r - 6][p] = st[2 * ss] + (b * v.x + d * v.y);
         }
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
-// SSPRK(5,4) stage update of component c at point p (src/euler.cpp:182-221).
-// At stage 0 the register e0 equals e (phase 2 copies e into e0 after the
-// BCs, src/runtime.cpp:422), so it is written here instead of in phase 2.
-FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double r) {
+// SSPRK(5,4) stage update of component c at point p (src/euler.cpp:182-221),
+// u = current e[c][p]. The RK registers read here (e0, e2, e3, rhs3) are never
+// written in the same stage, so they take the read-only path. At stage 0 the
+// register e0 equals e (phase 2 copies e into e0 after the BCs,
+// src/runtime.cpp:422), so it is written here instead of in phase 2.
+FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double u, double r) {
     const double dt = E.sc->dt;  // device-resident step size (finalize_dt_kernel)
     if (E.rhs[0]) E.rhs[c][p] = r;
-    double* u = E.e[c];
+    double* e = E.e[c];
     switch (stage) {
-        case 0: {
-            const double u0 = u[p];
-            E.e0[c][p] = u0;
-            u[p] = u0 + dt * SB0 * r;
+        case 0:
+            E.e0[c][p] = u;
+            e[p] = u + dt * SB0 * r;
             break;
-        }
         case 1: {
-            const double nu = SA20 * E.e0[c][p] + SA21 * u[p] + dt * SB1 * r;
-            u[p] = nu;
+            const double nu = SA20 * ld1(E.e0[c] + p) + SA21 * u + dt * SB1 * r;
+            e[p] = nu;
             E.e2[c][p] = nu;
             break;
         }
         case 2: {
-            const double nu = SA30 * E.e0[c][p] + SA32 * u[p] + dt * SB2 * r;
-            u[p] = nu;
+            const double nu = SA30 * ld1(E.e0[c] + p) + SA32 * u + dt * SB2 * r;
+            e[p] = nu;
             E.e3[c][p] = nu;
             break;
         }
         case 3:
             E.rhs3[c][p] = r;
-            u[p] = SA40 * E.e0[c][p] + SA43 * u[p] + dt * SB3 * r;
+            e[p] = SA40 * ld1(E.e0[c] + p) + SA43 * u + dt * SB3 * r;
             break;
         default:
-            u[p] = SC2 * E.e2[c][p] + SC3 * E.e3[c][p] + dt * SD3 * E.rhs3[c][p] + SC4 * u[p] + dt * SD4 * r;
+            e[p] = SC2 * ld1(E.e2[c] + p) + SC3 * ld1(E.e3[c] + p) + dt * SD3 * ld1(E.rhs3[c] + p) + SC4 * u +
+                   dt * SD4 * r;
             break;
     }
 }
 
 // Pass C (rows): D1 of mu grad w, rhs, SSPRK(5,4) stage update
+// staged per store(c): tA[c], iq1x, iq1y, e[c]
 struct PassC {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 4;
+    static constexpr int kStage = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
     FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const { return mk2(ld1(E.tS4[r] + p), ld1(E.tS5[r] + p)); }
-    FCSG_HD void store(int c, long p, double2 v, const LineCtx&, int, int) const {
-        ssprk_update(E, stage, c, p, E.tA[c][p] + (ld1(E.iq1x + p) * v.x + ld1(E.iq1y + p) * v.y));
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return mk2(ld1(E.tS4[r] + p), ld1(E.tS5[r] + p)); }
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        s[0] = E.tA[r] + p;
+        s[1] = E.iq1x + p;
+        s[2] = E.iq1y + p;
+        s[3] = E.e[r] + p;
+        return 4;
+    }
+    FCSG_HD void store(int c, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        ssprk_update(E, stage, c, p, st[3 * ss], st[0] + (st[ss] * v.x + st[2 * ss] * v.y));
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -315,23 +404,18 @@ struct PassC {
 // complex line transforms per stage. Engines with any curvilinear subpatch
 // use the general passes above.
 
-// A': D1 of F_c (rounds 0, 1) and of w (2, 3)
+// A': D1 of F_c (rounds 0, 1) and of w (2, 3); staged per store(r < 2): iq1x
 struct PassAc {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 4;
+    static constexpr int kStage = 1;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassAc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, int l, int i) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx& c) const {
         const Prim q = prim_rhs(E, p);
-        if (r == 0 && E.mask[p] == 1) {
-            const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
-            if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) {
-                const int il = c.rows ? i : c.line0 + l, jl = c.rows ? c.line0 + l : i;
-                raise_error(E.sc, 1, c.sub, il, jl);
-            }
-        }
+        if (r == 0) check_positive(E, q, p, c);
         if (r < 2) {
             const double2 f0 = flux_pair(q, 2 * r), f1 = flux_pair(q, 2 * r + 1);
             return mk2(f0.x, f1.x);
@@ -339,9 +423,14 @@ struct PassAc {
         if (r == 2) return mk2(q.rho, q.mx);
         return mk2(q.my, q.theta);
     }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        if (r >= 2) return 0;
+        s[0] = E.iq1x + p;
+        return 1;
+    }
+    FCSG_HD void store(int r, long p, double2 v, const double* st, int, const LineCtx&) const {
         if (r < 2) {
-            const double a = ld1(E.iq1x + p);
+            const double a = st[0];
             E.tA[2 * r][p] = a * v.x;
             E.tA[2 * r + 1][p] = a * v.y;
         } else {
@@ -354,14 +443,16 @@ struct PassAc {
 };
 
 // B': D2 of G_c (0, 1) and of w (2, 3) -> inviscid rhs, mu grad w; D2 of mu grad_y w (4, 5)
+// staged: iq2y and r<2: tA pair; r=2,3: iq1x, mu, tW pair; r=4,5: tA pair
 struct PassBc {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 6;
+    static constexpr int kStage = 5;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassBc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const {
         if (r >= 4) return mk2(E.tS5[2 * (r - 4)][p], E.tS5[2 * (r - 4) + 1][p]);
         const Prim q = prim_rhs(E, p);
         if (r < 2) {
@@ -371,66 +462,96 @@ struct PassBc {
         if (r == 2) return mk2(q.rho, q.mx);
         return mk2(q.my, q.theta);
     }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
-        const double d = ld1(E.iq2y + p);
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        s[0] = E.iq2y + p;
         if (r < 2) {
-            E.tA[2 * r][p] = -(E.tA[2 * r][p] + d * v.x);
-            E.tA[2 * r + 1][p] = -(E.tA[2 * r + 1][p] + d * v.y);
+            s[1] = E.tA[2 * r] + p;
+            s[2] = E.tA[2 * r + 1] + p;
+            return 3;
+        }
+        if (r < 4) {
+            const int c0 = 2 * (r - 2);
+            s[1] = E.tW[c0] + p;
+            s[2] = E.tW[c0 + 1] + p;
+            s[3] = E.iq1x + p;
+            s[4] = E.mu + p;
+            return 5;
+        }
+        s[1] = E.tA[2 * (r - 4)] + p;
+        s[2] = E.tA[2 * (r - 4) + 1] + p;
+        return 3;
+    }
+    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        const double d = st[0], t0 = st[ss], t1 = st[2 * ss];
+        if (r < 2) {
+            E.tA[2 * r][p] = -(t0 + d * v.x);
+            E.tA[2 * r + 1][p] = -(t1 + d * v.y);
         } else if (r < 4) {
             const int c0 = 2 * (r - 2);
-            const double mu = ld1(E.mu + p), a = ld1(E.iq1x + p);
-            E.tS4[c0][p] = mu * (a * E.tW[c0][p]);
-            E.tS4[c0 + 1][p] = mu * (a * E.tW[c0 + 1][p]);
+            const double a = st[3 * ss], mu = st[4 * ss];
+            E.tS4[c0][p] = mu * (a * t0);
+            E.tS4[c0 + 1][p] = mu * (a * t1);
             E.tS5[c0][p] = mu * (d * v.x);
             E.tS5[c0 + 1][p] = mu * (d * v.y);
         } else {
             const int c0 = 2 * (r - 4);
-            E.tA[c0][p] += d * v.x;
-            E.tA[c0 + 1][p] += d * v.y;
+            E.tA[c0][p] = t0 + d * v.x;
+            E.tA[c0 + 1][p] = t1 + d * v.y;
         }
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
-// C': D1 of mu grad_x w -> rhs -> SSPRK stage update
+// C': D1 of mu grad_x w -> rhs -> SSPRK stage update; staged: tA pair, iq1x, e pair
 struct PassCc {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 2;
+    static constexpr int kStage = 5;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
     FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const {
         return mk2(ld1(E.tS4[2 * r] + p), ld1(E.tS4[2 * r + 1] + p));
     }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
-        const double a = ld1(E.iq1x + p);
-        ssprk_update(E, stage, 2 * r, p, E.tA[2 * r][p] + a * v.x);
-        ssprk_update(E, stage, 2 * r + 1, p, E.tA[2 * r + 1][p] + a * v.y);
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        s[0] = E.tA[2 * r] + p;
+        s[1] = E.tA[2 * r + 1] + p;
+        s[2] = E.iq1x + p;
+        s[3] = E.e[2 * r] + p;
+        s[4] = E.e[2 * r + 1] + p;
+        return 5;
+    }
+    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        const double a = st[2 * ss];
+        ssprk_update(E, stage, 2 * r, p, st[3 * ss], st[0] + a * v.x);
+        ssprk_update(E, stage, 2 * r + 1, p, st[4 * ss], st[ss] + a * v.y);
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
 // Phase 2 rows: filter (or, at t=0, smear) rho, rho u, rho v, theta
-// (src/runtime.cpp:375-411, subpatch_data.cpp:30-67)
+// (src/runtime.cpp:375-411, subpatch_data.cpp:30-67). Writes tF only.
 struct PassFR {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 2;
+    static constexpr int kStage = 0;
     static constexpr bool kScaled = false;
     const EngineDev& E;
     bool smear;
     FCSG_HD PassFR(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
     FCSG_HD int mode(int) const { return smear ? 4 : 3; }
     FCSG_HD static double2 orig(const EngineDev& E, int r, long p) {
-        const double rho = E.e[0][p], mx = E.e[1][p];
+        const double rho = ld1(E.e[0] + p), mx = ld1(E.e[1] + p);
         if (r == 0) return mk2(rho, mx);
-        const double my = E.e[2][p], En = E.e[3][p];
+        const double my = ld1(E.e[2] + p), En = ld1(E.e[3] + p);
         const double th = kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho;
         return mk2(my, th);
     }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const { return orig(E, r, p); }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return orig(E, r, p); }
+    FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
+    FCSG_HD void store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
         if (smear) {
             const double m = E.m01[p];
             const double2 f = orig(E, r, p);
@@ -446,15 +567,15 @@ struct PassFR {
 struct PassFC {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 2;
+    static constexpr int kStage = 0;
     static constexpr bool kScaled = false;
     const EngineDev& E;
     bool smear;
     FCSG_HD PassFC(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
     FCSG_HD int mode(int) const { return smear ? 4 : 3; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, int, int) const {
-        return mk2(E.tF[2 * r][p], E.tF[2 * r + 1][p]);
-    }
-    FCSG_HD void store(int r, long p, double2 v, const LineCtx&, int, int) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return mk2(E.tF[2 * r][p], E.tF[2 * r + 1][p]); }
+    FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
+    FCSG_HD void store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
         if (smear) {
             const double m = E.m01[p];
             const double fa = E.tF[2 * r][p], fb = E.tF[2 * r + 1][p];
@@ -858,7 +979,8 @@ void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const 
 inline int line_lb() {
     static const int lb = [] {
         const char* v = std::getenv("FCSG_LINE_LB");
-        return (v && std::atoi(v) == 16) ? 16 : 8;
+        const int x = v ? std::atoi(v) : 8;
+        return (x == 16 || x == 4) ? x : 8;
     }();
     return lb;
 }
@@ -871,16 +993,20 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
 #if FCSG_CUDA
     const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? line_lb() : kLB;
     const int nblk = E.S * ((nlines + lb - 1) / lb);
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap) * sizeof(double2);
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap) * sizeof(double2) +
+                        static_cast<size_t>(Pass::kStage) * pl.n * lb * sizeof(double);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (ref_op && pl.n_ext == 280 && lb == 16) launch_line_pass<Pass, 280, 16>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ref_op && pl.n_ext == 280 && lb == 4) launch_line_pass<Pass, 280, 4>(nblk, smem, arg, E, pl, scr_cap, s);
     else if (ref_op && pl.n_ext == 280) launch_line_pass<Pass, 280, 8>(nblk, smem, arg, E, pl, scr_cap, s);
     else if (ref_op && pl.n_ext == 536 && lb == 16) launch_line_pass<Pass, 536, 16>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ref_op && pl.n_ext == 536 && lb == 4) launch_line_pass<Pass, 536, 4>(nblk, smem, arg, E, pl, scr_cap, s);
     else if (ref_op && pl.n_ext == 536) launch_line_pass<Pass, 536, 8>(nblk, smem, arg, E, pl, scr_cap, s);
     else launch_line_pass<Pass, 0, 8>(nblk, smem, arg, E, pl, scr_cap, s);
 #else
     const int nblk = E.S * ((nlines + kLB - 1) / kLB);
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2);
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2) +
+                        static_cast<size_t>(Pass::kStage) * pl.n * kLB * sizeof(double);
     (void)stream;
     const Pass P(E, arg);
     std::vector<double2> sm(smem / sizeof(double2));
