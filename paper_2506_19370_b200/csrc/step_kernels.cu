@@ -905,7 +905,7 @@ FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
 
 #if FCSG_CUDA
 template <int LB, class Pass, int NE, int NT>
-__global__ void __launch_bounds__(NT, 512 / NT)
+__global__ void __launch_bounds__(NT, 768 / NT)
     line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg) {
     extern __shared__ double2 smem[];
     const Pass P(E, arg);
@@ -975,12 +975,12 @@ void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const 
 }
 #endif
 
-// lines per CTA of the compile-time-plan passes (FCSG_LINE_LB=8|16, default 8)
-inline int line_lb() {
+// FCSG_LINE_LB=4|8|16 forces the lines per CTA of the compile-time-plan passes (0 = per-pass default)
+inline int line_lb_env() {
     static const int lb = [] {
         const char* v = std::getenv("FCSG_LINE_LB");
-        const int x = v ? std::atoi(v) : 8;
-        return (x == 16 || x == 4) ? x : 8;
+        const int x = v ? std::atoi(v) : 0;
+        return (x == 16 || x == 8 || x == 4) ? x : 0;
     }();
     return lb;
 }
@@ -991,7 +991,11 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
     // the compile-time plans assume the reference operator (n_cont 25, degree 2)
     const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
 #if FCSG_CUDA
-    const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? line_lb() : kLB;
+    // lines per CTA: passes with a large epilogue staging area use 4 (three
+    // 256-thread CTAs per SM fit in shared memory), the others 8;
+    // FCSG_LINE_LB overrides for experiments
+    const int lb_pref = Pass::kStage >= 3 ? 4 : 8;
+    const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? (line_lb_env() ? line_lb_env() : lb_pref) : kLB;
     const int nblk = E.S * ((nlines + lb - 1) / lb);
     const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap) * sizeof(double2) +
                         static_cast<size_t>(Pass::kStage) * pl.n * lb * sizeof(double);
