@@ -156,14 +156,20 @@ def run_reference(args):
 # product arm
 
 
-ALG_BYTES = {  # algorithmic bytes per point per launch
-    "pass_a": 32 + 16 + 1 + 64,
-    "pass_b": 32 + 32 + 32 + 32 + 8 + 96,
-    "pass_c": 64 + 32 + 16 + 32 + 32 + 64,
-    "viscosity": 32 + 1 + 8 + 8 + 32,
-    "filter": 32 + 32 + 32 + 32 + 8,
+# algorithmic HBM bytes per point per launch: every
+# input read once and every output written once; values produced and consumed
+# inside one kernel count zero. The Cartesian passes (every subpatch of the
+# workload) read fewer metric terms than the general ones.
+ALG_BYTES_CART = {
+    "pass_a": 32 + 8 + 1 + 64,               # e, iq1x, mask -> tA, tW
+    "pass_b": 32 + 32 + 32 + 8 + 8 + 8 + 96,  # e, tA, tW, iq2y, iq1x, mu -> tA, tS4, tS5
+    "pass_c": 32 + 32 + 8 + 32 + 38 + 32 + 26,  # tS4, tA, iq1x, e, RK regs (avg) -> e, RK regs (avg)
+    "viscosity": 32 + 1 + 8 + 8 * 4,         # e, mask, h_max -> proxy, speed, tau, mu_hat (+ proxy re-read in L1)
+    "filter": 32 + 32 + 32 + 32,             # rows e -> tF ; cols tF -> e
     "blend": 8 * 5 + 1 + 8,
 }
+ALG_BYTES_GEN = dict(ALG_BYTES_CART, pass_a=32 + 16 + 1 + 64, pass_b=32 + 32 + 32 + 32 + 8 + 96,
+                     pass_c=64 + 32 + 16 + 32 + 38 + 32 + 26)
 LAUNCHES = {"pass_a": 5, "pass_b": 5, "pass_c": 5, "viscosity": 1, "filter": 1, "blend": 1, "bc": 6,
             "exchange": 5}
 
@@ -207,13 +213,34 @@ def run_fcsg(args):
     from paper_2506_19370_b200 import _native as N, engine as EN
 
     ctx = N.Context(local)
-    dec, ic, _ = workload()
-    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+    DE = None
+    if world > 1:
+        # weak scaling: an (8 px) x (8 py) tiling, one contiguous 8x8 block per
+        # rank; halo copies over NCCL send/recv, dt by all-reduce(MIN)
+        from paper_2506_19370_b200 import distributed as D, problems as P
+
+        px = max(p for p in range(1, world + 1) if world % p == 0 and p * p <= world)
+        py = world // px
+        dec, ic, _ = P.vortex_tiles(r=R_TILES * py, s=S_TILES * px)
+        owner = D.partition_tiles(dec, world)
+        rp = D.split_plan(dec, owner, rank, world)
+        DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5))
+        E = DE.E
+    else:
+        dec, ic, _ = workload()
+        E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5))
     npts = E.total_points()
     stream = torch.cuda.ExternalStream(E.stream(), device=local)
 
+    def steps(n):
+        if DE is not None:
+            for _ in range(n):
+                DE.step()
+        else:
+            E.enqueue(n)
+
     # warm-up (includes the t=0 smear step and the CUDA-graph capture)
-    E.enqueue(max(args.warmup, 3))
+    steps(max(args.warmup, 3))
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
@@ -221,7 +248,7 @@ def run_fcsg(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        E.enqueue(args.steps)
+        steps(args.steps)
         ev1.record(stream)
         torch.cuda.synchronize()
     ms_total = ev0.elapsed_time(ev1)
@@ -230,7 +257,7 @@ def run_fcsg(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     t_now, steps_done = E.time()
-    E.run(0)  # surfaces a device-side InvalidStateError, if any
+    E.check_error()  # surfaces a device-side InvalidStateError, if any
     ms_step = ms_total / args.steps
     value = 5.0 * npts * world * args.steps / (ms_total * 1e-3)
 
@@ -247,7 +274,10 @@ def run_fcsg(args):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         E.set_state_bulk(host_in)
-        E.run(1)
+        if DE is not None:
+            DE.run(1)
+        else:
+            E.run(1)
         E.get_state_bulk(host_out)
     e2e_s = time.perf_counter() - t0
     if world > 1:
@@ -264,6 +294,7 @@ def run_fcsg(args):
     share = {g: groups[g] * LAUNCHES[g] for g in groups}
     dom = max(share, key=share.get)
     hbm, peak_kind = peaks()
+    ALG_BYTES = ALG_BYTES_CART if E.is_cartesian() else ALG_BYTES_GEN
     alg = ALG_BYTES.get(dom, 64) * npts
     achieved = alg / (groups[dom] * 1e-3) / 1e9
     fc_gbs, fc_ms = fc_derivative_gbs(ctx)
@@ -288,10 +319,11 @@ def run_fcsg(args):
         "vs_baseline": value / PAPER_1NODE,
         "vs_baseline_basis": "PAPER.md:1612 (BASELINE.md): 6.74e7 pt-stage/s, one 54-core Xeon 8273 node",
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config5-weak: {R_TILES}x{S_TILES} tiles of 256x256 per GPU "
+        "config": {"workload": f"config5-weak: {R_TILES}x{S_TILES} tiles of 256x256 per GPU"
+                               f"{'' if world == 1 else ' (one block of a ' + str(len(dec.subs)) + '-subpatch tiling, NCCL halo exchange)'} "
                                f"({npts} points/GPU, 19-point overlap), vortex + 1e-3 noise, ANN classifier, CFL 0.5",
                    "points_per_gpu": npts, "l2": "working set ~1.7 GB/GPU >> 126 MB L2 (no flush needed)",
-                   "cuda_graph": True},
+                   "cuda_graph": world == 1, "parallelism": f"subpatch blocks x{world}", "stage_passes": "cartesian" if E.is_cartesian() else "general"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                 "steps": e2e_steps, "path": "fcsg_engine_set_state_bulk + fcsg_engine_run + fcsg_engine_get_state_bulk"},
         "gpu_launches": E.launches_per_step() * args.steps,

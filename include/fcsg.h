@@ -182,6 +182,37 @@ int fcsg_engine_total_points(fcsg_engine* eng, long* n);
 int fcsg_engine_is_cartesian(fcsg_engine* eng, int* yes);
 /* the engine's CUDA stream (cudaStream_t), for event timing by the caller */
 int fcsg_engine_stream(fcsg_engine* eng, void** stream);
+/* ---- multi-rank (one process per GPU) -------------------------------------
+ * The reference's workers read donor subpatches directly after a barrier
+ * (src/runtime.cpp:436-452, 357-368). Across GPUs, each rank owns a block of
+ * subpatches; donors on other ranks are packed into a contiguous device
+ * buffer on the donor rank, moved by the caller's transport (NCCL send/recv
+ * over NVLink, gloo in the CPU tests), and unpacked into halo slots on the
+ * recipient, which its plan entries address with src_sub = -1. */
+/* donor points this rank packs (state: [k][4], mu_hat: [k]) and the number
+ * of values it receives; call before fcsg_engine_set_plan */
+int fcsg_engine_set_halo(fcsg_engine* eng, long n_send_e, const int* e_sub, const int* e_loc, long n_recv_e,
+                         long n_send_mu, const int* mu_sub, const int* mu_loc, long n_recv_mu);
+/* which: 0 = send e, 1 = recv e, 2 = send mu, 3 = recv mu */
+int fcsg_engine_halo_size(fcsg_engine* eng, int which, long* n);
+/* which: 0 = state e, 1 = mu_hat; d_buf is device memory on the engine's device */
+int fcsg_engine_pack(fcsg_engine* eng, int which, void* d_buf);
+int fcsg_engine_unpack(fcsg_engine* eng, int which, const void* d_buf);
+/* one part of a superstep, enqueued on the engine stream: 0 viscosity
+ * (phase 0), 1 blend + dt_local minimum (phase 1), 2 filter/smear + BC + dt
+ * (phase 2 + dt), 3 stage `stage` (RHS + SSPRK + BC), 4 exchange copies
+ * (phase 6), 5 advance. A multi-rank step: 0, mu halo, 1, all-reduce(min) of
+ * the dt minimum, 2, then 5 x (3, state halo, 4), then 5. */
+int fcsg_engine_enqueue_part(fcsg_engine* eng, int part, int stage);
+/* device address of the dt minimum (a positive double stored as its
+ * uint64 bit pattern, so an int64 MIN all-reduce is exact) */
+int fcsg_engine_dtmin_ptr(fcsg_engine* eng, void** dptr);
+/* 8-byte device copy of that minimum to (to_engine = 0) or from (1) a
+ * caller buffer, ordered on the engine stream */
+int fcsg_engine_copy_dtmin(fcsg_engine* eng, void* d_buf, int to_engine);
+/* synchronise the engine stream and raise a pending device-side error */
+int fcsg_engine_check_error(fcsg_engine* eng);
+
 /* profiling hooks: average device ms of one launch group over `reps`
  * back-to-back launches (0 viscosity/classifier, 1 blend+dt, 2 filter,
  * 3 pass A, 4 pass B, 5 pass C, 6 BC, 7 exchange), and the number of kernel

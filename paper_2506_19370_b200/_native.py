@@ -104,6 +104,14 @@ def _declare(L):
     L.fcsg_engine_is_cartesian.argtypes = [vp, ip]
     L.fcsg_engine_set_state_bulk.argtypes = [vp, vp]
     L.fcsg_engine_get_state_bulk.argtypes = [vp, vp]
+    L.fcsg_engine_set_halo.argtypes = [vp, C.c_long, ip, ip, C.c_long, C.c_long, ip, ip, C.c_long]
+    L.fcsg_engine_halo_size.argtypes = [vp, C.c_int, C.POINTER(C.c_long)]
+    L.fcsg_engine_pack.argtypes = [vp, C.c_int, vp]
+    L.fcsg_engine_unpack.argtypes = [vp, C.c_int, vp]
+    L.fcsg_engine_enqueue_part.argtypes = [vp, C.c_int, C.c_int]
+    L.fcsg_engine_dtmin_ptr.argtypes = [vp, C.POINTER(vp)]
+    L.fcsg_engine_check_error.argtypes = [vp]
+    L.fcsg_engine_copy_dtmin.argtypes = [vp, vp, C.c_int]
     L.fcsg_engine_time_group.argtypes = [vp, C.c_int, C.c_int, dp]
     L.fcsg_engine_launches_per_step.argtypes = [vp, ip]
     return L

@@ -438,3 +438,76 @@ int fcsg_engine_get_state_bulk(fcsg_engine* e, double* out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// multi-rank halo exchange and the part-wise superstep
+
+extern "C" {
+
+int fcsg_engine_set_halo(fcsg_engine* e, long n_send_e, const int* e_sub, const int* e_loc, long n_recv_e,
+                         long n_send_mu, const int* mu_sub, const int* mu_loc, long n_recv_mu) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        auto vi = [](const int* p, long n) { return (p && n > 0) ? std::vector<int>(p, p + n) : std::vector<int>(); };
+        e->eng->set_halo(vi(e_sub, n_send_e), vi(e_loc, n_send_e), n_recv_e, vi(mu_sub, n_send_mu),
+                         vi(mu_loc, n_send_mu), n_recv_mu);
+    });
+}
+
+int fcsg_engine_halo_size(fcsg_engine* e, int which, long* n) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { *n = e->eng->halo_size(which); });
+}
+
+int fcsg_engine_pack(fcsg_engine* e, int which, void* d_buf) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        if (which == 0) e->eng->pack_e(static_cast<double*>(d_buf));
+        else if (which == 1) e->eng->pack_mu(static_cast<double*>(d_buf));
+        else throw Error(kUsage, "bad halo selector");
+        dev::check("pack");
+    });
+}
+
+int fcsg_engine_unpack(fcsg_engine* e, int which, const void* d_buf) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        if (which == 0) e->eng->unpack_e(static_cast<const double*>(d_buf));
+        else if (which == 1) e->eng->unpack_mu(static_cast<const double*>(d_buf));
+        else throw Error(kUsage, "bad halo selector");
+        dev::check("unpack");
+    });
+}
+
+int fcsg_engine_enqueue_part(fcsg_engine* e, int part, int stage) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->enqueue_part(part, stage); });
+}
+
+int fcsg_engine_dtmin_ptr(fcsg_engine* e, void** dptr) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { *dptr = e->eng->dtmin_device_ptr(); });
+}
+
+int fcsg_engine_check_error(fcsg_engine* e) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        dev::sync(e->ctx->stream);
+        e->eng->check_error();
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int fcsg_engine_copy_dtmin(fcsg_engine* e, void* d_buf, int to_engine) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        void* p = e->eng->dtmin_device_ptr();
+        if (to_engine) dev::d2d(p, d_buf, 8, e->ctx->stream);
+        else dev::d2d(d_buf, p, 8, e->ctx->stream);
+    });
+}
+
+}  // extern "C"

@@ -54,18 +54,26 @@ void Engine::set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, st
     if (subs_.empty()) throw Error(kUsage, "add subpatches before the plan");
     const long sz = static_cast<long>(subs_[0].ni) * subs_[0].nj;
     const int S = static_cast<int>(subs_.size());
+    const long np = sz * S;
     auto gidx = [&](int sub, int loc) -> long {
         if (sub < 0 || sub >= S || loc < 0 || loc >= sz) throw Error(kUsage, "plan entry out of range");
         return sub * sz + loc;
+    };
+    // donors on other ranks (src_sub == -1) live in the halo slots after the local points
+    auto sidx = [&](int sub, int loc, long n_halo) -> long {
+        if (sub == -1) {
+            if (loc < 0 || loc >= n_halo) throw Error(kUsage, "halo slot out of range");
+            return np + loc;
+        }
+        return gidx(sub, loc);
     };
     x_dst_.clear();
     x_src_.clear();
     for (size_t k = 0; k < sol_dst.size(); ++k) {
         x_dst_.push_back(gidx(sol_dst_sub[k], sol_dst[k]));
-        x_src_.push_back(gidx(sol_src_sub[k], sol_src[k]));
+        x_src_.push_back(sidx(sol_src_sub[k], sol_src[k], n_recv_e_));
     }
     // CSR by recipient point, keeping the given (reference) order per point
-    const long np = sz * S;
     std::vector<long> dsts(v_dst.size());
     for (size_t k = 0; k < v_dst.size(); ++k) dsts[k] = gidx(v_dst_sub[k], v_dst[k]);
     std::vector<size_t> order(v_dst.size());
@@ -76,11 +84,67 @@ void Engine::set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, st
     visc_w_.clear();
     for (size_t k : order) {
         visc_off_[dsts[k] + 1]++;
-        visc_src_.push_back(gidx(v_src_sub[k], v_src[k]));
+        visc_src_.push_back(sidx(v_src_sub[k], v_src[k], n_recv_mu_));
         visc_w_.push_back(v_w[k]);
     }
     for (long p = 0; p < np; ++p) visc_off_[p + 1] += visc_off_[p];
     have_plan_ = true;
+}
+
+void Engine::set_halo(std::vector<int> e_sub, std::vector<int> e_loc, long n_recv_e, std::vector<int> mu_sub,
+                      std::vector<int> mu_loc, long n_recv_mu) {
+    if (finalized_) throw Error(kUsage, "engine already finalized");
+    if (have_plan_) throw Error(kUsage, "set the halo before the plan");
+    if (e_sub.size() != e_loc.size() || mu_sub.size() != mu_loc.size() || n_recv_e < 0 || n_recv_mu < 0)
+        throw Error(kUsage, "bad halo lists");
+    halo_e_src_.clear();
+    halo_mu_src_.clear();
+    for (size_t k = 0; k < e_sub.size(); ++k) halo_e_src_.emplace_back(e_sub[k], e_loc[k]);
+    for (size_t k = 0; k < mu_sub.size(); ++k) halo_mu_src_.emplace_back(mu_sub[k], mu_loc[k]);
+    n_recv_e_ = n_recv_e;
+    n_recv_mu_ = n_recv_mu;
+}
+
+long Engine::halo_size(int which) const {
+    switch (which) {
+        case 0: return static_cast<long>(halo_e_src_.size());
+        case 1: return n_recv_e_;
+        case 2: return static_cast<long>(halo_mu_src_.size());
+        case 3: return n_recv_mu_;
+    }
+    throw Error(kUsage, "bad halo selector");
+}
+
+void Engine::pack_e(double* d_buf) { launch_pack(E_, 0, d_halo_e_, static_cast<long>(halo_e_.size()), d_buf, ctx_.stream); }
+void Engine::unpack_e(const double* d_buf) { launch_unpack(E_, 0, n_recv_e_, d_buf, ctx_.stream); }
+void Engine::pack_mu(double* d_buf) { launch_pack(E_, 1, d_halo_mu_, static_cast<long>(halo_mu_.size()), d_buf, ctx_.stream); }
+void Engine::unpack_mu(const double* d_buf) { launch_unpack(E_, 1, n_recv_mu_, d_buf, ctx_.stream); }
+
+void Engine::enqueue_part(int part, int stage) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    void* s = ctx_.stream;
+    switch (part) {
+        case -1: launch_bc(E_, s); break;
+        case 0: launch_phase0(E_, host_step_ == 0, s); break;
+        case 1: launch_phase1(E_, s); break;
+        case 2:
+            launch_phase2(E_, plans_, host_step_ == 0, s);
+            launch_bc(E_, s);
+            launch_finalize_dt(E_, s);
+            break;
+        case 3:
+            if (stage < 0 || stage > 4) throw Error(kUsage, "bad stage");
+            launch_stage(E_, plans_, stage, s);
+            launch_bc(E_, s);
+            break;
+        case 4: launch_exchange(E_, s); break;
+        case 5:
+            launch_advance(E_, s);
+            ++host_step_;
+            break;
+        default: throw Error(kUsage, "bad step part");
+    }
+    dev::check("enqueue_part");
 }
 
 void Engine::set_mlp_packed(const std::vector<double>& w) {
@@ -198,13 +262,15 @@ void Engine::finalize() {
     const double** gp[7] = {&E.iq1x, &E.iq2x, &E.iq1y, &E.iq2y, &E.h_min, &E.h_max, &E.w_norm};
     for (int k = 0; k < 7; ++k) *gp[k] = static_cast<const double*>(up(geo[k].data(), geo[k].size() * sizeof(double)));
 
-    // state + temporaries in one pool
+    // state + temporaries in one pool; every field has room for the halo
+    // slots after its npts local points
     const int n_fields = 4 * 5 + (cfg_.debug_rhs ? 4 : 0) + 7 + 4 * 4;
-    pool_ = dev::alloc_n<double>(static_cast<size_t>(n_fields) * npts_);
+    const size_t fstride = npts_ + std::max(n_recv_e_, n_recv_mu_);
+    pool_ = dev::alloc_n<double>(static_cast<size_t>(n_fields) * fstride);
     allocs_.push_back(pool_);
-    dev::memset0(pool_, static_cast<size_t>(n_fields) * npts_ * sizeof(double), ctx_.stream);
+    dev::memset0(pool_, static_cast<size_t>(n_fields) * fstride * sizeof(double), ctx_.stream);
     int f = 0;
-    auto nextf = [&]() { return pool_ + static_cast<size_t>(f++) * npts_; };
+    auto nextf = [&]() { return pool_ + static_cast<size_t>(f++) * fstride; };
     for (int c = 0; c < 4; ++c) E.e[c] = nextf();
     for (int c = 0; c < 4; ++c) E.e0[c] = nextf();
     for (int c = 0; c < 4; ++c) E.e2[c] = nextf();
@@ -242,6 +308,18 @@ void Engine::finalize() {
         }
     }
     E.mlp = static_cast<const double*>(up(mlp_.data(), mlp_.size() * sizeof(double)));
+    halo_e_.clear();
+    halo_mu_.clear();
+    for (auto [sb, lc] : halo_e_src_) {
+        if (sb < 0 || sb >= S || lc < 0 || lc >= sz) throw Error(kUsage, "halo donor out of range");
+        halo_e_.push_back(sb * sz + lc);
+    }
+    for (auto [sb, lc] : halo_mu_src_) {
+        if (sb < 0 || sb >= S || lc < 0 || lc >= sz) throw Error(kUsage, "halo donor out of range");
+        halo_mu_.push_back(sb * sz + lc);
+    }
+    if (!halo_e_.empty()) d_halo_e_ = static_cast<long*>(up(halo_e_.data(), halo_e_.size() * sizeof(long)));
+    if (!halo_mu_.empty()) d_halo_mu_ = static_cast<long*>(up(halo_mu_.data(), halo_mu_.size() * sizeof(long)));
     StepScalars sc{};
     double inf = kInf;
     std::memcpy(&sc.dtmin_bits, &inf, 8);

@@ -56,6 +56,23 @@ class Engine {
     void set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, std::vector<int> sol_src_sub,
                   std::vector<int> sol_src, std::vector<int> v_dst_sub, std::vector<int> v_dst,
                   std::vector<int> v_src_sub, std::vector<int> v_src, std::vector<double> v_w);
+    // Cross-rank halo (multi-GPU): donor points this rank packs for other
+    // ranks (solution state and mu_hat), and how many values it receives.
+    // Received values land in extra slots after the local points; plan
+    // entries address them with src_sub = -1, src = slot. Call before
+    // set_plan.
+    void set_halo(std::vector<int> e_sub, std::vector<int> e_loc, long n_recv_e, std::vector<int> mu_sub,
+                  std::vector<int> mu_loc, long n_recv_mu);
+    void pack_e(double* d_buf);          // [k][4]
+    void unpack_e(const double* d_buf);  // [k][4] -> extra slots
+    void pack_mu(double* d_buf);
+    void unpack_mu(const double* d_buf);
+    long halo_size(int which) const;     // 0 send e, 1 recv e, 2 send mu, 3 recv mu
+    // one part of a superstep (multi-rank driver): 0 viscosity, 1 blend + dt
+    // minimum, 2 filter/smear + BC + dt, 3 stage `stage` (passes + BC),
+    // 4 exchange copies, 5 advance
+    void enqueue_part(int part, int stage);
+    unsigned long long* dtmin_device_ptr() const { return &E_.sc->dtmin_bits; }
     void set_mlp_packed(const std::vector<double>& w);  // kMlpWeights, per layer W then b
     void load_mlp_file(const std::string& path);        // FCNN v1 (src/viscosity.cpp:63-89)
     void finalize();
@@ -110,6 +127,11 @@ class Engine {
     std::vector<long> visc_src_;
     std::vector<double> visc_w_;
     bool have_plan_ = false;
+    std::vector<long> halo_e_, halo_mu_;  // packed donor points (global local-engine indices)
+    long n_recv_e_ = 0, n_recv_mu_ = 0;
+    std::vector<std::pair<int, int>> halo_e_src_, halo_mu_src_;
+    long* d_halo_e_ = nullptr;
+    long* d_halo_mu_ = nullptr;
     long host_step_ = 0;
     void* graph_exec_ = nullptr;
     void* graph_ = nullptr;

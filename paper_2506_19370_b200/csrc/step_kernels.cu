@@ -900,6 +900,29 @@ FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
     }
 }
 
+// halo pack (donor side) / unpack (recipient side) for the multi-rank exchange
+FCSG_HD void pack_body(Thr t, int block, int nblocks, const EngineDev& E, int which, const long* idx, long n,
+                       double* buf) {
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    for (long k = static_cast<long>(block) * t.nthr + t.tid; k < n; k += step) {
+        const long p = idx[k];
+        if (which == 0)
+            for (int c = 0; c < 4; ++c) buf[4 * k + c] = E.e[c][p];
+        else
+            buf[k] = E.mu_hat[p];
+    }
+}
+FCSG_HD void unpack_body(Thr t, int block, int nblocks, const EngineDev& E, int which, long n, const double* buf) {
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    for (long k = static_cast<long>(block) * t.nthr + t.tid; k < n; k += step) {
+        const long p = E.npts + k;
+        if (which == 0)
+            for (int c = 0; c < 4; ++c) E.e[c][p] = buf[4 * k + c];
+        else
+            E.mu_hat[p] = buf[k];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // kernels and launchers
 
@@ -923,6 +946,16 @@ __global__ void __launch_bounds__(kThreads) dilate_kernel(const __grid_constant_
 }
 __global__ void __launch_bounds__(kThreads) blend_kernel(const __grid_constant__ EngineDev E) {
     blend_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
+}
+__global__ void __launch_bounds__(kThreads)
+    pack_kernel(const __grid_constant__ EngineDev E, int which, const long* idx, long n, double* buf) {
+    pack_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E, which, idx, n,
+              buf);
+}
+__global__ void __launch_bounds__(kThreads)
+    unpack_kernel(const __grid_constant__ EngineDev E, int which, long n, const double* buf) {
+    unpack_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E, which, n,
+                buf);
 }
 __global__ void finalize_dt_kernel(const __grid_constant__ EngineDev E) { finalize_dt_body(E); }
 __global__ void advance_kernel(const __grid_constant__ EngineDev E) { advance_body(E); }
@@ -1124,6 +1157,26 @@ void launch_advance(const EngineDev& E, void* stream) {
 #else
     (void)stream;
     advance_body(E);
+#endif
+}
+
+void launch_pack(const EngineDev& E, int which, const long* idx, long n, double* buf, void* stream) {
+    if (n <= 0) return;
+#if FCSG_CUDA
+    pack_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E, which, idx, n, buf);
+#else
+    (void)stream;
+    pack_body(Thr{0, 1}, 0, 1, E, which, idx, n, buf);
+#endif
+}
+
+void launch_unpack(const EngineDev& E, int which, long n, const double* buf, void* stream) {
+    if (n <= 0) return;
+#if FCSG_CUDA
+    unpack_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E, which, n, buf);
+#else
+    (void)stream;
+    unpack_body(Thr{0, 1}, 0, 1, E, which, n, buf);
 #endif
 }
 

@@ -101,5 +101,8 @@ void launch_bc(const EngineDev& E, void* stream);
 void launch_exchange(const EngineDev& E, void* stream);
 void launch_finalize_dt(const EngineDev& E, void* stream);
 void launch_advance(const EngineDev& E, void* stream);
+// halo pack/unpack (which: 0 state e as [k][4], 1 mu_hat as [k])
+void launch_pack(const EngineDev& E, int which, const long* idx, long n, double* buf, void* stream);
+void launch_unpack(const EngineDev& E, int which, long n, const double* buf, void* stream);
 
 }  // namespace fcsg

@@ -1,0 +1,236 @@
+"""Multi-GPU FC-SDNN superstep: one process per GPU, subpatches sharded in
+contiguous spatial blocks.
+
+The reference runs all subpatches in one process: worker threads own
+subpatches round-robin (``assign_ranks``, src/runtime.cpp:16-23) and read
+donor subpatches directly after a barrier (phase 1 blend,
+src/runtime.cpp:352-371; phase 6 exchange, :433-454; the dt minimum,
+:492-497). Here every rank owns a contiguous block of subpatches (so only
+block edges cross ranks) and:
+
+* per stage, fringe copies whose donor lives on another rank are packed on
+  the donor rank into one device buffer per peer (``fcsg_engine_pack``),
+  moved with point-to-point send/recv, and unpacked into halo slots on the
+  recipient (``fcsg_engine_unpack``) before the exchange kernel runs;
+* per step, the mu_hat values the viscosity blend reads across ranks move
+  the same way before the blend;
+* dt_local's minimum is an all-reduce(MIN) of one int64 (the bit pattern of
+  a positive double, so the reduction is exact).
+
+Every per-subpatch computation is local and min is exact, so the result is
+bitwise independent of the number of ranks. Transport is torch.distributed:
+NCCL over NVLink on GPUs, gloo for the CPU tests (which drive the same engine
+code through the emulation build).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import geometry as G
+
+
+def partition_tiles(dec: G.Decomposition, world: int) -> np.ndarray:
+    """Owner rank of every subpatch: the (r x s) tile grid of a subdivide_Q
+    patch is cut into a (px x py) grid of equal contiguous blocks, px*py =
+    world, px chosen to keep blocks as square as the tiling allows."""
+    p = dec.patches[0]
+    i0s = sorted({sp.i0 for sp in p.subpatches})
+    j0s = sorted({sp.j0 for sp in p.subpatches})
+    r, s = len(i0s), len(j0s)
+    best = None
+    for px in range(1, world + 1):
+        if world % px or r % px or s % (world // px):
+            continue
+        py = world // px
+        score = abs(np.log((r / px) / (s / py)))
+        if best is None or score < best[0]:
+            best = (score, px, py)
+    if best is None:
+        raise ValueError(f"cannot split a {r}x{s} tiling over {world} ranks")
+    _, px, py = best
+    owner = np.zeros(len(dec.subs), dtype=np.int64)
+    for g, d in enumerate(dec.subs):
+        a, b = i0s.index(d.sp.i0), j0s.index(d.sp.j0)
+        owner[g] = (a // (r // px)) + px * (b // (s // py))
+    return owner
+
+
+@dataclass
+class RankPlan:
+    """This rank's share of the global CommPlan."""
+
+    rank: int
+    world: int
+    owner: np.ndarray
+    local: list  # global subpatch ids owned, in local order
+    plan: G.Plan  # local subpatch ids; src_sub == -1 addresses halo slots
+    e_send: dict = field(default_factory=dict)  # peer -> (local sub ids, local point index), in wire order
+    e_recv: dict = field(default_factory=dict)  # peer -> count
+    mu_send: dict = field(default_factory=dict)
+    mu_recv: dict = field(default_factory=dict)
+
+    def peers(self):
+        return sorted(set(self.e_send) | set(self.e_recv) | set(self.mu_send) | set(self.mu_recv))
+
+    @staticmethod
+    def _flat(send):
+        subs = [np.asarray(send[p][0], dtype=np.int32) for p in sorted(send)]
+        locs = [np.asarray(send[p][1], dtype=np.int32) for p in sorted(send)]
+        z = np.zeros(0, dtype=np.int32)
+        return (np.concatenate(subs) if subs else z), (np.concatenate(locs) if locs else z)
+
+    def flat_e_send(self):
+        return self._flat(self.e_send)
+
+    def flat_mu_send(self):
+        return self._flat(self.mu_send)
+
+
+def split_plan(dec: G.Decomposition, owner: np.ndarray, rank: int, world: int) -> RankPlan:
+    """Split the global plan (every rank holds it) into this rank's local
+    entries and its send/recv lists. Both sides walk the global entry list in
+    the same order, so the k-th value a peer sends is the k-th it expects."""
+    local = [g for g in range(len(dec.subs)) if owner[g] == rank]
+    g2l = {g: l for l, g in enumerate(local)}
+    pl = dec.plan
+
+    def split(dst_sub, dst, src_sub, src, w=None):
+        out = {k: [] for k in ("dst_sub", "dst", "src_sub", "src", "w")}
+        recv_entries = []  # (position in out, peer, j)
+        send, recv = {}, {}
+        for k in range(len(dst)):
+            d_own, s_own = owner[dst_sub[k]], owner[src_sub[k]]
+            if d_own == rank:
+                out["dst_sub"].append(g2l[dst_sub[k]])
+                out["dst"].append(dst[k])
+                if w is not None:
+                    out["w"].append(w[k])
+                if s_own == rank:
+                    out["src_sub"].append(g2l[src_sub[k]])
+                    out["src"].append(src[k])
+                else:
+                    j = recv.get(s_own, 0)
+                    recv[s_own] = j + 1
+                    out["src_sub"].append(-1)
+                    out["src"].append(-1)
+                    recv_entries.append((len(out["src"]) - 1, s_own, j))
+            elif s_own == rank:
+                lst = send.setdefault(d_own, ([], []))
+                lst[0].append(g2l[src_sub[k]])
+                lst[1].append(src[k])
+        base, acc = {}, 0
+        for peer in sorted(recv):
+            base[peer] = acc
+            acc += recv[peer]
+        for pos, peer, j in recv_entries:
+            out["src"][pos] = base[peer] + j
+        return out, send, recv
+
+    sol, e_send, e_recv = split(pl.sol_dst_sub, pl.sol_dst, pl.sol_src_sub, pl.sol_src)
+    vis, mu_send, mu_recv = split(pl.v_dst_sub, pl.v_dst, pl.v_src_sub, pl.v_src, pl.v_w)
+    a = lambda x, dt=np.int32: np.asarray(x, dtype=dt)
+    plan = G.Plan(a(sol["dst_sub"]), a(sol["dst"]), a(sol["src_sub"]), a(sol["src"]), a(vis["dst_sub"]),
+                  a(vis["dst"]), a(vis["src_sub"]), a(vis["src"]), a(vis["w"], np.float64))
+    return RankPlan(rank, world, owner, local, plan, e_send, e_recv, mu_send, mu_recv)
+
+
+class DistributedEngine:
+    """One rank of a multi-GPU superstep (see the module docstring)."""
+
+    def __init__(self, ctx, dec, rank_plan: RankPlan, ic=None, cfg=None, initial_states=None, group=None):
+        import torch
+
+        from . import engine as EN
+        from . import problems as P
+
+        self.rp = rank_plan
+        self.group = group
+        self.device = torch.device("cpu") if ctx.emulate else torch.device("cuda", torch.cuda.current_device())
+        cfg = cfg or EN.EngineConfig()
+        if initial_states is None and ic is not None:
+            initial_states = [P.initial_state(dec, ic, g) for g in rank_plan.local]
+        self.E = EN.Engine(ctx, dec, cfg=cfg, rank_plan=rank_plan, initial_states=None)
+        self.torch = torch
+        # wire buffers (state: [k][4], mu: [k]) and per-peer slices
+        self.n = {w: self.E.halo_size(w) for w in range(4)}
+        f = lambda n: torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
+        self.buf = {"e_send": f(4 * self.n[0]), "e_recv": f(4 * self.n[1]), "mu_send": f(self.n[2]),
+                    "mu_recv": f(self.n[3])}
+        self.dtmin = torch.zeros(1, dtype=torch.int64, device=self.device)
+        if initial_states is not None:
+            for l, e in enumerate(initial_states):
+                self.E.set_state(l, e)
+            self.finish_ic()
+
+    def _slices(self, counts, width):
+        out, acc = {}, 0
+        for peer in sorted(counts):
+            n = counts[peer] if isinstance(counts[peer], int) else len(counts[peer][0])
+            out[peer] = (acc * width, (acc + n) * width)
+            acc += n
+        return out
+
+    def _halo(self, which):
+        import torch.distributed as dist
+
+        name = "e" if which == 0 else "mu"
+        width = 4 if which == 0 else 1
+        send, recv = self.buf[name + "_send"], self.buf[name + "_recv"]
+        sends = self.rp.e_send if which == 0 else self.rp.mu_send
+        recvs = self.rp.e_recv if which == 0 else self.rp.mu_recv
+        self.E.pack(which, send)
+        self._sync_engine()
+        ops = []
+        for peer, (a, b) in self._slices(sends, width).items():
+            ops.append(dist.P2POp(dist.isend, send[a:b], peer, group=self.group))
+        for peer, (a, b) in self._slices(recvs, width).items():
+            ops.append(dist.P2POp(dist.irecv, recv[a:b], peer, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            if self.device.type == "cuda":  # NCCL completes on torch's stream; the engine has its own
+                self.torch.cuda.current_stream().synchronize()
+        self.E.unpack(which, recv)
+
+    def _sync_engine(self):
+        if self.device.type == "cuda":
+            self.torch.cuda.ExternalStream(self.E.stream()).synchronize()
+
+    def _allreduce_dtmin(self):
+        import torch.distributed as dist
+
+        self.E.copy_dtmin(self.dtmin, to_engine=False)
+        self._sync_engine()
+        dist.all_reduce(self.dtmin, op=dist.ReduceOp.MIN, group=self.group)
+        if self.device.type == "cuda":
+            self.torch.cuda.current_stream().synchronize()
+        self.E.copy_dtmin(self.dtmin, to_engine=True)
+
+    def finish_ic(self):
+        """apply_ic tail across ranks: BCs, then one exchange (src/runtime.cpp:284-286)."""
+        self.E.enqueue_part(-1)  # BC on every local subpatch
+        self._halo(0)
+        self.E.enqueue_part(4)
+        self._sync_engine()
+
+    def step(self):
+        """One superstep in Engine::run order (src/runtime.cpp:486-511)."""
+        E = self.E
+        E.enqueue_part(0)
+        self._halo(1)
+        E.enqueue_part(1)
+        self._allreduce_dtmin()
+        E.enqueue_part(2)
+        for s in range(5):
+            E.enqueue_part(3, s)
+            self._halo(0)
+            E.enqueue_part(4)
+        E.enqueue_part(5)
+
+    def run(self, n):
+        for _ in range(n):
+            self.step()
+        self.E.check_error()
+        return n

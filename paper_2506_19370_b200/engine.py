@@ -64,7 +64,9 @@ def _bc_arrays(d: G.SubData):
 
 class Engine:
     def __init__(self, ctx: N.Context, dec: G.Decomposition, ic=None, cfg: EngineConfig = EngineConfig(),
-                 initial_states=None):
+                 initial_states=None, rank_plan=None):
+        """rank_plan (distributed.RankPlan): build only this rank's subpatches,
+        with its halo lists and local plan (multi-GPU)."""
         self.ctx, self.dec, self.cfg = ctx, dec, cfg
         L = ctx.lib
         c = fcsg_engine_config(cfg.cfl, cfg.T, cfg.n_cont, cfg.filter_alpha, cfg.filter_p, cfg.filter_p_smear,
@@ -74,7 +76,9 @@ class Engine:
         ctx.check(L.fcsg_engine_create(ctx.h, C.byref(c), C.byref(h)))
         self.h = h
         self.shape = (dec.subs[0].nj, dec.subs[0].ni)
-        for d in dec.subs:
+        subs = dec.subs if rank_plan is None else [dec.subs[g] for g in rank_plan.local]
+        self.subs = subs
+        for d in subs:
             kind, state, press = _bc_arrays(d)
             arr = [np.ascontiguousarray(a, dtype=np.float64) for a in
                    (d.iq1x, d.iq2x, d.iq1y, d.iq2y, d.h_min, d.h_max, d.w_norm)]
@@ -83,8 +87,14 @@ class Engine:
             ctx.check(L.fcsg_engine_add_subpatch(
                 h, d.patch, d.sp.i0, d.sp.j0, d.ni, d.nj, d.h1, d.h2, mask.ctypes.data_as(C.POINTER(C.c_uint8)),
                 *[N.dptr(a) for a in arr], kind.ctypes.data_as(N.ip), N.dptr(state), N.dptr(press), C.byref(sid)))
-        pl = dec.plan
-        ptr = lambda a: np.ascontiguousarray(a, dtype=np.int32).ctypes.data_as(N.ip)
+        pl = dec.plan if rank_plan is None else rank_plan.plan
+        if rank_plan is not None:
+            es, el = rank_plan.flat_e_send()
+            ms, ml = rank_plan.flat_mu_send()
+            nre = sum(rank_plan.e_recv.values())
+            nrm = sum(rank_plan.mu_recv.values())
+            ctx.check(L.fcsg_engine_set_halo(h, len(es), es.ctypes.data_as(N.ip), el.ctypes.data_as(N.ip), nre,
+                                             len(ms), ms.ctypes.data_as(N.ip), ml.ctypes.data_as(N.ip), nrm))
         keep = [np.ascontiguousarray(a, dtype=np.int32) for a in
                 (pl.sol_dst_sub, pl.sol_dst, pl.sol_src_sub, pl.sol_src, pl.v_dst_sub, pl.v_dst, pl.v_src_sub,
                  pl.v_src)]
@@ -93,7 +103,7 @@ class Engine:
                                          len(keep[4]), *[k.ctypes.data_as(N.ip) for k in keep[4:]], N.dptr(vw)))
         ctx.check(L.fcsg_engine_load_mlp(h, cfg.weights.encode()))
         ctx.check(L.fcsg_engine_finalize(h))
-        if initial_states is None and ic is not None:
+        if initial_states is None and ic is not None and rank_plan is None:
             initial_states = [P.initial_state(dec, ic, k) for k in range(len(dec.subs))]
         if initial_states is not None:
             for k, e in enumerate(initial_states):
@@ -187,6 +197,27 @@ class Engine:
         n = C.c_long()
         self.ctx.check(self.ctx.lib.fcsg_engine_total_points(self.h, C.byref(n)))
         return n.value
+
+    # ---- multi-rank hooks (distributed.py) ---------------------------------
+    def halo_size(self, which):
+        n = C.c_long()
+        self.ctx.check(self.ctx.lib.fcsg_engine_halo_size(self.h, which, C.byref(n)))
+        return n.value
+
+    def pack(self, which, tensor):
+        self.ctx.check(self.ctx.lib.fcsg_engine_pack(self.h, which, C.c_void_p(tensor.data_ptr())))
+
+    def unpack(self, which, tensor):
+        self.ctx.check(self.ctx.lib.fcsg_engine_unpack(self.h, which, C.c_void_p(tensor.data_ptr())))
+
+    def enqueue_part(self, part, stage=0):
+        self.ctx.check(self.ctx.lib.fcsg_engine_enqueue_part(self.h, part, stage))
+
+    def copy_dtmin(self, tensor, to_engine):
+        self.ctx.check(self.ctx.lib.fcsg_engine_copy_dtmin(self.h, C.c_void_p(tensor.data_ptr()), int(to_engine)))
+
+    def check_error(self):
+        self.ctx.check(self.ctx.lib.fcsg_engine_check_error(self.h))
 
     GROUPS = ("viscosity", "blend", "filter", "pass_a", "pass_b", "pass_c", "bc", "exchange")
 
