@@ -308,6 +308,11 @@ void Engine::finalize() {
         }
     }
     E.mlp = static_cast<const double*>(up(mlp_.data(), mlp_.size() * sizeof(double)));
+    {
+        std::vector<double> tt(321);
+        for (int k = 0; k <= 320; ++k) tt[k] = static_cast<double>(tanhl(static_cast<long double>(k) / 16.0L));
+        E.tanh_tab = static_cast<const double*>(up(tt.data(), tt.size() * sizeof(double)));
+    }
     halo_e_.clear();
     halo_mu_.clear();
     for (auto [sb, lc] : halo_e_src_) {

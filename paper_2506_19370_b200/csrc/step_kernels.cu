@@ -646,10 +646,32 @@ struct MlpW {
 };
 #endif
 
-// MlpClassifier::forward + classify_stencil (src/viscosity.cpp:108-133) on a
-// raw 7-point stencil, with normalize_stencil's guard (src/viscosity.cpp:48-59)
-template <class WA>
-FCSG_HD int classify_stencil(const WA& W, const double* s, double abs_floor) {
+// tanh for the classifier. tanh(a + b) = (tanh a + tanh b) / (1 + tanh a tanh b)
+// with a = k/16 from a 321-entry table (tanh of the grid, correctly rounded,
+// kept in shared memory) and |b| <= 1/32, where the odd Taylor polynomial
+// through b^9 is exact to < 1e-18. Absolute error ~3 ulp, against ~1e-15 of
+// libm differences between the reference and any other build; tau parity is
+// gated on the logit margin (> 1e-9) anyway. For |x| >= 20 tanh is 1.0 in
+// double precision.
+constexpr int kTanhTable = 321;  // k/16, k = 0..320
+FCSG_HD double tanh_tab(double x, const double* tab) {
+    const double ax = fabs(x);
+    double r;
+    if (ax >= 20.0) {
+        r = 1.0;
+    } else {
+        const int k = static_cast<int>(ax * 16.0 + 0.5);
+        const double bb = ax - k * 0.0625;  // exact (Sterbenz / k = 0)
+        const double p = bb * bb;
+        const double tb = bb + bb * p * (-1.0 / 3.0 + p * (2.0 / 15.0 + p * (-17.0 / 315.0 + p * (62.0 / 2835.0))));
+        const double ta = tab[k];
+        r = (ta + tb) / (1.0 + ta * tb);
+    }
+    return x < 0.0 ? -r : r;
+}
+
+// normalize_stencil (src/viscosity.cpp:48-59): false = class-4 guard
+FCSG_HD bool normalize7(const double* s, double abs_floor, double* x) {
     double lo = s[0], hi = s[0];
 #pragma unroll
     for (int k = 1; k < kMlpIn; ++k) {
@@ -659,87 +681,165 @@ FCSG_HD int classify_stencil(const WA& W, const double* s, double abs_floor) {
     const double span = hi - lo;
     double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
     scale = scale > 1e-100 ? scale : 1e-100;
-    if (span <= 1e-13 * scale || span <= abs_floor) return 4;
-    double x[kMlpIn];
+    if (span <= 1e-13 * scale || span <= abs_floor) return false;
 #pragma unroll
     for (int k = 0; k < kMlpIn; ++k) x[k] = 2.0 * (s[k] - lo) / span - 1.0;
-    double h[kMlpHidden], g[kMlpHidden];
+    return true;
+}
+
+// MlpClassifier::forward + classify_stencil (src/viscosity.cpp:108-133) for
+// S stencils at once (a point's row and column windows): each weight is
+// fetched once for all S. The layer input lives in this thread's slice of
+// shared memory (hb[k * hs], k = s * 16 + j) and the 16 x S accumulators in
+// registers; the loop runs over inputs j outermost so each input is loaded
+// once per layer.
+template <int S, class WA>
+FCSG_HD void mlp_classes(const WA& W, const double (&x)[S][kMlpIn], const double* tab, double* hb, int hs,
+                         int (&cls)[S]) {
     constexpr int L0 = kMlpHidden * kMlpIn + kMlpHidden;     // layer 0 size (W then b)
     constexpr int LH = kMlpHidden * kMlpHidden + kMlpHidden;  // hidden layer size
+    double acc[S][kMlpHidden];
 #pragma unroll
     for (int i = 0; i < kMlpHidden; ++i) {
-        double acc = W(kMlpHidden * kMlpIn + i);
+        const double bi = W(kMlpHidden * kMlpIn + i);
 #pragma unroll
-        for (int j = 0; j < kMlpIn; ++j) acc += W(i * kMlpIn + j) * x[j];
-        h[i] = tanh(acc);
+        for (int s = 0; s < S; ++s) acc[s][i] = bi;
     }
 #pragma unroll
+    for (int j = 0; j < kMlpIn; ++j)
+#pragma unroll
+        for (int i = 0; i < kMlpHidden; ++i) {
+            const double w = W(i * kMlpIn + j);
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc[s][i] += w * x[s][j];
+        }
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+#pragma unroll
+        for (int i = 0; i < kMlpHidden; ++i) hb[(s * kMlpHidden + i) * hs] = tanh_tab(acc[s][i], tab);
+#pragma unroll 1
     for (int layer = 0; layer < 3; ++layer) {
         const int base = L0 + layer * LH;
 #pragma unroll
         for (int i = 0; i < kMlpHidden; ++i) {
-            double acc = W(base + kMlpHidden * kMlpHidden + i);
+            const double bi = W(base + kMlpHidden * kMlpHidden + i);
 #pragma unroll
-            for (int j = 0; j < kMlpHidden; ++j) acc += W(base + i * kMlpHidden + j) * h[j];
-            g[i] = tanh(acc);
+            for (int s = 0; s < S; ++s) acc[s][i] = bi;
         }
 #pragma unroll
-        for (int i = 0; i < kMlpHidden; ++i) h[i] = g[i];
+        for (int j = 0; j < kMlpHidden; ++j) {
+            double hj[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) hj[s] = hb[(s * kMlpHidden + j) * hs];
+#pragma unroll
+            for (int i = 0; i < kMlpHidden; ++i) {
+                const double w = W(base + i * kMlpHidden + j);
+#pragma unroll
+                for (int s = 0; s < S; ++s) acc[s][i] += w * hj[s];
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int i = 0; i < kMlpHidden; ++i) hb[(s * kMlpHidden + i) * hs] = tanh_tab(acc[s][i], tab);
     }
     constexpr int LO = L0 + 3 * LH;
-    double lg[kMlpOut];
+    double lg[S][kMlpOut];
 #pragma unroll
     for (int i = 0; i < kMlpOut; ++i) {
-        double acc = W(LO + kMlpOut * kMlpHidden + i);
+        const double bi = W(LO + kMlpOut * kMlpHidden + i);
 #pragma unroll
-        for (int j = 0; j < kMlpHidden; ++j) acc += W(LO + i * kMlpHidden + j) * h[j];
-        lg[i] = acc;
+        for (int s = 0; s < S; ++s) lg[s][i] = bi;
     }
-    int best = 0;
 #pragma unroll
-    for (int k = 1; k < kMlpOut; ++k)
-        if (lg[k] > lg[best]) best = k;
-    return best + 1;
+    for (int j = 0; j < kMlpHidden; ++j) {
+        double hj[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) hj[s] = hb[(s * kMlpHidden + j) * hs];
+#pragma unroll
+        for (int i = 0; i < kMlpOut; ++i) {
+            const double w = W(LO + i * kMlpHidden + j);
+#pragma unroll
+            for (int s = 0; s < S; ++s) lg[s][i] += w * hj[s];
+        }
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        int best = 0;  // lowest index wins ties
+#pragma unroll
+        for (int k = 1; k < kMlpOut; ++k)
+            if (lg[s][k] > lg[s][best]) best = k;
+        cls[s] = best + 1;
+    }
 }
 
-// Classifier::classify (src/viscosity.cpp:211-238) for one point of a
-// rectangular subpatch: min of the row-window and column-window classes.
+// Classifier::classify (src/viscosity.cpp:143-160,211-238) at one point of a
+// rectangular subpatch: the row window and the column window
+// (start = clamp(i - 3, 0, n - 7); lines shorter than 7 are class 4), min of
+// the two classes. Both windows go through the MLP together when both pass
+// the normalisation guard.
 template <class WA>
-FCSG_HD int classify_point(const WA& W, const double* f, long base, int ni, int nj, int i, int j, double abs_floor) {
+FCSG_HD int classify_point(const WA& W, const double* tab, double* hb, int hs, const double* f, long base, int ni,
+                           int nj, int i, int j, double abs_floor) {
     double s[kMlpIn];
-    int cr = 4, cc = 4;
+    double xr[kMlpIn], xc[kMlpIn];
+    bool okr = false, okc = false;
     if (ni >= kMlpIn) {
         int st = i - kMlpIn / 2;
         st = st < 0 ? 0 : (st > ni - kMlpIn ? ni - kMlpIn : st);
 #pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(j) * ni + st + k];
-        cr = classify_stencil(W, s, abs_floor);
+        okr = normalize7(s, abs_floor, xr);
     }
     if (nj >= kMlpIn) {
         int st = j - kMlpIn / 2;
         st = st < 0 ? 0 : (st > nj - kMlpIn ? nj - kMlpIn : st);
 #pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(st + k) * ni + i];
-        cc = classify_stencil(W, s, abs_floor);
+        okc = normalize7(s, abs_floor, xc);
     }
-    return cr < cc ? cr : cc;
+    if (okr && okc) {
+        double x[2][kMlpIn];
+        int c[2];
+#pragma unroll
+        for (int k = 0; k < kMlpIn; ++k) {
+            x[0][k] = xr[k];
+            x[1][k] = xc[k];
+        }
+        mlp_classes<2>(W, x, tab, hb, hs, c);
+        return c[0] < c[1] ? c[0] : c[1];
+    }
+    if (okr || okc) {
+        double x[1][kMlpIn];
+        int c[1];
+#pragma unroll
+        for (int k = 0; k < kMlpIn; ++k) x[0][k] = okr ? xr[k] : xc[k];
+        mlp_classes<1>(W, x, tab, hb, hs, c);
+        return c[0];
+    }
+    return 4;
 }
 
 // phase 0, part 2: tau, mu_hat = c(tau) h_max S on interior points
 // (src/viscosity.cpp:240-251); at t=0 also the density class for the smear seed
 template <class WA>
-FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, const EngineDev& E, bool step0) {
+FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, double* tab, double* hbuf,
+                           const double* tab_src, const EngineDev& E, bool step0) {
+    for (int k = t.tid; k < kTanhTable; k += t.nthr) tab[k] = tab_src[k];
+    FCSG_SYNC();
+    double* hb = hbuf + t.tid;  // this thread's slice: hb[k * nthr], k < 2 * 16
+    const int hs = t.nthr;
     const long sz = static_cast<long>(E.ni) * E.nj;
     const long step = static_cast<long>(nblocks) * t.nthr;
     for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
         const long base = (p / sz) * sz;
         const long loc = p - base;
         const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
-        const int tau = classify_point(W, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
+        const int tau = classify_point(W, tab, hb, hs, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
         E.tau[p] = tau;
         E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
         if (step0) {
-            const int tr = classify_point(W, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
+            const int tr = classify_point(W, tab, hb, hs, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
             E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
         }
     }
@@ -937,9 +1037,12 @@ __global__ void __launch_bounds__(NT, 768 / NT)
 __global__ void __launch_bounds__(kThreads) proxy_kernel(const __grid_constant__ EngineDev E) {
     proxy_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
 }
-__global__ void __launch_bounds__(kThreads) classify_kernel(const __grid_constant__ EngineDev E, bool step0) {
-    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, MlpW{}, E,
-                  step0);
+constexpr int kClsThreads = 128;
+__global__ void __launch_bounds__(kClsThreads, 3) classify_kernel(const __grid_constant__ EngineDev E, bool step0) {
+    __shared__ double tab[kTanhTable];
+    __shared__ double hbuf[2 * kMlpHidden * kClsThreads];
+    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, MlpW{}, tab,
+                  hbuf, E.tanh_tab, E, step0);
 }
 __global__ void __launch_bounds__(kThreads) dilate_kernel(const __grid_constant__ EngineDev E) {
     dilate_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
@@ -1075,11 +1178,16 @@ void launch_phase0(const EngineDev& E, bool step0, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     proxy_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E);
     cudaMemcpyToSymbolAsync(c_mlp, E.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
-    classify_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E, step0);
+    {
+        long g = (E.npts + kClsThreads - 1) / kClsThreads;
+        g = g > 148 * 24 ? 148 * 24 : g;
+        classify_kernel<<<static_cast<int>(g), kClsThreads, 0, s>>>(E, step0);
+    }
 #else
     (void)stream;
     proxy_body(Thr{0, 1}, 0, 1, E);
-    classify_body(Thr{0, 1}, 0, 1, MlpW{E.mlp}, E, step0);
+    std::vector<double> tab(kTanhTable), hbuf(2 * kMlpHidden);
+    classify_body(Thr{0, 1}, 0, 1, MlpW{E.mlp}, tab.data(), hbuf.data(), E.tanh_tab, E, step0);
 #endif
 }
 

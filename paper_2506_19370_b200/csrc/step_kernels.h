@@ -77,6 +77,7 @@ struct EngineDev {
     long n_x;
     // classifier weights
     const double* mlp;       // kMlpWeights
+    const double* tanh_tab;  // tanh(k/16), k = 0..320 (classifier tanh table)
     StepScalars* sc;
 };
 
