@@ -717,7 +717,7 @@ FCSG_HD void mlp_classes(const WA& W, const double (&x)[S][kMlpIn], const double
     for (int s = 0; s < S; ++s)
 #pragma unroll
         for (int i = 0; i < kMlpHidden; ++i) hb[(s * kMlpHidden + i) * hs] = tanh_tab(acc[s][i], tab);
-#pragma unroll 1
+#pragma unroll
     for (int layer = 0; layer < 3; ++layer) {
         const int base = L0 + layer * LH;
 #pragma unroll
