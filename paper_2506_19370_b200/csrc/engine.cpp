@@ -309,6 +309,20 @@ void Engine::finalize() {
     }
     E.mlp = static_cast<const double*>(up(mlp_.data(), mlp_.size() * sizeof(double)));
     {
+        // per layer W^T ([in][out]) then b, the classifier kernel's layout
+        const int rows[kMlpLayers] = {16, 16, 16, 16, 4}, cols[kMlpLayers] = {7, 16, 16, 16, 16};
+        std::vector<double> wt;
+        size_t off = 0;
+        for (int l = 0; l < kMlpLayers; ++l) {
+            for (int j = 0; j < cols[l]; ++j)
+                for (int i = 0; i < rows[l]; ++i) wt.push_back(mlp_[off + static_cast<size_t>(i) * cols[l] + j]);
+            off += static_cast<size_t>(rows[l]) * cols[l];
+            for (int i = 0; i < rows[l]; ++i) wt.push_back(mlp_[off + i]);
+            off += rows[l];
+        }
+        E.mlp_t = static_cast<const double*>(up(wt.data(), wt.size() * sizeof(double)));
+    }
+    {
         std::vector<double> tt(321);
         for (int k = 0; k <= 320; ++k) tt[k] = static_cast<double>(tanhl(static_cast<long double>(k) / 16.0L));
         E.tanh_tab = static_cast<const double*>(up(tt.data(), tt.size() * sizeof(double)));

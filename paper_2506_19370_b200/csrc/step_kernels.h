@@ -76,7 +76,8 @@ struct EngineDev {
     const long* x_src;
     long n_x;
     // classifier weights
-    const double* mlp;       // kMlpWeights
+    const double* mlp;       // kMlpWeights, FCNN order (per layer W row-major, then b)
+    const double* mlp_t;     // kMlpWeights, per layer W transposed ([in][out]), then b
     const double* tanh_tab;  // tanh(k/16), k = 0..320 (classifier tanh table)
     StepScalars* sc;
 };
