@@ -631,6 +631,21 @@ FCSG_HD void proxy_body(Thr t, int block, int nblocks, const EngineDev& E) {
     }
 }
 
+// classifier weights: in the CUDA build they live in the constant bank (every
+// thread of a warp reads the same weight at the same time, so each DFMA takes
+// its weight straight from c[][]); refreshed from E.mlp before each launch
+#if FCSG_CUDA
+__constant__ double c_mlp[kMlpWeights];
+struct MlpW {
+    FCSG_HD double operator()(int k) const { return c_mlp[k]; }
+};
+#else
+struct MlpW {
+    const double* p;
+    double operator()(int k) const { return p[k]; }
+};
+#endif
+
 // tanh for the classifier. tanh(a + b) = (tanh a + tanh b) / (1 + tanh a tanh b)
 // with a = k/16 from a 321-entry table (tanh of the grid, correctly rounded,
 // kept in shared memory) and |b| <= 1/32, where the odd Taylor polynomial
@@ -672,165 +687,102 @@ FCSG_HD bool normalize7(const double* s, double abs_floor, double* x) {
     return true;
 }
 
-// MlpClassifier::forward + classify_stencil (src/viscosity.cpp:108-133) for
-// S stencils at once (a point's row and column windows). Weights sit in
-// shared memory transposed per layer (wt[j][i], then the biases; see
-// Engine::finalize), so one broadcast 16-byte load feeds 2 x S DFMAs; the
-// loop over inputs j is not unrolled and tanh is applied in one loop over the
-// layer's outputs, which keeps the kernel small enough for the instruction
-// cache. hb is this thread's slice of shared memory (hb[k * hs]).
-template <int S>
-FCSG_HD void mlp_classes(const double* wt, const double (&x)[S][kMlpIn], const double* tab, double* hb, int hs,
-                         int (&cls)[S]) {
-    constexpr int H = kMlpHidden;
-    double acc[S][H];
-    // layer 0: 7 -> 16
-    {
-        const double* b = wt + kMlpIn * H;
+// MlpClassifier::forward + classify_stencil (src/viscosity.cpp:108-133) on a
+// raw 7-point stencil, with normalize_stencil's guard (src/viscosity.cpp:48-59)
+template <class WA>
+FCSG_HD int classify_stencil(const WA& W, const double* tab, const double* s, double abs_floor) {
+    double lo = s[0], hi = s[0];
 #pragma unroll
-        for (int i = 0; i < H; ++i)
+    for (int k = 1; k < kMlpIn; ++k) {
+        lo = s[k] < lo ? s[k] : lo;
+        hi = s[k] > hi ? s[k] : hi;
+    }
+    const double span = hi - lo;
+    double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+    scale = scale > 1e-100 ? scale : 1e-100;
+    if (span <= 1e-13 * scale || span <= abs_floor) return 4;
+    double x[kMlpIn];
 #pragma unroll
-            for (int s = 0; s < S; ++s) acc[s][i] = b[i];
+    for (int k = 0; k < kMlpIn; ++k) x[k] = 2.0 * (s[k] - lo) / span - 1.0;
+    double h[kMlpHidden], g[kMlpHidden];
+    constexpr int L0 = kMlpHidden * kMlpIn + kMlpHidden;     // layer 0 size (W then b)
+    constexpr int LH = kMlpHidden * kMlpHidden + kMlpHidden;  // hidden layer size
 #pragma unroll
-        for (int j = 0; j < kMlpIn; ++j) {
-            const double2* w2 = reinterpret_cast<const double2*>(wt + j * H);
+    for (int i = 0; i < kMlpHidden; ++i) {
+        double acc = W(kMlpHidden * kMlpIn + i);
 #pragma unroll
-            for (int i2 = 0; i2 < H / 2; ++i2) {
-                const double2 w = w2[i2];
+        for (int j = 0; j < kMlpIn; ++j) acc += W(i * kMlpIn + j) * x[j];
+        h[i] = tanh_tab(acc, tab);
+    }
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    acc[s][2 * i2] += w.x * x[s][j];
-                    acc[s][2 * i2 + 1] += w.y * x[s][j];
-                }
-            }
+    for (int layer = 0; layer < 3; ++layer) {
+        const int base = L0 + layer * LH;
+#pragma unroll
+        for (int i = 0; i < kMlpHidden; ++i) {
+            double acc = W(base + kMlpHidden * kMlpHidden + i);
+#pragma unroll
+            for (int j = 0; j < kMlpHidden; ++j) acc += W(base + i * kMlpHidden + j) * h[j];
+            g[i] = tanh_tab(acc, tab);
         }
+#pragma unroll
+        for (int i = 0; i < kMlpHidden; ++i) h[i] = g[i];
     }
-    const double* lw = wt + kMlpIn * H + H;
-    for (int layer = 0; layer < 4; ++layer) {
-        // tanh of the previous layer's outputs, through shared memory
+    constexpr int LO = L0 + 3 * LH;
+    double lg[kMlpOut];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
+    for (int i = 0; i < kMlpOut; ++i) {
+        double acc = W(LO + kMlpOut * kMlpHidden + i);
 #pragma unroll
-            for (int i = 0; i < H; ++i) hb[(s * H + i) * hs] = acc[s][i];
-#pragma unroll 1
-        for (int k = 0; k < S * H; ++k) hb[k * hs] = tanh_tab(hb[k * hs], tab);
-        const int rows = layer < 3 ? H : kMlpOut;
-        const double* b = lw + H * rows;
-#pragma unroll
-        for (int i = 0; i < H; ++i)
-#pragma unroll
-            for (int s = 0; s < S; ++s) acc[s][i] = i < rows ? b[i] : 0.0;
-        (void)0;
-#pragma unroll 2
-        for (int j = 0; j < H; ++j) {
-            double hj[S];
-#pragma unroll
-            for (int s = 0; s < S; ++s) hj[s] = hb[(s * H + j) * hs];
-            const double2* w2 = reinterpret_cast<const double2*>(lw + j * rows);
-            if (rows == H) {
-#pragma unroll
-                for (int i2 = 0; i2 < H / 2; ++i2) {
-                    const double2 w = w2[i2];
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        acc[s][2 * i2] += w.x * hj[s];
-                        acc[s][2 * i2 + 1] += w.y * hj[s];
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int i2 = 0; i2 < kMlpOut / 2; ++i2) {
-                    const double2 w = w2[i2];
-#pragma unroll
-                    for (int s = 0; s < S; ++s) {
-                        acc[s][2 * i2] += w.x * hj[s];
-                        acc[s][2 * i2 + 1] += w.y * hj[s];
-                    }
-                }
-            }
-        }
-        lw += H * rows + rows;
+        for (int j = 0; j < kMlpHidden; ++j) acc += W(LO + i * kMlpHidden + j) * h[j];
+        lg[i] = acc;
     }
+    int best = 0;
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-        int best = 0;  // lowest index wins ties
-        double bv = acc[s][0];
-#pragma unroll
-        for (int k = 1; k < kMlpOut; ++k)
-            if (acc[s][k] > bv) {
-                bv = acc[s][k];
-                best = k;
-            }
-        cls[s] = best + 1;
-    }
+    for (int k = 1; k < kMlpOut; ++k)
+        if (lg[k] > lg[best]) best = k;
+    return best + 1;
 }
 
-// Classifier::classify (src/viscosity.cpp:143-160,211-238) at one point of a
-// rectangular subpatch: the row window and the column window
-// (start = clamp(i - 3, 0, n - 7); lines shorter than 7 are class 4), min of
-// the two classes. Both windows go through the MLP together when both pass
-// the normalisation guard.
-FCSG_HD int classify_point(const double* wt, const double* tab, double* hb, int hs, const double* f, long base, int ni,
-                           int nj, int i, int j, double abs_floor) {
+// Classifier::classify (src/viscosity.cpp:211-238) for one point of a
+// rectangular subpatch: min of the row-window and column-window classes.
+template <class WA>
+FCSG_HD int classify_point(const WA& W, const double* tab, const double* f, long base, int ni, int nj, int i, int j, double abs_floor) {
     double s[kMlpIn];
-    double xr[kMlpIn], xc[kMlpIn];
-    bool okr = false, okc = false;
+    int cr = 4, cc = 4;
     if (ni >= kMlpIn) {
         int st = i - kMlpIn / 2;
         st = st < 0 ? 0 : (st > ni - kMlpIn ? ni - kMlpIn : st);
 #pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(j) * ni + st + k];
-        okr = normalize7(s, abs_floor, xr);
+        cr = classify_stencil(W, tab, s, abs_floor);
     }
     if (nj >= kMlpIn) {
         int st = j - kMlpIn / 2;
         st = st < 0 ? 0 : (st > nj - kMlpIn ? nj - kMlpIn : st);
 #pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(st + k) * ni + i];
-        okc = normalize7(s, abs_floor, xc);
+        cc = classify_stencil(W, tab, s, abs_floor);
     }
-    if (okr && okc) {
-        double x[2][kMlpIn];
-        int c[2];
-#pragma unroll
-        for (int k = 0; k < kMlpIn; ++k) {
-            x[0][k] = xr[k];
-            x[1][k] = xc[k];
-        }
-        mlp_classes<2>(wt, x, tab, hb, hs, c);
-        return c[0] < c[1] ? c[0] : c[1];
-    }
-    if (okr || okc) {
-        double x[1][kMlpIn];
-        int c[1];
-#pragma unroll
-        for (int k = 0; k < kMlpIn; ++k) x[0][k] = okr ? xr[k] : xc[k];
-        mlp_classes<1>(wt, x, tab, hb, hs, c);
-        return c[0];
-    }
-    return 4;
+    return cr < cc ? cr : cc;
 }
 
 // phase 0, part 2: tau, mu_hat = c(tau) h_max S on interior points
 // (src/viscosity.cpp:240-251); at t=0 also the density class for the smear seed
-FCSG_HD void classify_body(Thr t, int block, int nblocks, double* wt, double* tab, double* hbuf, const EngineDev& E,
-                           bool step0) {
+template <class WA>
+FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, double* tab, const EngineDev& E, bool step0) {
     for (int k = t.tid; k < kTanhTable; k += t.nthr) tab[k] = E.tanh_tab[k];
-    for (int k = t.tid; k < kMlpWeights; k += t.nthr) wt[k] = E.mlp_t[k];
     FCSG_SYNC();
-    double* hb = hbuf + t.tid;  // this thread's slice: hb[k * nthr], k < 2 * 16
-    const int hs = t.nthr;
     const long sz = static_cast<long>(E.ni) * E.nj;
     const long step = static_cast<long>(nblocks) * t.nthr;
     for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
         const long base = (p / sz) * sz;
         const long loc = p - base;
         const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
-        const int tau = classify_point(wt, tab, hb, hs, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
+        const int tau = classify_point(W, tab, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
         E.tau[p] = tau;
         E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
         if (step0) {
-            const int tr = classify_point(wt, tab, hb, hs, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
+            const int tr = classify_point(W, tab, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
             E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
         }
     }
@@ -1028,13 +980,11 @@ __global__ void __launch_bounds__(NT, 768 / NT)
 __global__ void __launch_bounds__(kThreads) proxy_kernel(const __grid_constant__ EngineDev E) {
     proxy_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
 }
-constexpr int kClsThreads = 128;
-__global__ void __launch_bounds__(kClsThreads, 3) classify_kernel(const __grid_constant__ EngineDev E, bool step0) {
+constexpr int kClsThreads = 256;
+__global__ void __launch_bounds__(kClsThreads) classify_kernel(const __grid_constant__ EngineDev E, bool step0) {
     __shared__ double tab[kTanhTable];
-    __shared__ double hbuf[2 * kMlpHidden * kClsThreads];
-    __shared__ __align__(16) double wt[kMlpWeights];
-    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, wt, tab,
-                  hbuf, E, step0);
+    classify_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, MlpW{}, tab, E,
+                  step0);
 }
 __global__ void __launch_bounds__(kThreads) dilate_kernel(const __grid_constant__ EngineDev E) {
     dilate_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
@@ -1169,6 +1119,7 @@ void launch_phase0(const EngineDev& E, bool step0, void* stream) {
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     proxy_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E);
+    cudaMemcpyToSymbolAsync(c_mlp, E.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
     {
         long g = (E.npts + kClsThreads - 1) / kClsThreads;
         g = g > 148 * 24 ? 148 * 24 : g;
@@ -1177,8 +1128,8 @@ void launch_phase0(const EngineDev& E, bool step0, void* stream) {
 #else
     (void)stream;
     proxy_body(Thr{0, 1}, 0, 1, E);
-    std::vector<double> tab(kTanhTable), hbuf(2 * kMlpHidden), wt(kMlpWeights);
-    classify_body(Thr{0, 1}, 0, 1, wt.data(), tab.data(), hbuf.data(), E, step0);
+    std::vector<double> tab(kTanhTable);
+    classify_body(Thr{0, 1}, 0, 1, MlpW{E.mlp}, tab.data(), E, step0);
 #endif
 }
 
