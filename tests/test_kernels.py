@@ -286,3 +286,14 @@ def test_bad_weights_rejected(backend, tmp_path):
         EN.Engine(ctx, dec, ic, EN.EngineConfig(weights=str(bad)))
     with pytest.raises(N.ConfigError):
         EN.Engine(ctx, dec, ic, EN.EngineConfig(weights=str(tmp_path / "missing.bin")))
+
+
+def test_superstep_256_subpatch_compile_time_plan(emu_ctx):
+    """The compile-time n_ext = 280 plan (warp-per-line transform on the GPU)
+    in the emulation harness: one 256x256 Riemann subpatch, 1 superstep."""
+    dec, ic, _ = P.riemann_quadrants(n=256, seed=4)
+    E = EN.Engine(emu_ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+    OE = oracle_engine(dec, ic)
+    OE.step()
+    assert E.run(1) == 1
+    _compare_engines(E, OE, 1)
