@@ -461,123 +461,6 @@ FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mod
     }
 }
 
-// ---------------------------------------------------------------------------
-// warp-per-line transform: one warp (WS lanes; WS = 1 in the CPU emulation)
-// transforms one complex line of the CTA's [pos][line] buffer with no block
-// barrier -- only __syncwarp between stages -- so warps of a CTA run ahead
-// independently and a round costs two block barriers (around the
-// cooperative, coalesced load/store loop) instead of one per stage.
-
-FCSG_HD void warp_sync() {
-#if FCSG_CUDA
-    __syncwarp();
-#endif
-}
-
-template <int P, int L, int NE, int LB, int WS, bool INV>
-FCSG_HD void wstage_reg(int lane, int line, double2* buf, const double2* tw) {
-    constexpr int m = L / P;
-    constexpr int nb = NE / P;
-    constexpr int tstep = NE / L;
-    constexpr int pitch = LB + 1;
-    constexpr int ms = m * pitch;
-#pragma unroll 2
-    for (int b = lane; b < nb; b += WS) {
-        const int blk = b / m;
-        const int j = b - blk * m;
-        double2* p = buf + (blk * L + j) * pitch + line;
-        double2 x[P];
-#pragma unroll
-        for (int q = 0; q < P; ++q) x[q] = p[q * ms];
-        if (!INV) {
-            dft_reg<P, false>(x, tw, NE);
-            if (m > 1 && j) {
-#pragma unroll
-                for (int q = 1; q < P; ++q) x[q] = cmul(x[q], ld2(tw + j * q * tstep));
-            }
-        } else {
-            if (m > 1 && j) {
-#pragma unroll
-                for (int q = 1; q < P; ++q) x[q] = cmulc(x[q], ld2(tw + j * q * tstep));
-            }
-            dft_reg<P, true>(x, tw, NE);
-        }
-#pragma unroll
-        for (int q = 0; q < P; ++q) p[q * ms] = x[q];
-    }
-}
-
-template <int NE, int S, int LB, int WS, bool INV, int END>
-FCSG_HD void wstages(int lane, int line, double2* buf, const double2* tw) {
-    constexpr Factors F = factor_stages(NE);
-    if constexpr (!INV && S < END) {
-        wstage_reg<F.r[S], F.span[S], NE, LB, WS, false>(lane, line, buf, tw);
-        warp_sync();
-        wstages<NE, S + 1, LB, WS, INV, END>(lane, line, buf, tw);
-    } else if constexpr (INV && S >= 0) {
-        wstage_reg<F.r[S], F.span[S], NE, LB, WS, true>(lane, line, buf, tw);
-        warp_sync();
-        wstages<NE, S - 1, LB, WS, INV, END>(lane, line, buf, tw);
-    }
-}
-
-// true when every stage of NE runs in registers (the warp path needs that)
-#if FCSG_CUDA
-__host__ __device__
-#endif
-constexpr bool all_register_radices(int ne) {
-    const Factors f = factor_stages(ne);
-    for (int s = 0; s < f.n; ++s)
-        if (!radix_in_registers(f.r[s])) return false;
-    return true;
-}
-
-// fc_transform for one line by one warp (reference operator: N = NE - 24,
-// 24 gap points, 3 boundary points)
-template <int NE, int LB, int WS>
-FCSG_HD void fc_transform_warp(int lane, int line, double2* buf, const FcPlanDev& pl, int mode) {
-    static_assert(all_register_radices(NE), "warp path needs register radices");
-    constexpr Factors F = factor_stages(NE);
-    constexpr int N = NE - 24;
-    constexpr int pitch = LB + 1;
-    const double* blend = pl.blend;
-    for (int g = lane; g < 24; g += WS) {
-        double2 a = mk2(0.0, 0.0), b = mk2(0.0, 0.0);
-        const double* Ar = blend + g * 3;
-        const double* Al = blend + (23 - g) * 3;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            const double2 fr = buf[(N - 3 + i) * pitch + line];
-            const double2 fl = buf[(2 - i) * pitch + line];
-            const double cr = ld1(Ar + i), cl = ld1(Al + i);
-            a = mk2(a.x + cr * fr.x, a.y + cr * fr.y);
-            b = mk2(b.x + cl * fl.x, b.y + cl * fl.y);
-        }
-        buf[(N + g) * pitch + line] = cadd(a, b);
-    }
-    warp_sync();
-    wstages<NE, 0, LB, WS, false, F.n - 1>(lane, line, buf, pl.tw);
-    {  // last DIF stage + multiplier + first DIT stage, in registers
-        constexpr int P = F.r[F.n - 1];
-        const double2* mult = pl.mult + (mode - 1) * NE;
-        for (int blk = lane; blk < NE / P; blk += WS) {
-            double2* p = buf + blk * P * pitch + line;
-            const double2* mm = mult + blk * P;
-            double2 x[P];
-#pragma unroll
-            for (int q = 0; q < P; ++q) x[q] = p[q * pitch];
-            dft_reg<P, false>(x, pl.tw, NE);
-#pragma unroll
-            for (int q = 0; q < P; ++q) x[q] = cmul(x[q], ld2(mm + q));
-            dft_reg<P, true>(x, pl.tw, NE);
-#pragma unroll
-            for (int q = 0; q < P; ++q) p[q * pitch] = x[q];
-        }
-    }
-    warp_sync();
-    wstages<NE, F.n - 2, LB, WS, true, 0>(lane, line, buf, pl.tw);
-}
-
 // the lengths with a compile-time plan (reference operator, n_cont = 25)
 #if FCSG_CUDA
 __host__ __device__

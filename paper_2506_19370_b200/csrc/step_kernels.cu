@@ -189,13 +189,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
             stage_commit();
         }
         FCSG_SYNC();
-        if constexpr (NE > 0 && all_register_radices(NE) && NTHR == 32 * LB) {
-            // one warp per line, no block barrier inside the transform
-            fc_transform_warp<NE, LB, 32>(tid & 31, tid >> 5, buf, pl, P.mode(r));
-            FCSG_SYNC();
-        } else if constexpr (NE > 0 && all_register_radices(NE) && NTHR == 1) {
-            for (int line = 0; line < LB; ++line) fc_transform_warp<NE, LB, 1>(0, line, buf, pl, P.mode(r));
-        } else if constexpr (NE > 0) {
+        if constexpr (NE > 0) {
             fc_transform_ct<NE, LB, NTHR>(tid, buf, pl, P.mode(r), scr, scr_cap);
         } else {
             fc_transform(Thr{tid, NTHR}, buf, pitch, LB, pl, P.mode(r), scr, scr_cap);
@@ -1054,13 +1048,8 @@ inline int line_threads() {
 template <class Pass, int NE, int LB>
 void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
                       cudaStream_t s) {
-    if constexpr (NE > 0 && all_register_radices(NE)) {
-        // warp-per-line transform: one warp per line of the CTA
-        launch_line_pass_nt<Pass, NE, 32 * LB, LB>(nblk, smem, arg, E, pl, scr_cap, s);
-    } else {
-        if (line_threads() == 128) launch_line_pass_nt<Pass, NE, 128, LB>(nblk, smem, arg, E, pl, scr_cap, s);
-        else launch_line_pass_nt<Pass, NE, 256, LB>(nblk, smem, arg, E, pl, scr_cap, s);
-    }
+    if (line_threads() == 128) launch_line_pass_nt<Pass, NE, 128, LB>(nblk, smem, arg, E, pl, scr_cap, s);
+    else launch_line_pass_nt<Pass, NE, 256, LB>(nblk, smem, arg, E, pl, scr_cap, s);
 }
 #endif
 
