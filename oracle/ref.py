@@ -41,6 +41,9 @@ def lib():
         L.ref_engine_rect.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
                                       C.c_int, C.c_int, ip, dp, dp, C.c_double, C.c_double, C.c_int,
                                       C.c_char_p, C.c_long]
+        L.ref_engine_affine.restype = C.c_void_p
+        L.ref_engine_affine.argtypes = [C.c_double] * 6 + [C.c_int] * 4 + [ip, dp, dp, C.c_double, C.c_double,
+                                                                            C.c_int, C.c_char_p, C.c_long]
         L.ref_engine_destroy.argtypes = [C.c_void_p]
         L.ref_engine_nsubs.argtypes = [C.c_void_p]
         L.ref_engine_dims.argtypes = [C.c_void_p, C.c_int, ip, ip]
@@ -139,16 +142,20 @@ def classify_line(path, values):
 
 
 class RefEngine:
-    """Engine over one rectangular I patch (ref_engine_rect)."""
+    """Engine over one affine I patch origin + q1 e1 + q2 e2 (ref_engine_affine);
+    (lx, ly) alone is the axis-aligned rectangle."""
 
     def __init__(self, x0, y0, lx, ly, r, s, n0, nv, side_kinds, side_states=None,
-                 side_pressure=None, cfl=0.5, T=1e300, workers=1, weight_path="", max_steps=10**9):
+                 side_pressure=None, cfl=0.5, T=1e300, workers=1, weight_path="", max_steps=10**9,
+                 e1=None, e2=None):
         kinds = np.ascontiguousarray(side_kinds, dtype=np.int32)
         states = np.zeros(16) if side_states is None else np.ascontiguousarray(side_states, dtype=np.float64).ravel()
         press = np.ones(4) if side_pressure is None else np.ascontiguousarray(side_pressure, dtype=np.float64)
-        h = lib().ref_engine_rect(x0, y0, lx, ly, r, s, n0, nv,
-                                  kinds.ctypes.data_as(C.POINTER(C.c_int)), _dp(states), _dp(press),
-                                  cfl, T, workers, weight_path.encode(), max_steps)
+        e1 = (lx, 0.0) if e1 is None else e1
+        e2 = (0.0, ly) if e2 is None else e2
+        h = lib().ref_engine_affine(x0, y0, e1[0], e1[1], e2[0], e2[1], r, s, n0, nv,
+                                    kinds.ctypes.data_as(C.POINTER(C.c_int)), _dp(states), _dp(press),
+                                    cfl, T, workers, weight_path.encode(), max_steps)
         if not h:
             _check(9)
         self.h = h

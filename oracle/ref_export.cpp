@@ -232,14 +232,14 @@ int ref_classify_line(const char* path, int n, const double* values, int* tau) {
  * 5 zero_normal_all; -1 = interior side). The engine is initialised with a
  * zero state; call ref_engine_set_state for every subpatch and then
  * ref_engine_finish_ic (== Engine::apply_ic with that state, runtime.cpp:276-287). */
-void* ref_engine_rect(double x0, double y0, double lx, double ly, int r, int s, int n0, int nv,
-                      const int* side_kinds, const double* side_states, const double* side_pressure,
-                      double cfl, double T, int workers, const char* weight_path, long max_steps) {
+void* ref_engine_affine(double x0, double y0, double e1x, double e1y, double e2x, double e2y, int r, int s, int n0,
+                        int nv, const int* side_kinds, const double* side_states, const double* side_pressure,
+                        double cfl, double T, int workers, const char* weight_path, long max_steps) {
     RefEngine* out = nullptr;
     guard([&] {
         geom::Patch p;
         p.kind = geom::PatchKind::I;
-        p.map = std::make_shared<geom::AffineMap>(Vec2{x0, y0}, Vec2{lx, 0}, Vec2{0, ly});
+        p.map = std::make_shared<geom::AffineMap>(Vec2{x0, y0}, Vec2{e1x, e1y}, Vec2{e2x, e2y});
         BcTable bcs;
         const char* names[4] = {"w", "e", "s", "n"};
         for (int k = 0; k < 4; ++k) {
@@ -277,6 +277,13 @@ void* ref_engine_rect(double x0, double y0, double lx, double ly, int r, int s, 
         out = re.release();
     });
     return out;
+}
+
+void* ref_engine_rect(double x0, double y0, double lx, double ly, int r, int s, int n0, int nv,
+                      const int* side_kinds, const double* side_states, const double* side_pressure,
+                      double cfl, double T, int workers, const char* weight_path, long max_steps) {
+    return ref_engine_affine(x0, y0, lx, 0.0, 0.0, ly, r, s, n0, nv, side_kinds, side_states, side_pressure, cfl, T,
+                             workers, weight_path, max_steps);
 }
 
 void ref_engine_destroy(void* h) { delete static_cast<RefEngine*>(h); }

@@ -346,6 +346,12 @@ class Decomposition:
 def rect_decomposition(origin, lx, ly, r, s, n0, nv, side_bcs, nf=5) -> Decomposition:
     """One affine I patch [x0, x0+lx] x [y0, y0+ly], subdivide_Q(r, s, n0, nv).
     side_bcs: 4 entries (W, E, S, N), a BcSpec (physical side) or None (interior side)."""
+    return affine_decomposition(origin, (lx, 0.0), (0.0, ly), r, s, n0, nv, side_bcs, nf)
+
+
+def affine_decomposition(origin, e1, e2, r, s, n0, nv, side_bcs, nf=5) -> Decomposition:
+    """One affine I patch origin + q1 e1 + q2 e2 (a rotated / sheared
+    parallelogram exercises every metric term), subdivide_Q(r, s, n0, nv)."""
     if nv <= nf:
         raise ValueError(f"window construction requires nv > nf (got nv={nv}, nf={nf})")
     names = ("w", "e", "s", "n")
@@ -356,7 +362,7 @@ def rect_decomposition(origin, lx, ly, r, s, n0, nv, side_bcs, nf=5) -> Decompos
         else:
             sides.append(SideInfo(True, names[k]))
             bcs[names[k]] = bc
-    p = AffinePatch(origin=tuple(origin), e1=(lx, 0.0), e2=(0.0, ly), sides=sides)
+    p = AffinePatch(origin=tuple(origin), e1=tuple(e1), e2=tuple(e2), sides=sides)
     subdivide_Q(p, r, s, n0, nv)
     for g, sp in enumerate(p.subpatches):
         sp.global_id = g

@@ -131,6 +131,35 @@ def vortex_tiles(r=8, s=8, seed=5, n0=238, nv=9, noise=1e-3, beta=5.0):
     return dec, ic, {"cfl": 0.5}
 
 
+def rotated_channel(theta=0.3, r=2, s=1, n0=30, nv=9, mach=0.6):
+    """A rotated affine channel (every metric term nonzero) with one side of
+    each boundary-condition kind: W inflow, E outflow_pressure, S slip wall,
+    N no-slip adiabatic wall; a smooth subsonic flow along the channel with a
+    Gaussian density bump. Exercises the general stage passes and
+    src/euler.cpp:105-165."""
+    c, sn = math.cos(theta), math.sin(theta)
+    L, H = 2.0, 1.0
+    e1 = (L * c, L * sn)
+    e2 = (-H * sn, H * c)
+    rho0, p0 = 1.0, 1.0 / GAMMA
+    u0 = mach * math.sqrt(GAMMA * p0 / rho0)
+    inflow = tuple(float(v) for v in conservative(rho0, u0 * c, u0 * sn, p0))
+    bcs = [G.BcSpec(G.INFLOW, inflow), G.BcSpec(G.OUTFLOW_PRESSURE, pressure=p0), G.BcSpec(G.SLIP_WALL),
+           G.BcSpec(G.NOSLIP_ADIABATIC)]
+    dec = G.affine_decomposition((0.0, 0.0), e1, e2, r, s, n0, nv, bcs)
+
+    def ic(x, y):
+        # channel coordinates
+        xi = x * c + y * sn
+        eta = -x * sn + y * c
+        rho = rho0 * (1.0 + 0.2 * np.exp(-((xi - 0.8) ** 2 + (eta - 0.5) ** 2) / 0.02))
+        return conservative(rho, u0 * c, u0 * sn, p0 * (rho / rho0) ** GAMMA)
+
+    return dec, ic, {"cfl": 0.5, "e1": e1, "e2": e2, "kinds": [G.INFLOW, G.OUTFLOW_PRESSURE, G.SLIP_WALL,
+                                                              G.NOSLIP_ADIABATIC], "inflow": inflow,
+                     "pressure": p0}
+
+
 def initial_state(dec, ic, sub):
     """Evaluate an IC on one subpatch (Engine::apply_ic, src/runtime.cpp:276-283)."""
     d = dec.subs[sub]

@@ -97,6 +97,25 @@ def engine_golden():
     for k in range(4):
         d[f"v2_sub{k}_e2"] = R.get_state(k)
         d[f"v2_sub{k}_tau2"] = R.get(k, "tau")
+    # rotated affine channel: all metric terms nonzero, one side of each BC kind
+    dec, ic, meta = P.rotated_channel()
+    states = np.zeros(16)
+    states[0:4] = meta["inflow"]
+    press = np.array([1.0, meta["pressure"], 1.0, 1.0])
+    R = ref.RefEngine(0, 0, 0, 0, 2, 1, 30, 9, meta["kinds"], side_states=states, side_pressure=press,
+                      weight_path=EN.DEFAULT_WEIGHTS, e1=meta["e1"], e2=meta["e2"])
+    for k in range(len(dec.subs)):
+        R.set_state(k, P.initial_state(dec, ic, k))
+    R.finish_ic()
+    for k in range(len(dec.subs)):
+        d[f"rc_sub{k}_e_init"] = R.get_state(k)
+        for f in ("w_norm", "mask", "iq1x", "iq2x", "iq1y", "iq2y"):
+            d[f"rc_sub{k}_geo_{f}"] = R.get(k, f)
+    for _ in range(3):
+        R.step()
+    for k in range(len(dec.subs)):
+        d[f"rc_sub{k}_e3"] = R.get_state(k)
+        d[f"rc_sub{k}_tau3"] = R.get(k, "tau")
     np.savez_compressed(os.path.join(OUT, "engine_golden.npz"), **d)
 
 

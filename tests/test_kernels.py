@@ -297,3 +297,19 @@ def test_superstep_256_subpatch_compile_time_plan(emu_ctx):
     OE.step()
     assert E.run(1) == 1
     _compare_engines(E, OE, 1)
+
+
+def test_superstep_rotated_channel_general_metrics(backend, engine_golden):
+    """General (curvilinear-metric) stage passes with every metric term nonzero
+    and all four BC kinds (inflow, outflow pressure, slip wall, no-slip
+    adiabatic wall): 3 supersteps against the reference's own run."""
+    kind, ctx = backend
+    g = engine_golden
+    dec, ic, _ = P.rotated_channel()
+    states = [g[f"rc_sub{k}_e_init"] for k in range(len(dec.subs))]
+    E = EN.Engine(ctx, dec, cfg=EN.EngineConfig(cfl=0.5), initial_states=states)
+    assert not E.is_cartesian()
+    assert E.run(3) == 3
+    for k in range(len(dec.subs)):
+        assert rel_err(E.get_state(k), g[f"rc_sub{k}_e3"]) < 1e-12
+        assert np.array_equal(E.get(k, "tau"), g[f"rc_sub{k}_tau3"])

@@ -139,3 +139,20 @@ def test_oracle_against_live_reference():
         op = O.get_op(n)
         assert line_rel_l2(op.derivative(f), ref.fc_apply(f, "d1")).max() < 1e-13
         assert line_rel_l2(op.filter(f), ref.fc_apply(f, "filter")).max() < 1e-13
+
+
+def test_engine_rotated_channel_matches_reference(engine_golden):
+    """Rotated affine channel (every metric term nonzero; inflow, outflow
+    pressure, slip and no-slip walls): 3 supersteps against the reference."""
+    g = engine_golden
+    dec, ic, _ = P.rotated_channel()
+    for k, d in enumerate(dec.subs):
+        for f in ("iq1x", "iq2x", "iq1y", "iq2y", "w_norm"):
+            assert rel_err(getattr(d, f), g[f"rc_sub{k}_geo_{f}"]) < 1e-14
+        assert np.array_equal(d.mask, g[f"rc_sub{k}_geo_mask"].astype(np.uint8))
+    E = oracle_engine(dec, states=[g[f"rc_sub{k}_e_init"] for k in range(len(dec.subs))])
+    for _ in range(3):
+        E.step()
+    for k in range(len(dec.subs)):
+        assert rel_err(E.subs[k].e, g[f"rc_sub{k}_e3"]) < 1e-12
+        assert np.array_equal(E.subs[k].tau, g[f"rc_sub{k}_tau3"])
