@@ -96,6 +96,7 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
     const int nblk = static_cast<int>((a.n_lines + lines_per_block - 1) / lines_per_block);
     if (nblk == 0) return;
     a.scr_cap = fc_lines_scr_cap(a.pl, LB);
+    if (a.pl.n_gap == 24 && a.pl.dp1 == 3 && a.pl.n_ext == 536) a.scr_cap = ct_scratch_slots(536, LB);
     const size_t smem = fc_lines_smem_bytes(a.pl, LB, a.scr_cap);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);

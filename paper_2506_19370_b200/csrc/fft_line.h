@@ -441,24 +441,85 @@ FCSG_HD void middle_fused_ct(int tid, double2* buf, const double2* tw, const dou
     }
 }
 
+// Large prime last radix P (e.g. 67 in 536): the last DIF stage, the
+// multiplier and the first DIT stage on P contiguous positions (m = 1, no
+// twiddles) as two direct DFT sweeps -- forward into a full scratch buffer
+// (scr[pos * LB + line], NE * LB slots), one barrier, inverse back into buf.
+// Rotations w_P^{rq} by recurrence, refreshed from the table every 8 steps.
+template <int NE, int LB, int NTHR>
+FCSG_HD void middle_generic_ct(int tid, double2* buf, const double2* tw, const double2* mult, double2* scr) {
+    constexpr Factors F = factor_stages(NE);
+    constexpr int P = F.r[F.n - 1];
+    constexpr int pstep = NE / P;
+    constexpr int pitch = LB + 1;
+    for (int w = tid; w < NE * LB; w += NTHR) {
+        const int line = w % LB;
+        const int pos = w / LB;
+        const int blk = pos / P;
+        const int q = pos - blk * P;
+        const double2* xin = buf + blk * P * pitch + line;
+        const double2 step = ld2(tw + q * pstep);
+        double2 cur = mk2(1.0, 0.0), acc = mk2(0.0, 0.0);
+        int idx = 0;
+        for (int r = 0; r < P; ++r) {
+            acc = cadd(acc, cmul(xin[r * pitch], cur));
+            idx += q;
+            if (idx >= P) idx -= P;
+            cur = ((r & 7) == 7) ? ld2(tw + idx * pstep) : cmul(cur, step);
+        }
+        scr[pos * LB + line] = cmul(acc, ld2(mult + pos));
+    }
+    FCSG_SYNC();
+    for (int w = tid; w < NE * LB; w += NTHR) {
+        const int line = w % LB;
+        const int pos = w / LB;
+        const int blk = pos / P;
+        const int r = pos - blk * P;
+        const double2* yin = scr + blk * P * LB + line;
+        double2 step = ld2(tw + r * pstep);
+        step.y = -step.y;
+        double2 cur = mk2(1.0, 0.0), acc = mk2(0.0, 0.0);
+        int idx = 0;
+        for (int q = 0; q < P; ++q) {
+            acc = cadd(acc, cmul(yin[q * LB], cur));
+            idx += r;
+            if (idx >= P) idx -= P;
+            if ((q & 7) == 7) {
+                cur = ld2(tw + idx * pstep);
+                cur.y = -cur.y;
+            } else {
+                cur = cmul(cur, step);
+            }
+        }
+        buf[pos * pitch + line] = acc;
+    }
+}
+
 // fc_transform for n_ext = NE with the reference continuation (n_cont = 25,
-// degree 2): N = NE - 24.
+// degree 2): N = NE - 24. When the last radix is a large prime, scr must hold
+// NE * LB complex values (see middle_generic_ct).
 template <int NE, int LB, int NTHR>
 FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mode, double2* scr, int scr_cap) {
     constexpr Factors F = factor_stages(NE);
     continuation_ct<NE - 24, 24, 3, LB, NTHR>(tid, buf, pl.blend);
     FCSG_SYNC();
+    dif_stages_ct<NE, 0, LB, NTHR, F.n - 1>(tid, buf, pl.tw, scr, scr_cap);
     if constexpr (radix_in_registers(F.r[F.n - 1])) {
-        dif_stages_ct<NE, 0, LB, NTHR, F.n - 1>(tid, buf, pl.tw, scr, scr_cap);
         middle_fused_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE);
-        FCSG_SYNC();
-        dit_stages_ct<NE, F.n - 2, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
     } else {
-        dif_stages_ct<NE, 0, LB, NTHR, F.n>(tid, buf, pl.tw, scr, scr_cap);
-        spec_mult_ct<NE, LB, NTHR>(tid, buf, pl.mult + (mode - 1) * NE);
-        FCSG_SYNC();
-        dit_stages_ct<NE, F.n - 1, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+        middle_generic_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
     }
+    FCSG_SYNC();
+    dit_stages_ct<NE, F.n - 2, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
+}
+
+// scratch (complex slots) fc_transform_ct<NE, LB> needs
+#if FCSG_CUDA
+__host__ __device__
+#endif
+constexpr int ct_scratch_slots(int ne, int lb) {
+    const Factors f = factor_stages(ne);
+    return radix_in_registers(f.r[f.n - 1]) ? 0 : ne * lb;
 }
 
 // the lengths with a compile-time plan (reference operator, n_cont = 25)

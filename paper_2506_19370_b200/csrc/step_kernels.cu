@@ -1074,6 +1074,7 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
     // FCSG_LINE_LB overrides for experiments
     const int lb_pref = Pass::kStage >= 3 ? 4 : 8;
     const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? (line_lb_env() ? line_lb_env() : lb_pref) : kLB;
+    if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, lb);  // full-scratch prime-67 middle
     const int nblk = E.S * ((nlines + lb - 1) / lb);
     const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap) * sizeof(double2) +
                         static_cast<size_t>(Pass::kStage) * pl.n * lb * sizeof(double);
@@ -1086,6 +1087,7 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
     else if (ref_op && pl.n_ext == 536) launch_line_pass<Pass, 536, 8>(nblk, smem, arg, E, pl, scr_cap, s);
     else launch_line_pass<Pass, 0, 8>(nblk, smem, arg, E, pl, scr_cap, s);
 #else
+    if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, kLB);
     const int nblk = E.S * ((nlines + kLB - 1) / kLB);
     const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2) +
                         static_cast<size_t>(Pass::kStage) * pl.n * kLB * sizeof(double);
