@@ -16,6 +16,7 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
     constexpr int pitch = LB + 1;
     double2* buf = smem;
     double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
+    const FcPlanDev spl = stage_tables(Thr{t.tid, NTHR}, pl, a.mode, scr + a.scr_cap);
     const int N = NE > 0 ? NE - 24 : pl.n;
     const long l0 = static_cast<long>(block) * 2 * LB;
     const long ls = a.line_stride, st = a.stride;
@@ -34,8 +35,8 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
         buf[i * pitch + c] = mk2(v0, v1);
     }
     FCSG_SYNC();
-    if constexpr (NE > 0) fc_transform_ct<NE, LB, NTHR>(t.tid, buf, pl, a.mode, scr, a.scr_cap);
-    else fc_transform(Thr{t.tid, NTHR}, buf, pitch, LB, pl, a.mode, scr, a.scr_cap);
+    if constexpr (NE > 0) fc_transform_ct<NE, LB, NTHR>(t.tid, buf, spl, a.mode, scr, a.scr_cap);
+    else fc_transform(Thr{t.tid, NTHR}, buf, pitch, LB, spl, a.mode, scr, a.scr_cap);
     for (int w = t.tid; w < total; w += NTHR) {
         int i, c;
         if (orows) { i = w % N; c = w / N; }
@@ -75,7 +76,7 @@ void launch_fc_lines_lb(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_
 #endif
 
 size_t fc_lines_smem_bytes(const FcPlanDev& pl, int LB, int scr_cap) {
-    return (static_cast<size_t>(pl.n_ext) * (LB + 1) + scr_cap) * sizeof(double2);
+    return (static_cast<size_t>(pl.n_ext) * (LB + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2);
 }
 
 int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {

@@ -22,19 +22,46 @@
 
 namespace fcsg {
 
-FCSG_HD double2 ld2(const double2* p) {
+// operator tables are read through plain loads: in the kernels they live in
+// shared memory (stage_tables), elsewhere in global memory
+FCSG_HD double2 ld2(const double2* p) { return *p; }
+FCSG_HD double ld1(const double* p) { return *p; }
+
+// read-only global data through the non-coherent path
+FCSG_HD double ldg1(const double* p) {
 #if FCSG_CUDA && defined(__CUDA_ARCH__)
     return __ldg(p);
 #else
     return *p;
 #endif
 }
-FCSG_HD double ld1(const double* p) {
-#if FCSG_CUDA && defined(__CUDA_ARCH__)
-    return __ldg(p);
-#else
-    return *p;
+
+// shared-memory slots (double2) for the staged tables of one operator
+FCSG_HD int table_slots(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
+#if FCSG_CUDA
+__host__
 #endif
+inline int table_slots_host(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
+
+// Copy the twiddles, the multiplier table of `mode` and the blend matrix into
+// shared memory (tab, table_slots() slots) once per CTA, so no stage waits on
+// a first-touch global load; returns a plan pointing at the copies (mult is
+// offset so that plan.mult + (mode-1)*n_ext is the staged table). The caller
+// synchronises before the first transform.
+FCSG_HD FcPlanDev stage_tables(Thr t, const FcPlanDev& pl, int mode, double2* tab) {
+    const int n = pl.n_ext;
+    const double2* msrc = pl.mult + (mode - 1) * n;
+    for (int k = t.tid; k < n; k += t.nthr) {
+        tab[k] = pl.tw[k];
+        tab[n + k] = msrc[k];
+    }
+    double* sb = reinterpret_cast<double*>(tab + 2 * n);
+    for (int k = t.tid; k < pl.n_gap * pl.dp1; k += t.nthr) sb[k] = pl.blend[k];
+    FcPlanDev q = pl;
+    q.tw = tab;
+    q.mult = tab + n - (mode - 1) * n;
+    q.blend = sb;
+    return q;
 }
 
 // ---------------------------------------------------------------------------

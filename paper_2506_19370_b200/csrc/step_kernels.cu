@@ -144,7 +144,9 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
     c.rows = rows;
     double2* buf = smem;
     double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
-    double* stg = reinterpret_cast<double*>(scr + scr_cap);
+    double2* tabs = scr + scr_cap;
+    double* stg = reinterpret_cast<double*>(tabs + table_slots(pl));
+    const FcPlanDev spl = stage_tables(Thr{t.tid, NTHR}, pl, P.mode(0), tabs);  // one mode per pass
     const double inv_len = P.kScaled ? (rows ? E.inv_len1[c.sub] : E.inv_len2[c.sub]) : 1.0;
     const int total = N * LB;
     const int tid = t.tid;
@@ -190,9 +192,9 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
         }
         FCSG_SYNC();
         if constexpr (NE > 0) {
-            fc_transform_ct<NE, LB, NTHR>(tid, buf, pl, P.mode(r), scr, scr_cap);
+            fc_transform_ct<NE, LB, NTHR>(tid, buf, spl, P.mode(r), scr, scr_cap);
         } else {
-            fc_transform(Thr{tid, NTHR}, buf, pitch, LB, pl, P.mode(r), scr, scr_cap);
+            fc_transform(Thr{tid, NTHR}, buf, pitch, LB, spl, P.mode(r), scr, scr_cap);
         }
         if constexpr (KS > 0) stage_wait();
     }
@@ -206,10 +208,10 @@ struct Prim {
 };
 FCSG_HD Prim prim_rhs(const EngineDev& E, long p) {
     Prim q;
-    q.rho = ld1(E.e[0] + p);  // e is read-only in the passes that call this (A, B)
-    q.mx = ld1(E.e[1] + p);
-    q.my = ld1(E.e[2] + p);
-    q.E = ld1(E.e[3] + p);
+    q.rho = ldg1(E.e[0] + p);  // e is read-only in the passes that call this (A, B)
+    q.mx = ldg1(E.e[1] + p);
+    q.my = ldg1(E.e[2] + p);
+    q.E = ldg1(E.e[3] + p);
     const double rs = (q.rho != 0.0) ? q.rho : 1e-300;
     const double pr = kGm1 * (q.E - 0.5 * (q.mx * q.mx + q.my * q.my) / rs);
     q.theta = pr / rs;
@@ -347,23 +349,23 @@ FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double u
             e[p] = u + dt * SB0 * r;
             break;
         case 1: {
-            const double nu = SA20 * ld1(E.e0[c] + p) + SA21 * u + dt * SB1 * r;
+            const double nu = SA20 * ldg1(E.e0[c] + p) + SA21 * u + dt * SB1 * r;
             e[p] = nu;
             E.e2[c][p] = nu;
             break;
         }
         case 2: {
-            const double nu = SA30 * ld1(E.e0[c] + p) + SA32 * u + dt * SB2 * r;
+            const double nu = SA30 * ldg1(E.e0[c] + p) + SA32 * u + dt * SB2 * r;
             e[p] = nu;
             E.e3[c][p] = nu;
             break;
         }
         case 3:
             E.rhs3[c][p] = r;
-            e[p] = SA40 * ld1(E.e0[c] + p) + SA43 * u + dt * SB3 * r;
+            e[p] = SA40 * ldg1(E.e0[c] + p) + SA43 * u + dt * SB3 * r;
             break;
         default:
-            e[p] = SC2 * ld1(E.e2[c] + p) + SC3 * ld1(E.e3[c] + p) + dt * SD3 * ld1(E.rhs3[c] + p) + SC4 * u +
+            e[p] = SC2 * ldg1(E.e2[c] + p) + SC3 * ldg1(E.e3[c] + p) + dt * SD3 * ldg1(E.rhs3[c] + p) + SC4 * u +
                    dt * SD4 * r;
             break;
     }
@@ -380,7 +382,7 @@ struct PassC {
     int stage;
     FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return mk2(ld1(E.tS4[r] + p), ld1(E.tS5[r] + p)); }
+    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return mk2(ldg1(E.tS4[r] + p), ldg1(E.tS5[r] + p)); }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         s[0] = E.tA[r] + p;
         s[1] = E.iq1x + p;
@@ -513,7 +515,7 @@ struct PassCc {
     FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
     FCSG_HD double2 load(int r, long p, const LineCtx&) const {
-        return mk2(ld1(E.tS4[2 * r] + p), ld1(E.tS4[2 * r + 1] + p));
+        return mk2(ldg1(E.tS4[2 * r] + p), ldg1(E.tS4[2 * r + 1] + p));
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         s[0] = E.tA[2 * r] + p;
@@ -543,9 +545,9 @@ struct PassFR {
     FCSG_HD PassFR(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
     FCSG_HD int mode(int) const { return smear ? 4 : 3; }
     FCSG_HD static double2 orig(const EngineDev& E, int r, long p) {
-        const double rho = ld1(E.e[0] + p), mx = ld1(E.e[1] + p);
+        const double rho = ldg1(E.e[0] + p), mx = ldg1(E.e[1] + p);
         if (r == 0) return mk2(rho, mx);
-        const double my = ld1(E.e[2] + p), En = ld1(E.e[3] + p);
+        const double my = ldg1(E.e[2] + p), En = ldg1(E.e[3] + p);
         const double th = kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho;
         return mk2(my, th);
     }
@@ -879,8 +881,8 @@ FCSG_HD void apply_bc_at(const EngineDev& E, const BcDev& bc, long p, long p1, l
             break;
         }
         case 2: {
-            double nx = axis == 0 ? ld1(E.iq1x + p) : ld1(E.iq2x + p);
-            double ny = axis == 0 ? ld1(E.iq1y + p) : ld1(E.iq2y + p);
+            double nx = axis == 0 ? ldg1(E.iq1x + p) : ldg1(E.iq2x + p);
+            double ny = axis == 0 ? ldg1(E.iq1y + p) : ldg1(E.iq2y + p);
             const double nn = hypot(nx, ny);
             nx /= nn;
             ny /= nn;
@@ -1076,7 +1078,7 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
     const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? (line_lb_env() ? line_lb_env() : lb_pref) : kLB;
     if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, lb);  // full-scratch prime-67 middle
     const int nblk = E.S * ((nlines + lb - 1) / lb);
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap) * sizeof(double2) +
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2) +
                         static_cast<size_t>(Pass::kStage) * pl.n * lb * sizeof(double);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (ref_op && pl.n_ext == 280 && lb == 16) launch_line_pass<Pass, 280, 16>(nblk, smem, arg, E, pl, scr_cap, s);
@@ -1089,7 +1091,7 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
 #else
     if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, kLB);
     const int nblk = E.S * ((nlines + kLB - 1) / kLB);
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap) * sizeof(double2) +
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2) +
                         static_cast<size_t>(Pass::kStage) * pl.n * kLB * sizeof(double);
     (void)stream;
     const Pass P(E, arg);
