@@ -24,19 +24,21 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
     const int total = N * LB;
     const bool rows = (st == 1);
     const bool orows = (ost == 1);
+#pragma unroll 4
     for (int w = t.tid; w < total; w += NTHR) {
         int i, c;
         if (rows) { i = w % N; c = w / N; }
         else { c = w % LB; i = w / LB; }
         const long l = l0 + 2 * c;
         double v0 = 0.0, v1 = 0.0;
-        if (l < a.n_lines) v0 = a.in[l * ls + i * st];
-        if (l + 1 < a.n_lines) v1 = a.in[(l + 1) * ls + i * st];
+        if (l < a.n_lines) v0 = ldg1(a.in + l * ls + i * st);
+        if (l + 1 < a.n_lines) v1 = ldg1(a.in + (l + 1) * ls + i * st);
         buf[i * pitch + c] = mk2(v0, v1);
     }
     FCSG_SYNC();
     if constexpr (NE > 0) fc_transform_ct<NE, LB, NTHR>(t.tid, buf, spl, a.mode, scr, a.scr_cap);
     else fc_transform(Thr{t.tid, NTHR}, buf, pitch, LB, spl, a.mode, scr, a.scr_cap);
+#pragma unroll 4
     for (int w = t.tid; w < total; w += NTHR) {
         int i, c;
         if (orows) { i = w % N; c = w / N; }
@@ -50,7 +52,7 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
 
 #if FCSG_CUDA
 template <int LB, int NE>
-__global__ void __launch_bounds__(256, 2) fc_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+__global__ void __launch_bounds__(256, NE > 0 ? 3 : 2) fc_lines_kernel(const __grid_constant__ FcLinesArgs a) {
     extern __shared__ double2 smem[];
     fc_lines_body<LB, NE, 256>(Thr{static_cast<int>(threadIdx.x), 256}, blockIdx.x, smem, a);
 }

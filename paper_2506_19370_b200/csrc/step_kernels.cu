@@ -973,7 +973,7 @@ FCSG_HD void unpack_body(Thr t, int block, int nblocks, const EngineDev& E, int 
 
 #if FCSG_CUDA
 template <int LB, class Pass, int NE, int NT>
-__global__ void __launch_bounds__(NT, 768 / NT)
+__global__ void __launch_bounds__(NT, (NE > 0 ? 768 : 512) / NT)
     line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg) {
     extern __shared__ double2 smem[];
     const Pass P(E, arg);
