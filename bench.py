@@ -158,18 +158,22 @@ def run_reference(args):
 
 # algorithmic HBM bytes per point per launch: every
 # input read once and every output written once; values produced and consumed
-# inside one kernel count zero. The Cartesian passes (every subpatch of the
-# workload) read fewer metric terms than the general ones.
+# inside one kernel count zero. Stage passes in the default flux form; the
+# RK registers are those of stage 1 (the stage time_group launches): e0 read,
+# e2 written. Cartesian (every subpatch of the workload): pass X (rows) and
+# pass Y (cols), no third pass.
 ALG_BYTES_CART = {
-    "pass_a": 32 + 8 + 1 + 64,               # e, iq1x, mask -> tA, tW
-    "pass_b": 32 + 32 + 32 + 8 + 8 + 8 + 96,  # e, tA, tW, iq2y, iq1x, mu -> tA, tS4, tS5
-    "pass_c": 32 + 32 + 8 + 32 + 38 + 32 + 26,  # tS4, tA, iq1x, e, RK regs (avg) -> e, RK regs (avg)
-    "viscosity": 32 + 1 + 8 + 8 * 4,         # e, mask, h_max -> proxy, speed, tau, mu_hat (+ proxy re-read in L1)
-    "filter": 32 + 32 + 32 + 32,             # rows e -> tF ; cols tF -> e
+    "pass_a": 32 + 8 + 8 + 1 + 32,                # e, iq1x, mu, mask -> tA
+    "pass_b": 32 + 8 + 8 + 32 + 32 + 32 + 32,     # e, iq2y, mu, tA, e0 -> e2, e
+    "pass_c": 0,
+    "viscosity": 32 + 1 + 8 + 8 * 4,              # e, mask, h_max -> proxy, speed, tau, mu_hat (+ proxy re-read in L1)
+    "filter": 32 + 32 + 32 + 32,                  # rows e -> tF ; cols tF -> e
     "blend": 8 * 5 + 1 + 8,
 }
-ALG_BYTES_GEN = dict(ALG_BYTES_CART, pass_a=32 + 16 + 1 + 64, pass_b=32 + 32 + 32 + 32 + 8 + 96,
-                     pass_c=64 + 32 + 16 + 32 + 38 + 32 + 26)
+# general: GA (rows, D1 w), GB (cols), C (rows)
+ALG_BYTES_GEN = dict(ALG_BYTES_CART, pass_a=32 + 1 + 32,                      # e, mask -> tW
+                     pass_b=32 + 32 + 8 + 32 + 32 + 32 + 32,                 # e, 4 metrics, mu, tW -> tS4, tS5, tA
+                     pass_c=64 + 32 + 16 + 32 + 32 + 32 + 32)                # tS4, tS5, tA, iq1x, iq1y, e, e0 -> e2, e
 LAUNCHES = {"pass_a": 5, "pass_b": 5, "pass_c": 5, "viscosity": 1, "filter": 1, "blend": 1, "bc": 6,
             "exchange": 5}
 
@@ -316,7 +320,8 @@ def run_fcsg(args):
     groups = {}
     for g in ("viscosity", "blend", "filter", "pass_a", "pass_b", "pass_c", "bc", "exchange"):
         groups[g] = E.time_group(g, reps=5)
-    share = {g: groups[g] * LAUNCHES[g] for g in groups}
+    launches = dict(LAUNCHES, pass_c=0 if E.is_cartesian() else 5)
+    share = {g: groups[g] * launches[g] for g in groups}
     dom = max(share, key=share.get)
     hbm, peak_kind = peaks()
     ALG_BYTES = ALG_BYTES_CART if E.is_cartesian() else ALG_BYTES_GEN

@@ -111,6 +111,8 @@ typedef struct {
     int smear_radius;        /* 10 */
     int debug_rhs;           /* keep the last stage's rhs readable (parity hooks) */
     int force_general;       /* 1: never use the Cartesian (zero metric term) passes */
+    int reference_order;     /* 1: accumulate the rhs in euler_rhs's order (40 line derivatives);
+                                0: flux form div(mu grad w - f), 24 */
 } fcsg_engine_config;
 
 /* BcKind codes (include/fcs/bc.hpp:10-17); -1 = no boundary condition */

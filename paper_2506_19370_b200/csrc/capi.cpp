@@ -258,6 +258,7 @@ int fcsg_engine_create(fcsg_ctx* ctx, const fcsg_engine_config* cfg, fcsg_engine
         c.smear_radius = cfg->smear_radius;
         c.debug_rhs = cfg->debug_rhs != 0;
         c.allow_cartesian = cfg->force_general == 0;
+        c.reference_order = cfg->reference_order != 0;
         auto* e = new fcsg_engine{ctx, std::make_unique<Engine>(*ctx, c)};
         *out = e;
     });
@@ -420,7 +421,7 @@ int fcsg_engine_time_group(fcsg_engine* e, int which, int reps, double* ms) {
 
 int fcsg_engine_launches_per_step(fcsg_engine* e, int* n) {
     if (!e) return FCSG_USAGE;
-    return guard(e->ctx, [&] { *n = kLaunchesPerStep; });
+    return guard(e->ctx, [&] { *n = e->eng->launches_per_step(); });
 }
 
 }  // extern "C"

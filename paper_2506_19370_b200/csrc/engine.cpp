@@ -217,6 +217,7 @@ void Engine::finalize() {
     E.abs_floor = cfg_.abs_floor;
     E.smear_radius = cfg_.smear_radius;
     E.cartesian = cfg_.allow_cartesian ? 1 : 0;
+    E.reference_order = cfg_.reference_order ? 1 : 0;
     for (const auto& sp : subs_)
         for (size_t k = 0; k < sp.iq2x.size(); ++k)
             if (sp.iq2x[k] != 0.0 || sp.iq1y[k] != 0.0) E.cartesian = 0;
@@ -492,7 +493,7 @@ void Engine::launch_group(int which) {
         case 1: launch_phase1(E_, s); break;
         case 2: launch_phase2(E_, plans_, false, s); break;
         case 3: launch_pass_a(E_, plans_, s); break;
-        case 4: launch_pass_b(E_, plans_, s); break;
+        case 4: launch_pass_b(E_, plans_, 1, s); break;
         case 5: launch_pass_c(E_, plans_, 1, s); break;
         case 6: launch_bc(E_, s); break;
         case 7: launch_exchange(E_, s); break;

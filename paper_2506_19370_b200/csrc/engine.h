@@ -34,6 +34,7 @@ struct EngineConfig {
     int smear_radius = 10;
     bool debug_rhs = false;                    // keep the last stage's rhs for parity hooks
     bool allow_cartesian = true;               // use the zero-metric-term passes when they apply
+    bool reference_order = false;              // euler_rhs's accumulation order instead of the flux form
 };
 
 struct SubSpec {
@@ -104,6 +105,7 @@ class Engine {
     // (filter rows + cols), 3 pass A, 4 pass B, 5 pass C (stage 1), 6 BC,
     // 7 exchange
     double time_pass(int which, int reps);
+    int launches_per_step() const { return fcsg::launches_per_step(E_); }
     void launch_group(int which);
     void* stream() const { return ctx_.stream; }
 

@@ -124,7 +124,11 @@ FCSG_HD void stage_wait() {
 // partials, metrics, mu, RK registers) are prefetched into shared memory with
 // cp.async right before the round's FFT and waited for after it, so their
 // latency hides behind the transform. Each thread stages and consumes only its
-// own slots (stage[k * total + w]).
+// own slots (stage[k * total + w]): kStage cp.async slots (a null source
+// leaves a slot as the previous round staged it), then kStash slots the pass
+// itself writes in load/store to keep per-point values across rounds. The
+// double2 store(r - 1) returns is handed to load(r) at the same point (a round
+// whose input is computed from the previous round's result).
 template <int LB, class Pass, int NE, int NTHR>
 FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const EngineDev& E, const FcPlanDev& pl,
                        int scr_cap) {
@@ -163,11 +167,12 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
             }
             if (l < c.nl_valid) {
                 const long p = pidx(c, l, i);
+                double2 carry = mk2(0.0, 0.0);
                 if (r > 0) {
                     const double2 v = buf[i * pitch + l];
-                    P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c);
+                    carry = P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c);
                 }
-                if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c);
+                if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c, carry, stg + w, total);
             } else if (r < Pass::kRounds) {
                 buf[i * pitch + l] = mk2(0.0, 0.0);
             }
@@ -186,7 +191,8 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
                 if (l >= c.nl_valid) continue;
                 const double* src[KS > 0 ? KS : 1];
                 const int n = P.stage_srcs(r, pidx(c, l, i), src);
-                for (int k = 0; k < n; ++k) stage_copy(stg + k * total + w, src[k]);
+                for (int k = 0; k < n; ++k)
+                    if (src[k]) stage_copy(stg + k * total + w, src[k]);
             }
             stage_commit();
         }
@@ -246,11 +252,13 @@ struct PassA {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 6;
     static constexpr int kStage = 2;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 8;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassA(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, double*, int) const {
         const Prim q = prim_rhs(E, p);
         if (r == 0) check_positive(E, q, p, c);
         if (r < 4) return flux_pair(q, r);
@@ -263,7 +271,7 @@ struct PassA {
         s[1] = E.iq1y + p;
         return 2;
     }
-    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
         if (r < 4) {
             E.tA[r][p] = st[0] * v.x + st[ss] * v.y;
         } else {
@@ -271,6 +279,7 @@ struct PassA {
             E.tW[c0][p] = v.x;
             E.tW[c0 + 1][p] = v.y;
         }
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -281,11 +290,13 @@ struct PassB {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 10;
     static constexpr int kStage = 7;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassB(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const {
         if (r >= 6) return mk2(E.tS4[r - 6][p], E.tS5[r - 6][p]);
         const Prim q = prim_rhs(E, p);
         if (r < 4) return flux_pair(q, r);
@@ -312,7 +323,7 @@ struct PassB {
         s[2] = E.tA[r - 6] + p;
         return 3;
     }
-    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
         const double b = st[0], d = st[ss];
         if (r < 4) {
             E.tA[r][p] = -(st[2 * ss] + (b * v.x + d * v.y));
@@ -330,6 +341,7 @@ struct PassB {
         } else {
             E.tA[r - 6][p] = st[2 * ss] + (b * v.x + d * v.y);
         }
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -377,12 +389,14 @@ struct PassC {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 4;
     static constexpr int kStage = 4;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
     FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return mk2(ldg1(E.tS4[r] + p), ldg1(E.tS5[r] + p)); }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const { return mk2(ldg1(E.tS4[r] + p), ldg1(E.tS5[r] + p)); }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         s[0] = E.tA[r] + p;
         s[1] = E.iq1x + p;
@@ -390,8 +404,9 @@ struct PassC {
         s[3] = E.e[r] + p;
         return 4;
     }
-    FCSG_HD void store(int c, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int c, long p, double2 v, const double* st, int ss, const LineCtx&) const {
         ssprk_update(E, stage, c, p, st[3 * ss], st[0] + (st[ss] * v.x + st[2 * ss] * v.y));
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -411,11 +426,13 @@ struct PassAc {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 4;
     static constexpr int kStage = 1;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 8;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassAc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, double*, int) const {
         const Prim q = prim_rhs(E, p);
         if (r == 0) check_positive(E, q, p, c);
         if (r < 2) {
@@ -430,7 +447,7 @@ struct PassAc {
         s[0] = E.iq1x + p;
         return 1;
     }
-    FCSG_HD void store(int r, long p, double2 v, const double* st, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int, const LineCtx&) const {
         if (r < 2) {
             const double a = st[0];
             E.tA[2 * r][p] = a * v.x;
@@ -440,6 +457,7 @@ struct PassAc {
             E.tW[c0][p] = v.x;
             E.tW[c0 + 1][p] = v.y;
         }
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -450,11 +468,13 @@ struct PassBc {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 6;
     static constexpr int kStage = 5;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassBc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const {
         if (r >= 4) return mk2(E.tS5[2 * (r - 4)][p], E.tS5[2 * (r - 4) + 1][p]);
         const Prim q = prim_rhs(E, p);
         if (r < 2) {
@@ -483,7 +503,7 @@ struct PassBc {
         s[2] = E.tA[2 * (r - 4) + 1] + p;
         return 3;
     }
-    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
         const double d = st[0], t0 = st[ss], t1 = st[2 * ss];
         if (r < 2) {
             E.tA[2 * r][p] = -(t0 + d * v.x);
@@ -500,6 +520,7 @@ struct PassBc {
             E.tA[c0][p] = t0 + d * v.x;
             E.tA[c0 + 1][p] = t1 + d * v.y;
         }
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -509,12 +530,14 @@ struct PassCc {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 2;
     static constexpr int kStage = 5;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
     FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const {
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const {
         return mk2(ldg1(E.tS4[2 * r] + p), ldg1(E.tS4[2 * r + 1] + p));
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
@@ -525,10 +548,228 @@ struct PassCc {
         s[4] = E.e[2 * r + 1] + p;
         return 5;
     }
-    FCSG_HD void store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
         const double a = st[2 * ss];
         ssprk_update(E, stage, 2 * r, p, st[3 * ss], st[0] + a * v.x);
         ssprk_update(E, stage, 2 * r + 1, p, st[4 * ss], st[ss] + a * v.y);
+        return {};
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// ---- flux form (default) ---------------------------------------------------
+// euler_rhs accumulates, per component c (src/euler.cpp:43-100),
+//   -(iq1x D1F + iq2x D2F) - (iq1y D1G + iq2y D2G) + (iq1x D1s4 + iq2x D2s4) + (iq1y D1s5 + iq2y D2s5)
+// with s4 = mu grad_x w and s5 = mu grad_y w. The FC derivative is linear and
+// the same metric factor multiplies D_k F and D_k s4 (resp. D_k G and D_k s5),
+// so the rhs equals
+//   iq1x D1(s4 - F) + iq2x D2(s4 - F) + iq1y D1(s5 - G) + iq2y D2(s5 - G),
+// i.e. div(mu grad w - f): the same operator, differing only by round-off
+// reassociation, with 24 line derivatives per stage instead of 40 (16 instead
+// of 24 on Cartesian subpatches, where iq2x = iq1y = 0 as above).
+// EngineConfig::reference_order keeps the reference's accumulation (passes
+// A/B/C and A'/B'/C' above).
+
+// Cartesian flux form, pass X (rows, 4 rounds): D1 of (rho, rho u) ->
+// Phi_x = mu iq1x D1 w - F (handed to the next round) -> D1 Phi_x ->
+// tA = iq1x D1 Phi_x; then the same for (rho v, theta).
+// slots: 0 iq1x, 1 mu (staged in the rounds that differentiate w, kept after)
+struct PassXc {
+    static constexpr bool kRows = true;
+    static constexpr int kRounds = 4;
+    static constexpr int kStage = 2;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    FCSG_HD PassXc(const EngineDev& e, int) : E(e) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2 carry, double*, int) const {
+        const Prim q = prim_rhs(E, p);
+        if (r & 1) {
+            const int c0 = r - 1;  // 0 or 2
+            const double2 f0 = flux_pair(q, c0), f1 = flux_pair(q, c0 + 1);
+            return mk2(carry.x - f0.x, carry.y - f1.x);
+        }
+        if (r == 0) {
+            check_positive(E, q, p, c);
+            return mk2(q.rho, q.mx);
+        }
+        return mk2(q.my, q.theta);
+    }
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        if (r & 1) return 0;
+        s[0] = E.iq1x + p;
+        s[1] = E.mu + p;
+        return 2;
+    }
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        const double a = st[0];
+        if (!(r & 1)) {
+            const double m = st[ss];
+            return mk2(m * (a * v.x), m * (a * v.y));  // s4 = mu (iq1x D1 w + 0 D2 w)
+        }
+        const int c0 = r - 1;
+        E.tA[c0][p] = a * v.x;
+        E.tA[c0 + 1][p] = a * v.y;
+        return {};
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// Cartesian flux form, pass Y (cols, 4 rounds): D2 of (rho v, theta) ->
+// Phi_y = mu iq2y D2 w - G -> D2 Phi_y -> rhs = tA + iq2y D2 Phi_y -> SSPRK
+// update of components 2, 3; then the same for (rho, rho u). Components 2, 3
+// are updated first: G_0 = rho v and G_1 = rho u v need the old rho v, kept in
+// stash slot 3 by the first load (rho and rho u are still unmodified then).
+// slots: 0 iq2y, 1 mu | 1, 2 tA pair (update rounds), 3 old rho v
+struct PassYc {
+    static constexpr bool kRows = false;
+    static constexpr int kRounds = 4;
+    static constexpr int kStage = 3;
+    static constexpr int kStash = 1;
+    static constexpr int kLB = 4;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    int stage;
+    FCSG_HD PassYc(const EngineDev& e, int s) : E(e), stage(s) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2 carry, double* st, int ss) const {
+        switch (r) {
+            case 0: {
+                const Prim q = prim_rhs(E, p);
+                st[3 * ss] = q.my;
+                return mk2(q.my, q.theta);
+            }
+            case 1: {
+                const Prim q = prim_rhs(E, p);  // e is still unmodified at this point
+                return mk2(carry.x - flux_pair(q, 2).y, carry.y - flux_pair(q, 3).y);
+            }
+            case 2: return mk2(ldg1(E.e[0] + p), ldg1(E.e[1] + p));
+            default: {
+                const double rho = ldg1(E.e[0] + p), mx = ldg1(E.e[1] + p), my = st[3 * ss];
+                const double v = my / rho;
+                return mk2(carry.x - my, carry.y - mx * v);  // G_0, G_1 (src/euler.cpp:64-75)
+            }
+        }
+    }
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        if (!(r & 1)) {
+            s[0] = E.iq2y + p;
+            s[1] = E.mu + p;
+            return 2;
+        }
+        const int c0 = r == 1 ? 2 : 0;
+        s[0] = nullptr;  // keep iq2y
+        s[1] = E.tA[c0] + p;
+        s[2] = E.tA[c0 + 1] + p;
+        return 3;
+    }
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        const double d = st[0];
+        if (!(r & 1)) {
+            const double m = st[ss];
+            return mk2(m * (d * v.x), m * (d * v.y));  // s5 = mu (0 D1 w + iq2y D2 w)
+        }
+        const int c0 = r == 1 ? 2 : 0;
+        ssprk_update(E, stage, c0, p, E.e[c0][p], st[ss] + d * v.x);
+        ssprk_update(E, stage, c0 + 1, p, E.e[c0 + 1][p], st[2 * ss] + d * v.y);
+        return {};
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// General flux form, pass A (rows, 2 rounds): D1 w -> tW
+struct PassGA {
+    static constexpr bool kRows = true;
+    static constexpr int kRounds = 2;
+    static constexpr int kStage = 0;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 8;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    FCSG_HD PassGA(const EngineDev& e, int) : E(e) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, double*, int) const {
+        const Prim q = prim_rhs(E, p);
+        if (r == 0) {
+            check_positive(E, q, p, c);
+            return mk2(q.rho, q.mx);
+        }
+        return mk2(q.my, q.theta);
+    }
+    FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
+    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
+        E.tW[2 * r][p] = v.x;
+        E.tW[2 * r + 1][p] = v.y;
+        return {};
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
+// General flux form, pass B (cols, 6 rounds per component pair):
+// D2 w -> Phi_x = mu grad_x w - F (tS4), Phi_y = mu grad_y w - G (tS5, and
+// the next round's input) -> D2 Phi_y -> tA = iq2y D2 Phi_y -> D2 Phi_x ->
+// tA += iq2x D2 Phi_x. Pass C then adds iq1x D1 Phi_x + iq1y D1 Phi_y and
+// updates (PassC reads tS4/tS5 = Phi_x/Phi_y).
+// slots: 0 iq1x, 1 iq2x, 2 iq1y, 3 iq2y, 4 mu, 5-6 tW pair (staged in the w rounds)
+struct PassGB {
+    static constexpr bool kRows = false;
+    static constexpr int kRounds = 6;
+    static constexpr int kStage = 7;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    FCSG_HD PassGB(const EngineDev& e, int) : E(e) {}
+    FCSG_HD int mode(int) const { return 1; }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2 carry, double*, int) const {
+        const int k = r % 3, c0 = 2 * (r / 3);
+        if (k == 1) return carry;
+        if (k == 2) return mk2(E.tS4[c0][p], E.tS4[c0 + 1][p]);  // written by this thread in round r - 2
+        const Prim q = prim_rhs(E, p);
+        return c0 == 0 ? mk2(q.rho, q.mx) : mk2(q.my, q.theta);
+    }
+    FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        if (r % 3 != 0) return 0;  // metric slots kept from the w round
+        const int c0 = 2 * (r / 3);
+        s[0] = E.iq1x + p;
+        s[1] = E.iq2x + p;
+        s[2] = E.iq1y + p;
+        s[3] = E.iq2y + p;
+        s[4] = E.mu + p;
+        s[5] = E.tW[c0] + p;
+        s[6] = E.tW[c0 + 1] + p;
+        return 7;
+    }
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+        const int k = r % 3, c0 = 2 * (r / 3);
+        if (k == 0) {
+            const double a = st[0], b = st[ss], cc = st[2 * ss], d = st[3 * ss], mu = st[4 * ss];
+            const double d1[2] = {st[5 * ss], st[6 * ss]};
+            const double d2[2] = {v.x, v.y};
+            const Prim q = prim_rhs(E, p);
+            double phy[2];
+            for (int j = 0; j < 2; ++j) {
+                const double2 fg = flux_pair(q, c0 + j);
+                const double gx = a * d1[j] + b * d2[j];
+                const double gy = cc * d1[j] + d * d2[j];
+                E.tS4[c0 + j][p] = mu * gx - fg.x;
+                phy[j] = mu * gy - fg.y;
+                E.tS5[c0 + j][p] = phy[j];
+            }
+            return mk2(phy[0], phy[1]);
+        }
+        if (k == 1) {
+            const double d = st[3 * ss];
+            E.tA[c0][p] = d * v.x;
+            E.tA[c0 + 1][p] = d * v.y;
+            return {};
+        }
+        const double b = st[ss];
+        E.tA[c0][p] = E.tA[c0][p] + b * v.x;
+        E.tA[c0 + 1][p] = E.tA[c0 + 1][p] + b * v.y;
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -539,6 +780,8 @@ struct PassFR {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 2;
     static constexpr int kStage = 0;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 8;
     static constexpr bool kScaled = false;
     const EngineDev& E;
     bool smear;
@@ -551,9 +794,9 @@ struct PassFR {
         const double th = kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho;
         return mk2(my, th);
     }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return orig(E, r, p); }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const { return orig(E, r, p); }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
-    FCSG_HD void store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
         if (smear) {
             const double m = E.m01[p];
             const double2 f = orig(E, r, p);
@@ -561,6 +804,7 @@ struct PassFR {
         }
         E.tF[2 * r][p] = v.x;
         E.tF[2 * r + 1][p] = v.y;
+        return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
@@ -570,14 +814,16 @@ struct PassFC {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 2;
     static constexpr int kStage = 0;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 8;
     static constexpr bool kScaled = false;
     const EngineDev& E;
     bool smear;
     FCSG_HD PassFC(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
     FCSG_HD int mode(int) const { return smear ? 4 : 3; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&) const { return mk2(E.tF[2 * r][p], E.tF[2 * r + 1][p]); }
+    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const { return mk2(E.tF[2 * r][p], E.tF[2 * r + 1][p]); }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
-    FCSG_HD void store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
         if (smear) {
             const double m = E.m01[p];
             const double fa = E.tF[2 * r][p], fb = E.tF[2 * r + 1][p];
@@ -590,6 +836,7 @@ struct PassFC {
             E.e[2][p] = v.x;
             E.tF[3][p] = v.y;  // theta, consumed by finish()
         }
+        return {};
     }
     FCSG_HD void finish(Thr t, const LineCtx& c, int N) const {
         // E = rho theta/(gamma-1) + |m|^2 / (2 rho)   (src/runtime.cpp:413-420)
@@ -1026,7 +1273,7 @@ int grid_for(long n) {
 
 #if FCSG_CUDA
 template <class Pass, int NE, int NT, int LB>
-void launch_line_pass_nt(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
+void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
                          cudaStream_t s) {
     auto k = line_pass_kernel<LB, Pass, NE, NT>;
     static bool attr_set = false;  // once per instantiation (not during graph capture)
@@ -1038,67 +1285,40 @@ void launch_line_pass_nt(int nblk, size_t smem, int arg, const EngineDev& E, con
     k<<<nblk, NT, smem, s>>>(E, pl, scr_cap, arg);
 }
 
-// CTA size of the line passes (FCSG_LINE_THREADS=128|256, default 256)
-inline int line_threads() {
-    static const int nt = [] {
-        const char* v = std::getenv("FCSG_LINE_THREADS");
-        return (v && std::atoi(v) == 128) ? 128 : 256;
-    }();
-    return nt;
-}
-
-template <class Pass, int NE, int LB>
-void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
-                      cudaStream_t s) {
-    if (line_threads() == 128) launch_line_pass_nt<Pass, NE, 128, LB>(nblk, smem, arg, E, pl, scr_cap, s);
-    else launch_line_pass_nt<Pass, NE, 256, LB>(nblk, smem, arg, E, pl, scr_cap, s);
-}
 #endif
 
-// FCSG_LINE_LB=4|8|16 forces the lines per CTA of the compile-time-plan passes (0 = per-pass default)
-inline int line_lb_env() {
-    static const int lb = [] {
-        const char* v = std::getenv("FCSG_LINE_LB");
-        const int x = v ? std::atoi(v) : 0;
-        return (x == 16 || x == 8 || x == 4) ? x : 0;
-    }();
-    return lb;
-}
-
+// Lines per CTA: Pass::kLB for the compile-time plans (4 where a large
+// staging area would otherwise cost occupancy: three 256-thread CTAs per SM
+// fit in shared memory), kLB for the generic plan.
 template <class Pass>
 void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap, void* stream) {
+    constexpr int kSlots = Pass::kStage + Pass::kStash;
     const int nlines = Pass::kRows ? E.nj : E.ni;
     // the compile-time plans assume the reference operator (n_cont 25, degree 2)
     const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
+    const bool ct = ref_op && (pl.n_ext == 280 || pl.n_ext == 536);
 #if FCSG_CUDA
-    // lines per CTA: passes with a large epilogue staging area use 4 (three
-    // 256-thread CTAs per SM fit in shared memory), the others 8;
-    // FCSG_LINE_LB overrides for experiments
-    const int lb_pref = Pass::kStage >= 3 ? 4 : 8;
-    const int lb = (ref_op && (pl.n_ext == 280 || pl.n_ext == 536)) ? (line_lb_env() ? line_lb_env() : lb_pref) : kLB;
+    constexpr int kCtLB = Pass::kLB;
+#else
+    constexpr int kCtLB = kLB;  // the emulation covers the loop structure, not the CTA shape
+#endif
+    const int lb = ct ? kCtLB : kLB;
     if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, lb);  // full-scratch prime-67 middle
     const int nblk = E.S * ((nlines + lb - 1) / lb);
     const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2) +
-                        static_cast<size_t>(Pass::kStage) * pl.n * lb * sizeof(double);
+                        static_cast<size_t>(kSlots) * pl.n * lb * sizeof(double);
+#if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (ref_op && pl.n_ext == 280 && lb == 16) launch_line_pass<Pass, 280, 16>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ref_op && pl.n_ext == 280 && lb == 4) launch_line_pass<Pass, 280, 4>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ref_op && pl.n_ext == 280) launch_line_pass<Pass, 280, 8>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ref_op && pl.n_ext == 536 && lb == 16) launch_line_pass<Pass, 536, 16>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ref_op && pl.n_ext == 536 && lb == 4) launch_line_pass<Pass, 536, 4>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ref_op && pl.n_ext == 536) launch_line_pass<Pass, 536, 8>(nblk, smem, arg, E, pl, scr_cap, s);
-    else launch_line_pass<Pass, 0, 8>(nblk, smem, arg, E, pl, scr_cap, s);
+    if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, s);
+    else if (ct) launch_line_pass<Pass, 536, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, s);
+    else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, s);
 #else
-    if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, kLB);
-    const int nblk = E.S * ((nlines + kLB - 1) / kLB);
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (kLB + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2) +
-                        static_cast<size_t>(Pass::kStage) * pl.n * kLB * sizeof(double);
     (void)stream;
     const Pass P(E, arg);
-    std::vector<double2> sm(smem / sizeof(double2));
+    std::vector<double2> sm(smem / sizeof(double2) + 1);
     for (int b = 0; b < nblk; ++b) {
-        if (ref_op && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
-        else if (ref_op && pl.n_ext == 536) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+        if (ct && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+        else if (ct) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
         else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
     }
 #endif
@@ -1160,22 +1380,40 @@ void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* str
 
 void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
     launch_pass_a(E, P, stream);
-    launch_pass_b(E, P, stream);
+    launch_pass_b(E, P, stage, stream);
     launch_pass_c(E, P, stage, stream);
 }
 
+// flux form: Cartesian X, Y (no third pass); general GA, GB, C.
+// reference order: A', B', C' / A, B, C.
 void launch_pass_a(const EngineDev& E, const LinePlans& P, void* stream) {
-    if (E.cartesian) run_line_pass<PassAc>(0, E, P.row, P.scr_row, stream);
-    else run_line_pass<PassA>(0, E, P.row, P.scr_row, stream);
+    if (E.reference_order) {
+        if (E.cartesian) run_line_pass<PassAc>(0, E, P.row, P.scr_row, stream);
+        else run_line_pass<PassA>(0, E, P.row, P.scr_row, stream);
+    } else {
+        if (E.cartesian) run_line_pass<PassXc>(0, E, P.row, P.scr_row, stream);
+        else run_line_pass<PassGA>(0, E, P.row, P.scr_row, stream);
+    }
 }
-void launch_pass_b(const EngineDev& E, const LinePlans& P, void* stream) {
-    if (E.cartesian) run_line_pass<PassBc>(0, E, P.col, P.scr_col, stream);
-    else run_line_pass<PassB>(0, E, P.col, P.scr_col, stream);
+void launch_pass_b(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
+    if (E.reference_order) {
+        if (E.cartesian) run_line_pass<PassBc>(0, E, P.col, P.scr_col, stream);
+        else run_line_pass<PassB>(0, E, P.col, P.scr_col, stream);
+    } else {
+        if (E.cartesian) run_line_pass<PassYc>(stage, E, P.col, P.scr_col, stream);
+        else run_line_pass<PassGB>(0, E, P.col, P.scr_col, stream);
+    }
 }
 void launch_pass_c(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
-    if (E.cartesian) run_line_pass<PassCc>(stage, E, P.row, P.scr_row, stream);
-    else run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
+    if (E.reference_order) {
+        if (E.cartesian) run_line_pass<PassCc>(stage, E, P.row, P.scr_row, stream);
+        else run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
+    } else if (!E.cartesian) {
+        run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
+    }
 }
+
+int stage_launches(const EngineDev& E) { return (E.cartesian && !E.reference_order) ? 2 : 3; }
 
 void launch_bc(const EngineDev& E, void* stream) {
 #if FCSG_CUDA

@@ -35,6 +35,7 @@ struct BcDev {
 struct EngineDev {
     int S, ni, nj;  // subpatches of one uniform rectangular shape
     int cartesian;  // 1: iq2x == iq1y == 0 at every point (axis-aligned maps)
+    int reference_order;  // 1: euler_rhs's own accumulation order (3 passes); 0: flux form
     long npts;      // S * ni * nj
     double cfl, T;
     double visc_c[4];
@@ -95,10 +96,12 @@ void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* str
 void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream);
 // the three line passes of a stage, separately (profiling hooks)
 void launch_pass_a(const EngineDev& E, const LinePlans& P, void* stream);
-void launch_pass_b(const EngineDev& E, const LinePlans& P, void* stream);
+void launch_pass_b(const EngineDev& E, const LinePlans& P, int stage, void* stream);
 void launch_pass_c(const EngineDev& E, const LinePlans& P, int stage, void* stream);
+// line-pass launches per stage (2 for the Cartesian flux form, else 3)
+int stage_launches(const EngineDev& E);
 // kernel launches per superstep (excluding the t=0 dilation)
-constexpr int kLaunchesPerStep = 33;
+inline int launches_per_step(const EngineDev& E) { return 18 + 5 * stage_launches(E); }
 void launch_bc(const EngineDev& E, void* stream);
 void launch_exchange(const EngineDev& E, void* stream);
 void launch_finalize_dt(const EngineDev& E, void* stream);

@@ -28,7 +28,7 @@ class fcsg_engine_config(C.Structure):
     _fields_ = [("cfl", C.c_double), ("T", C.c_double), ("n_cont", C.c_int), ("filter_alpha", C.c_double),
                 ("filter_p", C.c_int), ("filter_p_smear", C.c_int), ("visc_c", C.c_double * 4),
                 ("abs_floor", C.c_double), ("smear_radius", C.c_int), ("debug_rhs", C.c_int),
-                ("force_general", C.c_int)]
+                ("force_general", C.c_int), ("reference_order", C.c_int)]
 
 
 @dataclass
@@ -48,6 +48,9 @@ class EngineConfig:
     weights: str = DEFAULT_WEIGHTS
     debug_rhs: bool = False
     force_general: bool = False  # never use the Cartesian (zero metric term) stage passes
+    # accumulate the rhs in euler_rhs's own order (40 line derivatives per stage)
+    # instead of the flux form div(mu grad w - f) (24; round-off-level difference)
+    reference_order: bool = False
 
 
 def _bc_arrays(d: G.SubData):
@@ -71,7 +74,7 @@ class Engine:
         L = ctx.lib
         c = fcsg_engine_config(cfg.cfl, cfg.T, cfg.n_cont, cfg.filter_alpha, cfg.filter_p, cfg.filter_p_smear,
                                (C.c_double * 4)(*cfg.visc_c), cfg.abs_floor, cfg.smear_radius, int(cfg.debug_rhs),
-                               int(cfg.force_general))
+                               int(cfg.force_general), int(cfg.reference_order))
         h = C.c_void_p()
         ctx.check(L.fcsg_engine_create(ctx.h, C.byref(c), C.byref(h)))
         self.h = h

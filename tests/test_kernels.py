@@ -132,6 +132,13 @@ def test_fc_known_answers(backend):
 # full superstep
 
 
+# stage-pass families: (force_general, reference_order). The default is the
+# flux form (Cartesian: 2 passes / 16 derivatives per stage); reference_order
+# keeps euler_rhs's own accumulation (3 passes / 24 or 40).
+PASSES = [(False, False), (True, False), (False, True), (True, True)]
+PASS_IDS = ["cartesian", "general", "cartesian-reforder", "general-reforder"]
+
+
 def _compare_engines(E, OE, nsub, atol_tau_margin=1e-9):
     for k in range(nsub):
         d = OE.subs[k]
@@ -141,16 +148,17 @@ def _compare_engines(E, OE, nsub, atol_tau_margin=1e-9):
         assert np.array_equal(tau[sure], d.tau[sure])
 
 
-@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
-def test_superstep_phases_riemann(backend, engine_golden, general):
+@pytest.mark.parametrize("general,refo", PASSES, ids=PASS_IDS)
+def test_superstep_phases_riemann(backend, engine_golden, general, refo):
     """Riemann quadrants on one 64x64 subpatch: every phase of two steps
     against the oracle, and step 1 against the reference's own snapshots.
-    Run with the Cartesian stage passes (zero metric terms dropped) and with
-    the general 20-transform passes."""
+    Run with every stage-pass family (Cartesian / general, flux form /
+    reference accumulation order)."""
     kind, ctx = backend
     g = engine_golden
     dec, ic, _ = P.riemann_quadrants(n=64, seed=2)
-    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5, debug_rhs=True, force_general=general))
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5, debug_rhs=True, force_general=general,
+                                                 reference_order=refo))
     assert E.is_cartesian() == (not general)
     OE = oracle_engine(dec, ic)
     assert rel_err(E.get_state(0), g["r64_e_init"]) < 1e-15
@@ -182,15 +190,15 @@ def test_superstep_phases_riemann(backend, engine_golden, general):
     assert st == 2 and t == pytest.approx(OE.t, rel=1e-14)
 
 
-@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
-def test_superstep_tiles_exchange(backend, engine_golden, general):
+@pytest.mark.parametrize("general,refo", PASSES, ids=PASS_IDS)
+def test_superstep_tiles_exchange(backend, engine_golden, general, refo):
     """2x2 overlapping 48x48 subpatches: fringe copies + viscosity blend; graph
     path equals the phase path bit for bit; state vs the reference run."""
     kind, ctx = backend
     g = engine_golden
     dec, ic, _ = P.vortex_tiles(r=2, s=2, n0=30)
     states = [g[f"v2_sub{k}_e_init"] for k in range(4)]
-    cfg = EN.EngineConfig(cfl=0.5, force_general=general)
+    cfg = EN.EngineConfig(cfl=0.5, force_general=general, reference_order=refo)
     E = EN.Engine(ctx, dec, cfg=cfg, initial_states=states)
     E2 = EN.Engine(ctx, dec, cfg=cfg, initial_states=states)
     E.step_by_phases()
@@ -203,12 +211,12 @@ def test_superstep_tiles_exchange(backend, engine_golden, general):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
-def test_superstep_config2_full_size(gpu_ctx, general):
+@pytest.mark.parametrize("general,refo", PASSES, ids=PASS_IDS)
+def test_superstep_config2_full_size(gpu_ctx, general, refo):
     """BASELINE config 2 at full size (one 512x512 subpatch, seeded quadrants,
     ANN classifier, CFL 0.5): 3 supersteps against the oracle."""
     dec, ic, _ = P.riemann_quadrants(n=512, seed=2)
-    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general))
+    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general, reference_order=refo))
     OE = oracle_engine(dec, ic)
     for _ in range(3):
         OE.step()
@@ -217,12 +225,12 @@ def test_superstep_config2_full_size(gpu_ctx, general):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
-def test_superstep_config5_subpatch_size(gpu_ctx, general):
+@pytest.mark.parametrize("general,refo", PASSES, ids=PASS_IDS)
+def test_superstep_config5_subpatch_size(gpu_ctx, general, refo):
     """config 5 geometry (256x256 subpatches, 19-point overlap) on a 2x2 tiling,
     vortex + 1e-3 noise, 2 supersteps against the oracle."""
     dec, ic, _ = P.vortex_tiles(r=2, s=2)
-    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general))
+    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general, reference_order=refo))
     OE = oracle_engine(dec, ic)
     OE.step()
     OE.step()
@@ -289,8 +297,7 @@ def test_bad_weights_rejected(backend, tmp_path):
 
 
 def test_superstep_256_subpatch_compile_time_plan(emu_ctx):
-    """The compile-time n_ext = 280 plan (warp-per-line transform on the GPU)
-    in the emulation harness: one 256x256 Riemann subpatch, 1 superstep."""
+    """The compile-time n_ext = 280 plan in the emulation harness: one 256x256 Riemann subpatch, 1 superstep."""
     dec, ic, _ = P.riemann_quadrants(n=256, seed=4)
     E = EN.Engine(emu_ctx, dec, ic, EN.EngineConfig(cfl=0.5))
     OE = oracle_engine(dec, ic)
@@ -299,7 +306,8 @@ def test_superstep_256_subpatch_compile_time_plan(emu_ctx):
     _compare_engines(E, OE, 1)
 
 
-def test_superstep_rotated_channel_general_metrics(backend, engine_golden):
+@pytest.mark.parametrize("refo", [False, True], ids=["flux", "reforder"])
+def test_superstep_rotated_channel_general_metrics(backend, engine_golden, refo):
     """General (curvilinear-metric) stage passes with every metric term nonzero
     and all four BC kinds (inflow, outflow pressure, slip wall, no-slip
     adiabatic wall): 3 supersteps against the reference's own run."""
@@ -307,7 +315,7 @@ def test_superstep_rotated_channel_general_metrics(backend, engine_golden):
     g = engine_golden
     dec, ic, _ = P.rotated_channel()
     states = [g[f"rc_sub{k}_e_init"] for k in range(len(dec.subs))]
-    E = EN.Engine(ctx, dec, cfg=EN.EngineConfig(cfl=0.5), initial_states=states)
+    E = EN.Engine(ctx, dec, cfg=EN.EngineConfig(cfl=0.5, reference_order=refo), initial_states=states)
     assert not E.is_cartesian()
     assert E.run(3) == 3
     for k in range(len(dec.subs)):
