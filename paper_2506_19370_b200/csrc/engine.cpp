@@ -150,7 +150,11 @@ void Engine::enqueue_part(int part, int stage) {
 void Engine::set_mlp_packed(const std::vector<double>& w) {
     if (static_cast<int>(w.size()) != kMlpWeights) throw Error(kConfig, "weight file has wrong input/output dimensions");
     mlp_ = w;
-    if (finalized_) dev::h2d(const_cast<double*>(E_.mlp), mlp_.data(), mlp_.size() * sizeof(double), ctx_.stream);
+    if (finalized_) {
+        dev::h2d(const_cast<double*>(E_.mlp), mlp_.data(), mlp_.size() * sizeof(double), ctx_.stream);
+        const std::vector<double> fr = mlp_mma_fragments(mlp_);
+        dev::h2d(const_cast<double*>(E_.mlp_frag), fr.data(), fr.size() * sizeof(double), ctx_.stream);
+    }
 }
 
 void Engine::load_mlp_file(const std::string& path) {
@@ -310,18 +314,8 @@ void Engine::finalize() {
     }
     E.mlp = static_cast<const double*>(up(mlp_.data(), mlp_.size() * sizeof(double)));
     {
-        // per layer W^T ([in][out]) then b, the classifier kernel's layout
-        const int rows[kMlpLayers] = {16, 16, 16, 16, 4}, cols[kMlpLayers] = {7, 16, 16, 16, 16};
-        std::vector<double> wt;
-        size_t off = 0;
-        for (int l = 0; l < kMlpLayers; ++l) {
-            for (int j = 0; j < cols[l]; ++j)
-                for (int i = 0; i < rows[l]; ++i) wt.push_back(mlp_[off + static_cast<size_t>(i) * cols[l] + j]);
-            off += static_cast<size_t>(rows[l]) * cols[l];
-            for (int i = 0; i < rows[l]; ++i) wt.push_back(mlp_[off + i]);
-            off += rows[l];
-        }
-        E.mlp_t = static_cast<const double*>(up(wt.data(), wt.size() * sizeof(double)));
+        const std::vector<double> fr = mlp_mma_fragments(mlp_);
+        E.mlp_frag = static_cast<const double*>(up(fr.data(), fr.size() * sizeof(double)));
     }
     {
         std::vector<double> tt(321);

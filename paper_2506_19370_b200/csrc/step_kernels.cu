@@ -20,6 +20,7 @@
 #include "step_kernels.h"
 
 #include <cmath>
+#include <string>
 #include <cstdlib>
 #include <vector>
 
@@ -1037,6 +1038,183 @@ FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, double* t
     }
 }
 
+// ---- classifier on the FP64 tensor cores ----------------------------------
+// MlpClassifier::forward (src/viscosity.cpp:108-133) as mma.m8n8k4.f64 tiles:
+// a warp classifies 8 stencils at a time -- the row and column windows of 4
+// points -- with stencils as the M rows, neurons as N and layer inputs as K.
+// Lane (g, t) = (lane / 4, lane % 4) holds A[g][t] (input t of the k-step, of
+// stencil g), B[t][g] (weight of neuron g of the n-tile for input t) and
+// D[g][2t], D[g][2t+1]. A layer's D fragments are the next layer's A fragments
+// when the next layer's inputs are taken in the order
+// P(ks, t) = 8 (ks / 2) + 2t + ks % 2 (the neuron this lane holds in its
+// register ks), so activations never leave the registers: the permutation is
+// folded into the B fragments here. Fragment f of lane l is fr[f * 32 + l].
+std::vector<double> mlp_mma_fragments(const std::vector<double>& w) {
+    const int rows[kMlpLayers] = {16, 16, 16, 16, 4}, cols[kMlpLayers] = {7, 16, 16, 16, 16};
+    int wo[kMlpLayers], bo[kMlpLayers];
+    int off = 0;
+    for (int l = 0; l < kMlpLayers; ++l) {
+        wo[l] = off;
+        off += rows[l] * cols[l];
+        bo[l] = off;
+        off += rows[l];
+    }
+    auto W = [&](int l, int n, int k) { return w[wo[l] + n * cols[l] + k]; };
+    auto P = [](int ks, int t) { return 8 * (ks >> 1) + 2 * t + (ks & 1); };
+    std::vector<double> fr(static_cast<size_t>(kMlpFrags) * 32, 0.0);
+    for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        double* f = fr.data() + lane;
+        for (int nt = 0; nt < 2; ++nt)
+            for (int ks = 0; ks < 2; ++ks) {
+                const int k = 4 * ks + t;
+                f[(nt * 2 + ks) * 32] = k < kMlpIn ? W(0, 8 * nt + g, k) : 0.0;
+            }
+        for (int l = 0; l < 3; ++l)
+            for (int nt = 0; nt < 2; ++nt)
+                for (int ks = 0; ks < 4; ++ks) f[(4 + l * 8 + nt * 4 + ks) * 32] = W(l + 1, 8 * nt + g, P(ks, t));
+        for (int ks = 0; ks < 4; ++ks) f[(28 + ks) * 32] = g < kMlpOut ? W(4, g, P(ks, t)) : 0.0;
+        for (int L = 0; L < 4; ++L)
+            for (int nt = 0; nt < 2; ++nt)
+                for (int i = 0; i < 2; ++i) f[(32 + L * 4 + nt * 2 + i) * 32] = w[bo[L] + 8 * nt + 2 * t + i];
+        for (int i = 0; i < 2; ++i) f[(48 + i) * 32] = (2 * t + i < kMlpOut) ? w[bo[4] + 2 * t + i] : 0.0;
+    }
+    return fr;
+}
+
+#if FCSG_CUDA
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// Class 1..4 of the stencil held by this lane's quad, returned on all four
+// lanes; every lane of the warp calls. s_a, s_b are window values t and 4 + t
+// (s_b unused for t = 3); inactive quads get 4. normalize_stencil's min, max,
+// guard and 2 (s - lo) / span - 1 are computed exactly as the reference's
+// (src/viscosity.cpp:48-59).
+__device__ int classify_mma(const double* fr, const double* tab, double s_a, double s_b, bool active, double abs_floor,
+                            int lane) {
+    constexpr unsigned kAll = 0xffffffffu;
+    const int t = lane & 3;
+    const bool has_b = t < 3;
+    double lo = s_a, hi = s_a;
+    if (has_b) {
+        lo = s_b < lo ? s_b : lo;
+        hi = s_b > hi ? s_b : hi;
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        const double l2 = __shfl_xor_sync(kAll, lo, o), h2 = __shfl_xor_sync(kAll, hi, o);
+        lo = l2 < lo ? l2 : lo;
+        hi = h2 > hi ? h2 : hi;
+    }
+    const double span = hi - lo;
+    double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+    scale = scale > 1e-100 ? scale : 1e-100;
+    const bool guard = !active || span <= 1e-13 * scale || span <= abs_floor;
+    const double sp = guard ? 1.0 : span;
+    const double a0 = guard ? 0.0 : 2.0 * (s_a - lo) / sp - 1.0;
+    const double a1 = (guard || !has_b) ? 0.0 : 2.0 * (s_b - lo) / sp - 1.0;
+    const double* F = fr + lane;
+    double h[4];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+        double d0 = F[(32 + nt * 2) * 32], d1 = F[(33 + nt * 2) * 32];
+        dmma(d0, d1, a0, F[(nt * 2) * 32]);
+        dmma(d0, d1, a1, F[(nt * 2 + 1) * 32]);
+        h[nt * 2] = tanh_tab(d0, tab);
+        h[nt * 2 + 1] = tanh_tab(d1, tab);
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        double g[4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            double d0 = F[(36 + l * 4 + nt * 2) * 32], d1 = F[(37 + l * 4 + nt * 2) * 32];
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) dmma(d0, d1, h[ks], F[(4 + l * 8 + nt * 4 + ks) * 32]);
+            g[nt * 2] = tanh_tab(d0, tab);
+            g[nt * 2 + 1] = tanh_tab(d1, tab);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k] = g[k];
+    }
+    double d0 = F[48 * 32], d1 = F[49 * 32];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) dmma(d0, d1, h[ks], F[(28 + ks) * 32]);
+    // lane t = 0 holds logits 0, 1 and lane t = 1 logits 2, 3
+    const double l2 = __shfl_xor_sync(kAll, d0, 1), l3 = __shfl_xor_sync(kAll, d1, 1);
+    int best = 0;  // lowest-index argmax (strict >), without a dynamically indexed array
+    double bv = d0;
+    if (d1 > bv) { best = 1; bv = d1; }
+    if (l2 > bv) { best = 2; bv = l2; }
+    if (l3 > bv) best = 3;
+    const int cls = guard ? 4 : best + 1;
+    return __shfl_sync(kAll, cls, lane & ~3);
+}
+
+// window value k of this lane's stencil (row or column window of point (i, j))
+__device__ __forceinline__ double window_at(const double* f, long base, int ni, bool col, int st, int i, int j, int k) {
+    return col ? f[base + static_cast<long>(st + k) * ni + i] : f[base + static_cast<long>(j) * ni + st + k];
+}
+
+// phase 0, part 2 on the tensor cores: one warp per group of 4 points;
+// quads 0-3 hold the row windows, quads 4-7 the column windows
+// (Classifier::classify, src/viscosity.cpp:211-251)
+constexpr int kMmaThreads = 256;
+__global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_constant__ EngineDev E, bool step0) {
+    __shared__ double tab[kTanhTable];
+    __shared__ double fr[kMlpFrags * 32];
+    for (int k = threadIdx.x; k < kTanhTable; k += blockDim.x) tab[k] = E.tanh_tab[k];
+    for (int k = threadIdx.x; k < kMlpFrags * 32; k += blockDim.x) fr[k] = E.mlp_frag[k];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int q = g & 3;
+    const bool col = g >= 4;
+    const long sz = static_cast<long>(E.ni) * E.nj;
+    const long ngroups = (E.npts + 3) / 4;
+    const long wstep = static_cast<long>(gridDim.x) * (kMmaThreads / 32);
+    for (long grp = static_cast<long>(blockIdx.x) * (kMmaThreads / 32) + (threadIdx.x >> 5); grp < ngroups;
+         grp += wstep) {
+        const long p = 4 * grp + q;
+        const bool valid = p < E.npts;
+        const long pp = valid ? p : 0;
+        const long base = (pp / sz) * sz, loc = pp - base;
+        const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
+        const int n = col ? E.nj : E.ni;
+        const bool active = valid && n >= kMlpIn;
+        int st = (col ? j : i) - kMlpIn / 2;
+        st = st < 0 ? 0 : (st > n - kMlpIn ? n - kMlpIn : st);
+        double sa = 0.0, sb = 0.0;
+        if (active) {
+            sa = window_at(E.proxy, base, E.ni, col, st, i, j, t);
+            if (t < 3) sb = window_at(E.proxy, base, E.ni, col, st, i, j, 4 + t);
+        }
+        const int c1 = classify_mma(fr, tab, sa, sb, active, E.abs_floor, lane);
+        const int c1o = __shfl_xor_sync(0xffffffffu, c1, 16);
+        const int tau = c1 < c1o ? c1 : c1o;
+        int tr = 4;
+        if (step0) {
+            double ra = 0.0, rb = 0.0;
+            if (active) {
+                ra = window_at(E.e[0], base, E.ni, col, st, i, j, t);
+                if (t < 3) rb = window_at(E.e[0], base, E.ni, col, st, i, j, 4 + t);
+            }
+            const int c2 = classify_mma(fr, tab, ra, rb, active, E.abs_floor, lane);
+            const int c2o = __shfl_xor_sync(0xffffffffu, c2, 16);
+            tr = c2 < c2o ? c2 : c2o;
+        }
+        if (valid && !col && t == 0) {
+            E.tau[p] = tau;
+            E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
+            if (step0) E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
+        }
+    }
+}
+#endif
+
 // t=0 smear mask: box dilation of radius smear_radius (src/runtime.cpp:393-402)
 FCSG_HD void dilate_body(Thr t, int block, int nblocks, const EngineDev& E) {
     const long sz = static_cast<long>(E.ni) * E.nj;
@@ -1343,11 +1521,19 @@ void launch_phase0(const EngineDev& E, bool step0, void* stream) {
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     proxy_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E);
-    cudaMemcpyToSymbolAsync(c_mlp, E.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
-    {
+    static const bool scalar = [] {
+        const char* v = std::getenv("FCSG_CLASSIFIER");
+        return v && std::string(v) == "scalar";
+    }();
+    if (scalar) {  // CUDA-core classifier (constant-bank weights), for comparison
+        cudaMemcpyToSymbolAsync(c_mlp, E.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
         long g = (E.npts + kClsThreads - 1) / kClsThreads;
         g = g > 148 * 24 ? 148 * 24 : g;
         classify_kernel<<<static_cast<int>(g), kClsThreads, 0, s>>>(E, step0);
+    } else {
+        long g = ((E.npts + 3) / 4 + kMmaThreads / 32 - 1) / (kMmaThreads / 32);
+        g = g > 148 * 8 ? 148 * 8 : g;
+        classify_mma_kernel<<<static_cast<int>(g < 1 ? 1 : g), kMmaThreads, 0, s>>>(E, step0);
     }
 #else
     (void)stream;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "fcsg_common.h"
 
@@ -78,10 +79,17 @@ struct EngineDev {
     long n_x;
     // classifier weights
     const double* mlp;       // kMlpWeights, FCNN order (per layer W row-major, then b)
-    const double* mlp_t;     // kMlpWeights, per layer W transposed ([in][out]), then b
+    const double* mlp_frag;  // kMlpFrags x 32: per-lane DMMA operand fragments (mlp_mma_fragments)
     const double* tanh_tab;  // tanh(k/16), k = 0..320 (classifier tanh table)
     StepScalars* sc;
 };
+
+// The classifier on the FP64 tensor cores (mma.m8n8k4.f64): per warp, 8
+// stencils x 8 neurons per MMA tile. Fragments: 0-3 layer-1 B (W1^T), 4-27
+// hidden-layer B, 28-31 output-layer B, 32-47 hidden biases (C), 48-49 output
+// bias; see classify_mma in step_kernels.cu for the lane layout.
+constexpr int kMlpFrags = 50;
+std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
 
 // FC plans for the two line orientations (rows: n = ni, cols: n = nj)
 struct LinePlans {
