@@ -215,6 +215,9 @@ void Engine::finalize() {
     E.ni = ni_;
     E.nj = nj_;
     E.npts = npts_;
+    if (npts_ >= (1L << 31)) throw Error(kConfig, "more than 2^31 points on one device");
+    E.div_ni = make_fastdiv(static_cast<unsigned>(ni_));
+    E.div_sz = make_fastdiv(static_cast<unsigned>(sz));
     E.cfl = cfg_.cfl;
     E.T = cfg_.T;
     for (int k = 0; k < 4; ++k) E.visc_c[k] = cfg_.visc_c[k];
@@ -318,8 +321,8 @@ void Engine::finalize() {
         E.mlp_frag = static_cast<const double*>(up(fr.data(), fr.size() * sizeof(double)));
     }
     {
-        std::vector<double> tt(321);
-        for (int k = 0; k <= 320; ++k) tt[k] = static_cast<double>(tanhl(static_cast<long double>(k) / 16.0L));
+        std::vector<double> tt(kTanhTable);
+        for (int k = 0; k < kTanhTable; ++k) tt[k] = static_cast<double>(tanhl(static_cast<long double>(k) / 64.0L));
         E.tanh_tab = static_cast<const double*>(up(tt.data(), tt.size() * sizeof(double)));
     }
     halo_e_.clear();

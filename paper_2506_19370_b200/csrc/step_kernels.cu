@@ -20,8 +20,9 @@
 #include "step_kernels.h"
 
 #include <cmath>
-#include <string>
 #include <cstdlib>
+#include <cstring>
+#include <string>
 #include <vector>
 
 namespace fcsg {
@@ -896,28 +897,43 @@ struct MlpW {
 };
 #endif
 
-// tanh for the classifier. tanh(a + b) = (tanh a + tanh b) / (1 + tanh a tanh b)
-// with a = k/16 from a 321-entry table (tanh of the grid, correctly rounded,
-// kept in shared memory) and |b| <= 1/32, where the odd Taylor polynomial
-// through b^9 is exact to < 1e-18. Absolute error ~3 ulp, against ~1e-15 of
-// libm differences between the reference and any other build; tau parity is
-// gated on the logit margin (> 1e-9) anyway. For |x| >= 20 tanh is 1.0 in
-// double precision.
-constexpr int kTanhTable = 321;  // k/16, k = 0..320
+// tanh for the classifier: tanh(a + b) = (tanh a + tanh b) / (1 + tanh a tanh b)
+// with a = k/64 from a table (tanh of the grid, correctly rounded, kept in
+// shared memory) and |b| <= 1/128, where the odd Taylor polynomial through
+// b^7 is exact to < 1e-20. Branch-free: |x| is clamped at 20 (tanh = 1.0 in
+// double precision there), k = round(64 |x|) comes from the low mantissa bits
+// of 64 |x| + 1.5 2^52, and on the GPU the quotient uses the hardware
+// reciprocal approximation refined by two Newton steps (the denominator is in
+// [1, 2)). Error <= 3 ulp, against ~1e-16 of libm differences between the
+// reference and any other build; tau parity is gated on the logit margin
+// (> 1e-9) anyway.
 FCSG_HD double tanh_tab(double x, const double* tab) {
-    const double ax = fabs(x);
-    double r;
-    if (ax >= 20.0) {
-        r = 1.0;
-    } else {
-        const int k = static_cast<int>(ax * 16.0 + 0.5);
-        const double bb = ax - k * 0.0625;  // exact (Sterbenz / k = 0)
-        const double p = bb * bb;
-        const double tb = bb + bb * p * (-1.0 / 3.0 + p * (2.0 / 15.0 + p * (-17.0 / 315.0 + p * (62.0 / 2835.0))));
-        const double ta = tab[k];
-        r = (ta + tb) / (1.0 + ta * tb);
-    }
-    return x < 0.0 ? -r : r;
+    constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
+    const double ax = fmin(fabs(x), 20.0);
+    const double kd = fma(ax, 64.0, kMagic);
+#if FCSG_CUDA
+    const int k = __double2loint(kd);
+#else
+    unsigned long long bits;
+    std::memcpy(&bits, &kd, 8);
+    const int k = static_cast<int>(bits & 0xffffffffu);
+#endif
+    const double b = fma(kd - kMagic, -0.015625, ax);  // exact
+    const double p = b * b;
+    const double tb = fma(b * p, fma(p, fma(p, -17.0 / 315.0, 2.0 / 15.0), -1.0 / 3.0), b);
+    const double ta = tab[k];
+    const double n = ta + tb, d = fma(ta, tb, 1.0);
+#if FCSG_CUDA
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    return copysign(n * y, x);
+#else
+    return std::copysign(n / d, x);
+#endif
 }
 
 // normalize_stencil (src/viscosity.cpp:48-59): false = class-4 guard
@@ -1180,9 +1196,11 @@ __global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_
          grp += wstep) {
         const long p = 4 * grp + q;
         const bool valid = p < E.npts;
-        const long pp = valid ? p : 0;
-        const long base = (pp / sz) * sz, loc = pp - base;
-        const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
+        const unsigned pp = valid ? static_cast<unsigned>(p) : 0u;
+        const unsigned sub = fdiv(E.div_sz, pp);
+        const unsigned loc = pp - sub * E.div_sz.d;
+        const int j = static_cast<int>(fdiv(E.div_ni, loc)), i = static_cast<int>(loc) - j * E.ni;
+        const long base = static_cast<long>(sub) * sz;
         const int n = col ? E.nj : E.ni;
         const bool active = valid && n >= kMlpIn;
         int st = (col ? j : i) - kMlpIn / 2;

@@ -25,6 +25,27 @@ struct StepScalars {
     DevError err;
 };
 
+// n / d for 0 <= n < 2^31 by one multiply and shift: m = ceil(2^(31+l) / d),
+// l = ceil(log2 d), so n m / 2^(31+l) exceeds n / d by less than 1/d and the
+// floor is exact (n m < 2^63)
+struct FastDiv {
+    unsigned d;
+    int s;
+    unsigned long long m;
+};
+inline FastDiv make_fastdiv(unsigned d) {
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    FastDiv f;
+    f.d = d;
+    f.s = 31 + l;
+    f.m = ((1ull << f.s) + d - 1) / d;
+    return f;
+}
+FCSG_HD unsigned fdiv(const FastDiv& f, unsigned n) {
+    return static_cast<unsigned>((static_cast<unsigned long long>(n) * f.m) >> f.s);
+}
+
 // BC table entry for one line end (BcSpec, include/fcs/bc.hpp:19-23)
 struct BcDev {
     int kind;  // -1 none, else BcKind order: 0 inflow .. 5 zero_normal_all
@@ -37,7 +58,8 @@ struct EngineDev {
     int S, ni, nj;  // subpatches of one uniform rectangular shape
     int cartesian;  // 1: iq2x == iq1y == 0 at every point (axis-aligned maps)
     int reference_order;  // 1: euler_rhs's own accumulation order (3 passes); 0: flux form
-    long npts;      // S * ni * nj
+    long npts;      // S * ni * nj (< 2^31)
+    FastDiv div_ni, div_sz;  // by ni and by ni * nj (point index -> subpatch, row)
     double cfl, T;
     double visc_c[4];
     double abs_floor;
@@ -80,7 +102,7 @@ struct EngineDev {
     // classifier weights
     const double* mlp;       // kMlpWeights, FCNN order (per layer W row-major, then b)
     const double* mlp_frag;  // kMlpFrags x 32: per-lane DMMA operand fragments (mlp_mma_fragments)
-    const double* tanh_tab;  // tanh(k/16), k = 0..320 (classifier tanh table)
+    const double* tanh_tab;  // tanh(k/64), k = 0..1280 (classifier tanh table)
     StepScalars* sc;
 };
 
@@ -89,6 +111,7 @@ struct EngineDev {
 // hidden-layer B, 28-31 output-layer B, 32-47 hidden biases (C), 48-49 output
 // bias; see classify_mma in step_kernels.cu for the lane layout.
 constexpr int kMlpFrags = 50;
+constexpr int kTanhTable = 1281;  // tanh(k/64), k = 0..1280
 std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
 
 // FC plans for the two line orientations (rows: n = ni, cols: n = nj)
