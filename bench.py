@@ -47,6 +47,28 @@ def peaks():
         return 6650.0, "fallback"
 
 
+# kernel behind each timed group (for the ncu capture lookup)
+GROUP_KERNEL = {"pass_a": "PassXc", "pass_b": "PassYc", "viscosity": "classify_mma_kernel"}
+
+
+def ncu_traffic(group):
+    """DRAM bytes (read + write) per launch of the group's kernel from the
+    newest committed `ncu --set full` capture of the bench workload
+    (profiles/rNN_top_kernels_raw.csv, scripts/prof_top.sh), or None."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_top_kernels_raw.csv")))
+    key = GROUP_KERNEL.get(group)
+    if not files or not key:
+        return None, None
+    with open(files[-1]) as fh:
+        for row in csv.DictReader(fh):
+            if key in row["Kernel Name"]:
+                mb = float(row["dram__bytes_read.sum [MB]"]) + float(row["dram__bytes_write.sum [MB]"])
+                return mb * 1e6, os.path.basename(files[-1])
+    return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -327,6 +349,7 @@ def run_fcsg(args):
     ALG_BYTES = ALG_BYTES_CART if E.is_cartesian() else ALG_BYTES_GEN
     alg = ALG_BYTES.get(dom, 64) * npts
     achieved = alg / (groups[dom] * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(dom) if world == 1 else (None, None)
     fc_gbs, fc_ms = fc_derivative_gbs(ctx)
     cfg2 = config2_rate(ctx) if world == 1 else None
 
@@ -337,9 +360,9 @@ def run_fcsg(args):
     if not args.no_cpu:
         try:
             threads = os.cpu_count() or 1
-            rate, sps, cnpts = cpu_rate(1, 0, threads)
+            rate, sps, cnpts = cpu_rate(2, 1, threads)  # the t=0 (smear) step untimed, then 2 steady steps
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"1 superstep of {SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} tiles of 256x256 ({cnpts} points) "
+                   "sample": f"2 steady supersteps (after the untimed t=0 step) of {SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} tiles of 256x256 ({cnpts} points) "
                              f"of the same workload, reference Engine with {threads} worker threads "
                              f"(oracle/_ref; FFTW replaced by the oracle/shims FFT)"}
         except Exception as ex:  # the reference build is test infrastructure
@@ -359,7 +382,8 @@ def run_fcsg(args):
                 "steps": e2e_steps, "path": "fcsg_engine_set_state_bulk + fcsg_engine_run + fcsg_engine_get_state_bulk"},
         "gpu_launches": E.launches_per_step() * args.steps,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                     "alg_bytes_per_launch": alg, "peak_kind": peak_kind,
                      "alg_bytes_per_point": ALG_BYTES.get(dom), "ms_per_launch": groups[dom]},
         "kernel_groups_ms": groups,
         "fc_derivative": {"config": "config1: 4096 lines x N=256, n_cont=25 (n_ext=280), d/dx, HBM->HBM",

@@ -157,26 +157,52 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
     const int total = N * LB;
     const int tid = t.tid;
     for (int r = 0; r <= Pass::kRounds; ++r) {
-#pragma unroll 4
-        for (int w = tid; w < total; w += NTHR) {
-            int i, l;
-            if (rows) {
-                i = w % N;
-                l = w / N;
-            } else {
-                l = w % LB;
-                i = w / LB;
-            }
-            if (l < c.nl_valid) {
-                const long p = pidx(c, l, i);
-                double2 carry = mk2(0.0, 0.0);
-                if (r > 0) {
-                    const double2 v = buf[i * pitch + l];
-                    carry = P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c);
+        // the points of this thread, in chunks of KC: first every global read
+        // the loads of the chunk need (registers), then the epilogue of round
+        // r-1 and the load of round r per point. Issuing the reads first lets
+        // them overlap each other and the epilogue stores, which the compiler
+        // may not move them across (it cannot rule out aliasing).
+        constexpr int PPT = NE > 0 ? (NE - 24) * LB / NTHR : 1;
+        constexpr int KC = (NE > 0 && PPT >= 2) ? 2 : 1;
+        static_assert(NE == 0 || ((NE - 24) * LB) % NTHR == 0, "compile-time plans need whole points per thread");
+        const int nch = NE > 0 ? PPT / KC : (total - tid + NTHR - 1) / NTHR;
+        for (int ch = 0; ch < nch; ++ch) {
+            double fv[KC][Pass::kFetch];
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int w = tid + (ch * KC + k) * NTHR;
+                int i, l;
+                if (rows) {
+                    i = w % N;
+                    l = w / N;
+                } else {
+                    l = w % LB;
+                    i = w / LB;
                 }
-                if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c, carry, stg + w, total);
-            } else if (r < Pass::kRounds) {
-                buf[i * pitch + l] = mk2(0.0, 0.0);
+                if (r < Pass::kRounds && l < c.nl_valid) P.fetch(r, pidx(c, l, i), fv[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int w = tid + (ch * KC + k) * NTHR;
+                int i, l;
+                if (rows) {
+                    i = w % N;
+                    l = w / N;
+                } else {
+                    l = w % LB;
+                    i = w / LB;
+                }
+                if (l < c.nl_valid) {
+                    const long p = pidx(c, l, i);
+                    double2 carry = mk2(0.0, 0.0);
+                    if (r > 0) {
+                        const double2 v = buf[i * pitch + l];
+                        carry = P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c);
+                    }
+                    if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c, carry, fv[k], stg + w, total);
+                } else if (r < Pass::kRounds) {
+                    buf[i * pitch + l] = mk2(0.0, 0.0);
+                }
             }
         }
         if (r == Pass::kRounds) break;
@@ -214,17 +240,30 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
 struct Prim {
     double rho, mx, my, E, theta, p;
 };
-FCSG_HD Prim prim_rhs(const EngineDev& E, long p) {
+// the conserved values at p on the read-only path: no pass reads e at a point
+// after writing it there
+FCSG_HD void fetch_e(const EngineDev& E, long p, double* v) {
+    v[0] = ldg1(E.e[0] + p);
+    v[1] = ldg1(E.e[1] + p);
+    v[2] = ldg1(E.e[2] + p);
+    v[3] = ldg1(E.e[3] + p);
+}
+FCSG_HD Prim prim_of(const double* v) {
     Prim q;
-    q.rho = ldg1(E.e[0] + p);  // e is read-only in the passes that call this (A, B)
-    q.mx = ldg1(E.e[1] + p);
-    q.my = ldg1(E.e[2] + p);
-    q.E = ldg1(E.e[3] + p);
+    q.rho = v[0];
+    q.mx = v[1];
+    q.my = v[2];
+    q.E = v[3];
     const double rs = (q.rho != 0.0) ? q.rho : 1e-300;
     const double pr = kGm1 * (q.E - 0.5 * (q.mx * q.mx + q.my * q.my) / rs);
     q.theta = pr / rs;
     q.p = q.rho * q.theta;
     return q;
+}
+FCSG_HD Prim prim_rhs(const EngineDev& E, long p) {
+    double v[4];
+    fetch_e(E, p, v);
+    return prim_of(v);
 }
 
 // flux pair (F_c, G_c) (src/euler.cpp:44-55, 64-75)
@@ -260,8 +299,10 @@ struct PassA {
     const EngineDev& E;
     FCSG_HD PassA(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, double*, int) const {
-        const Prim q = prim_rhs(E, p);
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int, long p, double* v) const { fetch_e(E, p, v); }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, const double* fv, double*, int) const {
+        const Prim q = prim_of(fv);
         if (r == 0) check_positive(E, q, p, c);
         if (r < 4) return flux_pair(q, r);
         if (r == 4) return mk2(q.rho, q.mx);
@@ -298,9 +339,18 @@ struct PassB {
     const EngineDev& E;
     FCSG_HD PassB(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const {
-        if (r >= 6) return mk2(E.tS4[r - 6][p], E.tS5[r - 6][p]);
-        const Prim q = prim_rhs(E, p);
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        if (r >= 6) {  // written by this thread in round 4 or 5
+            v[0] = E.tS4[r - 6][p];
+            v[1] = E.tS5[r - 6][p];
+        } else {
+            fetch_e(E, p, v);
+        }
+    }
+    FCSG_HD double2 load(int r, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        if (r >= 6) return mk2(fv[0], fv[1]);
+        const Prim q = prim_of(fv);
         if (r < 4) return flux_pair(q, r);
         if (r == 4) return mk2(q.rho, q.mx);
         return mk2(q.my, q.theta);
@@ -398,7 +448,14 @@ struct PassC {
     int stage;
     FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const { return mk2(ldg1(E.tS4[r] + p), ldg1(E.tS5[r] + p)); }
+    static constexpr int kFetch = 2;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        v[0] = ldg1(E.tS4[r] + p);
+        v[1] = ldg1(E.tS5[r] + p);
+    }
+    FCSG_HD double2 load(int, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        return mk2(fv[0], fv[1]);
+    }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         s[0] = E.tA[r] + p;
         s[1] = E.iq1x + p;
@@ -434,8 +491,10 @@ struct PassAc {
     const EngineDev& E;
     FCSG_HD PassAc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, double*, int) const {
-        const Prim q = prim_rhs(E, p);
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int, long p, double* v) const { fetch_e(E, p, v); }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, const double* fv, double*, int) const {
+        const Prim q = prim_of(fv);
         if (r == 0) check_positive(E, q, p, c);
         if (r < 2) {
             const double2 f0 = flux_pair(q, 2 * r), f1 = flux_pair(q, 2 * r + 1);
@@ -476,9 +535,18 @@ struct PassBc {
     const EngineDev& E;
     FCSG_HD PassBc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const {
-        if (r >= 4) return mk2(E.tS5[2 * (r - 4)][p], E.tS5[2 * (r - 4) + 1][p]);
-        const Prim q = prim_rhs(E, p);
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        if (r >= 4) {  // written by this thread in round 2 or 3
+            v[0] = E.tS5[2 * (r - 4)][p];
+            v[1] = E.tS5[2 * (r - 4) + 1][p];
+        } else {
+            fetch_e(E, p, v);
+        }
+    }
+    FCSG_HD double2 load(int r, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        if (r >= 4) return mk2(fv[0], fv[1]);
+        const Prim q = prim_of(fv);
         if (r < 2) {
             const double2 f0 = flux_pair(q, 2 * r), f1 = flux_pair(q, 2 * r + 1);
             return mk2(f0.y, f1.y);
@@ -539,8 +607,13 @@ struct PassCc {
     int stage;
     FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const {
-        return mk2(ldg1(E.tS4[2 * r] + p), ldg1(E.tS4[2 * r + 1] + p));
+    static constexpr int kFetch = 2;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        v[0] = ldg1(E.tS4[2 * r] + p);
+        v[1] = ldg1(E.tS4[2 * r + 1] + p);
+    }
+    FCSG_HD double2 load(int, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        return mk2(fv[0], fv[1]);
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         s[0] = E.tA[2 * r] + p;
@@ -586,8 +659,10 @@ struct PassXc {
     const EngineDev& E;
     FCSG_HD PassXc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2 carry, double*, int) const {
-        const Prim q = prim_rhs(E, p);
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int, long p, double* v) const { fetch_e(E, p, v); }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2 carry, const double* fv, double*, int) const {
+        const Prim q = prim_of(fv);
         if (r & 1) {
             const int c0 = r - 1;  // 0 or 2
             const double2 f0 = flux_pair(q, c0), f1 = flux_pair(q, c0 + 1);
@@ -636,20 +711,29 @@ struct PassYc {
     int stage;
     FCSG_HD PassYc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2 carry, double* st, int ss) const {
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        if (r < 2) {  // e is still unmodified in rounds 0 and 1
+            fetch_e(E, p, v);
+        } else {      // rho, rho u: updated only in the last round
+            v[0] = ldg1(E.e[0] + p);
+            v[1] = ldg1(E.e[1] + p);
+        }
+    }
+    FCSG_HD double2 load(int r, long, const LineCtx&, double2 carry, const double* fv, double* st, int ss) const {
         switch (r) {
             case 0: {
-                const Prim q = prim_rhs(E, p);
+                const Prim q = prim_of(fv);
                 st[3 * ss] = q.my;
                 return mk2(q.my, q.theta);
             }
             case 1: {
-                const Prim q = prim_rhs(E, p);  // e is still unmodified at this point
+                const Prim q = prim_of(fv);
                 return mk2(carry.x - flux_pair(q, 2).y, carry.y - flux_pair(q, 3).y);
             }
-            case 2: return mk2(ldg1(E.e[0] + p), ldg1(E.e[1] + p));
+            case 2: return mk2(fv[0], fv[1]);
             default: {
-                const double rho = ldg1(E.e[0] + p), mx = ldg1(E.e[1] + p), my = st[3 * ss];
+                const double rho = fv[0], mx = fv[1], my = st[3 * ss];
                 const double v = my / rho;
                 return mk2(carry.x - my, carry.y - mx * v);  // G_0, G_1 (src/euler.cpp:64-75)
             }
@@ -692,8 +776,10 @@ struct PassGA {
     const EngineDev& E;
     FCSG_HD PassGA(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, double*, int) const {
-        const Prim q = prim_rhs(E, p);
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int, long p, double* v) const { fetch_e(E, p, v); }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2, const double* fv, double*, int) const {
+        const Prim q = prim_of(fv);
         if (r == 0) {
             check_positive(E, q, p, c);
             return mk2(q.rho, q.mx);
@@ -725,11 +811,21 @@ struct PassGB {
     const EngineDev& E;
     FCSG_HD PassGB(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2 carry, double*, int) const {
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        const int k = r % 3, c0 = 2 * (r / 3);
+        if (k == 0) {
+            fetch_e(E, p, v);
+        } else if (k == 2) {  // written by this thread in round r - 2
+            v[0] = E.tS4[c0][p];
+            v[1] = E.tS4[c0 + 1][p];
+        }
+    }
+    FCSG_HD double2 load(int r, long, const LineCtx&, double2 carry, const double* fv, double*, int) const {
         const int k = r % 3, c0 = 2 * (r / 3);
         if (k == 1) return carry;
-        if (k == 2) return mk2(E.tS4[c0][p], E.tS4[c0 + 1][p]);  // written by this thread in round r - 2
-        const Prim q = prim_rhs(E, p);
+        if (k == 2) return mk2(fv[0], fv[1]);
+        const Prim q = prim_of(fv);
         return c0 == 0 ? mk2(q.rho, q.mx) : mk2(q.my, q.theta);
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
@@ -796,7 +892,20 @@ struct PassFR {
         const double th = kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho;
         return mk2(my, th);
     }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const { return orig(E, r, p); }
+    static constexpr int kFetch = 4;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        v[0] = ldg1(E.e[0] + p);
+        v[1] = ldg1(E.e[1] + p);
+        if (r == 1) {
+            v[2] = ldg1(E.e[2] + p);
+            v[3] = ldg1(E.e[3] + p);
+        }
+    }
+    FCSG_HD double2 load(int r, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        if (r == 0) return mk2(fv[0], fv[1]);
+        const double rho = fv[0], mx = fv[1], my = fv[2], En = fv[3];
+        return mk2(my, kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho);
+    }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
     FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
         if (smear) {
@@ -823,7 +932,14 @@ struct PassFC {
     bool smear;
     FCSG_HD PassFC(const EngineDev& e, int sm) : E(e), smear(sm != 0) {}
     FCSG_HD int mode(int) const { return smear ? 4 : 3; }
-    FCSG_HD double2 load(int r, long p, const LineCtx&, double2, double*, int) const { return mk2(E.tF[2 * r][p], E.tF[2 * r + 1][p]); }
+    static constexpr int kFetch = 2;
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        v[0] = E.tF[2 * r][p];
+        v[1] = E.tF[2 * r + 1][p];
+    }
+    FCSG_HD double2 load(int, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        return mk2(fv[0], fv[1]);
+    }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
     FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
         if (smear) {

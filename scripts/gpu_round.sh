@@ -1,12 +1,11 @@
-# One measurement round on the GPU box: tests, bench (with the CPU baseline),
-# the kernel launch list of one superstep and full captures of the top kernels.
+# One measurement round on the GPU box: tests, smoke, bench (with the CPU
+# baseline), the reference arm, the kernel launch list of one superstep and
+# full captures of the top kernels.
 mkdir -p gpurun_out
-python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -1 gpurun_out/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | cut -c1-300
 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-300
 python scripts/profile_step.py 8 1 > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py 8 1 > gpurun_out/ncu1.log 2>&1
-python scripts/profile_step.py 4 1 > gpurun_out/plain4.log 2>&1 && \
-ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:"classify_kernel|PassBc|PassAc|PassCc" -s 3 -c 4 -o gpurun_out/prof_top python scripts/profile_step.py 4 1 > gpurun_out/ncu2.log 2>&1
-tail -1 gpurun_out/ncu2.log
+bash scripts/prof_top.sh
