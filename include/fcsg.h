@@ -129,15 +129,20 @@ enum {
 int fcsg_engine_create(fcsg_ctx* ctx, const fcsg_engine_config* cfg, fcsg_engine** out);
 int fcsg_engine_destroy(fcsg_engine* eng);
 
-/* One SubpatchData: lattice origin (i0, j0) of patch `patch` (for error
- * reports), shape, parameter spacings h1/h2 (LineInfo::inv_len =
- * 1/((n-1) h)), per-point mask (1 interior, 2 fringe), metrics iq1x, iq2x,
+/* One SubpatchData (include/fcs/subpatch_data.hpp:15-63, built by
+ * init_subpatch_data, src/subpatch_data.cpp:69-153): lattice origin (i0, j0)
+ * of patch `patch` (for error reports), shape ni x nj (subpatches of any
+ * shapes may be mixed), L-cut (geom::Subpatch::i_cut/j_cut - i0/j0: local
+ * points with i < cut_i && j < cut_j are not in the set; 0, 0 = rectangle;
+ * rows j < cut_j then begin at cut_i, columns i < cut_i at cut_j), parameter
+ * spacings h1/h2 (LineInfo::inv_len = 1/((n-1) h)), per-point mask (0 outside
+ * the set, 1 interior, 2 fringe), metrics iq1x, iq2x,
  * iq1y, iq2y, h_min, h_max, w_norm ([nj][ni] row-major), and the resolved
  * line-end BCs: bc_kind / bc_state[4] / bc_pressure for rows' low ends (nj),
  * rows' high ends (nj), columns' low ends (ni), columns' high ends (ni), in
  * that order. */
-int fcsg_engine_add_subpatch(fcsg_engine* eng, int patch, int i0, int j0, int ni, int nj, double h1, double h2,
-                             const uint8_t* mask, const double* iq1x, const double* iq2x, const double* iq1y,
+int fcsg_engine_add_subpatch(fcsg_engine* eng, int patch, int i0, int j0, int ni, int nj, int cut_i, int cut_j,
+                             double h1, double h2, const uint8_t* mask, const double* iq1x, const double* iq2x, const double* iq1y,
                              const double* iq2y, const double* h_min, const double* h_max, const double* w_norm,
                              const int* bc_kind, const double* bc_state, const double* bc_pressure, int* sub_id);
 /* CommPlan copies (include/fcs/runtime.hpp:17-22): solution copies
@@ -147,6 +152,15 @@ int fcsg_engine_add_subpatch(fcsg_engine* eng, int patch, int i0, int j0, int ni
 int fcsg_engine_set_plan(fcsg_engine* eng, long n_sol, const int* sol_dst_sub, const int* sol_dst,
                          const int* sol_src_sub, const int* sol_src, long n_visc, const int* v_dst_sub,
                          const int* v_dst, const int* v_src_sub, const int* v_src, const double* v_w);
+/* CommPlan interpolations (InterpEntry, include/fcs/runtime.hpp:25-31): which
+ * 0 = solution exchange (phase 6, src/runtime.cpp:440-452), 1 = viscosity
+ * blend (phase 1, src/runtime.cpp:359-368, weights w). Entry k: recipient
+ * (dst_sub[k], dst[k]) <- sum_b wy[6k+b] sum_a wx[6k+a] f(donor src_sub[k] at
+ * (si0[k]+a, sj0[k]+b)); donors must be local subpatches. Call after the
+ * copies (fcsg_engine_set_plan). */
+int fcsg_engine_set_plan_interps(fcsg_engine* eng, int which, long n, const int* dst_sub, const int* dst,
+                                 const int* src_sub, const int* si0, const int* sj0, const double* wx, const double* wy,
+                                 const double* w);
 /* MlpClassifier::load (src/viscosity.cpp:63-89): FCNN v1 file, 7-16-16-16-16-4 tanh */
 int fcsg_engine_load_mlp(fcsg_engine* eng, const char* path);
 int fcsg_engine_finalize(fcsg_engine* eng);

@@ -84,8 +84,10 @@ def _declare(L):
                                      C.c_long, C.c_double]
     L.fcsg_engine_create.argtypes = [vp, vp, C.POINTER(vp)]
     L.fcsg_engine_destroy.argtypes = [vp]
-    L.fcsg_engine_add_subpatch.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
-                                           C.POINTER(C.c_uint8), dp, dp, dp, dp, dp, dp, dp, ip, dp, dp, ip]
+    L.fcsg_engine_add_subpatch.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           C.c_double, C.c_double, C.POINTER(C.c_uint8), dp, dp, dp, dp, dp, dp, dp,
+                                           ip, dp, dp, ip]
+    L.fcsg_engine_set_plan_interps.argtypes = [vp, C.c_int, C.c_long, ip, ip, ip, ip, ip, dp, dp, dp]
     L.fcsg_engine_set_plan.argtypes = [vp, C.c_long, ip, ip, ip, ip, C.c_long, ip, ip, ip, ip, dp]
     L.fcsg_engine_load_mlp.argtypes = [vp, C.c_char_p]
     L.fcsg_engine_finalize.argtypes = [vp]

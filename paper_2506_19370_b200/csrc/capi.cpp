@@ -274,8 +274,8 @@ int fcsg_engine_destroy(fcsg_engine* eng) {
     return FCSG_OK;
 }
 
-int fcsg_engine_add_subpatch(fcsg_engine* e, int patch, int i0, int j0, int ni, int nj, double h1, double h2,
-                             const uint8_t* mask, const double* iq1x, const double* iq2x, const double* iq1y,
+int fcsg_engine_add_subpatch(fcsg_engine* e, int patch, int i0, int j0, int ni, int nj, int cut_i, int cut_j,
+                             double h1, double h2, const uint8_t* mask, const double* iq1x, const double* iq2x, const double* iq1y,
                              const double* iq2y, const double* h_min, const double* h_max, const double* w_norm,
                              const int* bc_kind, const double* bc_state, const double* bc_pressure, int* sub_id) {
     if (!e) return FCSG_USAGE;
@@ -287,6 +287,8 @@ int fcsg_engine_add_subpatch(fcsg_engine* e, int patch, int i0, int j0, int ni, 
         s.j0 = j0;
         s.ni = ni;
         s.nj = nj;
+        s.cut_i = cut_i;
+        s.cut_j = cut_j;
         s.h1 = h1;
         s.h2 = h2;
         const size_t n = static_cast<size_t>(ni) * nj;
@@ -314,6 +316,19 @@ int fcsg_engine_add_subpatch(fcsg_engine* e, int patch, int i0, int j0, int ni, 
         for (int i = 0; i < ni; ++i) s.col_hi.push_back(bc(k++));
         const int id = e->eng->add_subpatch(std::move(s));
         if (sub_id) *sub_id = id;
+    });
+}
+
+int fcsg_engine_set_plan_interps(fcsg_engine* e, int which, long n, const int* dst_sub, const int* dst,
+                                 const int* src_sub, const int* si0, const int* sj0, const double* wx, const double* wy,
+                                 const double* w) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        if (n < 0) throw Error(kUsage, "bad interpolation count");
+        auto vi = [&](const int* p) { return std::vector<int>(p, p + n); };
+        std::vector<double> vw = (which == 1 && n > 0) ? std::vector<double>(w, w + n) : std::vector<double>();
+        e->eng->set_plan_interps(which, vi(dst_sub), vi(dst), vi(src_sub), vi(si0), vi(sj0),
+                                 std::vector<double>(wx, wx + 6 * n), std::vector<double>(wy, wy + 6 * n), vw);
     });
 }
 

@@ -7,6 +7,7 @@
 #include "engine.h"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -26,11 +27,12 @@ Engine::~Engine() {
 }
 
 int Engine::add_subpatch(SubSpec s) {
-    if (finalized_) throw Error(kUsage, "engine already finalized");
+    if (finalized_ || laid_out_) throw Error(kUsage, "add every subpatch before the plan, halo and finalize");
     const size_t n = static_cast<size_t>(s.ni) * s.nj;
-    if (s.ni < 10 || s.nj < 10) throw Error(kConfig, "FcOperator: n_points must be >= 10");
-    if (!subs_.empty() && (s.ni != subs_[0].ni || s.nj != subs_[0].nj))
-        throw Error(kUsage, "all subpatches of one engine must share one shape");
+    if (s.cut_i < 0 || s.cut_j < 0 || s.cut_i >= s.ni || s.cut_j >= s.nj || ((s.cut_i == 0) != (s.cut_j == 0)))
+        throw Error(kUsage, "bad L-cut");
+    // FcOperator needs n >= 10 on every line (src/fc_core.cpp:192-193)
+    if (s.ni - s.cut_i < 10 || s.nj - s.cut_j < 10) throw Error(kConfig, "FcOperator: n_points must be >= 10");
     auto chk = [&](const std::vector<double>& v, const char* nm) {
         if (v.size() != n) throw Error(kUsage, std::string("subpatch field size mismatch: ") + nm);
     };
@@ -42,23 +44,65 @@ int Engine::add_subpatch(SubSpec s) {
     chk(s.h_min, "h_min");
     chk(s.h_max, "h_max");
     chk(s.w_norm, "w_norm");
-    for (auto m : s.mask)
-        if (m == 0) throw Error(kUsage, "L-shaped subpatches are not supported by this engine");
+    for (int j = 0; j < s.nj; ++j)
+        for (int i = 0; i < s.ni; ++i) {
+            const bool in_set = !(i < s.cut_i && j < s.cut_j);
+            if ((s.mask[static_cast<size_t>(j) * s.ni + i] != 0) != in_set)
+                throw Error(kUsage, "mask must be 0 exactly outside the subpatch's point set");
+        }
     subs_.push_back(std::move(s));
     return static_cast<int>(subs_.size()) - 1;
+}
+
+// Storage order: shape groups in order of first appearance, ids ascending
+// within a group (a group view is then one contiguous slab).
+void Engine::layout() {
+    if (laid_out_) return;
+    if (subs_.empty()) throw Error(kUsage, "engine has no subpatches");
+    groups_.clear();
+    std::vector<std::vector<int>> members;
+    for (int id = 0; id < static_cast<int>(subs_.size()); ++id) {
+        const auto& sp = subs_[id];
+        size_t g = 0;
+        while (g < groups_.size() && !(groups_[g].ni == sp.ni && groups_[g].nj == sp.nj)) ++g;
+        if (g == groups_.size()) {
+            groups_.push_back(Group{sp.ni, sp.nj, 0, 0, 0});
+            members.emplace_back();
+        }
+        members[g].push_back(id);
+    }
+    slot_of_.assign(subs_.size(), -1);
+    id_of_slot_.clear();
+    off_of_slot_.clear();
+    long off = 0;
+    for (size_t g = 0; g < groups_.size(); ++g) {
+        groups_[g].slot0 = static_cast<int>(id_of_slot_.size());
+        groups_[g].n = static_cast<int>(members[g].size());
+        groups_[g].p0 = off;
+        for (int id : members[g]) {
+            slot_of_[id] = static_cast<int>(id_of_slot_.size());
+            id_of_slot_.push_back(id);
+            off_of_slot_.push_back(off);
+            off += sub_points(id);
+        }
+    }
+    npts_ = off;
+    if (npts_ >= (1L << 31)) throw Error(kConfig, "more than 2^31 points on one device");
+    laid_out_ = true;
+}
+
+long Engine::gidx(int sub, int loc) const {
+    if (sub < 0 || sub >= static_cast<int>(subs_.size()) || loc < 0 || loc >= sub_points(sub))
+        throw Error(kUsage, "plan entry out of range");
+    return off_of_slot_[slot_of_[sub]] + loc;
 }
 
 void Engine::set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, std::vector<int> sol_src_sub,
                       std::vector<int> sol_src, std::vector<int> v_dst_sub, std::vector<int> v_dst,
                       std::vector<int> v_src_sub, std::vector<int> v_src, std::vector<double> v_w) {
-    if (subs_.empty()) throw Error(kUsage, "add subpatches before the plan");
-    const long sz = static_cast<long>(subs_[0].ni) * subs_[0].nj;
-    const int S = static_cast<int>(subs_.size());
-    const long np = sz * S;
-    auto gidx = [&](int sub, int loc) -> long {
-        if (sub < 0 || sub >= S || loc < 0 || loc >= sz) throw Error(kUsage, "plan entry out of range");
-        return sub * sz + loc;
-    };
+    if (finalized_) throw Error(kUsage, "engine already finalized");
+    layout();
+    const long np = npts_;
     // donors on other ranks (src_sub == -1) live in the halo slots after the local points
     auto sidx = [&](int sub, int loc, long n_halo) -> long {
         if (sub == -1) {
@@ -91,9 +135,64 @@ void Engine::set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, st
     have_plan_ = true;
 }
 
+void Engine::set_plan_interps(int which, std::vector<int> dst_sub, std::vector<int> dst, std::vector<int> src_sub,
+                              std::vector<int> si0, std::vector<int> sj0, std::vector<double> wx,
+                              std::vector<double> wy, std::vector<double> w) {
+    if (finalized_) throw Error(kUsage, "engine already finalized");
+    if (which != 0 && which != 1) throw Error(kUsage, "bad interpolation set");
+    layout();
+    const size_t n = dst.size();
+    if (dst_sub.size() != n || src_sub.size() != n || si0.size() != n || sj0.size() != n || wx.size() != 6 * n ||
+        wy.size() != 6 * n || (which == 1 && w.size() != n))
+        throw Error(kUsage, "interpolation arrays of inconsistent length");
+    std::vector<long> d(n), s0(n);
+    std::vector<int> pitch(n);
+    for (size_t k = 0; k < n; ++k) {
+        d[k] = gidx(dst_sub[k], dst[k]);
+        const int ss = src_sub[k];
+        if (ss < 0 || ss >= static_cast<int>(subs_.size()))
+            throw Error(kUsage, "interpolation donors must be local subpatches");
+        const auto& sp = subs_[ss];
+        if (si0[k] < 0 || sj0[k] < 0 || si0[k] + 6 > sp.ni || sj0[k] + 6 > sp.nj)
+            throw Error(kUsage, "interpolation stencil outside the donor subpatch");
+        s0[k] = gidx(ss, sj0[k] * sp.ni + si0[k]);
+        pitch[k] = sp.ni;
+    }
+    if (which == 0) {
+        xi_dst_ = d;
+        xi_src_ = s0;
+        xi_pitch_ = pitch;
+        xi_w_.assign(12 * n, 0.0);
+        for (size_t k = 0; k < n; ++k)
+            for (int a = 0; a < 6; ++a) {
+                xi_w_[12 * k + a] = wx[6 * k + a];
+                xi_w_[12 * k + 6 + a] = wy[6 * k + a];
+            }
+    } else {
+        std::vector<size_t> order(n);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return d[a] < d[b]; });
+        vi_off_.assign(npts_ + 1, 0);
+        vi_src_.clear();
+        vi_pitch_.clear();
+        vi_w_.clear();
+        for (size_t k : order) {
+            vi_off_[d[k] + 1]++;
+            vi_src_.push_back(s0[k]);
+            vi_pitch_.push_back(pitch[k]);
+            for (int a = 0; a < 6; ++a) vi_w_.push_back(wx[6 * k + a]);
+            for (int a = 0; a < 6; ++a) vi_w_.push_back(wy[6 * k + a]);
+            vi_w_.push_back(w[k]);
+        }
+        for (long p = 0; p < npts_; ++p) vi_off_[p + 1] += vi_off_[p];
+    }
+    have_plan_ = true;
+}
+
 void Engine::set_halo(std::vector<int> e_sub, std::vector<int> e_loc, long n_recv_e, std::vector<int> mu_sub,
                       std::vector<int> mu_loc, long n_recv_mu) {
     if (finalized_) throw Error(kUsage, "engine already finalized");
+    layout();
     if (have_plan_) throw Error(kUsage, "set the halo before the plan");
     if (e_sub.size() != e_loc.size() || mu_sub.size() != mu_loc.size() || n_recv_e < 0 || n_recv_mu < 0)
         throw Error(kUsage, "bad halo lists");
@@ -124,18 +223,18 @@ void Engine::enqueue_part(int part, int stage) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
     void* s = ctx_.stream;
     switch (part) {
-        case -1: launch_bc(E_, s); break;
-        case 0: launch_phase0(E_, host_step_ == 0, s); break;
+        case -1: launch_bc(G_, s); break;
+        case 0: launch_phase0(E_, G_, host_step_ == 0, s); break;
         case 1: launch_phase1(E_, s); break;
         case 2:
-            launch_phase2(E_, plans_, host_step_ == 0, s);
-            launch_bc(E_, s);
+            launch_phase2(G_, host_step_ == 0, s);
+            launch_bc(G_, s);
             launch_finalize_dt(E_, s);
             break;
         case 3:
             if (stage < 0 || stage > 4) throw Error(kUsage, "bad stage");
-            launch_stage(E_, plans_, stage, s);
-            launch_bc(E_, s);
+            launch_stage(G_, stage, s);
+            launch_bc(G_, s);
             break;
         case 4: launch_exchange(E_, s); break;
         case 5:
@@ -192,55 +291,44 @@ void Engine::finalize() {
     if (finalized_) throw Error(kUsage, "engine already finalized");
     if (subs_.empty()) throw Error(kUsage, "engine has no subpatches");
     if (mlp_.empty()) throw Error(kConfig, "ann classifier requires a weight file path");
+    layout();
     const int S = static_cast<int>(subs_.size());
-    ni_ = subs_[0].ni;
-    nj_ = subs_[0].nj;
-    const long sz = static_cast<long>(ni_) * nj_;
-    npts_ = sz * S;
-    op_row_ = ctx_.get_op(ni_, cfg_.n_cont, 2, cfg_.filter);
-    op_col_ = ctx_.get_op(nj_, cfg_.n_cont, 2, cfg_.filter);
-    plans_.row = ctx_.op(op_row_).plan;
-    plans_.col = ctx_.op(op_col_).plan;
-    plans_.scr_row = step_scr_cap(plans_.row);
-    plans_.scr_col = step_scr_cap(plans_.col);
 
     auto up = [&](const void* h, size_t bytes) {
-        void* d = dev::alloc(bytes);
+        void* d = dev::alloc(bytes > 0 ? bytes : 8);
         allocs_.push_back(d);
-        dev::h2d(d, h, bytes, ctx_.stream);
+        if (bytes) dev::h2d(d, h, bytes, ctx_.stream);
         return d;
     };
     EngineDev& E = E_;
     E.S = S;
-    E.ni = ni_;
-    E.nj = nj_;
+    E.ni = 0;
+    E.nj = 0;
+    E.sub_base = 0;
     E.npts = npts_;
-    if (npts_ >= (1L << 31)) throw Error(kConfig, "more than 2^31 points on one device");
-    E.div_ni = make_fastdiv(static_cast<unsigned>(ni_));
-    E.div_sz = make_fastdiv(static_cast<unsigned>(sz));
     E.cfl = cfg_.cfl;
     E.T = cfg_.T;
     for (int k = 0; k < 4; ++k) E.visc_c[k] = cfg_.visc_c[k];
     E.abs_floor = cfg_.abs_floor;
     E.smear_radius = cfg_.smear_radius;
-    E.cartesian = cfg_.allow_cartesian ? 1 : 0;
     E.reference_order = cfg_.reference_order ? 1 : 0;
-    for (const auto& sp : subs_)
-        for (size_t k = 0; k < sp.iq2x.size(); ++k)
-            if (sp.iq2x[k] != 0.0 || sp.iq1y[k] != 0.0) E.cartesian = 0;
-    std::vector<double> il1(S), il2(S);
-    std::vector<int> i0(S), j0(S), pt(S);
+    E.cartesian = 0;
+
+    // per-slot tables in storage order; BC tables per line (rows then columns
+    // of each slot)
+    std::vector<double> h1(S), h2(S);
+    std::vector<int> ci(S), cj(S);
     std::vector<BcDev> rlo, rhi, clo, chi;
-    std::vector<uint8_t> mask;
+    std::vector<long> row_off(S), col_off(S);
+    std::vector<uint8_t> mask(npts_);
     std::vector<double> geo[7];
-    for (int s = 0; s < S; ++s) {
-        const auto& sp = subs_[s];
-        // SubpatchData::LineInfo::inv_len (src/subpatch_data.cpp:134,147)
-        il1[s] = 1.0 / ((sp.ni - 1) * sp.h1);
-        il2[s] = 1.0 / ((sp.nj - 1) * sp.h2);
-        i0[s] = sp.i0;
-        j0[s] = sp.j0;
-        pt[s] = sp.patch;
+    for (int k = 0; k < 7; ++k) geo[k].resize(npts_);
+    for (int slot = 0; slot < S; ++slot) {
+        const auto& sp = subs_[id_of_slot_[slot]];
+        h1[slot] = sp.h1;
+        h2[slot] = sp.h2;
+        ci[slot] = sp.cut_i;
+        cj[slot] = sp.cut_j;
         auto pad = [](const std::vector<BcDev>& v, size_t n) {
             std::vector<BcDev> o = v;
             BcDev none{};
@@ -248,20 +336,22 @@ void Engine::finalize() {
             o.resize(n, none);
             return o;
         };
-        auto a = pad(sp.row_lo, nj_), b = pad(sp.row_hi, nj_), c = pad(sp.col_lo, ni_), d = pad(sp.col_hi, ni_);
-        rlo.insert(rlo.end(), a.begin(), a.end());
-        rhi.insert(rhi.end(), b.begin(), b.end());
-        clo.insert(clo.end(), c.begin(), c.end());
-        chi.insert(chi.end(), d.begin(), d.end());
-        mask.insert(mask.end(), sp.mask.begin(), sp.mask.end());
+        row_off[slot] = static_cast<long>(rlo.size());
+        col_off[slot] = static_cast<long>(clo.size());
+        auto ra = pad(sp.row_lo, sp.nj), rb = pad(sp.row_hi, sp.nj), ca = pad(sp.col_lo, sp.ni), cb = pad(sp.col_hi, sp.ni);
+        rlo.insert(rlo.end(), ra.begin(), ra.end());
+        rhi.insert(rhi.end(), rb.begin(), rb.end());
+        clo.insert(clo.end(), ca.begin(), ca.end());
+        chi.insert(chi.end(), cb.begin(), cb.end());
+        const long off = off_of_slot_[slot];
+        std::copy(sp.mask.begin(), sp.mask.end(), mask.begin() + off);
         const std::vector<double>* src[7] = {&sp.iq1x, &sp.iq2x, &sp.iq1y, &sp.iq2y, &sp.h_min, &sp.h_max, &sp.w_norm};
-        for (int k = 0; k < 7; ++k) geo[k].insert(geo[k].end(), src[k]->begin(), src[k]->end());
+        for (int k = 0; k < 7; ++k) std::copy(src[k]->begin(), src[k]->end(), geo[k].begin() + off);
     }
-    E.inv_len1 = static_cast<const double*>(up(il1.data(), S * sizeof(double)));
-    E.inv_len2 = static_cast<const double*>(up(il2.data(), S * sizeof(double)));
-    E.sub_i0 = static_cast<const int*>(up(i0.data(), S * sizeof(int)));
-    E.sub_j0 = static_cast<const int*>(up(j0.data(), S * sizeof(int)));
-    E.sub_patch = static_cast<const int*>(up(pt.data(), S * sizeof(int)));
+    E.h1 = static_cast<const double*>(up(h1.data(), S * sizeof(double)));
+    E.h2 = static_cast<const double*>(up(h2.data(), S * sizeof(double)));
+    E.cut_i = static_cast<const int*>(up(ci.data(), S * sizeof(int)));
+    E.cut_j = static_cast<const int*>(up(cj.data(), S * sizeof(int)));
     E.bc_row_lo = static_cast<const BcDev*>(up(rlo.data(), rlo.size() * sizeof(BcDev)));
     E.bc_row_hi = static_cast<const BcDev*>(up(rhi.data(), rhi.size() * sizeof(BcDev)));
     E.bc_col_lo = static_cast<const BcDev*>(up(clo.data(), clo.size() * sizeof(BcDev)));
@@ -314,6 +404,19 @@ void Engine::finalize() {
             E.visc_src = static_cast<const long*>(up(visc_src_.data(), visc_src_.size() * sizeof(long)));
             E.visc_w = static_cast<const double*>(up(visc_w_.data(), visc_w_.size() * sizeof(double)));
         }
+        if (!xi_dst_.empty()) {
+            E.xi_dst = static_cast<const long*>(up(xi_dst_.data(), xi_dst_.size() * sizeof(long)));
+            E.xi_src = static_cast<const long*>(up(xi_src_.data(), xi_src_.size() * sizeof(long)));
+            E.xi_pitch = static_cast<const int*>(up(xi_pitch_.data(), xi_pitch_.size() * sizeof(int)));
+            E.xi_w = static_cast<const double*>(up(xi_w_.data(), xi_w_.size() * sizeof(double)));
+        }
+        E.n_xi = static_cast<long>(xi_dst_.size());
+        if (!vi_src_.empty()) {
+            E.vi_off = static_cast<const int*>(up(vi_off_.data(), vi_off_.size() * sizeof(int)));
+            E.vi_src = static_cast<const long*>(up(vi_src_.data(), vi_src_.size() * sizeof(long)));
+            E.vi_pitch = static_cast<const int*>(up(vi_pitch_.data(), vi_pitch_.size() * sizeof(int)));
+            E.vi_w = static_cast<const double*>(up(vi_w_.data(), vi_w_.size() * sizeof(double)));
+        }
     }
     E.mlp = static_cast<const double*>(up(mlp_.data(), mlp_.size() * sizeof(double)));
     {
@@ -327,21 +430,152 @@ void Engine::finalize() {
     }
     halo_e_.clear();
     halo_mu_.clear();
-    for (auto [sb, lc] : halo_e_src_) {
-        if (sb < 0 || sb >= S || lc < 0 || lc >= sz) throw Error(kUsage, "halo donor out of range");
-        halo_e_.push_back(sb * sz + lc);
-    }
-    for (auto [sb, lc] : halo_mu_src_) {
-        if (sb < 0 || sb >= S || lc < 0 || lc >= sz) throw Error(kUsage, "halo donor out of range");
-        halo_mu_.push_back(sb * sz + lc);
-    }
+    for (auto [sb, lc] : halo_e_src_) halo_e_.push_back(gidx(sb, lc));
+    for (auto [sb, lc] : halo_mu_src_) halo_mu_.push_back(gidx(sb, lc));
     if (!halo_e_.empty()) d_halo_e_ = static_cast<long*>(up(halo_e_.data(), halo_e_.size() * sizeof(long)));
     if (!halo_mu_.empty()) d_halo_mu_ = static_cast<long*>(up(halo_mu_.data(), halo_mu_.size() * sizeof(long)));
     StepScalars sc{};
     double inf = kInf;
     std::memcpy(&sc.dtmin_bits, &inf, 8);
     E.sc = static_cast<StepScalars*>(up(&sc, sizeof(sc)));
+
+    // group views: every pointer offset to the group's first point / slot /
+    // line; line sets per orientation and length
+    G_.clear();
+    bool all_cart = true;
+    for (const Group& g : groups_) {
+        GroupLaunch gl;
+        EngineDev V = E;
+        V.S = g.n;
+        V.ni = g.ni;
+        V.nj = g.nj;
+        V.sub_base = g.slot0;
+        V.npts = static_cast<long>(g.n) * g.ni * g.nj;
+        V.div_ni = make_fastdiv(static_cast<unsigned>(g.ni));
+        V.div_sz = make_fastdiv(static_cast<unsigned>(g.ni * g.nj));
+        const long p0 = g.p0;
+        auto offp = [p0](auto* ptr) { return ptr ? ptr + p0 : ptr; };
+        V.mask = offp(E.mask);
+        V.iq1x = offp(E.iq1x);
+        V.iq2x = offp(E.iq2x);
+        V.iq1y = offp(E.iq1y);
+        V.iq2y = offp(E.iq2y);
+        V.h_min = offp(E.h_min);
+        V.h_max = offp(E.h_max);
+        V.w_norm = offp(E.w_norm);
+        for (int c = 0; c < 4; ++c) {
+            V.e[c] = offp(E.e[c]);
+            V.e0[c] = offp(E.e0[c]);
+            V.e2[c] = offp(E.e2[c]);
+            V.e3[c] = offp(E.e3[c]);
+            V.rhs3[c] = offp(E.rhs3[c]);
+            V.rhs[c] = offp(E.rhs[c]);
+            V.tA[c] = offp(E.tA[c]);
+            V.tW[c] = offp(E.tW[c]);
+            V.tS4[c] = offp(E.tS4[c]);
+            V.tS5[c] = offp(E.tS5[c]);
+            V.tF[c] = offp(E.tF[c]);
+        }
+        V.mu_hat = offp(E.mu_hat);
+        V.mu = offp(E.mu);
+        V.tau = offp(E.tau);
+        V.speed = offp(E.speed);
+        V.proxy = offp(E.proxy);
+        V.seed = offp(E.seed);
+        V.m01 = offp(E.m01);
+        V.h1 = E.h1 + g.slot0;
+        V.h2 = E.h2 + g.slot0;
+        V.cut_i = E.cut_i + g.slot0;
+        V.cut_j = E.cut_j + g.slot0;
+        V.bc_row_lo = E.bc_row_lo + row_off[g.slot0];
+        V.bc_row_hi = E.bc_row_hi + row_off[g.slot0];
+        V.bc_col_lo = E.bc_col_lo + col_off[g.slot0];
+        V.bc_col_hi = E.bc_col_hi + col_off[g.slot0];
+        // the global-view plan structures are not used through a group view
+        V.visc_off = nullptr;
+        V.vi_off = nullptr;
+        V.n_x = 0;
+        V.n_xi = 0;
+        // Cartesian group: iq2x == iq1y == 0 at every point
+        V.cartesian = cfg_.allow_cartesian ? 1 : 0;
+        for (int k = 0; k < g.n && V.cartesian; ++k) {
+            const auto& sp = subs_[id_of_slot_[g.slot0 + k]];
+            for (size_t q = 0; q < sp.iq2x.size(); ++q)
+                if (sp.iq2x[q] != 0.0 || sp.iq1y[q] != 0.0) {
+                    V.cartesian = 0;
+                    break;
+                }
+        }
+        all_cart = all_cart && V.cartesian;
+        // line sets: lengths n of the group's rows / columns; descriptor runs
+        // only when a subpatch of the group is L-shaped
+        bool any_l = false;
+        for (int k = 0; k < g.n; ++k) any_l = any_l || subs_[id_of_slot_[g.slot0 + k]].cut_i > 0;
+        for (int orient = 0; orient < 2; ++orient) {
+            const int nlines = orient == 0 ? g.nj : g.ni, nfull = orient == 0 ? g.ni : g.nj;
+            std::vector<LineSet>& sets = orient == 0 ? gl.rows : gl.cols;
+            auto make_set = [&](int n) {
+                LineSet L{};
+                const int op = ctx_.get_op(n, cfg_.n_cont, 2, cfg_.filter);
+                L.pl = ctx_.op(op).plan;
+                L.scr = step_scr_cap(L.pl);
+                return L;
+            };
+            if (!any_l) {
+                sets.push_back(make_set(nfull));
+                continue;
+            }
+            // runs of consecutive lines of one slot with one begin, per length
+            std::vector<std::pair<int, std::vector<std::array<int, 3>>>> runs;  // n -> (sub, line, begin)
+            for (int k = 0; k < g.n; ++k) {
+                const auto& sp = subs_[id_of_slot_[g.slot0 + k]];
+                for (int line = 0; line < nlines; ++line) {
+                    const int begin = orient == 0 ? (line < sp.cut_j ? sp.cut_i : 0) : (line < sp.cut_i ? sp.cut_j : 0);
+                    const int n = nfull - begin;
+                    size_t r = 0;
+                    while (r < runs.size() && runs[r].first != n) ++r;
+                    if (r == runs.size()) runs.push_back({n, {}});
+                    runs[r].second.push_back({k, line, begin});
+                }
+            }
+            for (auto& [n, lines] : runs) {
+                LineSet L = make_set(n);
+                for (int lb : {4, 8}) {
+                    std::vector<LineDesc> desc;
+                    for (size_t q = 0; q < lines.size();) {
+                        LineDesc d{lines[q][0], lines[q][1], 1, lines[q][2]};
+                        size_t r = q + 1;
+                        while (r < lines.size() && d.nl < lb && lines[r][0] == d.sub && lines[r][1] == d.line0 + d.nl &&
+                               lines[r][2] == d.begin) {
+                            ++d.nl;
+                            ++r;
+                        }
+                        desc.push_back(d);
+                        q = r;
+                    }
+                    const LineDesc* dd = static_cast<const LineDesc*>(up(desc.data(), desc.size() * sizeof(LineDesc)));
+                    if (lb == 4) {
+                        L.desc4 = dd;
+                        L.n4 = static_cast<int>(desc.size());
+                    } else {
+                        L.desc8 = dd;
+                        L.n8 = static_cast<int>(desc.size());
+                    }
+                }
+                sets.push_back(L);
+            }
+        }
+        gl.E = V;
+        G_.push_back(std::move(gl));
+    }
+    E.cartesian = all_cart ? 1 : 0;
     finalized_ = true;
+}
+
+bool Engine::cartesian() const {
+    for (const GroupLaunch& g : G_)
+        if (!g.E.cartesian) return false;
+    return !G_.empty();
 }
 
 double* Engine::field_ptr(const std::string& w, int c) {
@@ -374,33 +608,64 @@ double* Engine::field_ptr(const std::string& w, int c) {
 }
 
 void Engine::set_state(int sub, const double* e4) {
-    if (sub < 0 || sub >= E_.S) throw Error(kUsage, "bad subpatch id");
-    const long sz = static_cast<long>(ni_) * nj_;
-    for (int c = 0; c < 4; ++c) dev::h2d(E_.e[c] + sub * sz, e4 + c * sz, sz * sizeof(double), ctx_.stream);
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    if (sub < 0 || sub >= static_cast<int>(subs_.size())) throw Error(kUsage, "bad subpatch id");
+    const long sz = sub_points(sub), off = off_of_slot_[slot_of_[sub]];
+    for (int c = 0; c < 4; ++c) dev::h2d(E_.e[c] + off, e4 + c * sz, sz * sizeof(double), ctx_.stream);
 }
 
+// host layout [4][sum of points]: per component the subpatches in id order,
+// each [nj][ni]; one copy per component when the storage order is the id order
 void Engine::set_state_bulk(const double* e) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
-    for (int c = 0; c < 4; ++c) dev::h2d_async(E_.e[c], e + c * npts_, npts_ * sizeof(double), ctx_.stream);
+    bool identity = true;
+    for (size_t k = 0; k < slot_of_.size(); ++k) identity = identity && slot_of_[k] == static_cast<int>(k);
+    for (int c = 0; c < 4; ++c) {
+        if (identity) {
+            dev::h2d_async(E_.e[c], e + c * npts_, npts_ * sizeof(double), ctx_.stream);
+        } else {
+            long src = 0;
+            for (int id = 0; id < static_cast<int>(subs_.size()); ++id) {
+                const long sz = sub_points(id);
+                dev::h2d_async(E_.e[c] + off_of_slot_[slot_of_[id]], e + c * npts_ + src, sz * sizeof(double),
+                               ctx_.stream);
+                src += sz;
+            }
+        }
+    }
     dev::sync(ctx_.stream);
 }
 
 void Engine::get_state_bulk(double* e) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
-    for (int c = 0; c < 4; ++c) dev::d2h_async(e + c * npts_, E_.e[c], npts_ * sizeof(double), ctx_.stream);
+    bool identity = true;
+    for (size_t k = 0; k < slot_of_.size(); ++k) identity = identity && slot_of_[k] == static_cast<int>(k);
+    for (int c = 0; c < 4; ++c) {
+        if (identity) {
+            dev::d2h_async(e + c * npts_, E_.e[c], npts_ * sizeof(double), ctx_.stream);
+        } else {
+            long dst = 0;
+            for (int id = 0; id < static_cast<int>(subs_.size()); ++id) {
+                const long sz = sub_points(id);
+                dev::d2h_async(e + c * npts_ + dst, E_.e[c] + off_of_slot_[slot_of_[id]], sz * sizeof(double),
+                               ctx_.stream);
+                dst += sz;
+            }
+        }
+    }
     dev::sync(ctx_.stream);
 }
 
 void Engine::get_field(int sub, const std::string& name, int comp, double* out) {
-    if (sub < 0 || sub >= E_.S) throw Error(kUsage, "bad subpatch id");
-    const long sz = static_cast<long>(ni_) * nj_;
-    dev::d2h(out, field_ptr(name, comp) + sub * sz, sz * sizeof(double), ctx_.stream);
+    if (sub < 0 || sub >= static_cast<int>(subs_.size())) throw Error(kUsage, "bad subpatch id");
+    double* f = field_ptr(name, comp);
+    dev::d2h(out, f + off_of_slot_[slot_of_[sub]], sub_points(sub) * sizeof(double), ctx_.stream);
 }
 
 void Engine::set_field(int sub, const std::string& name, int comp, const double* in) {
-    if (sub < 0 || sub >= E_.S) throw Error(kUsage, "bad subpatch id");
-    const long sz = static_cast<long>(ni_) * nj_;
-    dev::h2d(field_ptr(name, comp) + sub * sz, in, sz * sizeof(double), ctx_.stream);
+    if (sub < 0 || sub >= static_cast<int>(subs_.size())) throw Error(kUsage, "bad subpatch id");
+    double* f = field_ptr(name, comp);
+    dev::h2d(f + off_of_slot_[slot_of_[sub]], in, sub_points(sub) * sizeof(double), ctx_.stream);
 }
 
 void Engine::check_error() {
@@ -409,17 +674,27 @@ void Engine::check_error() {
     if (sc.err.code == 0) return;
     // clear so the engine can report the next failure
     StepScalars clr = sc;
-    clr.err = DevError{0, 0, 0, 0};
+    clr.err = DevError{0, 0, 0, 0, -1};
     dev::h2d(E_.sc, &clr, sizeof(clr), ctx_.stream);
-    const auto& sp = subs_.at(sc.err.sub);
+    int slot = sc.err.sub, i = sc.err.i, j = sc.err.j;
+    if (sc.err.gp >= 0) {  // global point index -> (slot, i, j)
+        slot = static_cast<int>(std::upper_bound(off_of_slot_.begin(), off_of_slot_.end(), sc.err.gp) -
+                                off_of_slot_.begin()) - 1;
+        const long loc = sc.err.gp - off_of_slot_[slot];
+        const int ni = subs_[id_of_slot_[slot]].ni;
+        i = static_cast<int>(loc % ni);
+        j = static_cast<int>(loc / ni);
+    }
+    const int id = id_of_slot_.at(slot);
+    const auto& sp = subs_.at(id);
     const char* msg = sc.err.code == 1   ? "nonpositive density or pressure"
                       : sc.err.code == 2 ? "nonpositive density or pressure (viscosity proxy)"
                                          : "nonfinite wave speed";
-    throw StateError(msg, sp.patch, sc.err.sub, sp.i0 + sc.err.i, sp.j0 + sc.err.j, sc.t);
+    throw StateError(msg, sp.patch, id, sp.i0 + i, sp.j0 + j, sc.t);
 }
 
 void Engine::finish_ic() {
-    launch_bc(E_, ctx_.stream);
+    launch_bc(G_, ctx_.stream);
     launch_exchange(E_, ctx_.stream);
     dev::check("finish_ic");
     dev::sync(ctx_.stream);
@@ -428,16 +703,16 @@ void Engine::finish_ic() {
 void Engine::phase(int ph, int stage) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
     switch (ph) {
-        case 0: launch_phase0(E_, host_step_ == 0, ctx_.stream); break;
+        case 0: launch_phase0(E_, G_, host_step_ == 0, ctx_.stream); break;
         case 1: launch_phase1(E_, ctx_.stream); break;
         case 2:
-            launch_phase2(E_, plans_, host_step_ == 0, ctx_.stream);
-            launch_bc(E_, ctx_.stream);
+            launch_phase2(G_, host_step_ == 0, ctx_.stream);
+            launch_bc(G_, ctx_.stream);
             break;
         case 3:
             if (stage < 0 || stage > 4) throw Error(kUsage, "bad stage");
-            launch_stage(E_, plans_, stage, ctx_.stream);
-            launch_bc(E_, ctx_.stream);
+            launch_stage(G_, stage, ctx_.stream);
+            launch_bc(G_, ctx_.stream);
             break;
         case 6: launch_exchange(E_, ctx_.stream); break;
         default: throw Error(kUsage, "bad phase");
@@ -470,14 +745,14 @@ double Engine::time() {
 
 void Engine::enqueue_step(bool step0) {
     void* s = ctx_.stream;
-    launch_phase0(E_, step0, s);
+    launch_phase0(E_, G_, step0, s);
     launch_phase1(E_, s);
-    launch_phase2(E_, plans_, step0, s);
-    launch_bc(E_, s);
+    launch_phase2(G_, step0, s);
+    launch_bc(G_, s);
     launch_finalize_dt(E_, s);
     for (int st = 0; st < 5; ++st) {
-        launch_stage(E_, plans_, st, s);
-        launch_bc(E_, s);
+        launch_stage(G_, st, s);
+        launch_bc(G_, s);
         launch_exchange(E_, s);
     }
     launch_advance(E_, s);
@@ -486,13 +761,13 @@ void Engine::enqueue_step(bool step0) {
 void Engine::launch_group(int which) {
     void* s = ctx_.stream;
     switch (which) {
-        case 0: launch_phase0(E_, false, s); break;
+        case 0: launch_phase0(E_, G_, false, s); break;
         case 1: launch_phase1(E_, s); break;
-        case 2: launch_phase2(E_, plans_, false, s); break;
-        case 3: launch_pass_a(E_, plans_, s); break;
-        case 4: launch_pass_b(E_, plans_, 1, s); break;
-        case 5: launch_pass_c(E_, plans_, 1, s); break;
-        case 6: launch_bc(E_, s); break;
+        case 2: launch_phase2(G_, false, s); break;
+        case 3: launch_pass_a(G_, s); break;
+        case 4: launch_pass_b(G_, 1, s); break;
+        case 5: launch_pass_c(G_, 1, s); break;
+        case 6: launch_bc(G_, s); break;
         case 7: launch_exchange(E_, s); break;
         default: throw Error(kUsage, "bad launch group");
     }

@@ -40,6 +40,7 @@ struct EngineConfig {
 struct SubSpec {
     int patch = 0, i0 = 0, j0 = 0;
     int ni = 0, nj = 0;
+    int cut_i = 0, cut_j = 0;  // L-shaped: local points (i < cut_i && j < cut_j) are not in the set
     double h1 = 0, h2 = 0;
     std::vector<uint8_t> mask;
     std::vector<double> iq1x, iq2x, iq1y, iq2y, h_min, h_max, w_norm;
@@ -52,11 +53,17 @@ class Engine {
     ~Engine();
 
     int add_subpatch(SubSpec s);
-    // CommPlan (include/fcs/runtime.hpp:16-49), copies only: solution copies
+    // CommPlan (include/fcs/runtime.hpp:16-49) copies: solution copies
     // (dst_sub, dst, src_sub, src) and viscosity copies with weights.
     void set_plan(std::vector<int> sol_dst_sub, std::vector<int> sol_dst, std::vector<int> sol_src_sub,
                   std::vector<int> sol_src, std::vector<int> v_dst_sub, std::vector<int> v_dst,
                   std::vector<int> v_src_sub, std::vector<int> v_src, std::vector<double> v_w);
+    // CommPlan interpolations (InterpEntry, include/fcs/runtime.hpp:25-31):
+    // which 0 = solution, 1 = viscosity blend; donor stencil origin (si0, sj0)
+    // in the donor subpatch, weights wx[6], wy[6] per entry (and w for the blend)
+    void set_plan_interps(int which, std::vector<int> dst_sub, std::vector<int> dst, std::vector<int> src_sub,
+                          std::vector<int> si0, std::vector<int> sj0, std::vector<double> wx, std::vector<double> wy,
+                          std::vector<double> w);
     // Cross-rank halo (multi-GPU): donor points this rank packs for other
     // ranks (solution state and mu_hat), and how many values it receives.
     // Received values land in extra slots after the local points; plan
@@ -98,28 +105,39 @@ class Engine {
     double time();
     long steps() const { return host_step_; }
     long total_points() const { return npts_; }
-    bool cartesian() const { return E_.cartesian != 0; }
+    // every shape group on the Cartesian (zero metric term) passes
+    bool cartesian() const;
+    int n_groups() const { return static_cast<int>(G_.size()); }
     void check_error();
     // average device milliseconds of one launch group (profiling hook):
     // 0 phase 0 (proxy + classifier), 1 phase 1 (blend + dt), 2 phase 2
     // (filter rows + cols), 3 pass A, 4 pass B, 5 pass C (stage 1), 6 BC,
     // 7 exchange
     double time_pass(int which, int reps);
-    int launches_per_step() const { return fcsg::launches_per_step(E_); }
+    int launches_per_step() const { return fcsg::launches_per_step(G_); }
     void launch_group(int which);
     void* stream() const { return ctx_.stream; }
 
   private:
     double* field_ptr(const std::string& name, int comp);
+    void layout();                          // storage order by shape group (after the last add_subpatch)
+    long gidx(int sub, int loc) const;      // global point index of (subpatch id, local index)
+    long sub_points(int sub) const { return static_cast<long>(subs_.at(sub).ni) * subs_.at(sub).nj; }
     Ctx& ctx_;
     EngineConfig cfg_;
-    std::vector<SubSpec> subs_;
-    bool finalized_ = false;
-    int ni_ = 0, nj_ = 0;
+    std::vector<SubSpec> subs_;             // by subpatch id
+    bool finalized_ = false, laid_out_ = false;
     long npts_ = 0;
-    int op_row_ = -1, op_col_ = -1;
-    LinePlans plans_{};
-    EngineDev E_{};
+    // storage: subpatches grouped by (ni, nj), ids in order within a group
+    struct Group {
+        int ni, nj, slot0, n;
+        long p0;
+    };
+    std::vector<Group> groups_;
+    std::vector<int> slot_of_, id_of_slot_;
+    std::vector<long> off_of_slot_;         // first point of each storage slot
+    EngineDev E_{};                         // global view
+    std::vector<GroupLaunch> G_;            // group views + line sets
     std::vector<void*> allocs_;
     double* pool_ = nullptr;
     std::vector<double> mlp_;
@@ -128,6 +146,13 @@ class Engine {
     std::vector<int> visc_off_;
     std::vector<long> visc_src_;
     std::vector<double> visc_w_;
+    std::vector<long> xi_dst_, xi_src_;
+    std::vector<int> xi_pitch_;
+    std::vector<double> xi_w_;
+    std::vector<int> vi_off_;
+    std::vector<long> vi_src_;
+    std::vector<int> vi_pitch_;
+    std::vector<double> vi_w_;
     bool have_plan_ = false;
     std::vector<long> halo_e_, halo_mu_;  // packed donor points (global local-engine indices)
     long n_recv_e_ = 0, n_recv_mu_ = 0;

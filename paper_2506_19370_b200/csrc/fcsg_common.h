@@ -48,12 +48,15 @@ enum ErrKind : int {
     kOther = 9,
 };
 
-// device error word: code, subpatch, i, j (first failure wins)
+// device error word (first failure wins): code and either (storage slot of
+// the subpatch, i, j) or, from the kernels over all points, the global point
+// index gp (>= 0; the host maps it back to (subpatch, i, j))
 struct DevError {
     int code;  // 0 = none; 1 = nonpositive density or pressure (rhs), 2 = proxy/MWSB, 3 = nonfinite wave speed
     int sub;
     int i;
     int j;
+    long long gp;
 };
 
 struct Thr {

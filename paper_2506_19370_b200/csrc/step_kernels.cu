@@ -40,12 +40,13 @@ constexpr double SC2 = 0.517231671970585, SC3 = 0.096059710526147, SD3 = 0.06369
 constexpr int kThreads = 256;
 }  // namespace
 
-FCSG_HD void raise_error(StepScalars* sc, int code, int sub, int i, int j) {
+FCSG_HD void raise_error_at(StepScalars* sc, int code, int sub, int i, int j, long long gp) {
 #if FCSG_CUDA
     if (atomicCAS(&sc->err.code, 0, code) == 0) {
         sc->err.sub = sub;
         sc->err.i = i;
         sc->err.j = j;
+        sc->err.gp = gp;
     }
 #else
     if (sc->err.code == 0) {
@@ -53,9 +54,13 @@ FCSG_HD void raise_error(StepScalars* sc, int code, int sub, int i, int j) {
         sc->err.sub = sub;
         sc->err.i = i;
         sc->err.j = j;
+        sc->err.gp = gp;
     }
 #endif
 }
+// (storage slot, i, j) of a group view / a global point index
+FCSG_HD void raise_error(StepScalars* sc, int code, int sub, int i, int j) { raise_error_at(sc, code, sub, i, j, -1); }
+FCSG_HD void raise_error_gp(StepScalars* sc, int code, long gp) { raise_error_at(sc, code, -1, 0, 0, gp); }
 
 FCSG_HD unsigned long long dbits(double v) {
 #if FCSG_CUDA
@@ -82,13 +87,15 @@ struct LineCtx {
     int sub;
     int line0;
     int nl_valid;
+    int begin;  // first point along the line (L-shaped subpatches)
     long base;
     int ni;
     bool rows;
 };
 
 FCSG_HD long pidx(const LineCtx& c, int l, int i) {
-    return c.rows ? c.base + static_cast<long>(c.line0 + l) * c.ni + i : c.base + static_cast<long>(i) * c.ni + c.line0 + l;
+    return c.rows ? c.base + static_cast<long>(c.line0 + l) * c.ni + c.begin + i
+                  : c.base + static_cast<long>(c.begin + i) * c.ni + c.line0 + l;
 }
 
 // asynchronous 8-byte global -> shared copies (cp.async), used to prefetch the
@@ -133,18 +140,27 @@ FCSG_HD void stage_wait() {
 // whose input is computed from the previous round's result).
 template <int LB, class Pass, int NE, int NTHR>
 FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const EngineDev& E, const FcPlanDev& pl,
-                       int scr_cap) {
+                       int scr_cap, const LineDesc* desc) {
     constexpr bool rows = Pass::kRows;
     constexpr int pitch = LB + 1;
     constexpr int KS = Pass::kStage;
     const int ni = E.ni, nj = E.nj;
-    const int N = NE > 0 ? NE - 24 : (rows ? ni : nj);
-    const int nlines = rows ? nj : ni;
-    const int bps = (nlines + LB - 1) / LB;
+    const int N = NE > 0 ? NE - 24 : pl.n;  // the line length of this launch
     LineCtx c;
-    c.sub = block / bps;
-    c.line0 = (block - c.sub * bps) * LB;
-    c.nl_valid = (nlines - c.line0 < LB) ? nlines - c.line0 : LB;
+    if (desc) {  // explicit line runs (groups with L-shaped subpatches)
+        const LineDesc d = desc[block];
+        c.sub = d.sub;
+        c.line0 = d.line0;
+        c.nl_valid = d.nl;
+        c.begin = d.begin;
+    } else {     // every line of every subpatch of the view
+        const int nlines = rows ? nj : ni;
+        const int bps = (nlines + LB - 1) / LB;
+        c.sub = block / bps;
+        c.line0 = (block - c.sub * bps) * LB;
+        c.nl_valid = (nlines - c.line0 < LB) ? nlines - c.line0 : LB;
+        c.begin = 0;
+    }
     c.base = static_cast<long>(c.sub) * ni * nj;
     c.ni = ni;
     c.rows = rows;
@@ -153,7 +169,8 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
     double2* tabs = scr + scr_cap;
     double* stg = reinterpret_cast<double*>(tabs + table_slots(pl));
     const FcPlanDev spl = stage_tables(Thr{t.tid, NTHR}, pl, P.mode(0), tabs);  // one mode per pass
-    const double inv_len = P.kScaled ? (rows ? E.inv_len1[c.sub] : E.inv_len2[c.sub]) : 1.0;
+    // LineInfo::inv_len = 1 / ((n - 1) h) (src/subpatch_data.cpp:134,147)
+    const double inv_len = P.kScaled ? 1.0 / ((N - 1) * (rows ? E.h1[c.sub] : E.h2[c.sub])) : 1.0;
     const int total = N * LB;
     const int tid = t.tid;
     for (int r = 0; r <= Pass::kRounds; ++r) {
@@ -283,7 +300,7 @@ FCSG_HD void check_positive(const EngineDev& E, const Prim& q, long p, const Lin
     const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
     if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) {
         const long loc = p - c.base;
-        raise_error(E.sc, 1, c.sub, static_cast<int>(loc % c.ni), static_cast<int>(loc / c.ni));
+        raise_error(E.sc, 1, E.sub_base + c.sub, static_cast<int>(loc % c.ni), static_cast<int>(loc / c.ni));
     }
 }
 
@@ -985,9 +1002,7 @@ FCSG_HD void proxy_body(Thr t, int block, int nblocks, const EngineDev& E) {
         const double ke = 0.5 * rho * (u * u + v * v);
         const double pr = kGm1 * (En - ke);
         if (!(rho > 0.0) || !(pr > 0.0)) {
-            const long loc = p % (static_cast<long>(E.ni) * E.nj);
-            raise_error(E.sc, 2, static_cast<int>(p / (static_cast<long>(E.ni) * E.nj)), static_cast<int>(loc % E.ni),
-                        static_cast<int>(loc / E.ni));
+            raise_error_gp(E.sc, 2, p);
             E.proxy[p] = 0.0;
             E.speed[p] = 1.0;
             continue;
@@ -1126,21 +1141,24 @@ FCSG_HD int classify_stencil(const WA& W, const double* tab, const double* s, do
 }
 
 // Classifier::classify (src/viscosity.cpp:211-238) for one point of a
-// rectangular subpatch: min of the row-window and column-window classes.
+// subpatch: min of the row-window and column-window classes. The row of the
+// point is the segment [rb, ni), its column [cb, nj) (L-shaped subpatches:
+// row_begin / col_begin); window start = clamp(pos - 3, 0, n - 7) within it.
 template <class WA>
-FCSG_HD int classify_point(const WA& W, const double* tab, const double* f, long base, int ni, int nj, int i, int j, double abs_floor) {
+FCSG_HD int classify_point(const WA& W, const double* tab, const double* f, long base, int ni, int nj, int i, int j,
+                           int rb, int cb, double abs_floor) {
     double s[kMlpIn];
     int cr = 4, cc = 4;
-    if (ni >= kMlpIn) {
-        int st = i - kMlpIn / 2;
-        st = st < 0 ? 0 : (st > ni - kMlpIn ? ni - kMlpIn : st);
+    if (ni - rb >= kMlpIn) {
+        int st = i - rb - kMlpIn / 2;
+        st = rb + (st < 0 ? 0 : (st > ni - rb - kMlpIn ? ni - rb - kMlpIn : st));
 #pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(j) * ni + st + k];
         cr = classify_stencil(W, tab, s, abs_floor);
     }
-    if (nj >= kMlpIn) {
-        int st = j - kMlpIn / 2;
-        st = st < 0 ? 0 : (st > nj - kMlpIn ? nj - kMlpIn : st);
+    if (nj - cb >= kMlpIn) {
+        int st = j - cb - kMlpIn / 2;
+        st = cb + (st < 0 ? 0 : (st > nj - cb - kMlpIn ? nj - cb - kMlpIn : st));
 #pragma unroll
         for (int k = 0; k < kMlpIn; ++k) s[k] = f[base + static_cast<long>(st + k) * ni + i];
         cc = classify_stencil(W, tab, s, abs_floor);
@@ -1160,11 +1178,19 @@ FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, double* t
         const long base = (p / sz) * sz;
         const long loc = p - base;
         const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
-        const int tau = classify_point(W, tab, E.proxy, base, E.ni, E.nj, i, j, E.abs_floor);
+        const int sub = static_cast<int>(p / sz), ci = E.cut_i[sub], cj = E.cut_j[sub];
+        if (i < ci && j < cj) {  // not in the point set of an L-shaped subpatch
+            E.tau[p] = 4.0;
+            E.mu_hat[p] = 0.0;
+            if (step0) E.seed[p] = 0.0;
+            continue;
+        }
+        const int rb = j < cj ? ci : 0, cb = i < ci ? cj : 0;
+        const int tau = classify_point(W, tab, E.proxy, base, E.ni, E.nj, i, j, rb, cb, E.abs_floor);
         E.tau[p] = tau;
         E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
         if (step0) {
-            const int tr = classify_point(W, tab, E.e[0], base, E.ni, E.nj, i, j, E.abs_floor);
+            const int tr = classify_point(W, tab, E.e[0], base, E.ni, E.nj, i, j, rb, cb, E.abs_floor);
             E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
         }
     }
@@ -1317,10 +1343,13 @@ __global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_
         const unsigned loc = pp - sub * E.div_sz.d;
         const int j = static_cast<int>(fdiv(E.div_ni, loc)), i = static_cast<int>(loc) - j * E.ni;
         const long base = static_cast<long>(sub) * sz;
-        const int n = col ? E.nj : E.ni;
-        const bool active = valid && n >= kMlpIn;
-        int st = (col ? j : i) - kMlpIn / 2;
-        st = st < 0 ? 0 : (st > n - kMlpIn ? n - kMlpIn : st);
+        const int ci = E.cut_i[sub], cj = E.cut_j[sub];
+        const bool inset = !(i < ci && j < cj);  // L-shaped subpatches: row/column segments
+        const int beg = col ? (i < ci ? cj : 0) : (j < cj ? ci : 0);
+        const int n = (col ? E.nj : E.ni) - beg;
+        const bool active = valid && inset && n >= kMlpIn;
+        int st = (col ? j : i) - beg - kMlpIn / 2;
+        st = beg + (st < 0 ? 0 : (st > n - kMlpIn ? n - kMlpIn : st));
         double sa = 0.0, sb = 0.0;
         if (active) {
             sa = window_at(E.proxy, base, E.ni, col, st, i, j, t);
@@ -1343,7 +1372,7 @@ __global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_
         if (valid && !col && t == 0) {
             E.tau[p] = tau;
             E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
-            if (step0) E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
+            if (step0) E.seed[p] = (inset && E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
         }
     }
 }
@@ -1373,12 +1402,27 @@ FCSG_HD void dilate_body(Thr t, int block, int nblocks, const EngineDev& E) {
 FCSG_HD void blend_body(Thr t, int block, int nblocks, const EngineDev& E) {
     const long step = static_cast<long>(nblocks) * t.nthr;
     double best = INFINITY;
-    const long sz = static_cast<long>(E.ni) * E.nj;
     for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
         double m = E.w_norm[p] * E.mu_hat[p];
         if (E.visc_off) {
             const int e0 = E.visc_off[p], e1 = E.visc_off[p + 1];
             for (int k = e0; k < e1; ++k) m += E.visc_w[k] * E.mu_hat[E.visc_src[k]];
+        }
+        if (E.vi_off) {  // 6x6 Lagrange of the donor's mu_hat (src/runtime.cpp:359-368)
+            const int e0 = E.vi_off[p], e1 = E.vi_off[p + 1];
+            for (int k = e0; k < e1; ++k) {
+                const double* w = E.vi_w + 13 * static_cast<long>(k);
+                const double* src = E.mu_hat + E.vi_src[k];
+                const int pitch = E.vi_pitch[k];
+                double val = 0.0;
+                for (int b = 0; b < 6; ++b) {
+                    const double* row = src + static_cast<long>(b) * pitch;
+                    double sa = 0.0;
+                    for (int a = 0; a < 6; ++a) sa += w[a] * row[a];
+                    val += w[6 + b] * sa;
+                }
+                m += w[12] * val;
+            }
         }
         m = m > 0.0 ? m : 0.0;
         E.mu[p] = m;
@@ -1386,8 +1430,7 @@ FCSG_HD void blend_body(Thr t, int block, int nblocks, const EngineDev& E) {
             const double h = E.h_min[p];
             const double rate = E.speed[p] / h + m / (h * h);
             if (!(rate > 0.0) || !finite_d(rate)) {
-                const long loc = p % sz;
-                raise_error(E.sc, 3, static_cast<int>(p / sz), static_cast<int>(loc % E.ni), static_cast<int>(loc / E.ni));
+                raise_error_gp(E.sc, 3, p);
             } else {
                 const double v = 1.0 / rate;
                 best = v < best ? v : best;
@@ -1474,20 +1517,24 @@ FCSG_HD void apply_bc_at(const EngineDev& E, const BcDev& bc, long p, long p1, l
     }
 }
 
-// enforce_bc (src/euler.cpp:167-180): one CTA per subpatch, all row ends, then all column ends
+// enforce_bc (src/euler.cpp:167-180): one CTA per subpatch, all row ends, then
+// all column ends; a line of an L-shaped subpatch starts at its row/column
+// begin (LineInfo::begin)
 FCSG_HD void bc_body(Thr t, int sub, const EngineDev& E) {
     const int ni = E.ni, nj = E.nj;
+    const int ci = E.cut_i[sub], cj = E.cut_j[sub];
     const long base = static_cast<long>(sub) * ni * nj;
     for (int j = t.tid; j < nj; j += t.nthr) {
-        const long r = base + static_cast<long>(j) * ni;
+        const long r = base + static_cast<long>(j) * ni + (j < cj ? ci : 0);
+        const long re = base + static_cast<long>(j) * ni + ni - 1;
         const BcDev& lo = E.bc_row_lo[static_cast<long>(sub) * nj + j];
         const BcDev& hi = E.bc_row_hi[static_cast<long>(sub) * nj + j];
         if (lo.kind >= 0) apply_bc_at(E, lo, r, r + 1, r + 2, 0);
-        if (hi.kind >= 0) apply_bc_at(E, hi, r + ni - 1, r + ni - 2, r + ni - 3, 0);
+        if (hi.kind >= 0) apply_bc_at(E, hi, re, re - 1, re - 2, 0);
     }
     FCSG_SYNC();
     for (int i = t.tid; i < ni; i += t.nthr) {
-        const long c0 = base + i, c1 = base + static_cast<long>(nj - 1) * ni + i;
+        const long c0 = base + static_cast<long>(i < ci ? cj : 0) * ni + i, c1 = base + static_cast<long>(nj - 1) * ni + i;
         const BcDev& lo = E.bc_col_lo[static_cast<long>(sub) * ni + i];
         const BcDev& hi = E.bc_col_hi[static_cast<long>(sub) * ni + i];
         if (lo.kind >= 0) apply_bc_at(E, lo, c0, c0 + ni, c0 + 2 * ni, 1);
@@ -1495,12 +1542,32 @@ FCSG_HD void bc_body(Thr t, int sub, const EngineDev& E) {
     }
 }
 
-// phase 6: fringe copies (src/runtime.cpp:436-439)
+// phase 6: fringe copies, then 6x6 tensor Lagrange interpolations from
+// donor stencils (src/runtime.cpp:433-454). Donors are interior points, never
+// written here, so copies and interpolations are independent.
 FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
     const long step = static_cast<long>(nblocks) * t.nthr;
-    for (long k = static_cast<long>(block) * t.nthr + t.tid; k < E.n_x; k += step) {
-        const long d = E.x_dst[k], s = E.x_src[k];
-        for (int c = 0; c < 4; ++c) E.e[c][d] = E.e[c][s];
+    const long n = E.n_x + E.n_xi;
+    for (long k = static_cast<long>(block) * t.nthr + t.tid; k < n; k += step) {
+        if (k < E.n_x) {
+            const long d = E.x_dst[k], s = E.x_src[k];
+            for (int c = 0; c < 4; ++c) E.e[c][d] = E.e[c][s];
+        } else {
+            const long q = k - E.n_x;
+            const double* w = E.xi_w + 12 * q;
+            const long s0 = E.xi_src[q], d = E.xi_dst[q];
+            const int pitch = E.xi_pitch[q];
+            for (int c = 0; c < 4; ++c) {
+                double val = 0.0;
+                for (int b = 0; b < 6; ++b) {
+                    const double* row = E.e[c] + s0 + static_cast<long>(b) * pitch;
+                    double sa = 0.0;
+                    for (int a = 0; a < 6; ++a) sa += w[a] * row[a];
+                    val += w[6 + b] * sa;
+                }
+                E.e[c][d] = val;
+            }
+        }
     }
 }
 
@@ -1533,10 +1600,11 @@ FCSG_HD void unpack_body(Thr t, int block, int nblocks, const EngineDev& E, int 
 #if FCSG_CUDA
 template <int LB, class Pass, int NE, int NT>
 __global__ void __launch_bounds__(NT, (NE > 0 ? 768 : 512) / NT)
-    line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg) {
+    line_pass_kernel(const __grid_constant__ EngineDev E, const __grid_constant__ FcPlanDev pl, int scr_cap, int arg,
+                     const LineDesc* desc) {
     extern __shared__ double2 smem[];
     const Pass P(E, arg);
-    line_pass<LB, Pass, NE, NT>(Thr{static_cast<int>(threadIdx.x), NT}, blockIdx.x, smem, P, E, pl, scr_cap);
+    line_pass<LB, Pass, NE, NT>(Thr{static_cast<int>(threadIdx.x), NT}, blockIdx.x, smem, P, E, pl, scr_cap, desc);
 }
 __global__ void __launch_bounds__(kThreads) proxy_kernel(const __grid_constant__ EngineDev E) {
     proxy_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
@@ -1586,7 +1654,7 @@ int grid_for(long n) {
 #if FCSG_CUDA
 template <class Pass, int NE, int NT, int LB>
 void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
-                         cudaStream_t s) {
+                      const LineDesc* desc, cudaStream_t s) {
     auto k = line_pass_kernel<LB, Pass, NE, NT>;
     static bool attr_set = false;  // once per instantiation (not during graph capture)
     if (!attr_set) {
@@ -1594,17 +1662,19 @@ void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const 
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr_set = true;
     }
-    k<<<nblk, NT, smem, s>>>(E, pl, scr_cap, arg);
+    k<<<nblk, NT, smem, s>>>(E, pl, scr_cap, arg, desc);
 }
-
 #endif
 
-// Lines per CTA: Pass::kLB for the compile-time plans (4 where a large
-// staging area would otherwise cost occupancy: three 256-thread CTAs per SM
-// fit in shared memory), kLB for the generic plan.
+// One line set of one group view. Lines per CTA: Pass::kLB for the
+// compile-time plans (4 where a large staging area would otherwise cost
+// occupancy: three 256-thread CTAs per SM fit in shared memory), kLB for the
+// generic plan.
 template <class Pass>
-void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap, void* stream) {
+void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) {
     constexpr int kSlots = Pass::kStage + Pass::kStash;
+    const FcPlanDev& pl = L.pl;
+    int scr_cap = L.scr;
     const int nlines = Pass::kRows ? E.nj : E.ni;
     // the compile-time plans assume the reference operator (n_cont 25, degree 2)
     const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
@@ -1615,25 +1685,36 @@ void run_line_pass(int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap
     constexpr int kCtLB = kLB;  // the emulation covers the loop structure, not the CTA shape
 #endif
     const int lb = ct ? kCtLB : kLB;
+    const LineDesc* desc = lb == 4 ? L.desc4 : L.desc8;
     if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, lb);  // full-scratch prime-67 middle
-    const int nblk = E.S * ((nlines + lb - 1) / lb);
+    const int nblk = desc ? (lb == 4 ? L.n4 : L.n8) : E.S * ((nlines + lb - 1) / lb);
+    if (nblk == 0) return;
     const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2) +
                         static_cast<size_t>(kSlots) * pl.n * lb * sizeof(double);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, s);
-    else if (ct) launch_line_pass<Pass, 536, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, s);
-    else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, s);
+    if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct) launch_line_pass<Pass, 536, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
 #else
     (void)stream;
     const Pass P(E, arg);
     std::vector<double2> sm(smem / sizeof(double2) + 1);
     for (int b = 0; b < nblk; ++b) {
-        if (ct && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
-        else if (ct) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
-        else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap);
+        if (ct && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
     }
 #endif
+}
+
+template <class Pass>
+void run_rows(int arg, const GroupLaunch& g, void* stream) {
+    for (const LineSet& L : g.rows) run_line_pass<Pass>(arg, g.E, L, stream);
+}
+template <class Pass>
+void run_cols(int arg, const GroupLaunch& g, void* stream) {
+    for (const LineSet& L : g.cols) run_line_pass<Pass>(arg, g.E, L, stream);
 }
 
 }  // namespace
@@ -1651,103 +1732,131 @@ int step_scr_cap(const FcPlanDev& pl) {
     return cap;
 }
 
-void launch_phase0(const EngineDev& E, bool step0, void* stream) {
+void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream) {
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    proxy_kernel<<<grid_for(E.npts), kThreads, 0, s>>>(E);
+    proxy_kernel<<<grid_for(Eall.npts), kThreads, 0, s>>>(Eall);
     static const bool scalar = [] {
         const char* v = std::getenv("FCSG_CLASSIFIER");
         return v && std::string(v) == "scalar";
     }();
-    if (scalar) {  // CUDA-core classifier (constant-bank weights), for comparison
-        cudaMemcpyToSymbolAsync(c_mlp, E.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
-        long g = (E.npts + kClsThreads - 1) / kClsThreads;
-        g = g > 148 * 24 ? 148 * 24 : g;
-        classify_kernel<<<static_cast<int>(g), kClsThreads, 0, s>>>(E, step0);
-    } else {
-        long g = ((E.npts + 3) / 4 + kMmaThreads / 32 - 1) / (kMmaThreads / 32);
-        g = g > 148 * 8 ? 148 * 8 : g;
-        classify_mma_kernel<<<static_cast<int>(g < 1 ? 1 : g), kMmaThreads, 0, s>>>(E, step0);
+    if (scalar) cudaMemcpyToSymbolAsync(c_mlp, Eall.mlp, kMlpWeights * sizeof(double), 0, cudaMemcpyDeviceToDevice, s);
+    for (const GroupLaunch& g : G) {
+        const EngineDev& E = g.E;
+        if (scalar) {  // CUDA-core classifier (constant-bank weights), for comparison
+            long n = (E.npts + kClsThreads - 1) / kClsThreads;
+            n = n > 148 * 24 ? 148 * 24 : n;
+            classify_kernel<<<static_cast<int>(n), kClsThreads, 0, s>>>(E, step0);
+        } else {
+            long n = ((E.npts + 3) / 4 + kMmaThreads / 32 - 1) / (kMmaThreads / 32);
+            n = n > 148 * 8 ? 148 * 8 : n;
+            classify_mma_kernel<<<static_cast<int>(n < 1 ? 1 : n), kMmaThreads, 0, s>>>(E, step0);
+        }
     }
 #else
     (void)stream;
-    proxy_body(Thr{0, 1}, 0, 1, E);
+    proxy_body(Thr{0, 1}, 0, 1, Eall);
     std::vector<double> tab(kTanhTable);
-    classify_body(Thr{0, 1}, 0, 1, MlpW{E.mlp}, tab.data(), E, step0);
+    for (const GroupLaunch& g : G) classify_body(Thr{0, 1}, 0, 1, MlpW{g.E.mlp}, tab.data(), g.E, step0);
 #endif
 }
 
-void launch_phase1(const EngineDev& E, void* stream) {
+void launch_phase1(const EngineDev& Eall, void* stream) {
 #if FCSG_CUDA
-    blend_kernel<<<grid_for(E.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+    blend_kernel<<<grid_for(Eall.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(Eall);
 #else
     (void)stream;
-    blend_body(Thr{0, 1}, 0, 1, E);
+    blend_body(Thr{0, 1}, 0, 1, Eall);
 #endif
 }
 
-void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* stream) {
-    if (step0) {
+void launch_phase2(const std::vector<GroupLaunch>& G, bool step0, void* stream) {
+    for (const GroupLaunch& g : G) {
+        if (step0) {
 #if FCSG_CUDA
-        dilate_kernel<<<grid_for(E.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+            dilate_kernel<<<grid_for(g.E.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g.E);
 #else
-        dilate_body(Thr{0, 1}, 0, 1, E);
+            dilate_body(Thr{0, 1}, 0, 1, g.E);
 #endif
+        }
+        run_rows<PassFR>(step0 ? 1 : 0, g, stream);
+        run_cols<PassFC>(step0 ? 1 : 0, g, stream);
     }
-    run_line_pass<PassFR>(step0 ? 1 : 0, E, P.row, P.scr_row, stream);
-    run_line_pass<PassFC>(step0 ? 1 : 0, E, P.col, P.scr_col, stream);
 }
 
-void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
-    launch_pass_a(E, P, stream);
-    launch_pass_b(E, P, stage, stream);
-    launch_pass_c(E, P, stage, stream);
+void launch_stage(const std::vector<GroupLaunch>& G, int stage, void* stream) {
+    launch_pass_a(G, stream);
+    launch_pass_b(G, stage, stream);
+    launch_pass_c(G, stage, stream);
 }
 
 // flux form: Cartesian X, Y (no third pass); general GA, GB, C.
 // reference order: A', B', C' / A, B, C.
-void launch_pass_a(const EngineDev& E, const LinePlans& P, void* stream) {
-    if (E.reference_order) {
-        if (E.cartesian) run_line_pass<PassAc>(0, E, P.row, P.scr_row, stream);
-        else run_line_pass<PassA>(0, E, P.row, P.scr_row, stream);
-    } else {
-        if (E.cartesian) run_line_pass<PassXc>(0, E, P.row, P.scr_row, stream);
-        else run_line_pass<PassGA>(0, E, P.row, P.scr_row, stream);
+void launch_pass_a(const std::vector<GroupLaunch>& G, void* stream) {
+    for (const GroupLaunch& g : G) {
+        if (g.E.reference_order) {
+            if (g.E.cartesian) run_rows<PassAc>(0, g, stream);
+            else run_rows<PassA>(0, g, stream);
+        } else {
+            if (g.E.cartesian) run_rows<PassXc>(0, g, stream);
+            else run_rows<PassGA>(0, g, stream);
+        }
     }
 }
-void launch_pass_b(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
-    if (E.reference_order) {
-        if (E.cartesian) run_line_pass<PassBc>(0, E, P.col, P.scr_col, stream);
-        else run_line_pass<PassB>(0, E, P.col, P.scr_col, stream);
-    } else {
-        if (E.cartesian) run_line_pass<PassYc>(stage, E, P.col, P.scr_col, stream);
-        else run_line_pass<PassGB>(0, E, P.col, P.scr_col, stream);
+void launch_pass_b(const std::vector<GroupLaunch>& G, int stage, void* stream) {
+    for (const GroupLaunch& g : G) {
+        if (g.E.reference_order) {
+            if (g.E.cartesian) run_cols<PassBc>(0, g, stream);
+            else run_cols<PassB>(0, g, stream);
+        } else {
+            if (g.E.cartesian) run_cols<PassYc>(stage, g, stream);
+            else run_cols<PassGB>(0, g, stream);
+        }
     }
 }
-void launch_pass_c(const EngineDev& E, const LinePlans& P, int stage, void* stream) {
-    if (E.reference_order) {
-        if (E.cartesian) run_line_pass<PassCc>(stage, E, P.row, P.scr_row, stream);
-        else run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
-    } else if (!E.cartesian) {
-        run_line_pass<PassC>(stage, E, P.row, P.scr_row, stream);
+void launch_pass_c(const std::vector<GroupLaunch>& G, int stage, void* stream) {
+    for (const GroupLaunch& g : G) {
+        if (g.E.reference_order) {
+            if (g.E.cartesian) run_rows<PassCc>(stage, g, stream);
+            else run_rows<PassC>(stage, g, stream);
+        } else if (!g.E.cartesian) {
+            run_rows<PassC>(stage, g, stream);
+        }
     }
 }
 
-int stage_launches(const EngineDev& E) { return (E.cartesian && !E.reference_order) ? 2 : 3; }
+int stage_launches(const std::vector<GroupLaunch>& G) {
+    int n = 0;
+    for (const GroupLaunch& g : G) {
+        const int nr = static_cast<int>(g.rows.size()), nc = static_cast<int>(g.cols.size());
+        n += (g.E.cartesian && !g.E.reference_order) ? nr + nc : 2 * nr + nc;
+    }
+    return n;
+}
 
-void launch_bc(const EngineDev& E, void* stream) {
+int launches_per_step(const std::vector<GroupLaunch>& G) {
+    // proxy, blend, dt, advance; per group classify, bc x 6, filter rows + cols;
+    // per stage the passes and one exchange
+    int n = 4 + 5;
+    for (const GroupLaunch& g : G) n += 1 + 6 + static_cast<int>(g.rows.size() + g.cols.size());
+    return n + 5 * stage_launches(G);
+}
+
+void launch_bc(const std::vector<GroupLaunch>& G, void* stream) {
+    for (const GroupLaunch& g : G) {
 #if FCSG_CUDA
-    bc_kernel<<<E.S, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+        bc_kernel<<<g.E.S, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(g.E);
 #else
-    (void)stream;
-    for (int s = 0; s < E.S; ++s) bc_body(Thr{0, 1}, s, E);
+        (void)stream;
+        for (int s = 0; s < g.E.S; ++s) bc_body(Thr{0, 1}, s, g.E);
 #endif
+    }
 }
 
 void launch_exchange(const EngineDev& E, void* stream) {
-    if (E.n_x == 0) return;
+    if (E.n_x + E.n_xi == 0) return;
 #if FCSG_CUDA
-    exchange_kernel<<<grid_for(E.n_x), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
+    exchange_kernel<<<grid_for(E.n_x + E.n_xi), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E);
 #else
     (void)stream;
     exchange_body(Thr{0, 1}, 0, 1, E);

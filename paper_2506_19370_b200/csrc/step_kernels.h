@@ -54,23 +54,30 @@ struct BcDev {
     double pressure;
 };
 
+// Device view of the engine's data. The engine stores subpatches grouped by
+// shape (every field one array over all points, [slot][j][i] per subpatch);
+// a *group view* covers the subpatches of one shape (S, ni, nj set, every
+// pointer offset to the group's first point / subpatch / line), the *global
+// view* covers all points (S = all subpatches, ni = nj = 0) and is used by the
+// kernels that never need a point's (i, j): blend, exchange, dt, advance,
+// halo pack/unpack and the proxy.
 struct EngineDev {
-    int S, ni, nj;  // subpatches of one uniform rectangular shape
-    int cartesian;  // 1: iq2x == iq1y == 0 at every point (axis-aligned maps)
+    int S, ni, nj;
+    int sub_base;   // storage slot of the view's first subpatch (error reports)
+    int cartesian;  // 1: iq2x == iq1y == 0 at every point of the view
     int reference_order;  // 1: euler_rhs's own accumulation order (3 passes); 0: flux form
-    long npts;      // S * ni * nj (< 2^31)
-    FastDiv div_ni, div_sz;  // by ni and by ni * nj (point index -> subpatch, row)
+    long npts;      // points of the view (< 2^31)
+    FastDiv div_ni, div_sz;  // by ni and by ni * nj (group views)
     double cfl, T;
     double visc_c[4];
     double abs_floor;
     int smear_radius;
-    // per-subpatch
-    const double* inv_len1;  // S
-    const double* inv_len2;  // S
-    const int* sub_i0;       // S: global lattice origin (error reports)
-    const int* sub_j0;
-    const int* sub_patch;
-    const BcDev* bc_row_lo;  // S * nj
+    // per subpatch
+    const double* h1;        // S: lattice spacing along q1 (LineInfo::inv_len = 1/((n-1) h1))
+    const double* h2;
+    const int* cut_i;        // S: L-shaped subpatch: points (i < cut_i && j < cut_j) are not
+    const int* cut_j;        //    in the set (local, 0 = rectangular; geom::Subpatch::valid)
+    const BcDev* bc_row_lo;  // S * nj (group view)
     const BcDev* bc_row_hi;
     const BcDev* bc_col_lo;  // S * ni
     const BcDev* bc_col_hi;
@@ -91,19 +98,54 @@ struct EngineDev {
     double* tS4[4];  // mu * grad_x w
     double* tS5[4];  // mu * grad_y w
     double* tF[4];   // filter/smear row results
-    // viscosity blend plan, CSR by recipient point
+    // viscosity blend plan, CSR by recipient point (global view): copies,
+    // then 6x6 tensor Lagrange interpolations (w, wx[6], wy[6] per entry)
     const int* visc_off;     // npts + 1
     const long* visc_src;    // global point index of donor
     const double* visc_w;
-    // fringe exchange (copies): dst/src global point indices
+    const int* vi_off;       // npts + 1
+    const long* vi_src;      // global index of the donor stencil origin (si0, sj0)
+    const int* vi_pitch;     // donor ni
+    const double* vi_w;      // 13 per entry: wx[6], wy[6], w
+    // fringe exchange (global view): copies dst <- src, then interpolations
     const long* x_dst;
     const long* x_src;
     long n_x;
+    const long* xi_dst;
+    const long* xi_src;      // donor stencil origin
+    const int* xi_pitch;
+    const double* xi_w;      // 12 per entry: wx[6], wy[6]
+    long n_xi;
     // classifier weights
     const double* mlp;       // kMlpWeights, FCNN order (per layer W row-major, then b)
     const double* mlp_frag;  // kMlpFrags x 32: per-lane DMMA operand fragments (mlp_mma_fragments)
     const double* tanh_tab;  // tanh(k/64), k = 0..1280 (classifier tanh table)
     StepScalars* sc;
+};
+
+// A run of consecutive lines of one subpatch that starts at `begin` along the
+// line (L-shaped subpatches: rows j < cut_j begin at cut_i): one CTA's lines
+// when a line set is given by descriptors.
+struct LineDesc {
+    int sub, line0, nl, begin;
+};
+
+// One launch's set of lines of one length n and orientation: FC plan and,
+// for groups with L-shaped subpatches, descriptor lists for 4 and 8 lines
+// per CTA (null: every line of every subpatch of the view, begin 0).
+struct LineSet {
+    FcPlanDev pl;
+    int scr;
+    const LineDesc* desc4;
+    int n4;
+    const LineDesc* desc8;
+    int n8;
+};
+
+// everything the launchers need for one shape group
+struct GroupLaunch {
+    EngineDev E;
+    std::vector<LineSet> rows, cols;
 };
 
 // The classifier on the FP64 tensor cores (mma.m8n8k4.f64): per warp, 8
@@ -114,31 +156,26 @@ constexpr int kMlpFrags = 50;
 constexpr int kTanhTable = 1281;  // tanh(k/64), k = 0..1280
 std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
 
-// FC plans for the two line orientations (rows: n = ni, cols: n = nj)
-struct LinePlans {
-    FcPlanDev row, col;
-    int scr_row, scr_col;
-};
-
 int step_scr_cap(const FcPlanDev& pl);
-void launch_phase0(const EngineDev& E, bool step0, void* stream);
-void launch_phase1(const EngineDev& E, void* stream);
-void launch_phase2(const EngineDev& E, const LinePlans& P, bool step0, void* stream);
-void launch_stage(const EngineDev& E, const LinePlans& P, int stage, void* stream);
-// the three line passes of a stage, separately (profiling hooks)
-void launch_pass_a(const EngineDev& E, const LinePlans& P, void* stream);
-void launch_pass_b(const EngineDev& E, const LinePlans& P, int stage, void* stream);
-void launch_pass_c(const EngineDev& E, const LinePlans& P, int stage, void* stream);
-// line-pass launches per stage (2 for the Cartesian flux form, else 3)
-int stage_launches(const EngineDev& E);
+// phase 0: proxy over all points (global view), classifier per group
+void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream);
+void launch_phase1(const EngineDev& Eall, void* stream);
+void launch_phase2(const std::vector<GroupLaunch>& G, bool step0, void* stream);
+void launch_stage(const std::vector<GroupLaunch>& G, int stage, void* stream);
+// the line passes of a stage, separately (profiling hooks)
+void launch_pass_a(const std::vector<GroupLaunch>& G, void* stream);
+void launch_pass_b(const std::vector<GroupLaunch>& G, int stage, void* stream);
+void launch_pass_c(const std::vector<GroupLaunch>& G, int stage, void* stream);
+// line-pass launches per stage (2 per line set for the Cartesian flux form, else 3)
+int stage_launches(const std::vector<GroupLaunch>& G);
 // kernel launches per superstep (excluding the t=0 dilation)
-inline int launches_per_step(const EngineDev& E) { return 18 + 5 * stage_launches(E); }
-void launch_bc(const EngineDev& E, void* stream);
-void launch_exchange(const EngineDev& E, void* stream);
-void launch_finalize_dt(const EngineDev& E, void* stream);
-void launch_advance(const EngineDev& E, void* stream);
+int launches_per_step(const std::vector<GroupLaunch>& G);
+void launch_bc(const std::vector<GroupLaunch>& G, void* stream);
+void launch_exchange(const EngineDev& Eall, void* stream);
+void launch_finalize_dt(const EngineDev& Eall, void* stream);
+void launch_advance(const EngineDev& Eall, void* stream);
 // halo pack/unpack (which: 0 state e as [k][4], 1 mu_hat as [k])
-void launch_pack(const EngineDev& E, int which, const long* idx, long n, double* buf, void* stream);
-void launch_unpack(const EngineDev& E, int which, long n, const double* buf, void* stream);
+void launch_pack(const EngineDev& Eall, int which, const long* idx, long n, double* buf, void* stream);
+void launch_unpack(const EngineDev& Eall, int which, long n, const double* buf, void* stream);
 
 }  // namespace fcsg

@@ -78,9 +78,9 @@ class Engine:
         h = C.c_void_p()
         ctx.check(L.fcsg_engine_create(ctx.h, C.byref(c), C.byref(h)))
         self.h = h
-        self.shape = (dec.subs[0].nj, dec.subs[0].ni)
         subs = dec.subs if rank_plan is None else [dec.subs[g] for g in rank_plan.local]
         self.subs = subs
+        self.shapes = [(d.nj, d.ni) for d in subs]
         for d in subs:
             kind, state, press = _bc_arrays(d)
             arr = [np.ascontiguousarray(a, dtype=np.float64) for a in
@@ -88,7 +88,8 @@ class Engine:
             mask = np.ascontiguousarray(d.mask, dtype=np.uint8)
             sid = C.c_int()
             ctx.check(L.fcsg_engine_add_subpatch(
-                h, d.patch, d.sp.i0, d.sp.j0, d.ni, d.nj, d.h1, d.h2, mask.ctypes.data_as(C.POINTER(C.c_uint8)),
+                h, d.patch, d.sp.i0, d.sp.j0, d.ni, d.nj, getattr(d, "cut_i", 0), getattr(d, "cut_j", 0), d.h1, d.h2,
+                mask.ctypes.data_as(C.POINTER(C.c_uint8)),
                 *[N.dptr(a) for a in arr], kind.ctypes.data_as(N.ip), N.dptr(state), N.dptr(press), C.byref(sid)))
         pl = dec.plan if rank_plan is None else rank_plan.plan
         if rank_plan is not None:
@@ -104,6 +105,15 @@ class Engine:
         vw = np.ascontiguousarray(pl.v_w, dtype=np.float64)
         ctx.check(L.fcsg_engine_set_plan(h, len(keep[0]), *[k.ctypes.data_as(N.ip) for k in keep[:4]],
                                          len(keep[4]), *[k.ctypes.data_as(N.ip) for k in keep[4:]], N.dptr(vw)))
+        for which, ip_ in ((0, getattr(pl, "sol_interps", None)), (1, getattr(pl, "visc_interps", None))):
+            if ip_ is None or len(ip_["dst"]) == 0:
+                continue
+            ints = [np.ascontiguousarray(ip_[k], dtype=np.int32) for k in ("dst_sub", "dst", "src_sub", "si0", "sj0")]
+            wx = np.ascontiguousarray(ip_["wx"], dtype=np.float64)
+            wy = np.ascontiguousarray(ip_["wy"], dtype=np.float64)
+            w = np.ascontiguousarray(ip_.get("w", np.ones(len(ints[0]))), dtype=np.float64)
+            ctx.check(L.fcsg_engine_set_plan_interps(h, which, len(ints[0]), *[a.ctypes.data_as(N.ip) for a in ints],
+                                                     N.dptr(wx), N.dptr(wy), N.dptr(w)))
         ctx.check(L.fcsg_engine_load_mlp(h, cfg.weights.encode()))
         ctx.check(L.fcsg_engine_finalize(h))
         if initial_states is None and ic is not None and rank_plan is None:
@@ -130,7 +140,8 @@ class Engine:
         self.ctx.check(self.ctx.lib.fcsg_engine_set_state(self.h, sub, N.dptr(e)))
 
     def set_state_bulk(self, e):
-        """all subpatches, [4][S][nj][ni]; ``e`` may be a numpy array or a
+        """all subpatches, [4][sum of points] (per component the subpatches in
+        id order, each [nj][ni]; [4][S][nj][ni] for one shape); ``e`` may be a numpy array or a
         (pinned) CPU torch tensor"""
         ptr = e.data_ptr() if hasattr(e, "data_ptr") else np.ascontiguousarray(e, dtype=np.float64).ctypes.data
         self.ctx.check(self.ctx.lib.fcsg_engine_set_state_bulk(self.h, C.c_void_p(ptr)))
@@ -141,7 +152,7 @@ class Engine:
         return out
 
     def get(self, sub, name, comp=0):
-        out = np.empty(self.shape)
+        out = np.empty(self.shapes[sub])
         self.ctx.check(self.ctx.lib.fcsg_engine_get_field(self.h, sub, name.encode(), comp, N.dptr(out)))
         return out
 

@@ -195,11 +195,17 @@ class SubData:
     bc_row_hi: list = None
     bc_col_lo: list = None
     bc_col_hi: list = None
+    # L-shaped subpatch (geom::Subpatch::i_cut/j_cut, local): points
+    # (i < cut_i and j < cut_j) are not in the set
+    cut_i: int = 0
+    cut_j: int = 0
 
 
 @dataclass
 class Plan:
-    """CommPlan copies (include/fcs/runtime.hpp:16-49)."""
+    """CommPlan (include/fcs/runtime.hpp:16-49): copies, and optionally the
+    6x6 interpolations as dicts of arrays (dst_sub, dst, src_sub, si0, sj0,
+    wx (n, 6), wy (n, 6); plus w for the viscosity blend)."""
 
     sol_dst_sub: np.ndarray
     sol_dst: np.ndarray
@@ -210,6 +216,8 @@ class Plan:
     v_src_sub: np.ndarray
     v_src: np.ndarray
     v_w: np.ndarray
+    sol_interps: dict = None
+    visc_interps: dict = None
 
     def per_sub(self, nsub):
         """oracle-friendly view: per recipient (dst, src_sub, src) and (..., w)."""
