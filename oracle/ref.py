@@ -44,6 +44,14 @@ def lib():
         L.ref_engine_affine.restype = C.c_void_p
         L.ref_engine_affine.argtypes = [C.c_double] * 6 + [C.c_int] * 4 + [ip, dp, dp, C.c_double, C.c_double,
                                                                             C.c_int, C.c_char_p, C.c_long]
+        L.ref_engine_problem.restype = C.c_void_p
+        L.ref_engine_problem.argtypes = [C.c_char_p, C.c_double, C.c_double, C.c_double, C.c_int, C.c_char_p,
+                                         C.c_long]
+        L.ref_engine_testgeom.restype = C.c_void_p
+        L.ref_engine_testgeom.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_char_p]
+        L.ref_engine_sub_info.argtypes = [C.c_void_p, C.c_int, ip, dp]
+        L.ref_engine_lines.argtypes = [C.c_void_p, C.c_int, ip, ip, dp, ip, dp, ip, dp]
+        L.ref_engine_plan.argtypes = [C.c_void_p, C.c_int, C.c_int, ip, ip, dp, ip, dp]
         L.ref_engine_destroy.argtypes = [C.c_void_p]
         L.ref_engine_nsubs.argtypes = [C.c_void_p]
         L.ref_engine_dims.argtypes = [C.c_void_p, C.c_int, ip, ip]
@@ -165,6 +173,78 @@ class RefEngine:
             a, b = C.c_int(), C.c_int()
             _check(lib().ref_engine_dims(h, k, C.byref(a), C.byref(b)))
             self.dims.append((a.value, b.value))
+
+    @classmethod
+    def problem(cls, name, target_h=0.0, cfl=0.0, T=0.0, workers=1, weight_path="", max_steps=10**9):
+        """A named problem of the reference's workbench (src/problems.cpp:379-388)
+        with its own initial condition applied."""
+        self = cls.__new__(cls)
+        h = lib().ref_engine_problem(name.encode(), target_h, cfl, T, workers, weight_path.encode(), max_steps)
+        if not h:
+            _check(9)
+        self.h = h
+        self.nsubs = lib().ref_engine_nsubs(h)
+        self.dims = []
+        for k in range(self.nsubs):
+            a, b = C.c_int(), C.c_int()
+            _check(lib().ref_engine_dims(h, k, C.byref(a), C.byref(b)))
+            self.dims.append((a.value, b.value))
+        return self
+
+    @classmethod
+    def testgeom(cls, which, n0=30, nv=9, cfl=0.5, workers=1, weight_path=""):
+        """Test geometries through the reference's geometry API (ref_export.cpp
+        ref_engine_testgeom): 0 annulus, 1 two patches with interpolation,
+        2 C1 corner patch (L-shaped subpatch)."""
+        self = cls.__new__(cls)
+        h = lib().ref_engine_testgeom(which, n0, nv, cfl, workers, weight_path.encode())
+        if not h:
+            _check(9)
+        self.h = h
+        self.nsubs = lib().ref_engine_nsubs(h)
+        self.dims = []
+        for k in range(self.nsubs):
+            a, b = C.c_int(), C.c_int()
+            _check(lib().ref_engine_dims(h, k, C.byref(a), C.byref(b)))
+            self.dims.append((a.value, b.value))
+        return self
+
+    def sub_info(self, sub):
+        """dict: patch, i0, j0, ni, nj, cut_i, cut_j (local), periodic1, kind, h1, h2"""
+        info = np.zeros(9, dtype=np.int32)
+        hh = np.zeros(2)
+        _check(lib().ref_engine_sub_info(self.h, sub, info.ctypes.data_as(C.POINTER(C.c_int)), _dp(hh)))
+        keys = ("patch", "i0", "j0", "ni", "nj", "cut_i", "cut_j", "periodic1", "kind")
+        d = {k: int(v) for k, v in zip(keys, info)}
+        d["h1"], d["h2"] = float(hh[0]), float(hh[1])
+        return d
+
+    def lines(self, sub):
+        """LineInfo of rows then columns: begin, n, inv_len, (kind, state[4],
+        pressure) of the low and high ends"""
+        ni, nj = self.dims[sub]
+        m = ni + nj
+        ip_ = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+        begin, n = np.zeros(m, np.int32), np.zeros(m, np.int32)
+        inv = np.zeros(m)
+        klo, khi = np.zeros(m, np.int32), np.zeros(m, np.int32)
+        blo, bhi = np.zeros((m, 5)), np.zeros((m, 5))
+        _check(lib().ref_engine_lines(self.h, sub, ip_(begin), ip_(n), _dp(inv), ip_(klo), _dp(blo), ip_(khi),
+                                      _dp(bhi)))
+        return dict(begin=begin, n=n, inv_len=inv, kind_lo=klo, bc_lo=blo, kind_hi=khi, bc_hi=bhi)
+
+    def plan(self, sub, which):
+        """(copies (n, 3) dst/src_sub/src, copy_w, interps (m, 4) dst/src_sub/si0/sj0,
+        interp_w (m, 13) wx[6], wy[6], w) of recipient `sub`; which 0 solution, 1 viscosity"""
+        cnt = np.zeros(2, np.int32)
+        ip_ = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+        _check(lib().ref_engine_plan(self.h, sub, which, ip_(cnt), None, None, None, None))
+        cp = np.zeros((cnt[0], 3), np.int32)
+        cw = np.zeros(cnt[0])
+        it = np.zeros((cnt[1], 4), np.int32)
+        iw = np.zeros((cnt[1], 13))
+        _check(lib().ref_engine_plan(self.h, sub, which, ip_(cnt), ip_(cp), _dp(cw), ip_(it), _dp(iw)))
+        return cp, cw, it, iw
 
     def __del__(self):
         if getattr(self, "h", None):

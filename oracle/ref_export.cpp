@@ -10,6 +10,9 @@
  *   ref_blend_matrix  -> fc::FcOperator::blend_matrix      (fc_core.cpp:156-163)
  *   ref_fc_*          -> fc::OperatorCache::get + FcOperator (fc_core.cpp:190-306,391-402)
  *   ref_engine_*      -> run::Engine init/step_phase/run    (runtime.cpp:293-530)
+ *   ref_engine_problem -> wb::get_problem (problems.cpp:379-388), and the
+ *                        SubpatchData / CommPlan exporters (sub_info, lines,
+ *                        plan) that feed the same geometry and plan to the product
  *   ref_train_classifier -> visc::train_classifier + MlpClassifier::save
  *                                                           (viscosity.cpp:91-106,364-513)
  */
@@ -36,6 +39,7 @@
 #define private public
 #include "fcs/runtime.hpp"
 #undef private
+#include "fcs/workbench.hpp"  // after runtime.hpp, which it includes
 
 using namespace fcs;
 
@@ -284,6 +288,235 @@ void* ref_engine_rect(double x0, double y0, double lx, double ly, int r, int s, 
                       double cfl, double T, int workers, const char* weight_path, long max_steps) {
     return ref_engine_affine(x0, y0, lx, 0.0, 0.0, ly, r, s, n0, nv, side_kinds, side_states, side_pressure, cfl, T,
                              workers, weight_path, max_steps);
+}
+
+/* A named problem of the reference's workbench (flow-cylinder, wedge, prism,
+ * riemann4, sod, ...) with its own initial condition applied by
+ * Engine::init; cfl / T <= 0 keep the problem's values. */
+void* ref_engine_problem(const char* name, double target_h, double cfl, double T, int workers,
+                         const char* weight_path, long max_steps) {
+    RefEngine* out = nullptr;
+    guard([&] {
+        wb::ProblemSpec ps = wb::get_problem(name, target_h);
+        run::EngineConfig cfg;
+        cfg.cfl = cfl > 0 ? cfl : ps.cfl;
+        cfg.T = T > 0 ? T : ps.T;
+        cfg.workers = workers;
+        cfg.max_steps = max_steps;
+        if (weight_path && weight_path[0]) {
+            cfg.classifier.variant = visc::ClassifierConfig::Variant::ann;
+            cfg.classifier.weight_path = weight_path;
+        }
+        auto re = std::make_unique<RefEngine>();
+        re->eng = std::make_unique<run::Engine>(std::move(ps.dec), std::move(ps.bcs), ps.ic, cfg);
+        re->eng->init();
+        out = re.release();
+    });
+    return out;
+}
+
+/* Test geometries built through the reference's own geometry API (its named
+ * multi-patch problems -- flow-cylinder, wedge, prism, shock-cylinder-matrix
+ * -- fail their own minimum-overlap / window checks):
+ *   0  annulus: one periodic S patch (AnnulusMap, r 0.5..1), 3 subpatches,
+ *      curved no-slip wall inside, zero_normal_all outside
+ *   1  two patches with non-coincident lattices: a Cartesian I patch and a
+ *      bilinear S patch overlapping it (6x6 Lagrange interpolation both ways),
+ *      slip walls, inflow, supersonic outflow
+ *   2  a C1 corner patch alone (CurveSumMap of two non-orthogonal segments,
+ *      subdivide_L: one L-shaped subpatch), slip walls at the reentrant
+ *      corner; the overlap validation that asks for an S patch at the corner
+ *      is skipped (every fringe point of the lone patch is intra-patch)
+ * n0: points per preliminary cell (n1 for the C1 patch); IC: uniform flow
+ * plus a Gaussian density bump, applied by Engine::init. */
+void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, const char* weight_path) {
+    RefEngine* out = nullptr;
+    guard([&] {
+        using geom::Patch;
+        using geom::PatchKind;
+        using geom::SideInfo;
+        const SideInfo interior{false, ""};
+        geom::DomainDecomposition dec;
+        dec.nv = nv;
+        dec.n0 = n0;
+        BcTable bcs;
+        BcSpec slip;
+        slip.kind = BcKind::slip_wall;
+        BcSpec noslip;
+        noslip.kind = BcKind::noslip_adiabatic;
+        BcSpec zn;
+        zn.kind = BcKind::zero_normal_all;
+        BcSpec sup;
+        sup.kind = BcKind::supersonic_outflow;
+        BcSpec in;
+        in.kind = BcKind::inflow;
+        in.state = euler::conservative(1.0, 0.5, 0.0, 0.7);
+        bcs["wall"] = slip;
+        bcs["cyl"] = noslip;
+        bcs["outer"] = zn;
+        bcs["out"] = sup;
+        bcs["in"] = in;
+        Vec2 bump{0.0, 0.0};
+        double u0 = 0.5, v0 = 0.0;
+        if (which == 0) {
+            Patch ring;
+            ring.kind = PatchKind::S;
+            ring.map = std::make_shared<geom::AnnulusMap>(Vec2{0.0, 0.0}, 0.5, 1.0, -M_PI, 2 * M_PI);
+            ring.periodic1 = true;
+            ring.sides = {interior, interior, SideInfo{true, "cyl"}, SideInfo{true, "outer"}};
+            dec.patches.push_back(std::move(ring));
+            bump = {0.75, 0.0};
+            u0 = 0.2;
+            v0 = 0.1;
+        } else if (which == 1) {
+            Patch a;
+            a.kind = PatchKind::I;
+            a.map = std::make_shared<geom::AffineMap>(Vec2{0.0, 0.0}, Vec2{1.0, 0.0}, Vec2{0.0, 1.05});
+            a.sides = {SideInfo{true, "in"}, interior, SideInfo{true, "wall"}, SideInfo{true, "wall"}};
+            dec.patches.push_back(std::move(a));
+            Patch b;
+            b.kind = PatchKind::S;
+            // a trapezoid: walls continue A's walls through the overlap, the
+            // outflow side is slanted (non-constant Jacobian)
+            b.map = std::make_shared<geom::BilinearMap>(Vec2{0.5, 0.0}, Vec2{1.8, 0.0}, Vec2{0.5, 1.05},
+                                                        Vec2{1.5, 1.05});
+            b.sides = {interior, SideInfo{true, "out"}, SideInfo{true, "wall"}, SideInfo{true, "wall"}};
+            dec.patches.push_back(std::move(b));
+            bump = {0.85, 0.5};
+        } else if (which == 2) {
+            const Vec2 c{0.5, 0.5};
+            const double arm = 0.3, ang = 70.0 * M_PI / 180.0;
+            const Vec2 da{1.0, 0.0}, db{std::cos(ang), std::sin(ang)};
+            auto ellA = std::make_shared<geom::Segment>(c + arm * da, c - arm * da);
+            auto ellB = std::make_shared<geom::Segment>(c + arm * db, c - arm * db);
+            Patch p = geom::build_c1_patch(ellA, ellB, c, "wall");
+            for (auto& sd : p.sides) sd = SideInfo{true, "outer"};
+            dec.patches.push_back(std::move(p));
+            bump = {0.6, 0.6};
+            u0 = 0.3;
+            v0 = 0.2;
+        } else {
+            throw UsageError("unknown test geometry");
+        }
+        for (size_t k = 0; k < dec.patches.size(); ++k) dec.patches[k].index = static_cast<int>(k);
+        for (auto& p : dec.patches) {
+            if (p.kind == PatchKind::C1)
+                geom::subdivide_L(p, 2, n0, nv);
+            else if (p.periodic1)
+                geom::subdivide_Q(p, 3, 1, n0, nv);
+            else if (p.index == 1)
+                geom::subdivide_Q(p, 2, 1, n0 + 6, nv);  // a different lattice and subpatch shape
+            else
+                geom::subdivide_Q(p, 1, 1, n0, nv);
+        }
+        dec.assign_global_ids();
+        run::EngineConfig cfg;
+        cfg.cfl = cfl;
+        cfg.T = 1e300;
+        cfg.workers = workers;
+        // a lone C1 patch has no S patch at its corner; its plan is complete
+        // without one (every fringe point is intra-patch)
+        if (which == 2) cfg.validate_overlap = false;
+        if (weight_path && weight_path[0]) {
+            cfg.classifier.variant = visc::ClassifierConfig::Variant::ann;
+            cfg.classifier.weight_path = weight_path;
+        }
+        auto ic = [bump, u0, v0](double x, double y) {
+            const double r2 = (x - bump.x) * (x - bump.x) + (y - bump.y) * (y - bump.y);
+            const double rho = 1.0 + 0.2 * std::exp(-r2 / 0.02);
+            return euler::conservative(rho, u0, v0, 0.7);
+        };
+        auto re = std::make_unique<RefEngine>();
+        re->eng = std::make_unique<run::Engine>(std::move(dec), std::move(bcs), ic, cfg);
+        re->eng->init();
+        out = re.release();
+    });
+    return out;
+}
+
+/* info[9] = patch index, i0, j0, ni, nj, cut_i, cut_j (local; 0 = rectangle),
+ * periodic1, patch kind; hh[2] = h1, h2 (geom::Patch / Subpatch) */
+int ref_engine_sub_info(void* h, int id, int* info, double* hh) {
+    return guard([&] {
+        const auto& d = static_cast<RefEngine*>(h)->eng->subs().at(id);
+        const auto& sp = *d.sp;
+        const auto& p = *d.patch;
+        info[0] = p.index;
+        info[1] = sp.i0;
+        info[2] = sp.j0;
+        info[3] = d.ni;
+        info[4] = d.nj;
+        const bool l = sp.i_cut > sp.i0 && sp.j_cut > sp.j0;
+        info[5] = l ? sp.i_cut - sp.i0 : 0;
+        info[6] = l ? sp.j_cut - sp.j0 : 0;
+        info[7] = p.periodic1 ? 1 : 0;
+        info[8] = static_cast<int>(p.kind);
+        hh[0] = p.h1;
+        hh[1] = p.h2;
+    });
+}
+
+/* LineInfo tables (include/fcs/subpatch_data.hpp:34-43): per line (rows then
+ * columns) begin, n, inv_len, and the resolved BC of both ends: kind (-1 none,
+ * else the BcKind order), state[4], pressure. Arrays sized nj + ni. */
+int ref_engine_lines(void* h, int id, int* begin, int* n, double* inv_len, int* kind_lo, double* bc_lo, int* kind_hi,
+                     double* bc_hi) {
+    return guard([&] {
+        const auto& d = static_cast<RefEngine*>(h)->eng->subs().at(id);
+        int k = 0;
+        auto put = [&](const SubpatchData::LineInfo& li) {
+            begin[k] = li.begin;
+            n[k] = li.n;
+            inv_len[k] = li.inv_len;
+            const BcSpec* b[2] = {li.bc_lo, li.bc_hi};
+            int* kk[2] = {kind_lo, kind_hi};
+            double* bb[2] = {bc_lo, bc_hi};
+            for (int e = 0; e < 2; ++e) {
+                kk[e][k] = b[e] ? static_cast<int>(b[e]->kind) : -1;
+                for (int c = 0; c < 4; ++c) bb[e][5 * k + c] = b[e] ? b[e]->state[c] : 0.0;
+                bb[e][5 * k + 4] = b[e] ? b[e]->pressure : 1.0;
+            }
+            ++k;
+        };
+        for (const auto& li : d.rows) put(li);
+        for (const auto& li : d.cols) put(li);
+    });
+}
+
+/* CommPlan entries of recipient `id` (include/fcs/runtime.hpp:16-49); which
+ * 0 = solution, 1 = viscosity. counts[2] = copies, interps. With non-null
+ * arrays: copies (dst, src_sub, src) + copy_w; interps (dst, src_sub, si0,
+ * sj0) + interp_w (wx[6], wy[6], w). */
+int ref_engine_plan(void* h, int id, int which, int* counts, int* copies, double* copy_w, int* interps,
+                    double* interp_w) {
+    return guard([&] {
+        const auto& plan = static_cast<RefEngine*>(h)->eng->plan();
+        const auto& pe = (which == 0 ? plan.solution : plan.visc).at(id);
+        counts[0] = static_cast<int>(pe.copies.size());
+        counts[1] = static_cast<int>(pe.interps.size());
+        if (copies) {
+            for (size_t k = 0; k < pe.copies.size(); ++k) {
+                copies[3 * k] = pe.copies[k].dst;
+                copies[3 * k + 1] = pe.copies[k].src_sub;
+                copies[3 * k + 2] = pe.copies[k].src;
+                copy_w[k] = pe.copies[k].w;
+            }
+        }
+        if (interps) {
+            for (size_t k = 0; k < pe.interps.size(); ++k) {
+                const auto& e = pe.interps[k];
+                interps[4 * k] = e.dst;
+                interps[4 * k + 1] = e.src_sub;
+                interps[4 * k + 2] = e.si0;
+                interps[4 * k + 3] = e.sj0;
+                for (int a = 0; a < 6; ++a) {
+                    interp_w[13 * k + a] = e.wx[a];
+                    interp_w[13 * k + 6 + a] = e.wy[a];
+                }
+                interp_w[13 * k + 12] = e.w;
+            }
+        }
+    });
 }
 
 void ref_engine_destroy(void* h) { delete static_cast<RefEngine*>(h); }
