@@ -79,7 +79,26 @@ int guard(Ctx* c, F&& f) {
 }
 
 int pick_lb(long n_lines, int n_ext) {
-    // enough CTAs to cover the 148 SMs at least twice, shared memory permitting
+    // Complex lines per CTA. The compile-time plans (n_ext 280, 536) run three
+    // 256-thread CTAs per SM: pick the LB whose grid fills its last wave of
+    // 3 x 148 CTAs best (a 1.15-wave grid costs two CTA lifetimes), the
+    // smaller LB on ties. Runtime plans: enough CTAs for two per SM,
+    // shared memory permitting.
+    if (n_ext == 280 || n_ext == 536) {
+        const long slots = 3L * 148;
+        int best = 4;
+        double best_fill = -1.0;
+        for (int lb : {4, 5, 6, 8}) {
+            const long nblk = (n_lines + 2 * lb - 1) / (2 * lb);
+            const long waves = (nblk + slots - 1) / slots;
+            const double fill = waves > 0 ? static_cast<double>(nblk) / (waves * slots) : 0.0;
+            if (fill > best_fill + 1e-9) {
+                best_fill = fill;
+                best = lb;
+            }
+        }
+        return best;
+    }
     int lb = 16;
     while (lb > 4 && (n_lines + 2 * lb - 1) / (2 * lb) < 296) lb /= 2;
     while (lb > 4 && static_cast<long>(n_ext) * (lb + 1) * 16 > 96 * 1024) lb /= 2;

@@ -105,6 +105,8 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     switch (LB) {
         case 4: launch_fc_lines_lb<4>(a, nblk, smem, s); break;
+        case 5: launch_fc_lines_lb<5>(a, nblk, smem, s); break;
+        case 6: launch_fc_lines_lb<6>(a, nblk, smem, s); break;
         case 8: launch_fc_lines_lb<8>(a, nblk, smem, s); break;
         default: launch_fc_lines_lb<16>(a, nblk, smem, s); break;
     }

@@ -1247,70 +1247,114 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
         : "d"(a), "d"(b));
 }
 
-// Class 1..4 of the stencil held by this lane's quad, returned on all four
-// lanes; every lane of the warp calls. s_a, s_b are window values t and 4 + t
-// (s_b unused for t = 3); inactive quads get 4. normalize_stencil's min, max,
-// guard and 2 (s - lo) / span - 1 are computed exactly as the reference's
-// (src/viscosity.cpp:48-59).
-__device__ int classify_mma(const double* fr, const double* tab, double s_a, double s_b, bool active, double abs_floor,
-                            int lane) {
+// Classes 1..4 of NG independent stencil sets (each: the stencil held by this
+// lane's quad), returned on all four lanes of the quad; every lane of the warp
+// calls. s_a, s_b are window values t and 4 + t (s_b unused for t = 3);
+// inactive quads get 4. normalize_stencil's min, max, guard and
+// 2 (s - lo) / span - 1 are computed exactly as the reference's
+// (src/viscosity.cpp:48-59). The NG sets are interleaved so every thread has
+// 4 NG independent tanh chains per layer.
+template <int NG>
+__device__ void classify_mma(const double* fr, const double* tab, const double* s_a, const double* s_b,
+                             const bool* active, double abs_floor, int lane, int* cls) {
     constexpr unsigned kAll = 0xffffffffu;
     const int t = lane & 3;
     const bool has_b = t < 3;
-    double lo = s_a, hi = s_a;
-    if (has_b) {
-        lo = s_b < lo ? s_b : lo;
-        hi = s_b > hi ? s_b : hi;
-    }
+    double a0[NG], a1[NG];
+    bool guard[NG];
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-        const double l2 = __shfl_xor_sync(kAll, lo, o), h2 = __shfl_xor_sync(kAll, hi, o);
-        lo = l2 < lo ? l2 : lo;
-        hi = h2 > hi ? h2 : hi;
-    }
-    const double span = hi - lo;
-    double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
-    scale = scale > 1e-100 ? scale : 1e-100;
-    const bool guard = !active || span <= 1e-13 * scale || span <= abs_floor;
-    const double sp = guard ? 1.0 : span;
-    const double a0 = guard ? 0.0 : 2.0 * (s_a - lo) / sp - 1.0;
-    const double a1 = (guard || !has_b) ? 0.0 : 2.0 * (s_b - lo) / sp - 1.0;
-    const double* F = fr + lane;
-    double h[4];
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-        double d0 = F[(32 + nt * 2) * 32], d1 = F[(33 + nt * 2) * 32];
-        dmma(d0, d1, a0, F[(nt * 2) * 32]);
-        dmma(d0, d1, a1, F[(nt * 2 + 1) * 32]);
-        h[nt * 2] = tanh_tab(d0, tab);
-        h[nt * 2 + 1] = tanh_tab(d1, tab);
-    }
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-        double g[4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            double d0 = F[(36 + l * 4 + nt * 2) * 32], d1 = F[(37 + l * 4 + nt * 2) * 32];
-#pragma unroll
-            for (int ks = 0; ks < 4; ++ks) dmma(d0, d1, h[ks], F[(4 + l * 8 + nt * 4 + ks) * 32]);
-            g[nt * 2] = tanh_tab(d0, tab);
-            g[nt * 2 + 1] = tanh_tab(d1, tab);
+    for (int g = 0; g < NG; ++g) {
+        double lo = s_a[g], hi = s_a[g];
+        if (has_b) {
+            lo = s_b[g] < lo ? s_b[g] : lo;
+            hi = s_b[g] > hi ? s_b[g] : hi;
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) h[k] = g[k];
+        for (int o = 1; o <= 2; o <<= 1) {
+            const double l2 = __shfl_xor_sync(kAll, lo, o), h2 = __shfl_xor_sync(kAll, hi, o);
+            lo = l2 < lo ? l2 : lo;
+            hi = h2 > hi ? h2 : hi;
+        }
+        const double span = hi - lo;
+        double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+        scale = scale > 1e-100 ? scale : 1e-100;
+        guard[g] = !active[g] || span <= 1e-13 * scale || span <= abs_floor;
+        const double sp = guard[g] ? 1.0 : span;
+        a0[g] = guard[g] ? 0.0 : 2.0 * (s_a[g] - lo) / sp - 1.0;
+        a1[g] = (guard[g] || !has_b) ? 0.0 : 2.0 * (s_b[g] - lo) / sp - 1.0;
     }
-    double d0 = F[48 * 32], d1 = F[49 * 32];
+    const double* F = fr + lane;
+    double h[NG][4];
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) dmma(d0, d1, h[ks], F[(28 + ks) * 32]);
-    // lane t = 0 holds logits 0, 1 and lane t = 1 logits 2, 3
-    const double l2 = __shfl_xor_sync(kAll, d0, 1), l3 = __shfl_xor_sync(kAll, d1, 1);
-    int best = 0;  // lowest-index argmax (strict >), without a dynamically indexed array
-    double bv = d0;
-    if (d1 > bv) { best = 1; bv = d1; }
-    if (l2 > bv) { best = 2; bv = l2; }
-    if (l3 > bv) best = 3;
-    const int cls = guard ? 4 : best + 1;
-    return __shfl_sync(kAll, cls, lane & ~3);
+    for (int nt = 0; nt < 2; ++nt) {
+        const double b0 = F[(32 + nt * 2) * 32], b1 = F[(33 + nt * 2) * 32];
+        const double w0 = F[(nt * 2) * 32], w1 = F[(nt * 2 + 1) * 32];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            double d0 = b0, d1 = b1;
+            dmma(d0, d1, a0[g], w0);
+            dmma(d0, d1, a1[g], w1);
+            h[g][nt * 2] = d0;
+            h[g][nt * 2 + 1] = d1;
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[g][k] = tanh_tab(h[g][k], tab);
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        double z[NG][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const double b0 = F[(36 + l * 4 + nt * 2) * 32], b1 = F[(37 + l * 4 + nt * 2) * 32];
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                z[g][nt * 2] = b0;
+                z[g][nt * 2 + 1] = b1;
+            }
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const double w = F[(4 + l * 8 + nt * 4 + ks) * 32];
+#pragma unroll
+                for (int g = 0; g < NG; ++g) dmma(z[g][nt * 2], z[g][nt * 2 + 1], h[g][ks], w);
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) h[g][k] = tanh_tab(z[g][k], tab);
+    }
+    double d0[NG], d1[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        d0[g] = F[48 * 32];
+        d1[g] = F[49 * 32];
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+        const double w = F[(28 + ks) * 32];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) dmma(d0[g], d1[g], h[g][ks], w);
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        // lane t = 0 holds logits 0, 1 and lane t = 1 logits 2, 3
+        const double l2 = __shfl_xor_sync(kAll, d0[g], 1), l3 = __shfl_xor_sync(kAll, d1[g], 1);
+        int best = 0;  // lowest-index argmax (strict >), without a dynamically indexed array
+        double bv = d0[g];
+        if (d1[g] > bv) {
+            best = 1;
+            bv = d1[g];
+        }
+        if (l2 > bv) {
+            best = 2;
+            bv = l2;
+        }
+        if (l3 > bv) best = 3;
+        const int c = guard[g] ? 4 : best + 1;
+        cls[g] = __shfl_sync(kAll, c, lane & ~3);
+    }
 }
 
 // window value k of this lane's stencil (row or column window of point (i, j))
@@ -1334,46 +1378,82 @@ __global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_
     const long sz = static_cast<long>(E.ni) * E.nj;
     const long ngroups = (E.npts + 3) / 4;
     const long wstep = static_cast<long>(gridDim.x) * (kMmaThreads / 32);
-    for (long grp = static_cast<long>(blockIdx.x) * (kMmaThreads / 32) + (threadIdx.x >> 5); grp < ngroups;
-         grp += wstep) {
-        const long p = 4 * grp + q;
-        const bool valid = p < E.npts;
-        const unsigned pp = valid ? static_cast<unsigned>(p) : 0u;
+    // window of this lane's stencil in group grp: point p, validity, start
+    struct Win {
+        long p, base;
+        int i, j, st;
+        bool valid, active, inset;
+    };
+    auto window = [&](long grp) {
+        Win w;
+        w.p = 4 * grp + q;
+        w.valid = w.p < E.npts;
+        const unsigned pp = w.valid ? static_cast<unsigned>(w.p) : 0u;
         const unsigned sub = fdiv(E.div_sz, pp);
         const unsigned loc = pp - sub * E.div_sz.d;
-        const int j = static_cast<int>(fdiv(E.div_ni, loc)), i = static_cast<int>(loc) - j * E.ni;
-        const long base = static_cast<long>(sub) * sz;
+        w.j = static_cast<int>(fdiv(E.div_ni, loc));
+        w.i = static_cast<int>(loc) - w.j * E.ni;
+        w.base = static_cast<long>(sub) * sz;
         const int ci = E.cut_i[sub], cj = E.cut_j[sub];
-        const bool inset = !(i < ci && j < cj);  // L-shaped subpatches: row/column segments
-        const int beg = col ? (i < ci ? cj : 0) : (j < cj ? ci : 0);
+        w.inset = !(w.i < ci && w.j < cj);  // L-shaped subpatches: row/column segments
+        const int beg = col ? (w.i < ci ? cj : 0) : (w.j < cj ? ci : 0);
         const int n = (col ? E.nj : E.ni) - beg;
-        const bool active = valid && inset && n >= kMlpIn;
-        int st = (col ? j : i) - beg - kMlpIn / 2;
-        st = beg + (st < 0 ? 0 : (st > n - kMlpIn ? n - kMlpIn : st));
-        double sa = 0.0, sb = 0.0;
-        if (active) {
-            sa = window_at(E.proxy, base, E.ni, col, st, i, j, t);
-            if (t < 3) sb = window_at(E.proxy, base, E.ni, col, st, i, j, 4 + t);
-        }
-        const int c1 = classify_mma(fr, tab, sa, sb, active, E.abs_floor, lane);
-        const int c1o = __shfl_xor_sync(0xffffffffu, c1, 16);
-        const int tau = c1 < c1o ? c1 : c1o;
-        int tr = 4;
-        if (step0) {
-            double ra = 0.0, rb = 0.0;
-            if (active) {
-                ra = window_at(E.e[0], base, E.ni, col, st, i, j, t);
-                if (t < 3) rb = window_at(E.e[0], base, E.ni, col, st, i, j, 4 + t);
-            }
-            const int c2 = classify_mma(fr, tab, ra, rb, active, E.abs_floor, lane);
-            const int c2o = __shfl_xor_sync(0xffffffffu, c2, 16);
-            tr = c2 < c2o ? c2 : c2o;
-        }
-        if (valid && !col && t == 0) {
+        w.active = w.valid && w.inset && n >= kMlpIn;
+        const int st = (col ? w.j : w.i) - beg - kMlpIn / 2;
+        w.st = beg + (st < 0 ? 0 : (st > n - kMlpIn ? n - kMlpIn : st));
+        return w;
+    };
+    auto write = [&](const Win& w, int tau, int tr) {
+        if (w.valid && !col && t == 0) {
+            const long p = w.p;
             E.tau[p] = tau;
             E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
-            if (step0) E.seed[p] = (inset && E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
+            if (step0) E.seed[p] = (w.inset && E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
         }
+    };
+    auto minq = [](int c) {  // min of the row window (quad g) and column window (quad g + 4)
+        const int o = __shfl_xor_sync(0xffffffffu, c, 16);
+        return c < o ? c : o;
+    };
+    const long w0 = static_cast<long>(blockIdx.x) * (kMmaThreads / 32) + (threadIdx.x >> 5);
+    if (step0) {
+        // t = 0: the proxy windows and the density windows of one group together
+        for (long grp = w0; grp < ngroups; grp += wstep) {
+            const Win w = window(grp);
+            double sa[2] = {0.0, 0.0}, sb[2] = {0.0, 0.0};
+            const bool act[2] = {w.active, w.active};
+            if (w.active) {
+                sa[0] = window_at(E.proxy, w.base, E.ni, col, w.st, w.i, w.j, t);
+                sa[1] = window_at(E.e[0], w.base, E.ni, col, w.st, w.i, w.j, t);
+                if (t < 3) {
+                    sb[0] = window_at(E.proxy, w.base, E.ni, col, w.st, w.i, w.j, 4 + t);
+                    sb[1] = window_at(E.e[0], w.base, E.ni, col, w.st, w.i, w.j, 4 + t);
+                }
+            }
+            int c[2];
+            classify_mma<2>(fr, tab, sa, sb, act, E.abs_floor, lane, c);
+            write(w, minq(c[0]), minq(c[1]));
+        }
+        return;
+    }
+    // steady steps: two groups per iteration
+    const long npair = (ngroups + 1) / 2;
+    for (long pr = w0; pr < npair; pr += wstep) {
+        const Win wa = window(2 * pr), wb = window(2 * pr + 1);
+        double sa[2] = {0.0, 0.0}, sb[2] = {0.0, 0.0};
+        const bool act[2] = {wa.active, wb.active};
+        if (wa.active) {
+            sa[0] = window_at(E.proxy, wa.base, E.ni, col, wa.st, wa.i, wa.j, t);
+            if (t < 3) sb[0] = window_at(E.proxy, wa.base, E.ni, col, wa.st, wa.i, wa.j, 4 + t);
+        }
+        if (wb.active) {
+            sa[1] = window_at(E.proxy, wb.base, E.ni, col, wb.st, wb.i, wb.j, t);
+            if (t < 3) sb[1] = window_at(E.proxy, wb.base, E.ni, col, wb.st, wb.i, wb.j, 4 + t);
+        }
+        int c[2];
+        classify_mma<2>(fr, tab, sa, sb, act, E.abs_floor, lane, c);
+        write(wa, minq(c[0]), 4);
+        write(wb, minq(c[1]), 4);
     }
 }
 #endif
