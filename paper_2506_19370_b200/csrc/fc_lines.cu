@@ -3,8 +3,9 @@
 // One CTA owns LB complex lines = 2*LB real lines; real lines (2a, 2a+1) are
 // packed as one complex line, transformed with fc_transform (fft_line.h), and
 // unpacked. Loads/stores are coalesced along whichever axis is contiguous:
-// along the line for stride==1 (rows), across lines (one 16-byte load per
-// adjacent pair) when line_stride==1 (columns of a row-major field).
+// along the line for stride==1 (rows), across lines when line_stride==1
+// (columns of a row-major field; then thread w takes point w / LB of line
+// w % LB, the shared-memory order).
 #include "fc_lines.h"
 #include "fft_line.h"
 
@@ -13,7 +14,7 @@ namespace fcsg {
 template <int LB, int NE, int NTHR>
 FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a) {
     const FcPlanDev& pl = a.pl;
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;  // line index fastest, no padding: see fft_line.h
     double2* buf = smem;
     double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
     const FcPlanDev spl = stage_tables(Thr{t.tid, NTHR}, pl, a.mode, scr + a.scr_cap);
@@ -22,13 +23,10 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
     const long ls = a.line_stride, st = a.stride;
     const long ols = a.out_line_stride, ost = a.out_stride;
     const int total = N * LB;
-    const bool rows = (st == 1);
-    const bool orows = (ost == 1);
+    const bool rows = (st == 1), orows = (ost == 1);
 #pragma unroll 4
     for (int w = t.tid; w < total; w += NTHR) {
-        int i, c;
-        if (rows) { i = w % N; c = w / N; }
-        else { c = w % LB; i = w / LB; }
+        const int c = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
         const long l = l0 + 2 * c;
         double v0 = 0.0, v1 = 0.0;
         if (l < a.n_lines) v0 = ldg1(a.in + l * ls + i * st);
@@ -40,9 +38,7 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
     else fc_transform(Thr{t.tid, NTHR}, buf, pitch, LB, spl, a.mode, scr, a.scr_cap);
 #pragma unroll 4
     for (int w = t.tid; w < total; w += NTHR) {
-        int i, c;
-        if (orows) { i = w % N; c = w / N; }
-        else { c = w % LB; i = w / LB; }
+        const int c = orows ? w / N : w % LB, i = orows ? w % N : w / LB;
         const long l = l0 + 2 * c;
         const double2 v = buf[i * pitch + c];
         if (l < a.n_lines) a.out[l * ols + i * ost] = v.x * a.scale;
@@ -78,7 +74,7 @@ void launch_fc_lines_lb(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_
 #endif
 
 size_t fc_lines_smem_bytes(const FcPlanDev& pl, int LB, int scr_cap) {
-    return (static_cast<size_t>(pl.n_ext) * (LB + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2);
+    return (static_cast<size_t>(pl.n_ext) * LB + scr_cap + table_slots_host(pl)) * sizeof(double2);
 }
 
 int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {

@@ -1,7 +1,9 @@
 // Shared-memory FC line transform: continuation -> mixed-radix FFT -> spectral
 // multiplier -> inverse FFT, for a batch of LB complex lines held in shared
-// memory as buf[pos * pitch + line] (line index fastest, so the 32 lanes of a
-// warp touch consecutive 16-byte slots: conflict-free, and one twiddle per
+// memory as buf[pos * LB + line] (line index fastest, no padding: every pass
+// maps thread w to (line w % LB, position or butterfly w / LB), so 8
+// consecutive lanes -- one 128-byte shared-memory wavefront of 16-byte
+// accesses -- touch 8 consecutive slots: conflict-free, and one twiddle per
 // butterfly is a broadcast).
 //
 // Restates FcOperator::derivative / apply_profile (src/fc_core.cpp:221-238,
@@ -346,7 +348,7 @@ FCSG_HD void stage_reg_ct(int tid, double2* buf, const double2* tw) {
     constexpr int m = L / P;
     constexpr int total = (NE / P) * LB;
     constexpr int tstep = NE / L;
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;
     constexpr int ms = m * pitch;
 #pragma unroll 2
     for (int w = tid; w < total; w += NTHR) {
@@ -384,7 +386,7 @@ FCSG_HD void stage_ct(int tid, double2* buf, const double2* tw, double2* scr, in
     if constexpr (radix_in_registers(P)) {
         stage_reg_ct<P, L, NE, LB, NTHR, INV>(tid, buf, tw);
     } else {
-        stage_generic(Thr{tid, NTHR}, buf, LB + 1, LB, NE, L, P, tw, INV, scr, scr_cap);
+        stage_generic(Thr{tid, NTHR}, buf, LB, LB, NE, L, P, tw, INV, scr, scr_cap);
     }
 }
 
@@ -410,7 +412,7 @@ FCSG_HD void dit_stages_ct(int tid, double2* buf, const double2* tw, double2* sc
 // compile-time continuation for the reference operator (n_cont = 25, d = 2)
 template <int N, int G, int D1, int LB, int NTHR>
 FCSG_HD void continuation_ct(int tid, double2* buf, const double* blend) {
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;
     for (int w = tid; w < G * LB; w += NTHR) {
         const int line = w % LB;
         const int jj = w / LB;
@@ -431,7 +433,7 @@ FCSG_HD void continuation_ct(int tid, double2* buf, const double* blend) {
 
 template <int NE, int LB, int NTHR>
 FCSG_HD void spec_mult_ct(int tid, double2* buf, const double2* mult) {
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;
     for (int w = tid; w < NE * LB; w += NTHR) {
         const int line = w % LB;
         const int pos = w / LB;
@@ -449,7 +451,7 @@ FCSG_HD void middle_fused_ct(int tid, double2* buf, const double2* tw, const dou
     constexpr Factors F = factor_stages(NE);
     constexpr int P = F.r[F.n - 1];
     constexpr int total = (NE / P) * LB;
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;
 #pragma unroll 2
     for (int w = tid; w < total; w += NTHR) {
         const int line = w % LB;
@@ -478,7 +480,7 @@ FCSG_HD void middle_generic_ct(int tid, double2* buf, const double2* tw, const d
     constexpr Factors F = factor_stages(NE);
     constexpr int P = F.r[F.n - 1];
     constexpr int pstep = NE / P;
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;
     for (int w = tid; w < NE * LB; w += NTHR) {
         const int line = w % LB;
         const int pos = w / LB;

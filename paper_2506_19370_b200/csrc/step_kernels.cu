@@ -142,7 +142,7 @@ template <int LB, class Pass, int NE, int NTHR>
 FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const EngineDev& E, const FcPlanDev& pl,
                        int scr_cap, const LineDesc* desc) {
     constexpr bool rows = Pass::kRows;
-    constexpr int pitch = LB + 1;
+    constexpr int pitch = LB;  // line index fastest, no padding: see fft_line.h
     constexpr int KS = Pass::kStage;
     const int ni = E.ni, nj = E.nj;
     const int N = NE > 0 ? NE - 24 : pl.n;  // the line length of this launch
@@ -188,27 +188,17 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 const int w = tid + (ch * KC + k) * NTHR;
-                int i, l;
-                if (rows) {
-                    i = w % N;
-                    l = w / N;
-                } else {
-                    l = w % LB;
-                    i = w / LB;
-                }
+                // rows: consecutive lanes on consecutive points of one line
+                // (coalesced global access); columns: across lines
+                const int l = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
                 if (r < Pass::kRounds && l < c.nl_valid) P.fetch(r, pidx(c, l, i), fv[k]);
             }
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 const int w = tid + (ch * KC + k) * NTHR;
-                int i, l;
-                if (rows) {
-                    i = w % N;
-                    l = w / N;
-                } else {
-                    l = w % LB;
-                    i = w / LB;
-                }
+                // rows: consecutive lanes on consecutive points of one line
+                // (coalesced global access); columns: across lines
+                const int l = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
                 if (l < c.nl_valid) {
                     const long p = pidx(c, l, i);
                     double2 carry = mk2(0.0, 0.0);
@@ -225,14 +215,9 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
         if (r == Pass::kRounds) break;
         if constexpr (KS > 0) {
             for (int w = tid; w < total; w += NTHR) {
-                int i, l;
-                if (rows) {
-                    i = w % N;
-                    l = w / N;
-                } else {
-                    l = w % LB;
-                    i = w / LB;
-                }
+                // rows: consecutive lanes on consecutive points of one line
+                // (coalesced global access); columns: across lines
+                const int l = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
                 if (l >= c.nl_valid) continue;
                 const double* src[KS > 0 ? KS : 1];
                 const int n = P.stage_srcs(r, pidx(c, l, i), src);
@@ -1769,7 +1754,7 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, lb);  // full-scratch prime-67 middle
     const int nblk = desc ? (lb == 4 ? L.n4 : L.n8) : E.S * ((nlines + lb - 1) / lb);
     if (nblk == 0) return;
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * (lb + 1) + scr_cap + table_slots_host(pl)) * sizeof(double2) +
+    const size_t smem = (static_cast<size_t>(pl.n_ext) * lb + scr_cap + table_slots_host(pl)) * sizeof(double2) +
                         static_cast<size_t>(kSlots) * pl.n * lb * sizeof(double);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
