@@ -470,63 +470,96 @@ FCSG_HD void middle_fused_ct(int tid, double2* buf, const double2* tw, const dou
     }
 }
 
-// Large prime last radix P (e.g. 67 in 536): the last DIF stage, the
-// multiplier and the first DIT stage on P contiguous positions (m = 1, no
-// twiddles) as two direct DFT sweeps -- forward into a full scratch buffer
-// (scr[pos * LB + line], NE * LB slots), one barrier, inverse back into buf.
-// Rotations w_P^{rq} by recurrence, refreshed from the table every 8 steps.
+// Large prime last radix P, symmetric-pair form: with s_r = x_r + x_{P-r},
+// d_r = x_r - x_{P-r} (r = 1..H, H = (P-1)/2) and t = 2 pi r q / P,
+//   Y_q     = x_0 + sum_r (s_r cos t - i d_r sin t),
+//   Y_{P-q} = x_0 + sum_r (s_r cos t + i d_r sin t),
+// so one pass over H terms gives two outputs (a quarter of the direct DFT's
+// complex multiply-adds). Forward DFT + multiplier into the scratch as the
+// sums/differences of the multiplied pairs, then the inverse the same way
+// back into buf. scr holds NE * LB complex values (scr[pos * LB + line]).
 template <int NE, int LB, int NTHR>
-FCSG_HD void middle_generic_ct(int tid, double2* buf, const double2* tw, const double2* mult, double2* scr) {
+FCSG_HD void middle_sym_ct(int tid, double2* buf, const double2* tw, const double2* mult, double2* scr) {
     constexpr Factors F = factor_stages(NE);
     constexpr int P = F.r[F.n - 1];
+    constexpr int H = (P - 1) / 2;
     constexpr int pstep = NE / P;
+    constexpr int nblk = NE / P;
     constexpr int pitch = LB;
-    for (int w = tid; w < NE * LB; w += NTHR) {
+    // 1: s/d in place
+    for (int w = tid; w < nblk * H * LB; w += NTHR) {
         const int line = w % LB;
-        const int pos = w / LB;
-        const int blk = pos / P;
-        const int q = pos - blk * P;
-        const double2* xin = buf + blk * P * pitch + line;
-        const double2 step = ld2(tw + q * pstep);
-        double2 cur = mk2(1.0, 0.0), acc = mk2(0.0, 0.0);
-        int idx = 0;
-        for (int r = 0; r < P; ++r) {
-            acc = cadd(acc, cmul(xin[r * pitch], cur));
-            idx += q;
-            if (idx >= P) idx -= P;
-            cur = ((r & 7) == 7) ? ld2(tw + idx * pstep) : cmul(cur, step);
-        }
-        scr[pos * LB + line] = cmul(acc, ld2(mult + pos));
+        const int u = w / LB;
+        const int blk = u / H, r = 1 + (u - blk * H);
+        double2* xb = buf + blk * P * pitch + line;
+        const double2 a = xb[r * pitch], b = xb[(P - r) * pitch];
+        xb[r * pitch] = cadd(a, b);
+        xb[(P - r) * pitch] = csub(a, b);
     }
     FCSG_SYNC();
-    for (int w = tid; w < NE * LB; w += NTHR) {
+    // 2: Y_q, Y_{P-q}, times the multiplier, stored as their sum / difference
+    for (int w = tid; w < nblk * (H + 1) * LB; w += NTHR) {
         const int line = w % LB;
-        const int pos = w / LB;
-        const int blk = pos / P;
-        const int r = pos - blk * P;
-        const double2* yin = scr + blk * P * LB + line;
-        double2 step = ld2(tw + r * pstep);
-        step.y = -step.y;
-        double2 cur = mk2(1.0, 0.0), acc = mk2(0.0, 0.0);
-        int idx = 0;
-        for (int q = 0; q < P; ++q) {
-            acc = cadd(acc, cmul(yin[q * LB], cur));
-            idx += r;
-            if (idx >= P) idx -= P;
-            if ((q & 7) == 7) {
-                cur = ld2(tw + idx * pstep);
-                cur.y = -cur.y;
-            } else {
-                cur = cmul(cur, step);
-            }
+        const int u = w / LB;
+        const int blk = u / (H + 1), q = u - blk * (H + 1);
+        const double2* xb = buf + blk * P * pitch + line;
+        const double2 x0 = xb[0];
+        double2* sb = scr + blk * P * LB + line;
+        const double2* mb = mult + blk * P;
+        if (q == 0) {
+            double2 y = x0;
+            for (int r = 1; r <= H; ++r) y = cadd(y, xb[r * pitch]);
+            sb[0] = cmul(y, ld2(mb));
+            continue;
         }
-        buf[pos * pitch + line] = acc;
+        double2 A = x0, B = mk2(0.0, 0.0);
+        int k = 0;
+        for (int r = 1; r <= H; ++r) {
+            k += q;
+            if (k >= P) k -= P;
+            const double2 c = ld2(tw + k * pstep);  // (cos t, -sin t)
+            const double2 sr = xb[r * pitch], dr = xb[(P - r) * pitch];
+            A = mk2(A.x + sr.x * c.x, A.y + sr.y * c.x);
+            B = mk2(B.x - dr.x * c.y, B.y - dr.y * c.y);  // + d_r sin t
+        }
+        const double2 yq = cmul(mk2(A.x + B.y, A.y - B.x), ld2(mb + q));          // A - iB
+        const double2 yp = cmul(mk2(A.x - B.y, A.y + B.x), ld2(mb + P - q));      // A + iB
+        sb[q * LB] = cadd(yq, yp);
+        sb[(P - q) * LB] = csub(yq, yp);
+    }
+    FCSG_SYNC();
+    // 3: inverse, z_r = y_0 + sum_q (S_q cos t + i D_q sin t), z_{P-r} with -i
+    for (int w = tid; w < nblk * (H + 1) * LB; w += NTHR) {
+        const int line = w % LB;
+        const int u = w / LB;
+        const int blk = u / (H + 1), r = u - blk * (H + 1);
+        const double2* sb = scr + blk * P * LB + line;
+        double2* zb = buf + blk * P * pitch + line;
+        const double2 y0 = sb[0];
+        if (r == 0) {
+            double2 z = y0;
+            for (int q = 1; q <= H; ++q) z = cadd(z, sb[q * LB]);
+            zb[0] = z;
+            continue;
+        }
+        double2 A = y0, B = mk2(0.0, 0.0);
+        int k = 0;
+        for (int q = 1; q <= H; ++q) {
+            k += r;
+            if (k >= P) k -= P;
+            const double2 c = ld2(tw + k * pstep);
+            const double2 Sq = sb[q * LB], Dq = sb[(P - q) * LB];
+            A = mk2(A.x + Sq.x * c.x, A.y + Sq.y * c.x);
+            B = mk2(B.x - Dq.x * c.y, B.y - Dq.y * c.y);
+        }
+        zb[r * pitch] = mk2(A.x - B.y, A.y + B.x);        // A + iB
+        zb[(P - r) * pitch] = mk2(A.x + B.y, A.y - B.x);  // A - iB
     }
 }
 
 // fc_transform for n_ext = NE with the reference continuation (n_cont = 25,
 // degree 2): N = NE - 24. When the last radix is a large prime, scr must hold
-// NE * LB complex values (see middle_generic_ct).
+// NE * LB complex values (see middle_sym_ct).
 template <int NE, int LB, int NTHR>
 FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mode, double2* scr, int scr_cap) {
     constexpr Factors F = factor_stages(NE);
@@ -536,7 +569,7 @@ FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mod
     if constexpr (radix_in_registers(F.r[F.n - 1])) {
         middle_fused_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE);
     } else {
-        middle_generic_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
+        middle_sym_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
     }
     FCSG_SYNC();
     dit_stages_ct<NE, F.n - 2, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
