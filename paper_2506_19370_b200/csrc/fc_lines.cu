@@ -18,7 +18,7 @@ FCSG_HD void fc_lines_body(Thr t, int block, double2* smem, const FcLinesArgs& a
     double2* buf = smem;
     double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
     const FcPlanDev spl = stage_tables(Thr{t.tid, NTHR}, pl, a.mode, scr + a.scr_cap);
-    const int N = NE > 0 ? NE - 24 : pl.n;
+    const int N = NE > 0 ? NE - ct_gap(NE) : pl.n;
     const long l0 = static_cast<long>(block) * 2 * LB;
     const long ls = a.line_stride, st = a.stride;
     const long ols = a.out_line_stride, ost = a.out_stride;
@@ -66,9 +66,10 @@ void launch_fc_lines_t(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_t
 
 template <int LB>
 void launch_fc_lines_lb(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_t s) {
-    const bool ref_op = a.pl.n_gap == 24 && a.pl.dp1 == 3;
-    if (ref_op && a.pl.n_ext == 280) launch_fc_lines_t<LB, 280>(a, nblk, smem, s);
-    else if (ref_op && a.pl.n_ext == 536) launch_fc_lines_t<LB, 536>(a, nblk, smem, s);
+    const bool ct = ct_plan_for(a.pl);
+    if (ct && a.pl.n_ext == 280) launch_fc_lines_t<LB, 280>(a, nblk, smem, s);
+    else if (ct && a.pl.n_ext == 536) launch_fc_lines_t<LB, 536>(a, nblk, smem, s);
+    else if (ct && a.pl.n_ext == 282) launch_fc_lines_t<LB, 282>(a, nblk, smem, s);
     else launch_fc_lines_t<LB, 0>(a, nblk, smem, s);
 }
 #endif
@@ -95,7 +96,7 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
     const int nblk = static_cast<int>((a.n_lines + lines_per_block - 1) / lines_per_block);
     if (nblk == 0) return;
     a.scr_cap = fc_lines_scr_cap(a.pl, LB);
-    if (a.pl.n_gap == 24 && a.pl.dp1 == 3 && a.pl.n_ext == 536) a.scr_cap = ct_scratch_slots(536, LB);
+    if (ct_plan_for(a.pl)) a.scr_cap = std::max(a.scr_cap, ct_scratch_slots(a.pl.n_ext, LB));
     const size_t smem = fc_lines_smem_bytes(a.pl, LB, a.scr_cap);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -111,11 +112,11 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
     std::vector<double2> sm(smem / sizeof(double2));
     // same plan dispatch as the CUDA build, so the emulation covers the
     // compile-time plans too
-    const bool ref_op = a.pl.n_gap == 24 && a.pl.dp1 == 3;
-    const int ne = ref_op && (a.pl.n_ext == 280 || a.pl.n_ext == 536) ? a.pl.n_ext : 0;
+    const int ne = ct_plan_for(a.pl) ? a.pl.n_ext : 0;
     for (int b = 0; b < nblk; ++b) {
         if (ne == 280) fc_lines_body<4, 280, 1>(Thr{0, 1}, b, sm.data(), a);
         else if (ne == 536) fc_lines_body<4, 536, 1>(Thr{0, 1}, b, sm.data(), a);
+        else if (ne == 282) fc_lines_body<4, 282, 1>(Thr{0, 1}, b, sm.data(), a);
         else fc_lines_body<4, 0, 1>(Thr{0, 1}, b, sm.data(), a);
     }
 #endif

@@ -409,7 +409,22 @@ FCSG_HD void dit_stages_ct(int tid, double2* buf, const double2* tw, double2* sc
     }
 }
 
-// compile-time continuation for the reference operator (n_cont = 25, d = 2)
+// gap length (n_cont - 1) and boundary points (degree + 1) of the operator a
+// compile-time plan of length NE is built for
+#if FCSG_CUDA
+__host__ __device__
+#endif
+constexpr int ct_gap(int ne) {
+    return ne == 282 ? 26 : 24;
+}
+#if FCSG_CUDA
+__host__ __device__
+#endif
+constexpr int ct_dp1(int ne) {
+    return ne == 282 ? 5 : 3;
+}
+
+// compile-time continuation (gap G, D1 boundary points)
 template <int N, int G, int D1, int LB, int NTHR>
 FCSG_HD void continuation_ct(int tid, double2* buf, const double* blend) {
     constexpr int pitch = LB;
@@ -563,7 +578,7 @@ FCSG_HD void middle_sym_ct(int tid, double2* buf, const double2* tw, const doubl
 template <int NE, int LB, int NTHR>
 FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mode, double2* scr, int scr_cap) {
     constexpr Factors F = factor_stages(NE);
-    continuation_ct<NE - 24, 24, 3, LB, NTHR>(tid, buf, pl.blend);
+    continuation_ct<NE - ct_gap(NE), ct_gap(NE), ct_dp1(NE), LB, NTHR>(tid, buf, pl.blend);
     FCSG_SYNC();
     dif_stages_ct<NE, 0, LB, NTHR, F.n - 1>(tid, buf, pl.tw, scr, scr_cap);
     if constexpr (radix_in_registers(F.r[F.n - 1])) {
@@ -584,12 +599,18 @@ constexpr int ct_scratch_slots(int ne, int lb) {
     return radix_in_registers(f.r[f.n - 1]) ? 0 : ne * lb;
 }
 
-// the lengths with a compile-time plan (reference operator, n_cont = 25)
+// the lengths with a compile-time plan: the reference operator (degree 2,
+// n_cont = 25) at N = 256 and 512, and BASELINE config 1's operator (degree
+// 4, n_cont = 27) at N = 256
 #if FCSG_CUDA
 __host__ __device__
 #endif
 constexpr bool has_ct_plan(int n_ext) {
-    return n_ext == 280 || n_ext == 536;
+    return n_ext == 280 || n_ext == 536 || n_ext == 282;
+}
+// true when plan pl is the operator a compile-time plan of its length was built for
+inline bool ct_plan_for(const FcPlanDev& pl) {
+    return has_ct_plan(pl.n_ext) && pl.n_gap == ct_gap(pl.n_ext) && pl.dp1 == ct_dp1(pl.n_ext);
 }
 
 }  // namespace fcsg
