@@ -9,3 +9,4 @@ python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.log
 python scripts/profile_step.py 8 1 > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py 8 1 > gpurun_out/ncu1.log 2>&1
 bash scripts/prof_top.sh
+bash scripts/prof_fc.sh
