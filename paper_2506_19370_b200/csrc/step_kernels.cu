@@ -701,12 +701,15 @@ struct PassXc {
 // update of components 2, 3; then the same for (rho, rho u). Components 2, 3
 // are updated first: G_0 = rho v and G_1 = rho u v need the old rho v, kept in
 // stash slot 3 by the first load (rho and rho u are still unmodified then).
-// slots: 0 iq2y, 1 mu | 1, 2 tA pair (update rounds), 3 old rho v
+// The updates' current values u come from the stash too: slots 3, 4 hold
+// (rho v, E) from the first load for the first update, then (rho, rho u)
+// from the last load for the second.
+// slots: 0 iq2y, 1 mu | 1, 2 tA pair (update rounds), 3-4 stash
 struct PassYc {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 4;
     static constexpr int kStage = 3;
-    static constexpr int kStash = 1;
+    static constexpr int kStash = 2;
     static constexpr int kLB = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
@@ -727,6 +730,7 @@ struct PassYc {
             case 0: {
                 const Prim q = prim_of(fv);
                 st[3 * ss] = q.my;
+                st[4 * ss] = q.E;
                 return mk2(q.my, q.theta);
             }
             case 1: {
@@ -736,6 +740,8 @@ struct PassYc {
             case 2: return mk2(fv[0], fv[1]);
             default: {
                 const double rho = fv[0], mx = fv[1], my = st[3 * ss];
+                st[3 * ss] = rho;  // u of the last update
+                st[4 * ss] = mx;
                 const double v = my / rho;
                 return mk2(carry.x - my, carry.y - mx * v);  // G_0, G_1 (src/euler.cpp:64-75)
             }
@@ -760,8 +766,8 @@ struct PassYc {
             return mk2(m * (d * v.x), m * (d * v.y));  // s5 = mu (0 D1 w + iq2y D2 w)
         }
         const int c0 = r == 1 ? 2 : 0;
-        ssprk_update(E, stage, c0, p, E.e[c0][p], st[ss] + d * v.x);
-        ssprk_update(E, stage, c0 + 1, p, E.e[c0 + 1][p], st[2 * ss] + d * v.y);
+        ssprk_update(E, stage, c0, p, st[3 * ss], st[ss] + d * v.x);
+        ssprk_update(E, stage, c0 + 1, p, st[4 * ss], st[2 * ss] + d * v.y);
         return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
