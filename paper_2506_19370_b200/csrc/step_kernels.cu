@@ -655,21 +655,24 @@ struct PassXc {
     static constexpr bool kRows = true;
     static constexpr int kRounds = 4;
     static constexpr int kStage = 2;
-    static constexpr int kStash = 0;
+    static constexpr int kStash = 2;
     static constexpr int kLB = 4;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassXc(const EngineDev& e, int) : E(e) {}
     FCSG_HD int mode(int) const { return 1; }
+    // the w rounds read e and stash the pair of x-fluxes the next round needs
+    // (slots 2, 3); the Phi rounds read nothing from global memory
     static constexpr int kFetch = 4;
-    FCSG_HD void fetch(int, long p, double* v) const { fetch_e(E, p, v); }
-    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2 carry, const double* fv, double*, int) const {
+    FCSG_HD void fetch(int r, long p, double* v) const {
+        if (!(r & 1)) fetch_e(E, p, v);
+    }
+    FCSG_HD double2 load(int r, long p, const LineCtx& c, double2 carry, const double* fv, double* st, int ss) const {
+        if (r & 1) return mk2(carry.x - st[2 * ss], carry.y - st[3 * ss]);
         const Prim q = prim_of(fv);
-        if (r & 1) {
-            const int c0 = r - 1;  // 0 or 2
-            const double2 f0 = flux_pair(q, c0), f1 = flux_pair(q, c0 + 1);
-            return mk2(carry.x - f0.x, carry.y - f1.x);
-        }
+        const double2 f0 = flux_pair(q, r), f1 = flux_pair(q, r + 1);
+        st[2 * ss] = f0.x;
+        st[3 * ss] = f1.x;
         if (r == 0) {
             check_positive(E, q, p, c);
             return mk2(q.rho, q.mx);
