@@ -572,6 +572,124 @@ FCSG_HD void middle_sym_ct(int tid, double2* buf, const double2* tw, const doubl
     }
 }
 
+#if FCSG_CUDA
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// middle_sym_ct on the FP64 tensor cores. The sums over r of the symmetric
+// form are real matrix products: with the columns j = (block, line, re/im),
+//   A[q][j] = sum_r cos(2 pi q r / P) s_r[j],   B[q][j] = sum_r sin(2 pi q r / P) d_r[j]
+// (q = 0..H rows, r = 1..H), so one warp computes them for 4 block-lines
+// (8 real columns) per mma.m8n8k4 tile: A operand = the cos / sin matrices
+// (rows q, columns r, read from the twiddle table), B operand = s_r / d_r
+// straight from the line buffer. A lane's D fragment holds the real and
+// imaginary column of one block-line, so Y_q = A - iB and Y_{P-q} = A + iB
+// are formed in registers. The inverse is the same product over the sums /
+// differences of the multiplied outputs.
+template <int NE, int LB, int NTHR>
+__device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const double2* mult, double2* scr) {
+    constexpr Factors F = factor_stages(NE);
+    constexpr int P = F.r[F.n - 1];
+    constexpr int H = (P - 1) / 2;
+    constexpr int pstep = NE / P;
+    constexpr int nblk = NE / P;
+    constexpr int MT = (H + 1 + 7) / 8;  // m-tiles over q = 0..H
+    constexpr int KS = (H + 3) / 4;      // k-steps over r = 1..H
+    constexpr int NBL = nblk * LB;       // block-lines
+    constexpr int NTILE = (NBL + 3) / 4;
+    constexpr int NW = NTHR / 32;
+    constexpr int MC = MT <= 3 ? MT : 1;
+    static_assert(NTHR % 32 == 0, "whole warps");
+    const int lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    // 1: s_r, d_r in place
+    for (int w = tid; w < nblk * H * LB; w += NTHR) {
+        const int line = w % LB;
+        const int u = w / LB;
+        const int blk = u / H, r = 1 + (u - blk * H);
+        double2* xb = buf + blk * P * LB + line;
+        const double2 a = xb[r * LB], b = xb[(P - r) * LB];
+        xb[r * LB] = cadd(a, b);
+        xb[(P - r) * LB] = csub(a, b);
+    }
+    __syncthreads();
+    // cos / sin (2 pi q r / P) of this lane's A fragment (row q = 8 mt + g, column r)
+    auto cs = [&](int q, int r, double& c, double& sn) {
+        if (q <= H && r <= H) {
+            const double2 w = tw[((q * r) % P) * pstep];  // (cos, -sin)
+            c = w.x;
+            sn = -w.y;
+        } else {
+            c = 0.0;
+            sn = 0.0;
+        }
+    };
+    // 2: forward DFT + multiplier; src = buf (s at r, d at P - r), dst = scr
+    // 3: inverse; src = scr (S at q, D at P - q), dst = buf
+    for (int ph = 0; ph < 2; ++ph) {
+        const double2* src = ph == 0 ? buf : scr;
+        double2* dst = ph == 0 ? scr : buf;
+        for (int nt = warp; nt < NTILE; nt += NW) {
+            const int blB = nt * 4 + (g >> 1);  // B column n = g: block-line, real/imaginary part
+            const bool vB = blB < NBL;
+            const double* colB =
+                reinterpret_cast<const double*>(src + (vB ? (blB / LB) * P * LB + blB % LB : 0)) + (g & 1);
+            const int blD = nt * 4 + t;  // D columns 2t, 2t + 1: block-line blD, re / im
+            const bool vD = blD < NBL;
+            const int blk = vD ? blD / LB : 0, line = vD ? blD % LB : 0;
+            const double2 x0 = src[blk * P * LB + line];
+            double2* db = dst + blk * P * LB + line;
+            const double2* mb = mult + blk * P;
+            // m-tiles in chunks of MC (all at once for P = 47; one at a time
+            // for P = 67, whose 5 x 4 accumulators would not fit 80 registers)
+            for (int mt0 = 0; mt0 < MT; mt0 += MC) {
+                double aA[MC][2], aB[MC][2];
+#pragma unroll
+                for (int m = 0; m < MC; ++m) aA[m][0] = aA[m][1] = aB[m][0] = aB[m][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int r = 1 + 4 * ks + t;
+                    const bool vr = vB && r <= H;
+                    const double sv = vr ? colB[2 * r * LB] : 0.0;
+                    const double dv = vr ? colB[2 * (P - r) * LB] : 0.0;
+#pragma unroll
+                    for (int m = 0; m < MC; ++m) {
+                        double c, sn;
+                        cs(8 * (mt0 + m) + g, r, c, sn);
+                        dmma884(aA[m][0], aA[m][1], c, sv);
+                        dmma884(aB[m][0], aB[m][1], sn, dv);
+                    }
+                }
+                if (!vD) continue;
+#pragma unroll
+                for (int m = 0; m < MC; ++m) {
+                    const int q = 8 * (mt0 + m) + g;
+                    if (q > H) continue;
+                    const double ax = aA[m][0] + x0.x, ay = aA[m][1] + x0.y, bx = aB[m][0], by = aB[m][1];
+                    if (ph == 0) {
+                        const double2 yq = cmul(mk2(ax + by, ay - bx), ld2(mb + q));  // A - iB
+                        if (q == 0) {
+                            db[0] = yq;
+                        } else {
+                            const double2 yp = cmul(mk2(ax - by, ay + bx), ld2(mb + P - q));  // A + iB
+                            db[q * LB] = cadd(yq, yp);
+                            db[(P - q) * LB] = csub(yq, yp);
+                        }
+                    } else {
+                        db[q * LB] = mk2(ax - by, ay + bx);  // A + iB
+                        if (q > 0) db[(P - q) * LB] = mk2(ax + by, ay - bx);
+                    }
+                }
+            }
+        }
+        if (ph == 0) __syncthreads();  // the caller syncs after the inverse
+    }
+}
+#endif
+
 // fc_transform for n_ext = NE with the reference continuation (n_cont = 25,
 // degree 2): N = NE - 24. When the last radix is a large prime, scr must hold
 // NE * LB complex values (see middle_sym_ct).
@@ -584,7 +702,11 @@ FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mod
     if constexpr (radix_in_registers(F.r[F.n - 1])) {
         middle_fused_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE);
     } else {
+#if FCSG_CUDA
+        middle_dmma_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
+#else
         middle_sym_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
+#endif
     }
     FCSG_SYNC();
     dit_stages_ct<NE, F.n - 2, LB, NTHR>(tid, buf, pl.tw, scr, scr_cap);
