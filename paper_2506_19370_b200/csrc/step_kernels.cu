@@ -962,21 +962,15 @@ struct PassFC {
             E.e[0][p] = v.x;
             E.e[1][p] = v.y;
         } else {
-            E.e[2][p] = v.x;
-            E.tF[3][p] = v.y;  // theta, consumed by finish()
+            // E = rho theta/(gamma-1) + |m|^2 / (2 rho) (src/runtime.cpp:413-420);
+            // rho, rho u were written at this point by this thread in round 0
+            const double rho = E.e[0][p], mx = E.e[1][p], my = v.x;
+            E.e[2][p] = my;
+            E.e[3][p] = rho * v.y / kGm1 + 0.5 * (mx * mx + my * my) / rho;
         }
         return {};
     }
-    FCSG_HD void finish(Thr t, const LineCtx& c, int N) const {
-        // E = rho theta/(gamma-1) + |m|^2 / (2 rho)   (src/runtime.cpp:413-420)
-        const int total = N * c.nl_valid;
-        for (int w = t.tid; w < total; w += t.nthr) {
-            const int l = w % c.nl_valid, i = w / c.nl_valid;
-            const long p = pidx(c, l, i);
-            const double rho = E.e[0][p], mx = E.e[1][p], my = E.e[2][p];
-            E.e[3][p] = rho * E.tF[3][p] / kGm1 + 0.5 * (mx * mx + my * my) / rho;
-        }
-    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
 // ---------------------------------------------------------------------------
