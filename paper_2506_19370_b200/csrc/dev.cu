@@ -25,6 +25,18 @@ void* create_stream() {
     return s;
 }
 void destroy_stream(void* s) { cudaStreamDestroy(static_cast<cudaStream_t>(s)); }
+void* create_event() {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    return e;
+}
+void destroy_event(void* e) { cudaEventDestroy(static_cast<cudaEvent_t>(e)); }
+void record(void* event, void* stream) {
+    ck(cudaEventRecord(static_cast<cudaEvent_t>(event), static_cast<cudaStream_t>(stream)), "event record");
+}
+void wait(void* stream, void* event) {
+    ck(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(event), 0), "stream wait");
+}
 void* alloc(size_t bytes) {
     void* p = nullptr;
     if (bytes == 0) bytes = 16;
@@ -98,6 +110,10 @@ bool is_cuda() { return false; }
 void set_device(int) {}
 void* create_stream() { return nullptr; }
 void destroy_stream(void*) {}
+void* create_event() { return nullptr; }
+void destroy_event(void*) {}
+void record(void*, void*) {}
+void wait(void*, void*) {}
 void* alloc(size_t bytes) { return std::calloc(bytes ? bytes : 16, 1); }
 void free(void* p) { std::free(p); }
 void h2d(void* dst, const void* src, size_t bytes, void*) { std::memcpy(dst, src, bytes); }

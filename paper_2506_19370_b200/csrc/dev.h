@@ -12,6 +12,11 @@ namespace dev {
 void set_device(int device);
 void* create_stream();
 void destroy_stream(void* s);
+// events for fork / join between streams (also inside graph capture)
+void* create_event();
+void destroy_event(void* e);
+void record(void* event, void* stream);
+void wait(void* stream, void* event);
 void* alloc(size_t bytes);
 void free(void* p);
 void h2d(void* dst, const void* src, size_t bytes, void* stream);

@@ -23,6 +23,9 @@ Engine::Engine(Ctx& ctx, const EngineConfig& cfg) : ctx_(ctx), cfg_(cfg) {}
 
 Engine::~Engine() {
     if (graph_exec_) dev::graph_destroy(graph_exec_, graph_);
+    if (ev_fork_) dev::destroy_event(ev_fork_);
+    if (ev_join_) dev::destroy_event(ev_join_);
+    if (side_) dev::destroy_stream(side_);
     for (void* p : allocs_) dev::free(p);
 }
 
@@ -745,9 +748,27 @@ double Engine::time() {
 
 void Engine::enqueue_step(bool step0) {
     void* s = ctx_.stream;
-    launch_phase0(E_, G_, step0, s);
+    // phase 0 reads e only in the proxy (and, at t = 0, in the classifier's
+    // density windows); the phase-2 filter writes e and touches nothing
+    // phases 0-1 read or write, so in steady steps it runs on a side stream
+    // next to the classifier and the blend
+    const bool fork = !step0 && dev::is_cuda();
+    if (fork && !side_) {
+        side_ = dev::create_stream();
+        ev_fork_ = dev::create_event();
+        ev_join_ = dev::create_event();
+    }
+    launch_proxy(E_, s);
+    if (fork) {
+        dev::record(ev_fork_, s);
+        dev::wait(side_, ev_fork_);
+        launch_phase2(G_, false, side_);
+        dev::record(ev_join_, side_);
+    }
+    launch_classify(E_, G_, step0, s);
     launch_phase1(E_, s);
-    launch_phase2(G_, step0, s);
+    if (fork) dev::wait(s, ev_join_);
+    else launch_phase2(G_, step0, s);
     launch_bc(G_, s);
     launch_finalize_dt(E_, s);
     for (int st = 0; st < 5; ++st) {

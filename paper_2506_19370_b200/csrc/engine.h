@@ -162,6 +162,12 @@ class Engine {
     long host_step_ = 0;
     void* graph_exec_ = nullptr;
     void* graph_ = nullptr;
+    // side stream of the steady step: the filter (phase 2 line passes) runs
+    // next to the classifier and blend (phases 0-1), which neither read nor
+    // write what it touches
+    void* side_ = nullptr;
+    void* ev_fork_ = nullptr;
+    void* ev_join_ = nullptr;
 };
 
 }  // namespace fcsg

@@ -1800,10 +1800,18 @@ int step_scr_cap(const FcPlanDev& pl) {
     return cap;
 }
 
-void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream) {
+void launch_proxy(const EngineDev& Eall, void* stream) {
+#if FCSG_CUDA
+    proxy_kernel<<<grid_for(Eall.npts), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(Eall);
+#else
+    (void)stream;
+    proxy_body(Thr{0, 1}, 0, 1, Eall);
+#endif
+}
+
+void launch_classify(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream) {
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    proxy_kernel<<<grid_for(Eall.npts), kThreads, 0, s>>>(Eall);
     static const bool scalar = [] {
         const char* v = std::getenv("FCSG_CLASSIFIER");
         return v && std::string(v) == "scalar";
@@ -1823,10 +1831,15 @@ void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, boo
     }
 #else
     (void)stream;
-    proxy_body(Thr{0, 1}, 0, 1, Eall);
+    (void)Eall;
     std::vector<double> tab(kTanhTable);
     for (const GroupLaunch& g : G) classify_body(Thr{0, 1}, 0, 1, MlpW{g.E.mlp}, tab.data(), g.E, step0);
 #endif
+}
+
+void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream) {
+    launch_proxy(Eall, stream);
+    launch_classify(Eall, G, step0, stream);
 }
 
 void launch_phase1(const EngineDev& Eall, void* stream) {

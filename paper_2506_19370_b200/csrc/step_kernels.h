@@ -159,6 +159,8 @@ std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
 int step_scr_cap(const FcPlanDev& pl);
 // phase 0: proxy over all points (global view), classifier per group
 void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream);
+void launch_proxy(const EngineDev& Eall, void* stream);
+void launch_classify(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream);
 void launch_phase1(const EngineDev& Eall, void* stream);
 void launch_phase2(const std::vector<GroupLaunch>& G, bool step0, void* stream);
 void launch_stage(const std::vector<GroupLaunch>& G, int stage, void* stream);
