@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 namespace fcsg {
@@ -656,7 +657,8 @@ struct PassXc {
     static constexpr int kRounds = 4;
     static constexpr int kStage = 2;
     static constexpr int kStash = 2;
-    static constexpr int kLB = 4;
+    static constexpr int kLB = 2;
+    static constexpr int kNT = 128;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     FCSG_HD PassXc(const EngineDev& e, int) : E(e) {}
@@ -1713,6 +1715,16 @@ namespace {
 
 constexpr int kLB = 8;  // lines per CTA in the step passes
 
+// CTA size of a pass's compile-time-plan kernel (Pass::kNT if set, else 256)
+template <class P, class = void>
+struct NtOf {
+    static constexpr int v = kThreads;
+};
+template <class P>
+struct NtOf<P, std::void_t<decltype(P::kNT)>> {
+    static constexpr int v = P::kNT;
+};
+
 int grid_for(long n) {
     long g = (n + kThreads - 1) / kThreads;
     if (g > 148 * 16) g = 148 * 16;
@@ -1761,8 +1773,9 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
                         static_cast<size_t>(kSlots) * pl.n * lb * sizeof(double);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
-    else if (ct) launch_line_pass<Pass, 536, kThreads, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    constexpr int kNT = NtOf<Pass>::v;
+    if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct) launch_line_pass<Pass, 536, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
 #else
     (void)stream;
