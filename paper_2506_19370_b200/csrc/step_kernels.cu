@@ -1,21 +1,22 @@
 // Kernels of one FC-SDNN superstep (Engine::run body, src/runtime.cpp:482-511).
 //
-//  phase 0  proxy_kernel     proxy_value / mwsb_value per point   (src/viscosity.cpp:13-29, runtime.cpp:327-346)
-//           classify_kernel  row + column 7-point stencils -> MLP -> min -> mu_hat
-//                            (src/viscosity.cpp:48-59,108-160,211-251)
-//  phase 1  blend_kernel     mu = max(w_norm mu_hat + sum w mu_hat_src, 0) and the
-//                            dt_bound_local min (src/runtime.cpp:352-371, euler.cpp:223-236)
-//  phase 2  filter rows/cols + E rebuild (or the t=0 smear)   (src/runtime.cpp:373-424,
-//                            subpatch_data.cpp:30-67), dilation at t=0
-//  stage    pass A (rows)    D1 of F, G, w  ->  iq1x D1F + iq1y D1G, D1w
-//           pass B (cols)    D2 of F, G, w  ->  inviscid rhs, mu grad w; D2 of mu grad w
-//           pass C (rows)    D1 of mu grad w -> rhs -> SSPRK(5,4) update
-//                            (euler_rhs src/euler.cpp:25-101, ssprk_stage_update :182-221)
-//           bc_kernel        enforce_bc, row ends then column ends (src/euler.cpp:105-180)
-//           exchange_kernel  phase 6 fringe copies (src/runtime.cpp:433-454)
+//  phase 0  proxy_kernel         proxy_value / mwsb_value per point (src/viscosity.cpp:13-29,
+//                                runtime.cpp:327-346)
+//           classify_mma_kernel  row + column 7-point stencils -> MLP on the FP64 tensor
+//                                cores -> min -> mu_hat (src/viscosity.cpp:48-59,108-160,211-251)
+//  phase 1  blend_kernel         mu = max(w_norm mu_hat + copies + 6x6 interpolations, 0) and
+//                                the dt_bound_local min (src/runtime.cpp:352-371, euler.cpp:223-236)
+//  phase 2  filter rows/cols + E rebuild (or the t=0 smear) (src/runtime.cpp:373-424,
+//                                subpatch_data.cpp:30-67), dilation at t=0
+//  stage    line passes          euler_rhs (src/euler.cpp:25-101) in the flux form
+//                                div(mu grad w - f) and ssprk_stage_update (:182-221):
+//                                Cartesian X (rows) + Y (cols), general GA + GB + C;
+//                                reference accumulation order: A' B' C' / A B C
+//           bc_kernel            enforce_bc, row ends then column ends (src/euler.cpp:105-180)
+//           exchange_kernel      phase 6 copies and interpolations (src/runtime.cpp:433-454)
 //
-// The 40 line derivatives of euler_rhs are therefore done as 3 line passes;
-// each pass keeps two real quantities per complex FFT line (fft_line.h).
+// Each line pass keeps two real quantities per complex FFT line (fft_line.h)
+// and runs on one shape group of subpatches (step_kernels.h, EngineDev).
 #include "fft_line.h"
 #include "step_kernels.h"
 
