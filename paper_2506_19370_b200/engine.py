@@ -117,7 +117,10 @@ class Engine:
         ctx.check(L.fcsg_engine_load_mlp(h, cfg.weights.encode()))
         ctx.check(L.fcsg_engine_finalize(h))
         if initial_states is None and ic is not None and rank_plan is None:
-            initial_states = [P.initial_state(dec, ic, k) for k in range(len(dec.subs))]
+            if hasattr(dec, "initial_state"):  # multipatch.MultiPatchDecomposition
+                initial_states = [dec.initial_state(ic, k) for k in range(len(dec.subs))]
+            else:
+                initial_states = [P.initial_state(dec, ic, k) for k in range(len(dec.subs))]
         if initial_states is not None:
             for k, e in enumerate(initial_states):
                 self.set_state(k, e)
