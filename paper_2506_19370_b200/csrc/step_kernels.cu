@@ -121,6 +121,17 @@ FCSG_HD void stage_wait() {
 #endif
 }
 
+// Pass::kFetchAtEnd: the pass also prefetches (fetch) for the epilogue of
+// its last round, which runs after the last transform with no load
+template <class P, class = void>
+struct FetchAtEnd {
+    static constexpr bool v = false;
+};
+template <class P>
+struct FetchAtEnd<P, std::void_t<decltype(P::kFetchAtEnd)>> {
+    static constexpr bool v = P::kFetchAtEnd;
+};
+
 // One CTA owns LB lines of one subpatch (rows: stride-1 lines of length ni;
 // columns: stride-ni lines of length nj). For every round r of the pass it
 // loads two real quantities per point as one complex line, runs the FC
@@ -193,7 +204,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
                 // rows: consecutive lanes on consecutive points of one line
                 // (coalesced global access); columns: across lines
                 const int l = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
-                if (r < Pass::kRounds && l < c.nl_valid) P.fetch(r, pidx(c, l, i), fv[k]);
+                if ((r < Pass::kRounds || FetchAtEnd<Pass>::v) && l < c.nl_valid) P.fetch(r, pidx(c, l, i), fv[k]);
             }
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
@@ -206,7 +217,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
                     double2 carry = mk2(0.0, 0.0);
                     if (r > 0) {
                         const double2 v = buf[i * pitch + l];
-                        carry = P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c);
+                        carry = P.store(r - 1, p, mk2(v.x * inv_len, v.y * inv_len), stg + w, total, c, fv[k]);
                     }
                     if (r < Pass::kRounds) buf[i * pitch + l] = P.load(r, p, c, carry, fv[k], stg + w, total);
                 } else if (r < Pass::kRounds) {
@@ -318,7 +329,7 @@ struct PassA {
         s[1] = E.iq1y + p;
         return 2;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         if (r < 4) {
             E.tA[r][p] = st[0] * v.x + st[ss] * v.y;
         } else {
@@ -379,7 +390,7 @@ struct PassB {
         s[2] = E.tA[r - 6] + p;
         return 3;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         const double b = st[0], d = st[ss];
         if (r < 4) {
             E.tA[r][p] = -(st[2 * ss] + (b * v.x + d * v.y));
@@ -439,6 +450,30 @@ FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double u
     }
 }
 
+// ssprk_update with the register e0 already read (stages 1-3; other stages
+// read what they need themselves)
+FCSG_HD void ssprk_update_e0(const EngineDev& E, int stage, int c, long p, double u, double r, double e0v) {
+    if (stage < 1 || stage > 3) {
+        ssprk_update(E, stage, c, p, u, r);
+        return;
+    }
+    const double dt = E.sc->dt;
+    if (E.rhs[0]) E.rhs[c][p] = r;
+    double* e = E.e[c];
+    if (stage == 1) {
+        const double nu = SA20 * e0v + SA21 * u + dt * SB1 * r;
+        e[p] = nu;
+        E.e2[c][p] = nu;
+    } else if (stage == 2) {
+        const double nu = SA30 * e0v + SA32 * u + dt * SB2 * r;
+        e[p] = nu;
+        E.e3[c][p] = nu;
+    } else {
+        E.rhs3[c][p] = r;
+        e[p] = SA40 * e0v + SA43 * u + dt * SB3 * r;
+    }
+}
+
 // Pass C (rows): D1 of mu grad w, rhs, SSPRK(5,4) stage update
 // staged per store(c): tA[c], iq1x, iq1y, e[c]
 struct PassC {
@@ -467,7 +502,7 @@ struct PassC {
         s[3] = E.e[r] + p;
         return 4;
     }
-    FCSG_HD double2 store(int c, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int c, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         ssprk_update(E, stage, c, p, st[3 * ss], st[0] + (st[ss] * v.x + st[2 * ss] * v.y));
         return {};
     }
@@ -512,7 +547,7 @@ struct PassAc {
         s[0] = E.iq1x + p;
         return 1;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int, const LineCtx&, const double*) const {
         if (r < 2) {
             const double a = st[0];
             E.tA[2 * r][p] = a * v.x;
@@ -577,7 +612,7 @@ struct PassBc {
         s[2] = E.tA[2 * (r - 4) + 1] + p;
         return 3;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         const double d = st[0], t0 = st[ss], t1 = st[2 * ss];
         if (r < 2) {
             E.tA[2 * r][p] = -(t0 + d * v.x);
@@ -627,7 +662,7 @@ struct PassCc {
         s[4] = E.e[2 * r + 1] + p;
         return 5;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         const double a = st[2 * ss];
         ssprk_update(E, stage, 2 * r, p, st[3 * ss], st[0] + a * v.x);
         ssprk_update(E, stage, 2 * r + 1, p, st[4 * ss], st[ss] + a * v.y);
@@ -688,7 +723,7 @@ struct PassXc {
         s[1] = E.mu + p;
         return 2;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         const double a = st[0];
         if (!(r & 1)) {
             const double m = st[ss];
@@ -722,13 +757,24 @@ struct PassYc {
     int stage;
     FCSG_HD PassYc(const EngineDev& e, int s) : E(e), stage(s) {}
     FCSG_HD int mode(int) const { return 1; }
+    // fetch: the load's values in v[0..3] (rounds 0, 1) or v[0..1] (rounds 2,
+    // 3); in rounds 2 and 4 (after the last transform) also the register e0
+    // of the components the preceding update writes, in v[2..3]
     static constexpr int kFetch = 4;
+    static constexpr bool kFetchAtEnd = true;
     FCSG_HD void fetch(int r, long p, double* v) const {
         if (r < 2) {  // e is still unmodified in rounds 0 and 1
             fetch_e(E, p, v);
-        } else {      // rho, rho u: updated only in the last round
+            return;
+        }
+        if (r < 4) {  // rho, rho u: updated only in the last round
             v[0] = ldg1(E.e[0] + p);
             v[1] = ldg1(E.e[1] + p);
+        }
+        if (!(r & 1) && stage >= 1 && stage <= 3) {
+            const int c0 = r == 2 ? 2 : 0;
+            v[2] = ldg1(E.e0[c0] + p);
+            v[3] = ldg1(E.e0[c0 + 1] + p);
         }
     }
     FCSG_HD double2 load(int r, long, const LineCtx&, double2 carry, const double* fv, double* st, int ss) const {
@@ -765,15 +811,15 @@ struct PassYc {
         s[2] = E.tA[c0 + 1] + p;
         return 3;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double* fv) const {
         const double d = st[0];
         if (!(r & 1)) {
             const double m = st[ss];
             return mk2(m * (d * v.x), m * (d * v.y));  // s5 = mu (0 D1 w + iq2y D2 w)
         }
         const int c0 = r == 1 ? 2 : 0;
-        ssprk_update(E, stage, c0, p, st[3 * ss], st[ss] + d * v.x);
-        ssprk_update(E, stage, c0 + 1, p, st[4 * ss], st[2 * ss] + d * v.y);
+        ssprk_update_e0(E, stage, c0, p, st[3 * ss], st[ss] + d * v.x, fv[2]);
+        ssprk_update_e0(E, stage, c0 + 1, p, st[4 * ss], st[2 * ss] + d * v.y, fv[3]);
         return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
@@ -801,7 +847,7 @@ struct PassGA {
         return mk2(q.my, q.theta);
     }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
-    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&, const double*) const {
         E.tW[2 * r][p] = v.x;
         E.tW[2 * r + 1][p] = v.y;
         return {};
@@ -854,7 +900,7 @@ struct PassGB {
         s[6] = E.tW[c0 + 1] + p;
         return 7;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         const int k = r % 3, c0 = 2 * (r / 3);
         if (k == 0) {
             const double a = st[0], b = st[ss], cc = st[2 * ss], d = st[3 * ss], mu = st[4 * ss];
@@ -921,7 +967,7 @@ struct PassFR {
         return mk2(my, kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho);
     }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
-    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&, const double*) const {
         if (smear) {
             const double m = E.m01[p];
             const double2 f = orig(E, r, p);
@@ -955,7 +1001,7 @@ struct PassFC {
         return mk2(fv[0], fv[1]);
     }
     FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
-    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&) const {
+    FCSG_HD double2 store(int r, long p, double2 v, const double*, int, const LineCtx&, const double*) const {
         if (smear) {
             const double m = E.m01[p];
             const double fa = E.tF[2 * r][p], fb = E.tF[2 * r + 1][p];
