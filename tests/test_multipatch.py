@@ -130,3 +130,32 @@ def backend(request):
     if request.param == "emu":
         return "emu", request.getfixturevalue("emu_ctx")
     return "gpu", request.getfixturevalue("gpu_ctx")
+
+
+def test_engine_rejects_inconsistent_inputs(emu_ctx):
+    """Usage errors of the general engine inputs (include/fcsg.h): an L-cut
+    that disagrees with the mask, a malformed cut, interpolation stencils
+    outside the donor, interpolation donors on another rank."""
+    from paper_2506_19370_b200 import _native as N
+
+    patches, validate = _geometry(2)
+    D = M.build_decomposition(patches, _bcs(), NV, validate_overlap=validate)
+    d = D.subs[0]
+    bad = M.SubData(**{**d.__dict__, "cut_i": d.cut_i - 1})  # mask says otherwise
+    with pytest.raises(N.UsageError):
+        EN.Engine(emu_ctx, M.MultiPatchDecomposition(D.patches, [bad], D.plan, D.bcs))
+    bad = M.SubData(**{**d.__dict__, "cut_j": 0})  # only one of the two cuts
+    with pytest.raises(N.UsageError):
+        EN.Engine(emu_ctx, M.MultiPatchDecomposition(D.patches, [bad], D.plan, D.bcs))
+    patches, validate = _geometry(1)
+    D = M.build_decomposition(patches, _bcs(), NV, validate_overlap=validate)
+    si = {k: v.copy() for k, v in D.plan.sol_interps.items()}
+    si["si0"][0] = D.subs[si["src_sub"][0]].ni - 3  # stencil would leave the donor
+    plan = M.Plan(**{**D.plan.__dict__, "sol_interps": si})
+    with pytest.raises(N.UsageError):
+        EN.Engine(emu_ctx, M.MultiPatchDecomposition(D.patches, D.subs, plan, D.bcs))
+    si = {k: v.copy() for k, v in D.plan.sol_interps.items()}
+    si["src_sub"][0] = -1  # donors must be local
+    plan = M.Plan(**{**D.plan.__dict__, "sol_interps": si})
+    with pytest.raises(N.UsageError):
+        EN.Engine(emu_ctx, M.MultiPatchDecomposition(D.patches, D.subs, plan, D.bcs))
