@@ -830,9 +830,11 @@ class MultiPatchDecomposition:
         return np.ascontiguousarray(e * (d.mask != 0)[None])
 
 
-def build_decomposition(patches: list, bcs: dict, nv: int, nf: int = 5, validate_overlap: bool = True):
+def build_decomposition(patches: list, bcs: dict, nv: int, nf: int = 5, validate_overlap: bool = True,
+                        fast: bool = False):
     """Engine::init's geometry part (src/runtime.cpp:293-305): ids, overlap
-    check, SubpatchData, plan. Patches must already be subdivided."""
+    check, SubpatchData, plan. Patches must already be subdivided. fast: the
+    vectorised path (same results; for large decompositions)."""
     for k, p in enumerate(patches):
         p.index = k
         if p.nv <= nf:
@@ -844,7 +846,501 @@ def build_decomposition(patches: list, bcs: dict, nv: int, nf: int = 5, validate
             sp.global_id = gid
             gid += 1
     if validate_overlap:
-        check_min_overlap(patches, nv)
-    subs = [init_subpatch_data(p, sp, nf, bcs) for p in patches for sp in p.subpatches]
-    plan = build_plan(patches, subs, nf)
+        (_check_min_overlap_fast if fast else check_min_overlap)(patches, nv)
+    init = _init_subpatch_data_fast if fast else init_subpatch_data
+    subs = [init(p, sp, nf, bcs) for p in patches for sp in p.subpatches]
+    plan = (_build_plan_fast if fast else build_plan)(patches, subs, nf)
     return MultiPatchDecomposition(patches, subs, plan, bcs, nf)
+
+
+# ---------------------------------------------------------------------------
+# vectorised builder: the same computations as above on numpy arrays (one
+# subpatch or one patch side at a time), for decompositions of millions of
+# points. build_decomposition(..., fast=True) uses it; tests/
+# test_multipatch.py checks it against the scalar path.
+
+
+def _map_arr(M, q1, q2):
+    if isinstance(M, AnnulusMap):
+        th = M.t0 + q1 * M.dt
+        r = M.r0 + q2 * (M.r1 - M.r0)
+        return M.c[0] + r * np.cos(th), M.c[1] + r * np.sin(th)
+    return M(q1, q2)
+
+
+def _jac_arr(M, q1, q2):
+    if isinstance(M, AnnulusMap):
+        th = M.t0 + q1 * M.dt
+        r = M.r0 + q2 * (M.r1 - M.r0)
+        dr = M.r1 - M.r0
+        return (-r * M.dt * np.sin(th), dr * np.cos(th), r * M.dt * np.cos(th), dr * np.sin(th))
+    if isinstance(M, AffineMap):
+        J = M.jacobian(0.0, 0.0)
+        z = np.zeros_like(np.asarray(q1, dtype=np.float64))
+        return tuple(z + v for v in J)
+    return M.jacobian(q1, q2)
+
+
+def _invert_arr(M, X, Y, s1, s2, tol=1e-10, max_iter=50):
+    """Mapping.invert for arrays of points: (ok, q1, q2)"""
+    n = X.shape[0]
+    if isinstance(M, AffineMap):
+        a, b, c, d = M.jacobian(0.0, 0.0)
+        if abs(a * d - b * c) < 1e-300:
+            return np.zeros(n, bool), X * 0, Y * 0
+        ia, ib, ic, id_ = _inv((a, b, c, d))
+        vx, vy = X - M.o[0], Y - M.o[1]
+        return np.ones(n, bool), ia * vx + ib * vy, ic * vx + id_ * vy
+    if isinstance(M, AnnulusMap):
+        dx, dy = X - M.c[0], Y - M.c[1]
+        r = np.hypot(dx, dy)
+        ok = ~(r < 1e-300)
+        q2 = (r - M.r0) / (M.r1 - M.r0)
+        th = np.arctan2(dy, dx)
+        q1 = (th - M.t0) / M.dt
+        period = 2 * math.pi / abs(M.dt)
+        t = (q1 - s1) / period
+        q1 = q1 - period * (np.sign(t) * np.floor(np.abs(t) + 0.5))
+        return ok, q1, q2
+    q1, q2 = s1.astype(np.float64).copy(), s2.astype(np.float64).copy()
+    mx, my = _map_arr(M, q1, q2)
+    res = np.hypot(mx - X, my - Y)
+    active = np.ones(n, bool)   # still iterating
+    failed = np.zeros(n, bool)
+    for _ in range(max_iter):
+        active &= ~(res <= tol)
+        if not active.any():
+            break
+        idx = np.nonzero(active)[0]
+        a, b, c, d = _jac_arr(M, q1[idx], q2[idx])
+        det = a * d - b * c
+        sing = np.abs(det) < 1e-300
+        ia, ib, ic, id_ = d / det, -b / det, -c / det, a / det
+        mx, my = _map_arr(M, q1[idx], q2[idx])
+        vx, vy = X[idx] - mx, Y[idx] - my
+        dq1, dq2 = ia * vx + ib * vy, ic * vx + id_ * vy
+        step = np.ones(idx.size)
+        done = sing.copy()
+        for h in range(8):
+            qn1, qn2 = q1[idx] + step * dq1, q2[idx] + step * dq2
+            nx, ny = _map_arr(M, qn1, qn2)
+            rn = np.hypot(nx - X[idx], ny - Y[idx])
+            take = ~done & (rn < res[idx])
+            q1[idx[take]], q2[idx[take]], res[idx[take]] = qn1[take], qn2[take], rn[take]
+            done |= take
+            step = np.where(done, step, step * 0.5)
+        stalled = ~done
+        fail_idx = idx[sing | stalled]
+        failed[fail_idx] = True
+        active[fail_idx] = False
+    ok = ~failed & (res <= tol)
+    return ok, q1, q2
+
+
+def _contains_arr(p: Patch, X, Y, margin):
+    """Patch.contains for arrays of points: (ok, q1, q2)"""
+    ns = 9
+    samp = [(a / ns, b / ns) for a in range(ns + 1) for b in range(ns + 1)
+            if not (p.kind == C1 and a / ns < 0.5 and b / ns < 0.5)]
+    sx = np.array([p.map(q1, q2)[0] for q1, q2 in samp])
+    sy = np.array([p.map(q1, q2)[1] for q1, q2 in samp])
+    best = np.full(X.shape[0], 1e300)
+    bq1 = np.full(X.shape[0], 0.5)
+    bq2 = np.full(X.shape[0], 0.5)
+    for k, (q1, q2) in enumerate(samp):
+        dd = np.hypot(sx[k] - X, sy[k] - Y)
+        better = dd < best
+        best = np.where(better, dd, best)
+        bq1 = np.where(better, q1, bq1)
+        bq2 = np.where(better, q2, bq2)
+    ok, q1, q2 = _invert_arr(p.map, X, Y, bq1, bq2)
+    mx, my = _map_arr(p.map, q1, q2)
+    ok &= ~(np.hypot(mx - X, my - Y) > 1e-8)
+    lo, hi = -margin, 1.0 + margin
+    if p.periodic1:
+        ok &= ~((q2 < lo) | (q2 > hi))
+    else:
+        ok &= ~((q1 < lo) | (q1 > hi) | (q2 < lo) | (q2 > hi))
+    if p.kind == C1:
+        ok &= ~((q1 < 0.5 - margin) & (q2 < 0.5 - margin))
+    return ok, q1, q2
+
+
+def _raw_window_arr(p: Patch, sp: Subpatch, u, v, nf):
+    band = 2.0 * p.nv
+    eps = 1e-9
+
+    def ramp(dist):
+        t = np.minimum(np.maximum((dist - nf) / (band - nf), 0.0), 1.0)
+        s = np.sin(0.5 * math.pi * t)
+        return s * s
+
+    w = np.ones(np.broadcast(u, v).shape)
+    lo = np.where(v < sp.j_cut - eps, sp.i_cut, sp.i0).astype(np.float64)
+    internal = np.ones(w.shape, bool)
+    if not p.periodic1 and p.sides[0].on_gamma:
+        internal &= ~(lo == 0)
+    if p.kind == C1:
+        sel = (lo == p.i_corner) & (v < p.j_corner - eps)
+        internal = np.where(sel, not p.wall_q1.on_gamma, internal)
+    w = np.where(internal, w * ramp(u - lo), w)
+    if not (not p.periodic1 and sp.i1 == p.np1 - 1 and p.sides[1].on_gamma):
+        w = w * ramp(sp.i1 - u)
+    lo = np.where(u < sp.i_cut - eps, sp.j_cut, sp.j0).astype(np.float64)
+    internal = np.ones(w.shape, bool)
+    if p.sides[2].on_gamma:
+        internal &= ~(lo == 0)
+    if p.kind == C1:
+        sel = (lo == p.j_corner) & (u < p.i_corner - eps)
+        internal = np.where(sel, not p.wall_q2.on_gamma, internal)
+    w = np.where(internal, w * ramp(v - lo), w)
+    if not (sp.j1 == p.np2 - 1 and p.sides[3].on_gamma):
+        w = w * ramp(sp.j1 - v)
+    return w
+
+
+def _place_arr(p: Patch, sp: Subpatch, u, v, eps):
+    u = np.array(u, dtype=np.float64, copy=True)
+    if p.periodic1:
+        np1 = float(p.np1)
+        while True:
+            m = u < sp.i0 - eps
+            if not m.any():
+                break
+            u[m] += np1
+        while True:
+            m = u > sp.i1 + eps
+            if not m.any():
+                break
+            u[m] -= np1
+    ok = ~((u < sp.i0 - eps) | (u > sp.i1 + eps) | (v < sp.j0 - eps) | (v > sp.j1 + eps))
+    ok &= ~((u < sp.i_cut - eps) & (v < sp.j_cut - eps))
+    return ok, u
+
+
+def _init_subpatch_data_fast(p: Patch, sp: Subpatch, nf: int, bcs: dict) -> SubData:
+    ni, nj = sp.ni, sp.nj
+    mask = fringe_mask(p, sp, nf)
+    I, J = np.meshgrid(np.arange(sp.i0, sp.i1 + 1), np.arange(sp.j0, sp.j1 + 1))
+    valid = mask != 0
+    q1, q2 = I * p.h1, J * p.h2
+    M = p.map
+    x, y = _map_arr(M, q1, q2)
+    a, b, c, dd = _jac_arr(M, q1, q2)
+    det = a * dd - b * c
+    ia, ib, ic, id_ = dd / det, -b / det, -c / det, a / det
+    ax, ay = _map_arr(M, q1 + p.h1, q2)
+    bx, by = _map_arr(M, q1 - p.h1, q2)
+    cx, cy = _map_arr(M, q1, q2 + p.h2)
+    dx, dy = _map_arr(M, q1, q2 - p.h2)
+    h1p = np.maximum(np.hypot(ax - x, ay - y), np.hypot(x - bx, y - by))
+    h2p = np.maximum(np.hypot(cx - x, cy - y), np.hypot(x - dx, y - dy))
+    z = lambda arr: np.where(valid, arr, 0.0)  # noqa: E731
+    base = init_subpatch_data_lines(p, sp, bcs)
+    l_cut = sp.i_cut > sp.i0 and sp.j_cut > sp.j0
+    return SubData(sp, p.index, ni, nj, p.h1, p.h2, sp.i_cut - sp.i0 if l_cut else 0,
+                   sp.j_cut - sp.j0 if l_cut else 0, mask, z(x), z(y), z(ia), z(ic), z(ib), z(id_),
+                   z(np.minimum(h1p, h2p)), z(np.maximum(h1p, h2p)), np.zeros((nj, ni)), *base)
+
+
+def init_subpatch_data_lines(p: Patch, sp: Subpatch, bcs: dict):
+    """the resolved line-end BCs of init_subpatch_data (rows lo, hi; cols lo, hi)"""
+    def resolve(axis, line, high):
+        internal, side = classify_end(p, sp, axis, line, high)
+        if internal or side is None:
+            return None
+        if side.tag not in bcs:
+            raise ValueError(f"no boundary condition for side tag '{side.tag}'")
+        bc = bcs[side.tag]
+        return (bc.kind, tuple(bc.state), bc.pressure)
+
+    return ([resolve(0, j, False) for j in range(sp.j0, sp.j1 + 1)],
+            [resolve(0, j, True) for j in range(sp.j0, sp.j1 + 1)],
+            [resolve(1, i, False) for i in range(sp.i0, sp.i1 + 1)],
+            [resolve(1, i, True) for i in range(sp.i0, sp.i1 + 1)])
+
+
+def _check_min_overlap_fast(patches: list, nv: int):
+    depth = 2 * nv + 1
+    orphans = []
+    for pi, p in enumerate(patches):
+        pts = []
+        if not p.periodic1:
+            if not p.sides[0].on_gamma:
+                pts += [(0, i, j) for j in range(p.np2) for i in range(min(depth, p.np1))]
+            if not p.sides[1].on_gamma:
+                pts += [(1, i, j) for j in range(p.np2) for i in range(max(0, p.np1 - depth), p.np1)]
+        if not p.sides[2].on_gamma:
+            pts += [(2, i, j) for i in range(p.np1) for j in range(min(depth, p.np2))]
+        if not p.sides[3].on_gamma:
+            pts += [(3, i, j) for i in range(p.np1) for j in range(max(0, p.np2 - depth), p.np2)]
+        pts = [t for t in pts if p.lattice_valid(t[1], t[2])]
+        if not pts:
+            continue
+        arr = np.array(pts)
+        X, Y = _map_arr(p.map, arr[:, 1] * p.h1, arr[:, 2] * p.h2)
+        covered = np.zeros(len(pts), bool)
+        for po, p2 in enumerate(patches):
+            if po == pi:
+                continue
+            idx = np.nonzero(~covered)[0]
+            if idx.size == 0:
+                break
+            ok, _, _ = _contains_arr(p2, X[idx], Y[idx], 1e-9)
+            covered[idx[ok]] = True
+        for k in np.nonzero(~covered)[0]:
+            orphans.append((pi, int(arr[k, 0]), int(arr[k, 1]), int(arr[k, 2]), (float(X[k]), float(Y[k]))))
+    if orphans:
+        lines = [f"FAIL: {len(orphans)} orphan layer points"]
+        lines += [f"  patch {a} side {b} ({i},{j}) at ({x[0]:g},{x[1]:g})" for a, b, i, j, x in orphans[:8]]
+        raise DecompositionError("minimum-overlap check failed:\n" + "\n".join(lines))
+    _check_c1_corners(patches)  # the S-C1 corner rule (few points: scalar path)
+
+
+def _check_c1_corners(patches):
+    fails = []
+    for p in patches:
+        if p.kind != C1:
+            continue
+        corner = p.map(0.5, 0.5)
+        reached = False
+        for ps in patches:
+            if ps.kind != S:
+                continue
+            q = ps.contains(corner, 1e-7)
+            if q is None:
+                continue
+            tol = 1e-6
+            if ((ps.sides[0].on_gamma and abs(q[0]) < tol) or (ps.sides[1].on_gamma and abs(q[0] - 1) < tol)
+                    or (ps.sides[2].on_gamma and abs(q[1]) < tol) or (ps.sides[3].on_gamma and abs(q[1] - 1) < tol)):
+                reached = True
+                break
+        if not reached:
+            fails.append(f"C1 patch {p.index}: no S patch reaches its corner point")
+    if fails:
+        raise DecompositionError("minimum-overlap check failed:\nFAIL: 0 orphan layer points\n  " + "\n  ".join(fails))
+
+
+def _stencil_ok(mask):
+    """ok[sj, si]: the 6x6 block at (si, sj) is all interior (mask == 1)"""
+    m = (mask == 1).astype(np.int32)
+    c = np.zeros((m.shape[0] + 1, m.shape[1] + 1), np.int64)
+    c[1:, 1:] = m.cumsum(0).cumsum(1)
+    nj, ni = m.shape
+    if nj < 6 or ni < 6:
+        return np.zeros((max(nj - 5, 0), max(ni - 5, 0)), bool)
+    s = c[6:, 6:] - c[:-6, 6:] - c[6:, :-6] + c[:-6, :-6]
+    return s == 36
+
+
+def _lagrange_arr(t, origin):
+    w = []
+    for a in range(6):
+        num = np.ones_like(t)
+        den = 1.0
+        for b in range(6):
+            if a == b:
+                continue
+            num = num * (t - (origin + b))
+            den *= float(a - b)
+        w.append(num / den)
+    return np.stack(w, axis=-1)
+
+
+def _build_interp_arr(ds: SubData, okst, u, v, slack):
+    """build_interp (src/runtime.cpp:115-146) for arrays of points of one donor:
+    (found, si0, sj0, wx, wy)"""
+    sp2 = ds.sp
+    tu, tv = u - sp2.i0, v - sp2.j0
+    bi = np.floor(tu).astype(np.int64) - 2
+    bj = np.floor(tv).astype(np.int64) - 2
+    n = u.shape[0]
+    best_pen = np.full(n, 1e300)
+    bsi = np.full(n, -1, np.int64)
+    bsj = np.full(n, -1, np.int64)
+    for dj in range(-4, 5):
+        for di in range(-4, 5):
+            si, sj = bi + di, bj + dj
+            inb = (si >= 0) & (si + 5 < ds.ni) & (sj >= 0) & (sj + 5 < ds.nj)
+            out_u = np.maximum(np.maximum(0.0, si - tu), tu - (si + 5))
+            out_v = np.maximum(np.maximum(0.0, sj - tv), tv - (sj + 5))
+            cand = inb & ~(out_u > slack) & ~(out_v > slack)
+            ok = np.zeros(n, bool)
+            ci = np.nonzero(cand)[0]
+            ok[ci] = okst[sj[ci], si[ci]]
+            pen = out_u + out_v + 0.01 * (abs(di) + abs(dj))
+            take = ok & (pen < best_pen)
+            best_pen = np.where(take, pen, best_pen)
+            bsi = np.where(take, si, bsi)
+            bsj = np.where(take, sj, bsj)
+    found = bsi >= 0
+    wx = _lagrange_arr(tu, bsi.astype(np.float64))
+    wy = _lagrange_arr(tv, bsj.astype(np.float64))
+    return found, bsi, bsj, wx, wy
+
+
+def _build_plan_fast(patches: list, subs: list, nf: int) -> Plan:
+    by_gid = {d.sp.global_id: d for d in subs}
+    boxes = {}
+    for d in subs:
+        valid = d.mask != 0
+        b = boxes.setdefault(d.patch, [1e300, -1e300, 1e300, -1e300])
+        b[0], b[1] = min(b[0], float(d.x[valid].min())), max(b[1], float(d.x[valid].max()))
+        b[2], b[3] = min(b[2], float(d.y[valid].min())), max(b[3], float(d.y[valid].max()))
+    margin = {p.index: 2.0 * max(p.max_spacing()) for p in patches}
+    okst = {d.sp.global_id: _stencil_ok(d.mask) for d in subs}
+    sol_c, vis_c, sol_i, vis_i = [], [], [], []
+    for d in subs:
+        p = patches[d.patch]
+        sp = d.sp
+        gid = sp.global_id
+        # the recipient points in the reference's order (rows, then along the row)
+        jl, il = np.nonzero(d.mask != 0)
+        I, J = (il + sp.i0).astype(np.float64), (jl + sp.j0).astype(np.float64)
+        dst = jl * d.ni + il
+        X, Y = d.x[jl, il], d.y[jl, il]
+        n = dst.size
+        w_own = _raw_window_arr(p, sp, I, J, nf)
+        slots = []  # contributors in the reference's order: (copy, sub, ok, u, v, w, src)
+        for sp2 in p.subpatches:
+            if sp2.global_id == gid:
+                continue
+            ok, u = _place_arr(p, sp2, I, J, 1e-9)
+            if not ok.any():
+                continue
+            v = J
+            i2 = np.sign(u) * np.floor(np.abs(u) + 0.5)
+            j2 = np.sign(v) * np.floor(np.abs(v) + 0.5)
+            src = ((j2 - sp2.j0) * sp2.ni + (i2 - sp2.i0)).astype(np.int64)
+            w = np.where(ok, _raw_window_arr(p, sp2, u, v, nf), 0.0)
+            slots.append((True, sp2.global_id, ok, u, v, w, src))
+        for p2 in patches:
+            if p2.index == p.index:
+                continue
+            bb, m = boxes[p2.index], margin[p2.index]
+            inbox = ~((X < bb[0] - m) | (X > bb[1] + m) | (Y < bb[2] - m) | (Y > bb[3] + m))
+            idx = np.nonzero(inbox)[0]
+            if idx.size == 0:
+                continue
+            okc, q1, q2 = _contains_arr(p2, X[idx], Y[idx], 1e-9)
+            uu = np.zeros(n)
+            vv = np.zeros(n)
+            has = np.zeros(n, bool)
+            has[idx[okc]] = True
+            uu[idx] = q1 / p2.h1
+            vv[idx] = q2 / p2.h2
+            for sp2 in p2.subpatches:
+                ok, u = _place_arr(p2, sp2, uu, vv, 1e-7)
+                ok &= has
+                if not ok.any():
+                    continue
+                w = np.where(ok, _raw_window_arr(p2, sp2, u, vv, nf), 0.0)
+                slots.append((False, sp2.global_id, ok, u, vv, w, None))
+        denom = w_own.copy()
+        for s_ in slots:
+            denom = np.where(s_[2], denom + s_[5], denom)
+        if not (denom > 1e-14).all():
+            k = int(np.nonzero(~(denom > 1e-14))[0][0])
+            raise DecompositionError(f"window partition vanishes at ({X[k]:f}, {Y[k]:f}), subpatch {gid}")
+        d.w_norm[jl, il] = w_own / denom
+        for copy, sub, ok, u, v, w, src in slots:
+            wn = w / denom
+            sel = ok & ~(wn <= 1e-15)
+            if not sel.any():
+                continue
+            k = np.nonzero(sel)[0]
+            if copy:
+                vis_c.append((np.full(k.size, gid), dst[k], np.full(k.size, sub), src[k], wn[k]))
+            else:
+                ds = by_gid[sub]
+                found, si, sj, wx, wy = _build_interp_arr(ds, okst[sub], u[k], v[k], 2.5)
+                if not found.all():
+                    kk = k[np.nonzero(~found)[0][0]]
+                    raise DecompositionError(f"no admissible viscosity stencil in donor subpatch {sub} for "
+                                             f"({X[kk]:f}, {Y[kk]:f})")
+                vis_i.append((np.full(k.size, gid), dst[k], np.full(k.size, sub), si, sj, wx, wy, wn[k]))
+        # solution entries of the fringe points
+        fringe = d.mask[jl, il] == 2
+        best_w = np.full(n, -1.0)
+        best_sub = np.full(n, -1, np.int64)
+        best_src = np.zeros(n, np.int64)
+        for copy, sub, ok, u, v, w, src in slots:
+            if not copy:
+                continue
+            dm = by_gid[sub].mask.reshape(-1)
+            good = ok & fringe
+            gi = np.nonzero(good)[0]
+            good[gi] = dm[src[gi]] == 1
+            take = good & ((best_sub < 0) | (w > best_w))
+            best_w = np.where(take, w, best_w)
+            best_sub = np.where(take, sub, best_sub)
+            best_src = np.where(take, src, best_src)
+        hc = fringe & (best_sub >= 0)
+        k = np.nonzero(hc)[0]
+        if k.size:
+            sol_c.append((np.full(k.size, gid), dst[k], best_sub[k], best_src[k]))
+        need = np.nonzero(fringe & (best_sub < 0))[0]
+        if need.size:
+            cands = [(s_[1], s_[2], s_[3], s_[4], s_[5]) for s_ in slots if not s_[0]]
+            done = np.zeros(need.size, bool)
+            res = {}
+            # candidates by raw window, largest first (stable on ties)
+            W = np.stack([c[4][need] for c in cands], axis=1) if cands else np.zeros((need.size, 0))
+            OK = np.stack([c[1][need] for c in cands], axis=1) if cands else np.zeros((need.size, 0), bool)
+            order = np.argsort(-np.where(OK, W, -np.inf), axis=1, kind="stable")
+            for rank in range(len(cands)):
+                todo = np.nonzero(~done)[0]
+                if todo.size == 0:
+                    break
+                ci = order[todo, rank]
+                for cidx in np.unique(ci):
+                    sel = todo[ci == cidx]
+                    sel = sel[OK[sel, cidx]]
+                    if sel.size == 0:
+                        continue
+                    sub, ok, u, v, w = cands[cidx]
+                    pts = need[sel]
+                    found, si, sj, wx, wy = _build_interp_arr(by_gid[sub], okst[sub], u[pts], v[pts], 0.5)
+                    for q, f in enumerate(found):
+                        if f:
+                            res[int(sel[q])] = (sub, int(si[q]), int(sj[q]), wx[q], wy[q])
+                    done[sel[found]] = True
+            if not done.all():
+                kk = need[np.nonzero(~done)[0][0]]
+                raise DecompositionError(f"orphan fringe point at ({X[kk]:f}, {Y[kk]:f}), subpatch {gid}")
+            keys = sorted(res)
+            sol_i.append((np.full(len(keys), gid), dst[need[keys]],
+                          np.array([res[q][0] for q in keys]), np.array([res[q][1] for q in keys]),
+                          np.array([res[q][2] for q in keys]), np.array([res[q][3] for q in keys]),
+                          np.array([res[q][4] for q in keys])))
+    i32 = lambda a: np.asarray(a, dtype=np.int32)  # noqa: E731
+
+    def cat(parts, k, dt):
+        return np.concatenate([np.asarray(x[k], dtype=dt) for x in parts]) if parts else np.zeros(0, dt)
+
+    def cat6(parts, k):
+        return np.concatenate([np.asarray(x[k], dtype=np.float64).reshape(-1, 6) for x in parts]) if parts \
+            else np.zeros((0, 6))
+
+    # viscosity entries were gathered contributor by contributor; the
+    # reference lists them point by point, contributors in order: a stable
+    # sort by (recipient, point) restores that order
+    def point_major(parts):
+        if not parts:
+            return parts
+        cols = [np.concatenate([np.asarray(x[k]) for x in parts]) for k in range(len(parts[0]))]
+        o = np.lexsort((cols[1], cols[0]))
+        return [tuple(c[o] for c in cols)]
+
+    vis_c = point_major(vis_c)
+    vis_i = point_major(vis_i)
+    return Plan(i32(cat(sol_c, 0, np.int64)), i32(cat(sol_c, 1, np.int64)), i32(cat(sol_c, 2, np.int64)),
+                i32(cat(sol_c, 3, np.int64)), i32(cat(vis_c, 0, np.int64)), i32(cat(vis_c, 1, np.int64)),
+                i32(cat(vis_c, 2, np.int64)), i32(cat(vis_c, 3, np.int64)), cat(vis_c, 4, np.float64),
+                sol_interps=dict(dst_sub=i32(cat(sol_i, 0, np.int64)), dst=i32(cat(sol_i, 1, np.int64)),
+                                 src_sub=i32(cat(sol_i, 2, np.int64)), si0=i32(cat(sol_i, 3, np.int64)),
+                                 sj0=i32(cat(sol_i, 4, np.int64)), wx=cat6(sol_i, 5), wy=cat6(sol_i, 6)),
+                visc_interps=dict(dst_sub=i32(cat(vis_i, 0, np.int64)), dst=i32(cat(vis_i, 1, np.int64)),
+                                  src_sub=i32(cat(vis_i, 2, np.int64)), si0=i32(cat(vis_i, 3, np.int64)),
+                                  sj0=i32(cat(vis_i, 4, np.int64)), wx=cat6(vis_i, 5), wy=cat6(vis_i, 6),
+                                  w=cat(vis_i, 7, np.float64)))

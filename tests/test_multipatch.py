@@ -159,3 +159,29 @@ def test_engine_rejects_inconsistent_inputs(emu_ctx):
     plan = M.Plan(**{**D.plan.__dict__, "sol_interps": si})
     with pytest.raises(N.UsageError):
         EN.Engine(emu_ctx, M.MultiPatchDecomposition(D.patches, D.subs, plan, D.bcs))
+
+
+@pytest.mark.parametrize("which", GEOMS)
+def test_vectorised_builder_equals_scalar(which):
+    """build_decomposition(fast=True) -- the numpy path used for large
+    decompositions -- produces the scalar path's geometry and plan."""
+    patches, validate = _geometry(which)
+    A = M.build_decomposition(patches, _bcs(), NV, validate_overlap=validate)
+    patches, validate = _geometry(which)
+    B = M.build_decomposition(patches, _bcs(), NV, validate_overlap=validate, fast=True)
+    for a, b in zip(A.subs, B.subs):
+        assert np.array_equal(a.mask, b.mask)
+        for f in ("x", "y", "iq1x", "iq2x", "iq1y", "iq2y", "h_min", "h_max", "w_norm"):
+            assert rel_err(getattr(b, f), getattr(a, f)) < 1e-14, f
+        for f in ("bc_row_lo", "bc_row_hi", "bc_col_lo", "bc_col_hi"):
+            assert getattr(a, f) == getattr(b, f)
+    for f in ("sol_dst_sub", "sol_dst", "sol_src_sub", "sol_src", "v_dst_sub", "v_dst", "v_src_sub", "v_src"):
+        assert np.array_equal(getattr(A.plan, f), getattr(B.plan, f)), f
+    assert np.array_equal(A.plan.v_w, B.plan.v_w)
+    for nm in ("sol_interps", "visc_interps"):
+        a, b = getattr(A.plan, nm), getattr(B.plan, nm)
+        for k in a:
+            if k in ("wx", "wy", "w"):
+                assert rel_err(b[k], a[k]) < 1e-13 if len(a[k]) else len(b[k]) == 0
+            else:
+                assert np.array_equal(a[k], b[k]), (nm, k)
