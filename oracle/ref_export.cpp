@@ -323,6 +323,10 @@ void* ref_engine_problem(const char* name, double target_h, double cfl, double T
  *   1  two patches with non-coincident lattices: a Cartesian I patch and a
  *      bilinear S patch overlapping it (6x6 Lagrange interpolation both ways),
  *      slip walls, inflow, supersonic outflow
+ *   3  the config-3 cylinder layout of problems.cylinder_flow(full=False):
+ *      periodic annulus r in [1, 2.2] (subdivide_Q(8, 1, 65, 9)) and four
+ *      Cartesian I patches (n0 = 120) over [-4, 12] x [-6, 6], Mach 3 free
+ *      stream, slip walls, inflow / supersonic outflow (n0 ignored)
  *   2  a C1 corner patch alone (CurveSumMap of two non-orthogonal segments,
  *      subdivide_L: one L-shaped subpatch), slip walls at the reentrant
  *      corner; the overlap validation that asks for an S patch at the corner
@@ -358,6 +362,7 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
         bcs["in"] = in;
         Vec2 bump{0.0, 0.0};
         double u0 = 0.5, v0 = 0.0;
+        bool free_stream = false;
         if (which == 0) {
             Patch ring;
             ring.kind = PatchKind::S;
@@ -395,19 +400,46 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             bump = {0.6, 0.6};
             u0 = 0.3;
             v0 = 0.2;
+        } else if (which == 3) {
+            Patch ring;
+            ring.kind = PatchKind::S;
+            ring.map = std::make_shared<geom::AnnulusMap>(Vec2{0.0, 0.0}, 1.0, 2.2, -M_PI, 2 * M_PI);
+            ring.periodic1 = true;
+            ring.sides = {interior, interior, SideInfo{true, "wall"}, interior};
+            dec.patches.push_back(std::move(ring));
+            auto rect = [&](Vec2 o, Vec2 e1, Vec2 e2, std::array<SideInfo, 4> sd) {
+                Patch p;
+                p.kind = PatchKind::I;
+                p.map = std::make_shared<geom::AffineMap>(o, e1, e2);
+                p.sides = sd;
+                dec.patches.push_back(std::move(p));
+            };
+            rect({-4.0, -6.0}, {2.8, 0.0}, {0.0, 12.0},
+                 {SideInfo{true, "in"}, interior, SideInfo{true, "wall"}, SideInfo{true, "wall"}});
+            rect({1.2, -6.0}, {10.8, 0.0}, {0.0, 12.0},
+                 {interior, SideInfo{true, "out"}, SideInfo{true, "wall"}, SideInfo{true, "wall"}});
+            rect({-1.7, 1.2}, {3.4, 0.0}, {0.0, 4.8}, {interior, interior, interior, SideInfo{true, "wall"}});
+            rect({-1.7, -6.0}, {3.4, 0.0}, {0.0, 4.8}, {interior, interior, SideInfo{true, "wall"}, interior});
+            bcs["in"].state = euler::conservative(1.4, 3.0, 0.0, 1.0);
+            free_stream = true;
         } else {
             throw UsageError("unknown test geometry");
         }
         for (size_t k = 0; k < dec.patches.size(); ++k) dec.patches[k].index = static_cast<int>(k);
-        for (auto& p : dec.patches) {
-            if (p.kind == PatchKind::C1)
-                geom::subdivide_L(p, 2, n0, nv);
-            else if (p.periodic1)
-                geom::subdivide_Q(p, 3, 1, n0, nv);
-            else if (p.index == 1)
-                geom::subdivide_Q(p, 2, 1, n0 + 6, nv);  // a different lattice and subpatch shape
-            else
-                geom::subdivide_Q(p, 1, 1, n0, nv);
+        if (which == 3) {
+            const int rs[5][2] = {{8, 1}, {1, 5}, {5, 5}, {1, 2}, {1, 2}};
+            for (auto& p : dec.patches) geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], p.index ? 120 : 65, nv);
+        } else {
+            for (auto& p : dec.patches) {
+                if (p.kind == PatchKind::C1)
+                    geom::subdivide_L(p, 2, n0, nv);
+                else if (p.periodic1)
+                    geom::subdivide_Q(p, 3, 1, n0, nv);
+                else if (p.index == 1)
+                    geom::subdivide_Q(p, 2, 1, n0 + 6, nv);  // a different lattice and subpatch shape
+                else
+                    geom::subdivide_Q(p, 1, 1, n0, nv);
+            }
         }
         dec.assign_global_ids();
         run::EngineConfig cfg;
@@ -421,7 +453,8 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             cfg.classifier.variant = visc::ClassifierConfig::Variant::ann;
             cfg.classifier.weight_path = weight_path;
         }
-        auto ic = [bump, u0, v0](double x, double y) {
+        auto ic = [bump, u0, v0, free_stream](double x, double y) {
+            if (free_stream) return euler::conservative(1.4, 3.0, 0.0, 1.0);
             const double r2 = (x - bump.x) * (x - bump.x) + (y - bump.y) * (y - bump.y);
             const double rho = 1.0 + 0.2 * std::exp(-r2 / 0.02);
             return euler::conservative(rho, u0, v0, 0.7);

@@ -32,7 +32,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .geometry import BcSpec, DecompositionError, Plan, SideInfo  # noqa: F401  (re-exported)
+from .geometry import (INFLOW, NOSLIP_ADIABATIC, OUTFLOW_PRESSURE, SLIP_WALL, SUPERSONIC_OUTFLOW,  # noqa: F401
+                       ZERO_NORMAL_ALL, BcSpec, DecompositionError, Plan, SideInfo)
 
 
 class GeometryError(RuntimeError):

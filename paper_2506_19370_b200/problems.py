@@ -13,6 +13,9 @@ same generator as the reference's private Rng (src/viscosity.cpp:300-313).
 * ``vortex_tiles``      config 5: one I patch tiled by 256x256 subpatches
   (subdivide_Q(r, s, 238, 9): 19-point intra-patch overlap), isentropic vortex
   plus 1e-3 seeded noise on the primitives.
+* ``cylinder_flow``     config 3: Mach 3 flow past a unit cylinder in
+  [-4, 12] x [-6, 6]: a periodic annulus (2048 x 147) around the body and four
+  Cartesian I patches of 256 x 256 subpatches around it (multipatch.py).
 """
 from __future__ import annotations
 
@@ -168,3 +171,44 @@ def initial_state(dec, ic, sub):
         return np.ascontiguousarray(ic(d.x, d.y, I, J))
     except TypeError:
         return np.ascontiguousarray(ic(d.x, d.y))
+
+
+def cylinder_flow(full=True):
+    """BASELINE config 3 (multi-patch, curvilinear). The reference's own
+    cylinder decomposition fails its overlap check, so
+    the patches are laid out here: an annulus r in [1, 2.2] around the body
+    (periodic q1, slip wall at r = 1; subdivide_Q(16, 1, 129, 9): 2048 x 147,
+    SURVEY D4) and four Cartesian I patches covering the rest of
+    [-4, 12] x [-6, 6] (inflow on the left, supersonic outflow on the right,
+    slip walls at y = +-6) with 256 x 256 subpatches; free stream rho = 1.4,
+    p = 1, u = 3 (Mach 3). full=False: the same layout at about a quarter of
+    the resolution (0.70M points; ring 512 x 83, Cartesian 138 x 138)."""
+    from . import multipatch as M
+    SI = M.SideInfo
+    ring = M.Patch(M.S, M.AnnulusMap((0.0, 0.0), 1.0, 2.2, -math.pi, 2 * math.pi),
+                   [SI(), SI(), SI(True, "body"), SI()], periodic1=True)
+    left = M.Patch(M.I, M.AffineMap((-4.0, -6.0), (2.8, 0.0), (0.0, 12.0)),
+                   [SI(True, "in"), SI(), SI(True, "wall"), SI(True, "wall")])
+    right = M.Patch(M.I, M.AffineMap((1.2, -6.0), (10.8, 0.0), (0.0, 12.0)),
+                    [SI(), SI(True, "out"), SI(True, "wall"), SI(True, "wall")])
+    top = M.Patch(M.I, M.AffineMap((-1.7, 1.2), (3.4, 0.0), (0.0, 4.8)), [SI(), SI(), SI(), SI(True, "wall")])
+    bottom = M.Patch(M.I, M.AffineMap((-1.7, -6.0), (3.4, 0.0), (0.0, 4.8)), [SI(), SI(), SI(True, "wall"), SI()])
+    patches = [ring, left, right, top, bottom]
+    for k, p in enumerate(patches):
+        p.index = k
+    ring_r, ring_n0, n0 = (16, 129, 238) if full else (8, 65, 120)
+    M.subdivide_Q(ring, ring_r, 1, ring_n0, 9)
+    M.subdivide_Q(left, 1, 5, n0, 9)
+    M.subdivide_Q(right, 5, 5, n0, 9)
+    M.subdivide_Q(top, 1, 2, n0, 9)
+    M.subdivide_Q(bottom, 1, 2, n0, 9)
+    free = tuple(float(v) for v in conservative(1.4, 3.0, 0.0, 1.0))
+    bcs = {"in": M.BcSpec(M.INFLOW, free), "out": M.BcSpec(M.SUPERSONIC_OUTFLOW), "wall": M.BcSpec(M.SLIP_WALL),
+           "body": M.BcSpec(M.SLIP_WALL)}
+    dec = M.build_decomposition(patches, bcs, 9, fast=True)
+
+    def ic(x, y):
+        return np.broadcast_to(np.asarray(free).reshape(4, 1, 1), (4,) + np.shape(x)).copy()
+
+    return dec, ic, {"cfl": 0.5, "free_stream": free}
+

@@ -185,3 +185,33 @@ def test_vectorised_builder_equals_scalar(which):
                 assert rel_err(b[k], a[k]) < 1e-13 if len(a[k]) else len(b[k]) == 0
             else:
                 assert np.array_equal(a[k], b[k]), (nm, k)
+
+
+@pytest.mark.gpu
+def test_config3_cylinder_against_reference(gpu_ctx):
+    """BASELINE config 3's layout (problems.cylinder_flow, 0.70M-point
+    variant): the builder reproduces the reference's init (which builds the
+    same patches, ref_engine_testgeom 3) -- geometry, masks, windows, BCs and
+    every plan entry -- and the engine on it tracks the reference's run for
+    2 supersteps of Mach 3 flow (impulsive start, t = 0 smear)."""
+    import os
+    dec, ic, meta = PR.cylinder_flow(full=False)
+    R = ref.RefEngine.testgeom(3, 0, workers=os.cpu_count() or 1, weight_path=EN.DEFAULT_WEIGHTS)
+    RD = RefDecomposition(R)
+    for d, r in zip(dec.subs, RD.subs):
+        assert np.array_equal(d.mask, r.mask)
+        for f in ("x", "y", "iq1x", "iq2x", "iq1y", "iq2y", "h_min", "h_max", "w_norm"):
+            assert rel_err(getattr(d, f), getattr(r, f)) < 1e-13, f
+    for f in ("sol_dst_sub", "sol_dst", "sol_src_sub", "sol_src", "v_dst_sub", "v_dst", "v_src_sub", "v_src"):
+        assert np.array_equal(getattr(dec.plan, f), getattr(RD.plan, f)), f
+    for nm in ("sol_interps", "visc_interps"):
+        a, b = getattr(dec.plan, nm), getattr(RD.plan, nm)
+        assert np.array_equal(a["si0"], b["si0"]) and np.array_equal(a["sj0"], b["sj0"])
+    E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=meta["cfl"]))
+    assert not E.is_cartesian()
+    for k in range(R.nsubs):
+        assert rel_err(E.get_state(k), R.get_state(k)) < 1e-14
+    R.run(2)
+    assert E.run(2) == 2
+    for k in range(R.nsubs):
+        assert rel_err(E.get_state(k), R.get_state(k)) < 1e-10, k
