@@ -327,6 +327,8 @@ void* ref_engine_problem(const char* name, double target_h, double cfl, double T
  *      periodic annulus r in [1, 2.2] (subdivide_Q(8, 1, 65, 9)) and four
  *      Cartesian I patches (n0 = 120) over [-4, 12] x [-6, 6], Mach 3 free
  *      stream, slip walls, inflow / supersonic outflow (n0 ignored)
+ *   4  the same at full size (problems.cylinder_flow(full=True): annulus
+ *      subdivide_Q(16, 1, 129, 9), Cartesian n0 = 238; 2.57M points)
  *   2  a C1 corner patch alone (CurveSumMap of two non-orthogonal segments,
  *      subdivide_L: one L-shaped subpatch), slip walls at the reentrant
  *      corner; the overlap validation that asks for an S patch at the corner
@@ -400,7 +402,7 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             bump = {0.6, 0.6};
             u0 = 0.3;
             v0 = 0.2;
-        } else if (which == 3) {
+        } else if (which == 3 || which == 4) {
             Patch ring;
             ring.kind = PatchKind::S;
             ring.map = std::make_shared<geom::AnnulusMap>(Vec2{0.0, 0.0}, 1.0, 2.2, -M_PI, 2 * M_PI);
@@ -426,9 +428,12 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             throw UsageError("unknown test geometry");
         }
         for (size_t k = 0; k < dec.patches.size(); ++k) dec.patches[k].index = static_cast<int>(k);
-        if (which == 3) {
-            const int rs[5][2] = {{8, 1}, {1, 5}, {5, 5}, {1, 2}, {1, 2}};
-            for (auto& p : dec.patches) geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], p.index ? 120 : 65, nv);
+        if (which == 3 || which == 4) {
+            const bool full = which == 4;
+            const int rs[5][2] = {{full ? 16 : 8, 1}, {1, 5}, {5, 5}, {1, 2}, {1, 2}};
+            for (auto& p : dec.patches)
+                geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], p.index ? (full ? 238 : 120) : (full ? 129 : 65),
+                                  nv);
         } else {
             for (auto& p : dec.patches) {
                 if (p.kind == PatchKind::C1)

@@ -84,7 +84,7 @@ int pick_lb(long n_lines, int n_ext) {
     // 3 x 148 CTAs best (a 1.15-wave grid costs two CTA lifetimes), the
     // smaller LB on ties. Runtime plans: enough CTAs for two per SM,
     // shared memory permitting.
-    if (n_ext == 280 || n_ext == 536 || n_ext == 282) {  // fft_line.h has_ct_plan
+    if (n_ext == 280 || n_ext == 536 || n_ext == 282 || n_ext == 171) {  // fft_line.h has_ct_plan
         const long slots = 3L * 148;
         int best = 4;
         double best_fill = -1.0;

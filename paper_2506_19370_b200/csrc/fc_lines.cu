@@ -70,6 +70,7 @@ void launch_fc_lines_lb(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_
     if (ct && a.pl.n_ext == 280) launch_fc_lines_t<LB, 280>(a, nblk, smem, s);
     else if (ct && a.pl.n_ext == 536) launch_fc_lines_t<LB, 536>(a, nblk, smem, s);
     else if (ct && a.pl.n_ext == 282) launch_fc_lines_t<LB, 282>(a, nblk, smem, s);
+    else if (ct && a.pl.n_ext == 171) launch_fc_lines_t<LB, 171>(a, nblk, smem, s);
     else launch_fc_lines_t<LB, 0>(a, nblk, smem, s);
 }
 #endif
@@ -117,6 +118,7 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
         if (ne == 280) fc_lines_body<4, 280, 1>(Thr{0, 1}, b, sm.data(), a);
         else if (ne == 536) fc_lines_body<4, 536, 1>(Thr{0, 1}, b, sm.data(), a);
         else if (ne == 282) fc_lines_body<4, 282, 1>(Thr{0, 1}, b, sm.data(), a);
+        else if (ne == 171) fc_lines_body<4, 171, 1>(Thr{0, 1}, b, sm.data(), a);
         else fc_lines_body<4, 0, 1>(Thr{0, 1}, b, sm.data(), a);
     }
 #endif

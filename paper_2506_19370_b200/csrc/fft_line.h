@@ -722,13 +722,13 @@ constexpr int ct_scratch_slots(int ne, int lb) {
 }
 
 // the lengths with a compile-time plan: the reference operator (degree 2,
-// n_cont = 25) at N = 256 and 512, and BASELINE config 1's operator (degree
-// 4, n_cont = 27) at N = 256
+// n_cont = 25) at N = 256, 512 and 147 (config 3's annulus subpatches), and
+// BASELINE config 1's operator (degree 4, n_cont = 27) at N = 256
 #if FCSG_CUDA
 __host__ __device__
 #endif
 constexpr bool has_ct_plan(int n_ext) {
-    return n_ext == 280 || n_ext == 536 || n_ext == 282;
+    return n_ext == 280 || n_ext == 536 || n_ext == 282 || n_ext == 171;
 }
 // true when plan pl is the operator a compile-time plan of its length was built for
 inline bool ct_plan_for(const FcPlanDev& pl) {

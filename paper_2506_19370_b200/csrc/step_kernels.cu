@@ -20,6 +20,7 @@
 #include "fft_line.h"
 #include "step_kernels.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -192,15 +193,16 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
         // r-1 and the load of round r per point. Issuing the reads first lets
         // them overlap each other and the epilogue stores, which the compiler
         // may not move them across (it cannot rule out aliasing).
-        constexpr int PPT = NE > 0 ? (NE - 24) * LB / NTHR : 1;
+        constexpr int PPT = NE > 0 ? ((NE - 24) * LB + NTHR - 1) / NTHR : 1;
         constexpr int KC = (NE > 0 && PPT >= 2) ? 2 : 1;
-        static_assert(NE == 0 || ((NE - 24) * LB) % NTHR == 0, "compile-time plans need whole points per thread");
-        const int nch = NE > 0 ? PPT / KC : (total - tid + NTHR - 1) / NTHR;
+        constexpr bool kExact = NE > 0 && ((NE - 24) * LB) % (NTHR * KC) == 0;
+        const int nch = NE > 0 ? (PPT + KC - 1) / KC : (total - tid + NTHR - 1) / NTHR;
         for (int ch = 0; ch < nch; ++ch) {
             double fv[KC][Pass::kFetch];
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 const int w = tid + (ch * KC + k) * NTHR;
+                if (!kExact && w >= total) continue;
                 // rows: consecutive lanes on consecutive points of one line
                 // (coalesced global access); columns: across lines
                 const int l = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
@@ -209,6 +211,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 const int w = tid + (ch * KC + k) * NTHR;
+                if (!kExact && w >= total) continue;
                 // rows: consecutive lanes on consecutive points of one line
                 // (coalesced global access); columns: across lines
                 const int l = rows ? w / N : w % LB, i = rows ? w % N : w / LB;
@@ -1805,7 +1808,7 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     const int nlines = Pass::kRows ? E.nj : E.ni;
     // the compile-time plans assume the reference operator (n_cont 25, degree 2)
     const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
-    const bool ct = ref_op && (pl.n_ext == 280 || pl.n_ext == 536);
+    const bool ct = ref_op && (pl.n_ext == 280 || pl.n_ext == 536 || pl.n_ext == 171);
 #if FCSG_CUDA
     constexpr int kCtLB = Pass::kLB;
 #else
@@ -1813,7 +1816,7 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
 #endif
     const int lb = ct ? kCtLB : kLB;
     const LineDesc* desc = lb == 4 ? L.desc4 : L.desc8;
-    if (ref_op && pl.n_ext == 536) scr_cap = ct_scratch_slots(536, lb);  // full-scratch prime-67 middle
+    if (ct) scr_cap = std::max(scr_cap, ct_scratch_slots(pl.n_ext, lb));  // prime middles: full scratch
     const int nblk = desc ? (lb == 4 ? L.n4 : L.n8) : E.S * ((nlines + lb - 1) / lb);
     if (nblk == 0) return;
     const size_t smem = (static_cast<size_t>(pl.n_ext) * lb + scr_cap + table_slots_host(pl)) * sizeof(double2) +
@@ -1822,7 +1825,8 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     constexpr int kNT = NtOf<Pass>::v;
     if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
-    else if (ct) launch_line_pass<Pass, 536, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct && pl.n_ext == 536) launch_line_pass<Pass, 536, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct) launch_line_pass<Pass, 171, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
 #else
     (void)stream;
@@ -1830,7 +1834,8 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     std::vector<double2> sm(smem / sizeof(double2) + 1);
     for (int b = 0; b < nblk; ++b) {
         if (ct && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 536) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct) line_pass<kLB, Pass, 171, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
         else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
     }
 #endif
