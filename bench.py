@@ -253,6 +253,41 @@ def config2_rate(ctx, steps=10):
             "kernel_groups_ms": groups}
 
 
+def config3_rate(ctx, steps=20):
+    """BASELINE config 3 (Mach 3 flow past a cylinder: periodic annulus
+    2048 x 147 + four Cartesian patches of 256 x 256 subpatches, 2.57M points,
+    built from scratch by multipatch.py) on this GPU: device time per
+    superstep after the t = 0 step and two warm-up steps."""
+    import time
+
+    import torch
+
+    from paper_2506_19370_b200 import engine as EN, problems as P
+
+    t0 = time.time()
+    dec, ic, meta = P.cylinder_flow(full=True)
+    build_s = time.time() - t0
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=meta["cfl"]))
+    E.enqueue(3)
+    torch.cuda.synchronize()
+    st = torch.cuda.ExternalStream(E.stream())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    E.enqueue(steps)
+    b.record(st)
+    torch.cuda.synchronize()
+    E.check_error()
+    ms = a.elapsed_time(b) / steps
+    groups = {g: E.time_group(g, reps=3) for g in ("viscosity", "pass_a", "pass_b", "pass_c", "filter")}
+    npts = E.total_points()
+    E.close()
+    return {"config": "config3: Mach 3 flow past a unit cylinder in [-4,12]x[-6,6]; periodic annulus 2048x147 "
+                      "(r 1..2.2) + 4 Cartesian I patches of 256x256 subpatches (19-point overlaps, 6x6 "
+                      "interpolation); free stream rho 1.4, p 1, u 3; CFL 0.5",
+            "points": npts, "subpatches": len(dec.subs), "build_s": build_s, "ms_per_step": ms,
+            "value": 5.0 * npts / (ms * 1e-3), "unit": UNIT, "kernel_groups_ms": groups}
+
+
 def run_fcsg(args):
     import torch
 
@@ -354,6 +389,7 @@ def run_fcsg(args):
     fc_gbs, fc_ms = fc_derivative_gbs(ctx)
     fc4_gbs, fc4_ms = fc_derivative_gbs(ctx, n_cont=27, degree=4)
     cfg2 = config2_rate(ctx) if world == 1 else None
+    cfg3 = config3_rate(ctx) if world == 1 else None
 
     if rank != 0:
         return
@@ -395,6 +431,7 @@ def run_fcsg(args):
                                                      "4, d=5, C=27 (n_ext=282=2x3x47), d/dx, HBM->HBM",
                                            "gbs": fc4_gbs, "us_per_call": fc4_ms * 1e3, "frac_of_hbm": fc4_gbs / hbm},
         "config2": cfg2,
+        "config3": cfg3,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "sim_time": t_now, "steps_run": steps_done,
