@@ -156,8 +156,10 @@ int fcsg_engine_set_plan(fcsg_engine* eng, long n_sol, const int* sol_dst_sub, c
  * 0 = solution exchange (phase 6, src/runtime.cpp:440-452), 1 = viscosity
  * blend (phase 1, src/runtime.cpp:359-368, weights w). Entry k: recipient
  * (dst_sub[k], dst[k]) <- sum_b wy[6k+b] sum_a wx[6k+a] f(donor src_sub[k] at
- * (si0[k]+a, sj0[k]+b)); donors must be local subpatches. Call after the
- * copies (fcsg_engine_set_plan). */
+ * (si0[k]+a, sj0[k]+b)); donors must be local subpatches, except that a
+ * viscosity entry (which 1) with src_sub = -1 reads the value another rank
+ * evaluated into halo slot si0[k] (fcsg_engine_set_halo_interps). Call after
+ * the copies (fcsg_engine_set_plan). */
 int fcsg_engine_set_plan_interps(fcsg_engine* eng, int which, long n, const int* dst_sub, const int* dst,
                                  const int* src_sub, const int* si0, const int* sj0, const double* wx, const double* wy,
                                  const double* w);
@@ -209,6 +211,16 @@ int fcsg_engine_stream(fcsg_engine* eng, void** stream);
  * of values it receives; call before fcsg_engine_set_plan */
 int fcsg_engine_set_halo(fcsg_engine* eng, long n_send_e, const int* e_sub, const int* e_loc, long n_recv_e,
                          long n_send_mu, const int* mu_sub, const int* mu_loc, long n_recv_mu);
+/* Interpolated send entries (which 0 = state e, 1 = mu_hat): a send-list
+ * entry with e_loc / mu_loc = -1 - m sends the 6x6 Lagrange interpolation m
+ * of this list (donor subpatch, stencil origin si0 / sj0, wx[6 m..],
+ * wy[6 m..]) evaluated on this rank (InterpEntry, include/fcs/runtime.hpp:
+ * 25-31, whose donor lives here and whose recipient does not). Call after
+ * fcsg_engine_set_halo. On the recipient the value lands in a halo slot: a
+ * solution copy from that slot, or a viscosity interpolation entry with
+ * src_sub = -1 and si0 = the slot (fcsg_engine_set_plan_interps, which 1). */
+int fcsg_engine_set_halo_interps(fcsg_engine* eng, int which, long n, const int* sub, const int* si0, const int* sj0,
+                                 const double* wx, const double* wy);
 /* which: 0 = send e, 1 = recv e, 2 = send mu, 3 = recv mu */
 int fcsg_engine_halo_size(fcsg_engine* eng, int which, long* n);
 /* which: 0 = state e, 1 = mu_hat; d_buf is device memory on the engine's device */

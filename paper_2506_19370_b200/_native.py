@@ -88,6 +88,7 @@ def _declare(L):
                                            C.c_double, C.c_double, C.POINTER(C.c_uint8), dp, dp, dp, dp, dp, dp, dp,
                                            ip, dp, dp, ip]
     L.fcsg_engine_set_plan_interps.argtypes = [vp, C.c_int, C.c_long, ip, ip, ip, ip, ip, dp, dp, dp]
+    L.fcsg_engine_set_halo_interps.argtypes = [vp, C.c_int, C.c_long, ip, ip, ip, dp, dp]
     L.fcsg_engine_set_plan.argtypes = [vp, C.c_long, ip, ip, ip, ip, C.c_long, ip, ip, ip, ip, dp]
     L.fcsg_engine_load_mlp.argtypes = [vp, C.c_char_p]
     L.fcsg_engine_finalize.argtypes = [vp]

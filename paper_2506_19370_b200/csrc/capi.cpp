@@ -479,6 +479,17 @@ int fcsg_engine_get_state_bulk(fcsg_engine* e, double* out) {
 
 extern "C" {
 
+int fcsg_engine_set_halo_interps(fcsg_engine* e, int which, long n, const int* sub, const int* si0, const int* sj0,
+                                 const double* wx, const double* wy) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        if (n < 0) throw Error(kUsage, "bad interpolation count");
+        auto vi = [&](const int* p) { return std::vector<int>(p, p + n); };
+        e->eng->set_halo_interps(which, vi(sub), vi(si0), vi(sj0), std::vector<double>(wx, wx + 6 * n),
+                                 std::vector<double>(wy, wy + 6 * n));
+    });
+}
+
 int fcsg_engine_set_halo(fcsg_engine* e, long n_send_e, const int* e_sub, const int* e_loc, long n_recv_e,
                          long n_send_mu, const int* mu_sub, const int* mu_loc, long n_recv_mu) {
     if (!e) return FCSG_USAGE;

@@ -153,6 +153,12 @@ void Engine::set_plan_interps(int which, std::vector<int> dst_sub, std::vector<i
     for (size_t k = 0; k < n; ++k) {
         d[k] = gidx(dst_sub[k], dst[k]);
         const int ss = src_sub[k];
+        if (ss == -1 && which == 1) {  // evaluated by the donor's rank into halo slot si0
+            if (si0[k] < 0 || si0[k] >= n_recv_mu_) throw Error(kUsage, "halo slot out of range");
+            s0[k] = npts_ + si0[k];
+            pitch[k] = 0;
+            continue;
+        }
         if (ss < 0 || ss >= static_cast<int>(subs_.size()))
             throw Error(kUsage, "interpolation donors must be local subpatches");
         const auto& sp = subs_[ss];
@@ -217,9 +223,32 @@ long Engine::halo_size(int which) const {
     throw Error(kUsage, "bad halo selector");
 }
 
-void Engine::pack_e(double* d_buf) { launch_pack(E_, 0, d_halo_e_, static_cast<long>(halo_e_.size()), d_buf, ctx_.stream); }
+void Engine::set_halo_interps(int which, std::vector<int> sub, std::vector<int> si0, std::vector<int> sj0,
+                              std::vector<double> wx, std::vector<double> wy) {
+    if (finalized_) throw Error(kUsage, "engine already finalized");
+    if (which != 0 && which != 1) throw Error(kUsage, "bad halo list");
+    const size_t n = sub.size();
+    if (si0.size() != n || sj0.size() != n || wx.size() != 6 * n || wy.size() != 6 * n)
+        throw Error(kUsage, "interpolation arrays of inconsistent length");
+    HaloInterps& h = hi_[which];
+    h.sub = std::move(sub);
+    h.si0 = std::move(si0);
+    h.sj0 = std::move(sj0);
+    h.w.assign(12 * n, 0.0);
+    for (size_t k = 0; k < n; ++k)
+        for (int a = 0; a < 6; ++a) {
+            h.w[12 * k + a] = wx[6 * k + a];
+            h.w[12 * k + 6 + a] = wy[6 * k + a];
+        }
+}
+
+void Engine::pack_e(double* d_buf) {
+    launch_pack(E_, 0, d_halo_e_, static_cast<long>(halo_e_.size()), hp_[0], d_buf, ctx_.stream);
+}
 void Engine::unpack_e(const double* d_buf) { launch_unpack(E_, 0, n_recv_e_, d_buf, ctx_.stream); }
-void Engine::pack_mu(double* d_buf) { launch_pack(E_, 1, d_halo_mu_, static_cast<long>(halo_mu_.size()), d_buf, ctx_.stream); }
+void Engine::pack_mu(double* d_buf) {
+    launch_pack(E_, 1, d_halo_mu_, static_cast<long>(halo_mu_.size()), hp_[1], d_buf, ctx_.stream);
+}
 void Engine::unpack_mu(const double* d_buf) { launch_unpack(E_, 1, n_recv_mu_, d_buf, ctx_.stream); }
 
 void Engine::enqueue_part(int part, int stage) {
@@ -433,8 +462,36 @@ void Engine::finalize() {
     }
     halo_e_.clear();
     halo_mu_.clear();
-    for (auto [sb, lc] : halo_e_src_) halo_e_.push_back(gidx(sb, lc));
-    for (auto [sb, lc] : halo_mu_src_) halo_mu_.push_back(gidx(sb, lc));
+    // send lists: points, or (loc = -1 - m) interpolation m of hi_[which]
+    for (int which = 0; which < 2; ++which) {
+        const HaloInterps& h = hi_[which];
+        std::vector<long> src(h.sub.size());
+        std::vector<int> pitch(h.sub.size());
+        for (size_t m = 0; m < h.sub.size(); ++m) {
+            const int ss = h.sub[m];
+            if (ss < 0 || ss >= S) throw Error(kUsage, "halo interpolation donor out of range");
+            const auto& sp = subs_[ss];
+            if (h.si0[m] < 0 || h.sj0[m] < 0 || h.si0[m] + 6 > sp.ni || h.sj0[m] + 6 > sp.nj)
+                throw Error(kUsage, "interpolation stencil outside the donor subpatch");
+            src[m] = gidx(ss, h.sj0[m] * sp.ni + h.si0[m]);
+            pitch[m] = sp.ni;
+        }
+        if (!src.empty()) {
+            hp_[which].src = static_cast<const long*>(up(src.data(), src.size() * sizeof(long)));
+            hp_[which].pitch = static_cast<const int*>(up(pitch.data(), pitch.size() * sizeof(int)));
+            hp_[which].w = static_cast<const double*>(up(h.w.data(), h.w.size() * sizeof(double)));
+        }
+        auto& lst = which == 0 ? halo_e_src_ : halo_mu_src_;
+        auto& out = which == 0 ? halo_e_ : halo_mu_;
+        for (auto [sb, lc] : lst) {
+            if (lc < 0) {
+                if (-1 - lc >= static_cast<int>(h.sub.size())) throw Error(kUsage, "halo interpolation index out of range");
+                out.push_back(lc);
+            } else {
+                out.push_back(gidx(sb, lc));
+            }
+        }
+    }
     if (!halo_e_.empty()) d_halo_e_ = static_cast<long*>(up(halo_e_.data(), halo_e_.size() * sizeof(long)));
     if (!halo_mu_.empty()) d_halo_mu_ = static_cast<long*>(up(halo_mu_.data(), halo_mu_.size() * sizeof(long)));
     StepScalars sc{};

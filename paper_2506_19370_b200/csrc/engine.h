@@ -71,6 +71,12 @@ class Engine {
     // set_plan.
     void set_halo(std::vector<int> e_sub, std::vector<int> e_loc, long n_recv_e, std::vector<int> mu_sub,
                   std::vector<int> mu_loc, long n_recv_mu);
+    // interpolated send entries: an entry of set_halo's lists with loc = -1 - m
+    // sends the 6x6 Lagrange interpolation m of this list (donor sub, stencil
+    // origin si0 / sj0, wx[6], wy[6]) instead of a point value; call after
+    // set_halo (which 0 = state, 1 = mu_hat)
+    void set_halo_interps(int which, std::vector<int> sub, std::vector<int> si0, std::vector<int> sj0,
+                          std::vector<double> wx, std::vector<double> wy);
     void pack_e(double* d_buf);          // [k][4]
     void unpack_e(const double* d_buf);  // [k][4] -> extra slots
     void pack_mu(double* d_buf);
@@ -159,6 +165,12 @@ class Engine {
     std::vector<std::pair<int, int>> halo_e_src_, halo_mu_src_;
     long* d_halo_e_ = nullptr;
     long* d_halo_mu_ = nullptr;
+    // interpolated send entries per list: (sub, si0, sj0) and 12 weights
+    struct HaloInterps {
+        std::vector<int> sub, si0, sj0;
+        std::vector<double> w;
+    } hi_[2];
+    HaloPackDev hp_[2]{};
     long host_step_ = 0;
     void* graph_exec_ = nullptr;
     void* graph_ = nullptr;

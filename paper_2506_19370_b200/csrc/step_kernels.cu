@@ -75,6 +75,20 @@ FCSG_HD unsigned long long dbits(double v) {
 #endif
 }
 
+// 6x6 tensor Lagrange interpolation of field f from stencil origin s0
+// (row pitch, weights wx[6] then wy[6]) in the reference's summation order
+// (src/runtime.cpp:359-368, 443-451)
+FCSG_HD double interp66(const double* f, long s0, int pitch, const double* w) {
+    double val = 0.0;
+    for (int b = 0; b < 6; ++b) {
+        const double* row = f + s0 + static_cast<long>(b) * pitch;
+        double sa = 0.0;
+        for (int a = 0; a < 6; ++a) sa += w[a] * row[a];
+        val += w[6 + b] * sa;
+    }
+    return val;
+}
+
 FCSG_HD bool finite_d(double v) {
 #if FCSG_CUDA
     return isfinite(v);
@@ -1532,15 +1546,10 @@ FCSG_HD void blend_body(Thr t, int block, int nblocks, const EngineDev& E) {
             const int e0 = E.vi_off[p], e1 = E.vi_off[p + 1];
             for (int k = e0; k < e1; ++k) {
                 const double* w = E.vi_w + 13 * static_cast<long>(k);
-                const double* src = E.mu_hat + E.vi_src[k];
                 const int pitch = E.vi_pitch[k];
-                double val = 0.0;
-                for (int b = 0; b < 6; ++b) {
-                    const double* row = src + static_cast<long>(b) * pitch;
-                    double sa = 0.0;
-                    for (int a = 0; a < 6; ++a) sa += w[a] * row[a];
-                    val += w[6 + b] * sa;
-                }
+                // pitch 0: a donor on another rank evaluated the interpolation
+                // into a halo slot
+                const double val = pitch ? interp66(E.mu_hat, E.vi_src[k], pitch, w) : E.mu_hat[E.vi_src[k]];
                 m += w[12] * val;
             }
         }
@@ -1691,16 +1700,26 @@ FCSG_HD void exchange_body(Thr t, int block, int nblocks, const EngineDev& E) {
     }
 }
 
-// halo pack (donor side) / unpack (recipient side) for the multi-rank exchange
+// halo pack (donor side) / unpack (recipient side) for the multi-rank
+// exchange; interpolated entries are evaluated on the donor
 FCSG_HD void pack_body(Thr t, int block, int nblocks, const EngineDev& E, int which, const long* idx, long n,
-                       double* buf) {
+                       HaloPackDev hp, double* buf) {
     const long step = static_cast<long>(nblocks) * t.nthr;
     for (long k = static_cast<long>(block) * t.nthr + t.tid; k < n; k += step) {
         const long p = idx[k];
-        if (which == 0)
-            for (int c = 0; c < 4; ++c) buf[4 * k + c] = E.e[c][p];
-        else
-            buf[k] = E.mu_hat[p];
+        if (p >= 0) {
+            if (which == 0)
+                for (int c = 0; c < 4; ++c) buf[4 * k + c] = E.e[c][p];
+            else
+                buf[k] = E.mu_hat[p];
+        } else {
+            const long m = -1 - p;
+            const double* w = hp.w + 12 * m;
+            if (which == 0)
+                for (int c = 0; c < 4; ++c) buf[4 * k + c] = interp66(E.e[c], hp.src[m], hp.pitch[m], w);
+            else
+                buf[k] = interp66(E.mu_hat, hp.src[m], hp.pitch[m], w);
+        }
     }
 }
 FCSG_HD void unpack_body(Thr t, int block, int nblocks, const EngineDev& E, int which, long n, const double* buf) {
@@ -1742,9 +1761,9 @@ __global__ void __launch_bounds__(kThreads) blend_kernel(const __grid_constant__
     blend_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E);
 }
 __global__ void __launch_bounds__(kThreads)
-    pack_kernel(const __grid_constant__ EngineDev E, int which, const long* idx, long n, double* buf) {
+    pack_kernel(const __grid_constant__ EngineDev E, int which, const long* idx, long n, HaloPackDev hp, double* buf) {
     pack_body(Thr{static_cast<int>(threadIdx.x), static_cast<int>(blockDim.x)}, blockIdx.x, gridDim.x, E, which, idx, n,
-              buf);
+              hp, buf);
 }
 __global__ void __launch_bounds__(kThreads)
     unpack_kernel(const __grid_constant__ EngineDev E, int which, long n, const double* buf) {
@@ -2027,13 +2046,14 @@ void launch_advance(const EngineDev& E, void* stream) {
 #endif
 }
 
-void launch_pack(const EngineDev& E, int which, const long* idx, long n, double* buf, void* stream) {
+void launch_pack(const EngineDev& E, int which, const long* idx, long n, const HaloPackDev& hp, double* buf,
+                 void* stream) {
     if (n <= 0) return;
 #if FCSG_CUDA
-    pack_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E, which, idx, n, buf);
+    pack_kernel<<<grid_for(n), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(E, which, idx, n, hp, buf);
 #else
     (void)stream;
-    pack_body(Thr{0, 1}, 0, 1, E, which, idx, n, buf);
+    pack_body(Thr{0, 1}, 0, 1, E, which, idx, n, hp, buf);
 #endif
 }
 

@@ -176,8 +176,17 @@ void launch_bc(const std::vector<GroupLaunch>& G, void* stream);
 void launch_exchange(const EngineDev& Eall, void* stream);
 void launch_finalize_dt(const EngineDev& Eall, void* stream);
 void launch_advance(const EngineDev& Eall, void* stream);
+// halo send list: idx[k] >= 0 is a point (global index); idx[k] = -1 - m
+// sends the 6x6 interpolation m (stencil origin src[m], donor row pitch[m],
+// weights w[12 m..]: wx[6], wy[6])
+struct HaloPackDev {
+    const long* src;
+    const int* pitch;
+    const double* w;
+};
 // halo pack/unpack (which: 0 state e as [k][4], 1 mu_hat as [k])
-void launch_pack(const EngineDev& Eall, int which, const long* idx, long n, double* buf, void* stream);
+void launch_pack(const EngineDev& Eall, int which, const long* idx, long n, const HaloPackDev& hp, double* buf,
+                 void* stream);
 void launch_unpack(const EngineDev& Eall, int which, long n, const double* buf, void* stream);
 
 }  // namespace fcsg

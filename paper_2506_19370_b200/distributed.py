@@ -11,14 +11,18 @@ block edges cross ranks) and:
 * per stage, fringe copies whose donor lives on another rank are packed on
   the donor rank into one device buffer per peer (``fcsg_engine_pack``),
   moved with point-to-point send/recv, and unpacked into halo slots on the
-  recipient (``fcsg_engine_unpack``) before the exchange kernel runs;
+  recipient (``fcsg_engine_unpack``) before the exchange kernel runs; a 6x6
+  interpolation whose donor stencil lives on another rank is evaluated there
+  while packing (the donor has the stencil, the recipient only needs the
+  value) and arrives as a halo value;
 * per step, the mu_hat values the viscosity blend reads across ranks move
   the same way before the blend;
 * dt_local's minimum is an all-reduce(MIN) of one int64 (the bit pattern of
   a positive double, so the reduction is exact).
 
 Every per-subpatch computation is local and min is exact, so the result is
-bitwise independent of the number of ranks. Transport is torch.distributed:
+bitwise independent of the number of ranks (interpolations are evaluated
+with the same arithmetic on whichever rank holds the donor). Transport is torch.distributed:
 NCCL over NVLink on GPUs, gloo for the CPU tests (which drive the same engine
 code through the emulation build).
 """
@@ -70,6 +74,10 @@ class RankPlan:
     e_recv: dict = field(default_factory=dict)  # peer -> count
     mu_send: dict = field(default_factory=dict)
     mu_recv: dict = field(default_factory=dict)
+    # interpolations this rank evaluates for other ranks: send entries with
+    # point index -1 - m refer to entry m (local donor sub, si0, sj0, wx, wy)
+    e_interps: list = field(default_factory=list)
+    mu_interps: list = field(default_factory=list)
 
     def peers(self):
         return sorted(set(self.e_send) | set(self.e_recv) | set(self.mu_send) | set(self.mu_recv))
@@ -88,52 +96,125 @@ class RankPlan:
         return self._flat(self.mu_send)
 
 
-def split_plan(dec: G.Decomposition, owner: np.ndarray, rank: int, world: int) -> RankPlan:
+def split_plan(dec, owner: np.ndarray, rank: int, world: int) -> RankPlan:
     """Split the global plan (every rank holds it) into this rank's local
-    entries and its send/recv lists. Both sides walk the global entry list in
-    the same order, so the k-th value a peer sends is the k-th it expects."""
+    entries and its send/recv lists. Both sides walk the global entry lists
+    in the same order (copies, then interpolations), so the k-th value a peer
+    sends is the k-th it expects."""
     local = [g for g in range(len(dec.subs)) if owner[g] == rank]
     g2l = {g: l for l, g in enumerate(local)}
     pl = dec.plan
+    a = lambda x, dt=np.int32: np.asarray(x, dtype=dt)  # noqa: E731
 
-    def split(dst_sub, dst, src_sub, src, w=None):
-        out = {k: [] for k in ("dst_sub", "dst", "src_sub", "src", "w")}
-        recv_entries = []  # (position in out, peer, j)
-        send, recv = {}, {}
+    class Wire:
+        def __init__(self):
+            self.send, self.recv, self.interps = {}, {}, []
+            self.pending = []  # (list, position, peer, j): halo slot fixed up once the counts are known
+
+        def slot(self, peer, lst, pos):
+            j = self.recv.get(peer, 0)
+            self.recv[peer] = j + 1
+            self.pending.append((lst, pos, peer, j))
+
+        def resolve(self):
+            base, acc = {}, 0
+            for peer in sorted(self.recv):
+                base[peer] = acc
+                acc += self.recv[peer]
+            for lst, pos, peer, j in self.pending:
+                lst[pos] = base[peer] + j
+
+    def split(wire, dst_sub, dst, src_sub, src, w, sint, visc):
+        cp = {k: [] for k in ("dst_sub", "dst", "src_sub", "src", "w")}
+        it = {k: [] for k in ("dst_sub", "dst", "src_sub", "si0", "sj0", "wx", "wy", "w")}
         for k in range(len(dst)):
             d_own, s_own = owner[dst_sub[k]], owner[src_sub[k]]
             if d_own == rank:
-                out["dst_sub"].append(g2l[dst_sub[k]])
-                out["dst"].append(dst[k])
+                cp["dst_sub"].append(g2l[dst_sub[k]])
+                cp["dst"].append(dst[k])
                 if w is not None:
-                    out["w"].append(w[k])
+                    cp["w"].append(w[k])
                 if s_own == rank:
-                    out["src_sub"].append(g2l[src_sub[k]])
-                    out["src"].append(src[k])
+                    cp["src_sub"].append(g2l[src_sub[k]])
+                    cp["src"].append(src[k])
                 else:
-                    j = recv.get(s_own, 0)
-                    recv[s_own] = j + 1
-                    out["src_sub"].append(-1)
-                    out["src"].append(-1)
-                    recv_entries.append((len(out["src"]) - 1, s_own, j))
+                    cp["src_sub"].append(-1)
+                    cp["src"].append(-1)
+                    wire.slot(s_own, cp["src"], len(cp["src"]) - 1)
             elif s_own == rank:
-                lst = send.setdefault(d_own, ([], []))
+                lst = wire.send.setdefault(d_own, ([], []))
                 lst[0].append(g2l[src_sub[k]])
                 lst[1].append(src[k])
-        base, acc = {}, 0
-        for peer in sorted(recv):
-            base[peer] = acc
-            acc += recv[peer]
-        for pos, peer, j in recv_entries:
-            out["src"][pos] = base[peer] + j
-        return out, send, recv
+        if sint is not None:
+            for k in range(len(sint["dst"])):
+                ds, ss = int(sint["dst_sub"][k]), int(sint["src_sub"][k])
+                d_own, s_own = owner[ds], owner[ss]
+                if d_own == rank and s_own == rank:
+                    it["dst_sub"].append(g2l[ds])
+                    it["dst"].append(sint["dst"][k])
+                    it["src_sub"].append(g2l[ss])
+                    it["si0"].append(sint["si0"][k])
+                    it["sj0"].append(sint["sj0"][k])
+                    it["wx"].append(sint["wx"][k])
+                    it["wy"].append(sint["wy"][k])
+                    if visc:
+                        it["w"].append(sint["w"][k])
+                elif d_own == rank:
+                    # evaluated on the donor's rank: a value in a halo slot
+                    if visc:
+                        it["dst_sub"].append(g2l[ds])
+                        it["dst"].append(sint["dst"][k])
+                        it["src_sub"].append(-1)
+                        it["si0"].append(-1)
+                        it["sj0"].append(0)
+                        it["wx"].append(np.zeros(6))
+                        it["wy"].append(np.zeros(6))
+                        it["w"].append(sint["w"][k])
+                        wire.slot(s_own, it["si0"], len(it["si0"]) - 1)
+                    else:
+                        cp["dst_sub"].append(g2l[ds])
+                        cp["dst"].append(sint["dst"][k])
+                        cp["src_sub"].append(-1)
+                        cp["src"].append(-1)
+                        wire.slot(s_own, cp["src"], len(cp["src"]) - 1)
+                elif s_own == rank:
+                    m = len(wire.interps)
+                    wire.interps.append((g2l[ss], int(sint["si0"][k]), int(sint["sj0"][k]), np.asarray(sint["wx"][k]),
+                                         np.asarray(sint["wy"][k])))
+                    lst = wire.send.setdefault(d_own, ([], []))
+                    lst[0].append(g2l[ss])
+                    lst[1].append(-1 - m)
+        wire.resolve()
+        itd = None
+        if sint is not None:
+            itd = {k: a(v) for k, v in it.items() if k not in ("wx", "wy", "w")}
+            itd["wx"] = np.asarray(it["wx"], dtype=np.float64).reshape(-1, 6)
+            itd["wy"] = np.asarray(it["wy"], dtype=np.float64).reshape(-1, 6)
+            if visc:
+                itd["w"] = np.asarray(it["w"], dtype=np.float64)
+        return cp, itd
 
-    sol, e_send, e_recv = split(pl.sol_dst_sub, pl.sol_dst, pl.sol_src_sub, pl.sol_src)
-    vis, mu_send, mu_recv = split(pl.v_dst_sub, pl.v_dst, pl.v_src_sub, pl.v_src, pl.v_w)
-    a = lambda x, dt=np.int32: np.asarray(x, dtype=dt)
+    we, wm = Wire(), Wire()
+    sol, sol_i = split(we, pl.sol_dst_sub, pl.sol_dst, pl.sol_src_sub, pl.sol_src, None,
+                       getattr(pl, "sol_interps", None), False)
+    vis, vis_i = split(wm, pl.v_dst_sub, pl.v_dst, pl.v_src_sub, pl.v_src, pl.v_w,
+                       getattr(pl, "visc_interps", None), True)
     plan = G.Plan(a(sol["dst_sub"]), a(sol["dst"]), a(sol["src_sub"]), a(sol["src"]), a(vis["dst_sub"]),
-                  a(vis["dst"]), a(vis["src_sub"]), a(vis["src"]), a(vis["w"], np.float64))
-    return RankPlan(rank, world, owner, local, plan, e_send, e_recv, mu_send, mu_recv)
+                  a(vis["dst"]), a(vis["src_sub"]), a(vis["src"]), a(vis["w"], np.float64),
+                  sol_interps=sol_i, visc_interps=vis_i)
+    return RankPlan(rank, world, owner, local, plan, we.send, we.recv, wm.send, wm.recv, we.interps, wm.interps)
+
+
+def partition_subpatches(dec, world: int) -> np.ndarray:
+    """Owner rank of every subpatch of a general decomposition: consecutive
+    global ids (patch by patch, so neighbours mostly share a rank) in
+    contiguous runs of about equal point counts."""
+    pts = np.array([int((d.mask != 0).sum()) for d in dec.subs], dtype=np.float64)
+    c = np.cumsum(pts) - 0.5 * pts
+    owner = np.minimum((c / pts.sum() * world).astype(np.int64), world - 1)
+    if len(set(owner.tolist())) != world:
+        raise ValueError(f"cannot split {len(dec.subs)} subpatches over {world} ranks")
+    return owner
 
 
 class DistributedEngine:
@@ -150,7 +231,10 @@ class DistributedEngine:
         self.device = torch.device("cpu") if ctx.emulate else torch.device("cuda", torch.cuda.current_device())
         cfg = cfg or EN.EngineConfig()
         if initial_states is None and ic is not None:
-            initial_states = [P.initial_state(dec, ic, g) for g in rank_plan.local]
+            if hasattr(dec, "initial_state"):  # multipatch.MultiPatchDecomposition
+                initial_states = [dec.initial_state(ic, g) for g in rank_plan.local]
+            else:
+                initial_states = [P.initial_state(dec, ic, g) for g in rank_plan.local]
         self.E = EN.Engine(ctx, dec, cfg=cfg, rank_plan=rank_plan, initial_states=None)
         self.torch = torch
         # wire buffers (state: [k][4], mu: [k]) and per-peer slices

@@ -99,6 +99,14 @@ class Engine:
             nrm = sum(rank_plan.mu_recv.values())
             ctx.check(L.fcsg_engine_set_halo(h, len(es), es.ctypes.data_as(N.ip), el.ctypes.data_as(N.ip), nre,
                                              len(ms), ms.ctypes.data_as(N.ip), ml.ctypes.data_as(N.ip), nrm))
+            for which, lst in ((0, rank_plan.e_interps), (1, rank_plan.mu_interps)):
+                if not lst:
+                    continue
+                ints = [np.ascontiguousarray([t[k] for t in lst], dtype=np.int32) for k in range(3)]
+                wx = np.ascontiguousarray(np.stack([t[3] for t in lst]), dtype=np.float64)
+                wy = np.ascontiguousarray(np.stack([t[4] for t in lst]), dtype=np.float64)
+                ctx.check(L.fcsg_engine_set_halo_interps(h, which, len(lst), *[x.ctypes.data_as(N.ip) for x in ints],
+                                                         N.dptr(wx), N.dptr(wy)))
         keep = [np.ascontiguousarray(a, dtype=np.int32) for a in
                 (pl.sol_dst_sub, pl.sol_dst, pl.sol_src_sub, pl.sol_src, pl.v_dst_sub, pl.v_dst, pl.v_src_sub,
                  pl.v_src)]

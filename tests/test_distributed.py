@@ -77,3 +77,65 @@ def test_two_ranks_bitwise_equal_single_rank(tmp_path, emu_ctx):
     for r in range(2):
         tr = np.load(tmp_path / f"time{r}.npy")
         assert tr[0] == t and tr[1] == st
+
+
+def _worker_interp(rank, world, port, out_dir, steps):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_19370_b200 import _native as N, engine as EN, multipatch as M
+
+    from tests import test_multipatch as TM
+
+    ctx = N.Context(emulate=True)
+    patches, validate = TM._geometry(1)
+    dec = M.build_decomposition(patches, TM._bcs(), TM.NV, validate_overlap=validate, fast=True)
+    owner = np.array([0, 1, 1])  # the Cartesian patch on rank 0, the bilinear one on rank 1
+    rp = D.split_plan(dec, owner, rank, world)
+    np.save(os.path.join(out_dir, f"ninterp{rank}.npy"), np.array([len(rp.e_interps), len(rp.mu_interps)]))
+    DE = D.DistributedEngine(ctx, dec, rp, TM._ic(1), EN.EngineConfig(cfl=0.5))
+    DE.run(steps)
+    for l, g in enumerate(rp.local):
+        np.save(os.path.join(out_dir, f"sub{g}.npy"), DE.E.get_state(l))
+        np.save(os.path.join(out_dir, f"mu{g}.npy"), DE.E.get(l, "mu"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_with_interpolation_donors_across_ranks(tmp_path, emu_ctx):
+    """Two patches with non-coincident lattices on two gloo ranks: every
+    solution and viscosity interpolation between them has its donor stencil on
+    the other rank, is evaluated there while packing and arrives as a halo
+    value. Bitwise equal to the single-rank run after 2 supersteps."""
+    from paper_2506_19370_b200 import engine as EN, multipatch as M
+
+    from tests import test_multipatch as TM
+
+    steps = 2
+    mp.start_processes(_worker_interp, args=(2, _free_port(), str(tmp_path), steps), nprocs=2, join=True,
+                       start_method="spawn")
+    for r in range(2):
+        ne, nm = np.load(tmp_path / f"ninterp{r}.npy")
+        assert ne > 0 and nm > 0
+    patches, validate = TM._geometry(1)
+    dec = M.build_decomposition(patches, TM._bcs(), TM.NV, validate_overlap=validate, fast=True)
+    E = EN.Engine(emu_ctx, dec, TM._ic(1), EN.EngineConfig(cfl=0.5))
+    E.run(steps)
+    for g in range(len(dec.subs)):
+        assert np.array_equal(np.load(tmp_path / f"sub{g}.npy"), E.get_state(g)), g
+        assert np.array_equal(np.load(tmp_path / f"mu{g}.npy"), E.get(g, "mu")), g
+
+
+def test_partition_subpatches_balances_points():
+    from paper_2506_19370_b200 import multipatch as M
+
+    from tests import test_multipatch as TM
+
+    patches, validate = TM._geometry(1)
+    dec = M.build_decomposition(patches, TM._bcs(), TM.NV, validate_overlap=validate, fast=True)
+    owner = D.partition_subpatches(dec, 2)
+    assert sorted(set(owner.tolist())) == [0, 1]
+    with pytest.raises(ValueError):
+        D.partition_subpatches(dec, 5)
