@@ -327,6 +327,10 @@ void* ref_engine_problem(const char* name, double target_h, double cfl, double T
  *      periodic annulus r in [1, 2.2] (subdivide_Q(8, 1, 65, 9)) and four
  *      Cartesian I patches (n0 = 120) over [-4, 12] x [-6, 6], Mach 3 free
  *      stream, slip walls, inflow / supersonic outflow (n0 ignored)
+ *   5  the config-4 forward-facing step layout of problems.step_flow(1): C1
+ *      corner patch at the step's top (0.6, 0.2) (one L-shaped subpatch),
+ *      S patches along the step top and face, two I patches; Mach 3 inflow,
+ *      supersonic outflow, slip walls (n0 ignored)
  *   4  the same at full size (problems.cylinder_flow(full=True): annulus
  *      subdivide_Q(16, 1, 129, 9), Cartesian n0 = 238; 2.57M points)
  *   2  a C1 corner patch alone (CurveSumMap of two non-orthogonal segments,
@@ -424,11 +428,43 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             rect({-1.7, -6.0}, {3.4, 0.0}, {0.0, 4.8}, {interior, interior, SideInfo{true, "wall"}, interior});
             bcs["in"].state = euler::conservative(1.4, 3.0, 0.0, 1.0);
             free_stream = true;
+        } else if (which == 5) {
+            const Vec2 c{0.6, 0.2};
+            const double a = 0.15;
+            auto ellA = std::make_shared<geom::Segment>(Vec2{c.x + a, c.y}, Vec2{c.x - a, c.y});
+            auto ellB = std::make_shared<geom::Segment>(Vec2{c.x, c.y - a}, Vec2{c.x, c.y + a});
+            Patch p = geom::build_c1_patch(ellA, ellB, c, "wall");
+            dec.patches.push_back(std::move(p));
+            auto rect = [&](PatchKind kind, Vec2 o, Vec2 e1, Vec2 e2, std::array<SideInfo, 4> sd) {
+                Patch q;
+                q.kind = kind;
+                q.map = std::make_shared<geom::AffineMap>(o, e1, e2);
+                q.sides = sd;
+                dec.patches.push_back(std::move(q));
+            };
+            rect(PatchKind::I, {0.0, 0.0}, {0.57, 0.0}, {0.0, 1.0},
+                 {SideInfo{true, "in"}, interior, SideInfo{true, "wall"}, SideInfo{true, "wall"}});
+            rect(PatchKind::I, {0.4, 0.26}, {2.6, 0.0}, {0.0, 0.74},
+                 {interior, SideInfo{true, "out"}, interior, SideInfo{true, "wall"}});
+            rect(PatchKind::S, {0.6, 0.2}, {2.4, 0.0}, {0.0, 0.25},
+                 {interior, SideInfo{true, "out"}, SideInfo{true, "wall"}, interior});
+            rect(PatchKind::S, {0.3, 0.0}, {0.3, 0.0}, {0.0, 0.2},
+                 {interior, SideInfo{true, "wall"}, SideInfo{true, "wall"}, interior});
+            bcs["in"].state = euler::conservative(1.4, 3.0, 0.0, 1.0);
+            free_stream = true;
         } else {
             throw UsageError("unknown test geometry");
         }
         for (size_t k = 0; k < dec.patches.size(); ++k) dec.patches[k].index = static_cast<int>(k);
-        if (which == 3 || which == 4) {
+        if (which == 5) {
+            const int rs[5][2] = {{2, 0}, {2, 4}, {11, 3}, {10, 1}, {1, 1}};
+            for (auto& p : dec.patches) {
+                if (p.kind == PatchKind::C1)
+                    geom::subdivide_L(p, 2, 40, nv);
+                else
+                    geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], 75, nv);
+            }
+        } else if (which == 3 || which == 4) {
             const bool full = which == 4;
             const int rs[5][2] = {{full ? 16 : 8, 1}, {1, 5}, {5, 5}, {1, 2}, {1, 2}};
             for (auto& p : dec.patches)

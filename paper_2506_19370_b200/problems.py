@@ -16,6 +16,8 @@ same generator as the reference's private Rng (src/viscosity.cpp:300-313).
 * ``cylinder_flow``     config 3: Mach 3 flow past a unit cylinder in
   [-4, 12] x [-6, 6]: a periodic annulus (2048 x 147) around the body and four
   Cartesian I patches of 256 x 256 subpatches around it (multipatch.py).
+* ``step_flow``         config 4: Mach 3 forward-facing step; C1 corner patch
+  (L-shaped subpatch), S and I patches (multipatch.py).
 """
 from __future__ import annotations
 
@@ -212,3 +214,44 @@ def cylinder_flow(full=True):
 
     return dec, ic, {"cfl": 0.5, "free_stream": free}
 
+
+
+def step_flow(scale=1):
+    """BASELINE config 4: Mach 3 flow over a forward-facing step in
+    [0, 3] x [0, 1] (step of height 0.2 at x = 0.6). The reference's own
+    corner-patch problems fail their overlap checks, so
+    the layout is ours: a C1 corner patch at the step's top (0.6, 0.2) (arms
+    of 0.15 along the step top and face: one L-shaped subpatch at scale 1),
+    S patches along the step top and the step face (the latter with the foot
+    corner, an axis-aligned 90-degree corner), and two Cartesian I patches;
+    inflow rho = 1.4, p = 1, u = 3 on the left, supersonic outflow on the
+    right, slip walls. scale k multiplies the cells per patch side (about
+    0.46M k^2 points; the C1 patch gets 2k cells per arm)."""
+    from . import multipatch as M
+    SI = M.SideInfo
+    c, a = (0.6, 0.2), 0.15
+    c1 = M.build_c1_patch(M.Segment((c[0] + a, c[1]), (c[0] - a, c[1])),
+                          M.Segment((c[0], c[1] - a), (c[0], c[1] + a)), c, "wall")
+    left = M.Patch(M.I, M.AffineMap((0.0, 0.0), (0.57, 0.0), (0.0, 1.0)),
+                   [SI(True, "in"), SI(), SI(True, "wall"), SI(True, "wall")])
+    top = M.Patch(M.I, M.AffineMap((0.4, 0.26), (2.6, 0.0), (0.0, 0.74)),
+                  [SI(), SI(True, "out"), SI(), SI(True, "wall")])
+    s_top = M.Patch(M.S, M.AffineMap((0.6, 0.2), (2.4, 0.0), (0.0, 0.25)),
+                    [SI(), SI(True, "out"), SI(True, "wall"), SI()])
+    s_face = M.Patch(M.S, M.AffineMap((0.3, 0.0), (0.3, 0.0), (0.0, 0.2)),
+                     [SI(), SI(True, "wall"), SI(True, "wall"), SI()])
+    patches = [c1, left, top, s_top, s_face]
+    for k, p in enumerate(patches):
+        p.index = k
+    k = int(scale)
+    M.subdivide_L(c1, 2 * k, 40, 9)
+    for p, (r, s) in zip(patches[1:], ((2, 4), (11, 3), (10, 1), (1, 1))):
+        M.subdivide_Q(p, r * k, s * k, 75, 9)
+    free = tuple(float(v) for v in conservative(1.4, 3.0, 0.0, 1.0))
+    bcs = {"in": M.BcSpec(M.INFLOW, free), "out": M.BcSpec(M.SUPERSONIC_OUTFLOW), "wall": M.BcSpec(M.SLIP_WALL)}
+    dec = M.build_decomposition(patches, bcs, 9, fast=True)
+
+    def ic(x, y):
+        return np.broadcast_to(np.asarray(free).reshape(4, 1, 1), (4,) + np.shape(x)).copy()
+
+    return dec, ic, {"cfl": 0.5, "free_stream": free}
