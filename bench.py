@@ -288,6 +288,39 @@ def config3_rate(ctx, steps=20):
             "value": 5.0 * npts / (ms * 1e-3), "unit": UNIT, "kernel_groups_ms": groups}
 
 
+def config4_rate(ctx, steps=20):
+    """BASELINE config 4 (Mach 3 forward-facing step: C1 corner patch, S and
+    I patches, problems.step_flow(2), 3.2M points -- about the per-GPU share
+    of the 16M-point 8-GPU case) on this GPU."""
+    import time
+
+    import torch
+
+    from paper_2506_19370_b200 import engine as EN, problems as P
+
+    t0 = time.time()
+    dec, ic, meta = P.step_flow(2)
+    build_s = time.time() - t0
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=meta["cfl"]))
+    E.enqueue(3)
+    torch.cuda.synchronize()
+    st = torch.cuda.ExternalStream(E.stream())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    E.enqueue(steps)
+    b.record(st)
+    torch.cuda.synchronize()
+    E.check_error()
+    ms = a.elapsed_time(b) / steps
+    npts = E.total_points()
+    E.close()
+    return {"config": "config4: Mach 3 forward-facing step in [0,3]x[0,1] (step 0.2 high at x = 0.6); C1 corner "
+                      "patch at the step top (L-shaped subpatches), S patches along the step top and face, 2 "
+                      "Cartesian I patches of 256x256 subpatches; inflow rho 1.4, p 1, u 3; CFL 0.5",
+            "points": npts, "subpatches": len(dec.subs), "build_s": build_s, "ms_per_step": ms,
+            "value": 5.0 * npts / (ms * 1e-3), "unit": UNIT}
+
+
 def run_fcsg(args):
     import torch
 
@@ -390,6 +423,7 @@ def run_fcsg(args):
     fc4_gbs, fc4_ms = fc_derivative_gbs(ctx, n_cont=27, degree=4)
     cfg2 = config2_rate(ctx) if world == 1 else None
     cfg3 = config3_rate(ctx) if world == 1 else None
+    cfg4 = config4_rate(ctx) if world == 1 else None
 
     if rank != 0:
         return
@@ -432,6 +466,7 @@ def run_fcsg(args):
                                            "gbs": fc4_gbs, "us_per_call": fc4_ms * 1e3, "frac_of_hbm": fc4_gbs / hbm},
         "config2": cfg2,
         "config3": cfg3,
+        "config4": cfg4,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "sim_time": t_now, "steps_run": steps_done,

@@ -329,8 +329,8 @@ void* ref_engine_problem(const char* name, double target_h, double cfl, double T
  *      stream, slip walls, inflow / supersonic outflow (n0 ignored)
  *   5  the config-4 forward-facing step layout of problems.step_flow(1): C1
  *      corner patch at the step's top (0.6, 0.2) (one L-shaped subpatch),
- *      S patches along the step top and face, two I patches; Mach 3 inflow,
- *      supersonic outflow, slip walls (n0 ignored)
+ *      S patches along the step top and face, two I patches (256 x 256
+ *      subpatches); Mach 3 inflow, supersonic outflow, slip walls (n0 ignored)
  *   4  the same at full size (problems.cylinder_flow(full=True): annulus
  *      subdivide_Q(16, 1, 129, 9), Cartesian n0 = 238; 2.57M points)
  *   2  a C1 corner patch alone (CurveSumMap of two non-orthogonal segments,
@@ -457,12 +457,12 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
         }
         for (size_t k = 0; k < dec.patches.size(); ++k) dec.patches[k].index = static_cast<int>(k);
         if (which == 5) {
-            const int rs[5][2] = {{2, 0}, {2, 4}, {11, 3}, {10, 1}, {1, 1}};
+            const int rs[5][2] = {{2, 0}, {1, 2}, {5, 1}, {4, 1}, {1, 1}};
             for (auto& p : dec.patches) {
                 if (p.kind == PatchKind::C1)
-                    geom::subdivide_L(p, 2, 40, nv);
+                    geom::subdivide_L(p, 2, 59, nv);
                 else
-                    geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], 75, nv);
+                    geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], 238, nv);
             }
         } else if (which == 3 || which == 4) {
             const bool full = which == 4;

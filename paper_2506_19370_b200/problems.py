@@ -225,8 +225,9 @@ def step_flow(scale=1):
     S patches along the step top and the step face (the latter with the foot
     corner, an axis-aligned 90-degree corner), and two Cartesian I patches;
     inflow rho = 1.4, p = 1, u = 3 on the left, supersonic outflow on the
-    right, slip walls. scale k multiplies the cells per patch side (about
-    0.46M k^2 points; the C1 patch gets 2k cells per arm)."""
+    right, slip walls. The I and S patches are split into 256 x 256
+    subpatches (as config 5); scale k multiplies the cells per patch side
+    (about 0.87M k^2 points; the C1 patch gets 2k cells of 60 points)."""
     from . import multipatch as M
     SI = M.SideInfo
     c, a = (0.6, 0.2), 0.15
@@ -244,9 +245,9 @@ def step_flow(scale=1):
     for k, p in enumerate(patches):
         p.index = k
     k = int(scale)
-    M.subdivide_L(c1, 2 * k, 40, 9)
-    for p, (r, s) in zip(patches[1:], ((2, 4), (11, 3), (10, 1), (1, 1))):
-        M.subdivide_Q(p, r * k, s * k, 75, 9)
+    M.subdivide_L(c1, 2 * k, 59, 9)
+    for p, (r, s) in zip(patches[1:], ((1, 2), (5, 1), (4, 1), (1, 1))):
+        M.subdivide_Q(p, r * k, s * k, 238, 9)  # 256 x 256 subpatches, as config 5
     free = tuple(float(v) for v in conservative(1.4, 3.0, 0.0, 1.0))
     bcs = {"in": M.BcSpec(M.INFLOW, free), "out": M.BcSpec(M.SUPERSONIC_OUTFLOW), "wall": M.BcSpec(M.SLIP_WALL)}
     dec = M.build_decomposition(patches, bcs, 9, fast=True)
