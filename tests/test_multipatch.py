@@ -250,8 +250,8 @@ def test_config4_step_against_reference(gpu_ctx):
         ties += int((~same).sum())
         assert (~same).sum() <= max(1, len(same) // 1000), nm  # donor stencils tied to round-off
     E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=meta["cfl"]))
-    for k in range(R.nsubs):
-        assert rel_err(E.get_state(k), R.get_state(k)) < 1e-14
+    for k in range(R.nsubs):  # after apply_ic's BCs (slip-wall normals from the metrics)
+        assert rel_err(E.get_state(k), R.get_state(k)) < 1e-12
     R.run(2)
     assert E.run(2) == 2
     for k in range(R.nsubs):
