@@ -117,8 +117,66 @@ FCSG_HD void dft8(double2* x) {
     x[7] = csub(e3, w3o);
 }
 
-// odd P: symmetric-pair form. cos/sin(2 pi k / P) come from the n-point
-// twiddle table (P divides n): tw[k n / P] = (cos, -sin).
+// cos / sin (2 pi k / P) for the odd radices in registers, the quad-precision
+// values rounded to double (the same values the twiddle table holds at
+// tw[k n / P], fc_tables.cpp): constants folded into the instructions instead
+// of shared-memory loads
+FCSG_HD constexpr double root_cos(int P, int k) {
+    switch (P * 16 + k) {
+        case 3 * 16 + 1: return -0.5;
+        case 5 * 16 + 1: return 0.30901699437494745;
+        case 5 * 16 + 2: return -0.80901699437494745;
+        case 7 * 16 + 1: return 0.62348980185873348;
+        case 7 * 16 + 2: return -0.22252093395631439;
+        case 7 * 16 + 3: return -0.90096886790241915;
+        case 9 * 16 + 1: return 0.76604444311897801;
+        case 9 * 16 + 2: return 0.17364817766693036;
+        case 9 * 16 + 3: return -0.5;
+        case 9 * 16 + 4: return -0.93969262078590843;
+        case 11 * 16 + 1: return 0.84125353283118121;
+        case 11 * 16 + 2: return 0.41541501300188644;
+        case 11 * 16 + 3: return -0.14231483827328514;
+        case 11 * 16 + 4: return -0.6548607339452851;
+        case 11 * 16 + 5: return -0.95949297361449737;
+        case 13 * 16 + 1: return 0.88545602565320991;
+        case 13 * 16 + 2: return 0.56806474673115581;
+        case 13 * 16 + 3: return 0.12053668025532305;
+        case 13 * 16 + 4: return -0.35460488704253562;
+        case 13 * 16 + 5: return -0.74851074817110108;
+        case 13 * 16 + 6: return -0.97094181742605201;
+        default: return 0.0;
+    }
+}
+FCSG_HD constexpr double root_sin(int P, int k) {
+    switch (P * 16 + k) {
+        case 3 * 16 + 1: return 0.8660254037844386;
+        case 5 * 16 + 1: return 0.95105651629515353;
+        case 5 * 16 + 2: return 0.58778525229247314;
+        case 7 * 16 + 1: return 0.7818314824680298;
+        case 7 * 16 + 2: return 0.97492791218182362;
+        case 7 * 16 + 3: return 0.43388373911755812;
+        case 9 * 16 + 1: return 0.64278760968653936;
+        case 9 * 16 + 2: return 0.98480775301220802;
+        case 9 * 16 + 3: return 0.8660254037844386;
+        case 9 * 16 + 4: return 0.34202014332566871;
+        case 11 * 16 + 1: return 0.54064081745559756;
+        case 11 * 16 + 2: return 0.90963199535451833;
+        case 11 * 16 + 3: return 0.98982144188093268;
+        case 11 * 16 + 4: return 0.75574957435425827;
+        case 11 * 16 + 5: return 0.28173255684142967;
+        case 13 * 16 + 1: return 0.46472317204376856;
+        case 13 * 16 + 2: return 0.82298386589365635;
+        case 13 * 16 + 3: return 0.99270887409805397;
+        case 13 * 16 + 4: return 0.93501624268541483;
+        case 13 * 16 + 5: return 0.66312265824079519;
+        case 13 * 16 + 6: return 0.23931566428755777;
+        default: return 0.0;
+    }
+}
+
+// odd P: symmetric-pair form. cos/sin(2 pi k / P): compile-time constants for
+// P <= 13, else from the n-point twiddle table (P divides n):
+// tw[k n / P] = (cos, -sin).
 template <int P, bool INV>
 FCSG_HD void dft_odd(double2* x, const double2* tw, int n) {
     constexpr int H = (P - 1) / 2;
@@ -132,14 +190,24 @@ FCSG_HD void dft_odd(double2* x, const double2* tw, int n) {
     const int st = n / P;
     double2 y[P];
     y[0] = y0;
+#pragma unroll
     for (int q = 1; q <= H; ++q) {
         double2 re = x[0];
         double2 im = mk2(0.0, 0.0);
         int idx = 0;
+#pragma unroll
         for (int k = 1; k <= H; ++k) {
             idx += q;
             if (idx >= P) idx -= P;
-            const double2 w = ld2(tw + idx * st);
+            double2 w;
+            if constexpr (P <= 13) {
+                // idx and P - idx share cos, sin flips sign; idx = 0 when P
+                // is composite (9)
+                const int ii = idx <= H ? idx : P - idx;
+                w = idx == 0 ? mk2(1.0, 0.0) : mk2(root_cos(P, ii), idx <= H ? -root_sin(P, ii) : root_sin(P, ii));
+            } else {
+                w = ld2(tw + idx * st);
+            }
             re = mk2(re.x + a[k - 1].x * w.x, re.y + a[k - 1].y * w.x);
             im = mk2(im.x - b[k - 1].x * w.y, im.y - b[k - 1].y * w.y);
         }
@@ -157,6 +225,28 @@ FCSG_HD void dft_reg(double2* x, const double2* tw, int n) {
     else if constexpr (P == 4) dft4<INV>(x);
     else if constexpr (P == 8) dft8<INV>(x);
     else dft_odd<P, INV>(x, tw, n);
+}
+
+// x[q] *= w^q (CONJ: conj(w)^q), q = 1 .. P-1, for the butterfly's twiddle
+// w = w_n^(j tstep): one table load, the powers by products in two chains
+// (odd and even exponents, each advanced by w^2: at most 4 products deep, a
+// few ulp against the table, far below the transform's round-off), three
+// complex registers live instead of P - 1
+template <int P, bool CONJ>
+FCSG_HD void apply_twiddles(double2* x, double2 w) {
+    if (CONJ) w.y = -w.y;
+    const double2 w2 = cmul(w, w);
+    double2 odd = w, even = w2;
+#pragma unroll
+    for (int q = 1; q < P; ++q) {
+        if (q & 1) {
+            x[q] = cmul(x[q], odd);
+            odd = cmul(odd, w2);
+        } else {
+            x[q] = cmul(x[q], even);
+            even = cmul(even, w2);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -179,11 +269,9 @@ FCSG_HD void stage_reg(Thr t, double2* buf, int pitch, int LB, int n, int L, con
         for (int q = 0; q < P; ++q) x[q] = p[q * ms];
         if (!inv) {
             dft_reg<P, false>(x, tw, n);
-            if (j)
-                for (int q = 1; q < P; ++q) x[q] = cmul(x[q], ld2(tw + j * q * tstep));
+            if (j) apply_twiddles<P, false>(x, ld2(tw + j * tstep));
         } else {
-            if (j)
-                for (int q = 1; q < P; ++q) x[q] = cmulc(x[q], ld2(tw + j * q * tstep));
+            if (j) apply_twiddles<P, true>(x, ld2(tw + j * tstep));
             dft_reg<P, true>(x, tw, n);
         }
         for (int q = 0; q < P; ++q) p[q * ms] = x[q];
@@ -362,15 +450,9 @@ FCSG_HD void stage_reg_ct(int tid, double2* buf, const double2* tw) {
         for (int q = 0; q < P; ++q) x[q] = p[q * ms];
         if (!INV) {
             dft_reg<P, false>(x, tw, NE);
-            if (m > 1 && j) {
-#pragma unroll
-                for (int q = 1; q < P; ++q) x[q] = cmul(x[q], ld2(tw + j * q * tstep));
-            }
+            if (m > 1 && j) apply_twiddles<P, false>(x, ld2(tw + j * tstep));
         } else {
-            if (m > 1 && j) {
-#pragma unroll
-                for (int q = 1; q < P; ++q) x[q] = cmulc(x[q], ld2(tw + j * q * tstep));
-            }
+            if (m > 1 && j) apply_twiddles<P, true>(x, ld2(tw + j * tstep));
             dft_reg<P, true>(x, tw, NE);
         }
 #pragma unroll
