@@ -4,6 +4,7 @@
 // point has the global index sub*ni*nj + j*ni + i. All subpatches of one
 // engine share one rectangular shape (every configuration measured here);
 // the FC operators for rows (n = ni) and columns (n = nj) are shared too.
+#include <cstdlib>
 #include "engine.h"
 
 #include <algorithm>
@@ -19,13 +20,18 @@ namespace {
 constexpr double kInf = std::numeric_limits<double>::infinity();
 }
 
-Engine::Engine(Ctx& ctx, const EngineConfig& cfg) : ctx_(ctx), cfg_(cfg) {}
+Engine::Engine(Ctx& ctx, const EngineConfig& cfg) : ctx_(ctx), cfg_(cfg) {
+    if (const char* v = std::getenv("FCSG_STAGE_CHUNKS")) cfg_.stage_chunks = std::atoi(v);
+}
 
 Engine::~Engine() {
     if (graph_exec_) dev::graph_destroy(graph_exec_, graph_);
     if (ev_fork_) dev::destroy_event(ev_fork_);
     if (ev_join_) dev::destroy_event(ev_join_);
     if (side_) dev::destroy_stream(side_);
+    for (void* e : cevents_) dev::destroy_event(e);
+    for (void* st : cstreams_) dev::destroy_stream(st);
+    if (ev_stage_) dev::destroy_event(ev_stage_);
     for (void* p : allocs_) dev::free(p);
 }
 
@@ -502,18 +508,20 @@ void Engine::finalize() {
     // group views: every pointer offset to the group's first point / slot /
     // line; line sets per orientation and length
     G_.clear();
+    chunks_.clear();
     bool all_cart = true;
-    for (const Group& g : groups_) {
-        GroupLaunch gl;
+    // view of slots [g.slot0 + k0, g.slot0 + k0 + n) of group g
+    auto make_view = [&](const Group& g, int k0, int n) {
         EngineDev V = E;
-        V.S = g.n;
+        const int slot0 = g.slot0 + k0;
+        V.S = n;
         V.ni = g.ni;
         V.nj = g.nj;
-        V.sub_base = g.slot0;
-        V.npts = static_cast<long>(g.n) * g.ni * g.nj;
+        V.sub_base = slot0;
+        V.npts = static_cast<long>(n) * g.ni * g.nj;
         V.div_ni = make_fastdiv(static_cast<unsigned>(g.ni));
         V.div_sz = make_fastdiv(static_cast<unsigned>(g.ni * g.nj));
-        const long p0 = g.p0;
+        const long p0 = g.p0 + static_cast<long>(k0) * g.ni * g.nj;
         auto offp = [p0](auto* ptr) { return ptr ? ptr + p0 : ptr; };
         V.mask = offp(E.mask);
         V.iq1x = offp(E.iq1x);
@@ -543,19 +551,24 @@ void Engine::finalize() {
         V.proxy = offp(E.proxy);
         V.seed = offp(E.seed);
         V.m01 = offp(E.m01);
-        V.h1 = E.h1 + g.slot0;
-        V.h2 = E.h2 + g.slot0;
-        V.cut_i = E.cut_i + g.slot0;
-        V.cut_j = E.cut_j + g.slot0;
-        V.bc_row_lo = E.bc_row_lo + row_off[g.slot0];
-        V.bc_row_hi = E.bc_row_hi + row_off[g.slot0];
-        V.bc_col_lo = E.bc_col_lo + col_off[g.slot0];
-        V.bc_col_hi = E.bc_col_hi + col_off[g.slot0];
+        V.h1 = E.h1 + slot0;
+        V.h2 = E.h2 + slot0;
+        V.cut_i = E.cut_i + slot0;
+        V.cut_j = E.cut_j + slot0;
+        V.bc_row_lo = E.bc_row_lo + row_off[slot0];
+        V.bc_row_hi = E.bc_row_hi + row_off[slot0];
+        V.bc_col_lo = E.bc_col_lo + col_off[slot0];
+        V.bc_col_hi = E.bc_col_hi + col_off[slot0];
         // the global-view plan structures are not used through a group view
         V.visc_off = nullptr;
         V.vi_off = nullptr;
         V.n_x = 0;
         V.n_xi = 0;
+        return V;
+    };
+    for (const Group& g : groups_) {
+        GroupLaunch gl;
+        EngineDev V = make_view(g, 0, g.n);
         // Cartesian group: iq2x == iq1y == 0 at every point
         V.cartesian = cfg_.allow_cartesian ? 1 : 0;
         for (int k = 0; k < g.n && V.cartesian; ++k) {
@@ -626,10 +639,35 @@ void Engine::finalize() {
             }
         }
         gl.E = V;
+        // stage chunks: the group's slots in up to stage_chunks contiguous
+        // runs (groups with explicit line runs stay whole)
+        // (a chunk keeps >= kChunkPoints points: smaller kernels lose more to
+        // launch gaps than they gain from the overlap)
+        const long by_size = static_cast<long>(g.n) * g.ni * g.nj / kChunkPoints;
+        const int nch = any_l ? 1 : static_cast<int>(std::max(1L, std::min<long>({by_size, cfg_.stage_chunks, g.n})));
+        for (int c = 0; c < nch; ++c) {
+            const int k0 = static_cast<int>(static_cast<long>(g.n) * c / nch);
+            const int k1 = static_cast<int>(static_cast<long>(g.n) * (c + 1) / nch);
+            GroupLaunch cl = gl;
+            if (nch > 1) {
+                cl.E = make_view(g, k0, k1 - k0);
+                cl.E.cartesian = V.cartesian;
+            }
+            chunks_.push_back({cl});
+        }
         G_.push_back(std::move(gl));
     }
     E.cartesian = all_cart ? 1 : 0;
     finalized_ = true;
+}
+
+int Engine::launches_per_step() const {
+    int n = fcsg::launches_per_step(G_);
+    if (dev::is_cuda() && chunks_.size() > 1) {  // enqueue_step's chunked stages
+        n -= 5 * (stage_launches(G_) + static_cast<int>(G_.size()));
+        for (const auto& c : chunks_) n += 5 * (stage_launches(c) + 1);
+    }
+    return n;
 }
 
 bool Engine::cartesian() const {
@@ -828,9 +866,39 @@ void Engine::enqueue_step(bool step0) {
     else launch_phase2(G_, step0, s);
     launch_bc(G_, s);
     launch_finalize_dt(E_, s);
+    // RK stages: the chunks' line passes and BCs on side streams (a chunk's
+    // passes and BCs touch only its own subpatches), joined before the
+    // exchange. The GPU then runs one chunk's pass Y next to another's pass X
+    // and fills each kernel's last wave with the next kernel's blocks.
+    const bool chunked = dev::is_cuda() && chunks_.size() > 1;
+    if (chunked && cstreams_.empty()) {
+        int ns = kStageStreams;
+        if (const char* v = std::getenv("FCSG_STAGE_STREAMS")) ns = std::atoi(v);
+        ns = std::max(1, std::min<int>(ns, static_cast<int>(chunks_.size())));
+        for (int k = 0; k < ns; ++k) {
+            cstreams_.push_back(dev::create_stream());
+            cevents_.push_back(dev::create_event());
+        }
+        ev_stage_ = dev::create_event();
+    }
     for (int st = 0; st < 5; ++st) {
-        launch_stage(G_, st, s);
-        launch_bc(G_, s);
+        if (chunked) {
+            const int ns = static_cast<int>(cstreams_.size());
+            dev::record(ev_stage_, s);
+            for (int k = 0; k < ns; ++k) dev::wait(cstreams_[k], ev_stage_);
+            for (size_t c = 0; c < chunks_.size(); ++c) {
+                void* cs = cstreams_[c % ns];
+                launch_stage(chunks_[c], st, cs);
+                launch_bc(chunks_[c], cs);
+            }
+            for (int k = 0; k < ns; ++k) {
+                dev::record(cevents_[k], cstreams_[k]);
+                dev::wait(s, cevents_[k]);
+            }
+        } else {
+            launch_stage(G_, st, s);
+            launch_bc(G_, s);
+        }
         launch_exchange(E_, s);
     }
     launch_advance(E_, s);

@@ -35,6 +35,7 @@ struct EngineConfig {
     bool debug_rhs = false;                    // keep the last stage's rhs for parity hooks
     bool allow_cartesian = true;               // use the zero-metric-term passes when they apply
     bool reference_order = false;              // euler_rhs's accumulation order instead of the flux form
+    int stage_chunks = 2;                      // RK-stage line passes of a large shape group in up to this many slot runs
 };
 
 struct SubSpec {
@@ -120,7 +121,7 @@ class Engine {
     // (filter rows + cols), 3 pass A, 4 pass B, 5 pass C (stage 1), 6 BC,
     // 7 exchange
     double time_pass(int which, int reps);
-    int launches_per_step() const { return fcsg::launches_per_step(G_); }
+    int launches_per_step() const;
     void launch_group(int which);
     void* stream() const { return ctx_.stream; }
 
@@ -144,6 +145,7 @@ class Engine {
     std::vector<long> off_of_slot_;         // first point of each storage slot
     EngineDev E_{};                         // global view
     std::vector<GroupLaunch> G_;            // group views + line sets
+    std::vector<std::vector<GroupLaunch>> chunks_;  // stage chunks (one view each)
     std::vector<void*> allocs_;
     double* pool_ = nullptr;
     std::vector<double> mlp_;
@@ -180,6 +182,11 @@ class Engine {
     void* side_ = nullptr;
     void* ev_fork_ = nullptr;
     void* ev_join_ = nullptr;
+    // streams of the RK-stage chunks (enqueue_step)
+    static constexpr int kStageStreams = 8;
+    static constexpr long kChunkPoints = 1L << 21;
+    std::vector<void*> cstreams_, cevents_;
+    void* ev_stage_ = nullptr;
 };
 
 }  // namespace fcsg
