@@ -841,6 +841,18 @@ double Engine::time() {
     return sc.t;
 }
 
+void Engine::ensure_streams() {
+    if (!cstreams_.empty()) return;
+    int ns = kStageStreams;
+    if (const char* v = std::getenv("FCSG_STAGE_STREAMS")) ns = std::atoi(v);
+    ns = std::max(2, ns);
+    for (int k = 0; k < ns; ++k) {
+        cstreams_.push_back(dev::create_stream());
+        cevents_.push_back(dev::create_event());
+    }
+    ev_stage_ = dev::create_event();
+}
+
 void Engine::enqueue_step(bool step0) {
     void* s = ctx_.stream;
     // phase 0 reads e only in the proxy (and, at t = 0, in the classifier's
@@ -848,22 +860,42 @@ void Engine::enqueue_step(bool step0) {
     // phases 0-1 read or write, so in steady steps it runs on a side stream
     // next to the classifier and the blend
     const bool fork = !step0 && dev::is_cuda();
-    if (fork && !side_) {
-        side_ = dev::create_stream();
-        ev_fork_ = dev::create_event();
-        ev_join_ = dev::create_event();
+    if (fork && G_.size() > 1) {
+        // several shape groups: each group's classifier and filter on its own
+        // stream (classifiers on the first half of the pool, filters on the
+        // second); the blend joins the classifiers, the BCs the filters
+        ensure_streams();
+        const int ns = static_cast<int>(cstreams_.size()), half = ns / 2;
+        launch_proxy(E_, s);
+        dev::record(ev_stage_, s);
+        for (int k = 0; k < ns; ++k) dev::wait(cstreams_[k], ev_stage_);
+        for (size_t g = 0; g < G_.size(); ++g) {
+            const std::vector<GroupLaunch> one{G_[g]};
+            launch_classify(E_, one, false, cstreams_[g % half]);
+            launch_phase2(one, false, cstreams_[half + g % (ns - half)]);
+        }
+        for (int k = 0; k < ns; ++k) dev::record(cevents_[k], cstreams_[k]);
+        for (int k = 0; k < half; ++k) dev::wait(s, cevents_[k]);
+        launch_phase1(E_, s);
+        for (int k = half; k < ns; ++k) dev::wait(s, cevents_[k]);
+    } else {
+        if (fork && !side_) {
+            side_ = dev::create_stream();
+            ev_fork_ = dev::create_event();
+            ev_join_ = dev::create_event();
+        }
+        launch_proxy(E_, s);
+        if (fork) {
+            dev::record(ev_fork_, s);
+            dev::wait(side_, ev_fork_);
+            launch_phase2(G_, false, side_);
+            dev::record(ev_join_, side_);
+        }
+        launch_classify(E_, G_, step0, s);
+        launch_phase1(E_, s);
+        if (fork) dev::wait(s, ev_join_);
+        else launch_phase2(G_, step0, s);
     }
-    launch_proxy(E_, s);
-    if (fork) {
-        dev::record(ev_fork_, s);
-        dev::wait(side_, ev_fork_);
-        launch_phase2(G_, false, side_);
-        dev::record(ev_join_, side_);
-    }
-    launch_classify(E_, G_, step0, s);
-    launch_phase1(E_, s);
-    if (fork) dev::wait(s, ev_join_);
-    else launch_phase2(G_, step0, s);
     launch_bc(G_, s);
     launch_finalize_dt(E_, s);
     // RK stages: the chunks' line passes and BCs on side streams (a chunk's
@@ -871,19 +903,10 @@ void Engine::enqueue_step(bool step0) {
     // exchange. The GPU then runs one chunk's pass Y next to another's pass X
     // and fills each kernel's last wave with the next kernel's blocks.
     const bool chunked = dev::is_cuda() && chunks_.size() > 1;
-    if (chunked && cstreams_.empty()) {
-        int ns = kStageStreams;
-        if (const char* v = std::getenv("FCSG_STAGE_STREAMS")) ns = std::atoi(v);
-        ns = std::max(1, std::min<int>(ns, static_cast<int>(chunks_.size())));
-        for (int k = 0; k < ns; ++k) {
-            cstreams_.push_back(dev::create_stream());
-            cevents_.push_back(dev::create_event());
-        }
-        ev_stage_ = dev::create_event();
-    }
+    if (chunked) ensure_streams();
     for (int st = 0; st < 5; ++st) {
         if (chunked) {
-            const int ns = static_cast<int>(cstreams_.size());
+            const int ns = std::min(static_cast<int>(cstreams_.size()), static_cast<int>(chunks_.size()));
             dev::record(ev_stage_, s);
             for (int k = 0; k < ns; ++k) dev::wait(cstreams_[k], ev_stage_);
             for (size_t c = 0; c < chunks_.size(); ++c) {

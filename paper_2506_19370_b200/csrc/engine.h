@@ -186,6 +186,7 @@ class Engine {
     static constexpr int kStageStreams = 8;
     static constexpr long kChunkPoints = 1L << 21;
     std::vector<void*> cstreams_, cevents_;
+    void ensure_streams();
     void* ev_stage_ = nullptr;
 };
 
