@@ -113,6 +113,10 @@ typedef struct {
     int force_general;       /* 1: never use the Cartesian (zero metric term) passes */
     int reference_order;     /* 1: accumulate the rhs in euler_rhs's order (40 line derivatives);
                                 0: flux form div(mu grad w - f), 24 */
+    int classifier;          /* ClassifierConfig::variant (include/fcs/viscosity.hpp:45-52):
+                                0 ann (the MLP; fcsg_engine_load_mlp before finalize),
+                                1 fallback (FC-spectrum decay, src/viscosity.cpp:161-208) */
+    int classifier_window;   /* ClassifierConfig::window of the fallback variant, 32 (<= 64) */
 } fcsg_engine_config;
 
 /* BcKind codes (include/fcs/bc.hpp:10-17); -1 = no boundary condition */

@@ -14,7 +14,8 @@ parity tolerances (1e-11 per FC line, 1e-8 per solution):
                        :257-284 (derivative), :286-306 (filters)
 * line sweeps       -> src/subpatch_data.cpp:9-67
 * Euler physics     -> src/euler.cpp:10-12,16-101,105-180,182-221,223-236
-* SDNN viscosity    -> src/viscosity.cpp:13-29,48-59,63-89,108-133,143-160,211-251
+* SDNN viscosity    -> src/viscosity.cpp:13-29,48-59,63-89,108-133,143-208,211-251
+                       (ann and fallback classifier variants)
 * superstep         -> src/runtime.cpp:327-454,482-511
 
 The blend matrix is also generalised to Gram degree d (degree 2 reproduces
@@ -365,6 +366,45 @@ def classify_lines(mlp: Mlp, lines: np.ndarray, abs_floor: float = ABS_FLOOR, wi
     srt = np.sort(logits, axis=-1)
     margin = srt[..., -1] - srt[..., -2]
     tau = np.where(ok, best + 1, 4).astype(np.int32)
+    margin = np.where(ok, margin, np.inf)
+    return tau, margin
+
+
+def classify_lines_spectrum(lines: np.ndarray, window: int = 32, abs_floor: float = ABS_FLOOR,
+                            n_cont: int = 25):
+    """Classifier::classify_line, fallback variant (src/viscosity.cpp:161-208):
+    FcOperator::spectrum (src/fc_core.cpp:308-316) of every window, then the
+    log-log least-squares decay exponent of the top quarter of the modes.
+    Returns (tau, margin) where margin is the distance of the decision
+    variables from their thresholds (decay exponent from 1.6 / 2.6 / 3.6,
+    tail peak from 2e-4, relative), for gating parity on near-ties."""
+    n = lines.shape[-1]
+    w = min(window, n)
+    if w < 12:
+        return np.full(lines.shape, 4, dtype=np.int32), np.full(lines.shape, np.inf)
+    op = get_op(w, n_cont)
+    nb = op.n_ext // 2 + 1
+    k_lo = (3 * (nb - 1)) // 4
+    idx = np.arange(n)
+    start = np.clip(idx - w // 2, 0, n - w)
+    gather = start[:, None] + np.arange(w)[None, :]
+    st = lines[..., gather]  # (..., n, w)
+    nrm, ok = normalize_stencils(st, abs_floor)
+    ext = op._extend(nrm)
+    mag = np.abs(np.fft.rfft(ext, axis=-1)) / op.n_ext
+    tail = mag[..., k_lo:nb]
+    ks = np.arange(k_lo, nb, dtype=np.float64)
+    lx = np.log(ks)
+    ly = np.log(np.maximum(tail, 1e-300))
+    cnt = nb - k_lo
+    sx, sxx = lx.sum(), (lx * lx).sum()
+    sy = ly.sum(axis=-1)
+    sxy = (ly * lx).sum(axis=-1)
+    s = -(cnt * sxy - sx * sy) / (cnt * sxx - sx * sx)
+    peak = tail.max(axis=-1)
+    tau = np.where(peak < 2e-4, 4, np.where(s < 1.6, 1, np.where(s < 2.6, 2, np.where(s < 3.6, 3, 4))))
+    margin = np.minimum(np.abs(peak - 2e-4) / 2e-4, np.min(np.abs(s[..., None] - np.array([1.6, 2.6, 3.6])), axis=-1))
+    tau = np.where(ok, tau, 4).astype(np.int32)
     margin = np.where(ok, margin, np.inf)
     return tau, margin
 

@@ -37,6 +37,7 @@ def lib():
         L.ref_train_classifier.argtypes = [C.c_char_p, dp]
         L.ref_mlp_forward.argtypes = [C.c_char_p, C.c_int, dp, dp, ip]
         L.ref_classify_line.argtypes = [C.c_char_p, C.c_int, dp, ip]
+        L.ref_classify_line_fallback.argtypes = [C.c_int, C.c_double, C.c_int, dp, ip]
         L.ref_engine_rect.restype = C.c_void_p
         L.ref_engine_rect.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
                                       C.c_int, C.c_int, ip, dp, dp, C.c_double, C.c_double, C.c_int,
@@ -146,6 +147,14 @@ def classify_line(path, values):
     tau = np.zeros(len(values), dtype=np.int32)
     _check(lib().ref_classify_line(path.encode(), len(values), _dp(values),
                                    tau.ctypes.data_as(C.POINTER(C.c_int))))
+    return tau
+
+
+def classify_line_fallback(values, window=32, abs_floor=1e-4):
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    tau = np.zeros(len(values), dtype=np.int32)
+    _check(lib().ref_classify_line_fallback(int(window), C.c_double(abs_floor), len(values), _dp(values),
+                                            tau.ctypes.data_as(C.POINTER(C.c_int))))
     return tau
 
 

@@ -230,6 +230,20 @@ int ref_classify_line(const char* path, int n, const double* values, int* tau) {
     });
 }
 
+/* Classifier::classify_line (fallback variant: FC-spectrum decay). */
+int ref_classify_line_fallback(int window, double abs_floor, int n, const double* values, int* tau) {
+    return guard([&] {
+        visc::ClassifierConfig cc;
+        cc.variant = visc::ClassifierConfig::Variant::fallback;
+        cc.window = window;
+        cc.abs_floor = abs_floor;
+        visc::Classifier c(cc);
+        std::vector<uint8_t> t(n);
+        c.classify_line(values, n, t.data());
+        for (int i = 0; i < n; ++i) tau[i] = t[i];
+    });
+}
+
 /* One rectangular I patch [x0,x0+lx]x[y0,y0+ly] split by subdivide_Q(r,s,n0,nv)
  * (geometry.cpp:213-255), sides W,E,S,N with BC kind codes (0 inflow,
  * 1 outflow_pressure, 2 slip_wall, 3 noslip_adiabatic, 4 supersonic_outflow,

@@ -278,6 +278,8 @@ int fcsg_engine_create(fcsg_ctx* ctx, const fcsg_engine_config* cfg, fcsg_engine
         c.debug_rhs = cfg->debug_rhs != 0;
         c.allow_cartesian = cfg->force_general == 0;
         c.reference_order = cfg->reference_order != 0;
+        c.classifier = cfg->classifier;
+        c.classifier_window = cfg->classifier_window;
         auto* e = new fcsg_engine{ctx, std::make_unique<Engine>(*ctx, c)};
         *out = e;
     });

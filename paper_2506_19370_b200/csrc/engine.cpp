@@ -4,12 +4,12 @@
 // point has the global index sub*ni*nj + j*ni + i. All subpatches of one
 // engine share one rectangular shape (every configuration measured here);
 // the FC operators for rows (n = ni) and columns (n = nj) are shared too.
-#include <cstdlib>
 #include "engine.h"
 
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <numeric>
@@ -328,7 +328,8 @@ void Engine::load_mlp_file(const std::string& path) {
 void Engine::finalize() {
     if (finalized_) throw Error(kUsage, "engine already finalized");
     if (subs_.empty()) throw Error(kUsage, "engine has no subpatches");
-    if (mlp_.empty()) throw Error(kConfig, "ann classifier requires a weight file path");
+    // Classifier ctor (src/viscosity.cpp:134-141)
+    if (cfg_.classifier == 0 && mlp_.empty()) throw Error(kConfig, "ann classifier requires a weight file path");
     layout();
     const int S = static_cast<int>(subs_.size());
 
@@ -456,6 +457,7 @@ void Engine::finalize() {
             E.vi_w = static_cast<const double*>(up(vi_w_.data(), vi_w_.size() * sizeof(double)));
         }
     }
+    if (static_cast<int>(mlp_.size()) != kMlpWeights) mlp_.assign(kMlpWeights, 0.0);  // fallback: unused
     E.mlp = static_cast<const double*>(up(mlp_.data(), mlp_.size() * sizeof(double)));
     {
         const std::vector<double> fr = mlp_mma_fragments(mlp_);
@@ -465,6 +467,24 @@ void Engine::finalize() {
         std::vector<double> tt(kTanhTable);
         for (int k = 0; k < kTanhTable; ++k) tt[k] = static_cast<double>(tanhl(static_cast<long double>(k) / 64.0L));
         E.tanh_tab = static_cast<const double*>(up(tt.data(), tt.size() * sizeof(double)));
+    }
+    if (cfg_.classifier != 0 && cfg_.classifier != 1) throw Error(kConfig, "unknown classifier variant");
+    if (cfg_.classifier == 1 && cfg_.classifier_window > kFbMaxWindow)
+        throw Error(kConfig, "fallback classifier window > 64 is not supported");
+    E.cls_variant = cfg_.classifier;
+    E.fb_window = cfg_.classifier_window;
+    E.fb_ncont = 25;  // OperatorCache::get(w) (src/fc_core.cpp:404-406)
+    if (cfg_.classifier == 1) {
+        // one table per window length the lines can produce: w = min(window, n), n >= 12
+        std::vector<int> off(kFbMaxWindow + 1, -1);
+        std::vector<double> tab;
+        for (int w = kFbMinWindow; w <= cfg_.classifier_window; ++w) {
+            const SpectrumTail t = build_spectrum_tail(w, E.fb_ncont);
+            off[w] = static_cast<int>(tab.size());
+            tab.insert(tab.end(), t.table.begin(), t.table.end());
+        }
+        E.fb_off = static_cast<const int*>(up(off.data(), off.size() * sizeof(int)));
+        E.fb_tab = static_cast<const double*>(up(tab.data(), tab.size() * sizeof(double)));
     }
     halo_e_.clear();
     halo_mu_.clear();

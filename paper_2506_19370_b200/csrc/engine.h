@@ -35,6 +35,8 @@ struct EngineConfig {
     bool debug_rhs = false;                    // keep the last stage's rhs for parity hooks
     bool allow_cartesian = true;               // use the zero-metric-term passes when they apply
     bool reference_order = false;              // euler_rhs's accumulation order instead of the flux form
+    int classifier = 0;                        // ClassifierConfig::Variant: 0 ann (MLP), 1 fallback (FC spectrum)
+    int classifier_window = 32;                // ClassifierConfig::window (fallback), 12..64
     int stage_chunks = 2;                      // RK-stage line passes of a large shape group in up to this many slot runs
 };
 

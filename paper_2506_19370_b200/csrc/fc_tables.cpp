@@ -223,4 +223,56 @@ FcTables build_fc_tables(int n_points, int n_cont, int degree, FilterSpec f) {
     return t;
 }
 
+SpectrumTail build_spectrum_tail(int w, int n_cont) {
+    if (w < kFbMinWindow || w > kFbMaxWindow) throw Error(kConfig, "fallback classifier: window out of range");
+    constexpr int d = 2;  // FcOperator::degree
+    const std::vector<double> A = build_blend_matrix(n_cont, d);
+    const int g = n_cont - 1;
+    SpectrumTail t;
+    t.w = w;
+    t.n_ext = w + g;
+    t.nb = t.n_ext / 2 + 1;
+    t.k_lo = (3 * (t.nb - 1)) / 4;  // src/viscosity.cpp:177
+    t.nk = t.nb - t.k_lo;
+    // ext = E x: x itself, then the gap (FcOperator::continuation,
+    // src/fc_core.cpp:221-238): right blend of x[w-1-d .. w-1] plus the
+    // reflected left blend of x[d .. 0]
+    std::vector<q128> E(static_cast<size_t>(t.n_ext) * w, q128(0));
+    for (int i = 0; i < w; ++i) E[static_cast<size_t>(i) * w + i] = 1;
+    for (int j = 0; j < g; ++j) {
+        q128* row = E.data() + static_cast<size_t>(w + j) * w;
+        for (int i = 0; i <= d; ++i) row[w - 1 - d + i] += A[static_cast<size_t>(j) * (d + 1) + i];
+        const int jr = g - 1 - j;
+        for (int i = 0; i <= d; ++i) row[d - i] += A[static_cast<size_t>(jr) * (d + 1) + i];
+    }
+    const q128 twopi = 2 * acosq(q128(-1));
+    const int nk2 = 2 * t.nk;
+    t.table.assign(static_cast<size_t>(w) * nk2 + t.nk + 2, 0.0);
+    for (int kk = 0; kk < t.nk; ++kk) {
+        const int k = t.k_lo + kk;
+        for (int i = 0; i < w; ++i) {
+            q128 re = 0, im = 0;
+            for (int j = 0; j < t.n_ext; ++j) {
+                const q128 e = E[static_cast<size_t>(j) * w + i];
+                if (e == 0) continue;
+                const q128 a = twopi * ((static_cast<long>(j) * k) % t.n_ext) / t.n_ext;
+                re += e * cosq(a);
+                im -= e * sinq(a);
+            }
+            t.table[static_cast<size_t>(i) * nk2 + 2 * kk] = static_cast<double>(re);
+            t.table[static_cast<size_t>(i) * nk2 + 2 * kk + 1] = static_cast<double>(im);
+        }
+    }
+    double sx = 0.0, sxx = 0.0;
+    double* lx = t.table.data() + static_cast<size_t>(w) * nk2;
+    for (int kk = 0; kk < t.nk; ++kk) {
+        lx[kk] = std::log(static_cast<double>(t.k_lo + kk));
+        sx += lx[kk];
+        sxx += lx[kk] * lx[kk];
+    }
+    lx[t.nk] = sx;
+    lx[t.nk + 1] = sxx;
+    return t;
+}
+
 }  // namespace fcsg

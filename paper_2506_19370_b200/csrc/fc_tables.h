@@ -44,4 +44,20 @@ std::vector<double> build_blend_matrix(int n_cont, int degree);
 // plan and multiplier tables of this implementation.
 FcTables build_fc_tables(int n_points, int n_cont, int degree, FilterSpec f);
 
+// FC-spectrum ("fallback") classifier, one window length w (<= 64):
+// Classifier::classify_line's variant (src/viscosity.cpp:161-208) over
+// FcOperator::spectrum (src/fc_core.cpp:308-316) of OperatorCache::get(w)
+// (n_cont 25, degree 2). Only the top quarter of the modes, k in [k_lo, nb),
+// enters the decision, and continuation + DFT restricted to those modes is one
+// linear map of the window: T[i][2 (k - k_lo) + {0, 1}] = (Re, Im) of the
+// contribution of window value i to c_k (no 1/n_ext; the caller divides |c_k|
+// like the reference). Layout of one table (doubles): T (w x 2 nk, i-major),
+// then lx[nk] = log(k), then sx, sxx (the fit's constant sums, accumulated in
+// the reference's order).
+struct SpectrumTail {
+    int w = 0, n_ext = 0, nb = 0, k_lo = 0, nk = 0;
+    std::vector<double> table;
+};
+SpectrumTail build_spectrum_tail(int w, int n_cont);
+
 }  // namespace fcsg

@@ -113,6 +113,8 @@ constexpr Factors factor_stages(int len) {
     return f;
 }
 constexpr int kMaxGap = 64;     // n_cont - 1
+constexpr int kFbMinWindow = 12;  // fallback classifier: shorter windows are class 4 (src/viscosity.cpp:164)
+constexpr int kFbMaxWindow = 64;  // fallback classifier: longest supported window
 constexpr int kMaxDeg = 6;      // degree + 1 <= 7
 
 // Device-side description of one FC operator (n points, n_cont, degree):

@@ -1250,6 +1250,116 @@ FCSG_HD void classify_body(Thr t, int block, int nblocks, const WA& W, double* t
     }
 }
 
+// ---- FC-spectrum ("fallback") classifier -----------------------------------
+// Classifier::classify_line's default variant (src/viscosity.cpp:161-208):
+// per point, the window of w = min(window, n) values starting at
+// clamp(pos - w/2, 0, n - w) is normalised (normalize_stencil, class 4 under
+// the guard), continued and transformed (FcOperator::spectrum), and the decay
+// exponent s = -slope of the least-squares fit of log |c_k| / n_ext against
+// log k over the top quarter of the modes picks the class (tail peak < 2e-4:
+// 4; s < 1.6: 1; < 2.6: 2; < 3.6: 3; else 4). Continuation + DFT of the NK
+// tail modes is one linear map (build_spectrum_tail): 2 NK multiply-adds per
+// window value, no FFT. Window value k sits at f[p0 + k * stride].
+template <int NK>
+FCSG_HD int spectrum_class(const double* f, long p0, long stride, int w, int n_ext, const double* tab,
+                           double abs_floor) {
+    double lo = f[p0], hi = lo;
+    for (int k = 1; k < w; ++k) {
+        const double v = f[p0 + k * stride];
+        lo = v < lo ? v : lo;  // std::min(lo, v)
+        hi = hi < v ? v : hi;  // std::max(hi, v)
+    }
+    const double span = hi - lo;
+    double scale = fabs(lo);
+    scale = scale < fabs(hi) ? fabs(hi) : scale;
+    scale = scale < 1e-100 ? 1e-100 : scale;
+    if (span <= 1e-13 * scale || span <= abs_floor) return 4;
+    double acc[2 * NK];
+#pragma unroll
+    for (int q = 0; q < 2 * NK; ++q) acc[q] = 0.0;
+    for (int k = 0; k < w; ++k) {
+        const double x = 2.0 * (f[p0 + k * stride] - lo) / span - 1.0;
+        const double* T = tab + k * 2 * NK;
+#pragma unroll
+        for (int q = 0; q < 2 * NK; ++q) acc[q] = fma(ldg1(T + q), x, acc[q]);
+    }
+    const double* lx = tab + w * 2 * NK;
+    const double sx = ldg1(lx + NK), sxx = ldg1(lx + NK + 1);
+    double sy = 0.0, sxy = 0.0, tail_peak = 0.0;
+#pragma unroll
+    for (int q = 0; q < NK; ++q) {
+        const double m = hypot(acc[2 * q], acc[2 * q + 1]) / n_ext;  // std::abs(c_k) / n_ext
+        tail_peak = tail_peak < m ? m : tail_peak;
+        const double ly = log(m > 1e-300 ? m : 1e-300);
+        sy += ly;
+        sxy += ldg1(lx + q) * ly;
+    }
+    const double slope = (NK * sxy - sx * sy) / (NK * sxx - sx * sx);
+    const double sd = -slope;
+    if (tail_peak < 2e-4) return 4;
+    if (sd < 1.6) return 1;
+    if (sd < 2.6) return 2;
+    if (sd < 3.6) return 3;
+    return 4;
+}
+
+// one window of a line of n points (n >= kFbMinWindow) around position pos
+FCSG_HD int spectrum_line_class(const EngineDev& E, const double* f, long line0, long stride, int n, int pos) {
+    const int w = n < E.fb_window ? n : E.fb_window;
+    int st = pos - w / 2;
+    st = st < 0 ? 0 : (st > n - w ? n - w : st);
+    const double* tab = E.fb_tab + E.fb_off[w];
+    const int n_ext = w + E.fb_ncont - 1;
+    const int nb = n_ext / 2 + 1;
+    const long p0 = line0 + st * stride;
+    switch (nb - (3 * (nb - 1)) / 4) {
+        case 6: return spectrum_class<6>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+        case 7: return spectrum_class<7>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+        case 8: return spectrum_class<8>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+        case 9: return spectrum_class<9>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+        case 10: return spectrum_class<10>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+        case 11: return spectrum_class<11>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+        default: return spectrum_class<12>(f, p0, stride, w, n_ext, tab, E.abs_floor);
+    }
+}
+
+// Classifier::classify (src/viscosity.cpp:211-238) with the spectrum variant:
+// rows (segment [rb, ni)), then columns ([cb, nj)) by min; lines shorter than
+// 12 points are class 4
+FCSG_HD int spectrum_point(const EngineDev& E, const double* f, long base, int i, int j, int rb, int cb) {
+    int cr = 4, cc = 4;
+    if (E.fb_window < kFbMinWindow) return 4;  // w = min(window, n) < 12 on every line
+    if (E.ni - rb >= kFbMinWindow) cr = spectrum_line_class(E, f, base + static_cast<long>(j) * E.ni + rb, 1, E.ni - rb, i - rb);
+    if (E.nj - cb >= kFbMinWindow)
+        cc = spectrum_line_class(E, f, base + static_cast<long>(cb) * E.ni + i, E.ni, E.nj - cb, j - cb);
+    return cr < cc ? cr : cc;
+}
+
+FCSG_HD void classify_spectrum_body(Thr t, int block, int nblocks, const EngineDev& E, bool step0) {
+    const long sz = static_cast<long>(E.ni) * E.nj;
+    const long step = static_cast<long>(nblocks) * t.nthr;
+    for (long p = static_cast<long>(block) * t.nthr + t.tid; p < E.npts; p += step) {
+        const long base = (p / sz) * sz;
+        const long loc = p - base;
+        const int i = static_cast<int>(loc % E.ni), j = static_cast<int>(loc / E.ni);
+        const int sub = static_cast<int>(p / sz), ci = E.cut_i[sub], cj = E.cut_j[sub];
+        if (i < ci && j < cj) {  // not in the point set of an L-shaped subpatch
+            E.tau[p] = 4.0;
+            E.mu_hat[p] = 0.0;
+            if (step0) E.seed[p] = 0.0;
+            continue;
+        }
+        const int rb = j < cj ? ci : 0, cb = i < ci ? cj : 0;
+        const int tau = spectrum_point(E, E.proxy, base, i, j, rb, cb);
+        E.tau[p] = tau;
+        E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
+        if (step0) {
+            const int tr = spectrum_point(E, E.e[0], base, i, j, rb, cb);
+            E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
+        }
+    }
+}
+
 // ---- classifier on the FP64 tensor cores ----------------------------------
 // MlpClassifier::forward (src/viscosity.cpp:108-133) as mma.m8n8k4.f64 tiles:
 // a warp classifies 8 stencils at a time -- the row and column windows of 4
@@ -1893,7 +2003,28 @@ void launch_proxy(const EngineDev& Eall, void* stream) {
 #endif
 }
 
+#if FCSG_CUDA
+constexpr int kSpecThreads = 128;
+__global__ void __launch_bounds__(kSpecThreads) classify_spectrum_kernel(const __grid_constant__ EngineDev E, bool step0) {
+    classify_spectrum_body(Thr{static_cast<int>(threadIdx.x), kSpecThreads}, blockIdx.x, gridDim.x, E, step0);
+}
+#endif
+
 void launch_classify(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream) {
+    if (Eall.cls_variant == 1) {  // FC-spectrum classifier
+#if FCSG_CUDA
+        for (const GroupLaunch& g : G) {
+            long n = (g.E.npts + kSpecThreads - 1) / kSpecThreads;
+            n = n > 148 * 32 ? 148 * 32 : (n < 1 ? 1 : n);
+            classify_spectrum_kernel<<<static_cast<int>(n), kSpecThreads, 0, static_cast<cudaStream_t>(stream)>>>(g.E,
+                                                                                                                  step0);
+        }
+#else
+        (void)stream;
+        for (const GroupLaunch& g : G) classify_spectrum_body(Thr{0, 1}, 0, 1, g.E, step0);
+#endif
+        return;
+    }
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     static const bool scalar = [] {

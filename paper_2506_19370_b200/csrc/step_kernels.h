@@ -120,6 +120,13 @@ struct EngineDev {
     const double* mlp;       // kMlpWeights, FCNN order (per layer W row-major, then b)
     const double* mlp_frag;  // kMlpFrags x 32: per-lane DMMA operand fragments (mlp_mma_fragments)
     const double* tanh_tab;  // tanh(k/64), k = 0..1280 (classifier tanh table)
+    // classifier variant (ClassifierConfig::Variant, include/fcs/viscosity.hpp:45-52):
+    // 0 = ann (the MLP), 1 = fallback (FC spectrum decay, window fb_window)
+    int cls_variant;
+    int fb_window;
+    int fb_ncont;
+    const int* fb_off;     // fb_tab offset of window length w's table (build_spectrum_tail), w <= 64
+    const double* fb_tab;
     StepScalars* sc;
 };
 

@@ -28,7 +28,8 @@ class fcsg_engine_config(C.Structure):
     _fields_ = [("cfl", C.c_double), ("T", C.c_double), ("n_cont", C.c_int), ("filter_alpha", C.c_double),
                 ("filter_p", C.c_int), ("filter_p_smear", C.c_int), ("visc_c", C.c_double * 4),
                 ("abs_floor", C.c_double), ("smear_radius", C.c_int), ("debug_rhs", C.c_int),
-                ("force_general", C.c_int), ("reference_order", C.c_int)]
+                ("force_general", C.c_int), ("reference_order", C.c_int), ("classifier", C.c_int),
+                ("classifier_window", C.c_int)]
 
 
 @dataclass
@@ -51,6 +52,10 @@ class EngineConfig:
     # accumulate the rhs in euler_rhs's own order (40 line derivatives per stage)
     # instead of the flux form div(mu grad w - f) (24; round-off-level difference)
     reference_order: bool = False
+    # ClassifierConfig (include/fcs/viscosity.hpp:45-52): "ann" (the MLP, weights
+    # above) or "fallback" (FC-spectrum decay over a window of classifier_window)
+    classifier: str = "ann"
+    classifier_window: int = 32
 
 
 def _bc_arrays(d: G.SubData):
@@ -74,7 +79,8 @@ class Engine:
         L = ctx.lib
         c = fcsg_engine_config(cfg.cfl, cfg.T, cfg.n_cont, cfg.filter_alpha, cfg.filter_p, cfg.filter_p_smear,
                                (C.c_double * 4)(*cfg.visc_c), cfg.abs_floor, cfg.smear_radius, int(cfg.debug_rhs),
-                               int(cfg.force_general), int(cfg.reference_order))
+                               int(cfg.force_general), int(cfg.reference_order),
+                               {"ann": 0, "fallback": 1}[cfg.classifier], int(cfg.classifier_window))
         h = C.c_void_p()
         ctx.check(L.fcsg_engine_create(ctx.h, C.byref(c), C.byref(h)))
         self.h = h
@@ -122,7 +128,8 @@ class Engine:
             w = np.ascontiguousarray(ip_.get("w", np.ones(len(ints[0]))), dtype=np.float64)
             ctx.check(L.fcsg_engine_set_plan_interps(h, which, len(ints[0]), *[a.ctypes.data_as(N.ip) for a in ints],
                                                      N.dptr(wx), N.dptr(wy), N.dptr(w)))
-        ctx.check(L.fcsg_engine_load_mlp(h, cfg.weights.encode()))
+        if cfg.classifier == "ann":
+            ctx.check(L.fcsg_engine_load_mlp(h, cfg.weights.encode()))
         ctx.check(L.fcsg_engine_finalize(h))
         if initial_states is None and ic is not None and rank_plan is None:
             if hasattr(dec, "initial_state"):  # multipatch.MultiPatchDecomposition

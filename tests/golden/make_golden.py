@@ -12,6 +12,10 @@ Outputs (small, committed):
                      one 64x64 subpatch (phase-level snapshots of step 1 and the
                      state after 3 steps) and the vortex tiling on 2x2
                      subpatches of 48x48 (geometry + state after 2 steps)
+  classifier_golden.npz
+                     Classifier::classify_line, fallback variant (FC-spectrum
+                     decay), on seeded lines of lengths 12..256 (smooth,
+                     noisy, step, kink, white noise) at windows 32 and 16
   ../../paper_2506_19370_b200/data/fcnn_v1.bin
                      train_classifier(TrainConfig{}) weights (seed 20240601,
                      include/fcs/viscosity.hpp:91-98) saved as FCNN v1
@@ -119,10 +123,44 @@ def engine_golden():
     np.savez_compressed(os.path.join(OUT, "engine_golden.npz"), **d)
 
 
+def classifier_lines(seed=7):
+    """Seeded test lines for the fallback classifier: lengths and kinds."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for n in (12, 20, 31, 32, 40, 64, 100, 256):
+        x = np.linspace(0.0, 1.0, n)
+        for kind in range(5):
+            if kind == 0:
+                v = np.sin(2 * np.pi * x * rng.uniform(0.5, 4))
+            elif kind == 1:
+                v = np.sin(2 * np.pi * x * rng.uniform(0.5, 4)) + rng.normal(0, 10 ** rng.uniform(-6, -1), n)
+            elif kind == 2:
+                v = np.where(x > rng.uniform(0.2, 0.8), 1.0, 0.0) + 0.01 * x
+            elif kind == 3:
+                v = np.abs(x - rng.uniform(0.3, 0.7)) ** rng.uniform(0.5, 3)
+            else:
+                v = rng.normal(size=n)
+            out.append(v)
+    return out
+
+
+def classifier_golden():
+    d = {}
+    for k, v in enumerate(classifier_lines()):
+        d[f"line{k}"] = v
+        for w in (32, 16):
+            d[f"line{k}_w{w}"] = ref.classify_line_fallback(v, w)
+    np.savez_compressed(os.path.join(OUT, "classifier_golden.npz"), **d)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["classifier"]:
+        classifier_golden()
+        sys.exit(0)
     if not os.path.exists(EN.DEFAULT_WEIGHTS) or "--retrain" in sys.argv:
         print("holdout accuracy", ref.train_classifier(EN.DEFAULT_WEIGHTS))
     fc_golden()
     engine_golden()
+    classifier_golden()
     for f in ("fc_golden.npz", "engine_golden.npz"):
         print(f, os.path.getsize(os.path.join(OUT, f)))
