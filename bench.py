@@ -321,6 +321,30 @@ def config4_rate(ctx, steps=20):
             "value": 5.0 * npts / (ms * 1e-3), "unit": UNIT}
 
 
+def fallback_rate(ctx, steps=10):
+    """The bench workload with ClassifierConfig's default variant (FC-spectrum
+    decay over 32-point windows, src/viscosity.cpp:161-208) instead of the MLP."""
+    import torch
+
+    from paper_2506_19370_b200 import engine as EN
+
+    dec, ic, _ = workload()
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5, classifier="fallback"))
+    E.enqueue(3)
+    torch.cuda.synchronize()
+    st = torch.cuda.ExternalStream(E.stream())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    E.enqueue(steps)
+    b.record(st)
+    torch.cuda.synchronize()
+    E.check_error()
+    ms = a.elapsed_time(b) / steps
+    return {"config": "config5 workload (8x8 tiles of 256x256), fallback classifier (window 32)",
+            "ms_per_step": ms, "value": 5.0 * E.total_points() / (ms * 1e-3), "unit": UNIT,
+            "viscosity_ms": E.time_group("viscosity", reps=3)}
+
+
 def run_fcsg(args):
     import torch
 
@@ -424,6 +448,7 @@ def run_fcsg(args):
     cfg2 = config2_rate(ctx) if world == 1 else None
     cfg3 = config3_rate(ctx) if world == 1 else None
     cfg4 = config4_rate(ctx) if world == 1 else None
+    fb = fallback_rate(ctx) if world == 1 else None
 
     if rank != 0:
         return
@@ -467,6 +492,7 @@ def run_fcsg(args):
         "config2": cfg2,
         "config3": cfg3,
         "config4": cfg4,
+        "config5_fallback_classifier": fb,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "sim_time": t_now, "steps_run": steps_done,
