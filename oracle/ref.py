@@ -37,6 +37,8 @@ def lib():
         L.ref_train_classifier.argtypes = [C.c_char_p, dp]
         L.ref_mlp_forward.argtypes = [C.c_char_p, C.c_int, dp, dp, ip]
         L.ref_classify_line.argtypes = [C.c_char_p, C.c_int, dp, ip]
+        L.ref_engine_mesh_json.argtypes = [C.c_void_p, C.c_char_p, C.c_long, C.POINTER(C.c_long)]
+        L.ref_mesh_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_long, C.POINTER(C.c_long)]
         L.ref_classify_line_fallback.argtypes = [C.c_int, C.c_double, C.c_int, dp, ip]
         L.ref_engine_rect.restype = C.c_void_p
         L.ref_engine_rect.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
@@ -158,6 +160,22 @@ def classify_line_fallback(values, window=32, abs_floor=1e-4):
     return tau
 
 
+def _json_out(call):
+    n = C.c_long()
+    _check(call(None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(call(buf, n.value + 1, C.byref(n)))
+    import json
+    return json.loads(buf.value.decode())
+
+
+def mesh_roundtrip(mesh: dict) -> dict:
+    """DomainDecomposition::from_json + to_json of a mesh (the reference reading it)."""
+    import json
+    text = json.dumps(mesh).encode()
+    return _json_out(lambda b, c, n: lib().ref_mesh_roundtrip(text, b, c, n))
+
+
 class RefEngine:
     """Engine over one affine I patch origin + q1 e1 + q2 e2 (ref_engine_affine);
     (lx, ly) alone is the axis-aligned rectangle."""
@@ -217,6 +235,10 @@ class RefEngine:
             _check(lib().ref_engine_dims(h, k, C.byref(a), C.byref(b)))
             self.dims.append((a.value, b.value))
         return self
+
+    def mesh_json(self) -> dict:
+        """the reference's fcs-mesh v1 JSON of this engine's decomposition"""
+        return _json_out(lambda b, c, n: lib().ref_engine_mesh_json(self.h, b, c, n))
 
     def sub_info(self, sub):
         """dict: patch, i0, j0, ni, nj, cut_i, cut_j (local), periodic1, kind, h1, h2"""

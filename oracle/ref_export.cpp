@@ -607,6 +607,35 @@ int ref_engine_plan(void* h, int id, int which, int* counts, int* copies, double
     });
 }
 
+/* DomainDecomposition::to_json (src/geometry.cpp:573-594) of the engine's
+ * decomposition, dumped; *len = full length (truncated to cap - 1). */
+int ref_engine_mesh_json(void* h, char* buf, long cap, long* len) {
+    return guard([&] {
+        const std::string t = static_cast<RefEngine*>(h)->eng->dec().to_json().dump();
+        *len = static_cast<long>(t.size());
+        if (cap > 0) {
+            const size_t n = std::min<size_t>(t.size(), static_cast<size_t>(cap - 1));
+            std::memcpy(buf, t.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
+/* DomainDecomposition::from_json (src/geometry.cpp:596-629) of a mesh file's
+ * text, written back with to_json: what the reference makes of a mesh file. */
+int ref_mesh_roundtrip(const char* in, char* buf, long cap, long* len) {
+    return guard([&] {
+        const auto dec = geom::DomainDecomposition::from_json(nlohmann::json::parse(in));
+        const std::string t = dec.to_json().dump();
+        *len = static_cast<long>(t.size());
+        if (cap > 0) {
+            const size_t n = std::min<size_t>(t.size(), static_cast<size_t>(cap - 1));
+            std::memcpy(buf, t.data(), n);
+            buf[n] = 0;
+        }
+    });
+}
+
 void ref_engine_destroy(void* h) { delete static_cast<RefEngine*>(h); }
 
 int ref_engine_nsubs(void* h) { return static_cast<int>(static_cast<RefEngine*>(h)->eng->subs().size()); }

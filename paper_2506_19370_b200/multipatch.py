@@ -10,7 +10,7 @@ CommPlan with the normalised windows (``Engine::build_plan``,
 src/runtime.cpp:89-274) -- which ``engine.Engine`` uploads through the C ABI.
 Restated from the reference's published definitions:
 
-* mappings (affine, annulus, bilinear, curve sum of segments) and their
+* mappings (affine, annulus, bilinear, curve sum of segments / arcs) and their
   Jacobians / inversion        include/fcs/geometry.hpp:57-136, src/geometry.cpp:35-99
 * Patch.contains / max_spacing  src/geometry.cpp:161-208
 * subdivide_Q / subdivide_L     src/geometry.cpp:210-334
@@ -19,6 +19,8 @@ Restated from the reference's published definitions:
 * raw_window                    src/viscosity.cpp:253-293
 * init_subpatch_data            src/subpatch_data.cpp:69-154
 * build_plan                    src/runtime.cpp:57-274
+* fcs-mesh v1 JSON              src/geometry.cpp:17-31,71-135,573-629 (mesh_to_json,
+                                mesh_from_json, save_mesh, load_mesh)
 
 Scalar arithmetic follows the reference's operation order (Python floats are
 IEEE doubles and the reference is compiled without FMA contraction), so the
@@ -175,6 +177,23 @@ class Segment:
 
     def derivative(self, t):
         return self.b[0] - self.a[0], self.b[1] - self.a[1]
+
+
+class CircularArc:
+    """include/fcs/geometry.hpp:37-55: center c, radius r, angle t0 -> t1"""
+
+    def __init__(self, center, radius, theta0, theta1):
+        self.c, self.r, self.t0, self.t1 = tuple(center), radius, theta0, theta1
+
+    def point(self, t):
+        cos, sin = (np.cos, np.sin) if isinstance(t, np.ndarray) else (math.cos, math.sin)
+        th = self.t0 + t * (self.t1 - self.t0)
+        return self.c[0] + self.r * cos(th), self.c[1] + self.r * sin(th)
+
+    def derivative(self, t):
+        cos, sin = (np.cos, np.sin) if isinstance(t, np.ndarray) else (math.cos, math.sin)
+        th = self.t0 + t * (self.t1 - self.t0)
+        return -self.r * (self.t1 - self.t0) * sin(th), self.r * (self.t1 - self.t0) * cos(th)
 
 
 class CurveSumMap(Mapping):
@@ -1345,3 +1364,123 @@ def _build_plan_fast(patches: list, subs: list, nf: int) -> Plan:
                                   src_sub=i32(cat(vis_i, 2, np.int64)), si0=i32(cat(vis_i, 3, np.int64)),
                                   sj0=i32(cat(vis_i, 4, np.int64)), wx=cat6(vis_i, 5), wy=cat6(vis_i, 6),
                                   w=cat(vis_i, 7, np.float64)))
+
+
+# ---------------------------------------------------------------------------
+# fcs-mesh v1 JSON (DomainDecomposition::to_json / from_json,
+# src/geometry.cpp:573-629; curves and mappings :17-31, :71-135): the
+# reference's mesh file, read and written with the same keys and values, so a
+# decomposition moves between the two codes. Python's float repr and
+# nlohmann::json both print the shortest round-trip form, so the numbers
+# survive either way exactly.
+
+MESH_FORMAT, MESH_VERSION = "fcs-mesh", 1
+
+
+def curve_to_json(c) -> dict:
+    if isinstance(c, Segment):
+        return {"type": "segment", "a": list(c.a), "b": list(c.b)}
+    if isinstance(c, CircularArc):
+        return {"type": "arc", "center": list(c.c), "r": c.r, "theta0": c.t0, "theta1": c.t1}
+    raise GeometryError(f"curve has no fcs-mesh form: {type(c).__name__}")
+
+
+def curve_from_json(j: dict):
+    t = j["type"]
+    if t == "segment":
+        return Segment(tuple(j["a"]), tuple(j["b"]))
+    if t == "arc":
+        return CircularArc(tuple(j["center"]), j["r"], j["theta0"], j["theta1"])
+    raise GeometryError("unknown curve type: " + t)
+
+
+def mapping_to_json(M) -> dict:
+    if isinstance(M, AffineMap):
+        return {"type": "affine", "o": list(M.o), "e1": list(M.e1), "e2": list(M.e2)}
+    if isinstance(M, AnnulusMap):
+        return {"type": "annulus", "center": list(M.c), "r0": M.r0, "r1": M.r1, "theta0": M.t0,
+                "theta_extent": M.dt}
+    if isinstance(M, BilinearMap):
+        a, b, c, d = M.a, M.b, M.c, M.d
+        p10 = (a[0] + b[0], a[1] + b[1])
+        p01 = (a[0] + c[0], a[1] + c[1])
+        p11 = (((a[0] + b[0]) + c[0]) + d[0], ((a[1] + b[1]) + c[1]) + d[1])
+        return {"type": "bilinear", "p00": list(a), "p10": list(p10), "p01": list(p01), "p11": list(p11)}
+    if isinstance(M, CurveSumMap):
+        return {"type": "curve_sum", "a": curve_to_json(M.A), "b": curve_to_json(M.B), "corner": list(M.C)}
+    raise GeometryError(f"mapping has no fcs-mesh form: {type(M).__name__}")
+
+
+def mapping_from_json(j: dict) -> Mapping:
+    t = j["type"]
+    if t == "affine":
+        return AffineMap(tuple(j["o"]), tuple(j["e1"]), tuple(j["e2"]))
+    if t == "annulus":
+        return AnnulusMap(tuple(j["center"]), j["r0"], j["r1"], j["theta0"], j["theta_extent"])
+    if t == "bilinear":
+        return BilinearMap(tuple(j["p00"]), tuple(j["p10"]), tuple(j["p01"]), tuple(j["p11"]))
+    if t == "curve_sum":
+        return CurveSumMap(curve_from_json(j["a"]), curve_from_json(j["b"]), tuple(j["corner"]))
+    raise GeometryError("unknown mapping type: " + t)
+
+
+def mesh_to_json(patches: list, nv: int, n0: int = 83, n1: int = 43, nf: int = 5) -> dict:
+    """DomainDecomposition::to_json (src/geometry.cpp:573-594) of subdivided
+    patches; nv, n0, n1, nf are the decomposition's fields."""
+    jp = []
+    for p in patches:
+        pj = {"kind": p.kind, "mapping": mapping_to_json(p.map), "r": p.r, "s": p.s, "n_cell": p.n_cell,
+              "nv": p.nv, "periodic1": bool(p.periodic1),
+              "sides": [{"on_gamma": bool(sd.on_gamma), "tag": sd.tag} for sd in p.sides]}
+        if p.kind == C1:
+            pj["wall_q1_tag"] = p.wall_q1.tag
+            pj["wall_q2_tag"] = p.wall_q2.tag
+        pj["subpatches"] = [[sp.i0, sp.i1, sp.j0, sp.j1, sp.i_cut, sp.j_cut] for sp in p.subpatches]
+        jp.append(pj)
+    return {"format": MESH_FORMAT, "version": MESH_VERSION, "nv": nv, "n0": n0, "n1": n1, "nf": nf,
+            "patches": jp}
+
+
+def mesh_from_json(j: dict):
+    """DomainDecomposition::from_json (src/geometry.cpp:596-629): patches
+    rebuilt from their mapping, sides and subdivision parameters (the
+    subpatch table is only checked for its length, as in the reference).
+    Returns (patches, {"nv", "n0", "n1", "nf"})."""
+    if j.get("format", "") != MESH_FORMAT or j.get("version", 0) != MESH_VERSION:
+        raise GeometryError("mesh file: unknown format/version")
+    patches = []
+    for idx, pj in enumerate(j["patches"]):
+        kind = pj["kind"]
+        if kind not in (S, C1, C2, I):
+            raise GeometryError("unknown patch kind: " + str(kind))
+        sides = [SideInfo(bool(pj["sides"][k]["on_gamma"]), pj["sides"][k]["tag"]) for k in range(4)]
+        p = Patch(kind, mapping_from_json(pj["mapping"]), sides, periodic1=bool(pj.get("periodic1", False)),
+                  index=idx)
+        if kind == C1:
+            p.wall_q1 = SideInfo(True, pj.get("wall_q1_tag", "wall"))
+            p.wall_q2 = SideInfo(True, pj.get("wall_q2_tag", "wall"))
+            subdivide_L(p, pj["r"], pj["n_cell"], pj["nv"])
+        else:
+            subdivide_Q(p, pj["r"], pj["s"], pj["n_cell"], pj["nv"])
+        if "subpatches" in pj and len(pj["subpatches"]) != len(p.subpatches):
+            raise GeometryError("mesh file: subpatch table does not match r/s parameters")
+        patches.append(p)
+    gid = 0
+    for p in patches:
+        for sp in p.subpatches:
+            sp.patch_index = p.index
+            sp.global_id = gid
+            gid += 1
+    return patches, {k: j[k] for k in ("nv", "n0", "n1", "nf")}
+
+
+def save_mesh(path: str, patches: list, nv: int, n0: int = 83, n1: int = 43, nf: int = 5):
+    import json
+    with open(path, "w") as f:
+        json.dump(mesh_to_json(patches, nv, n0, n1, nf), f, indent=2)
+
+
+def load_mesh(path: str):
+    import json
+    with open(path) as f:
+        return mesh_from_json(json.load(f))
