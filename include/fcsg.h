@@ -174,8 +174,32 @@ int fcsg_engine_finalize(fcsg_engine* eng);
 /* state e = (rho, rho u, rho v, E), [4][nj][ni] (State, include/fcs/subpatch_data.hpp:15) */
 int fcsg_engine_set_state(fcsg_engine* eng, int sub, const double* e4);
 /* fields: "e","e0","e2","e3","rhs3","rhs" (comp 0..3), "mu_hat","mu","tau",
- * "speed","proxy","m01","iq1x","iq2x","iq1y","iq2y","h_min","h_max","w_norm" */
+ * "speed","proxy","m01","iq1x","iq2x","iq1y","iq2y","h_min","h_max","w_norm",
+ * "grad" (after fcsg_engine_gradient) */
 int fcsg_engine_get_field(fcsg_engine* eng, int sub, const char* name, int comp, double* out);
+
+/* Measurements on the device (src/workbench.cpp:187-294, replacing the
+ * per-subpatch CPU loops of energy_integral / area_integral /
+ * density_gradient_raster; the writers and the raster's point location stay
+ * with the caller).
+ * fcsg_engine_gradient: |grad e_comp| = hypot(iq1x d1 + iq2x d2, iq1y d1 + iq2y d2)
+ *   with d1, d2 the FC derivatives along rows / columns (deriv_q1/q2), into
+ *   the "grad" field.
+ * fcsg_engine_set_quadrature: per-point weights of window_quadrature for one
+ *   subpatch, [nj][ni]: w_norm |det J|, halved on the first/last point of
+ *   each row segment and of each column segment, 0 outside the set.
+ * fcsg_engine_integrals: per subpatch (id order) h1 h2 sum wq v, v = 1
+ *   (comp = -1, area_integral) or e_comp (comp = 3: energy_integral); the
+ *   caller adds them in id order.
+ * fcsg_engine_sample: bilinear samples of "grad" at n points given as
+ *   (subpatch id, local cell origin il, jl, fractions fu, fv) -- the raster
+ *   pixel's containing subpatch as density_gradient_raster picks it; sub < 0
+ *   gives 0. */
+int fcsg_engine_gradient(fcsg_engine* eng, int comp);
+int fcsg_engine_set_quadrature(fcsg_engine* eng, int sub, const double* wq);
+int fcsg_engine_integrals(fcsg_engine* eng, int comp, double* per_sub);
+int fcsg_engine_sample(fcsg_engine* eng, long n, const int* sub, const int* il, const int* jl, const double* fu,
+                       const double* fv, double* out);
 /* whole state of every subpatch in one call, component-major host layout
  * [4][S][nj][ni] (pinned host memory gives full PCIe/C2C bandwidth) */
 int fcsg_engine_set_state_bulk(fcsg_engine* eng, const double* e);

@@ -37,6 +37,12 @@ def lib():
         L.ref_train_classifier.argtypes = [C.c_char_p, dp]
         L.ref_mlp_forward.argtypes = [C.c_char_p, C.c_int, dp, dp, ip]
         L.ref_classify_line.argtypes = [C.c_char_p, C.c_int, dp, ip]
+        L.ref_engine_integrals.argtypes = [C.c_void_p, dp, dp]
+        L.ref_engine_raster.argtypes = [C.c_void_p, C.c_int, C.c_int, dp, dp]
+        L.ref_write_schlieren_pgm.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, C.c_char_p]
+        L.ref_fit_shock_angle.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, C.c_double, C.c_double, C.c_double,
+                                          dp]
+        L.ref_engine_write_csv.argtypes = [C.c_void_p, C.c_char_p]
         L.ref_engine_mesh_json.argtypes = [C.c_void_p, C.c_char_p, C.c_long, C.POINTER(C.c_long)]
         L.ref_mesh_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_long, C.POINTER(C.c_long)]
         L.ref_classify_line_fallback.argtypes = [C.c_int, C.c_double, C.c_int, dp, ip]
@@ -176,6 +182,61 @@ def mesh_roundtrip(mesh: dict) -> dict:
     return _json_out(lambda b, c, n: lib().ref_mesh_roundtrip(text, b, c, n))
 
 
+# The reference's file writers (std::ofstream) crash when called in a process
+# that has numpy loaded (observed with this image's numpy wheels), so they run
+# in a child interpreter that loads only ctypes; inputs travel as raw doubles.
+def _isolated(code: str, *args):
+    import subprocess
+    import sys
+    script = "import ctypes as C, array, sys\nL = C.CDLL(%r)\n" % LIB_PATH + code
+    r = subprocess.run([sys.executable, "-c", script, *map(str, args)], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RefError(9, f"isolated reference call failed ({r.returncode}): {r.stderr[-400:]}")
+    return r.stdout
+
+
+def write_schlieren_pgm(v, meta, beta, path):
+    """write_pgm(schlieren(raster, beta), path) of the reference"""
+    import tempfile
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    with tempfile.NamedTemporaryFile(suffix=".bin", delete=False) as f:
+        f.write(np.ascontiguousarray(meta, dtype=np.float64).tobytes() + v.tobytes())
+        blob = f.name
+    try:
+        _isolated("""
+a = array.array("d"); a.frombytes(open(sys.argv[1], "rb").read())
+nx, ny = int(sys.argv[2]), int(sys.argv[3])
+meta = (C.c_double * 4)(*a[:4]); v = (C.c_double * (nx * ny))(*a[4:])
+L.ref_write_schlieren_pgm.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_double, C.c_char_p]
+rc = L.ref_write_schlieren_pgm(nx, ny, meta, v, float(sys.argv[4]), sys.argv[5].encode())
+sys.exit(rc)
+""", blob, v.shape[1], v.shape[0], repr(float(beta)), path)
+    finally:
+        os.unlink(blob)
+
+
+def testgeom_write_csv(which, n0, out_dir, weight_path=""):
+    """write_subpatch_csv of ref_engine_testgeom(which, n0) right after
+    Engine::init"""
+    _isolated("""
+L.ref_engine_testgeom.restype = C.c_void_p
+L.ref_engine_testgeom.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_char_p]
+L.ref_engine_write_csv.argtypes = [C.c_void_p, C.c_char_p]
+h = L.ref_engine_testgeom(int(sys.argv[1]), int(sys.argv[2]), 9, 0.5, 1, sys.argv[4].encode())
+if not h:
+    sys.exit(3)
+sys.exit(L.ref_engine_write_csv(h, sys.argv[3].encode()))
+""", which, n0, out_dir, weight_path or "")
+
+
+def fit_shock_angle(v, meta, x_lo, x_hi, y_lo, y_hi):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    m = np.ascontiguousarray(meta, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().ref_fit_shock_angle(v.shape[1], v.shape[0], _dp(m), _dp(v), x_lo, x_hi, y_lo, y_hi, C.byref(out)))
+    return out.value
+
+
 class RefEngine:
     """Engine over one affine I patch origin + q1 e1 + q2 e2 (ref_engine_affine);
     (lx, ly) alone is the axis-aligned rectangle."""
@@ -235,6 +296,19 @@ class RefEngine:
             _check(lib().ref_engine_dims(h, k, C.byref(a), C.byref(b)))
             self.dims.append((a.value, b.value))
         return self
+
+    def integrals(self):
+        """(energy_integral, area_integral)"""
+        e, a = C.c_double(), C.c_double()
+        _check(lib().ref_engine_integrals(self.h, C.byref(e), C.byref(a)))
+        return e.value, a.value
+
+    def raster(self, nx, ny):
+        """density_gradient_raster: (v[ny, nx], (x0, y0, dx, dy))"""
+        v = np.zeros((ny, nx))
+        meta = np.zeros(4)
+        _check(lib().ref_engine_raster(self.h, nx, ny, _dp(v), _dp(meta)))
+        return v, meta
 
     def mesh_json(self) -> dict:
         """the reference's fcs-mesh v1 JSON of this engine's decomposition"""

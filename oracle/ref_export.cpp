@@ -105,6 +105,8 @@ const Field* field_by_name(const SubpatchData& d, const std::string& w, int c) {
     if (w == "h_min") return &d.h_min;
     if (w == "h_max") return &d.h_max;
     if (w == "w_norm") return &d.w_norm;
+    if (w == "det") return &d.det;
+    if (w == "grad") return &d.s1;  // |grad rho| after density_gradient_raster
     if (w == "mu_hat") return &d.mu_hat;
     if (w == "mu") return &d.mu;
     if (w == "tau") return &d.tau;
@@ -634,6 +636,57 @@ int ref_mesh_roundtrip(const char* in, char* buf, long cap, long* len) {
             buf[n] = 0;
         }
     });
+}
+
+/* energy_integral / area_integral (src/workbench.cpp:212-220) */
+int ref_engine_integrals(void* h, double* energy, double* area) {
+    return guard([&] {
+        const auto& eng = *static_cast<RefEngine*>(h)->eng;
+        *energy = wb::energy_integral(eng);
+        *area = wb::area_integral(eng);
+    });
+}
+
+/* density_gradient_raster (src/workbench.cpp:222-305): v[ny][nx], meta = x0, y0, dx, dy */
+int ref_engine_raster(void* h, int nx, int ny, double* v, double* meta) {
+    return guard([&] {
+        const wb::Raster r = wb::density_gradient_raster(*static_cast<RefEngine*>(h)->eng, nx, ny);
+        std::copy(r.v.begin(), r.v.end(), v);
+        meta[0] = r.x0;
+        meta[1] = r.y0;
+        meta[2] = r.dx;
+        meta[3] = r.dy;
+    });
+}
+
+namespace {
+wb::Raster raster_of(int nx, int ny, const double* meta, const double* v) {
+    wb::Raster r;
+    r.nx = nx;
+    r.ny = ny;
+    r.x0 = meta[0];
+    r.y0 = meta[1];
+    r.dx = meta[2];
+    r.dy = meta[3];
+    r.v.assign(v, v + static_cast<size_t>(nx) * ny);
+    return r;
+}
+}  // namespace
+
+/* write_pgm(schlieren(raster, beta)) (src/workbench.cpp:307-333) */
+int ref_write_schlieren_pgm(int nx, int ny, const double* meta, const double* v, double beta, const char* path) {
+    return guard([&] { wb::write_pgm(wb::schlieren(raster_of(nx, ny, meta, v), beta), path); });
+}
+
+/* fit_shock_angle (src/workbench.cpp:335-366) */
+int ref_fit_shock_angle(int nx, int ny, const double* meta, const double* v, double x_lo, double x_hi, double y_lo,
+                        double y_hi, double* deg) {
+    return guard([&] { *deg = wb::fit_shock_angle(raster_of(nx, ny, meta, v), x_lo, x_hi, y_lo, y_hi); });
+}
+
+/* write_subpatch_csv (src/workbench.cpp:368-386) */
+int ref_engine_write_csv(void* h, const char* dir) {
+    return guard([&] { wb::write_subpatch_csv(*static_cast<RefEngine*>(h)->eng, dir); });
 }
 
 void ref_engine_destroy(void* h) { delete static_cast<RefEngine*>(h); }

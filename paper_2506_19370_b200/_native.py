@@ -95,6 +95,10 @@ def _declare(L):
     L.fcsg_engine_set_state.argtypes = [vp, C.c_int, dp]
     L.fcsg_engine_get_field.argtypes = [vp, C.c_int, C.c_char_p, C.c_int, dp]
     L.fcsg_engine_set_field.argtypes = [vp, C.c_int, C.c_char_p, C.c_int, dp]
+    L.fcsg_engine_gradient.argtypes = [vp, C.c_int]
+    L.fcsg_engine_set_quadrature.argtypes = [vp, C.c_int, dp]
+    L.fcsg_engine_integrals.argtypes = [vp, C.c_int, dp]
+    L.fcsg_engine_sample.argtypes = [vp, C.c_long, ip, ip, ip, dp, dp, dp]
     L.fcsg_engine_finish_ic.argtypes = [vp]
     L.fcsg_engine_phase.argtypes = [vp, C.c_int, C.c_int]
     L.fcsg_engine_reduce_dt.argtypes = [vp, dp]

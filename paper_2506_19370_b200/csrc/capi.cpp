@@ -385,6 +385,27 @@ int fcsg_engine_get_field(fcsg_engine* e, int sub, const char* name, int comp, d
     return guard(e->ctx, [&] { e->eng->get_field(sub, name, comp, out); });
 }
 
+int fcsg_engine_gradient(fcsg_engine* e, int comp) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->gradient(comp); });
+}
+
+int fcsg_engine_set_quadrature(fcsg_engine* e, int sub, const double* wq) {
+    if (!e || !wq) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->set_quadrature(sub, wq); });
+}
+
+int fcsg_engine_integrals(fcsg_engine* e, int comp, double* per_sub) {
+    if (!e || !per_sub) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->integrals(comp, per_sub); });
+}
+
+int fcsg_engine_sample(fcsg_engine* e, long n, const int* sub, const int* il, const int* jl, const double* fu,
+                       const double* fv, double* out) {
+    if (!e || (n > 0 && (!sub || !il || !jl || !fu || !fv || !out))) return FCSG_USAGE;
+    return guard(e->ctx, [&] { e->eng->sample(n, sub, il, jl, fu, fv, out); });
+}
+
 int fcsg_engine_set_field(fcsg_engine* e, int sub, const char* name, int comp, const double* in) {
     if (!e) return FCSG_USAGE;
     return guard(e->ctx, [&] { e->eng->set_field(sub, name, comp, in); });

@@ -426,10 +426,11 @@ void Engine::finalize() {
     for (int c = 0; c < 4; ++c) E.tS4[c] = nextf();
     for (int c = 0; c < 4; ++c) E.tS5[c] = nextf();
     for (int c = 0; c < 4; ++c) E.tF[c] = E.tA[c];  // phase 2 and the stage passes never overlap
-    // tau starts at 4 everywhere (Classifier::classify fills 4, src/viscosity.cpp:212)
+    // tau is 0 until the first phase 0 (a zero-filled Field, as in the
+    // reference; Classifier::classify then writes every point)
     {
-        std::vector<double> four(npts_, 4.0), one(npts_, 1.0);
-        dev::h2d(E.tau, four.data(), npts_ * sizeof(double), ctx_.stream);
+        std::vector<double> one(npts_, 1.0);
+        dev::memset0(E.tau, npts_ * sizeof(double), ctx_.stream);
         dev::h2d(E.speed, one.data(), npts_ * sizeof(double), ctx_.stream);
     }
     if (have_plan_) {
@@ -722,6 +723,10 @@ double* Engine::field_ptr(const std::string& w, int c) {
     if (w == "h_min") return const_cast<double*>(E.h_min);
     if (w == "h_max") return const_cast<double*>(E.h_max);
     if (w == "w_norm") return const_cast<double*>(E.w_norm);
+    if (w == "grad") {
+        if (!E.diag) throw Error(kUsage, "grad: call fcsg_engine_gradient first");
+        return E.diag;
+    }
     throw Error(kUsage, "unknown field " + w);
 }
 
@@ -784,6 +789,96 @@ void Engine::set_field(int sub, const std::string& name, int comp, const double*
     if (sub < 0 || sub >= static_cast<int>(subs_.size())) throw Error(kUsage, "bad subpatch id");
     double* f = field_ptr(name, comp);
     dev::h2d(f + off_of_slot_[slot_of_[sub]], in, sub_points(sub) * sizeof(double), ctx_.stream);
+}
+
+void Engine::gradient(int comp) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    if (comp < 0 || comp > 3) throw Error(kUsage, "bad component");
+    if (!E_.diag) {
+        E_.diag = static_cast<double*>(dev::alloc(npts_ * sizeof(double)));
+        allocs_.push_back(E_.diag);
+        dev::memset0(E_.diag, npts_ * sizeof(double), ctx_.stream);
+        // views: the same offset as their state pointers
+        auto fix = [&](GroupLaunch& g) { g.E.diag = E_.diag + (g.E.e[0] - E_.e[0]); };
+        for (auto& g : G_) fix(g);
+        for (auto& c : chunks_)
+            for (auto& g : c) fix(g);
+    }
+    launch_gradient(G_, comp, ctx_.stream);
+    dev::check("gradient");
+}
+
+void Engine::set_quadrature(int sub, const double* wq) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    if (sub < 0 || sub >= static_cast<int>(subs_.size())) throw Error(kUsage, "bad subpatch id");
+    if (!E_.wq) {
+        double* w = static_cast<double*>(dev::alloc(npts_ * sizeof(double)));
+        allocs_.push_back(w);
+        dev::memset0(w, npts_ * sizeof(double), ctx_.stream);
+        E_.wq = w;
+        wq_set_.assign(subs_.size(), 0);
+    }
+    dev::h2d(const_cast<double*>(E_.wq) + off_of_slot_[slot_of_[sub]], wq, sub_points(sub) * sizeof(double),
+             ctx_.stream);
+    wq_set_[sub] = 1;
+}
+
+void Engine::integrals(int comp, double* per_sub) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    if (comp < -1 || comp > 3) throw Error(kUsage, "bad component");
+    const int S = static_cast<int>(subs_.size());
+    for (int k = 0; k < S; ++k)
+        if (!E_.wq || !wq_set_[k]) throw Error(kUsage, "quadrature weights not set for every subpatch");
+    if (!d_slot_off_) {
+        std::vector<long> off(S + 1);
+        for (int s = 0; s < S; ++s) off[s] = off_of_slot_[s];
+        off[S] = npts_;
+        d_slot_off_ = static_cast<long*>(dev::alloc(off.size() * sizeof(long)));
+        allocs_.push_back(d_slot_off_);
+        dev::h2d(d_slot_off_, off.data(), off.size() * sizeof(long), ctx_.stream);
+        d_quad_out_ = static_cast<double*>(dev::alloc(S * sizeof(double)));
+        allocs_.push_back(d_quad_out_);
+    }
+    launch_integrals(E_, comp, d_slot_off_, S, d_quad_out_, ctx_.stream);
+    std::vector<double> by_slot(S);
+    dev::d2h(by_slot.data(), d_quad_out_, S * sizeof(double), ctx_.stream);
+    // total += acc * p.h1 * p.h2 per subpatch (src/workbench.cpp:207)
+    for (int id = 0; id < S; ++id) per_sub[id] = by_slot[slot_of_[id]] * subs_[id].h1 * subs_[id].h2;
+}
+
+void Engine::sample(long n, const int* sub, const int* il, const int* jl, const double* fu, const double* fv,
+                    double* out) {
+    if (!E_.diag) throw Error(kUsage, "sample: call fcsg_engine_gradient first");
+    std::vector<long> base(n);
+    std::vector<int> pitch(n);
+    for (long k = 0; k < n; ++k) {
+        const int s = sub[k];
+        if (s < 0) {
+            base[k] = -1;
+            pitch[k] = 0;
+            continue;
+        }
+        if (s >= static_cast<int>(subs_.size())) throw Error(kUsage, "bad subpatch id");
+        const SubSpec& d = subs_[s];
+        if (il[k] < 0 || jl[k] < 0 || il[k] > d.ni - 2 || jl[k] > d.nj - 2) throw Error(kUsage, "sample outside subpatch");
+        base[k] = off_of_slot_[slot_of_[s]] + static_cast<long>(jl[k]) * d.ni + il[k];
+        pitch[k] = d.ni;
+    }
+    const size_t nb = static_cast<size_t>(n);
+    long* db = static_cast<long*>(dev::alloc(nb * sizeof(long)));
+    int* dp = static_cast<int*>(dev::alloc(nb * sizeof(int)));
+    double* du = static_cast<double*>(dev::alloc(nb * sizeof(double)));
+    double* dv = static_cast<double*>(dev::alloc(nb * sizeof(double)));
+    double* dout = static_cast<double*>(dev::alloc(nb * sizeof(double)));
+    dev::h2d(db, base.data(), nb * sizeof(long), ctx_.stream);
+    dev::h2d(dp, pitch.data(), nb * sizeof(int), ctx_.stream);
+    dev::h2d(du, fu, nb * sizeof(double), ctx_.stream);
+    dev::h2d(dv, fv, nb * sizeof(double), ctx_.stream);
+    launch_sample(E_.diag, n, db, dp, du, dv, dout, ctx_.stream);
+    dev::d2h(out, dout, nb * sizeof(double), ctx_.stream);
+    for (void* p : {static_cast<void*>(db), static_cast<void*>(dp), static_cast<void*>(du), static_cast<void*>(dv),
+                    static_cast<void*>(dout)})
+        dev::free(p);
 }
 
 void Engine::check_error() {

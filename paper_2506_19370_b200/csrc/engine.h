@@ -118,6 +118,16 @@ class Engine {
     bool cartesian() const;
     int n_groups() const { return static_cast<int>(G_.size()); }
     void check_error();
+
+    // diagnostics (src/workbench.cpp:187-239): |grad e_comp| into the "grad"
+    // field; per-subpatch window quadrature h1 h2 sum wq value (value = 1 for
+    // comp < 0, else e_comp) once every subpatch's weights are set; bilinear
+    // samples of "grad" at raster pixels (sub < 0: outside -> 0)
+    void gradient(int comp);
+    void set_quadrature(int sub, const double* wq);
+    void integrals(int comp, double* per_sub);
+    void sample(long n, const int* sub, const int* il, const int* jl, const double* fu, const double* fv,
+                double* out);
     // average device milliseconds of one launch group (profiling hook):
     // 0 phase 0 (proxy + classifier), 1 phase 1 (blend + dt), 2 phase 2
     // (filter rows + cols), 3 pass A, 4 pass B, 5 pass C (stage 1), 6 BC,
@@ -189,6 +199,9 @@ class Engine {
     static constexpr long kChunkPoints = 1L << 21;
     std::vector<void*> cstreams_, cevents_;
     void ensure_streams();
+    std::vector<char> wq_set_;
+    long* d_slot_off_ = nullptr;
+    double* d_quad_out_ = nullptr;
     void* ev_stage_ = nullptr;
 };
 

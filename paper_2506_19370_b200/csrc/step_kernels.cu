@@ -526,6 +526,60 @@ struct PassC {
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
+// ---- diagnostics: |grad e_c| (density_gradient_raster, src/workbench.cpp:222-239)
+// rows: d/dq1 of e_c into tA[0] (SubpatchData::deriv_q1); columns: d/dq2,
+// then gx = iq1x d1 + iq2x d2, gy = iq1y d1 + iq2y d2, |grad| = hypot(gx, gy)
+// at the points of the set, 0 elsewhere
+struct PassDiagR {
+    static constexpr bool kRows = true;
+    static constexpr int kRounds = 1;
+    static constexpr int kStage = 0;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 8;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    int comp;
+    FCSG_HD PassDiagR(const EngineDev& e, int c) : E(e), comp(c) {}
+    FCSG_HD int mode(int) const { return 1; }
+    static constexpr int kFetch = 1;
+    FCSG_HD void fetch(int, long p, double* v) const { v[0] = ldg1(E.e[comp] + p); }
+    FCSG_HD double2 load(int, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        return mk2(fv[0], 0.0);
+    }
+    FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
+    FCSG_HD double2 store(int, long p, double2 v, const double*, int, const LineCtx&, const double*) const {
+        E.tA[0][p] = v.x;
+        return {};
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+struct PassDiagC {
+    static constexpr bool kRows = false;
+    static constexpr int kRounds = 1;
+    static constexpr int kStage = 0;
+    static constexpr int kStash = 0;
+    static constexpr int kLB = 4;
+    static constexpr bool kScaled = true;
+    const EngineDev& E;
+    int comp;
+    FCSG_HD PassDiagC(const EngineDev& e, int c) : E(e), comp(c) {}
+    FCSG_HD int mode(int) const { return 1; }
+    static constexpr int kFetch = 1;
+    FCSG_HD void fetch(int, long p, double* v) const { v[0] = ldg1(E.e[comp] + p); }
+    FCSG_HD double2 load(int, long, const LineCtx&, double2, const double* fv, double*, int) const {
+        return mk2(fv[0], 0.0);
+    }
+    FCSG_HD int stage_srcs(int, long, const double**) const { return 0; }
+    FCSG_HD double2 store(int, long p, double2 v, const double*, int, const LineCtx&, const double*) const {
+        const double d1 = E.tA[0][p], d2 = v.x;
+        const double gx = E.iq1x[p] * d1 + E.iq2x[p] * d2;
+        const double gy = E.iq1y[p] * d1 + E.iq2y[p] * d2;
+        E.diag[p] = hypot(gx, gy);
+        return {};
+    }
+    FCSG_HD void finish(Thr, const LineCtx&, int) const {}
+};
+
 // ---- Cartesian subpatches --------------------------------------------------
 // When iq2x and iq1y vanish identically (axis-aligned affine maps, every
 // subpatch of BASELINE configs 2 and 5), the reference still computes
@@ -2119,6 +2173,83 @@ void launch_pass_c(const std::vector<GroupLaunch>& G, int stage, void* stream) {
             run_rows<PassC>(stage, g, stream);
         }
     }
+}
+
+void launch_gradient(const std::vector<GroupLaunch>& G, int comp, void* stream) {
+    for (const GroupLaunch& g : G) {
+        run_rows<PassDiagR>(comp, g, stream);
+        run_cols<PassDiagC>(comp, g, stream);
+    }
+}
+
+// window_quadrature (src/workbench.cpp:187-210), one block per storage slot
+FCSG_HD double integrand(const EngineDev& E, int comp, long p) { return comp < 0 ? 1.0 : E.e[comp][p]; }
+#if FCSG_CUDA
+constexpr int kQuadThreads = 256;
+__global__ void __launch_bounds__(kQuadThreads) integrals_kernel(const __grid_constant__ EngineDev E, int comp,
+                                                                  const long* slot_off, double* out) {
+    __shared__ double red[kQuadThreads];
+    const long p0 = slot_off[blockIdx.x], p1 = slot_off[blockIdx.x + 1];
+    double acc = 0.0;
+    for (long p = p0 + threadIdx.x; p < p1; p += kQuadThreads) acc += E.wq[p] * integrand(E, comp, p);
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int h = kQuadThreads / 2; h > 0; h >>= 1) {
+        if (static_cast<int>(threadIdx.x) < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+__global__ void sample_kernel(const double* f, long n, const long* base, const int* pitch, const double* fu,
+                              const double* fv, double* out) {
+    for (long k = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+         k += static_cast<long>(gridDim.x) * blockDim.x) {
+        const long b = base[k];
+        if (b < 0) {
+            out[k] = 0.0;
+            continue;
+        }
+        const long w = pitch[k];
+        const double u = fu[k], v = fv[k];
+        // src/workbench.cpp:293-294, same expression order
+        out[k] = (1 - u) * (1 - v) * f[b] + u * (1 - v) * f[b + 1] + (1 - u) * v * f[b + w] + u * v * f[b + w + 1];
+    }
+}
+#endif
+
+void launch_integrals(const EngineDev& Eall, int comp, const long* slot_off, int S, double* out, void* stream) {
+#if FCSG_CUDA
+    integrals_kernel<<<S, kQuadThreads, 0, static_cast<cudaStream_t>(stream)>>>(Eall, comp, slot_off, out);
+#else
+    (void)stream;
+    for (int s = 0; s < S; ++s) {
+        double acc = 0.0;
+        for (long p = slot_off[s]; p < slot_off[s + 1]; ++p) acc += Eall.wq[p] * integrand(Eall, comp, p);
+        out[s] = acc;
+    }
+#endif
+}
+
+void launch_sample(const double* f, long n, const long* base, const int* pitch, const double* fu, const double* fv,
+                   double* out, void* stream) {
+    if (n <= 0) return;
+#if FCSG_CUDA
+    long g = (n + 255) / 256;
+    g = g > 148 * 16 ? 148 * 16 : g;
+    sample_kernel<<<static_cast<int>(g), 256, 0, static_cast<cudaStream_t>(stream)>>>(f, n, base, pitch, fu, fv, out);
+#else
+    (void)stream;
+    for (long k = 0; k < n; ++k) {
+        const long b = base[k];
+        if (b < 0) {
+            out[k] = 0.0;
+            continue;
+        }
+        const long w = pitch[k];
+        const double u = fu[k], v = fv[k];
+        out[k] = (1 - u) * (1 - v) * f[b] + u * (1 - v) * f[b + 1] + (1 - u) * v * f[b + w] + u * v * f[b + w + 1];
+    }
+#endif
 }
 
 int stage_launches(const std::vector<GroupLaunch>& G) {

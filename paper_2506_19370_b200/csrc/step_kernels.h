@@ -98,6 +98,11 @@ struct EngineDev {
     double* tS4[4];  // mu * grad_x w
     double* tS5[4];  // mu * grad_y w
     double* tF[4];   // filter/smear row results
+    // diagnostics (workbench.cpp measurements): |grad e_c| per point
+    // (allocated on first use) and the quadrature weights w_norm |det J|
+    // x trapezoid factors (set by the caller)
+    double* diag;
+    const double* wq;
     // viscosity blend plan, CSR by recipient point (global view): copies,
     // then 6x6 tensor Lagrange interpolations (w, wx[6], wy[6] per entry)
     const int* visc_off;     // npts + 1
@@ -177,6 +182,15 @@ void launch_pass_b(const std::vector<GroupLaunch>& G, int stage, void* stream);
 void launch_pass_c(const std::vector<GroupLaunch>& G, int stage, void* stream);
 // line-pass launches per stage (2 per line set for the Cartesian flux form, else 3)
 int stage_launches(const std::vector<GroupLaunch>& G);
+// diagnostics: |grad e_comp| into E.diag (two line passes per group);
+// per-slot window quadrature sums of wq * (comp < 0 ? 1 : e_comp) into
+// out[slot] (device, S doubles; slot_off = S + 1 point offsets); bilinear
+// samples of E.diag at n raster pixels (corner point index, row pitch,
+// fractions; base < 0 = outside the domain -> 0) into out (device)
+void launch_gradient(const std::vector<GroupLaunch>& G, int comp, void* stream);
+void launch_integrals(const EngineDev& Eall, int comp, const long* slot_off, int S, double* out, void* stream);
+void launch_sample(const double* f, long n, const long* base, const int* pitch, const double* fu, const double* fv,
+                   double* out, void* stream);
 // kernel launches per superstep (excluding the t=0 dilation)
 int launches_per_step(const std::vector<GroupLaunch>& G);
 void launch_bc(const std::vector<GroupLaunch>& G, void* stream);

@@ -177,6 +177,33 @@ class Engine:
     def get_state(self, sub, name="e"):
         return np.stack([self.get(sub, name, c) for c in range(4)])
 
+    # -- diagnostics (fcsg_engine_gradient / set_quadrature / integrals /
+    #    sample; diagnostics.py builds on these) -----------------------------
+    def gradient(self, comp=0):
+        """|grad e_comp| into the "grad" field (FC derivatives on the device)"""
+        self.ctx.check(self.ctx.lib.fcsg_engine_gradient(self.h, int(comp)))
+
+    def set_quadrature(self, sub, wq):
+        a = np.ascontiguousarray(wq, dtype=np.float64)
+        if a.shape != tuple(self.shapes[sub]):
+            raise ValueError("quadrature weights must have the subpatch's shape")
+        self.ctx.check(self.ctx.lib.fcsg_engine_set_quadrature(self.h, sub, N.dptr(a)))
+
+    def integrals(self, comp):
+        """per subpatch h1 h2 sum wq v (v = 1 for comp = -1, else e_comp)"""
+        out = np.zeros(len(self.shapes))
+        self.ctx.check(self.ctx.lib.fcsg_engine_integrals(self.h, int(comp), N.dptr(out)))
+        return out
+
+    def sample(self, sub, il, jl, fu, fv):
+        """bilinear samples of "grad" at (sub, il, jl, fu, fv); sub < 0 -> 0"""
+        ints = [np.ascontiguousarray(a, dtype=np.int32) for a in (sub, il, jl)]
+        dbl = [np.ascontiguousarray(a, dtype=np.float64) for a in (fu, fv)]
+        out = np.zeros(ints[0].size)
+        self.ctx.check(self.ctx.lib.fcsg_engine_sample(self.h, ints[0].size, *[a.ctypes.data_as(N.ip) for a in ints],
+                                                       N.dptr(dbl[0]), N.dptr(dbl[1]), N.dptr(out)))
+        return out
+
     def set(self, sub, name, arr, comp=0):
         a = np.ascontiguousarray(arr, dtype=np.float64)
         self.ctx.check(self.ctx.lib.fcsg_engine_set_field(self.h, sub, name.encode(), comp, N.dptr(a)))

@@ -199,6 +199,7 @@ class SubData:
     # (i < cut_i and j < cut_j) are not in the set
     cut_i: int = 0
     cut_j: int = 0
+    det: np.ndarray = None  # |det J| (SubpatchData::det): window quadrature
 
 
 @dataclass
@@ -268,7 +269,8 @@ def init_subpatch_data(p: AffinePatch, sp: Subpatch, nf: int, bcs: dict) -> SubD
                    mask=fringe_mask(p, sp, nf), x=x, y=y, iq1x=iq1x, iq2x=iq2x, iq1y=iq1y, iq2y=iq2y,
                    h_min=np.minimum(h1p, h2p), h_max=np.maximum(h1p, h2p),
                    bc_row_lo=[resolve(0, False)] * sp.nj, bc_row_hi=[resolve(0, True)] * sp.nj,
-                   bc_col_lo=[resolve(1, False)] * sp.ni, bc_col_hi=[resolve(1, True)] * sp.ni)
+                   bc_col_lo=[resolve(1, False)] * sp.ni, bc_col_hi=[resolve(1, True)] * sp.ni,
+                   det=np.full(sh, abs(det)))
 
 
 def build_plan(p: AffinePatch, subs: list, nf: int) -> Plan:

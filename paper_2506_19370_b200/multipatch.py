@@ -605,6 +605,7 @@ class SubData:
     bc_row_hi: list
     bc_col_lo: list
     bc_col_hi: list
+    det: np.ndarray = None  # |det J| (SubpatchData::det, src/subpatch_data.cpp:110): quadrature
 
 
 def init_subpatch_data(p: Patch, sp: Subpatch, nf: int, bcs: dict) -> SubData:
@@ -615,6 +616,7 @@ def init_subpatch_data(p: Patch, sp: Subpatch, nf: int, bcs: dict) -> SubData:
     x, y = np.zeros(sh), np.zeros(sh)
     iq1x, iq2x, iq1y, iq2y = (np.zeros(sh) for _ in range(4))
     hmin, hmax = np.zeros(sh), np.zeros(sh)
+    detJ = np.zeros(sh)
     M = p.map
     for j in range(sp.j0, sp.j1 + 1):
         for i in range(sp.i0, sp.i1 + 1):
@@ -624,8 +626,10 @@ def init_subpatch_data(p: Patch, sp: Subpatch, nf: int, bcs: dict) -> SubData:
             q1, q2 = i * p.h1, j * p.h2
             xp = M(q1, q2)
             x[jl, il], y[jl, il] = xp
-            Ji = _inv(M.jacobian(q1, q2))
+            Jm = M.jacobian(q1, q2)
+            Ji = _inv(Jm)
             iq1x[jl, il], iq2x[jl, il], iq1y[jl, il], iq2y[jl, il] = Ji[0], Ji[2], Ji[1], Ji[3]
+            detJ[jl, il] = abs(Jm[0] * Jm[3] - Jm[1] * Jm[2])
             a, b = M(q1 + p.h1, q2), M(q1 - p.h1, q2)
             c, d = M(q1, q2 + p.h2), M(q1, q2 - p.h2)
             h1p = max(_hypot(a[0] - xp[0], a[1] - xp[1]), _hypot(xp[0] - b[0], xp[1] - b[1]))
@@ -648,7 +652,7 @@ def init_subpatch_data(p: Patch, sp: Subpatch, nf: int, bcs: dict) -> SubData:
                    [resolve(0, j, False) for j in range(sp.j0, sp.j1 + 1)],
                    [resolve(0, j, True) for j in range(sp.j0, sp.j1 + 1)],
                    [resolve(1, i, False) for i in range(sp.i0, sp.i1 + 1)],
-                   [resolve(1, i, True) for i in range(sp.i0, sp.i1 + 1)])
+                   [resolve(1, i, True) for i in range(sp.i0, sp.i1 + 1)], detJ)
 
 
 def _place(p: Patch, sp: Subpatch, u, v, eps):
@@ -1060,7 +1064,7 @@ def _init_subpatch_data_fast(p: Patch, sp: Subpatch, nf: int, bcs: dict) -> SubD
     l_cut = sp.i_cut > sp.i0 and sp.j_cut > sp.j0
     return SubData(sp, p.index, ni, nj, p.h1, p.h2, sp.i_cut - sp.i0 if l_cut else 0,
                    sp.j_cut - sp.j0 if l_cut else 0, mask, z(x), z(y), z(ia), z(ic), z(ib), z(id_),
-                   z(np.minimum(h1p, h2p)), z(np.maximum(h1p, h2p)), np.zeros((nj, ni)), *base)
+                   z(np.minimum(h1p, h2p)), z(np.maximum(h1p, h2p)), np.zeros((nj, ni)), *base, z(np.abs(det)))
 
 
 def init_subpatch_data_lines(p: Patch, sp: Subpatch, bcs: dict):
