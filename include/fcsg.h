@@ -218,6 +218,16 @@ int fcsg_engine_advance(fcsg_engine* eng);
  * steps replay one CUDA graph. Stops when t >= T - 1e-15. *done = steps run.
  * Errors: FCSG_INVALID_STATE with fcsg_last_error's patch/subpatch/i/j/t. */
 int fcsg_engine_run(fcsg_engine* eng, long n, int use_graph, long* done);
+/* n supersteps with host I/O every step (Engine::run plus the host-side state
+ * exchange a driver does around it): step k reads its state from
+ * in + k * in_stride and leaves its result in out + k * out_stride (doubles;
+ * layout of fcsg_engine_set_state_bulk / get_state_bulk; stride 0 = the same
+ * buffer every step). The copies run on two copy streams through device
+ * staging buffers, so step k+1's upload and step k-1's download overlap step
+ * k's kernels; use pinned host memory for that overlap. Returns when every
+ * result is in host memory (errors as fcsg_engine_run). */
+int fcsg_engine_run_host(fcsg_engine* eng, long n, const double* in, long in_stride, double* out, long out_stride,
+                         long* done);
 /* enqueue n supersteps on `stream`-ordered engine work without any host
  * synchronisation (benchmark path; errors surface at the next sync). */
 int fcsg_engine_enqueue(fcsg_engine* eng, long n);

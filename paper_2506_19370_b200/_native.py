@@ -96,6 +96,7 @@ def _declare(L):
     L.fcsg_engine_get_field.argtypes = [vp, C.c_int, C.c_char_p, C.c_int, dp]
     L.fcsg_engine_set_field.argtypes = [vp, C.c_int, C.c_char_p, C.c_int, dp]
     L.fcsg_engine_gradient.argtypes = [vp, C.c_int]
+    L.fcsg_engine_run_host.argtypes = [vp, C.c_long, C.c_void_p, C.c_long, C.c_void_p, C.c_long, C.POINTER(C.c_long)]
     L.fcsg_engine_set_quadrature.argtypes = [vp, C.c_int, dp]
     L.fcsg_engine_integrals.argtypes = [vp, C.c_int, dp]
     L.fcsg_engine_sample.argtypes = [vp, C.c_long, ip, ip, ip, dp, dp, dp]

@@ -485,6 +485,15 @@ int fcsg_engine_launches_per_step(fcsg_engine* e, int* n) {
 
 extern "C" {
 
+int fcsg_engine_run_host(fcsg_engine* e, long n, const double* in, long in_stride, double* out, long out_stride,
+                         long* done) {
+    if (!e || !in || !out) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        const long d = e->eng->run_host(n, in, in_stride, out, out_stride);
+        if (done) *done = d;
+    });
+}
+
 int fcsg_engine_set_state_bulk(fcsg_engine* e, const double* e4s) {
     if (!e) return FCSG_USAGE;
     return guard(e->ctx, [&] { e->eng->set_state_bulk(e4s); });

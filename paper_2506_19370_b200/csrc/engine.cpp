@@ -29,6 +29,11 @@ Engine::~Engine() {
     if (ev_fork_) dev::destroy_event(ev_fork_);
     if (ev_join_) dev::destroy_event(ev_join_);
     if (side_) dev::destroy_stream(side_);
+    for (int b = 0; b < 2; ++b)
+        for (void* e : {ev_in_ready_[b], ev_in_used_[b], ev_out_ready_[b], ev_out_done_[b]})
+            if (e) dev::destroy_event(e);
+    if (cp_in_) dev::destroy_stream(cp_in_);
+    if (cp_out_) dev::destroy_stream(cp_out_);
     for (void* e : cevents_) dev::destroy_event(e);
     for (void* st : cstreams_) dev::destroy_stream(st);
     if (ev_stage_) dev::destroy_event(ev_stage_);
@@ -1092,6 +1097,88 @@ void Engine::enqueue_steps(long n) {
         ++host_step_;
     }
     dev::check("enqueue");
+}
+
+// state <-> a bulk buffer ([4][sum of points], subpatches in id order) on the device
+void Engine::bulk_d2d(double* bulk, const double* src, bool to_state, void* stream) {
+    bool identity = true;
+    for (size_t k = 0; k < slot_of_.size(); ++k) identity = identity && slot_of_[k] == static_cast<int>(k);
+    for (int c = 0; c < 4; ++c) {
+        if (identity) {
+            if (to_state) dev::d2d(E_.e[c], src + c * npts_, npts_ * sizeof(double), stream);
+            else dev::d2d(bulk + c * npts_, E_.e[c], npts_ * sizeof(double), stream);
+            continue;
+        }
+        long pos = 0;
+        for (int id = 0; id < static_cast<int>(subs_.size()); ++id) {
+            const long sz = sub_points(id), off = off_of_slot_[slot_of_[id]];
+            if (to_state) dev::d2d(E_.e[c] + off, src + c * npts_ + pos, sz * sizeof(double), stream);
+            else dev::d2d(bulk + c * npts_ + pos, E_.e[c] + off, sz * sizeof(double), stream);
+            pos += sz;
+        }
+    }
+}
+
+long Engine::run_host(long n, const double* in, long in_stride, double* out, long out_stride) {
+    if (!finalized_) throw Error(kUsage, "engine not finalized");
+    if (n <= 0) return 0;
+    const bool finite_T = std::isfinite(cfg_.T);
+    if (!dev::is_cuda() || finite_T) {  // one step at a time (and the T check)
+        long done = 0;
+        for (; done < n; ++done) {
+            if (finite_T && time() >= cfg_.T - 1e-15) break;
+            set_state_bulk(in + done * in_stride);
+            run_steps(1, true);
+            get_state_bulk(out + done * out_stride);
+        }
+        return done;
+    }
+    const size_t bytes = 4 * static_cast<size_t>(npts_) * sizeof(double);
+    if (!cp_in_) {
+        for (int b = 0; b < 2; ++b) {
+            stage_in_[b] = static_cast<double*>(dev::alloc(bytes));
+            stage_out_[b] = static_cast<double*>(dev::alloc(bytes));
+            allocs_.push_back(stage_in_[b]);
+            allocs_.push_back(stage_out_[b]);
+            ev_in_ready_[b] = dev::create_event();
+            ev_in_used_[b] = dev::create_event();
+            ev_out_ready_[b] = dev::create_event();
+            ev_out_done_[b] = dev::create_event();
+        }
+        cp_in_ = dev::create_stream();
+        cp_out_ = dev::create_stream();
+    }
+    void* s = ctx_.stream;
+    // nothing queued on s may still use the staging buffers
+    dev::sync(s);
+    for (int b = 0; b < 2; ++b) {
+        dev::record(ev_in_used_[b], s);
+        dev::record(ev_out_done_[b], s);
+    }
+    for (long k = 0; k < n; ++k) {
+        const int b = static_cast<int>(k & 1);
+        // upload: into the staging buffer step k-2 has finished reading
+        dev::wait(cp_in_, ev_in_used_[b]);
+        dev::h2d_async(stage_in_[b], in + k * in_stride, bytes, cp_in_);
+        dev::record(ev_in_ready_[b], cp_in_);
+        // the step: state <- staging, superstep, staging <- state
+        dev::wait(s, ev_in_ready_[b]);
+        bulk_d2d(nullptr, stage_in_[b], true, s);
+        dev::record(ev_in_used_[b], s);
+        enqueue_steps(1);
+        dev::wait(s, ev_out_done_[b]);
+        bulk_d2d(stage_out_[b], nullptr, false, s);
+        dev::record(ev_out_ready_[b], s);
+        // download on the other copy engine
+        dev::wait(cp_out_, ev_out_ready_[b]);
+        dev::d2h_async(out + k * out_stride, stage_out_[b], bytes, cp_out_);
+        dev::record(ev_out_done_[b], cp_out_);
+    }
+    dev::sync(cp_in_);
+    dev::sync(s);
+    dev::sync(cp_out_);
+    check_error();
+    return n;
 }
 
 long Engine::run_steps(long n, bool use_graph) {

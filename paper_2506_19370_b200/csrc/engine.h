@@ -111,6 +111,12 @@ class Engine {
     void enqueue_step(bool step0);
     // n supersteps enqueued without host synchronisation (graph replay after step 0)
     void enqueue_steps(long n);
+    // n supersteps with host I/O per step: state <- in + k in_stride, one
+    // superstep, out + k out_stride <- state (layouts as set/get_state_bulk).
+    // Copies go through device staging buffers on two copy streams, so the
+    // upload of step k+1's input and the download of step k-1's result
+    // overlap step k's kernels; returns the steps done.
+    long run_host(long n, const double* in, long in_stride, double* out, long out_stride);
     double time();
     long steps() const { return host_step_; }
     long total_points() const { return npts_; }
@@ -200,6 +206,16 @@ class Engine {
     std::vector<void*> cstreams_, cevents_;
     void ensure_streams();
     std::vector<char> wq_set_;
+    // run_host staging: two input and two output state buffers, copy streams
+    double* stage_in_[2] = {nullptr, nullptr};
+    double* stage_out_[2] = {nullptr, nullptr};
+    void* cp_in_ = nullptr;
+    void* cp_out_ = nullptr;
+    void* ev_in_ready_[2] = {nullptr, nullptr};
+    void* ev_in_used_[2] = {nullptr, nullptr};
+    void* ev_out_ready_[2] = {nullptr, nullptr};
+    void* ev_out_done_[2] = {nullptr, nullptr};
+    void bulk_d2d(double* dst_state, const double* src_bulk, bool to_state, void* stream);
     long* d_slot_off_ = nullptr;
     double* d_quad_out_ = nullptr;
     void* ev_stage_ = nullptr;

@@ -164,6 +164,18 @@ class Engine:
         ptr = e.data_ptr() if hasattr(e, "data_ptr") else np.ascontiguousarray(e, dtype=np.float64).ctypes.data
         self.ctx.check(self.ctx.lib.fcsg_engine_set_state_bulk(self.h, C.c_void_p(ptr)))
 
+    def run_host(self, state_in, state_out, steps=1, in_stride=0, out_stride=0):
+        """steps supersteps with host I/O per step (fcsg_engine_run_host):
+        step k reads its state from state_in (+ k in_stride doubles) and
+        leaves its result in state_out (+ k out_stride); uploads/downloads
+        overlap the neighbouring steps' kernels (pinned buffers)."""
+        pi = state_in.data_ptr() if hasattr(state_in, "data_ptr") else state_in.ctypes.data
+        po = state_out.data_ptr() if hasattr(state_out, "data_ptr") else state_out.ctypes.data
+        done = C.c_long()
+        self.ctx.check(self.ctx.lib.fcsg_engine_run_host(self.h, steps, C.c_void_p(pi), in_stride, C.c_void_p(po),
+                                                         out_stride, C.byref(done)))
+        return done.value
+
     def get_state_bulk(self, out):
         ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
         self.ctx.check(self.ctx.lib.fcsg_engine_get_state_bulk(self.h, C.c_void_p(ptr)))
