@@ -2064,10 +2064,137 @@ __global__ void __launch_bounds__(kSpecThreads) classify_spectrum_kernel(const _
 }
 #endif
 
+#if FCSG_CUDA
+// The fallback classifier on the FP64 tensor cores, for 32-point windows (the
+// default) in groups without L-shaped subpatches and with lines of >= 32
+// points: as classify_mma_kernel, a warp takes the row and column windows of
+// 4 points (quad g: window g, lane t: window values t, t+4, ..., t+28); the
+// window x (8 rows of A per tile) times the 32 x 16 tail matrix (B, held in
+// registers for the whole kernel) gives, in lane t's accumulators, Re/Im of
+// tail modes t and t + 4 of its window: 16 DMMA.884 per 8 windows instead of
+// 512 multiply-adds per window. The fit's sums are reduced over the quad.
+constexpr int kSpecMmaThreads = 256;
+__global__ void __launch_bounds__(kSpecMmaThreads) classify_spectrum_mma_kernel(const __grid_constant__ EngineDev E,
+                                                                                 bool step0) {
+    constexpr int W = 32, NK = 8;
+    constexpr unsigned kAll = 0xffffffffu;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, q = g & 3;
+    const bool col = g >= 4;
+    const double* T = E.fb_tab + E.fb_off[W];
+    double bf[2][8];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) bf[nt][ks] = ldg1(T + (4 * ks + t) * 2 * NK + 8 * nt + g);
+    const double* lx = T + W * 2 * NK;
+    const double lx0 = ldg1(lx + t), lx1 = ldg1(lx + 4 + t), sx = ldg1(lx + NK), sxx = ldg1(lx + NK + 1);
+    const double n_ext = static_cast<double>(W + E.fb_ncont - 1);
+    const double ln_ext = log(n_ext);
+    const double kLogFloor = log(1e-300);
+    const long sz = static_cast<long>(E.ni) * E.nj;
+    const long ngroups = (E.npts + 3) / 4;
+    const long wstep = static_cast<long>(gridDim.x) * (kSpecMmaThreads / 32);
+    for (long grp = static_cast<long>(blockIdx.x) * (kSpecMmaThreads / 32) + (threadIdx.x >> 5); grp < ngroups;
+         grp += wstep) {
+        const long p = 4 * grp + q;
+        const bool valid = p < E.npts;
+        const unsigned pp = valid ? static_cast<unsigned>(p) : 0u;
+        const unsigned sub = fdiv(E.div_sz, pp);
+        const unsigned loc = pp - sub * E.div_sz.d;
+        const int j = static_cast<int>(fdiv(E.div_ni, loc));
+        const int i = static_cast<int>(loc) - j * E.ni;
+        const long base = static_cast<long>(sub) * sz;
+        const int n = col ? E.nj : E.ni, pos = col ? j : i;
+        int st = pos - W / 2;
+        st = st < 0 ? 0 : (st > n - W ? n - W : st);
+        const long stride = col ? E.ni : 1;
+        const long p0 = col ? base + static_cast<long>(st) * E.ni + i : base + static_cast<long>(j) * E.ni + st;
+        int cls[2] = {4, 4};
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            if (f == 1 && !step0) break;
+            const double* src = f == 0 ? E.proxy : E.e[0];
+            double v[8];
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) v[ks] = valid ? src[p0 + (4 * ks + t) * stride] : 0.0;
+            double lo = v[0], hi = v[0];
+#pragma unroll
+            for (int ks = 1; ks < 8; ++ks) {
+                lo = v[ks] < lo ? v[ks] : lo;
+                hi = hi < v[ks] ? v[ks] : hi;
+            }
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                const double l2 = __shfl_xor_sync(kAll, lo, o), h2 = __shfl_xor_sync(kAll, hi, o);
+                lo = l2 < lo ? l2 : lo;
+                hi = hi < h2 ? h2 : hi;
+            }
+            const double span = hi - lo;
+            double scale = fabs(lo);
+            scale = scale < fabs(hi) ? fabs(hi) : scale;
+            scale = scale < 1e-100 ? 1e-100 : scale;
+            const bool guard = !valid || span <= 1e-13 * scale || span <= E.abs_floor;
+            // 2 (v - lo) / span - 1 as (v - lo) (2 / span) - 1: one division per
+            // window (<= 1 ulp per value against normalize_stencil, far below
+            // the spectrum's own round-off)
+            const double r2 = 2.0 / (guard ? 1.0 : span);
+            double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const double a = guard ? 0.0 : fma(v[ks] - lo, r2, -1.0);
+                dmma(d[0][0], d[0][1], a, bf[0][ks]);
+                dmma(d[1][0], d[1][1], a, bf[1][ks]);
+            }
+            // log(|c_k| / n_ext) = 0.5 log(|c_k|^2) - log(n_ext); |c_k| = 0
+            // takes the reference's floor log(1e-300); the tail peak needs one
+            // square root (of the largest |c_k|^2 of the window)
+            const double s0 = fma(d[0][0], d[0][0], d[0][1] * d[0][1]);
+            const double s1 = fma(d[1][0], d[1][0], d[1][1] * d[1][1]);
+            const double ly0 = s0 > 0.0 ? fma(0.5, log(s0), -ln_ext) : kLogFloor;
+            const double ly1 = s1 > 0.0 ? fma(0.5, log(s1), -ln_ext) : kLogFloor;
+            double sy = ly0 + ly1, sxy = lx0 * ly0 + lx1 * ly1, smax = s0 < s1 ? s1 : s0;
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+                sy += __shfl_xor_sync(kAll, sy, o);
+                sxy += __shfl_xor_sync(kAll, sxy, o);
+                const double p2 = __shfl_xor_sync(kAll, smax, o);
+                smax = smax < p2 ? p2 : smax;
+            }
+            const double pk = sqrt(smax) / n_ext;
+            const double sd = -((NK * sxy - sx * sy) / (NK * sxx - sx * sx));
+            int c = 4;
+            if (!(pk < 2e-4)) c = sd < 1.6 ? 1 : (sd < 2.6 ? 2 : (sd < 3.6 ? 3 : 4));
+            cls[f] = guard ? 4 : c;
+        }
+        // min of the row window (quad g) and the column window (quad g + 4)
+        const int tau = min(cls[0], __shfl_xor_sync(kAll, cls[0], 16));
+        const int tr = min(cls[1], __shfl_xor_sync(kAll, cls[1], 16));
+        if (valid && !col && t == 0) {
+            E.tau[p] = tau;
+            E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
+            if (step0) E.seed[p] = (E.mask[p] != 0 && (tau <= 2 || tr <= 2)) ? 1.0 : 0.0;
+        }
+    }
+}
+#endif
+
 void launch_classify(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream) {
     if (Eall.cls_variant == 1) {  // FC-spectrum classifier
 #if FCSG_CUDA
+        static const bool scalar = [] {
+            const char* v = std::getenv("FCSG_CLASSIFIER");
+            return v && std::string(v) == "scalar";
+        }();
         for (const GroupLaunch& g : G) {
+            // tensor-core path: 32-point windows, full lines of >= 32 points
+            const bool rect = g.rows.size() == 1 && g.rows[0].desc4 == nullptr;
+            if (!scalar && rect && g.E.fb_window == 32 && g.E.ni >= 32 && g.E.nj >= 32) {
+                long n = ((g.E.npts + 3) / 4 + kSpecMmaThreads / 32 - 1) / (kSpecMmaThreads / 32);
+                n = n > 148 * 8 ? 148 * 8 : (n < 1 ? 1 : n);
+                classify_spectrum_mma_kernel<<<static_cast<int>(n), kSpecMmaThreads, 0,
+                                               static_cast<cudaStream_t>(stream)>>>(g.E, step0);
+                continue;
+            }
             long n = (g.E.npts + kSpecThreads - 1) / kSpecThreads;
             n = n > 148 * 32 ? 148 * 32 : (n < 1 ? 1 : n);
             classify_spectrum_kernel<<<static_cast<int>(n), kSpecThreads, 0, static_cast<cudaStream_t>(stream)>>>(g.E,
