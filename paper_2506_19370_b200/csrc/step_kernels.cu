@@ -1991,7 +1991,13 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     const int nlines = Pass::kRows ? E.nj : E.ni;
     // the compile-time plans assume the reference operator (n_cont 25, degree 2)
     const bool ref_op = pl.n_gap == 24 && pl.dp1 == 3;
-    const bool ct = ref_op && (pl.n_ext == 280 || pl.n_ext == 536 || pl.n_ext == 171);
+    // compile-time plans: 280 (N = 256), 536 (512), 171 (147, the config-3
+    // annulus), and the config-4 C1 patch's lengths 94 (N = 70), 102 (78),
+    // 103 (79), 163 (139); prime last radices (17, 19, 47, 67, 103, 163) on DMMA
+    auto is_ct = [](int ne) {
+        return ne == 280 || ne == 536 || ne == 171 || ne == 94 || ne == 102 || ne == 103 || ne == 163;
+    };
+    const bool ct = ref_op && is_ct(pl.n_ext);
 #if FCSG_CUDA
     constexpr int kCtLB = Pass::kLB;
 #else
@@ -2009,7 +2015,11 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     constexpr int kNT = NtOf<Pass>::v;
     if (ct && pl.n_ext == 280) launch_line_pass<Pass, 280, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else if (ct && pl.n_ext == 536) launch_line_pass<Pass, 536, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
-    else if (ct) launch_line_pass<Pass, 171, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct && pl.n_ext == 171) launch_line_pass<Pass, 171, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct && pl.n_ext == 94) launch_line_pass<Pass, 94, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct && pl.n_ext == 102) launch_line_pass<Pass, 102, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct && pl.n_ext == 103) launch_line_pass<Pass, 103, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (ct) launch_line_pass<Pass, 163, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
 #else
     (void)stream;
@@ -2018,7 +2028,11 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     for (int b = 0; b < nblk; ++b) {
         if (ct && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
         else if (ct && pl.n_ext == 536) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct) line_pass<kLB, Pass, 171, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 171) line_pass<kLB, Pass, 171, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 94) line_pass<kLB, Pass, 94, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 102) line_pass<kLB, Pass, 102, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 103) line_pass<kLB, Pass, 103, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct) line_pass<kLB, Pass, 163, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
         else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
     }
 #endif

@@ -321,3 +321,21 @@ def test_superstep_rotated_channel_general_metrics(backend, engine_golden, refo)
     for k in range(len(dec.subs)):
         assert rel_err(E.get_state(k), g[f"rc_sub{k}_e3"]) < 1e-12
         assert np.array_equal(E.get(k, "tau"), g[f"rc_sub{k}_tau3"])
+
+
+@pytest.mark.parametrize("n0,n_ext", [(52, 94), (60, 102), (61, 103), (121, 163)],
+                         ids=["n_ext94", "n_ext102", "n_ext103", "n_ext163"])
+@pytest.mark.parametrize("general", [False, True], ids=["cartesian", "general"])
+def test_superstep_small_compile_time_plans(backend, n0, n_ext, general):
+    """the compile-time plans of the config-4 corner patch's line lengths
+    (prime last radices 47, 17, 103 and 163 on the tensor cores):
+    one subpatch of (n0 + 18)^2 points, 2 supersteps against the oracle"""
+    kind, ctx = backend
+    dec, ic, _ = P.vortex_tiles(r=1, s=1, n0=n0)
+    assert dec.subs[0].ni + 24 == n_ext
+    E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5, force_general=general))
+    OE = oracle_engine(dec, ic)
+    OE.step()
+    OE.step()
+    assert E.run(2) == 2
+    _compare_engines(E, OE, 1)
