@@ -156,6 +156,13 @@ def cpu_rate(steps, warmup, threads):
     return 5.0 * npts * n / wall, wall / max(n, 1), npts
 
 
+def workload_name(n_subs_total=None):
+    """the config-5 weak-scaling workload as both arms name it"""
+    block = "" if n_subs_total is None else f" (one block of a {n_subs_total}-subpatch tiling, NCCL halo exchange)"
+    return (f"config5-weak: {R_TILES}x{S_TILES} tiles of 256x256 per GPU{block} ({R_TILES * S_TILES * 65536} "
+            f"points/GPU, 19-point overlap), vortex + 1e-3 noise, ANN classifier, CFL 0.5")
+
+
 def run_reference(args):
     world, rank, _ = dist_init()
     if rank != 0:
@@ -168,7 +175,10 @@ def run_reference(args):
     out = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": sps * 1e3, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": rate / PAPER_1NODE, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": "config5-weak (sampled)", "tiles_per_step": list(SAMPLE_TILES)},
+           "config": {"workload": workload_name(), "points_per_gpu": R_TILES * S_TILES * 256 * 256,
+                      "sampled_per_step": f"{SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} of the {R_TILES}x{S_TILES} tiles "
+                                          f"({npts} points): the CPU rate is per point, the sample bounds the "
+                                          f"run time"},
            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -472,9 +482,7 @@ def run_fcsg(args):
         "vs_baseline": value / PAPER_1NODE,
         "vs_baseline_basis": "PAPER.md:1612 (BASELINE.md): 6.74e7 pt-stage/s, one 54-core Xeon 8273 node",
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config5-weak: {R_TILES}x{S_TILES} tiles of 256x256 per GPU"
-                               f"{'' if world == 1 else ' (one block of a ' + str(len(dec.subs)) + '-subpatch tiling, NCCL halo exchange)'} "
-                               f"({npts} points/GPU, 19-point overlap), vortex + 1e-3 noise, ANN classifier, CFL 0.5",
+        "config": {"workload": workload_name(None if world == 1 else len(dec.subs)),
                    "points_per_gpu": npts, "l2": "working set ~1.7 GB/GPU >> 126 MB L2 (no flush needed)",
                    "cuda_graph": world == 1, "parallelism": f"subpatch blocks x{world}", "stage_passes": "cartesian" if E.is_cartesian() else "general"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
