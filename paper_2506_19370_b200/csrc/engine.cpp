@@ -392,6 +392,23 @@ void Engine::finalize() {
         const std::vector<double>* src[7] = {&sp.iq1x, &sp.iq2x, &sp.iq1y, &sp.iq2y, &sp.h_min, &sp.h_max, &sp.w_norm};
         for (int k = 0; k < 7; ++k) std::copy(src[k]->begin(), src[k]->end(), geo[k].begin() + off);
     }
+    // per-slot uniform metric (affine axis-aligned subpatches: iq1x and iq2y
+    // are one value over the whole point set): the Cartesian passes then read
+    // it per subpatch instead of staging it per point
+    std::vector<double> q1c(S, 0.0), q2c(S, 0.0);
+    std::vector<char> quni(S, 0);
+    for (int slot = 0; slot < S; ++slot) {
+        const auto& sp = subs_[id_of_slot_[slot]];
+        if (sp.cut_i > 0 || sp.iq1x.empty()) continue;
+        const double a = sp.iq1x[0], b = sp.iq2y[0];
+        bool u = true;
+        for (size_t q = 0; q < sp.iq1x.size() && u; ++q) u = sp.iq1x[q] == a && sp.iq2y[q] == b;
+        quni[slot] = u;
+        q1c[slot] = a;
+        q2c[slot] = b;
+    }
+    E.iq1x_c = static_cast<const double*>(up(q1c.data(), S * sizeof(double)));
+    E.iq2y_c = static_cast<const double*>(up(q2c.data(), S * sizeof(double)));
     E.h1 = static_cast<const double*>(up(h1.data(), S * sizeof(double)));
     E.h2 = static_cast<const double*>(up(h2.data(), S * sizeof(double)));
     E.cut_i = static_cast<const int*>(up(ci.data(), S * sizeof(int)));
@@ -578,6 +595,10 @@ void Engine::finalize() {
         V.seed = offp(E.seed);
         V.m01 = offp(E.m01);
         V.h1 = E.h1 + slot0;
+        V.iq1x_c = E.iq1x_c + slot0;
+        V.iq2y_c = E.iq2y_c + slot0;
+        V.uniform_q = 1;
+        for (int k = 0; k < n; ++k) V.uniform_q = V.uniform_q && quni[slot0 + k];
         V.h2 = E.h2 + slot0;
         V.cut_i = E.cut_i + slot0;
         V.cut_j = E.cut_j + slot0;

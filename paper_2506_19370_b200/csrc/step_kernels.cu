@@ -108,6 +108,7 @@ struct LineCtx {
     long base;
     int ni;
     bool rows;
+    double qy;  // the subpatch's uniform iq2y (EngineDev::uniform_q)
 };
 
 FCSG_HD long pidx(const LineCtx& c, int l, int i) {
@@ -192,6 +193,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
     c.base = static_cast<long>(c.sub) * ni * nj;
     c.ni = ni;
     c.rows = rows;
+    c.qy = E.uniform_q ? E.iq2y_c[c.sub] : 0.0;
     double2* buf = smem;
     double2* scr = smem + (NE > 0 ? NE : pl.n_ext) * pitch;
     double2* tabs = scr + scr_cap;
@@ -790,7 +792,7 @@ struct PassXc {
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         if (r & 1) return 0;
-        s[0] = E.iq1x + p;
+        s[0] = E.iq1x + p;  // (staged even when uniform: measured faster than a per-subpatch value here)
         s[1] = E.mu + p;
         return 2;
     }
@@ -872,7 +874,7 @@ struct PassYc {
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
         if (!(r & 1)) {
-            s[0] = E.iq2y + p;
+            s[0] = E.uniform_q ? nullptr : E.iq2y + p;  // uniform: read per subpatch in store
             s[1] = E.mu + p;
             return 2;
         }
@@ -882,8 +884,9 @@ struct PassYc {
         s[2] = E.tA[c0 + 1] + p;
         return 3;
     }
-    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double* fv) const {
-        const double d = st[0];
+    FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx& c,
+                          const double* fv) const {
+        const double d = E.uniform_q ? c.qy : st[0];
         if (!(r & 1)) {
             const double m = st[ss];
             return mk2(m * (d * v.x), m * (d * v.y));  // s5 = mu (0 D1 w + iq2y D2 w)

@@ -74,6 +74,9 @@ struct EngineDev {
     int smear_radius;
     // per subpatch
     const double* h1;        // S: lattice spacing along q1 (LineInfo::inv_len = 1/((n-1) h1))
+    const double* iq1x_c;    // S: iq1x / iq2y of subpatches where each is one value (uniform_q)
+    const double* iq2y_c;
+    int uniform_q;           // every subpatch of this view has uniform iq1x and iq2y
     const double* h2;
     const int* cut_i;        // S: L-shaped subpatch: points (i < cut_i && j < cut_j) are not
     const int* cut_j;        //    in the set (local, 0 = rectangular; geom::Subpatch::valid)
