@@ -49,12 +49,16 @@ def peaks():
 
 # kernel behind each timed group (for the ncu capture lookup)
 GROUP_KERNEL = {"pass_a": "PassXc", "pass_b": "PassYc", "viscosity": "classify_mma_kernel"}
+GROUP_LB = {"pass_a": 2, "pass_b": 4}  # lines per block of the captured pass (256-point lines)
 
 
-def ncu_traffic(group):
-    """DRAM bytes (read + write) per launch of the group's kernel from the
-    newest committed `ncu --set full` capture of the bench workload
-    (profiles/rNN_top_kernels_raw.csv, scripts/prof_top.sh), or None."""
+def ncu_traffic(group, npts):
+    """DRAM bytes (read + write) of the group's kernel over npts points, from
+    the newest committed `ncu --set full` capture of the bench workload
+    (profiles/rNN_top_kernels_raw.csv, scripts/prof_top.sh), or None. The
+    captured launch may cover part of the points (the RK-stage passes launch
+    per half group): its bytes are scaled by npts over the points it covered
+    (grid x lines per block x 256)."""
     import csv
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_top_kernels_raw.csv")))
@@ -65,6 +69,10 @@ def ncu_traffic(group):
         for row in csv.DictReader(fh):
             if key in row["Kernel Name"]:
                 mb = float(row["dram__bytes_read.sum [MB]"]) + float(row["dram__bytes_write.sum [MB]"])
+                lb = GROUP_LB.get(group)
+                if lb:
+                    covered = float(row["launch__grid_size"]) * lb * 256
+                    mb *= npts / covered
                 return mb * 1e6, os.path.basename(files[-1])
     return None, None
 
@@ -454,7 +462,7 @@ def run_fcsg(args):
     ALG_BYTES = ALG_BYTES_CART if E.is_cartesian() else ALG_BYTES_GEN
     alg = ALG_BYTES.get(dom, 64) * npts
     achieved = alg / (groups[dom] * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic(dom) if world == 1 else (None, None)
+    traffic, traffic_src = ncu_traffic(dom, npts) if world == 1 else (None, None)
     fc_gbs, fc_ms = fc_derivative_gbs(ctx)
     fc4_gbs, fc4_ms = fc_derivative_gbs(ctx, n_cont=27, degree=4)
     cfg2 = config2_rate(ctx) if world == 1 else None
