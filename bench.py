@@ -369,9 +369,10 @@ def config4_rate(ctx, steps=20):
     ms = a.elapsed_time(b) / steps
     npts = E.total_points()
     E.close()
-    return {"config": "config4: Mach 3 forward-facing step in [0,3]x[0,1] (step 0.2 high at x = 0.6); C1 corner "
-                      "patch at the step top (L-shaped subpatches), S patches along the step top and face, 2 "
-                      "Cartesian I patches of 256x256 subpatches; inflow rho 1.4, p 1, u 3; CFL 0.5",
+    return {"config": "config4: Mach 3 forward-facing step in [0,3]x[0,1] (step 0.2 high at x = 0.6); convex C1 "
+                      "corner patch at the step top (L-shaped subpatches), concave C2 corner patch at its foot, an "
+                      "S patch along the step top, 2 Cartesian I patches of 256x256 subpatches; inflow rho 1.4, "
+                      "p 1, u 3; CFL 0.5",
             "points": npts, "subpatches": len(dec.subs), "build_s": build_s, "ms_per_step": ms,
             "value": 5.0 * npts / (ms * 1e-3), "unit": UNIT}
 

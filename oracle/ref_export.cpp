@@ -464,8 +464,10 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
                  {interior, SideInfo{true, "out"}, interior, SideInfo{true, "wall"}});
             rect(PatchKind::S, {0.6, 0.2}, {2.4, 0.0}, {0.0, 0.25},
                  {interior, SideInfo{true, "out"}, SideInfo{true, "wall"}, interior});
-            rect(PatchKind::S, {0.3, 0.0}, {0.3, 0.0}, {0.0, 0.2},
-                 {interior, SideInfo{true, "wall"}, SideInfo{true, "wall"}, interior});
+            // concave corner at the step's foot: C2 between the floor and the face
+            dec.patches.push_back(geom::build_c2_patch(std::make_shared<geom::Segment>(Vec2{0.3, 0.0}, Vec2{0.6, 0.0}),
+                                                       std::make_shared<geom::Segment>(Vec2{0.6, 0.2}, Vec2{0.6, 0.0}),
+                                                       Vec2{0.6, 0.0}, "wall"));
             bcs["in"].state = euler::conservative(1.4, 3.0, 0.0, 1.0);
             free_stream = true;
         } else {

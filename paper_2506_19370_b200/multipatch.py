@@ -422,10 +422,57 @@ def subdivide_L(p: Patch, r: int, n1: int, nv: int):
                 add_cell(a, b)
 
 
-def build_c1_patch(ellA: Segment, ellB: Segment, corner, wall_tag="wall"):
-    """src/geometry.cpp:351-369 (without its Jacobian sign sweep)"""
-    return Patch(C1, CurveSumMap(ellA, ellB, corner), [SideInfo() for _ in range(4)],
-                 wall_q1=SideInfo(True, wall_tag), wall_q2=SideInfo(True, wall_tag))
+def _det_sign_sweep(p: Patch, n_samples: int = 100):
+    """src/geometry.cpp:334-347: the mapping's Jacobian keeps one sign"""
+    sign = 0
+    for a in range(n_samples + 1):
+        for b in range(n_samples + 1):
+            q1, q2 = a / n_samples, b / n_samples
+            if p.kind == C1 and q1 < 0.5 and q2 < 0.5:
+                continue
+            J = p.map.jacobian(q1, q2)
+            d = J[0] * J[3] - J[1] * J[2]
+            if abs(d) < 1e-14:
+                raise GeometryError("mapping Jacobian vanishes")
+            sg = 1 if d > 0 else -1
+            if sign == 0:
+                sign = sg
+            if sg != sign:
+                raise GeometryError("mapping Jacobian changes sign")
+
+
+def _corner_checks(ellA, ellB, corner, t, who):
+    pa0, pa1 = ellA.point(0.0), ellA.point(1.0)
+    scale = max(1e-12, _hypot(pa0[0] - pa1[0], pa0[1] - pa1[1]))
+    for c in (ellA, ellB):
+        q = c.point(t)
+        if _hypot(q[0] - corner[0], q[1] - corner[1]) > 1e-8 * scale:
+            where = "pass through the corner at t=1/2" if t == 0.5 else "end at the corner (t=1)"
+            raise GeometryError(f"{who}: curves must {where}")
+    ta, tb = ellA.derivative(t), ellB.derivative(t)
+    if abs(ta[0] * tb[1] - ta[1] * tb[0]) < 1e-12 * _hypot(*ta) * _hypot(*tb):
+        raise GeometryError(f"{who}: tangents at the corner are parallel")
+
+
+def build_c1_patch(ellA, ellB, corner, wall_tag="wall"):
+    """src/geometry.cpp:351-369: convex-corner patch l_A(q1) + l_B(q2) - C,
+    the curves crossing at the corner at t = 1/2; L-shaped point set"""
+    _corner_checks(ellA, ellB, corner, 0.5, "build_c1_patch")
+    p = Patch(C1, CurveSumMap(ellA, ellB, corner), [SideInfo() for _ in range(4)],
+              wall_q1=SideInfo(True, wall_tag), wall_q2=SideInfo(True, wall_tag))
+    _det_sign_sweep(p)
+    return p
+
+
+def build_c2_patch(ellA, ellB, corner, wall_tag="wall"):
+    """src/geometry.cpp:371-389: concave-corner patch l_A(q1) + l_B(q2) - C,
+    both curves ending at the corner (t = 1): E (= l_B) and N (= l_A) are
+    walls, W and S interior"""
+    _corner_checks(ellA, ellB, corner, 1.0, "build_c2_patch")
+    p = Patch(C2, CurveSumMap(ellA, ellB, corner),
+              [SideInfo(), SideInfo(True, wall_tag), SideInfo(), SideInfo(True, wall_tag)])
+    _det_sign_sweep(p)
+    return p
 
 
 def classify_end(p: Patch, sp: Subpatch, axis: int, line: int, high: bool):

@@ -220,10 +220,11 @@ def step_flow(scale=1):
     """BASELINE config 4: Mach 3 flow over a forward-facing step in
     [0, 3] x [0, 1] (step of height 0.2 at x = 0.6). The reference's own
     corner-patch problems fail their overlap checks, so
-    the layout is ours: a C1 corner patch at the step's top (0.6, 0.2) (arms
-    of 0.15 along the step top and face: one L-shaped subpatch at scale 1),
-    S patches along the step top and the step face (the latter with the foot
-    corner, an axis-aligned 90-degree corner), and two Cartesian I patches;
+    the layout is ours: a convex-corner C1 patch at the step's top (0.6, 0.2)
+    (arms of 0.15 along the step top and face: one L-shaped subpatch at scale
+    1), an S patch along the step top, a concave-corner C2 patch at the
+    step's foot (0.6, 0) between the floor and the face, and two Cartesian I
+    patches;
     inflow rho = 1.4, p = 1, u = 3 on the left, supersonic outflow on the
     right, slip walls. The I and S patches are split into 256 x 256
     subpatches (as config 5); scale k multiplies the cells per patch side
@@ -239,8 +240,10 @@ def step_flow(scale=1):
                   [SI(), SI(True, "out"), SI(), SI(True, "wall")])
     s_top = M.Patch(M.S, M.AffineMap((0.6, 0.2), (2.4, 0.0), (0.0, 0.25)),
                     [SI(), SI(True, "out"), SI(True, "wall"), SI()])
-    s_face = M.Patch(M.S, M.AffineMap((0.3, 0.0), (0.3, 0.0), (0.0, 0.2)),
-                     [SI(), SI(True, "wall"), SI(True, "wall"), SI()])
+    # concave corner at the step's foot (0.6, 0): a C2 patch between the
+    # floor and the step face, both ending at the corner (walls on E and N)
+    s_face = M.build_c2_patch(M.Segment((0.3, 0.0), (0.6, 0.0)), M.Segment((0.6, 0.2), (0.6, 0.0)), (0.6, 0.0),
+                              "wall")
     patches = [c1, left, top, s_top, s_face]
     for k, p in enumerate(patches):
         p.index = k

@@ -59,12 +59,13 @@ def test_read_reference_mesh_rebuilds_decomposition(which, tmp_path):
 
 
 def test_config4_layout_mesh_equals_reference():
-    """the forward-facing-step layout (problems.step_flow: C1 corner, S and I
-    patches of 256 x 256 subpatches) as a mesh file equals the reference's"""
+    """the forward-facing-step layout (problems.step_flow: convex C1 corner at
+    the step top, concave C2 corner at its foot, S and I patches of 256 x 256
+    subpatches) as a mesh file equals the reference's"""
     R = ref.RefEngine.testgeom(5, 0, weight_path="")
     j = R.mesh_json()
     patches, meta = M.mesh_from_json(j)
-    assert [p.kind for p in patches] == ["C1", "I", "I", "S", "S"]
+    assert [p.kind for p in patches] == ["C1", "I", "I", "S", "C2"]
     assert M.mesh_to_json(patches, **meta) == j
     assert sum(len(p.subpatches) for p in patches) == R.nsubs
 
@@ -73,9 +74,10 @@ def test_arc_curves_and_bilinear_round_trip():
     """a C1 patch between two circular arcs and a bilinear patch: keys the
     test geometries do not use, read back by the reference unchanged"""
     SI = M.SideInfo
-    A = M.CircularArc((0.0, 0.0), 1.0, 0.25 * math.pi, -0.25 * math.pi)
-    B = M.CircularArc((1.0, 1.0), 0.7, 1.2 * math.pi, 1.6 * math.pi)
-    c1 = M.build_c1_patch(A, B, (0.7, 0.1), "hull")
+    # two arcs crossing at (1, 0) at t = 1/2 with perpendicular tangents
+    A = M.CircularArc((0.0, 0.0), 1.0, math.pi / 6, -math.pi / 6)
+    B = M.CircularArc((1.0, 1.0), 1.0, 1.5 * math.pi - math.pi / 6, 1.5 * math.pi + math.pi / 6)
+    c1 = M.build_c1_patch(A, B, (1.0, 0.0), "hull")
     c1.sides = [SI(True, "far") for _ in range(4)]
     c1.index = 0
     M.subdivide_L(c1, 2, 21, NV)
@@ -91,7 +93,20 @@ def test_arc_curves_and_bilinear_round_trip():
     x, y = back[0].map(0.3, 0.6)
     ax, ay = A.point(0.3)
     bx, by = B.point(0.6)
-    assert (x, y) == ((ax + bx) - 0.7, (ay + by) - 0.1)
+    assert (x, y) == ((ax + bx) - 1.0, (ay + by) - 0.0)
+
+
+def test_corner_patch_checks():
+    """build_c1_patch / build_c2_patch input checks (src/geometry.cpp:351-389)"""
+    seg = M.Segment
+    c2 = M.build_c2_patch(seg((0.3, 0.0), (0.6, 0.0)), seg((0.6, 0.2), (0.6, 0.0)), (0.6, 0.0), "wall")
+    assert c2.kind == "C2" and [sd.on_gamma for sd in c2.sides] == [False, True, False, True]
+    with pytest.raises(M.GeometryError, match="end at the corner"):
+        M.build_c2_patch(seg((0.3, 0.0), (0.6, 0.0)), seg((0.6, 0.0), (0.6, 0.2)), (0.6, 0.0))
+    with pytest.raises(M.GeometryError, match="parallel"):
+        M.build_c2_patch(seg((0.3, 0.0), (0.6, 0.0)), seg((0.9, 0.0), (0.6, 0.0)), (0.6, 0.0))
+    with pytest.raises(M.GeometryError, match="t=1/2"):
+        M.build_c1_patch(seg((0.0, 0.0), (1.0, 0.0)), seg((0.5, -0.5), (0.5, 0.5)), (0.4, 0.0))
 
 
 def test_mesh_errors_match_reference():

@@ -224,9 +224,10 @@ def test_config3_cylinder_against_reference(gpu_ctx, full):
 
 @pytest.mark.gpu
 def test_config4_step_against_reference(gpu_ctx):
-    """BASELINE config 4's layout (problems.step_flow(1): C1 corner patch with
-    an L-shaped subpatch at the step's top, S and I patches of 256 x 256
-    subpatches; 0.80M points): the reference builds the same patches
+    """BASELINE config 4's layout (problems.step_flow(1): convex C1 corner
+    patch with an L-shaped subpatch at the step's top, concave C2 corner patch
+    at its foot, S and I patches of 256 x 256 subpatches; 0.80M points): the
+    reference builds the same patches
     (ref_engine_testgeom 5, its overlap checks including the S-C1 corner rule
     pass), the builder reproduces its init (up to viscosity stencils tied to
     round-off), and the engine tracks its run for 2 supersteps of Mach 3
@@ -248,7 +249,9 @@ def test_config4_step_against_reference(gpu_ctx):
         a, b = getattr(dec.plan, nm), getattr(RD.plan, nm)
         same = (a["si0"] == b["si0"]) & (a["sj0"] == b["sj0"])
         ties += int((~same).sum())
-        assert (~same).sum() <= max(1, len(same) // 1000), nm  # donor stencils tied to round-off
+        # donor stencils tied to round-off: recipients on the donor's lattice
+        # lines, located through the corner patches' Newton inversion
+        assert (~same).sum() <= max(1, len(same) // 200), nm
     E = EN.Engine(gpu_ctx, dec, ic, EN.EngineConfig(cfl=meta["cfl"]))
     for k in range(R.nsubs):  # after apply_ic's BCs (slip-wall normals from the metrics)
         assert rel_err(E.get_state(k), R.get_state(k)) < 1e-12
