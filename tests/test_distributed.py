@@ -38,7 +38,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir, steps):
+def _worker(rank, world, port, out_dir, steps, classifier="ann"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -50,7 +50,7 @@ def _worker(rank, world, port, out_dir, steps):
     dec, ic, _ = P.vortex_tiles(r=4, s=2, n0=30)
     owner = D.partition_tiles(dec, world)
     rp = D.split_plan(dec, owner, rank, world)
-    DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5))
+    DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5, classifier=classifier))
     DE.run(steps)
     for l, g in enumerate(rp.local):
         np.save(os.path.join(out_dir, f"sub{g}.npy"), DE.E.get_state(l))
@@ -60,16 +60,18 @@ def _worker(rank, world, port, out_dir, steps):
     dist.destroy_process_group()
 
 
-def test_two_ranks_bitwise_equal_single_rank(tmp_path, emu_ctx):
+@pytest.mark.parametrize("classifier", ["ann", "fallback"])
+def test_two_ranks_bitwise_equal_single_rank(tmp_path, emu_ctx, classifier):
     """The same 4x2 tiling stepped by 2 gloo ranks (2x2 subpatches each) and
-    by one rank: identical states after 2 supersteps (bitwise), identical t."""
+    by one rank: identical states after 2 supersteps (bitwise), identical t;
+    with either classifier variant."""
     from paper_2506_19370_b200 import engine as EN
 
     steps = 2
-    mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), steps), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), steps, classifier), nprocs=2, join=True,
                        start_method="spawn")
     dec, ic, _ = P.vortex_tiles(r=4, s=2, n0=30)
-    E = EN.Engine(emu_ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+    E = EN.Engine(emu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, classifier=classifier))
     E.run(steps)
     for g in range(len(dec.subs)):
         assert np.array_equal(np.load(tmp_path / f"sub{g}.npy"), E.get_state(g)), g
