@@ -2238,7 +2238,7 @@ void launch_classify(const EngineDev& Eall, const std::vector<GroupLaunch>& G, b
             classify_kernel<<<static_cast<int>(n), kClsThreads, 0, s>>>(E, step0);
         } else {
             long n = ((E.npts + 3) / 4 + kMmaThreads / 32 - 1) / (kMmaThreads / 32);
-            n = n > 148 * 8 ? 148 * 8 : n;
+            n = n > 148 * 16 ? 148 * 16 : n;  // 4 waves of 4 x 148: -2% against 2 (tail)
             classify_mma_kernel<<<static_cast<int>(n < 1 ? 1 : n), kMmaThreads, 0, s>>>(E, step0);
         }
     }
