@@ -467,7 +467,7 @@ def run_fcsg(args):
     host_in = torch.empty((4, npts), dtype=torch.float64, pin_memory=True)
     host_out = torch.empty((4, npts), dtype=torch.float64, pin_memory=True)
     E.get_state_bulk(host_in)
-    e2e_steps = max(2, min(2 * args.steps, 20))
+    e2e_steps = max(2, min(4 * args.steps, 40))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
