@@ -136,6 +136,10 @@ def raster_plan(patches, subs, nf: int, nx: int, ny: int) -> RasterPlan:
     fu = np.zeros(n)
     fv = np.zeros(n)
     todo = np.ones(n, bool)
+    sub_i0 = np.array([d.sp.i0 for d in subs], dtype=np.int64)
+    sub_j0 = np.array([d.sp.j0 for d in subs], dtype=np.int64)
+    sub_ni = np.array([d.ni for d in subs], dtype=np.int64)
+    sub_nj = np.array([d.nj for d in subs], dtype=np.int64)
     for p in patches:
         idx = np.nonzero(todo)[0]
         if idx.size == 0:
@@ -169,17 +173,15 @@ def raster_plan(patches, subs, nf: int, nx: int, ny: int) -> RasterPlan:
             bu = np.where(better, u, bu)
             bv = np.where(better, v, bv)
         hit = best >= 0
-        for k in np.nonzero(hit)[0]:
-            g = int(best[k])
-            d = subs[g]
-            sp = d.sp
-            i0l = min(max(int(math.floor(bu[k])) - sp.i0, 0), d.ni - 2)
-            j0l = min(max(int(math.floor(bv[k])) - sp.j0, 0), d.nj - 2)
-            q = idx[k]
-            sub[q], il[q], jl[q] = g, i0l, j0l
-            fu[q] = min(max(bu[k] - sp.i0 - i0l, 0.0), 1.0)
-            fv[q] = min(max(bv[k] - sp.j0 - j0l, 0.0), 1.0)
-        todo[idx[hit]] = False
+        g = best[hit]
+        i0, j0 = sub_i0[g], sub_j0[g]
+        i0l = np.minimum(np.maximum(np.floor(bu[hit]).astype(np.int64) - i0, 0), sub_ni[g] - 2)
+        j0l = np.minimum(np.maximum(np.floor(bv[hit]).astype(np.int64) - j0, 0), sub_nj[g] - 2)
+        q = idx[hit]
+        sub[q], il[q], jl[q] = g, i0l, j0l
+        fu[q] = np.minimum(np.maximum(bu[hit] - i0 - i0l, 0.0), 1.0)
+        fv[q] = np.minimum(np.maximum(bv[hit] - j0 - j0l, 0.0), 1.0)
+        todo[q] = False
     return RasterPlan(r, sub, il, jl, fu, fv)
 
 
