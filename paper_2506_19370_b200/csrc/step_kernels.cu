@@ -437,8 +437,7 @@ struct PassB {
 // written in the same stage, so they take the read-only path. At stage 0 the
 // register e0 equals e (phase 2 copies e into e0 after the BCs,
 // src/runtime.cpp:422), so it is written here instead of in phase 2.
-FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double u, double r) {
-    const double dt = E.sc->dt;  // device-resident step size (finalize_dt_kernel)
+FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double u, double r, double dt) {
     if (E.rhs[0]) E.rhs[c][p] = r;
     double* e = E.e[c];
     switch (stage) {
@@ -471,12 +470,12 @@ FCSG_HD void ssprk_update(const EngineDev& E, int stage, int c, long p, double u
 
 // ssprk_update with the register e0 already read (stages 1-3; other stages
 // read what they need themselves)
-FCSG_HD void ssprk_update_e0(const EngineDev& E, int stage, int c, long p, double u, double r, double e0v) {
+FCSG_HD void ssprk_update_e0(const EngineDev& E, int stage, int c, long p, double u, double r, double e0v,
+                             double dt) {
     if (stage < 1 || stage > 3) {
-        ssprk_update(E, stage, c, p, u, r);
+        ssprk_update(E, stage, c, p, u, r, dt);
         return;
     }
-    const double dt = E.sc->dt;
     if (E.rhs[0]) E.rhs[c][p] = r;
     double* e = E.e[c];
     if (stage == 1) {
@@ -504,7 +503,8 @@ struct PassC {
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
-    FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s) {}
+    double dt;  // the step size (finalize_dt_kernel), read once per block
+    FCSG_HD PassC(const EngineDev& e, int s) : E(e), stage(s), dt(e.sc->dt) {}
     FCSG_HD int mode(int) const { return 1; }
     static constexpr int kFetch = 2;
     FCSG_HD void fetch(int r, long p, double* v) const {
@@ -522,7 +522,7 @@ struct PassC {
         return 4;
     }
     FCSG_HD double2 store(int c, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
-        ssprk_update(E, stage, c, p, st[3 * ss], st[0] + (st[ss] * v.x + st[2 * ss] * v.y));
+        ssprk_update(E, stage, c, p, st[3 * ss], st[0] + (st[ss] * v.x + st[2 * ss] * v.y), dt);
         return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
@@ -717,7 +717,8 @@ struct PassCc {
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
-    FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s) {}
+    double dt;  // the step size (finalize_dt_kernel), read once per block
+    FCSG_HD PassCc(const EngineDev& e, int s) : E(e), stage(s), dt(e.sc->dt) {}
     FCSG_HD int mode(int) const { return 1; }
     static constexpr int kFetch = 2;
     FCSG_HD void fetch(int r, long p, double* v) const {
@@ -737,8 +738,8 @@ struct PassCc {
     }
     FCSG_HD double2 store(int r, long p, double2 v, const double* st, int ss, const LineCtx&, const double*) const {
         const double a = st[2 * ss];
-        ssprk_update(E, stage, 2 * r, p, st[3 * ss], st[0] + a * v.x);
-        ssprk_update(E, stage, 2 * r + 1, p, st[4 * ss], st[ss] + a * v.y);
+        ssprk_update(E, stage, 2 * r, p, st[3 * ss], st[0] + a * v.x, dt);
+        ssprk_update(E, stage, 2 * r + 1, p, st[4 * ss], st[ss] + a * v.y, dt);
         return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
@@ -828,7 +829,8 @@ struct PassYc {
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
-    FCSG_HD PassYc(const EngineDev& e, int s) : E(e), stage(s) {}
+    double dt;  // the step size (finalize_dt_kernel), read once per block
+    FCSG_HD PassYc(const EngineDev& e, int s) : E(e), stage(s), dt(e.sc->dt) {}
     FCSG_HD int mode(int) const { return 1; }
     // fetch: the load's values in v[0..3] (rounds 0, 1) or v[0..1] (rounds 2,
     // 3); in rounds 2 and 4 (after the last transform) also the register e0
@@ -892,8 +894,8 @@ struct PassYc {
             return mk2(m * (d * v.x), m * (d * v.y));  // s5 = mu (0 D1 w + iq2y D2 w)
         }
         const int c0 = r == 1 ? 2 : 0;
-        ssprk_update_e0(E, stage, c0, p, st[3 * ss], st[ss] + d * v.x, fv[2]);
-        ssprk_update_e0(E, stage, c0 + 1, p, st[4 * ss], st[2 * ss] + d * v.y, fv[3]);
+        ssprk_update_e0(E, stage, c0, p, st[3 * ss], st[ss] + d * v.x, fv[2], dt);
+        ssprk_update_e0(E, stage, c0 + 1, p, st[4 * ss], st[2 * ss] + d * v.y, fv[3], dt);
         return {};
     }
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
