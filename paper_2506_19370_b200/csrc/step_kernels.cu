@@ -313,9 +313,9 @@ FCSG_HD double2 flux_pair(const Prim& q, int c) {
 
 // interior positivity diagnostic of euler_rhs (src/euler.cpp:37-39)
 FCSG_HD void check_positive(const EngineDev& E, const Prim& q, long p, const LineCtx& c) {
-    if (E.mask[p] != 1) return;
     const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
-    if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) {
+    // the mask (interior points only) is read only for a failing point
+    if ((!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) && E.mask[p] == 1) {
         const long loc = p - c.base;
         raise_error(E.sc, 1, E.sub_base + c.sub, static_cast<int>(loc % c.ni), static_cast<int>(loc / c.ni));
     }
