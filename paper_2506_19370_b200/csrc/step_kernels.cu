@@ -838,8 +838,13 @@ struct PassYc {
     static constexpr int kFetch = 4;
     static constexpr bool kFetchAtEnd = true;
     FCSG_HD void fetch(int r, long p, double* v) const {
-        if (r < 2) {  // e is still unmodified in rounds 0 and 1
+        if (r == 0) {
             fetch_e(E, p, v);
+            return;
+        }
+        if (r == 1) {  // rho v and E come from the round-0 stash (e is unmodified until round 2)
+            v[0] = ldg1(E.e[0] + p);
+            v[1] = ldg1(E.e[1] + p);
             return;
         }
         if (r < 4) {  // rho, rho u: updated only in the last round
@@ -861,7 +866,8 @@ struct PassYc {
                 return mk2(q.my, q.theta);
             }
             case 1: {
-                const Prim q = prim_of(fv);
+                const double f4[4] = {fv[0], fv[1], st[3 * ss], st[4 * ss]};
+                const Prim q = prim_of(f4);
                 return mk2(carry.x - flux_pair(q, 2).y, carry.y - flux_pair(q, 3).y);
             }
             case 2: return mk2(fv[0], fv[1]);
