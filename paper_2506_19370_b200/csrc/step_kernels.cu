@@ -847,9 +847,9 @@ struct PassYc {
             v[1] = ldg1(E.e[1] + p);
             return;
         }
-        if (r < 4) {  // rho, rho u: updated only in the last round
+        if (r < 4) {  // rho (and in round 2 rho u): updated only in the last round
             v[0] = ldg1(E.e[0] + p);
-            v[1] = ldg1(E.e[1] + p);
+            if (r == 2) v[1] = ldg1(E.e[1] + p);  // round 3 takes rho u from the stash
         }
         if (!(r & 1) && stage >= 1 && stage <= 3) {
             const int c0 = r == 2 ? 2 : 0;
@@ -870,9 +870,11 @@ struct PassYc {
                 const Prim q = prim_of(f4);
                 return mk2(carry.x - flux_pair(q, 2).y, carry.y - flux_pair(q, 3).y);
             }
-            case 2: return mk2(fv[0], fv[1]);
+            case 2:
+                st[4 * ss] = fv[1];  // rho u for round 3 (slot 4's E was last read by store(1))
+                return mk2(fv[0], fv[1]);
             default: {
-                const double rho = fv[0], mx = fv[1], my = st[3 * ss];
+                const double rho = fv[0], mx = st[4 * ss], my = st[3 * ss];
                 st[3 * ss] = rho;  // u of the last update
                 st[4 * ss] = mx;
                 const double v = my / rho;
