@@ -792,7 +792,8 @@ struct PassXc {
         return mk2(q.my, q.theta);
     }
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
-        if (r & 1) return 0;
+        // iq1x and mu once, in round 0: the slots keep them for every later round
+        if (r != 0) return 0;
         s[0] = E.iq1x + p;  // (staged even when uniform: measured faster than a per-subpatch value here)
         s[1] = E.mu + p;
         return 2;
