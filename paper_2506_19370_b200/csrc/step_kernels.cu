@@ -883,15 +883,20 @@ struct PassYc {
             }
         }
     }
+    // slots: 0 iq2y, 1 mu (even rounds) / tA pair in 1, 2 (odd rounds); with a
+    // uniform iq2y (read per subpatch) the tA pair goes to 0, 2 instead, so mu
+    // staged in round 0 stays in slot 1 for round 2
     FCSG_HD int stage_srcs(int r, long p, const double** s) const {
+        const bool u = E.uniform_q;
         if (!(r & 1)) {
-            s[0] = E.uniform_q ? nullptr : E.iq2y + p;  // uniform: read per subpatch in store
+            if (u && r == 2) return 0;
+            s[0] = u ? nullptr : E.iq2y + p;
             s[1] = E.mu + p;
             return 2;
         }
         const int c0 = r == 1 ? 2 : 0;
-        s[0] = nullptr;  // keep iq2y
-        s[1] = E.tA[c0] + p;
+        s[0] = u ? E.tA[c0] + p : nullptr;  // not uniform: keep iq2y
+        s[1] = u ? nullptr : E.tA[c0] + p;  // uniform: keep mu
         s[2] = E.tA[c0 + 1] + p;
         return 3;
     }
@@ -903,7 +908,8 @@ struct PassYc {
             return mk2(m * (d * v.x), m * (d * v.y));  // s5 = mu (0 D1 w + iq2y D2 w)
         }
         const int c0 = r == 1 ? 2 : 0;
-        ssprk_update_e0(E, stage, c0, p, st[3 * ss], st[ss] + d * v.x, fv[2], dt);
+        const double ta = E.uniform_q ? st[0] : st[ss];
+        ssprk_update_e0(E, stage, c0, p, st[3 * ss], ta + d * v.x, fv[2], dt);
         ssprk_update_e0(E, stage, c0 + 1, p, st[4 * ss], st[2 * ss] + d * v.y, fv[3], dt);
         return {};
     }
