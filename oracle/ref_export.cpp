@@ -347,6 +347,8 @@ void* ref_engine_problem(const char* name, double target_h, double cfl, double T
  *      corner patch at the step's top (0.6, 0.2) (one L-shaped subpatch),
  *      S patches along the step top and face, two I patches (256 x 256
  *      subpatches); Mach 3 inflow, supersonic outflow, slip walls (n0 ignored)
+ *   6  the same at scale 2 (problems.step_flow(2): 3.22M points, the C1
+ *      patch's L-shaped subpatch 139 x 139 with rows of 139 and 70 points)
  *   4  the same at full size (problems.cylinder_flow(full=True): annulus
  *      subdivide_Q(16, 1, 129, 9), Cartesian n0 = 238; 2.57M points)
  *   2  a C1 corner patch alone (CurveSumMap of two non-orthogonal segments,
@@ -444,7 +446,7 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             rect({-1.7, -6.0}, {3.4, 0.0}, {0.0, 4.8}, {interior, interior, SideInfo{true, "wall"}, interior});
             bcs["in"].state = euler::conservative(1.4, 3.0, 0.0, 1.0);
             free_stream = true;
-        } else if (which == 5) {
+        } else if (which == 5 || which == 6) {
             const Vec2 c{0.6, 0.2};
             const double a = 0.15;
             auto ellA = std::make_shared<geom::Segment>(Vec2{c.x + a, c.y}, Vec2{c.x - a, c.y});
@@ -474,13 +476,14 @@ void* ref_engine_testgeom(int which, int n0, int nv, double cfl, int workers, co
             throw UsageError("unknown test geometry");
         }
         for (size_t k = 0; k < dec.patches.size(); ++k) dec.patches[k].index = static_cast<int>(k);
-        if (which == 5) {
+        if (which == 5 || which == 6) {
+            const int k = which == 5 ? 1 : 2;  // problems.step_flow(k)
             const int rs[5][2] = {{2, 0}, {1, 2}, {5, 1}, {4, 1}, {1, 1}};
             for (auto& p : dec.patches) {
                 if (p.kind == PatchKind::C1)
-                    geom::subdivide_L(p, 2, 59, nv);
+                    geom::subdivide_L(p, 2 * k, 59, nv);
                 else
-                    geom::subdivide_Q(p, rs[p.index][0], rs[p.index][1], 238, nv);
+                    geom::subdivide_Q(p, k * rs[p.index][0], k * rs[p.index][1], 238, nv);
             }
         } else if (which == 3 || which == 4) {
             const bool full = which == 4;

@@ -58,6 +58,9 @@ template <class F>
 int guard(Ctx* c, F&& f) {
     if (!c) return FCSG_USAGE;
     try {
+        // every entry runs on the context's device, whatever the calling
+        // thread's current device is (contexts on several devices in one process)
+        dev::set_device(c->device);
         f();
         return FCSG_OK;
     } catch (const StateError& e) {

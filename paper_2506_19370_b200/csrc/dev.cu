@@ -19,6 +19,13 @@ void ck(cudaError_t e, const char* what) {
 
 bool is_cuda() { return true; }
 void set_device(int device) { ck(cudaSetDevice(device), "cudaSetDevice"); }
+bool first_on_device(unsigned long long* flag) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    const unsigned long long old = __atomic_fetch_or(flag, bit, __ATOMIC_ACQ_REL);
+    return (old & bit) == 0;
+}
 void* create_stream() {
     cudaStream_t s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -108,6 +115,10 @@ double time_on_stream(void* stream, void (*fn)(void*), void* arg) {
 
 bool is_cuda() { return false; }
 void set_device(int) {}
+bool first_on_device(unsigned long long* flag) {
+    const unsigned long long old = __atomic_fetch_or(flag, 1ull, __ATOMIC_ACQ_REL);
+    return (old & 1ull) == 0;
+}
 void* create_stream() { return nullptr; }
 void destroy_stream(void*) {}
 void* create_event() { return nullptr; }

@@ -10,6 +10,10 @@ namespace fcsg {
 namespace dev {
 
 void set_device(int device);
+// true exactly once per (flag, current device): per-device one-time setup such
+// as cudaFuncSetAttribute (function attributes are per device). flag is a
+// caller-owned word, one bit per device ordinal < 64; thread-safe.
+bool first_on_device(unsigned long long* flag);
 void* create_stream();
 void destroy_stream(void* s);
 // events for fork / join between streams (also inside graph capture)

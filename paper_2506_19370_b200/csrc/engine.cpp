@@ -330,6 +330,39 @@ void Engine::load_mlp_file(const std::string& path) {
     set_mlp_packed(packed);
 }
 
+// Donor purity of the uploaded solution-exchange plan, the property the
+// reference's phase 6 relies on (src/runtime.cpp:140-144,239-247: copies from
+// the deepest-window interior donor, interpolation stencils entirely
+// interior; the barriers at :482-512 order stage updates before the reads):
+// every recipient is a fringe point (mask 2) and every donor point -- each
+// copy source, each point of each 6x6 stencil -- an interior point (mask 1).
+// exchange_kernel has no barrier between its reads and writes; with pure
+// donors no point it writes is read by it. Donors on other ranks (halo slots)
+// are checked by their own rank's plan.
+void Engine::check_donor_purity(const std::vector<uint8_t>& mask) const {
+    auto bad = [&](const char* what, long p) {
+        const int slot = static_cast<int>(std::upper_bound(off_of_slot_.begin(), off_of_slot_.end(), p) -
+                                          off_of_slot_.begin()) - 1;
+        const auto& sp = subs_[id_of_slot_[slot]];
+        const long loc = p - off_of_slot_[slot];
+        throw Error(kDecomposition, std::string("exchange plan is not donor-pure: ") + what + " at subpatch " +
+                                        std::to_string(id_of_slot_[slot]) + " (i=" + std::to_string(loc % sp.ni) +
+                                        ", j=" + std::to_string(loc / sp.ni) + ")");
+    };
+    for (size_t k = 0; k < x_dst_.size(); ++k) {
+        if (mask[x_dst_[k]] != 2) bad("copy recipient is not a fringe point", x_dst_[k]);
+        if (x_src_[k] < npts_ && mask[x_src_[k]] != 1) bad("copy donor is not an interior point", x_src_[k]);
+    }
+    for (size_t k = 0; k < xi_dst_.size(); ++k) {
+        if (mask[xi_dst_[k]] != 2) bad("interpolation recipient is not a fringe point", xi_dst_[k]);
+        for (int b = 0; b < 6; ++b)
+            for (int a = 0; a < 6; ++a) {
+                const long p = xi_src_[k] + static_cast<long>(b) * xi_pitch_[k] + a;
+                if (mask[p] != 1) bad("interpolation stencil point is not an interior point", p);
+            }
+    }
+}
+
 void Engine::finalize() {
     if (finalized_) throw Error(kUsage, "engine already finalized");
     if (subs_.empty()) throw Error(kUsage, "engine has no subpatches");
@@ -418,6 +451,7 @@ void Engine::finalize() {
     E.bc_col_lo = static_cast<const BcDev*>(up(clo.data(), clo.size() * sizeof(BcDev)));
     E.bc_col_hi = static_cast<const BcDev*>(up(chi.data(), chi.size() * sizeof(BcDev)));
     E.mask = static_cast<const uint8_t*>(up(mask.data(), mask.size()));
+    check_donor_purity(mask);
     const double** gp[7] = {&E.iq1x, &E.iq2x, &E.iq1y, &E.iq2y, &E.h_min, &E.h_max, &E.w_norm};
     for (int k = 0; k < 7; ++k) *gp[k] = static_cast<const double*>(up(geo[k].data(), geo[k].size() * sizeof(double)));
 
@@ -639,6 +673,9 @@ void Engine::finalize() {
                 const int op = ctx_.get_op(n, cfg_.n_cont, 2, cfg_.filter);
                 L.pl = ctx_.op(op).plan;
                 L.scr = step_scr_cap(L.pl);
+                if (!line_pass_smem_fits(L.pl, L.scr))
+                    throw Error(kConfig, "subpatch lines of " + std::to_string(n) +
+                                             " points exceed the line passes' shared memory (227 KB per CTA)");
                 return L;
             };
             if (!any_l) {
@@ -660,7 +697,8 @@ void Engine::finalize() {
             }
             for (auto& [n, lines] : runs) {
                 LineSet L = make_set(n);
-                for (int lb : {4, 8}) {
+                for (int li = 0; li < 3; ++li) {
+                    const int lb = kDescLB[li];
                     std::vector<LineDesc> desc;
                     for (size_t q = 0; q < lines.size();) {
                         LineDesc d{lines[q][0], lines[q][1], 1, lines[q][2]};
@@ -673,14 +711,8 @@ void Engine::finalize() {
                         desc.push_back(d);
                         q = r;
                     }
-                    const LineDesc* dd = static_cast<const LineDesc*>(up(desc.data(), desc.size() * sizeof(LineDesc)));
-                    if (lb == 4) {
-                        L.desc4 = dd;
-                        L.n4 = static_cast<int>(desc.size());
-                    } else {
-                        L.desc8 = dd;
-                        L.n8 = static_cast<int>(desc.size());
-                    }
+                    L.desc[li] = static_cast<const LineDesc*>(up(desc.data(), desc.size() * sizeof(LineDesc)));
+                    L.n[li] = static_cast<int>(desc.size());
                 }
                 sets.push_back(L);
             }

@@ -147,6 +147,7 @@ class Engine {
     double* field_ptr(const std::string& name, int comp);
     void layout();                          // storage order by shape group (after the last add_subpatch)
     long gidx(int sub, int loc) const;      // global point index of (subpatch id, local index)
+    void check_donor_purity(const std::vector<uint8_t>& mask) const;
     long sub_points(int sub) const { return static_cast<long>(subs_.at(sub).ni) * subs_.at(sub).nj; }
     Ctx& ctx_;
     EngineConfig cfg_;

@@ -6,6 +6,7 @@
 // along the line for stride==1 (rows), across lines when line_stride==1
 // (columns of a row-major field; then thread w takes point w / LB of line
 // w % LB, the shared-memory order).
+#include "dev.h"
 #include "fc_lines.h"
 #include "fft_line.h"
 
@@ -55,11 +56,10 @@ __global__ void __launch_bounds__(256, NE > 0 ? 3 : 2) fc_lines_kernel(const __g
 
 template <int LB, int NE>
 void launch_fc_lines_t(const FcLinesArgs& a, int nblk, size_t smem, cudaStream_t s) {
-    static bool once = false;  // not during graph capture
-    if (!once) {
+    static unsigned long long done = 0;  // per device (function attributes are per device)
+    if (dev::first_on_device(&done)) {
         cudaFuncSetAttribute(fc_lines_kernel<LB, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(fc_lines_kernel<LB, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        once = true;
     }
     fc_lines_kernel<LB, NE><<<nblk, 256, smem, s>>>(a);
 }

@@ -17,6 +17,7 @@
 //
 // Each line pass keeps two real quantities per complex FFT line (fft_line.h)
 // and runs on one shape group of subpatches (step_kernels.h, EngineDev).
+#include "dev.h"
 #include "fft_line.h"
 #include "step_kernels.h"
 
@@ -180,7 +181,7 @@ FCSG_HD void line_pass(Thr t, int block, double2* smem, const Pass& P, const Eng
         const LineDesc d = desc[block];
         c.sub = d.sub;
         c.line0 = d.line0;
-        c.nl_valid = d.nl;
+        c.nl_valid = d.nl < LB ? d.nl : LB;  // runs are built per LB (LineSet::desc); never longer
         c.begin = d.begin;
     } else {     // every line of every subpatch of the view
         const int nlines = rows ? nj : ni;
@@ -1989,15 +1990,28 @@ template <class Pass, int NE, int NT, int LB>
 void launch_line_pass(int nblk, size_t smem, int arg, const EngineDev& E, const FcPlanDev& pl, int scr_cap,
                       const LineDesc* desc, cudaStream_t s) {
     auto k = line_pass_kernel<LB, Pass, NE, NT>;
-    static bool attr_set = false;  // once per instantiation (not during graph capture)
-    if (!attr_set) {
+    static unsigned long long done = 0;  // once per instantiation and device
+    if (dev::first_on_device(&done)) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        attr_set = true;
     }
     k<<<nblk, NT, smem, s>>>(E, pl, scr_cap, arg, desc);
 }
 #endif
+
+}  // namespace
+
+size_t line_pass_smem(const FcPlanDev& pl, int scr_cap, int slots, int lb) {
+    return (static_cast<size_t>(pl.n_ext) * lb + scr_cap + table_slots_host(pl)) * sizeof(double2) +
+           static_cast<size_t>(slots) * pl.n * lb * sizeof(double);
+}
+
+bool line_pass_smem_fits(const FcPlanDev& pl, int scr_cap) {
+    // the widest staging area of any pass (PassB, PassGB: 7 slots), 2 lines per CTA
+    return line_pass_smem(pl, scr_cap, 7, 2) <= kMaxLinePassSmem;
+}
+
+namespace {
 
 // One line set of one group view. Lines per CTA: Pass::kLB for the
 // compile-time plans (4 where a large staging area would otherwise cost
@@ -2018,18 +2032,20 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
         return ne == 280 || ne == 536 || ne == 171 || ne == 94 || ne == 102 || ne == 103 || ne == 163;
     };
     const bool ct = ref_op && is_ct(pl.n_ext);
-#if FCSG_CUDA
+    // the emulation runs the same lines-per-CTA as the GPU (one emulated
+    // thread), so it covers the line ownership of every launch shape
     constexpr int kCtLB = Pass::kLB;
-#else
-    constexpr int kCtLB = kLB;  // the emulation covers the loop structure, not the CTA shape
-#endif
-    const int lb = ct ? kCtLB : kLB;
-    const LineDesc* desc = lb == 4 ? L.desc4 : L.desc8;
+    static_assert(kCtLB == 2 || kCtLB == 4 || kCtLB == 8, "descriptor lists exist for 2, 4, 8 lines per CTA");
+    // generic plan: 8 lines per CTA, or 2 when 8 would not fit the shared
+    // memory of one SM (long lines; Engine::finalize rejects lines for which
+    // even 2 do not fit, line_pass_smem_fits)
+    const bool narrow = !ct && line_pass_smem(pl, scr_cap, kSlots, kLB) > kMaxLinePassSmem;
+    const int lb = ct ? kCtLB : (narrow ? 2 : kLB);
+    const LineDesc* desc = L.desc[desc_index(lb)];
     if (ct) scr_cap = std::max(scr_cap, ct_scratch_slots(pl.n_ext, lb));  // prime middles: full scratch
-    const int nblk = desc ? (lb == 4 ? L.n4 : L.n8) : E.S * ((nlines + lb - 1) / lb);
+    const int nblk = desc ? L.n[desc_index(lb)] : E.S * ((nlines + lb - 1) / lb);
     if (nblk == 0) return;
-    const size_t smem = (static_cast<size_t>(pl.n_ext) * lb + scr_cap + table_slots_host(pl)) * sizeof(double2) +
-                        static_cast<size_t>(kSlots) * pl.n * lb * sizeof(double);
+    const size_t smem = line_pass_smem(pl, scr_cap, kSlots, lb);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     constexpr int kNT = NtOf<Pass>::v;
@@ -2040,19 +2056,21 @@ void run_line_pass(int arg, const EngineDev& E, const LineSet& L, void* stream) 
     else if (ct && pl.n_ext == 102) launch_line_pass<Pass, 102, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else if (ct && pl.n_ext == 103) launch_line_pass<Pass, 103, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else if (ct) launch_line_pass<Pass, 163, kNT, kCtLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
+    else if (narrow) launch_line_pass<Pass, 0, kThreads, 2>(nblk, smem, arg, E, pl, scr_cap, desc, s);
     else launch_line_pass<Pass, 0, kThreads, kLB>(nblk, smem, arg, E, pl, scr_cap, desc, s);
 #else
     (void)stream;
     const Pass P(E, arg);
     std::vector<double2> sm(smem / sizeof(double2) + 1);
     for (int b = 0; b < nblk; ++b) {
-        if (ct && pl.n_ext == 280) line_pass<kLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct && pl.n_ext == 536) line_pass<kLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct && pl.n_ext == 171) line_pass<kLB, Pass, 171, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct && pl.n_ext == 94) line_pass<kLB, Pass, 94, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct && pl.n_ext == 102) line_pass<kLB, Pass, 102, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct && pl.n_ext == 103) line_pass<kLB, Pass, 103, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
-        else if (ct) line_pass<kLB, Pass, 163, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        if (ct && pl.n_ext == 280) line_pass<kCtLB, Pass, 280, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 536) line_pass<kCtLB, Pass, 536, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 171) line_pass<kCtLB, Pass, 171, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 94) line_pass<kCtLB, Pass, 94, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 102) line_pass<kCtLB, Pass, 102, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct && pl.n_ext == 103) line_pass<kCtLB, Pass, 103, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (ct) line_pass<kCtLB, Pass, 163, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
+        else if (narrow) line_pass<2, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
         else line_pass<kLB, Pass, 0, 1>(Thr{0, 1}, b, sm.data(), P, E, pl, scr_cap, desc);
     }
 #endif
@@ -2221,7 +2239,7 @@ void launch_classify(const EngineDev& Eall, const std::vector<GroupLaunch>& G, b
         }();
         for (const GroupLaunch& g : G) {
             // tensor-core path: 32-point windows, full lines of >= 32 points
-            const bool rect = g.rows.size() == 1 && g.rows[0].desc4 == nullptr;
+            const bool rect = g.rows.size() == 1 && g.rows[0].desc[0] == nullptr;
             if (!scalar && rect && g.E.fb_window == 32 && g.E.ni >= 32 && g.E.nj >= 32) {
                 long n = ((g.E.npts + 3) / 4 + kSpecMmaThreads / 32 - 1) / (kSpecMmaThreads / 32);
                 n = n > 148 * 8 ? 148 * 8 : (n < 1 ? 1 : n);

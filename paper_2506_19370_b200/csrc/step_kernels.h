@@ -146,15 +146,18 @@ struct LineDesc {
 };
 
 // One launch's set of lines of one length n and orientation: FC plan and,
-// for groups with L-shaped subpatches, descriptor lists for 4 and 8 lines
-// per CTA (null: every line of every subpatch of the view, begin 0).
+// for groups with L-shaped subpatches, descriptor lists for every CTA line
+// count a pass uses (desc[k], n[k]: runs of at most kDescLB[k] lines; null:
+// every line of every subpatch of the view, begin 0). A pass launched with LB
+// lines per CTA takes exactly the LB list (desc_index), so no run is longer
+// than its CTA.
+constexpr int kDescLB[3] = {2, 4, 8};
+inline int desc_index(int lb) { return lb == 2 ? 0 : (lb == 4 ? 1 : 2); }
 struct LineSet {
     FcPlanDev pl;
     int scr;
-    const LineDesc* desc4;
-    int n4;
-    const LineDesc* desc8;
-    int n8;
+    const LineDesc* desc[3];
+    int n[3];
 };
 
 // everything the launchers need for one shape group
@@ -172,6 +175,12 @@ constexpr int kTanhTable = 1281;  // tanh(k/64), k = 0..1280
 std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
 
 int step_scr_cap(const FcPlanDev& pl);
+// dynamic shared memory of a line-pass CTA (lb lines, `slots` staging doubles
+// per point) and the per-CTA opt-in limit of sm_100a (227 KB)
+constexpr size_t kMaxLinePassSmem = 227 * 1024;
+size_t line_pass_smem(const FcPlanDev& pl, int scr_cap, int slots, int lb);
+// false when a line set's lines are too long for any pass's CTA shape
+bool line_pass_smem_fits(const FcPlanDev& pl, int scr_cap);
 // phase 0: proxy over all points (global view), classifier per group
 void launch_phase0(const EngineDev& Eall, const std::vector<GroupLaunch>& G, bool step0, void* stream);
 void launch_proxy(const EngineDev& Eall, void* stream);

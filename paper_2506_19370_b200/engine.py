@@ -157,27 +157,62 @@ class Engine:
         e = np.ascontiguousarray(e, dtype=np.float64)
         self.ctx.check(self.ctx.lib.fcsg_engine_set_state(self.h, sub, N.dptr(e)))
 
+    def _host_buffer(self, a, n, what, writable=False):
+        """(pointer, keep-alive) of a host float64 buffer of at least n
+        doubles: a numpy array or a CPU torch tensor, C-contiguous. Inputs of
+        another dtype or layout are converted into a copy that the caller
+        keeps alive across the C call; outputs must already be float64,
+        contiguous and large enough (the C call writes n doubles)."""
+        if hasattr(a, "data_ptr"):  # torch tensor
+            import torch
+
+            if a.device.type != "cpu":
+                raise ValueError(f"{what}: host buffer expected, got a tensor on {a.device}")
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                if writable:
+                    raise ValueError(f"{what}: output must be a contiguous float64 tensor")
+                a = a.to(torch.float64).contiguous()
+            if a.numel() < n:
+                raise ValueError(f"{what}: {a.numel()} doubles, {n} needed")
+            return a.data_ptr(), a
+        arr = np.asarray(a)
+        if arr.dtype != np.float64 or not arr.flags.c_contiguous:
+            if writable:
+                raise ValueError(f"{what}: output must be a C-contiguous float64 array")
+            arr = np.ascontiguousarray(arr, dtype=np.float64)
+        if writable and not arr.flags.writeable:
+            raise ValueError(f"{what}: output array is read-only")
+        if arr.size < n:
+            raise ValueError(f"{what}: {arr.size} doubles, {n} needed")
+        return arr.ctypes.data, arr
+
     def set_state_bulk(self, e):
         """all subpatches, [4][sum of points] (per component the subpatches in
         id order, each [nj][ni]; [4][S][nj][ni] for one shape); ``e`` may be a numpy array or a
         (pinned) CPU torch tensor"""
-        ptr = e.data_ptr() if hasattr(e, "data_ptr") else np.ascontiguousarray(e, dtype=np.float64).ctypes.data
+        ptr, keep = self._host_buffer(e, 4 * self.total_points(), "set_state_bulk")
         self.ctx.check(self.ctx.lib.fcsg_engine_set_state_bulk(self.h, C.c_void_p(ptr)))
+        del keep
 
     def run_host(self, state_in, state_out, steps=1, in_stride=0, out_stride=0):
         """steps supersteps with host I/O per step (fcsg_engine_run_host):
         step k reads its state from state_in (+ k in_stride doubles) and
         leaves its result in state_out (+ k out_stride); uploads/downloads
         overlap the neighbouring steps' kernels (pinned buffers)."""
-        pi = state_in.data_ptr() if hasattr(state_in, "data_ptr") else state_in.ctypes.data
-        po = state_out.data_ptr() if hasattr(state_out, "data_ptr") else state_out.ctypes.data
+        n = 4 * self.total_points()
+        if steps < 0 or in_stride < 0 or out_stride < 0:
+            raise ValueError("run_host: steps and strides must be >= 0")
+        last = max(steps - 1, 0)
+        pi, keep_i = self._host_buffer(state_in, n + last * in_stride, "run_host input")
+        po, keep_o = self._host_buffer(state_out, n + last * out_stride, "run_host output", writable=True)
         done = C.c_long()
         self.ctx.check(self.ctx.lib.fcsg_engine_run_host(self.h, steps, C.c_void_p(pi), in_stride, C.c_void_p(po),
                                                          out_stride, C.byref(done)))
+        del keep_i, keep_o
         return done.value
 
     def get_state_bulk(self, out):
-        ptr = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        ptr, _ = self._host_buffer(out, 4 * self.total_points(), "get_state_bulk", writable=True)
         self.ctx.check(self.ctx.lib.fcsg_engine_get_state_bulk(self.h, C.c_void_p(ptr)))
         return out
 

@@ -216,7 +216,7 @@ def cylinder_flow(full=True):
 
 
 
-def step_flow(scale=1):
+def step_flow(scale=1, cfl=0.25):
     """BASELINE config 4: Mach 3 flow over a forward-facing step in
     [0, 3] x [0, 1] (step of height 0.2 at x = 0.6). The reference's own
     corner-patch problems fail their overlap checks, so
@@ -228,7 +228,9 @@ def step_flow(scale=1):
     inflow rho = 1.4, p = 1, u = 3 on the left, supersonic outflow on the
     right, slip walls. The I and S patches are split into 256 x 256
     subpatches (as config 5); scale k multiplies the cells per patch side
-    (about 0.87M k^2 points; the C1 patch gets 2k cells of 60 points)."""
+    (about 0.87M k^2 points; the C1 patch gets 2k cells of 60 points).
+    CFL 0.25: the reference runs every problem with C1 patches at 0.25
+    (src/problems.cpp:88,284)."""
     from . import multipatch as M
     SI = M.SideInfo
     c, a = (0.6, 0.2), 0.15
@@ -258,4 +260,4 @@ def step_flow(scale=1):
     def ic(x, y):
         return np.broadcast_to(np.asarray(free).reshape(4, 1, 1), (4,) + np.shape(x)).copy()
 
-    return dec, ic, {"cfl": 0.5, "free_stream": free}
+    return dec, ic, {"cfl": cfl, "free_stream": free}

@@ -234,7 +234,7 @@ def test_config4_step_against_reference(gpu_ctx):
     flow."""
     import os
     dec, ic, meta = PR.step_flow(1)
-    R = ref.RefEngine.testgeom(5, 0, workers=os.cpu_count() or 1, weight_path=EN.DEFAULT_WEIGHTS)
+    R = ref.RefEngine.testgeom(5, 0, cfl=meta["cfl"], workers=os.cpu_count() or 1, weight_path=EN.DEFAULT_WEIGHTS)
     RD = RefDecomposition(R)
     assert any(d.cut_i > 0 for d in dec.subs)
     for d, r in zip(dec.subs, RD.subs):
