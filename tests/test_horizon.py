@@ -99,11 +99,15 @@ def test_config4_benched_size_20_steps_against_reference(gpu_ctx):
     assert E.shapes == [tuple(d.mask.shape) for d in RD.subs]
     R.run(20)
     assert E.run(20) == 20
-    worst = 0.0
+    # relative L2 per field over the whole domain: in the Mach 3 free stream
+    # rho v is zero up to round-off on most subpatches, so a per-subpatch
+    # relative norm of it would compare round-off with round-off
+    dn, wn = np.zeros(4), np.zeros(4)
     for k in range(R.nsubs):
         got, want = E.get_state(k), R.get_state(k)
-        for c in range(4):
-            err = rel_l2(got[c], want[c])
-            worst = max(worst, err)
-            assert err <= 1e-8, (k, c, err)
-    print(f"config4 step_flow(2) 20 steps at CFL 0.25: worst per-field rel L2 {worst:.3e}")
+        dn += ((got - want) ** 2).sum(axis=(1, 2))
+        wn += (want ** 2).sum(axis=(1, 2))
+        assert np.array_equal(E.get(k, "tau"), R.get(k, "tau")), k
+    err = np.sqrt(dn / wn)
+    print(f"config4 step_flow(2), 20 steps at CFL 0.25: rel L2 per field over the domain {err}")
+    assert err.max() <= 1e-8, err
