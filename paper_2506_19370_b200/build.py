@@ -24,7 +24,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
-CU_SOURCES = ["dev.cu", "fc_lines.cu", "step_kernels.cu"]
+CU_SOURCES = ["dev.cu", "fc_lines.cu", "step_kernels.cu", "wpass.cu"]
 CPP_SOURCES = ["fc_tables.cpp", "capi.cpp", "engine.cpp"]
 
 
@@ -57,6 +57,7 @@ def build(emulate: bool = False, verbose: bool = False, force: bool = False) -> 
     lib = os.path.join(out_dir, "libfcsg_emu.so" if emulate else "libfcsg.so")
     hdrs = _headers()
     objs = []
+    cmds = []
     common_inc = [f"-I{CSRC}", f"-I{os.path.join(ROOT, 'include')}"]
     for src in CU_SOURCES + CPP_SOURCES:
         path = os.path.join(CSRC, src)
@@ -74,9 +75,13 @@ def build(emulate: bool = False, verbose: bool = False, force: bool = False) -> 
                    "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", *common_inc, "-c", path, "-o", obj]
         else:
             cmd = ["g++", "-std=c++17", "-O3", "-fPIC", f"-I{CUDA_HOME}/include", *common_inc, "-c", path, "-o", obj]
-        r = _run(cmd)
-        if verbose and r.stderr:
-            sys.stderr.write(r.stderr)
+        cmds.append(cmd)
+    # translation units compile in parallel (the step kernels dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for r in ex.map(_run, cmds):
+            if verbose and r.stderr:
+                sys.stderr.write(r.stderr)
     if force or _stale(lib, objs):
         if emulate:
             _run(["g++", "-shared", "-o", lib, *objs, "-lquadmath", "-lpthread"])

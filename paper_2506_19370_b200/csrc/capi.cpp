@@ -39,6 +39,12 @@ int Ctx::get_op(int n, int n_cont, int degree, FilterSpec f) {
     p.tw = op->d_tw;
     p.blend = op->d_blend;
     p.mult = op->d_mult;
+    p.mult_pfa = nullptr;
+    if (!t.mult_pfa.empty()) {
+        op->d_mult_pfa = dev::alloc_n<double2>(t.mult_pfa.size());
+        dev::h2d(op->d_mult_pfa, t.mult_pfa.data(), t.mult_pfa.size() * sizeof(double2), stream);
+        p.mult_pfa = op->d_mult_pfa;
+    }
     const int id = static_cast<int>(ops.size());
     ops.push_back(std::move(op));
     op_index[key] = id;

@@ -21,7 +21,9 @@ struct DevOp {
     double2* d_tw = nullptr;
     double* d_blend = nullptr;
     double2* d_mult = nullptr;
+    double2* d_mult_pfa = nullptr;
     ~DevOp() {
+        dev::free(d_mult_pfa);
         dev::free(d_tw);
         dev::free(d_blend);
         dev::free(d_mult);

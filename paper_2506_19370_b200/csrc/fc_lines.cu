@@ -6,6 +6,8 @@
 // along the line for stride==1 (rows), across lines when line_stride==1
 // (columns of a row-major field; then thread w takes point w / LB of line
 // w % LB, the shared-memory order).
+#include <cstdlib>
+
 #include "dev.h"
 #include "fc_lines.h"
 #include "fft_line.h"
@@ -90,6 +92,10 @@ int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {
 }
 
 void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
+    if (w280_lines_applies(a.pl) && !std::getenv("FCSG_NO_WARP_LINES")) {
+        launch_w280_lines(a, stream);
+        return;
+    }
 #if !FCSG_CUDA
     LB = 4;  // the emulation runs one block shape
 #endif

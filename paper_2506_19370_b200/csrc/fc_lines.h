@@ -25,5 +25,9 @@ struct FcLinesArgs {
 size_t fc_lines_smem_bytes(const FcPlanDev& pl, int LB, int scr_cap);
 int fc_lines_scr_cap(const FcPlanDev& pl, int LB);
 void launch_fc_lines(FcLinesArgs a, int LB, void* stream);
+// the warp-per-line prime-factor kernel (wpass.cu) for the N = 256 reference
+// operator (n_ext = 280); launch_fc_lines takes it when it applies
+bool w280_lines_applies(const FcPlanDev& pl);
+void launch_w280_lines(const FcLinesArgs& a, void* stream);
 
 }  // namespace fcsg

@@ -220,6 +220,20 @@ FcTables build_fc_tables(int n_points, int n_cont, int degree, FilterSpec f) {
         t.mult[2 * n + pos] = double2{t.filter_profile[kk] * inv_n, 0.0};
         t.mult[3 * n + pos] = double2{t.smear_profile[kk] * inv_n, 0.0};
     }
+    // the prime-factor order of the warp transform (wline.h): entry
+    // (k1 * 5 + k2) * 7 + k3 holds frequency (105 k1 + 56 k2 + 120 k3) mod 280
+    if (n == 280) {
+        std::vector<int> pos_of_freq(n);
+        for (int pos = 0; pos < n; ++pos) pos_of_freq[t.freq_of_pos[pos]] = pos;
+        t.mult_pfa.assign(4 * static_cast<size_t>(n), double2{0.0, 0.0});
+        for (int k1 = 0; k1 < 8; ++k1)
+            for (int k2 = 0; k2 < 5; ++k2)
+                for (int k3 = 0; k3 < 7; ++k3) {
+                    const int idx = (k1 * 5 + k2) * 7 + k3;
+                    const int pos = pos_of_freq[(105 * k1 + 56 * k2 + 120 * k3) % n];
+                    for (int m = 0; m < 4; ++m) t.mult_pfa[m * n + idx] = t.mult[m * n + pos];
+                }
+    }
     return t;
 }
 

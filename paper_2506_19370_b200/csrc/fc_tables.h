@@ -34,6 +34,7 @@ struct FcTables {
     std::vector<int> freq_of_pos;        // DIF output position -> frequency index
     std::vector<double2> tw;             // n_ext
     std::vector<double2> mult;           // 4 x n_ext (d1, d2, filter, smear) in position order
+    std::vector<double2> mult_pfa;       // n_ext = 280: 4 x 280 in the (k1, k2, k3) order of wline.h
 };
 
 // Blend-to-zero matrix for Gram degree d (d = 2 is the reference's

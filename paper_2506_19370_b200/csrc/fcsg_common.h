@@ -132,6 +132,8 @@ struct FcPlanDev {
     const double2* tw;      // exp(-2 pi i k / n_ext), k < n_ext
     const double* blend;    // n_gap x dp1, row-major (FcOperator::blend_matrix)
     const double2* mult;    // 4 x n_ext multipliers in DIF output order: d1, d2, filter, smear
+    const double2* mult_pfa;  // n_ext = 280 only (else null): the same 4 tables in the prime-factor
+                              // order (k1, k2, k3) of wline.h, k3 fastest
 };
 
 }  // namespace fcsg

@@ -38,6 +38,14 @@ FCSG_HD double ldg1(const double* p) {
 #endif
 }
 
+FCSG_HD double2 ldg2(const double2* p) {
+#if FCSG_CUDA && defined(__CUDA_ARCH__)
+    return __ldg(p);
+#else
+    return *p;
+#endif
+}
+
 // shared-memory slots (double2) for the staged tables of one operator
 FCSG_HD int table_slots(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
 #if FCSG_CUDA

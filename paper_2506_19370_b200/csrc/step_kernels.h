@@ -175,6 +175,10 @@ constexpr int kTanhTable = 1281;  // tanh(k/64), k = 0..1280
 std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
 
 int step_scr_cap(const FcPlanDev& pl);
+// warp-per-line Cartesian flux passes on the n_ext = 280 prime-factor
+// transform (wpass.cu): rows = pass X, else pass Y (stage = RK stage)
+bool wpass_applies(const EngineDev& E, const FcPlanDev& pl, bool rows);
+void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage, void* stream);
 // dynamic shared memory of a line-pass CTA (lb lines, `slots` staging doubles
 // per point) and the per-CTA opt-in limit of sm_100a (227 KB)
 constexpr size_t kMaxLinePassSmem = 227 * 1024;

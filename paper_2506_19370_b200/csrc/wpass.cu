@@ -1,0 +1,462 @@
+// Warp-per-line kernels on the n_ext = 280 prime-factor transform (wline.h):
+// the N = 256 lines of the reference operator (every subpatch of BASELINE
+// configs 1 and 5, and the Cartesian I / S patches of configs 3 and 4).
+//
+//  * fc_lines (FcOperator::derivative / filter / strong_filter over a batch
+//    of lines, src/fc_core.cpp:257-306): one complex line = two real lines
+//    per warp.
+//  * pass X / pass Y of the Cartesian flux form (step_kernels.cu PassXc /
+//    PassYc, euler_rhs src/euler.cpp:25-101 as div(mu grad w - f), and the
+//    SSPRK(5,4) stage update src/euler.cpp:182-221): one row (X) or column
+//    (Y) of one subpatch per warp, 4 transform rounds, the per-point values a
+//    later round needs kept in the lane's registers.
+//
+// A CTA is kWarps independent warps; the only block barrier orders the copy
+// of the multiplier table into shared memory before the first transform.
+// Each warp's lane l owns the points i = l + 32 m (m < 8) of its line for
+// loads and epilogues (coalesced along rows), and the butterflies of the
+// transform (wline.h).
+#include "dev.h"
+#include "fc_lines.h"
+#include "pass_common.h"
+#include "step_kernels.h"
+#include "wline.h"
+
+namespace fcsg {
+
+namespace {
+constexpr int kWarps = 8;  // warps per CTA
+constexpr int kWThreads = kWarps * 32;
+}  // namespace
+
+// conservative -> primitive as prim_of (src/euler.cpp:29-41) with one
+// reciprocal of the density instead of four divisions per point (the
+// products differ from the quotients by an ulp, far inside the parity gates)
+struct PrimR {
+    double rho, mx, my, E, ir, theta, p;
+};
+FCSG_HD PrimR prim_r(double rho, double mx, double my, double E) {
+    PrimR q;
+    q.rho = rho;
+    q.mx = mx;
+    q.my = my;
+    q.E = E;
+    q.ir = 1.0 / ((rho != 0.0) ? rho : 1e-300);
+    const double pr = kGm1 * (E - 0.5 * (mx * mx + my * my) * q.ir);
+    q.theta = pr * q.ir;
+    q.p = rho * q.theta;
+    return q;
+}
+// x-flux F_c and y-flux G_c (src/euler.cpp:44-55, 64-75)
+FCSG_HD double flux_x(const PrimR& q, int c) {
+    const double u = q.mx * q.ir;
+    switch (c) {
+        case 0: return q.mx;
+        case 1: return q.mx * u + q.p;
+        case 2: return q.my * u;
+        default: return u * (q.E + q.p);
+    }
+}
+FCSG_HD double flux_y(const PrimR& q, int c) {
+    const double v = q.my * q.ir;
+    switch (c) {
+        case 0: return q.my;
+        case 1: return q.mx * v;
+        case 2: return q.my * v + q.p;
+        default: return v * (q.E + q.p);
+    }
+}
+
+// L2 prefetch of one 32-byte sector (the epilogue inputs of the next round,
+// issued before the transform so their DRAM latency hides behind it)
+FCSG_HD void pf_l2(const double* p) {
+#if FCSG_CUDA
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+#else
+    (void)p;
+#endif
+}
+// L2 prefetch of a contiguous range (multiple of 16 bytes, 16-byte aligned)
+FCSG_HD void pf_l2_bulk(const double* p, unsigned bytes) {
+#if FCSG_CUDA
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+#else
+    (void)p;
+    (void)bytes;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// FC line batch
+
+template <int NL>
+FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* mult, const FcLinesArgs& a) {
+    using namespace w280;
+    const long l = 2 * pair;
+    const long ls = a.line_stride, st = a.stride, ols = a.out_line_stride, ost = a.out_stride;
+    const bool have1 = l + 1 < a.n_lines;
+    constexpr int PPL = kN / NL;
+#pragma unroll 4
+    for (int m = 0; m < PPL; ++m) {
+        const int i = lane + NL * m;
+        const double v0 = ldg1(a.in + l * ls + i * st);
+        const double v1 = have1 ? ldg1(a.in + (l + 1) * ls + i * st) : 0.0;
+        buf[slot_of(i)] = mk2(v0, v1);
+    }
+    FCSG_SYNCWARP();
+    transform<NL, 1>(lane, buf, kSlots, mult, a.pl.blend);
+#pragma unroll 4
+    for (int m = 0; m < PPL; ++m) {
+        const int i = lane + NL * m;
+        const double2 v = buf[slot_of(i)];
+        a.out[l * ols + i * ost] = v.x * a.scale;
+        if (have1) a.out[(l + 1) * ols + i * ost] = v.y * a.scale;
+    }
+}
+
+#if FCSG_CUDA
+__global__ void __launch_bounds__(kWThreads, 3) w280_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+    extern __shared__ double2 wsm[];
+    // the multiplier table (global, read through L1 by wline.h's ldg2)
+    const double2* mult = a.pl.mult_pfa + (a.mode - 1) * w280::kNE;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* buf = wsm + warp * w280::kSlots;
+    const long npairs = (a.n_lines + 1) / 2;
+    for (long pair = static_cast<long>(blockIdx.x) * kWarps + warp; pair < npairs;
+         pair += static_cast<long>(gridDim.x) * kWarps)
+        w280_lines_body<32>(lane, pair, buf, mult, a);
+}
+#endif
+
+bool w280_lines_applies(const FcPlanDev& pl) {
+    return pl.n_ext == 280 && pl.n == 256 && pl.n_gap == 24 && pl.dp1 == 3 && pl.mult_pfa != nullptr;
+}
+
+void launch_w280_lines(const FcLinesArgs& a, void* stream) {
+    const long npairs = (a.n_lines + 1) / 2;
+    if (npairs == 0) return;
+#if FCSG_CUDA
+    const size_t smem = kWarps * w280::kSlots * sizeof(double2);
+    static unsigned long long done = 0;
+    if (dev::first_on_device(&done))
+        cudaFuncSetAttribute(w280_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    const long nblk = (npairs + kWarps - 1) / kWarps;
+    w280_lines_kernel<<<static_cast<int>(nblk), kWThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
+#else
+    (void)stream;
+    std::vector<double2> buf(w280::kSlots);
+    const double2* mult = a.pl.mult_pfa + (a.mode - 1) * w280::kNE;
+    for (long pair = 0; pair < npairs; ++pair) w280_lines_body<1>(0, pair, buf.data(), mult, a);
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Cartesian flux-form passes (PassXc / PassYc restated per warp)
+//
+// Both passes transform two complex lines at once: the pass's rounds come in
+// two independent pairs (X: D1 (rho, rho u) and D1 (rho v, theta); Y: D2
+// (rho v, theta) and D2 (rho, rho u)), so a pass is two "double rounds":
+// load -> transform both -> epilogue (Phi = mu grad w - f for both pairs) ->
+// transform both -> epilogue (tA, or rhs + SSPRK update of all four
+// components). The per-point values the second epilogue needs are re-read
+// (L1 / L2 hits) instead of kept: pass Y updates e only in its last
+// epilogue, so the state it reads there is still the stage's input.
+
+constexpr int kBP = w280::kSlots + 1;  // pitch between line buffers (double2): odd, spreads the quad's buffers over the banks
+
+// interior positivity diagnostic of euler_rhs (src/euler.cpp:37-39)
+FCSG_HD void w_check_positive(const EngineDev& E, double rho, double theta, long p, int sub, int i, int j) {
+    const double pr = theta * ((rho != 0.0) ? rho : 1e-300);
+    if ((!(rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) && E.mask[p] == 1)
+        raise_error(E.sc, 1, E.sub_base + sub, i, j);
+}
+
+// Pass X (rows, second pass of the stage): D1 (rho, rho u) and D1 (rho v,
+// theta) -> Phi_x = mu iq1x D1 w - F_c -> D1 Phi_x -> rhs_c = tA_c + iq1x
+// D1 Phi_x_c (tA = iq2y D2 Phi_y from pass Y) -> SSPRK(5,4) update of the
+// four components. One row per warp; lane l owns the points l + 32 m
+// (coalesced).
+template <int NL>
+FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult, const EngineDev& E,
+                          const double* blend, int stage) {
+    using namespace w280;
+    constexpr int PPL = kN / NL;
+    constexpr int KC = PPL >= 2 ? 2 : 1;  // points per load chunk of the update epilogue (12 loads each)
+    constexpr int KL = PPL >= 4 ? 4 : 1;  // points per load chunk of the other phases
+    const int ni = E.ni, nj = E.nj;
+    const int sub = line / nj, row = line - sub * nj;
+    const long rb = static_cast<long>(sub) * ni * nj + static_cast<long>(row) * ni;
+    const double inv_len = 1.0 / ((kN - 1) * E.h1[sub]);  // LineInfo::inv_len (src/subpatch_data.cpp:134)
+    const bool uq = E.uniform_q != 0;
+    const double qc = uq ? E.iq1x_c[sub] : 0.0;
+    const double dt = E.sc->dt;
+    const bool e0r = stage >= 1 && stage <= 3;  // stages whose update reads the register e0
+    double2* bA = buf;
+    double2* bB = buf + kBP;
+    // load: e -> (rho, rho u) | (rho v, theta)
+#pragma unroll 1
+    for (int m0 = 0; m0 < PPL; m0 += KL) {
+        double v[KL][4];
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const long p = rb + lane + NL * (m0 + k);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[k][c] = ldg1(E.e[c] + p);
+        }
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const int i = lane + NL * (m0 + k);
+            const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
+            w_check_positive(E, q.rho, q.theta, rb + i, sub, i, row);
+            const int s = slot_of(i);
+            bA[s] = mk2(q.rho, q.mx);
+            bB[s] = mk2(q.my, q.theta);
+        }
+    }
+    if (lane == 0) {  // the epilogue's row of mu (and iq1x) into L2 behind the transform
+        pf_l2_bulk(E.mu + rb, kN * sizeof(double));
+        if (!uq) pf_l2_bulk(E.iq1x + rb, kN * sizeof(double));
+    }
+    FCSG_SYNCWARP();
+    transform<NL, 2>(lane, buf, kBP, mult, blend);
+    // epilogue: s4 = mu (iq1x D1 w); the next input Phi_x = s4 - F
+#pragma unroll 1
+    for (int m0 = 0; m0 < PPL; m0 += KL) {
+        double v[KL][4], mu[KL], a[KL];
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const long p = rb + lane + NL * (m0 + k);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[k][c] = ldg1(E.e[c] + p);
+            mu[k] = ldg1(E.mu + p);
+            a[k] = uq ? qc : ldg1(E.iq1x + p);
+        }
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const int s = slot_of(lane + NL * (m0 + k));
+            const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
+            const double2 wa = bA[s], wb = bB[s];
+            const double ax = a[k] * (wa.x * inv_len), ay = a[k] * (wa.y * inv_len);
+            const double bx = a[k] * (wb.x * inv_len), by = a[k] * (wb.y * inv_len);
+            bA[s] = mk2(mu[k] * ax - flux_x(q, 0), mu[k] * ay - flux_x(q, 1));
+            bB[s] = mk2(mu[k] * bx - flux_x(q, 2), mu[k] * by - flux_x(q, 3));
+        }
+    }
+    if (lane == 0) {  // the update's inputs into L2 behind the transform
+        for (int c = 0; c < 4; ++c) {
+            pf_l2_bulk(E.tA[c] + rb, kN * sizeof(double));
+            if (e0r) pf_l2_bulk(E.e0[c] + rb, kN * sizeof(double));
+            if (stage == 4) {
+                pf_l2_bulk(E.e2[c] + rb, kN * sizeof(double));
+                pf_l2_bulk(E.e3[c] + rb, kN * sizeof(double));
+                pf_l2_bulk(E.rhs3[c] + rb, kN * sizeof(double));
+            }
+        }
+    }
+    FCSG_SYNCWARP();
+    transform<NL, 2>(lane, buf, kBP, mult, blend);
+    // epilogue: rhs = tA + iq1x D1 Phi_x, SSPRK update; u = the stage's input
+    // state (pass Y does not write e)
+#pragma unroll 1
+    for (int m0 = 0; m0 < PPL; m0 += KC) {
+        double u[KC][4], ta[KC][4], z[KC][4], a[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const long p = rb + lane + NL * (m0 + k);
+            a[k] = uq ? qc : ldg1(E.iq1x + p);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                u[k][c] = ldg1(E.e[c] + p);
+                ta[k][c] = ldg1(E.tA[c] + p);
+                z[k][c] = e0r ? ldg1(E.e0[c] + p) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const long p = rb + lane + NL * (m0 + k);
+            const int s = slot_of(lane + NL * (m0 + k));
+            const double2 wa = bA[s], wb = bB[s];
+            ssprk_update_e0(E, stage, 0, p, u[k][0], ta[k][0] + a[k] * (wa.x * inv_len), z[k][0], dt);
+            ssprk_update_e0(E, stage, 1, p, u[k][1], ta[k][1] + a[k] * (wa.y * inv_len), z[k][1], dt);
+            ssprk_update_e0(E, stage, 2, p, u[k][2], ta[k][2] + a[k] * (wb.x * inv_len), z[k][2], dt);
+            ssprk_update_e0(E, stage, 3, p, u[k][3], ta[k][3] + a[k] * (wb.y * inv_len), z[k][3], dt);
+        }
+    }
+}
+
+// Pass Y (columns, first pass of the stage): D2 (rho v, theta) and D2 (rho,
+// rho u) -> Phi_y = mu iq2y D2 w - G_c -> D2 Phi_y -> tA_c = iq2y D2 Phi_y_c
+// (pass X adds iq1x D1 Phi_x and updates: the terms of rhs_c commute, so
+// this order only changes which partial is rounded first).
+//
+// Columns are strided in memory (pitch ni), so a CTA takes a quad of 4
+// adjacent columns: thread t of NT handles column c = t % 4 at rows
+// i = t / 4 + (NT / 4) k for the loads and epilogues -- one warp instruction
+// reads 8 rows x 32 contiguous bytes -- and writes into the buffers of the
+// warp that transforms that column (warp c). Block barriers order the
+// loads before the transforms and the transforms before the epilogues; the
+// transforms themselves are per warp.
+constexpr int kQuad = 4;
+
+template <int NT>
+FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult, const EngineDev& E,
+                          const double* blend) {
+    using namespace w280;
+    constexpr int PPT = kQuad * kN / NT;  // points per thread
+    constexpr int KC = PPT >= 4 ? 4 : 1;  // points per load chunk
+    const int ni = E.ni, nj = E.nj;
+    const int qps = (ni + kQuad - 1) / kQuad;
+    const int sub = quad / qps, c0 = (quad - sub * qps) * kQuad;
+    const long gb = static_cast<long>(sub) * ni * nj + c0;
+    const double inv_len = 1.0 / ((kN - 1) * E.h2[sub]);
+    const bool uq = E.uniform_q != 0;
+    const double qc = uq ? E.iq2y_c[sub] : 0.0;
+    const int ncol = ni - c0 < kQuad ? ni - c0 : kQuad;
+    // point k of this thread: w = tid + NT k, column w % 4, row w / 4
+    auto col = [&](int k) { return (tid + NT * k) & (kQuad - 1); };
+    auto row = [&](int k) { return (tid + NT * k) >> 2; };
+    auto pt = [&](int k) { return gb + static_cast<long>(row(k)) * ni + col(k); };
+    // line buffers: column c, line A (rho v, theta) at c * 2 kBP, line B (rho, rho u) at + kBP
+    auto bA = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + slot_of(row(k))]; };
+    auto bB = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + kBP + slot_of(row(k))]; };
+    // the next epilogue's inputs into L2 behind the transforms: one thread per
+    // 32-byte sector (the quad's 4 columns of one row)
+    auto prefetch = [&](const double* const* f, int nf) {
+        if (col(0) != 0) return;
+        for (int k = 0; k < PPT; ++k)
+            for (int q = 0; q < nf; ++q) pf_l2(f[q] + pt(k));
+    };
+    auto transform_all = [&]() {
+        FCSG_SYNC();
+#if FCSG_CUDA
+        const int warp = tid >> 5;
+        if (warp < kQuad) transform<32, 2>(tid & 31, bufs + warp * 2 * kBP, kBP, mult, blend);
+#else
+        for (int c = 0; c < kQuad; ++c) transform<1, 2>(0, bufs + c * 2 * kBP, kBP, mult, blend);
+#endif
+        FCSG_SYNC();
+    };
+    auto load_e = [&](int k, double* v) {
+        const bool ok = col(k) < ncol;
+        const long p = ok ? pt(k) : gb;
+        v[0] = ok ? ldg1(E.e[0] + p) : 1.0;
+        v[1] = ok ? ldg1(E.e[1] + p) : 0.0;
+        v[2] = ok ? ldg1(E.e[2] + p) : 0.0;
+        v[3] = ok ? ldg1(E.e[3] + p) : 1.0;
+    };
+    // load: (rho v, theta) | (rho, rho u)
+#pragma unroll 1
+    for (int k0 = 0; k0 < PPT; k0 += KC) {
+        double v[KC][4];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) load_e(k0 + k, v[k]);
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
+            bA(k0 + k) = mk2(q.my, q.theta);
+            bB(k0 + k) = mk2(q.rho, q.mx);
+        }
+    }
+    {
+        const double* f[2] = {E.mu, E.iq2y};
+        prefetch(f, uq ? 1 : 2);
+    }
+    transform_all();
+    // epilogue: Phi_y = mu iq2y D2 w - (G_2, G_3) | - (G_0, G_1)
+#pragma unroll 1
+    for (int k0 = 0; k0 < PPT; k0 += KC) {
+        double v[KC][4], mu[KC], d[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            load_e(k0 + k, v[k]);
+            const bool ok = col(k0 + k) < ncol;
+            const long p = ok ? pt(k0 + k) : gb;
+            mu[k] = ok ? ldg1(E.mu + p) : 0.0;
+            d[k] = uq ? qc : (ok ? ldg1(E.iq2y + p) : 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
+            double2& a = bA(k0 + k);
+            double2& b = bB(k0 + k);
+            const double2 wa = a, wb = b;
+            a = mk2(mu[k] * (d[k] * (wa.x * inv_len)) - flux_y(q, 2), mu[k] * (d[k] * (wa.y * inv_len)) - flux_y(q, 3));
+            b = mk2(mu[k] * (d[k] * (wb.x * inv_len)) - flux_y(q, 0), mu[k] * (d[k] * (wb.y * inv_len)) - flux_y(q, 1));
+        }
+    }
+    transform_all();
+    // epilogue: tA = iq2y D2 Phi_y (components 2, 3 from line A, 0, 1 from B)
+#pragma unroll 2
+    for (int k = 0; k < PPT; ++k) {
+        if (col(k) >= ncol) continue;
+        const long p = pt(k);
+        const double d = uq ? qc : ldg1(E.iq2y + p);
+        const double2 wa = bA(k), wb = bB(k);
+        E.tA[2][p] = d * (wa.x * inv_len);
+        E.tA[3][p] = d * (wa.y * inv_len);
+        E.tA[0][p] = d * (wb.x * inv_len);
+        E.tA[1][p] = d * (wb.y * inv_len);
+    }
+}
+
+#if FCSG_CUDA
+// pass X: CTA of kXWarps independent warps, each with two line buffers
+constexpr int kXWarps = 4;
+constexpr int kXThreads = kXWarps * 32;
+constexpr size_t kXSmem = kXWarps * 2 * kBP * sizeof(double2);
+// pass Y: CTA = one column quad (4 warps), 8 line buffers
+constexpr int kYThreads = kQuad * 32;
+constexpr size_t kYSmem = kQuad * 2 * kBP * sizeof(double2);
+
+__global__ void __launch_bounds__(kXThreads, 5) wpass_x_kernel(const __grid_constant__ EngineDev E,
+                                                               const double2* __restrict__ mult,
+                                                               const double* __restrict__ blend, int stage) {
+    extern __shared__ double2 wsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int line = blockIdx.x * kXWarps + warp;
+    if (line >= E.S * E.nj) return;
+    wpass_x_body<32>(lane, line, wsm + warp * 2 * kBP, mult, E, blend, stage);
+}
+
+__global__ void __launch_bounds__(kYThreads, 5) wpass_y_kernel(const __grid_constant__ EngineDev E,
+                                                               const double2* __restrict__ mult,
+                                                               const double* __restrict__ blend) {
+    extern __shared__ double2 wsm[];
+    wpass_y_quad<kYThreads>(threadIdx.x, blockIdx.x, wsm, mult, E, blend);
+}
+#endif
+
+bool wpass_applies(const EngineDev& E, const FcPlanDev& pl, bool rows) {
+    return pl.n_ext == 280 && pl.n == 256 && pl.n_gap == 24 && pl.dp1 == 3 && pl.mult_pfa != nullptr &&
+           (rows ? E.ni : E.nj) == 256;
+}
+
+void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage, void* stream) {
+    const int nlines = E.S * (rows ? E.nj : E.ni);
+    if (nlines == 0) return;
+    const double2* mult = pl.mult_pfa;  // mode 1: d/dq
+    const int nquads = E.S * ((E.ni + kQuad - 1) / kQuad);
+#if FCSG_CUDA
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static unsigned long long done = 0;
+    if (dev::first_on_device(&done)) {
+        cudaFuncSetAttribute(wpass_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kXSmem));
+        cudaFuncSetAttribute(wpass_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kYSmem));
+    }
+    if (rows)
+        wpass_x_kernel<<<(nlines + kXWarps - 1) / kXWarps, kXThreads, kXSmem, s>>>(E, mult, pl.blend, stage);
+    else
+        wpass_y_kernel<<<nquads, kYThreads, kYSmem, s>>>(E, mult, pl.blend);
+#else
+    (void)stream;
+    if (rows) {
+        std::vector<double2> buf(2 * kBP);
+        for (int line = 0; line < nlines; ++line) wpass_x_body<1>(0, line, buf.data(), mult, E, pl.blend, stage);
+    } else {
+        std::vector<double2> bufs(kQuad * 2 * kBP);
+        for (int q = 0; q < nquads; ++q) wpass_y_quad<1>(0, q, bufs.data(), mult, E, pl.blend);
+    }
+#endif
+}
+
+}  // namespace fcsg
