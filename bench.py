@@ -48,8 +48,8 @@ def peaks():
 
 
 # kernel behind each timed group (for the ncu capture lookup)
-GROUP_KERNEL = {"pass_a": "PassXc", "pass_b": "PassYc", "viscosity": "classify_mma_kernel"}
-GROUP_LB = {"pass_a": 2, "pass_b": 4}  # lines per block of the captured pass (256-point lines)
+GROUP_KERNEL = {"pass_a": "wpass_y_kernel", "pass_b": "wpass_x_kernel", "viscosity": "classify_mma_kernel"}
+GROUP_LB = {"pass_a": 4, "pass_b": 4}  # lines per block of the captured pass (256-point lines)
 
 
 def ncu_traffic(group, npts):
@@ -237,11 +237,13 @@ def run_reference(args):
 # input read once and every output written once; values produced and consumed
 # inside one kernel count zero. Stage passes in the default flux form; the
 # RK registers are those of stage 1 (the stage time_group launches): e0 read,
-# e2 written. Cartesian (every subpatch of the workload): pass X (rows) and
-# pass Y (cols), no third pass.
+# e2 written. Cartesian 256 x 256 subpatches (every subpatch of the workload):
+# the warp passes, pass Y first (columns: tA = iq2y D2 Phi_y), then pass X
+# (rows: rhs = tA + iq1x D1 Phi_x and the SSPRK update); the metrics are one
+# value per subpatch (uniform), the mask is read only for a failing point.
 ALG_BYTES_CART = {
-    "pass_a": 32 + 8 + 8 + 1 + 32,                # e, iq1x, mu, mask -> tA
-    "pass_b": 32 + 8 + 8 + 32 + 32 + 32 + 32,     # e, iq2y, mu, tA, e0 -> e2, e
+    "pass_a": 32 + 8 + 32,                        # e, mu -> tA
+    "pass_b": 32 + 8 + 32 + 32 + 32 + 32,         # e, mu, tA, e0 -> e, e2
     "pass_c": 0,
     "viscosity": 32 + 1 + 8 + 8 * 4,              # e, mask, h_max -> proxy, speed, tau, mu_hat (+ proxy re-read in L1)
     "filter": 32 + 32 + 32 + 32,                  # rows e -> tF ; cols tF -> e

@@ -296,6 +296,15 @@ void Engine::set_mlp_packed(const std::vector<double>& w) {
         dev::h2d(const_cast<double*>(E_.mlp), mlp_.data(), mlp_.size() * sizeof(double), ctx_.stream);
         const std::vector<double> fr = mlp_mma_fragments(mlp_);
         dev::h2d(const_cast<double*>(E_.mlp_frag), fr.data(), fr.size() * sizeof(double), ctx_.stream);
+        E_.cls_fast_margin = mlp_fast_margin(mlp_);
+        for (auto& g : G_) g.E.cls_fast_margin = E_.cls_fast_margin;
+        for (auto& cv : chunks_)
+            for (auto& c : cv) c.E.cls_fast_margin = E_.cls_fast_margin;
+        if (graph_exec_) {  // the captured launches hold the old margin by value
+            dev::graph_destroy(graph_exec_, graph_);
+            graph_exec_ = nullptr;
+            graph_ = nullptr;
+        }
     }
 }
 
@@ -519,6 +528,7 @@ void Engine::finalize() {
     {
         const std::vector<double> fr = mlp_mma_fragments(mlp_);
         E.mlp_frag = static_cast<const double*>(up(fr.data(), fr.size() * sizeof(double)));
+        E.cls_fast_margin = mlp_fast_margin(mlp_);
     }
     {
         std::vector<double> tt(kTanhTable);

@@ -1029,6 +1029,23 @@ FCSG_HD double tanh_tab(double x, const double* tab) {
 #endif
 }
 
+#if FCSG_CUDA
+// tanh on the FP32 pipe and the SFU (|error| <= 4e-7 absolute: ex2 and rcp
+// approximations, two roundings to float), for the classifier's fast pass:
+// the FP64 pipe stays with the DMMA layers. Only the argmax of the logits
+// is used, and the fast pass's result is kept only where its logit margin
+// exceeds EngineDev::cls_fast_margin, twice a rigorous bound of the logit
+// error this tanh can cause (mlp_fast_margin); elsewhere the group is
+// classified again with tanh_tab.
+__device__ __forceinline__ double tanh_fast(double z) {
+    const float x = __double2float_rn(z);
+    float t, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(2.8853900817779268f * fabsf(x)));  // e^(2|x|)
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t + 1.0f));
+    return static_cast<double>(copysignf(fmaf(-2.0f, r, 1.0f), x));  // 1 - 2 / (e^(2|x|) + 1)
+}
+#endif
+
 // normalize_stencil (src/viscosity.cpp:48-59): false = class-4 guard
 FCSG_HD bool normalize7(const double* s, double abs_floor, double* x) {
     double lo = s[0], hi = s[0];
@@ -1279,6 +1296,34 @@ FCSG_HD void classify_spectrum_body(Thr t, int block, int nblocks, const EngineD
 // P(ks, t) = 8 (ks / 2) + 2t + ks % 2 (the neuron this lane holds in its
 // register ks), so activations never leave the registers: the permutation is
 // folded into the B fragments here. Fragment f of lane l is fr[f * 32 + l].
+// Twice a rigorous bound of how far the fast pass's logits can be from
+// the exact pass's (tanh_fast within kEps of tanh_tab's values, tanh
+// 1-Lipschitz, identical inputs and layer arithmetic otherwise): the error
+// of layer l's activations is at most |W_l| (error of layer l-1) + kEps, the
+// logits' at most |W_out| times the last one. A fast margin above twice that
+// fixes the exact argmax. FCSG_EXACT_TANH=1 disables the fast pass.
+double mlp_fast_margin(const std::vector<double>& w) {
+    if (std::getenv("FCSG_EXACT_TANH")) return INFINITY;
+    constexpr double kEps = 1e-6;  // 2.5x the measured worst case of tanh_fast
+    const int rows[kMlpLayers] = {16, 16, 16, 16, 4}, cols[kMlpLayers] = {7, 16, 16, 16, 16};
+    std::vector<double> err(16, kEps), nxt;
+    int off = rows[0] * cols[0] + rows[0];
+    double bound = 0.0;
+    for (int l = 1; l < kMlpLayers; ++l) {
+        nxt.assign(rows[l], 0.0);
+        for (int n = 0; n < rows[l]; ++n) {
+            double a = 0.0;
+            for (int k = 0; k < cols[l]; ++k) a += std::fabs(w[off + n * cols[l] + k]) * err[k];
+            nxt[n] = a * (1.0 + 1e-12) + (l + 1 < kMlpLayers ? kEps : 0.0);
+            if (l + 1 == kMlpLayers) bound = std::max(bound, nxt[n]);
+        }
+        err = nxt;
+        off += rows[l] * cols[l] + rows[l];
+    }
+    if (!std::isfinite(bound)) return INFINITY;
+    return 2.0 * bound + 1e-9;
+}
+
 std::vector<double> mlp_mma_fragments(const std::vector<double>& w) {
     const int rows[kMlpLayers] = {16, 16, 16, 16, 4}, cols[kMlpLayers] = {7, 16, 16, 16, 16};
     int wo[kMlpLayers], bo[kMlpLayers];
@@ -1326,9 +1371,14 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // 2 (s - lo) / span - 1 are computed exactly as the reference's
 // (src/viscosity.cpp:48-59). The NG sets are interleaved so every thread has
 // 4 NG independent tanh chains per layer.
-template <int NG>
+template <int NG, bool FAST>
 __device__ void classify_mma(const double* fr, const double* tab, const double* s_a, const double* s_b,
-                             const bool* active, double abs_floor, int lane, int* cls) {
+                             const bool* active, double abs_floor, int lane, int* cls, bool* low = nullptr,
+                             double fast_margin = 0.0) {
+    auto act = [&](double z) {
+        if constexpr (FAST) return tanh_fast(z);
+        else return tanh_tab(z, tab);
+    };
     constexpr unsigned kAll = 0xffffffffu;
     const int t = lane & 3;
     const bool has_b = t < 3;
@@ -1373,7 +1423,7 @@ __device__ void classify_mma(const double* fr, const double* tab, const double* 
 #pragma unroll
     for (int g = 0; g < NG; ++g)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) h[g][k] = tanh_tab(h[g][k], tab);
+        for (int k = 0; k < 4; ++k) h[g][k] = act(h[g][k]);
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
         double z[NG][4];
@@ -1395,7 +1445,7 @@ __device__ void classify_mma(const double* fr, const double* tab, const double* 
 #pragma unroll
         for (int g = 0; g < NG; ++g)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) h[g][k] = tanh_tab(z[g][k], tab);
+            for (int k = 0; k < 4; ++k) h[g][k] = act(z[g][k]);
     }
     double d0[NG], d1[NG];
 #pragma unroll
@@ -1426,7 +1476,28 @@ __device__ void classify_mma(const double* fr, const double* tab, const double* 
         if (l3 > bv) best = 3;
         const int c = guard[g] ? 4 : best + 1;
         cls[g] = __shfl_sync(kAll, c, lane & ~3);
+        if constexpr (FAST) {
+            // margin top1 - top2 of the fast logits (lane t = 0 holds all four)
+            const double m1 = fmax(d0[g], d1[g]), n1 = fmin(d0[g], d1[g]);
+            const double m2 = fmax(l2, l3), n2 = fmin(l2, l3);
+            const double top = fmax(m1, m2), second = fmax(fmin(m1, m2), fmax(n1, n2));
+            const bool lw = !guard[g] && !(top - second > fast_margin);
+            low[g] = __shfl_sync(kAll, lw, lane & ~3);
+        }
     }
+}
+
+// classify_mma with the fast tanh, then exactly (tanh_tab) for the whole
+// warp when any of its stencils lands within the fast pass's error margin
+template <int NG>
+__device__ void classify_mma_checked(const double* fr, const double* tab, const double* s_a, const double* s_b,
+                                     const bool* active, double abs_floor, int lane, int* cls, double fast_margin) {
+    bool low[NG];
+    classify_mma<NG, true>(fr, tab, s_a, s_b, active, abs_floor, lane, cls, low, fast_margin);
+    bool any = false;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) any = any || low[g];
+    if (__any_sync(0xffffffffu, any)) classify_mma<NG, false>(fr, tab, s_a, s_b, active, abs_floor, lane, cls);
 }
 
 // window value k of this lane's stencil (row or column window of point (i, j))
@@ -1503,7 +1574,7 @@ __global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_
                 }
             }
             int c[2];
-            classify_mma<2>(fr, tab, sa, sb, act, E.abs_floor, lane, c);
+            classify_mma_checked<2>(fr, tab, sa, sb, act, E.abs_floor, lane, c, E.cls_fast_margin);
             write(w, minq(c[0]), minq(c[1]));
         }
         return;
@@ -1523,7 +1594,7 @@ __global__ void __launch_bounds__(kMmaThreads) classify_mma_kernel(const __grid_
             if (t < 3) sb[1] = window_at(E.proxy, wb.base, E.ni, col, wb.st, wb.i, wb.j, 4 + t);
         }
         int c[2];
-        classify_mma<2>(fr, tab, sa, sb, act, E.abs_floor, lane, c);
+        classify_mma_checked<2>(fr, tab, sa, sb, act, E.abs_floor, lane, c, E.cls_fast_margin);
         write(wa, minq(c[0]), 4);
         write(wb, minq(c[1]), 4);
     }

@@ -128,6 +128,7 @@ struct EngineDev {
     const double* mlp;       // kMlpWeights, FCNN order (per layer W row-major, then b)
     const double* mlp_frag;  // kMlpFrags x 32: per-lane DMMA operand fragments (mlp_mma_fragments)
     const double* tanh_tab;  // tanh(k/64), k = 0..1280 (classifier tanh table)
+    double cls_fast_margin;  // logit margin above which the fast-tanh class is exact (mlp_fast_margin)
     // classifier variant (ClassifierConfig::Variant, include/fcs/viscosity.hpp:45-52):
     // 0 = ann (the MLP), 1 = fallback (FC spectrum decay, window fb_window)
     int cls_variant;
@@ -173,6 +174,7 @@ struct GroupLaunch {
 constexpr int kMlpFrags = 50;
 constexpr int kTanhTable = 1281;  // tanh(k/64), k = 0..1280
 std::vector<double> mlp_mma_fragments(const std::vector<double>& packed);
+double mlp_fast_margin(const std::vector<double>& packed);
 
 int step_scr_cap(const FcPlanDev& pl);
 // warp-per-line Cartesian flux passes on the n_ext = 280 prime-factor
