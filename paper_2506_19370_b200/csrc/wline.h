@@ -58,9 +58,10 @@ FCSG_HD int slot_of(int i) {
 // (natural position i at slot_of(i), i < 256, already written and
 // synchronised by the caller): continuation (FcOperator::continuation,
 // src/fc_core.cpp:221-238: g_j = sum_i A[j][i] f[N-3+i] + sum_i A[23-j][i]
-// f[2-i], blend matrix A read through L1), forward PFA DFT, multiplier
+// f[2-i]), forward PFA DFT, multiplier
 // `mult` (280 double2 in (k1,k2,k3) order, k3 fastest), inverse PFA DFT.
-// Unnormalised like FFTW's c2r: the multiplier tables carry 1/n_ext. The
+// Unnormalised like FFTW's c2r: the multiplier tables carry 1/n_ext. blend
+// and mult are the kernels' shared-memory copies of the operator tables. The
 // butterflies of all lines share each stage's loop, so two lines per warp
 // fill 70 / 112 / 80 butterfly slots per stage instead of 35 / 56 / 40 (the
 // remainder iterations of one line leave most lanes idle). Ends
@@ -75,7 +76,7 @@ FCSG_HD void transform(int lane, double2* buf, int pitch, const double2* mult, c
         for (int i = 0; i < kD1; ++i) {
             const double2 fr = b[slot_of(kN - kD1 + i)];
             const double2 fl = b[slot_of(kD1 - 1 - i)];
-            const double cr = ldg1(blend + j * kD1 + i), cl = ldg1(blend + (kGap - 1 - j) * kD1 + i);
+            const double cr = blend[j * kD1 + i], cl = blend[(kGap - 1 - j) * kD1 + i];
             a = mk2(a.x + cr * fr.x, a.y + cr * fr.y);
             c = mk2(c.x + cl * fl.x, c.y + cl * fl.y);
         }
@@ -121,7 +122,7 @@ FCSG_HD void transform(int lane, double2* buf, int pitch, const double2* mult, c
         for (int q = 0; q < 7; ++q) x[q] = p[q];
         dft_odd<7, false>(x, nullptr, 7);
 #pragma unroll
-        for (int q = 0; q < 7; ++q) x[q] = cmul(x[q], ldg2(mk + q));
+        for (int q = 0; q < 7; ++q) x[q] = cmul(x[q], mk[q]);
         dft_odd<7, true>(x, nullptr, 7);
 #pragma unroll
         for (int q = 0; q < 7; ++q) p[q] = x[q];

@@ -16,6 +16,8 @@
 // Each warp's lane l owns the points i = l + 32 m (m < 8) of its line for
 // loads and epilogues (coalesced along rows), and the butterflies of the
 // transform (wline.h).
+#include <algorithm>
+
 #include "dev.h"
 #include "fc_lines.h"
 #include "pass_common.h"
@@ -86,11 +88,21 @@ FCSG_HD void pf_l2_bulk(const double* p, unsigned bytes) {
 #endif
 }
 
+// the operator tables a CTA keeps in shared memory: the multiplier (280
+// double2, prime-factor order) and the 24 x 3 blend matrix
+constexpr int kTabSlots = w280::kNE + (w280::kGap * w280::kD1 + 1) / 2;
+FCSG_HD void stage_w280_tables(int tid, int nthr, const double2* mult_src, const double* blend_src, double2* mult,
+                               double* blend) {
+    for (int k = tid; k < w280::kNE; k += nthr) mult[k] = ldg2(mult_src + k);
+    for (int k = tid; k < w280::kGap * w280::kD1; k += nthr) blend[k] = ldg1(blend_src + k);
+}
+
 // ---------------------------------------------------------------------------
 // FC line batch
 
 template <int NL>
-FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* mult, const FcLinesArgs& a) {
+FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* mult, const double* blend,
+                             const FcLinesArgs& a) {
     using namespace w280;
     const long l = 2 * pair;
     const long ls = a.line_stride, st = a.stride, ols = a.out_line_stride, ost = a.out_stride;
@@ -104,7 +116,7 @@ FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* m
         buf[slot_of(i)] = mk2(v0, v1);
     }
     FCSG_SYNCWARP();
-    transform<NL, 1>(lane, buf, kSlots, mult, a.pl.blend);
+    transform<NL, 1>(lane, buf, kSlots, mult, blend);
 #pragma unroll 4
     for (int m = 0; m < PPL; ++m) {
         const int i = lane + NL * m;
@@ -117,14 +129,16 @@ FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* m
 #if FCSG_CUDA
 __global__ void __launch_bounds__(kWThreads, 3) w280_lines_kernel(const __grid_constant__ FcLinesArgs a) {
     extern __shared__ double2 wsm[];
-    // the multiplier table (global, read through L1 by wline.h's ldg2)
-    const double2* mult = a.pl.mult_pfa + (a.mode - 1) * w280::kNE;
+    double2* mult = wsm;
+    double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
+    stage_w280_tables(threadIdx.x, kWThreads, a.pl.mult_pfa + (a.mode - 1) * w280::kNE, a.pl.blend, mult, blend);
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double2* buf = wsm + warp * w280::kSlots;
+    double2* buf = wsm + kTabSlots + warp * w280::kSlots;
     const long npairs = (a.n_lines + 1) / 2;
     for (long pair = static_cast<long>(blockIdx.x) * kWarps + warp; pair < npairs;
          pair += static_cast<long>(gridDim.x) * kWarps)
-        w280_lines_body<32>(lane, pair, buf, mult, a);
+        w280_lines_body<32>(lane, pair, buf, mult, blend, a);
 }
 #endif
 
@@ -136,7 +150,7 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream) {
     const long npairs = (a.n_lines + 1) / 2;
     if (npairs == 0) return;
 #if FCSG_CUDA
-    const size_t smem = kWarps * w280::kSlots * sizeof(double2);
+    const size_t smem = (kTabSlots + kWarps * w280::kSlots) * sizeof(double2);
     static unsigned long long done = 0;
     if (dev::first_on_device(&done))
         cudaFuncSetAttribute(w280_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -146,7 +160,7 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream) {
     (void)stream;
     std::vector<double2> buf(w280::kSlots);
     const double2* mult = a.pl.mult_pfa + (a.mode - 1) * w280::kNE;
-    for (long pair = 0; pair < npairs; ++pair) w280_lines_body<1>(0, pair, buf.data(), mult, a);
+    for (long pair = 0; pair < npairs; ++pair) w280_lines_body<1>(0, pair, buf.data(), mult, a.pl.blend, a);
 #endif
 }
 
@@ -403,26 +417,71 @@ FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult,
 // pass X: CTA of kXWarps independent warps, each with two line buffers
 constexpr int kXWarps = 4;
 constexpr int kXThreads = kXWarps * 32;
-constexpr size_t kXSmem = kXWarps * 2 * kBP * sizeof(double2);
+constexpr size_t kXSmem = (kTabSlots + kXWarps * 2 * kBP) * sizeof(double2);
 // pass Y: CTA = one column quad (4 warps), 8 line buffers
 constexpr int kYThreads = kQuad * 32;
-constexpr size_t kYSmem = kQuad * 2 * kBP * sizeof(double2);
+constexpr size_t kYSmem = (kTabSlots + kQuad * 2 * kBP) * sizeof(double2);
 
+// Both kernels are persistent (grid = resident CTAs): a CTA stages the
+// operator tables once and walks its work items, prefetching the next
+// item's state into L2 before it starts on the current one.
 __global__ void __launch_bounds__(kXThreads, 5) wpass_x_kernel(const __grid_constant__ EngineDev E,
-                                                               const double2* __restrict__ mult,
-                                                               const double* __restrict__ blend, int stage) {
+                                                               const double2* __restrict__ mult_src,
+                                                               const double* __restrict__ blend_src, int stage) {
     extern __shared__ double2 wsm[];
+    double2* mult = wsm;
+    double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
+    stage_w280_tables(threadIdx.x, kXThreads, mult_src, blend_src, mult, blend);
+    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int line = blockIdx.x * kXWarps + warp;
-    if (line >= E.S * E.nj) return;
-    wpass_x_body<32>(lane, line, wsm + warp * 2 * kBP, mult, E, blend, stage);
+    double2* buf = wsm + kTabSlots + warp * 2 * kBP;
+    const int nlines = E.S * E.nj;
+    const int stride = gridDim.x * kXWarps;
+    for (int line = blockIdx.x * kXWarps + warp; line < nlines; line += stride) {
+        const int nxt = line + stride;
+        if (nxt < nlines && lane < 4) {  // the next row's state (4 x 2 KB)
+            const int sub = nxt / E.nj, row = nxt - sub * E.nj;
+            pf_l2_bulk(E.e[lane] + static_cast<long>(sub) * E.ni * E.nj + static_cast<long>(row) * E.ni,
+                       w280::kN * sizeof(double));
+        }
+        wpass_x_body<32>(lane, line, buf, mult, E, blend, stage);
+    }
 }
 
 __global__ void __launch_bounds__(kYThreads, 5) wpass_y_kernel(const __grid_constant__ EngineDev E,
-                                                               const double2* __restrict__ mult,
-                                                               const double* __restrict__ blend) {
+                                                               const double2* __restrict__ mult_src,
+                                                               const double* __restrict__ blend_src) {
     extern __shared__ double2 wsm[];
-    wpass_y_quad<kYThreads>(threadIdx.x, blockIdx.x, wsm, mult, E, blend);
+    double2* mult = wsm;
+    double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
+    stage_w280_tables(threadIdx.x, kYThreads, mult_src, blend_src, mult, blend);
+    const int qps = (E.ni + kQuad - 1) / kQuad;
+    const int nquads = E.S * qps;
+    for (int quad = blockIdx.x; quad < nquads; quad += gridDim.x) {
+        const int nxt = quad + gridDim.x;
+        if (nxt < nquads) {  // the next quad's state: one 32-byte sector per row and component
+            const int sub = nxt / qps, c0 = (nxt - sub * qps) * kQuad;
+            const long gb = static_cast<long>(sub) * E.ni * E.nj + c0;
+            for (int r = threadIdx.x; r < 4 * w280::kN; r += kYThreads)
+                pf_l2(E.e[r >> 8] + gb + static_cast<long>(r & (w280::kN - 1)) * E.ni);
+        }
+        __syncthreads();  // tables staged; the previous quad's buffers consumed
+        wpass_y_quad<kYThreads>(threadIdx.x, quad, wsm + kTabSlots, mult, E, blend);
+    }
+}
+
+// resident CTAs of a kernel (grid of the persistent launches), per device
+template <class K>
+int resident_ctas(K kernel, int threads, size_t smem, unsigned long long* done, int* cache) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (dev::first_on_device(done)) {
+        int sms = 0, per = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+        cache[d & 63] = sms * (per > 0 ? per : 1);
+    }
+    return cache[d & 63];
 }
 #endif
 
@@ -438,15 +497,20 @@ void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage,
     const int nquads = E.S * ((E.ni + kQuad - 1) / kQuad);
 #if FCSG_CUDA
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    static unsigned long long done = 0;
+    static unsigned long long done = 0, occ_x = 0, occ_y = 0;
+    static int res_x[64], res_y[64];
     if (dev::first_on_device(&done)) {
         cudaFuncSetAttribute(wpass_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kXSmem));
         cudaFuncSetAttribute(wpass_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kYSmem));
     }
-    if (rows)
-        wpass_x_kernel<<<(nlines + kXWarps - 1) / kXWarps, kXThreads, kXSmem, s>>>(E, mult, pl.blend, stage);
-    else
-        wpass_y_kernel<<<nquads, kYThreads, kYSmem, s>>>(E, mult, pl.blend);
+    if (rows) {
+        const int need = (nlines + kXWarps - 1) / kXWarps;
+        const int grid = std::min(need, resident_ctas(wpass_x_kernel, kXThreads, kXSmem, &occ_x, res_x));
+        wpass_x_kernel<<<grid, kXThreads, kXSmem, s>>>(E, mult, pl.blend, stage);
+    } else {
+        const int grid = std::min(nquads, resident_ctas(wpass_y_kernel, kYThreads, kYSmem, &occ_y, res_y));
+        wpass_y_kernel<<<grid, kYThreads, kYSmem, s>>>(E, mult, pl.blend);
+    }
 #else
     (void)stream;
     if (rows) {
