@@ -78,9 +78,17 @@ FCSG_HD void pf_l2(const double* p) {
     (void)p;
 #endif
 }
-// L2 prefetch of a contiguous range (multiple of 16 bytes, 16-byte aligned)
+// L2 prefetch of a contiguous range (bytes a multiple of 16). The bulk
+// prefetch needs a 16-byte aligned start; a group view's fields start at the
+// group's first point, which is only 8-byte aligned after a group with an odd
+// number of points -- then the range is prefetched from its first aligned byte.
 FCSG_HD void pf_l2_bulk(const double* p, unsigned bytes) {
 #if FCSG_CUDA
+    const unsigned long long a = reinterpret_cast<unsigned long long>(p);
+    if (a & 15) {
+        p += 1;
+        bytes -= 16;
+    }
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 #else
     (void)p;
