@@ -36,6 +36,7 @@ UNIT = "pt-stage/s"
 # paper Table 2, one 54-core Xeon node, weak/refinement N=550,854
 PAPER_1NODE = 6.74e7
 R_TILES, S_TILES = 8, 8
+STRONG_TILES = (32, 16)  # strong scaling: 512 subpatches of 256x256 (33.5M points) in total
 
 
 def peaks():
@@ -201,8 +202,12 @@ def cpu_rate(steps, warmup, threads):
     return 5.0 * npts * n / wall, wall / max(n, 1), npts
 
 
-def workload_name(n_subs_total=None):
+def workload_name(n_subs_total=None, strong=False):
     """the config-5 weak-scaling workload as both arms name it"""
+    if strong:
+        return (f"config5-strong: {STRONG_TILES[0]}x{STRONG_TILES[1]} tiles of 256x256 ({n_subs_total} subpatches, "
+                f"{STRONG_TILES[0] * STRONG_TILES[1] * 65536} points) split in contiguous blocks over the GPUs, "
+                f"19-point overlap, vortex + 1e-3 noise, ANN classifier, CFL 0.5")
     block = "" if n_subs_total is None else f" (one block of a {n_subs_total}-subpatch tiling, NCCL halo exchange)"
     return (f"config5-weak: {R_TILES}x{S_TILES} tiles of 256x256 per GPU{block} ({R_TILES * S_TILES * 65536} "
             f"points/GPU, 19-point overlap), vortex + 1e-3 noise, ANN classifier, CFL 0.5")
@@ -416,30 +421,33 @@ def run_fcsg(args):
 
     ctx = N.Context(local)
     DE = None
+    strong = args.scaling == "strong"
     if world > 1:
-        # weak scaling: an (8 px) x (8 py) tiling, one contiguous 8x8 block per
-        # rank; halo copies over NCCL send/recv, dt by all-reduce(MIN)
+        # weak: an (8 py) x (8 px) tiling, one contiguous 8x8 block per rank;
+        # strong: the 32 x 16 tiling (512 subpatches) split into world blocks.
+        # The engine's own transport: halo pack -> grouped ncclSend/Recv to the
+        # neighbour ranks -> unpack, and ncclAllReduce(MIN) of dt, all on the
+        # engine stream inside the superstep (one CUDA graph per step)
         from paper_2506_19370_b200 import distributed as D, problems as P
 
-        px = max(p for p in range(1, world + 1) if world % p == 0 and p * p <= world)
-        py = world // px
-        dec, ic, _ = P.vortex_tiles(r=R_TILES * py, s=S_TILES * px)
+        if strong:
+            dec, ic, _ = P.vortex_tiles(r=STRONG_TILES[0], s=STRONG_TILES[1])
+        else:
+            px = max(p for p in range(1, world + 1) if world % p == 0 and p * p <= world)
+            py = world // px
+            dec, ic, _ = P.vortex_tiles(r=R_TILES * py, s=S_TILES * px)
         owner = D.partition_tiles(dec, world)
         rp = D.split_plan(dec, owner, rank, world)
-        DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5))
+        DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5), transport="native")
         E = DE.E
     else:
-        dec, ic, _ = workload()
+        dec, ic, _ = workload(STRONG_TILES if strong else (R_TILES, S_TILES))
         E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5))
     npts = E.total_points()
     stream = torch.cuda.ExternalStream(E.stream(), device=local)
 
     def steps(n):
-        if DE is not None:
-            for _ in range(n):
-                DE.step()
-        else:
-            E.enqueue(n)
+        E.enqueue(n)  # graph replays; multi-rank halos and the dt all-reduce inside
 
     # warm-up (includes the t=0 smear step and the CUDA-graph capture)
     steps(max(args.warmup, 3))
@@ -461,7 +469,12 @@ def run_fcsg(args):
     t_now, steps_done = E.time()
     E.check_error()  # surfaces a device-side InvalidStateError, if any
     ms_step = ms_total / args.steps
-    value = 5.0 * npts * world * args.steps / (ms_total * 1e-3)
+    npts_all = npts
+    if world > 1:
+        t = torch.tensor([npts], device="cuda", dtype=torch.int64)
+        dist.all_reduce(t)
+        npts_all = int(t.item())
+    value = 5.0 * npts_all * args.steps / (ms_total * 1e-3)
 
     # e2e through the public API with HOST buffers: per step, H2D of the state
     # from pinned memory, one superstep (fcsg_engine_run, which also checks the
@@ -469,28 +482,22 @@ def run_fcsg(args):
     host_in = torch.empty((4, npts), dtype=torch.float64, pin_memory=True)
     host_out = torch.empty((4, npts), dtype=torch.float64, pin_memory=True)
     E.get_state_bulk(host_in)
-    if DE is None:  # untimed warm-up: run_host allocates its staging buffers on first use
-        E.run_host(host_in, host_out, steps=1)
+    E.run_host(host_in, host_out, steps=1)  # untimed: run_host allocates its staging buffers on first use
     e2e_steps = max(2, min(4 * args.steps, 40))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
-    if DE is not None:
-        for _ in range(e2e_steps):
-            E.set_state_bulk(host_in)
-            DE.run(1)
-            E.get_state_bulk(host_out)
-    else:
-        # fcsg_engine_run_host: per step the H2D of its input and the D2H of
-        # its result, pipelined against the neighbouring steps' kernels
-        assert E.run_host(host_in, host_out, steps=e2e_steps) == e2e_steps
+    # fcsg_engine_run_host: per step the H2D of its input and the D2H of its
+    # result, pipelined against the neighbouring steps' kernels (multi-rank:
+    # the same call on every rank, the halos inside each step)
+    assert E.run_host(host_in, host_out, steps=e2e_steps) == e2e_steps
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = 5.0 * npts * world * e2e_steps / e2e_s
+    e2e = 5.0 * npts_all * e2e_steps / e2e_s
     nbytes = 4 * npts * 8
 
     # per-kernel-group device time (profiling hook, same engine and stream)
@@ -528,17 +535,21 @@ def run_fcsg(args):
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": value / PAPER_1NODE,
         "vs_baseline_basis": "PAPER.md:1612 (BASELINE.md): 6.74e7 pt-stage/s, one 54-core Xeon 8273 node",
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(None if world == 1 else len(dec.subs)),
-                   "points_per_gpu": npts, "l2": "working set ~1.7 GB/GPU >> 126 MB L2 (no flush needed)",
-                   "cuda_graph": world == 1, "parallelism": f"subpatch blocks x{world}", "stage_passes": "cartesian" if E.is_cartesian() else "general"},
+        "config": {"workload": workload_name(None if world == 1 and not strong else len(dec.subs), strong),
+                   "points_per_gpu": npts, "points_total": npts_all,
+                   "l2": f"working set ~{47 * 8 * npts / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)",
+                   "cuda_graph": True, "parallelism": f"subpatch blocks x{world}",
+                   "transport": "none" if world == 1 else "engine stream: pack + grouped ncclSend/Recv + unpack, ncclAllReduce(MIN) dt, no host sync",
+                   "stage_passes": "cartesian" if E.is_cartesian() else "general"},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-                "steps": e2e_steps, "path": ("fcsg_engine_run_host (per step: H2D of the state from pinned memory, one superstep, D2H of "
-                         "the result; copies on two copy streams overlap the neighbouring steps)" if DE is None else
-                         "fcsg_engine_set_state_bulk + fcsg_engine_run + fcsg_engine_get_state_bulk")},
+                "steps": e2e_steps, "path": "fcsg_engine_run_host (per step: H2D of the state from pinned memory, one superstep, D2H of "
+                         "the result; copies on two copy streams overlap the neighbouring steps)",
+                "note": "each step re-uploads the same input (in_stride 0), so step k+1's upload does not wait for step k's "
+                        "result; a time-marching driver that feeds each output back in cannot overlap its copies this way"},
         "gpu_launches": E.launches_per_step() * args.steps,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
@@ -569,6 +580,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fcsg", choices=["fcsg", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: 64 subpatches per GPU (default); strong: 512 subpatches in total")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

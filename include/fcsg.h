@@ -94,8 +94,9 @@ int fcsg_fc_lines_host(fcsg_ctx* ctx, int op_id, int mode, const double* h_in, l
  * src/runtime.cpp:316-530) for subpatches whose init-time data
  * (SubpatchData geometry/masks/metrics/line BCs, init_subpatch_data,
  * src/subpatch_data.cpp:69-154; CommPlan, build_plan, src/runtime.cpp:89-274)
- * is built by the caller and uploaded once. All subpatches of one engine
- * share one rectangular shape ni x nj. */
+ * is built by the caller and uploaded once. Subpatches may have different
+ * shapes (ni x nj, with an L-cut for corner patches); the engine stores them
+ * grouped by shape and runs each group's line passes on its own plans. */
 typedef struct fcsg_engine fcsg_engine;
 
 /* EngineConfig (include/fcs/runtime.hpp:59-73) fields used by the step */
@@ -276,6 +277,25 @@ int fcsg_engine_dtmin_ptr(fcsg_engine* eng, void** dptr);
 /* 8-byte device copy of that minimum to (to_engine = 0) or from (1) a
  * caller buffer, ordered on the engine stream */
 int fcsg_engine_copy_dtmin(fcsg_engine* eng, void* d_buf, int to_engine);
+/* ---- device-ordered multi-rank transport ----------------------------------
+ * Replaces the caller-driven parts above with the engine's own transport:
+ * after fcsg_engine_attach_comm every superstep the engine enqueues
+ * (fcsg_engine_finish_ic, _phase / _reduce_dt, _run, _enqueue, _run_host)
+ * packs its halos, exchanges them with the neighbour ranks only (grouped
+ * ncclSend / ncclRecv over NVLink) and all-reduces the dt minimum
+ * (ncclAllReduce MIN on its bits) on the engine stream, with no host
+ * synchronisation, so a steady multi-rank superstep is one CUDA graph.
+ * Stands for the reference's barriers and cross-worker reads
+ * (src/runtime.cpp:352-371, 433-454, 482-512).
+ * fcsg_comm_unique_id: a rendezvous id (ncclUniqueId, 128 bytes) made on rank
+ * 0 and broadcast by the caller. fcsg_engine_attach_comm (collective, after
+ * finalize and the halo lists): peers = the other ranks this one exchanges
+ * with, ascending; per peer the number of values (points) in the packed send
+ * and receive buffers of the state and mu_hat halos, in that peer order (the
+ * sums equal fcsg_engine_halo_size 0..3). */
+int fcsg_comm_unique_id(char* id);
+int fcsg_engine_attach_comm(fcsg_engine* eng, int nranks, int rank, const char* id, int n_peers, const int* peers,
+                            const long* e_send, const long* e_recv, const long* mu_send, const long* mu_recv);
 /* synchronise the engine stream and raise a pending device-side error */
 int fcsg_engine_check_error(fcsg_engine* eng);
 

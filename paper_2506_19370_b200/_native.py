@@ -122,6 +122,9 @@ def _declare(L):
     L.fcsg_engine_copy_dtmin.argtypes = [vp, vp, C.c_int]
     L.fcsg_engine_time_group.argtypes = [vp, C.c_int, C.c_int, dp]
     L.fcsg_engine_launches_per_step.argtypes = [vp, ip]
+    L.fcsg_comm_unique_id.argtypes = [C.c_char_p]
+    lp = C.POINTER(C.c_long)
+    L.fcsg_engine_attach_comm.argtypes = [vp, C.c_int, C.c_int, C.c_char_p, C.c_int, ip, lp, lp, lp, lp]
     return L
 
 

@@ -25,7 +25,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
 CU_SOURCES = ["dev.cu", "fc_lines.cu", "step_kernels.cu", "wpass.cu"]
-CPP_SOURCES = ["fc_tables.cpp", "capi.cpp", "engine.cpp"]
+CPP_SOURCES = ["fc_tables.cpp", "capi.cpp", "engine.cpp", "comm.cpp"]
 
 
 def _run(cmd):
@@ -84,9 +84,9 @@ def build(emulate: bool = False, verbose: bool = False, force: bool = False) -> 
                 sys.stderr.write(r.stderr)
     if force or _stale(lib, objs):
         if emulate:
-            _run(["g++", "-shared", "-o", lib, *objs, "-lquadmath", "-lpthread"])
+            _run(["g++", "-shared", "-o", lib, *objs, "-lquadmath", "-lpthread", "-lrt"])
         else:
-            _run([NVCC, ARCH, "-shared", "-o", lib, *objs, "-lquadmath", "-cudart", "static"])
+            _run([NVCC, ARCH, "-shared", "-o", lib, *objs, "-lquadmath", "-ldl", "-cudart", "static"])
     return lib
 
 

@@ -576,6 +576,32 @@ int fcsg_engine_dtmin_ptr(fcsg_engine* e, void** dptr) {
     return guard(e->ctx, [&] { *dptr = e->eng->dtmin_device_ptr(); });
 }
 
+int fcsg_comm_unique_id(char* id) {
+    if (!id) return FCSG_USAGE;
+    try {  // no context (and no device switch): rank 0 calls this before any engine exists
+        comm_unique_id(id);
+        return FCSG_OK;
+    } catch (const Error& e) {
+        return e.kind;
+    } catch (...) {
+        return FCSG_OTHER;
+    }
+}
+
+int fcsg_engine_attach_comm(fcsg_engine* e, int nranks, int rank, const char* id, int n_peers, const int* peers,
+                            const long* e_send, const long* e_recv, const long* mu_send, const long* mu_recv) {
+    if (!e) return FCSG_USAGE;
+    return guard(e->ctx, [&] {
+        if (!id || n_peers < 0 || (n_peers > 0 && !(peers && e_send && e_recv && mu_send && mu_recv)))
+            throw Error(kUsage, "bad transport arguments");
+        auto vl = [n_peers](const long* p) { return std::vector<long>(p, p + n_peers); };
+        std::vector<int> pv(peers, peers + n_peers);
+        dev::set_device(e->ctx->device);
+        auto comm = comm_create(nranks, rank, id);
+        e->eng->attach_comm(std::move(comm), pv, vl(e_send), vl(e_recv), vl(mu_send), vl(mu_recv));
+    });
+}
+
 int fcsg_engine_check_error(fcsg_engine* e) {
     if (!e) return FCSG_USAGE;
     return guard(e->ctx, [&] {

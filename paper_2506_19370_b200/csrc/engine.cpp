@@ -1,9 +1,9 @@
 // Host Engine (see engine.h). Device layout: every per-point field is one
 // contiguous array over all subpatches, [sub][j][i] (the reference's Field
 // order, include/fcs/field.hpp:9-23), so a subpatch is a (nj, ni) slab and a
-// point has the global index sub*ni*nj + j*ni + i. All subpatches of one
-// engine share one rectangular shape (every configuration measured here);
-// the FC operators for rows (n = ni) and columns (n = nj) are shared too.
+// point has the global index sub*ni*nj + j*ni + i. Subpatches of any shapes
+// are stored grouped by shape (layout()); each group shares its row and
+// column FC operators.
 #include "engine.h"
 
 #include <algorithm>
@@ -261,6 +261,70 @@ void Engine::pack_mu(double* d_buf) {
     launch_pack(E_, 1, d_halo_mu_, static_cast<long>(halo_mu_.size()), hp_[1], d_buf, ctx_.stream);
 }
 void Engine::unpack_mu(const double* d_buf) { launch_unpack(E_, 1, n_recv_mu_, d_buf, ctx_.stream); }
+
+void Engine::attach_comm(std::unique_ptr<Comm> comm, std::vector<int> peers, std::vector<long> e_send,
+                         std::vector<long> e_recv, std::vector<long> mu_send, std::vector<long> mu_recv) {
+    if (!finalized_) throw Error(kUsage, "attach the transport after finalize");
+    if (comm_) throw Error(kUsage, "transport already attached");
+    const size_t np = peers.size();
+    if (e_send.size() != np || e_recv.size() != np || mu_send.size() != np || mu_recv.size() != np)
+        throw Error(kUsage, "per-peer count lists must match the peer list");
+    for (size_t k = 0; k < np; ++k) {
+        if (peers[k] < 0 || peers[k] >= comm->size() || peers[k] == comm->rank() || (k && peers[k] <= peers[k - 1]))
+            throw Error(kUsage, "peers must be distinct other ranks in ascending order");
+        if (e_send[k] < 0 || e_recv[k] < 0 || mu_send[k] < 0 || mu_recv[k] < 0) throw Error(kUsage, "negative count");
+    }
+    const long want[4] = {static_cast<long>(halo_e_.size()), n_recv_e_, static_cast<long>(halo_mu_.size()),
+                          n_recv_mu_};
+    std::vector<long>* cnt[4] = {&e_send, &e_recv, &mu_send, &mu_recv};
+    for (int w = 0; w < 4; ++w) {
+        long sum = 0;
+        for (long c : *cnt[w]) sum += c;
+        if (sum != want[w]) throw Error(kUsage, "per-peer counts do not add up to the halo sizes");
+        wire_cnt_[w] = *cnt[w];
+        const long vals = (w < 2 ? 4 : 1) * std::max(sum, 1L);
+        d_wire_[w] = dev::alloc_n<double>(vals);
+        allocs_.push_back(d_wire_[w]);
+    }
+    peers_ = std::move(peers);
+    comm_ = std::move(comm);
+    if (graph_exec_) {  // a captured step without the transport
+        dev::graph_destroy(graph_exec_, graph_);
+        graph_exec_ = nullptr;
+        graph_ = nullptr;
+    }
+}
+
+// One halo of the multi-rank step, enqueued on `stream` (no host sync):
+// pack the donor values this rank owes its peers (6x6 interpolations whose
+// stencil lives here evaluated while packing), one grouped send / recv to the
+// neighbour ranks, unpack into the halo slots the plan addresses with
+// src_sub = -1. Buffers are per-peer slices in ascending peer order, the
+// order both sides' plan split walked (distributed.split_plan).
+void Engine::halo(int which, void* stream) {
+    if (!comm_) return;
+    const int width = which == 0 ? 4 : 1;
+    double* snd = d_wire_[which == 0 ? 0 : 2];
+    double* rcv = d_wire_[which == 0 ? 1 : 3];
+    const std::vector<long>& cs = wire_cnt_[which == 0 ? 0 : 2];
+    const std::vector<long>& cr = wire_cnt_[which == 0 ? 1 : 3];
+    if (which == 0) launch_pack(E_, 0, d_halo_e_, static_cast<long>(halo_e_.size()), hp_[0], snd, stream);
+    else launch_pack(E_, 1, d_halo_mu_, static_cast<long>(halo_mu_.size()), hp_[1], snd, stream);
+    comm_->group_start();
+    long os = 0, orv = 0;
+    for (size_t k = 0; k < peers_.size(); ++k) {
+        if (cs[k]) comm_->send(snd + width * os, static_cast<size_t>(width * cs[k]), peers_[k]);
+        if (cr[k]) comm_->recv(rcv + width * orv, static_cast<size_t>(width * cr[k]), peers_[k]);
+        os += cs[k];
+        orv += cr[k];
+    }
+    comm_->group_end(stream);
+    launch_unpack(E_, which, which == 0 ? n_recv_e_ : n_recv_mu_, rcv, stream);
+}
+
+void Engine::reduce_dtmin(void* stream) {
+    if (comm_) comm_->allreduce_min_u64(&E_.sc->dtmin_bits, stream);
+}
 
 void Engine::enqueue_part(int part, int stage) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
@@ -756,6 +820,10 @@ int Engine::launches_per_step() const {
         n -= 5 * (stage_launches(G_) + static_cast<int>(G_.size()));
         for (const auto& c : chunks_) n += 5 * (stage_launches(c) + 1);
     }
+    if (comm_) {  // pack / unpack kernels of the halos (NCCL's own kernels not counted)
+        n += (halo_mu_.empty() ? 0 : 1) + (n_recv_mu_ ? 1 : 0);
+        n += 5 * ((halo_e_.empty() ? 0 : 1) + (n_recv_e_ ? 1 : 0));
+    }
     return n;
 }
 
@@ -976,6 +1044,7 @@ void Engine::check_error() {
 
 void Engine::finish_ic() {
     launch_bc(G_, ctx_.stream);
+    halo(0, ctx_.stream);
     launch_exchange(E_, ctx_.stream);
     dev::check("finish_ic");
     dev::sync(ctx_.stream);
@@ -985,7 +1054,10 @@ void Engine::phase(int ph, int stage) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
     switch (ph) {
         case 0: launch_phase0(E_, G_, host_step_ == 0, ctx_.stream); break;
-        case 1: launch_phase1(E_, ctx_.stream); break;
+        case 1:
+            halo(1, ctx_.stream);
+            launch_phase1(E_, ctx_.stream);
+            break;
         case 2:
             launch_phase2(G_, host_step_ == 0, ctx_.stream);
             launch_bc(G_, ctx_.stream);
@@ -995,7 +1067,10 @@ void Engine::phase(int ph, int stage) {
             launch_stage(G_, stage, ctx_.stream);
             launch_bc(G_, ctx_.stream);
             break;
-        case 6: launch_exchange(E_, ctx_.stream); break;
+        case 6:
+            halo(0, ctx_.stream);
+            launch_exchange(E_, ctx_.stream);
+            break;
         default: throw Error(kUsage, "bad phase");
     }
     dev::check("phase");
@@ -1004,6 +1079,7 @@ void Engine::phase(int ph, int stage) {
 }
 
 double Engine::reduce_dt() {
+    reduce_dtmin(ctx_.stream);
     launch_finalize_dt(E_, ctx_.stream);
     dev::check("finalize_dt");
     StepScalars sc;
@@ -1059,7 +1135,9 @@ void Engine::enqueue_step(bool step0) {
         }
         for (int k = 0; k < ns; ++k) dev::record(cevents_[k], cstreams_[k]);
         for (int k = 0; k < half; ++k) dev::wait(s, cevents_[k]);
+        halo(1, s);
         launch_phase1(E_, s);
+        reduce_dtmin(s);
         for (int k = half; k < ns; ++k) dev::wait(s, cevents_[k]);
     } else {
         if (fork && !side_) {
@@ -1075,7 +1153,9 @@ void Engine::enqueue_step(bool step0) {
             dev::record(ev_join_, side_);
         }
         launch_classify(E_, G_, step0, s);
+        halo(1, s);
         launch_phase1(E_, s);
+        reduce_dtmin(s);
         if (fork) dev::wait(s, ev_join_);
         else launch_phase2(G_, step0, s);
     }
@@ -1105,6 +1185,7 @@ void Engine::enqueue_step(bool step0) {
             launch_stage(G_, st, s);
             launch_bc(G_, s);
         }
+        halo(0, s);
         launch_exchange(E_, s);
     }
     launch_advance(E_, s);

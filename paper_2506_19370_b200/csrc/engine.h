@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "context.h"
 #include "fc_tables.h"
 #include "step_kernels.h"
@@ -85,6 +86,14 @@ class Engine {
     void pack_mu(double* d_buf);
     void unpack_mu(const double* d_buf);
     long halo_size(int which) const;     // 0 send e, 1 recv e, 2 send mu, 3 recv mu
+    // Device-ordered multi-rank transport (after finalize): the halos and the
+    // dt minimum are then part of every superstep the engine enqueues
+    // (finish_ic, phase / reduce_dt, enqueue_step, hence the CUDA graph).
+    // peers in wire order (ascending rank) with the per-peer value counts of
+    // the packed send / receive buffers (sums = the set_halo sizes).
+    void attach_comm(std::unique_ptr<Comm> comm, std::vector<int> peers, std::vector<long> e_send,
+                     std::vector<long> e_recv, std::vector<long> mu_send, std::vector<long> mu_recv);
+    bool has_comm() const { return comm_ != nullptr; }
     // one part of a superstep (multi-rank driver): 0 viscosity, 1 blend + dt
     // minimum, 2 filter/smear + BC + dt, 3 stage `stage` (passes + BC),
     // 4 exchange copies, 5 advance
@@ -192,6 +201,14 @@ class Engine {
         std::vector<double> w;
     } hi_[2];
     HaloPackDev hp_[2]{};
+    // attached transport: peers, per-peer counts (0 e send, 1 e recv, 2 mu
+    // send, 3 mu recv) and the device wire buffers
+    std::unique_ptr<Comm> comm_;
+    std::vector<int> peers_;
+    std::vector<long> wire_cnt_[4];
+    double* d_wire_[4] = {nullptr, nullptr, nullptr, nullptr};
+    void halo(int which, void* stream);  // pack -> grouped send / recv -> unpack (which 0 = e, 1 = mu_hat)
+    void reduce_dtmin(void* stream);     // all-reduce(MIN) of the dt minimum's bits
     long host_step_ = 0;
     void* graph_exec_ = nullptr;
     void* graph_ = nullptr;

@@ -1037,12 +1037,23 @@ FCSG_HD double tanh_tab(double x, const double* tab) {
 // exceeds EngineDev::cls_fast_margin, twice a rigorous bound of the logit
 // error this tanh can cause (mlp_fast_margin); elsewhere the group is
 // classified again with tanh_tab.
+//
+// The double <-> float conversions are done on the integer bits (ALU pipe)
+// instead of F2F, which issues on the same XU pipe as the two MUFU ops and
+// made it the classifier's limiter: |z| is truncated to float (relative error
+// 2^-23, i.e. <= 6e-8 absolute on tanh; |z| < 2^-126 becomes 0, |z| > 2^128
+// FLT_MAX), the result in [0, 1] is widened exactly.
 __device__ __forceinline__ double tanh_fast(double z) {
-    const float x = __double2float_rn(z);
+    const unsigned hi = static_cast<unsigned>(__double2hiint(z)), lo = static_cast<unsigned>(__double2loint(z));
+    int a = static_cast<int>(hi & 0x7fffffffu) - 0x38000000;  // exponent bias 1023 -> 127
+    a = min(max(a, 0), 0x0fefffff);
+    const float ax = __uint_as_float((static_cast<unsigned>(a) << 3) | (lo >> 29));
     float t, r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(2.8853900817779268f * fabsf(x)));  // e^(2|x|)
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(2.8853900817779268f * ax));  // e^(2|x|)
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t + 1.0f));
-    return static_cast<double>(copysignf(fmaf(-2.0f, r, 1.0f), x));  // 1 - 2 / (e^(2|x|) + 1)
+    const unsigned yb = __float_as_uint(fmaxf(fmaf(-2.0f, r, 1.0f), 0.0f));  // tanh |x| = 1 - 2 / (e^(2|x|) + 1)
+    const unsigned dhi = yb == 0u ? 0u : (yb >> 3) + 0x38000000u;
+    return __hiloint2double(static_cast<int>(dhi | (hi & 0x80000000u)), static_cast<int>(yb << 29));
 }
 #endif
 

@@ -22,9 +22,21 @@ block edges cross ranks) and:
 
 Every per-subpatch computation is local and min is exact, so the result is
 bitwise independent of the number of ranks (interpolations are evaluated
-with the same arithmetic on whichever rank holds the donor). Transport is torch.distributed:
-NCCL over NVLink on GPUs, gloo for the CPU tests (which drive the same engine
-code through the emulation build).
+with the same arithmetic on whichever rank holds the donor).
+
+Two transports:
+
+* ``"native"`` (default): the engine's own (``fcsg_engine_attach_comm``,
+  csrc/comm.cpp). Pack, grouped ncclSend/ncclRecv to the neighbour ranks,
+  unpack and ncclAllReduce(MIN) are enqueued on the engine stream inside the
+  superstep -- no host synchronisation -- so a steady multi-rank superstep is
+  one CUDA graph replay. torch.distributed only broadcasts the NCCL unique
+  id. In the CPU tests the emulation build runs the same engine code over
+  shared-memory mailboxes.
+* ``"torch"``: the caller-driven parts (``fcsg_engine_enqueue_part`` +
+  ``pack``/``unpack``) with torch.distributed point-to-point between them
+  (gloo in the CPU tests; with host staging when gloo carries CUDA ranks).
+  Kept as the reference for the native path: both must agree bitwise.
 """
 from __future__ import annotations
 
@@ -220,14 +232,18 @@ def partition_subpatches(dec, world: int) -> np.ndarray:
 class DistributedEngine:
     """One rank of a multi-GPU superstep (see the module docstring)."""
 
-    def __init__(self, ctx, dec, rank_plan: RankPlan, ic=None, cfg=None, initial_states=None, group=None):
+    def __init__(self, ctx, dec, rank_plan: RankPlan, ic=None, cfg=None, initial_states=None, group=None,
+                 transport="native"):
         import torch
 
         from . import engine as EN
         from . import problems as P
 
+        if transport not in ("native", "torch"):
+            raise ValueError(f"unknown transport {transport!r}")
         self.rp = rank_plan
         self.group = group
+        self.transport = transport
         self.device = torch.device("cpu") if ctx.emulate else torch.device("cuda", torch.cuda.current_device())
         cfg = cfg or EN.EngineConfig()
         if initial_states is None and ic is not None:
@@ -243,10 +259,42 @@ class DistributedEngine:
         self.buf = {"e_send": f(4 * self.n[0]), "e_recv": f(4 * self.n[1]), "mu_send": f(self.n[2]),
                     "mu_recv": f(self.n[3])}
         self.dtmin = torch.zeros(1, dtype=torch.int64, device=self.device)
+        # host staging for gloo carrying CUDA tensors (gloo moves host memory)
+        self.stage = None
+        if self.device.type == "cuda" and transport == "torch":
+            import torch.distributed as dist
+
+            if dist.get_backend(group) == "gloo":
+                self.stage = {k: torch.zeros_like(v, device="cpu") for k, v in self.buf.items()}
+                self.stage["dtmin"] = torch.zeros(1, dtype=torch.int64)
+        if transport == "native":
+            self._attach_native()
         if initial_states is not None:
             for l, e in enumerate(initial_states):
                 self.E.set_state(l, e)
             self.finish_ic()
+
+    def _attach_native(self):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        lib = self.E.ctx.lib
+        obj = [None]
+        if self.rp.rank == 0:
+            idb = C.create_string_buffer(128)
+            rc = lib.fcsg_comm_unique_id(idb)
+            if rc != 0:
+                raise RuntimeError(f"fcsg_comm_unique_id failed ({rc})")
+            obj = [idb.raw]
+        dist.broadcast_object_list(obj, src=0, group=self.group)
+        peers = self.rp.peers()
+
+        def cnt(d):
+            return [(d[p] if isinstance(d[p], int) else len(d[p][0])) if p in d else 0 for p in peers]
+
+        self.E.attach_comm(self.rp.world, self.rp.rank, obj[0], peers, cnt(self.rp.e_send), cnt(self.rp.e_recv),
+                           cnt(self.rp.mu_send), cnt(self.rp.mu_recv))
 
     def _slices(self, counts, width):
         out, acc = {}, 0
@@ -266,6 +314,10 @@ class DistributedEngine:
         recvs = self.rp.e_recv if which == 0 else self.rp.mu_recv
         self.E.pack(which, send)
         self._sync_engine()
+        dsend, drecv = send, recv
+        if self.stage is not None:  # gloo: through host memory
+            send, recv = self.stage[name + "_send"], self.stage[name + "_recv"]
+            send.copy_(dsend)
         ops = []
         for peer, (a, b) in self._slices(sends, width).items():
             ops.append(dist.P2POp(dist.isend, send[a:b], peer, group=self.group))
@@ -276,7 +328,10 @@ class DistributedEngine:
                 req.wait()
             if self.device.type == "cuda":  # NCCL completes on torch's stream; the engine has its own
                 self.torch.cuda.current_stream().synchronize()
-        self.E.unpack(which, recv)
+        if self.stage is not None:
+            drecv.copy_(recv)
+            self.torch.cuda.current_stream().synchronize()
+        self.E.unpack(which, drecv)
 
     def _sync_engine(self):
         if self.device.type == "cuda":
@@ -287,13 +342,22 @@ class DistributedEngine:
 
         self.E.copy_dtmin(self.dtmin, to_engine=False)
         self._sync_engine()
-        dist.all_reduce(self.dtmin, op=dist.ReduceOp.MIN, group=self.group)
+        t = self.dtmin
+        if self.stage is not None:
+            t = self.stage["dtmin"]
+            t.copy_(self.dtmin)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        if self.stage is not None:
+            self.dtmin.copy_(t)
         if self.device.type == "cuda":
             self.torch.cuda.current_stream().synchronize()
         self.E.copy_dtmin(self.dtmin, to_engine=True)
 
     def finish_ic(self):
         """apply_ic tail across ranks: BCs, then one exchange (src/runtime.cpp:284-286)."""
+        if self.transport == "native":
+            self.E.finish_ic()
+            return
         self.E.enqueue_part(-1)  # BC on every local subpatch
         self._halo(0)
         self.E.enqueue_part(4)
@@ -301,6 +365,9 @@ class DistributedEngine:
 
     def step(self):
         """One superstep in Engine::run order (src/runtime.cpp:486-511)."""
+        if self.transport == "native":
+            self.E.enqueue(1)
+            return
         E = self.E
         E.enqueue_part(0)
         self._halo(1)
@@ -313,8 +380,18 @@ class DistributedEngine:
             E.enqueue_part(4)
         E.enqueue_part(5)
 
-    def run(self, n):
+    def run(self, n, use_graph=True):
+        """n supersteps; native: the engine's own loop (one CUDA graph replay
+        per steady step), torch: part by part with the transfers between"""
+        if self.transport == "native":
+            return self.E.run(n, use_graph=use_graph)
         for _ in range(n):
             self.step()
         self.E.check_error()
         return n
+
+    def enqueue(self, n):
+        """n supersteps enqueued without waiting (native transport)"""
+        if self.transport != "native":
+            raise RuntimeError("enqueue needs the native transport")
+        self.E.enqueue(n)

@@ -316,6 +316,21 @@ class Engine:
     def unpack(self, which, tensor):
         self.ctx.check(self.ctx.lib.fcsg_engine_unpack(self.h, which, C.c_void_p(tensor.data_ptr())))
 
+    def attach_comm(self, world, rank, comm_id: bytes, peers, e_send, e_recv, mu_send, mu_recv):
+        """device-ordered transport (fcsg_engine_attach_comm): from now on
+        every superstep this engine enqueues carries its own halos and dt
+        all-reduce (NCCL on the GPU)"""
+        n = len(peers)
+        ints = np.ascontiguousarray(peers, dtype=np.int32)
+        cnt = [np.ascontiguousarray(c, dtype=np.int64) for c in (e_send, e_recv, mu_send, mu_recv)]
+        if any(len(c) != n for c in cnt):
+            raise ValueError("per-peer counts must match the peer list")
+        lp = C.POINTER(C.c_long)
+        self._comm_keep = (ints, cnt)
+        self.ctx.check(self.ctx.lib.fcsg_engine_attach_comm(self.h, world, rank, C.c_char_p(comm_id), n,
+                                                            ints.ctypes.data_as(N.ip),
+                                                            *[c.ctypes.data_as(lp) for c in cnt]))
+
     def enqueue_part(self, part, stage=0):
         self.ctx.check(self.ctx.lib.fcsg_engine_enqueue_part(self.h, part, stage))
 

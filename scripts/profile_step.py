@@ -14,6 +14,10 @@ ctx = N.Context(0)
 dec, ic, _ = P.vortex_tiles(r=tiles, s=tiles)
 E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5))
 E.run(1)  # step 0 (smear) outside the profiled window
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # ncu --profile-from-start off captures only the steady steps
 E.run(steps, use_graph=False)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 torch.cuda.synchronize()
 print("ok", E.time())

@@ -38,7 +38,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir, steps, classifier="ann"):
+def _worker(rank, world, port, out_dir, steps, classifier="ann", transport="native"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -50,7 +50,7 @@ def _worker(rank, world, port, out_dir, steps, classifier="ann"):
     dec, ic, _ = P.vortex_tiles(r=4, s=2, n0=30)
     owner = D.partition_tiles(dec, world)
     rp = D.split_plan(dec, owner, rank, world)
-    DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5, classifier=classifier))
+    DE = D.DistributedEngine(ctx, dec, rp, ic, EN.EngineConfig(cfl=0.5, classifier=classifier), transport=transport)
     DE.run(steps)
     for l, g in enumerate(rp.local):
         np.save(os.path.join(out_dir, f"sub{g}.npy"), DE.E.get_state(l))
@@ -60,16 +60,19 @@ def _worker(rank, world, port, out_dir, steps, classifier="ann"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("classifier", ["ann", "fallback"])
-def test_two_ranks_bitwise_equal_single_rank(tmp_path, emu_ctx, classifier):
-    """The same 4x2 tiling stepped by 2 gloo ranks (2x2 subpatches each) and
-    by one rank: identical states after 2 supersteps (bitwise), identical t;
-    with either classifier variant."""
+@pytest.mark.parametrize("classifier,transport", [("ann", "native"), ("ann", "torch"), ("fallback", "native")])
+def test_two_ranks_bitwise_equal_single_rank(tmp_path, emu_ctx, classifier, transport):
+    """The same 4x2 tiling stepped by 2 ranks (2x2 subpatches each) and by
+    one rank: identical states after 2 supersteps (bitwise), identical t;
+    with either classifier variant, and through either transport: the
+    engine's own device-ordered one (halos and the dt all-reduce inside the
+    superstep; shared-memory mailboxes in the emulation build) or gloo
+    point-to-point between the caller-driven parts."""
     from paper_2506_19370_b200 import engine as EN
 
     steps = 2
-    mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), steps, classifier), nprocs=2, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), steps, classifier, transport), nprocs=2,
+                       join=True, start_method="spawn")
     dec, ic, _ = P.vortex_tiles(r=4, s=2, n0=30)
     E = EN.Engine(emu_ctx, dec, ic, EN.EngineConfig(cfl=0.5, classifier=classifier))
     E.run(steps)
@@ -81,7 +84,7 @@ def test_two_ranks_bitwise_equal_single_rank(tmp_path, emu_ctx, classifier):
         assert tr[0] == t and tr[1] == st
 
 
-def _worker_interp(rank, world, port, out_dir, steps):
+def _worker_interp(rank, world, port, out_dir, steps, transport="native"):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -97,7 +100,7 @@ def _worker_interp(rank, world, port, out_dir, steps):
     owner = np.array([0, 1, 1])  # the Cartesian patch on rank 0, the bilinear one on rank 1
     rp = D.split_plan(dec, owner, rank, world)
     np.save(os.path.join(out_dir, f"ninterp{rank}.npy"), np.array([len(rp.e_interps), len(rp.mu_interps)]))
-    DE = D.DistributedEngine(ctx, dec, rp, TM._ic(1), EN.EngineConfig(cfl=0.5))
+    DE = D.DistributedEngine(ctx, dec, rp, TM._ic(1), EN.EngineConfig(cfl=0.5), transport=transport)
     DE.run(steps)
     for l, g in enumerate(rp.local):
         np.save(os.path.join(out_dir, f"sub{g}.npy"), DE.E.get_state(l))
@@ -106,7 +109,8 @@ def _worker_interp(rank, world, port, out_dir, steps):
     dist.destroy_process_group()
 
 
-def test_two_ranks_with_interpolation_donors_across_ranks(tmp_path, emu_ctx):
+@pytest.mark.parametrize("transport", ["native", "torch"])
+def test_two_ranks_with_interpolation_donors_across_ranks(tmp_path, emu_ctx, transport):
     """Two patches with non-coincident lattices on two gloo ranks: every
     solution and viscosity interpolation between them has its donor stencil on
     the other rank, is evaluated there while packing and arrives as a halo
@@ -116,8 +120,8 @@ def test_two_ranks_with_interpolation_donors_across_ranks(tmp_path, emu_ctx):
     from tests import test_multipatch as TM
 
     steps = 2
-    mp.start_processes(_worker_interp, args=(2, _free_port(), str(tmp_path), steps), nprocs=2, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker_interp, args=(2, _free_port(), str(tmp_path), steps, transport), nprocs=2,
+                       join=True, start_method="spawn")
     for r in range(2):
         ne, nm = np.load(tmp_path / f"ninterp{r}.npy")
         assert ne > 0 and nm > 0
