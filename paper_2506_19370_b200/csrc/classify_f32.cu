@@ -1,0 +1,268 @@
+// Steady-step SDNN classifier (phase 0, Classifier::classify over the proxy,
+// src/viscosity.cpp:211-251) with an FP32 screening pass and an exact FP64
+// decision wherever the screen is not conclusive.
+//
+// The classifier's output is an argmax (classify_stencil, src/viscosity.cpp:
+// 126-133), so an approximate evaluation decides the class exactly whenever
+// its logit margin (top1 - top2) exceeds twice a rigorous bound of its error
+// against the exact-arithmetic MLP (mlp_f32_margin): then every evaluation
+// within that bound -- the reference's FP64 one included, which is within
+// ~1e-13 -- has the same argmax. One thread per point:
+//   * the row and column windows (start = clamp(pos - 3, 0, n - 7), row /
+//     column segments of L-shaped subpatches) are read from the proxy field
+//     and normalised in FP64 exactly as normalize_stencil (src/viscosity.cpp:
+//     48-59), guard included (class 4);
+//   * the 7 -> 16 -> 16 -> 16 -> 16 -> 4 MLP runs in FP32 FMAs with the
+//     weights as kernel parameters (constant bank: every FFMA takes its
+//     weight straight from c[0][..], broadcast to the warp), tanh on the SFU;
+//   * a point with a stencil whose FP32 margin is not above the bound is
+//     appended to a list, and a second kernel classifies the listed points
+//     again in FP64 (classify_stencil: FP64 FMAs, the table tanh) -- ~0.2% of
+//     the stencils of the config-5 vortex;
+//   * tau = min(row, column), mu_hat = c(tau) h_max S on interior points
+//     (preliminary_viscosity, src/viscosity.cpp:240-251).
+// The FP64 tensor-core classifier (classify_mma_kernel) stays for step 0,
+// where the density windows are classified too.
+#include "classify_f32.h"
+
+#include <algorithm>
+#include <cmath>
+
+#include "dev.h"
+#include "fft_line.h"  // ldg1
+
+namespace fcsg {
+
+// Rigorous bound of |logit_fp32 - logit_exact| for inputs |x| <= 1 (the
+// normalised stencil, and tanh outputs for the hidden layers), doubled: with
+// u = 2^-24, per layer the error of a pre-activation is at most
+//   sum_j |W_ij| E_j  (propagated)  +  (gamma_{n+1} + 2u) (|b_i| + sum_j |W_ij|)
+// (n FMAs in sequence plus the bias: gamma_{n+1} = (n+1)u / (1 - (n+1)u);
+// 2u for rounding W and b to float), E_0 = u (rounding x to float); tanh is
+// 1-Lipschitz and tanh_f32 is within kTanhErr of tanh.
+double mlp_f32_margin(const std::vector<double>& w) {
+    constexpr double u = 0x1p-24, kTanhErr = 1e-6;  // tanh_f32: 2.5x its measured worst case (4e-7)
+    const int rows[kMlpLayers] = {16, 16, 16, 16, 4}, cols[kMlpLayers] = {7, 16, 16, 16, 16};
+    std::vector<double> err(7, u), nxt;
+    int off = 0;
+    double bound = 0.0;
+    for (int l = 0; l < kMlpLayers; ++l) {
+        const int n = cols[l];
+        const double g = (n + 1) * u / (1.0 - (n + 1) * u) + 2.0 * u;
+        nxt.assign(rows[l], 0.0);
+        for (int i = 0; i < rows[l]; ++i) {
+            double prop = 0.0, mag = std::fabs(w[off + rows[l] * n + i]);
+            for (int j = 0; j < n; ++j) {
+                prop += std::fabs(w[off + i * n + j]) * err[j];
+                mag += std::fabs(w[off + i * n + j]);
+            }
+            nxt[i] = (prop + g * mag) * (1.0 + 1e-12) + (l + 1 < kMlpLayers ? kTanhErr : 0.0);
+            if (l + 1 == kMlpLayers) bound = std::max(bound, nxt[i]);
+        }
+        err = nxt;
+        off += rows[l] * n + rows[l];
+    }
+    if (!std::isfinite(bound)) return INFINITY;
+    return 2.0 * bound + 1e-9;
+}
+
+MlpF32 mlp_f32_weights(const std::vector<double>& w) {
+    MlpF32 m{};
+    for (int k = 0; k < kMlpWeights; ++k) m.w[k] = static_cast<float>(w[k]);
+    return m;
+}
+
+#if FCSG_CUDA
+namespace {
+
+constexpr int kF32Threads = 256;
+
+// tanh on the FP32 pipe and the SFU: 1 - 2 / (e^(2|x|) + 1), |error| <= 4e-7
+__device__ __forceinline__ float tanh_f32(float x) {
+    float t, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(2.8853900817779268f * fabsf(x)));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t + 1.0f));
+    return copysignf(fmaxf(fmaf(-2.0f, r, 1.0f), 0.0f), x);
+}
+
+// FP32 forward pass of one normalised stencil: the four logits
+__device__ __forceinline__ void forward_f32(const MlpF32& W, const float* x, float* lg) {
+    constexpr int L0 = 16 * 7 + 16, LH = 16 * 16 + 16;
+    float h[16], g[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        float acc = W.w[16 * 7 + i];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) acc = fmaf(W.w[i * 7 + j], x[j], acc);
+        h[i] = tanh_f32(acc);
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        const int b = L0 + l * LH;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            float acc = W.w[b + 256 + i];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc = fmaf(W.w[b + i * 16 + j], h[j], acc);
+            g[i] = tanh_f32(acc);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) h[i] = g[i];
+    }
+    constexpr int LO = L0 + 3 * LH;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        float acc = W.w[LO + 64 + i];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc = fmaf(W.w[LO + i * 16 + j], h[j], acc);
+        lg[i] = acc;
+    }
+}
+
+// the class of one raw window: the guard and the normalisation in FP64 as
+// normalize_stencil, the MLP in FP32; 0 when the FP32 margin is not conclusive
+__device__ __forceinline__ int class_of(const MlpF32& W, const EngineDev& E, const double* s) {
+    double lo = s[0], hi = s[0];
+#pragma unroll
+    for (int k = 1; k < kMlpIn; ++k) {
+        lo = s[k] < lo ? s[k] : lo;
+        hi = s[k] > hi ? s[k] : hi;
+    }
+    const double span = hi - lo;
+    double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
+    scale = scale > 1e-100 ? scale : 1e-100;
+    if (span <= 1e-13 * scale || span <= E.abs_floor) return 4;
+    const double inv = 2.0 / span;  // the screen needs x to ~1e-16 relative, not the reference's rounding
+    float x[kMlpIn];
+#pragma unroll
+    for (int k = 0; k < kMlpIn; ++k) x[k] = static_cast<float>(fma(s[k] - lo, inv, -1.0));
+    float lg[4];
+    forward_f32(W, x, lg);
+    int best = 0;
+    float top = lg[0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+        if (lg[k] > top) {
+            top = lg[k];
+            best = k;
+        }
+    float second = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (k != best) second = fmaxf(second, lg[k]);
+    return static_cast<double>(top) - static_cast<double>(second) > E.cls_margin32 ? best + 1 : 0;
+}
+
+// window geometry of point p: subpatch base, (i, j), row / column segment
+// begins and the window starts (-1: the segment is shorter than a stencil)
+struct PointWin {
+    long base;
+    int i, j, rst, cst;
+    bool inset;
+};
+__device__ __forceinline__ PointWin point_windows(const EngineDev& E, long p) {
+    PointWin w;
+    const unsigned pp = static_cast<unsigned>(p);
+    const unsigned sub = fdiv(E.div_sz, pp);
+    const unsigned loc = pp - sub * E.div_sz.d;
+    w.j = static_cast<int>(fdiv(E.div_ni, loc));
+    w.i = static_cast<int>(loc) - w.j * E.ni;
+    w.base = static_cast<long>(sub) * E.ni * E.nj;
+    const int ci = E.cut_i[sub], cj = E.cut_j[sub];
+    w.inset = !(w.i < ci && w.j < cj);
+    const int rb = w.j < cj ? ci : 0, cb = w.i < ci ? cj : 0;  // row / column segment begin
+    w.rst = w.cst = -1;
+    if (E.ni - rb >= kMlpIn) {
+        const int st = w.i - rb - kMlpIn / 2;
+        w.rst = rb + (st < 0 ? 0 : (st > E.ni - rb - kMlpIn ? E.ni - rb - kMlpIn : st));
+    }
+    if (E.nj - cb >= kMlpIn) {
+        const int st = w.j - cb - kMlpIn / 2;
+        w.cst = cb + (st < 0 ? 0 : (st > E.nj - cb - kMlpIn ? E.nj - cb - kMlpIn : st));
+    }
+    return w;
+}
+__device__ __forceinline__ void row_window(const EngineDev& E, const PointWin& w, double* s) {
+    const double* f = E.proxy + w.base + static_cast<long>(w.j) * E.ni + w.rst;
+#pragma unroll
+    for (int k = 0; k < kMlpIn; ++k) s[k] = ldg1(f + k);
+}
+__device__ __forceinline__ void col_window(const EngineDev& E, const PointWin& w, double* s) {
+    const double* f = E.proxy + w.base + static_cast<long>(w.cst) * E.ni + w.i;
+#pragma unroll
+    for (int k = 0; k < kMlpIn; ++k) s[k] = ldg1(f + static_cast<long>(k) * E.ni);
+}
+__device__ __forceinline__ void write_tau(const EngineDev& E, long p, int tau) {
+    E.tau[p] = tau;
+    E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
+}
+
+__global__ void __launch_bounds__(kF32Threads) classify_f32_kernel(const __grid_constant__ EngineDev E,
+                                                                   const __grid_constant__ MlpF32 W) {
+    const long step = static_cast<long>(gridDim.x) * blockDim.x;
+    for (long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; p < E.npts; p += step) {
+        const PointWin w = point_windows(E, p);
+        int tau = 4;
+        bool redo = false;
+        if (w.inset) {
+            double s[kMlpIn];
+            if (w.rst >= 0) {
+                row_window(E, w, s);
+                const int c = class_of(W, E, s);
+                redo = c == 0;
+                tau = redo ? 4 : c;
+            }
+            if (w.cst >= 0 && !redo && tau > 1) {  // min(row, column): class 1 is final
+                col_window(E, w, s);
+                const int c = class_of(W, E, s);
+                redo = c == 0;
+                tau = c < tau ? c : tau;
+            }
+        }
+        if (redo) {  // exact FP64 classification of this point by classify_fix_kernel
+            const unsigned k = atomicAdd(E.cls_fix_count, 1u);
+            E.cls_fix_list[k] = static_cast<int>(p);
+        } else {
+            write_tau(E, p, tau);
+        }
+    }
+}
+
+// the listed points: both windows in FP64 (classify_stencil, as the reference)
+__global__ void __launch_bounds__(kF32Threads) classify_fix_kernel(const __grid_constant__ EngineDev E) {
+    __shared__ double tab[kTanhTable];
+    for (int k = threadIdx.x; k < kTanhTable; k += blockDim.x) tab[k] = E.tanh_tab[k];
+    __syncthreads();
+    const unsigned n = *E.cls_fix_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const long p = E.cls_fix_list[k];
+        const PointWin w = point_windows(E, p);
+        double s[kMlpIn];
+        int tau = 4;
+        if (w.rst >= 0) {
+            row_window(E, w, s);
+            tau = classify_stencil(MlpPtr{E.mlp}, tab, s, E.abs_floor);
+        }
+        if (w.cst >= 0) {
+            col_window(E, w, s);
+            const int c = classify_stencil(MlpPtr{E.mlp}, tab, s, E.abs_floor);
+            tau = c < tau ? c : tau;
+        }
+        write_tau(E, p, tau);
+    }
+}
+
+}  // namespace
+
+void launch_classify_f32(const EngineDev& E, const MlpF32& W, void* stream) {
+    if (E.npts == 0) return;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaMemsetAsync(E.cls_fix_count, 0, sizeof(unsigned), s);
+    long n = (E.npts + kF32Threads - 1) / kF32Threads;
+    n = n > 148 * 8 ? 148 * 8 : n;
+    classify_f32_kernel<<<static_cast<int>(n), kF32Threads, 0, s>>>(E, W);
+    classify_fix_kernel<<<148, kF32Threads, 0, s>>>(E);
+}
+#endif
+
+}  // namespace fcsg

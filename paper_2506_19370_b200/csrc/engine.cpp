@@ -6,6 +6,8 @@
 // column FC operators.
 #include "engine.h"
 
+#include "classify_f32.h"
+
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -361,9 +363,17 @@ void Engine::set_mlp_packed(const std::vector<double>& w) {
         const std::vector<double> fr = mlp_mma_fragments(mlp_);
         dev::h2d(const_cast<double*>(E_.mlp_frag), fr.data(), fr.size() * sizeof(double), ctx_.stream);
         E_.cls_fast_margin = mlp_fast_margin(mlp_);
-        for (auto& g : G_) g.E.cls_fast_margin = E_.cls_fast_margin;
+        E_.cls_margin32 = mlp_f32_margin(mlp_);
+        *mlp32_ = mlp_f32_weights(mlp_);
+        for (auto& g : G_) {
+            g.E.cls_fast_margin = E_.cls_fast_margin;
+            g.E.cls_margin32 = E_.cls_margin32;
+        }
         for (auto& cv : chunks_)
-            for (auto& c : cv) c.E.cls_fast_margin = E_.cls_fast_margin;
+            for (auto& c : cv) {
+                c.E.cls_fast_margin = E_.cls_fast_margin;
+                c.E.cls_margin32 = E_.cls_margin32;
+            }
         if (graph_exec_) {  // the captured launches hold the old margin by value
             dev::graph_destroy(graph_exec_, graph_);
             graph_exec_ = nullptr;
@@ -555,6 +565,11 @@ void Engine::finalize() {
     for (int c = 0; c < 4; ++c) E.tS4[c] = nextf();
     for (int c = 0; c < 4; ++c) E.tS5[c] = nextf();
     for (int c = 0; c < 4; ++c) E.tF[c] = E.tA[c];  // phase 2 and the stage passes never overlap
+    // the FP32-screened classifier's fixup lists (one counter per shape group)
+    E.cls_fix_list = dev::alloc_n<int>(static_cast<size_t>(std::max(npts_, 1L)));
+    E.cls_fix_count = dev::alloc_n<unsigned>(std::max<size_t>(groups_.size(), 1));
+    allocs_.push_back(E.cls_fix_list);
+    allocs_.push_back(E.cls_fix_count);
     // tau is 0 until the first phase 0 (a zero-filled Field, as in the
     // reference; Classifier::classify then writes every point)
     {
@@ -593,6 +608,8 @@ void Engine::finalize() {
         const std::vector<double> fr = mlp_mma_fragments(mlp_);
         E.mlp_frag = static_cast<const double*>(up(fr.data(), fr.size() * sizeof(double)));
         E.cls_fast_margin = mlp_fast_margin(mlp_);
+        E.cls_margin32 = mlp_f32_margin(mlp_);
+        mlp32_ = std::make_unique<MlpF32>(mlp_f32_weights(mlp_));
     }
     {
         std::vector<double> tt(kTanhTable);
@@ -792,6 +809,9 @@ void Engine::finalize() {
             }
         }
         gl.E = V;
+        gl.E.cls_fix_list = E.cls_fix_list + g.p0;
+        gl.E.cls_fix_count = E.cls_fix_count + (&g - groups_.data());
+        if (cfg_.classifier == 0) gl.w32 = mlp32_.get();
         // stage chunks: the group's slots in up to stage_chunks contiguous
         // runs (groups with explicit line runs stay whole)
         // (a chunk keeps >= kChunkPoints points: smaller kernels lose more to

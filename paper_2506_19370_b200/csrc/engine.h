@@ -177,6 +177,7 @@ class Engine {
     std::vector<void*> allocs_;
     double* pool_ = nullptr;
     std::vector<double> mlp_;
+    std::unique_ptr<MlpF32> mlp32_;         // FP32 copy for the classifier's screening pass (stable address)
     // plan (host staging until finalize)
     std::vector<long> x_dst_, x_src_;
     std::vector<int> visc_off_;

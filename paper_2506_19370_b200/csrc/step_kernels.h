@@ -129,6 +129,9 @@ struct EngineDev {
     const double* mlp_frag;  // kMlpFrags x 32: per-lane DMMA operand fragments (mlp_mma_fragments)
     const double* tanh_tab;  // tanh(k/64), k = 0..1280 (classifier tanh table)
     double cls_fast_margin;  // logit margin above which the fast-tanh class is exact (mlp_fast_margin)
+    double cls_margin32;     // logit margin above which the FP32 screen's class is exact (mlp_f32_margin)
+    int* cls_fix_list;       // points the FP32 screen left to the exact classifier (capacity npts)
+    unsigned* cls_fix_count; // (one counter per shape group view)
     // classifier variant (ClassifierConfig::Variant, include/fcs/viscosity.hpp:45-52):
     // 0 = ann (the MLP), 1 = fallback (FC spectrum decay, window fb_window)
     int cls_variant;
@@ -162,9 +165,11 @@ struct LineSet {
 };
 
 // everything the launchers need for one shape group
+struct MlpF32;
 struct GroupLaunch {
     EngineDev E;
     std::vector<LineSet> rows, cols;
+    const MlpF32* w32 = nullptr;  // FP32 classifier weights (steady steps, ann variant), host copy
 };
 
 // The classifier on the FP64 tensor cores (mma.m8n8k4.f64): per warp, 8
