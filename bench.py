@@ -265,7 +265,9 @@ LAUNCHES = {"pass_a": 5, "pass_b": 5, "pass_c": 5, "viscosity": 1, "filter": 1, 
 def fc_derivative_gbs(ctx, n_cont=25, degree=2):
     """config 1 (4096 lines x N=256) from HBM to HBM, rotating buffers larger
     than L2 between launches: the reference operator (n_cont 25, degree 2) or
-    BASELINE's five-point variant (C = 27, degree 4)."""
+    BASELINE's five-point variant (C = 27, degree 4). The 64 timed launches
+    replay as one CUDA graph: a Python loop of launches is host-bound (~13 us
+    of ctypes + launch per call against a ~10 us kernel)."""
     import torch
 
     from paper_2506_19370_b200 import fc, problems as P
@@ -276,14 +278,22 @@ def fc_derivative_gbs(ctx, n_cont=25, degree=2):
     nbuf = 16  # 16 x 2 x 8 MiB = 256 MiB > 126 MB L2
     ins = [src.clone() for _ in range(nbuf)]
     outs = [torch.empty_like(src) for _ in range(nbuf)]
-    for k in range(4):
-        op.apply(ins[k], 1, out=outs[k])
-    torch.cuda.synchronize()
     reps = 64
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        for k in range(4):
+            op.apply(ins[k], 1, out=outs[k])
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for k in range(reps):
+                op.apply(ins[k % nbuf], 1, out=outs[k % nbuf])
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for k in range(reps):
-        op.apply(ins[k % nbuf], 1, out=outs[k % nbuf])
+    a.record()  # replay() launches on the current stream
+    g.replay()
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps

@@ -107,22 +107,38 @@ FCSG_HD void stage_w280_tables(int tid, int nthr, const double2* mult_src, const
 
 // ---------------------------------------------------------------------------
 // FC line batch
+//
+// One complex line (two real lines) per warp, one pass over the batch: a
+// single wave for config 1 (2048 pairs). The kernel is latency-bound (16 MB
+// moved in a few microseconds), so every lane issues all 16 of its loads at
+// once, before the CTA stages the operator tables, and CTAs are two warps so
+// the 2048 warps spread evenly (14 per SM).
 
 template <int NL>
-FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* mult, const double* blend,
-                             const FcLinesArgs& a) {
+FCSG_HD void w280_load(int lane, long pair, const FcLinesArgs& a, double* v0, double* v1) {
     using namespace w280;
     const long l = 2 * pair;
-    const long ls = a.line_stride, st = a.stride, ols = a.out_line_stride, ost = a.out_stride;
+    const long ls = a.line_stride, st = a.stride;
     const bool have1 = l + 1 < a.n_lines;
     constexpr int PPL = kN / NL;
-#pragma unroll 4
+#pragma unroll
     for (int m = 0; m < PPL; ++m) {
         const int i = lane + NL * m;
-        const double v0 = ldg1(a.in + l * ls + i * st);
-        const double v1 = have1 ? ldg1(a.in + (l + 1) * ls + i * st) : 0.0;
-        buf[slot_of(i)] = mk2(v0, v1);
+        v0[m] = ldg1(a.in + l * ls + i * st);
+        v1[m] = have1 ? ldg1(a.in + (l + 1) * ls + i * st) : 0.0;
     }
+}
+
+template <int NL>
+FCSG_HD void w280_finish(int lane, long pair, double2* buf, const double2* mult, const double* blend,
+                         const FcLinesArgs& a, const double* v0, const double* v1) {
+    using namespace w280;
+    const long l = 2 * pair;
+    const long ols = a.out_line_stride, ost = a.out_stride;
+    const bool have1 = l + 1 < a.n_lines;
+    constexpr int PPL = kN / NL;
+#pragma unroll
+    for (int m = 0; m < PPL; ++m) buf[slot_of(lane + NL * m)] = mk2(v0[m], v1[m]);
     FCSG_SYNCWARP();
     transform<NL, 1>(lane, buf, kSlots, mult, blend);
 #pragma unroll 4
@@ -135,18 +151,27 @@ FCSG_HD void w280_lines_body(int lane, long pair, double2* buf, const double2* m
 }
 
 #if FCSG_CUDA
-__global__ void __launch_bounds__(kWThreads, 3) w280_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+constexpr int kLWarps = 2;  // warps per CTA of the line batch
+__global__ void __launch_bounds__(kLWarps * 32) w280_lines_kernel(const __grid_constant__ FcLinesArgs a) {
     extern __shared__ double2 wsm[];
     double2* mult = wsm;
     double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
-    stage_w280_tables(threadIdx.x, kWThreads, a.pl.mult_pfa + (a.mode - 1) * w280::kNE, a.pl.blend, mult, blend);
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* buf = wsm + kTabSlots + warp * w280::kSlots;
     const long npairs = (a.n_lines + 1) / 2;
-    for (long pair = static_cast<long>(blockIdx.x) * kWarps + warp; pair < npairs;
-         pair += static_cast<long>(gridDim.x) * kWarps)
-        w280_lines_body<32>(lane, pair, buf, mult, blend, a);
+    long pair = static_cast<long>(blockIdx.x) * kLWarps + warp;
+    double v0[w280::kN / 32], v1[w280::kN / 32];
+    if (pair < npairs) w280_load<32>(lane, pair, a, v0, v1);  // in flight while the tables are staged
+    stage_w280_tables(threadIdx.x, kLWarps * 32, a.pl.mult_pfa + (a.mode - 1) * w280::kNE, a.pl.blend, mult, blend);
+    __syncthreads();
+    for (; pair < npairs; pair += static_cast<long>(gridDim.x) * kLWarps) {
+        w280_finish<32>(lane, pair, buf, mult, blend, a, v0, v1);
+        const long nxt = pair + static_cast<long>(gridDim.x) * kLWarps;
+        if (nxt < npairs) {
+            FCSG_SYNCWARP();
+            w280_load<32>(lane, nxt, a, v0, v1);
+        }
+    }
 }
 #endif
 
@@ -158,17 +183,19 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream) {
     const long npairs = (a.n_lines + 1) / 2;
     if (npairs == 0) return;
 #if FCSG_CUDA
-    const size_t smem = (kTabSlots + kWarps * w280::kSlots) * sizeof(double2);
-    static unsigned long long done = 0;
-    if (dev::first_on_device(&done))
-        cudaFuncSetAttribute(w280_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const long nblk = (npairs + kWarps - 1) / kWarps;
-    w280_lines_kernel<<<static_cast<int>(nblk), kWThreads, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    const size_t smem = (kTabSlots + kLWarps * w280::kSlots) * sizeof(double2);
+    const long nblk = (npairs + kLWarps - 1) / kLWarps;
+    const int grid = static_cast<int>(std::min<long>(nblk, 148L * 64));
+    w280_lines_kernel<<<grid, kLWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
 #else
     (void)stream;
     std::vector<double2> buf(w280::kSlots);
     const double2* mult = a.pl.mult_pfa + (a.mode - 1) * w280::kNE;
-    for (long pair = 0; pair < npairs; ++pair) w280_lines_body<1>(0, pair, buf.data(), mult, a.pl.blend, a);
+    double v0[w280::kN], v1[w280::kN];
+    for (long pair = 0; pair < npairs; ++pair) {
+        w280_load<1>(0, pair, a, v0, v1);
+        w280_finish<1>(0, pair, buf.data(), mult, a.pl.blend, a, v0, v1);
+    }
 #endif
 }
 

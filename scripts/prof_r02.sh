@@ -15,7 +15,7 @@ ncu --profile-from-start off --set full --clock-control none -o /tmp/all -f \
     python scripts/profile_step.py 8 1 > gpurun_out/ncu_all.log 2>&1
 ncu -i /tmp/all.ncu-rep --page raw --csv > gpurun_out/${R}_all_raw.csv 2>/dev/null
 ncu -i /tmp/all.ncu-rep --page details --csv > gpurun_out/${R}_all_details.csv 2>/dev/null
-for k in wpass_x_kernel wpass_y_kernel classify_mma_kernel; do
+for k in wpass_x_kernel wpass_y_kernel classify_f32_kernel; do
   ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:$k -c 1 \
       -o gpurun_out/${R}_$k -f python scripts/profile_step.py 8 1 > gpurun_out/ncu_$k.log 2>&1
 done

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_kernels.py -m gpu -q -x > gpurun_out/pytest_d.log 2>&1; tail -2 gpurun_out/pytest_d.log
+timeout 600 python scripts/time_groups.py > gpurun_out/tg.log 2>&1; cat gpurun_out/tg.log
