@@ -48,34 +48,49 @@ def peaks():
         return 6650.0, "fallback"
 
 
-# kernel behind each timed group (for the ncu capture lookup)
-GROUP_KERNEL = {"pass_a": "wpass_y_kernel", "pass_b": "wpass_x_kernel", "viscosity": "classify_mma_kernel"}
-GROUP_LB = {"pass_a": 4, "pass_b": 4}  # lines per block of the captured pass (256-point lines)
+def fp64_peak():
+    """measured FP64 peak (TFLOP/s): DFMA alone, DMMA alone and both
+    interleaved share one FP64 datapath on the B200 (scripts/fp64_peak.cu,
+    profiles/r02_fp64_peak.json)"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as fh:
+            return float(json.load(fh)["dfma_tflops"]), "measured (scripts/fp64_peak.cu)"
+    except Exception:
+        return 37.1, "fallback (B200 nominal DFMA)"
+
+
+# kernel behind each timed group (for the ncu capture lookup) and its launches
+# per group timing (the RK-stage passes launch once per stage chunk)
+GROUP_KERNEL = {"pass_a": "wpass_y_kernel", "pass_b": "wpass_x_kernel", "viscosity": "classify_f32_kernel"}
+GROUP_LAUNCHES_PER_STEP = {"pass_a": 5, "pass_b": 5, "viscosity": 1}
 
 
 def ncu_traffic(group, npts):
-    """DRAM bytes (read + write) of the group's kernel over npts points, from
-    the newest committed `ncu --set full` capture of the bench workload
-    (profiles/rNN_top_kernels_raw.csv, scripts/prof_top.sh), or None. The
-    captured launch may cover part of the points (the RK-stage passes launch
-    per half group): its bytes are scaled by npts over the points it covered
-    (grid x lines per block x 256)."""
+    """DRAM bytes (read + write) per group launch of the group's kernel, from
+    the newest committed `ncu --set full` capture of every kernel of one steady
+    superstep of the bench workload (profiles/rNN_all_raw.csv,
+    scripts/prof_r02.sh): the bytes of all its launches in the step divided by
+    the group's launches per step, or None."""
     import csv
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_top_kernels_raw.csv")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_all_raw.csv")))
     key = GROUP_KERNEL.get(group)
     if not files or not key:
         return None, None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     with open(files[-1]) as fh:
-        for row in csv.DictReader(fh):
-            if key in row["Kernel Name"]:
-                mb = float(row["dram__bytes_read.sum [MB]"]) + float(row["dram__bytes_write.sum [MB]"])
-                lb = GROUP_LB.get(group)
-                if lb:
-                    covered = float(row["launch__grid_size"]) * lb * 256
-                    mb *= npts / covered
-                return mb * 1e6, os.path.basename(files[-1])
-    return None, None
+        rows = list(csv.reader(fh))
+    hdr, units = rows[0], rows[1]
+    ik = hdr.index("Kernel Name")
+    ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    total, n = 0.0, 0
+    for r in rows[2:]:
+        if key in r[ik]:
+            total += float(r[ir]) * scale.get(units[ir], 1.0) + float(r[iw]) * scale.get(units[iw], 1.0)
+            n += 1
+    if n == 0:
+        return None, None
+    return total / GROUP_LAUNCHES_PER_STEP[group], os.path.basename(files[-1])
 
 
 class ClockSampler:
@@ -194,6 +209,22 @@ def reference_engine(tiles, threads):
     return R, dec.total_points()
 
 
+def cpu_model():
+    """the host CPU the CPU legs ran on (/proc/cpuinfo)"""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+SHIM_FFT = ("oracle/shims/fftw3.h: FFTW3 absent from the image, its r2c/c2r restated as a mixed-radix FFT with "
+            "half-length packing and precomputed twiddles (slower than FFTW, so the CPU rate is a lower bound)")
+
+
 def cpu_rate(steps, warmup, threads):
     R, npts = reference_engine(SAMPLE_TILES, threads)
     if warmup:
@@ -229,7 +260,8 @@ def run_reference(args):
                       "sampled_per_step": f"{SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} of the {R_TILES}x{S_TILES} tiles "
                                           f"({npts} points): the CPU rate is per point, the sample bounds the "
                                           f"run time"},
-           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample,
+                            "cpu_model": cpu_model(), "fft": SHIM_FFT},
            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -258,6 +290,12 @@ ALG_BYTES_CART = {
 ALG_BYTES_GEN = dict(ALG_BYTES_CART, pass_a=32 + 1 + 32,                      # e, mask -> tW
                      pass_b=32 + 32 + 8 + 32 + 32 + 32 + 32,                 # e, 4 metrics, mu, tW -> tS4, tS5, tA
                      pass_c=64 + 32 + 16 + 32 + 32 + 32 + 32)                # tS4, tS5, tA, iq1x, iq1y, e, e0 -> e2, e
+# algorithmic FP64 flops per point per launch (47.7 per real line
+# derivative at N = 256): pass Y 8 derivatives (D2 of 4 w, D2 of 4 Phi_y) +
+# primitives, fluxes and Phi (~60); pass X 8 derivatives + the same + the rhs
+# and SSPRK update (~30); the classifier 2 stencils x 1977 + mu_hat
+FLOP_PER_POINT = {"pass_a": 8 * 47.7 + 60, "pass_b": 8 * 47.7 + 90, "viscosity": 2 * 1977 + 20}
+STEP_FLOP = (80 * 47.7 + 8 * 47.7 + 2 * 1977 + 800) / 5  # per point-stage, flux form
 LAUNCHES = {"pass_a": 5, "pass_b": 5, "pass_c": 5, "viscosity": 1, "filter": 1, "blend": 1, "bc": 6,
             "exchange": 5}
 
@@ -518,6 +556,7 @@ def run_fcsg(args):
     share = {g: groups[g] * launches[g] for g in groups}
     dom = max(share, key=share.get)
     hbm, peak_kind = peaks()
+    fp64, fp64_kind = fp64_peak()
     ALG_BYTES = ALG_BYTES_CART if E.is_cartesian() else ALG_BYTES_GEN
     alg = ALG_BYTES.get(dom, 64) * npts
     achieved = alg / (groups[dom] * 1e-3) / 1e9
@@ -536,11 +575,14 @@ def run_fcsg(args):
     if not args.no_cpu:
         try:
             threads = os.cpu_count() or 1
-            rate, sps, cnpts = cpu_rate(3, 2, threads)  # t=0 (smear) + 1 steady step untimed, then 3 timed
+            # the same sample and step counts as the reference arm (--impl reference)
+            rate, sps, cnpts = cpu_rate(args.steps, args.warmup, threads)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"3 steady supersteps (after the untimed t=0 step and one steady step) of {SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} tiles of 256x256 ({cnpts} points) "
-                             f"of the same workload, reference Engine with {threads} worker threads "
-                             f"(oracle/_ref; FFTW replaced by the oracle/shims FFT)"}
+                   "sample": f"{args.steps} supersteps after {args.warmup} untimed ones (the t=0 step first) of "
+                             f"{SAMPLE_TILES[0]}x{SAMPLE_TILES[1]} tiles of 256x256 ({cnpts} points) of the same "
+                             f"workload, reference Engine::run with {threads} worker threads (oracle/_ref), the "
+                             f"same sample and steps as the --impl reference arm",
+                   "cpu_model": cpu_model(), "fft": SHIM_FFT}
         except Exception as ex:  # the reference build is test infrastructure
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
     out = {
@@ -565,6 +607,20 @@ def run_fcsg(args):
                      "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "alg_bytes_per_launch": alg, "peak_kind": peak_kind,
                      "alg_bytes_per_point": ALG_BYTES.get(dom), "ms_per_launch": groups[dom]},
+        "roofline_fp64": {
+            "note": "the line passes and the classifier are bound by the FP64 pipe and instruction issue, not HBM "
+                    "(ncu: FP64 pipe 33-38%, DRAM 11-28% of peak, profiles/README.md); algorithmic flops by "
+                    "SURVEY 8(d)'s convention (FFT 2 x 2.5 n_ext log2 n_ext + continuation + multiplier per real "
+                    "line derivative = 47.7 flop/pt at N = 256)",
+            "peak_tflops": fp64, "peak_kind": fp64_kind,
+            "dominant_kernel": {"kernel": dom, "alg_flop_per_point": FLOP_PER_POINT.get(dom),
+                                "achieved_tflops": FLOP_PER_POINT.get(dom, 0) * npts / (groups[dom] * 1e-3) / 1e12,
+                                "frac": FLOP_PER_POINT.get(dom, 0) * npts / (groups[dom] * 1e-3) / 1e12 / fp64},
+            "step": {"alg_flop_per_pt_stage": STEP_FLOP, "achieved_tflops": value / max(world, 1) * STEP_FLOP / 1e12,
+                     "frac": value / max(world, 1) * STEP_FLOP / 1e12 / fp64,
+                     "basis": "flux form: 16 line derivatives per stage, the per-step filter (8 lines), 2 MLP stencils "
+                              "(1977 flop each) and ~800 flop of pointwise work per point per step, over 5 stages; "
+                              "the reference's 40-derivative order would count 2930"}},
         "kernel_groups_ms": groups,
         "fc_derivative": {"config": "config1: 4096 lines x N=256, reference operator (degree 2, n_cont=25, "
                                     "n_ext=280), d/dx, HBM->HBM",
