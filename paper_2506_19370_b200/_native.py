@@ -15,7 +15,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libfcsg.so")
-EMU_PATH = os.path.join(os.path.dirname(HERE), "build", "emu", "libfcsg_emu.so")
+EMU_PATH = os.environ.get("FCSG_EMU_LIB") or os.path.join(os.path.dirname(HERE), "build", "emu", "libfcsg_emu.so")
 
 # include/fcsg.h error kinds -> reference exception names (include/fcs/errors.hpp)
 OK, CONFIG, USAGE, GEOMETRY, DECOMPOSITION, INVALID_STATE, CUDA_ERROR, OTHER = 0, 1, 2, 3, 4, 5, 8, 9

@@ -49,10 +49,14 @@ def _headers():
     ]
 
 
-def build(emulate: bool = False, verbose: bool = False, force: bool = False) -> str:
-    objdir = os.path.join(ROOT, "build", "emu_obj" if emulate else "obj")
+def build(emulate: bool = False, verbose: bool = False, force: bool = False, sanitize: bool = False) -> str:
+    """sanitize (with emulate): the emulation build under AddressSanitizer +
+    UndefinedBehaviorSanitizer (build/emu_asan/), the bounds / UB check of the
+    kernel bodies' index logic (scripts/asan_emu.sh)"""
+    sanitize = sanitize and emulate
+    objdir = os.path.join(ROOT, "build", "emu_asan_obj" if sanitize else ("emu_obj" if emulate else "obj"))
     os.makedirs(objdir, exist_ok=True)
-    out_dir = EMU_DIR if emulate else LIBDIR
+    out_dir = os.path.join(ROOT, "build", "emu_asan") if sanitize else (EMU_DIR if emulate else LIBDIR)
     os.makedirs(out_dir, exist_ok=True)
     lib = os.path.join(out_dir, "libfcsg_emu.so" if emulate else "libfcsg.so")
     hdrs = _headers()
@@ -69,7 +73,8 @@ def build(emulate: bool = False, verbose: bool = False, force: bool = False) -> 
             continue
         if emulate:
             lang = ["-x", "c++"] if src.endswith(".cu") else []
-            cmd = ["g++", "-std=c++17", "-O2", "-fPIC", "-DFCSG_EMULATE", *common_inc, *lang, "-c", path, "-o", obj]
+            san = ["-fsanitize=address,undefined", "-fno-omit-frame-pointer", "-g", "-O1"] if sanitize else ["-O2"]
+            cmd = ["g++", "-std=c++17", *san, "-fPIC", "-DFCSG_EMULATE", *common_inc, *lang, "-c", path, "-o", obj]
         elif src.endswith(".cu"):
             cmd = [NVCC, ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xptxas=-v" if verbose else "-Xptxas=-O3",
                    "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", *common_inc, "-c", path, "-o", obj]
@@ -84,12 +89,13 @@ def build(emulate: bool = False, verbose: bool = False, force: bool = False) -> 
                 sys.stderr.write(r.stderr)
     if force or _stale(lib, objs):
         if emulate:
-            _run(["g++", "-shared", "-o", lib, *objs, "-lquadmath", "-lpthread", "-lrt"])
+            san = ["-fsanitize=address,undefined"] if sanitize else []
+            _run(["g++", "-shared", *san, "-o", lib, *objs, "-lquadmath", "-lpthread", "-lrt"])
         else:
             _run([NVCC, ARCH, "-shared", "-o", lib, *objs, "-lquadmath", "-ldl", "-cudart", "static"])
     return lib
 
 
 if __name__ == "__main__":
-    emu = "--emulate" in sys.argv
-    print(build(emulate=emu, verbose="-v" in sys.argv, force="--force" in sys.argv))
+    emu = "--emulate" in sys.argv or "--asan" in sys.argv
+    print(build(emulate=emu, verbose="-v" in sys.argv, force="--force" in sys.argv, sanitize="--asan" in sys.argv))

@@ -230,10 +230,15 @@ __global__ void __launch_bounds__(kF32Threads) classify_f32_kernel(const __grid_
 
 // the listed points: both windows in FP64 (classify_stencil, as the reference)
 __global__ void __launch_bounds__(kF32Threads) classify_fix_kernel(const __grid_constant__ EngineDev E) {
-    __shared__ double tab[kTanhTable];
-    for (int k = threadIdx.x; k < kTanhTable; k += blockDim.x) tab[k] = E.tanh_tab[k];
-    __syncthreads();
     const unsigned n = *E.cls_fix_count;
+    if (static_cast<unsigned>(blockIdx.x) * blockDim.x >= n) return;  // (~0.2% of the points: most blocks idle)
+    // the table tanh and the FP64 weights in shared memory: each listed point
+    // is one thread's serial FP64 MLP, whose latency is the kernel's
+    __shared__ double tab[kTanhTable];
+    __shared__ double wt[kMlpWeights];
+    for (int k = threadIdx.x; k < kTanhTable; k += blockDim.x) tab[k] = E.tanh_tab[k];
+    for (int k = threadIdx.x; k < kMlpWeights; k += blockDim.x) wt[k] = E.mlp[k];
+    __syncthreads();
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const long p = E.cls_fix_list[k];
         const PointWin w = point_windows(E, p);
@@ -241,11 +246,11 @@ __global__ void __launch_bounds__(kF32Threads) classify_fix_kernel(const __grid_
         int tau = 4;
         if (w.rst >= 0) {
             row_window(E, w, s);
-            tau = classify_stencil(MlpPtr{E.mlp}, tab, s, E.abs_floor);
+            tau = classify_stencil(MlpPtr{wt}, tab, s, E.abs_floor);
         }
         if (w.cst >= 0) {
             col_window(E, w, s);
-            const int c = classify_stencil(MlpPtr{E.mlp}, tab, s, E.abs_floor);
+            const int c = classify_stencil(MlpPtr{wt}, tab, s, E.abs_floor);
             tau = c < tau ? c : tau;
         }
         write_tau(E, p, tau);
@@ -261,7 +266,9 @@ void launch_classify_f32(const EngineDev& E, const MlpF32& W, void* stream) {
     long n = (E.npts + kF32Threads - 1) / kF32Threads;
     n = n > 148 * 8 ? 148 * 8 : n;
     classify_f32_kernel<<<static_cast<int>(n), kF32Threads, 0, s>>>(E, W);
-    classify_fix_kernel<<<148, kF32Threads, 0, s>>>(E);
+    // enough threads for one listed point each up to 2% of the points
+    const long nfix = std::max(1L, std::min((E.npts / 50 + kF32Threads - 1) / kF32Threads, 148L * 16));
+    classify_fix_kernel<<<static_cast<int>(nfix), kF32Threads, 0, s>>>(E);
 }
 #endif
 

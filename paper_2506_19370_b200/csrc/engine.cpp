@@ -16,10 +16,49 @@
 #include <fstream>
 #include <numeric>
 
+#if !defined(FCSG_EMULATE)
+#include <nvtx3/nvToolsExt.h>
+#endif
+
 namespace fcsg {
 
 namespace {
 constexpr double kInf = std::numeric_limits<double>::infinity();
+
+// NVTX range around host-side enqueueing of a phase / stage (nsys, ncu
+// --nvtx --nvtx-include "fcsg stage 1/"): the reference's RunStats timing
+// (src/runtime.cpp:469,522-528) split by phase. Inside CUDA-graph capture the
+// ranges mark the capture; eager steps (step 0, the phase hooks,
+// FCSG_NO_GRAPH) carry them per launch.
+struct Range {
+    explicit Range(const char* name) {
+#if !defined(FCSG_EMULATE)
+        nvtxRangePushA(name);
+#else
+        (void)name;
+#endif
+    }
+    ~Range() {
+#if !defined(FCSG_EMULATE)
+        nvtxRangePop();
+#endif
+    }
+    Range(const Range&) = delete;
+    Range& operator=(const Range&) = delete;
+};
+void range_push(const char* name) {
+#if !defined(FCSG_EMULATE)
+    nvtxRangePushA(name);
+#else
+    (void)name;
+#endif
+}
+void range_pop() {
+#if !defined(FCSG_EMULATE)
+    nvtxRangePop();
+#endif
+}
+const char* kStageRange[5] = {"fcsg stage 0", "fcsg stage 1", "fcsg stage 2", "fcsg stage 3", "fcsg stage 4"};
 }
 
 Engine::Engine(Ctx& ctx, const EngineConfig& cfg) : ctx_(ctx), cfg_(cfg) {
@@ -305,6 +344,7 @@ void Engine::attach_comm(std::unique_ptr<Comm> comm, std::vector<int> peers, std
 // order both sides' plan split walked (distributed.split_plan).
 void Engine::halo(int which, void* stream) {
     if (!comm_) return;
+    const Range range(which == 0 ? "fcsg halo e" : "fcsg halo mu_hat");
     const int width = which == 0 ? 4 : 1;
     double* snd = d_wire_[which == 0 ? 0 : 2];
     double* rcv = d_wire_[which == 0 ? 1 : 3];
@@ -1072,6 +1112,9 @@ void Engine::finish_ic() {
 
 void Engine::phase(int ph, int stage) {
     if (!finalized_) throw Error(kUsage, "engine not finalized");
+    static const char* kPhaseRange[7] = {"fcsg phase 0", "fcsg phase 1", "fcsg phase 2", "fcsg phase 3", "", "",
+                                         "fcsg phase 6"};
+    const Range range(ph >= 0 && ph < 7 && kPhaseRange[ph][0] ? kPhaseRange[ph] : "fcsg phase");
     switch (ph) {
         case 0: launch_phase0(E_, G_, host_step_ == 0, ctx_.stream); break;
         case 1:
@@ -1133,6 +1176,8 @@ void Engine::ensure_streams() {
 }
 
 void Engine::enqueue_step(bool step0) {
+    const Range step_range(step0 ? "fcsg superstep (t=0)" : "fcsg superstep");
+    range_push("fcsg phases 0-2 (classifier, blend, filter, BC, dt)");
     void* s = ctx_.stream;
     // phase 0 reads e only in the proxy (and, at t = 0, in the classifier's
     // density windows); the phase-2 filter writes e and touches nothing
@@ -1181,6 +1226,7 @@ void Engine::enqueue_step(bool step0) {
     }
     launch_bc(G_, s);
     launch_finalize_dt(E_, s);
+    range_pop();
     // RK stages: the chunks' line passes and BCs on side streams (a chunk's
     // passes and BCs touch only its own subpatches), joined before the
     // exchange. The GPU then runs one chunk's pass Y next to another's pass X
@@ -1188,6 +1234,7 @@ void Engine::enqueue_step(bool step0) {
     const bool chunked = dev::is_cuda() && chunks_.size() > 1;
     if (chunked) ensure_streams();
     for (int st = 0; st < 5; ++st) {
+        const Range stage_range(kStageRange[st]);
         if (chunked) {
             const int ns = std::min(static_cast<int>(cstreams_.size()), static_cast<int>(chunks_.size()));
             dev::record(ev_stage_, s);

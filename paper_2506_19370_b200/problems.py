@@ -175,7 +175,7 @@ def initial_state(dec, ic, sub):
         return np.ascontiguousarray(ic(d.x, d.y))
 
 
-def cylinder_flow(full=True):
+def cylinder_flow(full=True, fine=False):
     """BASELINE config 3 (multi-patch, curvilinear). The reference's own
     cylinder decomposition fails its overlap check, so
     the patches are laid out here: an annulus r in [1, 2.2] around the body
@@ -184,7 +184,10 @@ def cylinder_flow(full=True):
     [-4, 12] x [-6, 6] (inflow on the left, supersonic outflow on the right,
     slip walls at y = +-6) with 256 x 256 subpatches; free stream rho = 1.4,
     p = 1, u = 3 (Mach 3). full=False: the same layout at about a quarter of
-    the resolution (0.70M points; ring 512 x 83, Cartesian 138 x 138)."""
+    the resolution (0.70M points; ring 512 x 83, Cartesian 138 x 138).
+    fine=True: BASELINE's ~4M points -- the ring at 3072 x 147 and the
+    Cartesian patches cut into 6, 36, 4 and 4 subpatches of 256 x 256 (the
+    cells anisotropic where a patch side does not divide evenly)."""
     from . import multipatch as M
     SI = M.SideInfo
     ring = M.Patch(M.S, M.AnnulusMap((0.0, 0.0), 1.0, 2.2, -math.pi, 2 * math.pi),
@@ -199,11 +202,12 @@ def cylinder_flow(full=True):
     for k, p in enumerate(patches):
         p.index = k
     ring_r, ring_n0, n0 = (16, 129, 238) if full else (8, 65, 120)
+    cuts = ((1, 5), (5, 5), (1, 2), (1, 2))
+    if fine:
+        ring_r, cuts = 24, ((1, 6), (6, 6), (2, 2), (2, 2))
     M.subdivide_Q(ring, ring_r, 1, ring_n0, 9)
-    M.subdivide_Q(left, 1, 5, n0, 9)
-    M.subdivide_Q(right, 5, 5, n0, 9)
-    M.subdivide_Q(top, 1, 2, n0, 9)
-    M.subdivide_Q(bottom, 1, 2, n0, 9)
+    for p, (r, s) in zip((left, right, top, bottom), cuts):
+        M.subdivide_Q(p, r, s, n0, 9)
     free = tuple(float(v) for v in conservative(1.4, 3.0, 0.0, 1.0))
     bcs = {"in": M.BcSpec(M.INFLOW, free), "out": M.BcSpec(M.SUPERSONIC_OUTFLOW), "wall": M.BcSpec(M.SLIP_WALL),
            "body": M.BcSpec(M.SLIP_WALL)}
