@@ -13,8 +13,9 @@
 //     and normalised in FP64 exactly as normalize_stencil (src/viscosity.cpp:
 //     48-59), guard included (class 4);
 //   * the 7 -> 16 -> 16 -> 16 -> 16 -> 4 MLP runs in FP32 FMAs with the
-//     weights as kernel parameters (constant bank: every FFMA takes its
-//     weight straight from c[0][..], broadcast to the warp), tanh on the SFU;
+//     weights as kernel parameters (constant bank, broadcast to the warp),
+//     the point's row and column stencils packed in FFMA2 pairs, tanh on the
+//     SFU (|error| <= 4e-7);
 //   * a point with a stencil whose FP32 margin is not above the bound is
 //     appended to a list, and a second kernel classifies the listed points
 //     again in FP64 (classify_stencil: FP64 FMAs, the table tanh) -- ~0.2% of
@@ -77,34 +78,45 @@ namespace {
 
 constexpr int kF32Threads = 256;
 
-// tanh on the FP32 pipe and the SFU: 1 - 2 / (e^(2|x|) + 1), |error| <= 4e-7
-__device__ __forceinline__ float tanh_f32(float x) {
-    float t, r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(2.8853900817779268f * fabsf(x)));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(t + 1.0f));
-    return copysignf(fmaxf(fmaf(-2.0f, r, 1.0f), 0.0f), x);
+// The point's row and column stencils run as the two halves of packed FP32
+// pairs: Blackwell's FFMA2 does both FMAs in one instruction, with the weight
+// broadcast from a uniform register (LDCU.128 fetches four), so the MLP costs
+// 944 FFMA2 per point instead of 1888 FFMA. Each half rounds exactly as a
+// scalar FFMA (IEEE round-to-nearest), so mlp_f32_margin bounds both.
+__device__ __forceinline__ float2 dup(float w) { return make_float2(w, w); }
+
+__device__ __forceinline__ float2 tanh_f32x2(float2 z) {
+    const float2 a = __fmul2_rn(make_float2(fabsf(z.x), fabsf(z.y)), dup(2.8853900817779268f));  // 2|x| log2 e
+    float tx, ty, rx, ry;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(tx) : "f"(a.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(ty) : "f"(a.y));
+    const float2 d = __fadd2_rn(make_float2(tx, ty), dup(1.0f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rx) : "f"(d.x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ry) : "f"(d.y));
+    const float2 y = __ffma2_rn(dup(-2.0f), make_float2(rx, ry), dup(1.0f));  // 1 - 2 / (e^(2|x|) + 1)
+    return make_float2(copysignf(fmaxf(y.x, 0.0f), z.x), copysignf(fmaxf(y.y, 0.0f), z.y));
 }
 
-// FP32 forward pass of one normalised stencil: the four logits
-__device__ __forceinline__ void forward_f32(const MlpF32& W, const float* x, float* lg) {
+// FP32 forward pass of two normalised stencils (row in .x, column in .y)
+__device__ __forceinline__ void forward_f32x2(const MlpF32& W, const float2* x, float2* lg) {
     constexpr int L0 = 16 * 7 + 16, LH = 16 * 16 + 16;
-    float h[16], g[16];
+    float2 h[16], g[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-        float acc = W.w[16 * 7 + i];
+        float2 acc = dup(W.w[16 * 7 + i]);
 #pragma unroll
-        for (int j = 0; j < 7; ++j) acc = fmaf(W.w[i * 7 + j], x[j], acc);
-        h[i] = tanh_f32(acc);
+        for (int j = 0; j < 7; ++j) acc = __ffma2_rn(dup(W.w[i * 7 + j]), x[j], acc);
+        h[i] = tanh_f32x2(acc);
     }
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
         const int b = L0 + l * LH;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-            float acc = W.w[b + 256 + i];
+            float2 acc = dup(W.w[b + 256 + i]);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc = fmaf(W.w[b + i * 16 + j], h[j], acc);
-            g[i] = tanh_f32(acc);
+            for (int j = 0; j < 16; ++j) acc = __ffma2_rn(dup(W.w[b + i * 16 + j]), h[j], acc);
+            g[i] = tanh_f32x2(acc);
         }
 #pragma unroll
         for (int i = 0; i < 16; ++i) h[i] = g[i];
@@ -112,16 +124,17 @@ __device__ __forceinline__ void forward_f32(const MlpF32& W, const float* x, flo
     constexpr int LO = L0 + 3 * LH;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        float acc = W.w[LO + 64 + i];
+        float2 acc = dup(W.w[LO + 64 + i]);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc = fmaf(W.w[LO + i * 16 + j], h[j], acc);
+        for (int j = 0; j < 16; ++j) acc = __ffma2_rn(dup(W.w[LO + i * 16 + j]), h[j], acc);
         lg[i] = acc;
     }
 }
 
-// the class of one raw window: the guard and the normalisation in FP64 as
-// normalize_stencil, the MLP in FP32; 0 when the FP32 margin is not conclusive
-__device__ __forceinline__ int class_of(const MlpF32& W, const EngineDev& E, const double* s) {
+// normalize_stencil (src/viscosity.cpp:48-59) in FP64: false = the class-4
+// guard; else the normalised values rounded to float (the screen needs them
+// to ~1e-16 relative, not the reference's exact rounding)
+__device__ __forceinline__ bool normalise_f32(const EngineDev& E, const double* s, float* x) {
     double lo = s[0], hi = s[0];
 #pragma unroll
     for (int k = 1; k < kMlpIn; ++k) {
@@ -131,13 +144,16 @@ __device__ __forceinline__ int class_of(const MlpF32& W, const EngineDev& E, con
     const double span = hi - lo;
     double scale = fabs(lo) > fabs(hi) ? fabs(lo) : fabs(hi);
     scale = scale > 1e-100 ? scale : 1e-100;
-    if (span <= 1e-13 * scale || span <= E.abs_floor) return 4;
-    const double inv = 2.0 / span;  // the screen needs x to ~1e-16 relative, not the reference's rounding
-    float x[kMlpIn];
+    if (span <= 1e-13 * scale || span <= E.abs_floor) return false;
+    const double inv = 2.0 / span;
 #pragma unroll
     for (int k = 0; k < kMlpIn; ++k) x[k] = static_cast<float>(fma(s[k] - lo, inv, -1.0));
-    float lg[4];
-    forward_f32(W, x, lg);
+    return true;
+}
+
+// class 1..4 of FP32 logits, 0 when the margin is not above the bound
+__device__ __forceinline__ int screen_class(const EngineDev& E, float l0, float l1, float l2, float l3) {
+    const float lg[4] = {l0, l1, l2, l3};
     int best = 0;
     float top = lg[0];
 #pragma unroll
@@ -197,33 +213,40 @@ __device__ __forceinline__ void write_tau(const EngineDev& E, long p, int tau) {
     E.mu_hat[p] = (E.mask[p] == 1) ? E.visc_c[tau - 1] * E.h_max[p] * E.speed[p] : 0.0;
 }
 
-__global__ void __launch_bounds__(kF32Threads) classify_f32_kernel(const __grid_constant__ EngineDev E,
+__global__ void __launch_bounds__(kF32Threads, 3) classify_f32_kernel(const __grid_constant__ EngineDev E,
                                                                    const __grid_constant__ MlpF32 W) {
-    const long step = static_cast<long>(gridDim.x) * blockDim.x;
-    for (long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; p < E.npts; p += step) {
+    // one point per thread and no grid-stride loop: in a loop the weights are
+    // loop-invariant and ptxas keeps hundreds of them in registers
+    const long p = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < E.npts) {
         const PointWin w = point_windows(E, p);
-        int tau = 4;
-        bool redo = false;
+        // per window: 4 (guard / no window) or -1 (to the MLP)
+        int cr = 4, cc = 4;
+        float xr[kMlpIn], xc[kMlpIn];
         if (w.inset) {
             double s[kMlpIn];
             if (w.rst >= 0) {
                 row_window(E, w, s);
-                const int c = class_of(W, E, s);
-                redo = c == 0;
-                tau = redo ? 4 : c;
+                cr = normalise_f32(E, s, xr) ? -1 : 4;
             }
-            if (w.cst >= 0 && !redo && tau > 1) {  // min(row, column): class 1 is final
+            if (w.cst >= 0) {
                 col_window(E, w, s);
-                const int c = class_of(W, E, s);
-                redo = c == 0;
-                tau = c < tau ? c : tau;
+                cc = normalise_f32(E, s, xc) ? -1 : 4;
             }
         }
-        if (redo) {  // exact FP64 classification of this point by classify_fix_kernel
+        if (cr < 0 || cc < 0) {
+            float2 x[kMlpIn], lg[4];
+#pragma unroll
+            for (int k = 0; k < kMlpIn; ++k) x[k] = make_float2(cr < 0 ? xr[k] : 0.0f, cc < 0 ? xc[k] : 0.0f);
+            forward_f32x2(W, x, lg);
+            if (cr < 0) cr = screen_class(E, lg[0].x, lg[1].x, lg[2].x, lg[3].x);
+            if (cc < 0) cc = screen_class(E, lg[0].y, lg[1].y, lg[2].y, lg[3].y);
+        }
+        if (cr == 0 || cc == 0) {  // exact FP64 classification of this point by classify_fix_kernel
             const unsigned k = atomicAdd(E.cls_fix_count, 1u);
             E.cls_fix_list[k] = static_cast<int>(p);
         } else {
-            write_tau(E, p, tau);
+            write_tau(E, p, cr < cc ? cr : cc);
         }
     }
 }
@@ -263,8 +286,7 @@ void launch_classify_f32(const EngineDev& E, const MlpF32& W, void* stream) {
     if (E.npts == 0) return;
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaMemsetAsync(E.cls_fix_count, 0, sizeof(unsigned), s);
-    long n = (E.npts + kF32Threads - 1) / kF32Threads;
-    n = n > 148 * 8 ? 148 * 8 : n;
+    const long n = (E.npts + kF32Threads - 1) / kF32Threads;
     classify_f32_kernel<<<static_cast<int>(n), kF32Threads, 0, s>>>(E, W);
     // enough threads for one listed point each up to 2% of the points
     const long nfix = std::max(1L, std::min((E.npts / 50 + kF32Threads - 1) / kF32Threads, 148L * 16));

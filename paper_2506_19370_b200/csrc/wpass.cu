@@ -97,13 +97,34 @@ FCSG_HD void pf_l2_bulk(const double* p, unsigned bytes) {
 }
 
 // the operator tables a CTA keeps in shared memory: the multiplier (280
-// double2, prime-factor order) and the 24 x 3 blend matrix
-constexpr int kTabSlots = w280::kNE + (w280::kGap * w280::kD1 + 1) / 2;
+// double2, prime-factor order), the 24 x 3 blend matrix and the slot of each
+// natural position i < 256 (slot_of: ~12 integer instructions, which the
+// loads and epilogues would otherwise spend per point -- a quarter of the
+// passes' instructions were integer before the table)
+constexpr int kBlendSlots = (w280::kGap * w280::kD1 + 1) / 2;
+constexpr int kSlotTabSlots = w280::kN * 2 / 16;  // 256 ushort
+constexpr int kTabSlots = w280::kNE + kBlendSlots + kSlotTabSlots;
 FCSG_HD void stage_w280_tables(int tid, int nthr, const double2* mult_src, const double* blend_src, double2* mult,
                                double* blend) {
     for (int k = tid; k < w280::kNE; k += nthr) mult[k] = ldg2(mult_src + k);
     for (int k = tid; k < w280::kGap * w280::kD1; k += nthr) blend[k] = ldg1(blend_src + k);
+    unsigned short* st = reinterpret_cast<unsigned short*>(mult + w280::kNE + kBlendSlots);
+    for (int k = tid; k < w280::kN; k += nthr) st[k] = static_cast<unsigned short>(w280::slot_of(k));
 }
+FCSG_HD const unsigned short* slot_table(const double2* mult) {
+    return reinterpret_cast<const unsigned short*>(mult + w280::kNE + kBlendSlots);
+}
+#if !FCSG_CUDA
+// the emulation build's copy (its tables are not staged)
+inline const unsigned short* host_slot_table() {
+    static const std::vector<unsigned short> t = [] {
+        std::vector<unsigned short> v(w280::kN);
+        for (int k = 0; k < w280::kN; ++k) v[k] = static_cast<unsigned short>(w280::slot_of(k));
+        return v;
+    }();
+    return t.data();
+}
+#endif
 
 // ---------------------------------------------------------------------------
 // FC line batch
@@ -131,20 +152,20 @@ FCSG_HD void w280_load(int lane, long pair, const FcLinesArgs& a, double* v0, do
 
 template <int NL>
 FCSG_HD void w280_finish(int lane, long pair, double2* buf, const double2* mult, const double* blend,
-                         const FcLinesArgs& a, const double* v0, const double* v1) {
+                         const unsigned short* st, const FcLinesArgs& a, const double* v0, const double* v1) {
     using namespace w280;
     const long l = 2 * pair;
     const long ols = a.out_line_stride, ost = a.out_stride;
     const bool have1 = l + 1 < a.n_lines;
     constexpr int PPL = kN / NL;
 #pragma unroll
-    for (int m = 0; m < PPL; ++m) buf[slot_of(lane + NL * m)] = mk2(v0[m], v1[m]);
+    for (int m = 0; m < PPL; ++m) buf[st[lane + NL * m]] = mk2(v0[m], v1[m]);
     FCSG_SYNCWARP();
     transform<NL, 1>(lane, buf, kSlots, mult, blend);
 #pragma unroll 4
     for (int m = 0; m < PPL; ++m) {
         const int i = lane + NL * m;
-        const double2 v = buf[slot_of(i)];
+        const double2 v = buf[st[i]];
         a.out[l * ols + i * ost] = v.x * a.scale;
         if (have1) a.out[(l + 1) * ols + i * ost] = v.y * a.scale;
     }
@@ -165,7 +186,7 @@ __global__ void __launch_bounds__(kLWarps * 32) w280_lines_kernel(const __grid_c
     stage_w280_tables(threadIdx.x, kLWarps * 32, a.pl.mult_pfa + (a.mode - 1) * w280::kNE, a.pl.blend, mult, blend);
     __syncthreads();
     for (; pair < npairs; pair += static_cast<long>(gridDim.x) * kLWarps) {
-        w280_finish<32>(lane, pair, buf, mult, blend, a, v0, v1);
+        w280_finish<32>(lane, pair, buf, mult, blend, slot_table(mult), a, v0, v1);
         const long nxt = pair + static_cast<long>(gridDim.x) * kLWarps;
         if (nxt < npairs) {
             FCSG_SYNCWARP();
@@ -194,7 +215,7 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream) {
     double v0[w280::kN], v1[w280::kN];
     for (long pair = 0; pair < npairs; ++pair) {
         w280_load<1>(0, pair, a, v0, v1);
-        w280_finish<1>(0, pair, buf.data(), mult, a.pl.blend, a, v0, v1);
+        w280_finish<1>(0, pair, buf.data(), mult, a.pl.blend, host_slot_table(), a, v0, v1);
     }
 #endif
 }
@@ -227,7 +248,7 @@ FCSG_HD void w_check_positive(const EngineDev& E, double rho, double theta, long
 // (coalesced).
 template <int NL>
 FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult, const EngineDev& E,
-                          const double* blend, int stage) {
+                          const double* blend, const unsigned short* st, int stage) {
     using namespace w280;
     constexpr int PPL = kN / NL;
     constexpr int KC = PPL >= 2 ? 2 : 1;  // points per load chunk of the update epilogue (12 loads each)
@@ -257,7 +278,7 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
             const int i = lane + NL * (m0 + k);
             const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
             w_check_positive(E, q.rho, q.theta, rb + i, sub, i, row);
-            const int s = slot_of(i);
+            const int s = st[i];
             bA[s] = mk2(q.rho, q.mx);
             bB[s] = mk2(q.my, q.theta);
         }
@@ -282,7 +303,7 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
         }
 #pragma unroll
         for (int k = 0; k < KL; ++k) {
-            const int s = slot_of(lane + NL * (m0 + k));
+            const int s = st[lane + NL * (m0 + k)];
             const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
             const double2 wa = bA[s], wb = bB[s];
             const double ax = a[k] * (wa.x * inv_len), ay = a[k] * (wa.y * inv_len);
@@ -323,7 +344,7 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
             const long p = rb + lane + NL * (m0 + k);
-            const int s = slot_of(lane + NL * (m0 + k));
+            const int s = st[lane + NL * (m0 + k)];
             const double2 wa = bA[s], wb = bB[s];
             ssprk_update_e0(E, stage, 0, p, u[k][0], ta[k][0] + a[k] * (wa.x * inv_len), z[k][0], dt);
             ssprk_update_e0(E, stage, 1, p, u[k][1], ta[k][1] + a[k] * (wa.y * inv_len), z[k][1], dt);
@@ -349,7 +370,7 @@ constexpr int kQuad = 4;
 
 template <int NT>
 FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult, const EngineDev& E,
-                          const double* blend) {
+                          const double* blend, const unsigned short* st) {
     using namespace w280;
     constexpr int PPT = kQuad * kN / NT;  // points per thread
     constexpr int KC = PPT >= 4 ? 4 : 1;  // points per load chunk
@@ -366,8 +387,8 @@ FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult,
     auto row = [&](int k) { return (tid + NT * k) >> 2; };
     auto pt = [&](int k) { return gb + static_cast<long>(row(k)) * ni + col(k); };
     // line buffers: column c, line A (rho v, theta) at c * 2 kBP, line B (rho, rho u) at + kBP
-    auto bA = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + slot_of(row(k))]; };
-    auto bB = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + kBP + slot_of(row(k))]; };
+    auto bA = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + st[row(k)]]; };
+    auto bB = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + kBP + st[row(k)]]; };
     // the next epilogue's inputs into L2 behind the transforms: one thread per
     // 32-byte sector (the quad's 4 columns of one row)
     auto prefetch = [&](const double* const* f, int nf) {
@@ -479,7 +500,7 @@ __global__ void __launch_bounds__(kXThreads, 5) wpass_x_kernel(const __grid_cons
             pf_l2_bulk(E.e[lane] + static_cast<long>(sub) * E.ni * E.nj + static_cast<long>(row) * E.ni,
                        w280::kN * sizeof(double));
         }
-        wpass_x_body<32>(lane, line, buf, mult, E, blend, stage);
+        wpass_x_body<32>(lane, line, buf, mult, E, blend, slot_table(mult), stage);
     }
 }
 
@@ -501,7 +522,7 @@ __global__ void __launch_bounds__(kYThreads, 5) wpass_y_kernel(const __grid_cons
                 pf_l2(E.e[r >> 8] + gb + static_cast<long>(r & (w280::kN - 1)) * E.ni);
         }
         __syncthreads();  // tables staged; the previous quad's buffers consumed
-        wpass_y_quad<kYThreads>(threadIdx.x, quad, wsm + kTabSlots, mult, E, blend);
+        wpass_y_quad<kYThreads>(threadIdx.x, quad, wsm + kTabSlots, mult, E, blend, slot_table(mult));
     }
 }
 
@@ -550,10 +571,11 @@ void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage,
     (void)stream;
     if (rows) {
         std::vector<double2> buf(2 * kBP);
-        for (int line = 0; line < nlines; ++line) wpass_x_body<1>(0, line, buf.data(), mult, E, pl.blend, stage);
+        for (int line = 0; line < nlines; ++line)
+            wpass_x_body<1>(0, line, buf.data(), mult, E, pl.blend, host_slot_table(), stage);
     } else {
         std::vector<double2> bufs(kQuad * 2 * kBP);
-        for (int q = 0; q < nquads; ++q) wpass_y_quad<1>(0, q, bufs.data(), mult, E, pl.blend);
+        for (int q = 0; q < nquads; ++q) wpass_y_quad<1>(0, q, bufs.data(), mult, E, pl.blend, host_slot_table());
     }
 #endif
 }

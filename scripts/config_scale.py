@@ -5,7 +5,7 @@ for 1000 supersteps, config 4 (forward-facing step, problems.step_flow(4):
 superstep (CUDA events over a steady window, graph replays), the rate, the
 simulated time reached and the minimum density / pressure over all points at
 the end (no InvalidStateError = positivity held at every stage).
-    python scripts/config_scale.py [out.json]"""
+    python scripts/config_scale.py [out.json] [c3,c3_025,c3_coarse,c4]"""
 import json
 import os
 import sys
@@ -37,7 +37,11 @@ def run(name, build, steps, cfl):
     E.check_error()
     ms = a.elapsed_time(b) / timed
     t1 = time.perf_counter()
-    E.run(steps - 3 - timed)
+    failure = None
+    try:
+        E.run(steps - 3 - timed)
+    except N.InvalidStateError as ex:  # where and when positivity was lost
+        failure = {"error": str(ex), "patch": ex.patch, "subpatch": ex.subpatch, "i": ex.i, "j": ex.j, "t": ex.t}
     wall = time.perf_counter() - t1
     t, n = E.time()
     rmin = pmin = np.inf
@@ -49,15 +53,21 @@ def run(name, build, steps, cfl):
         rmin, pmin = min(rmin, rho.min()), min(pmin, p.min())
     out = {"config": name, "points": npts, "subpatches": len(dec.subs), "build_s": tb, "cfl": cfl,
            "steps": n, "t_final": t, "ms_per_step": ms, "pt_stage_per_s": 5 * npts / (ms * 1e-3),
-           "rest_wall_s": wall, "min_rho": float(rmin), "min_p": float(pmin)}
+           "rest_wall_s": wall, "min_rho": float(rmin), "min_p": float(pmin), "failure": failure}
     print(json.dumps(out), flush=True)
     E.close()
     return out
 
 
-res = [run("config3: Mach 3 cylinder, ring 3072x147 + 50 Cartesian 256^2 subpatches",
+which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["c3", "c3_025", "c3_coarse", "c4"]
+cases = {
+    "c3": ("config3: Mach 3 cylinder, ring 3072x147 + 50 Cartesian 256^2 subpatches, CFL 0.5",
            lambda: P.cylinder_flow(True, fine=True), 1000, 0.5),
-       run("config4: Mach 3 forward-facing step, step_flow(4)", lambda: P.step_flow(4), 2000, 0.25)]
+    "c3_025": ("config3: the same at CFL 0.25", lambda: P.cylinder_flow(True, fine=True), 1000, 0.25),
+    "c3_coarse": ("config3 (2.57M layout), CFL 0.5", lambda: P.cylinder_flow(True), 1000, 0.5),
+    "c4": ("config4: Mach 3 forward-facing step, step_flow(4), CFL 0.25", lambda: P.step_flow(4), 2000, 0.25),
+}
+res = [run(*cases[k]) for k in which]
 if len(sys.argv) > 1:
     with open(sys.argv[1], "w") as fh:
         json.dump(res, fh, indent=1)
