@@ -306,10 +306,10 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
             const int s = st[lane + NL * (m0 + k)];
             const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
             const double2 wa = bA[s], wb = bB[s];
-            const double ax = a[k] * (wa.x * inv_len), ay = a[k] * (wa.y * inv_len);
-            const double bx = a[k] * (wb.x * inv_len), by = a[k] * (wb.y * inv_len);
-            bA[s] = mk2(mu[k] * ax - flux_x(q, 0), mu[k] * ay - flux_x(q, 1));
-            bB[s] = mk2(mu[k] * bx - flux_x(q, 2), mu[k] * by - flux_x(q, 3));
+            // mu iq1x inv_len once per point, then one FMA per component
+            const double ms = mu[k] * (a[k] * inv_len);
+            bA[s] = mk2(fma(ms, wa.x, -flux_x(q, 0)), fma(ms, wa.y, -flux_x(q, 1)));
+            bB[s] = mk2(fma(ms, wb.x, -flux_x(q, 2)), fma(ms, wb.y, -flux_x(q, 3)));
         }
     }
     if (lane == 0) {  // the update's inputs into L2 behind the transform
@@ -346,10 +346,11 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
             const long p = rb + lane + NL * (m0 + k);
             const int s = st[lane + NL * (m0 + k)];
             const double2 wa = bA[s], wb = bB[s];
-            ssprk_update_e0(E, stage, 0, p, u[k][0], ta[k][0] + a[k] * (wa.x * inv_len), z[k][0], dt);
-            ssprk_update_e0(E, stage, 1, p, u[k][1], ta[k][1] + a[k] * (wa.y * inv_len), z[k][1], dt);
-            ssprk_update_e0(E, stage, 2, p, u[k][2], ta[k][2] + a[k] * (wb.x * inv_len), z[k][2], dt);
-            ssprk_update_e0(E, stage, 3, p, u[k][3], ta[k][3] + a[k] * (wb.y * inv_len), z[k][3], dt);
+            const double sa = a[k] * inv_len;
+            ssprk_update_e0(E, stage, 0, p, u[k][0], fma(sa, wa.x, ta[k][0]), z[k][0], dt);
+            ssprk_update_e0(E, stage, 1, p, u[k][1], fma(sa, wa.y, ta[k][1]), z[k][1], dt);
+            ssprk_update_e0(E, stage, 2, p, u[k][2], fma(sa, wb.x, ta[k][2]), z[k][2], dt);
+            ssprk_update_e0(E, stage, 3, p, u[k][3], fma(sa, wb.y, ta[k][3]), z[k][3], dt);
         }
     }
 }
@@ -450,8 +451,9 @@ FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult,
             double2& a = bA(k0 + k);
             double2& b = bB(k0 + k);
             const double2 wa = a, wb = b;
-            a = mk2(mu[k] * (d[k] * (wa.x * inv_len)) - flux_y(q, 2), mu[k] * (d[k] * (wa.y * inv_len)) - flux_y(q, 3));
-            b = mk2(mu[k] * (d[k] * (wb.x * inv_len)) - flux_y(q, 0), mu[k] * (d[k] * (wb.y * inv_len)) - flux_y(q, 1));
+            const double ms = mu[k] * (d[k] * inv_len);
+            a = mk2(fma(ms, wa.x, -flux_y(q, 2)), fma(ms, wa.y, -flux_y(q, 3)));
+            b = mk2(fma(ms, wb.x, -flux_y(q, 0)), fma(ms, wb.y, -flux_y(q, 1)));
         }
     }
     transform_all();
@@ -460,12 +462,12 @@ FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult,
     for (int k = 0; k < PPT; ++k) {
         if (col(k) >= ncol) continue;
         const long p = pt(k);
-        const double d = uq ? qc : ldg1(E.iq2y + p);
+        const double d = (uq ? qc : ldg1(E.iq2y + p)) * inv_len;
         const double2 wa = bA(k), wb = bB(k);
-        E.tA[2][p] = d * (wa.x * inv_len);
-        E.tA[3][p] = d * (wa.y * inv_len);
-        E.tA[0][p] = d * (wb.x * inv_len);
-        E.tA[1][p] = d * (wb.y * inv_len);
+        E.tA[2][p] = d * wa.x;
+        E.tA[3][p] = d * wa.y;
+        E.tA[0][p] = d * wb.x;
+        E.tA[1][p] = d * wb.y;
     }
 }
 

@@ -175,7 +175,7 @@ def initial_state(dec, ic, sub):
         return np.ascontiguousarray(ic(d.x, d.y))
 
 
-def cylinder_flow(full=True, fine=False):
+def cylinder_flow(full=True, fine=False, body="slip"):
     """BASELINE config 3 (multi-patch, curvilinear). The reference's own
     cylinder decomposition fails its overlap check, so
     the patches are laid out here: an annulus r in [1, 2.2] around the body
@@ -185,6 +185,8 @@ def cylinder_flow(full=True, fine=False):
     slip walls at y = +-6) with 256 x 256 subpatches; free stream rho = 1.4,
     p = 1, u = 3 (Mach 3). full=False: the same layout at about a quarter of
     the resolution (0.70M points; ring 512 x 83, Cartesian 138 x 138).
+    body="noslip": the body as the reference's flow-cylinder has it
+    (noslip_adiabatic, src/problems.cpp:205) instead of a slip wall.
     fine=True: BASELINE's ~4M points -- the ring at 3072 x 147 and the
     Cartesian patches cut into 6, 36, 4 and 4 subpatches of 256 x 256 (the
     cells anisotropic where a patch side does not divide evenly)."""
@@ -209,8 +211,9 @@ def cylinder_flow(full=True, fine=False):
     for p, (r, s) in zip((left, right, top, bottom), cuts):
         M.subdivide_Q(p, r, s, n0, 9)
     free = tuple(float(v) for v in conservative(1.4, 3.0, 0.0, 1.0))
+    body_bc = M.BcSpec(M.SLIP_WALL) if body == "slip" else M.BcSpec(M.NOSLIP_ADIABATIC)
     bcs = {"in": M.BcSpec(M.INFLOW, free), "out": M.BcSpec(M.SUPERSONIC_OUTFLOW), "wall": M.BcSpec(M.SLIP_WALL),
-           "body": M.BcSpec(M.SLIP_WALL)}
+           "body": body_bc}
     dec = M.build_decomposition(patches, bcs, 9, fast=True)
 
     def ic(x, y):

@@ -111,3 +111,42 @@ def test_config4_benched_size_20_steps_against_reference(gpu_ctx):
     err = np.sqrt(dn / wn)
     print(f"config4 step_flow(2), 20 steps at CFL 0.25: rel L2 per field over the domain {err}")
     assert err.max() <= 1e-8, err
+
+
+@pytest.mark.gpu
+def test_config3_positivity_loss_matches_reference(gpu_ctx):
+    """The config-3 cylinder layout (0.70M points, ref_engine_testgeom 3) at
+    the reference's CFL 0.5 from the impulsive Mach 3 start: the reference's
+    own Engine::run loses positivity at the body wall after a few steps
+    (InvalidStateError, src/euler.cpp:37-39 / src/viscosity.cpp:13-29); the
+    product must fail at the same superstep and the same point, with the
+    states equal to round-off until then."""
+    from paper_2506_19370_b200 import _native as N
+
+    from .helpers import engine_from_reference
+
+    R = ref.RefEngine.testgeom(3, 0, cfl=0.5, workers=THREADS, weight_path=EN.DEFAULT_WEIGHTS)
+    E, _ = engine_from_reference(gpu_ctx, R, EN.EngineConfig(cfl=0.5))
+    ours, last = None, None
+    for k in range(1, 40):
+        last = [E.get_state(s) for s in range(R.nsubs)]  # the state after step k - 1
+        try:
+            E.run(1)
+        except N.InvalidStateError as ex:
+            ours = (k, ex.patch, ex.subpatch, ex.i, ex.j)
+            break
+    assert ours is not None, "the product did not lose positivity within 40 steps"
+    R.run(ours[0] - 1)
+    dn = wn = 0.0
+    for s in range(R.nsubs):
+        want = R.get_state(s)
+        dn += float(((last[s] - want) ** 2).sum())
+        wn += float((want ** 2).sum())
+    assert (dn / wn) ** 0.5 <= 1e-8, (dn / wn) ** 0.5
+    with pytest.raises(Exception) as ei:
+        R.run(ours[0] + 5)
+    msg = str(ei.value)
+    assert R.time()[1] == ours[0] - 1, (R.time(), ours)
+    assert f"patch {ours[1]} subpatch {ours[2]} ({ours[3]},{ours[4]})" in msg, (msg, ours)
+    print(f"config3 layout: positivity lost at step {ours[0]}, patch {ours[1]} subpatch {ours[2]} "
+          f"({ours[3]},{ours[4]}) in both; reference: {msg}")
