@@ -77,17 +77,28 @@ std::vector<double> extension(const FcOperator& op, const double* in, int stride
 }
 
 // unnormalised forward DFT bins 0..n_ext/2 of a real sequence (FFTW's r2c
-// convention), summed in long double
+// convention), summed in long double over a cached root table per length
 std::vector<std::pair<long double, long double>> dft_half(const std::vector<double>& x) {
+    static std::mutex m;
+    static std::map<int, std::vector<std::pair<long double, long double>>> roots;
     const int n = static_cast<int>(x.size());
-    const long double w = 2.0L * 3.14159265358979323846264338327950288L / n;
+    const std::vector<std::pair<long double, long double>>* r;
+    {
+        std::lock_guard<std::mutex> lock(m);
+        auto& t = roots[n];
+        if (t.empty()) {
+            const long double w = 2.0L * 3.14159265358979323846264338327950288L / n;
+            t.resize(n);
+            for (int j = 0; j < n; ++j) t[j] = {std::cos(w * j), std::sin(w * j)};
+        }
+        r = &t;
+    }
     std::vector<std::pair<long double, long double>> out(n / 2 + 1);
     for (int k = 0; k <= n / 2; ++k) {
         long double re = 0.0L, im = 0.0L;
-        for (int j = 0; j < n; ++j) {
-            const long double a = w * static_cast<long double>((static_cast<long>(k) * j) % n);
-            re += x[j] * std::cos(a);
-            im -= x[j] * std::sin(a);
+        for (int j = 0, kj = 0; j < n; ++j, kj = (kj + k) % n) {
+            re += x[j] * (*r)[kj].first;
+            im -= x[j] * (*r)[kj].second;
         }
         out[k] = {re, im};
     }
@@ -105,6 +116,7 @@ FcOperator::FcOperator(int n_points, int n_cont, FilterSpec filter) : n_(n_point
     if (n_points < 10) throw ConfigError("FcOperator: n_points must be >= 10");
     if (n_cont < 4) throw ConfigError("FcOperator: n_cont must be >= 4");
     impl_ = std::make_unique<Impl>();
+    blend_ = &blend_matrix(n_cont_);  // takes the GPU lock itself (not held here: std::mutex is not recursive)
     std::lock_guard<std::mutex> lock(gpu_mutex());
     fcsg_ctx* c = context();
     raise(c, fcsg_operator(c, n_points, n_cont, degree, filter.alpha, filter.p, filter.p_smear, &impl_->op_id));
@@ -113,7 +125,6 @@ FcOperator::FcOperator(int n_points, int n_cont, FilterSpec filter) : n_(n_point
     smear_profile_.resize(n_modes_);
     raise(c, fcsg_operator_info(c, impl_->op_id, nullptr, nullptr, nullptr, nullptr, filter_profile_.data(),
                                 smear_profile_.data()));
-    blend_ = &blend_matrix(n_cont_);
 }
 
 FcOperator::~FcOperator() = default;
