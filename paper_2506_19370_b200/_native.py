@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfcsg.so")
+LIB_PATH = os.environ.get("FCSG_LIB") or os.path.join(HERE, "lib", "libfcsg.so")  # override: A/B experiments
 EMU_PATH = os.environ.get("FCSG_EMU_LIB") or os.path.join(os.path.dirname(HERE), "build", "emu", "libfcsg_emu.so")
 
 # include/fcsg.h error kinds -> reference exception names (include/fcs/errors.hpp)

@@ -2142,6 +2142,14 @@ void launch_phase2(const std::vector<GroupLaunch>& G, bool step0, void* stream) 
             dilate_body(Thr{0, 1}, 0, 1, g.E);
 #endif
         }
+        // steady steps on whole 256-point lines: the warp transform
+        const bool full = g.rows.size() == 1 && g.cols.size() == 1 && g.rows[0].desc[0] == nullptr;
+        if (!step0 && full && wpass_applies(g.E, g.rows[0].pl, true) && wpass_applies(g.E, g.cols[0].pl, false) &&
+            use_warp_passes()) {
+            launch_wfilter(g.E, g.rows[0].pl, true, stream);
+            launch_wfilter(g.E, g.cols[0].pl, false, stream);
+            continue;
+        }
         run_rows<PassFR>(step0 ? 1 : 0, g, stream);
         run_cols<PassFC>(step0 ? 1 : 0, g, stream);
     }

@@ -186,6 +186,9 @@ int step_scr_cap(const FcPlanDev& pl);
 // transform (wpass.cu): rows = pass X, else pass Y (stage = RK stage)
 bool wpass_applies(const EngineDev& E, const FcPlanDev& pl, bool rows);
 void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage, void* stream);
+// the phase-2 per-step filter (steady steps) on the same transform: rows
+// (e -> tF) or columns (tF -> e)
+void launch_wfilter(const EngineDev& E, const FcPlanDev& pl, bool rows, void* stream);
 // dynamic shared memory of a line-pass CTA (lb lines, `slots` staging doubles
 // per point) and the per-CTA opt-in limit of sm_100a (227 KB)
 constexpr size_t kMaxLinePassSmem = 227 * 1024;

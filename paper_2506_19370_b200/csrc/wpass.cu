@@ -17,6 +17,7 @@
 // loads and epilogues (coalesced along rows), and the butterflies of the
 // transform (wline.h).
 #include <algorithm>
+#include <cstdlib>
 
 #include "dev.h"
 #include "fc_lines.h"
@@ -232,7 +233,10 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream) {
 // (L1 / L2 hits) instead of kept: pass Y updates e only in its last
 // epilogue, so the state it reads there is still the stage's input.
 
-constexpr int kBP = w280::kSlots + 1;  // pitch between line buffers (double2): odd, spreads the quad's buffers over the banks
+// pitch between line buffers (double2): 313 = 1 (mod 8) spreads the quad's
+// buffers over the banks (309 and 311, which would fit a fifth CTA per SM,
+// measured 5-9% slower passes at either 4 or 5 CTAs)
+constexpr int kBP = w280::kSlots + 1;
 
 // interior positivity diagnostic of euler_rhs (src/euler.cpp:37-39)
 FCSG_HD void w_check_positive(const EngineDev& E, double rho, double theta, long p, int sub, int i, int j) {
@@ -471,6 +475,101 @@ FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult,
     }
 }
 
+// ---------------------------------------------------------------------------
+// Phase-2 filter of steady steps on the warp transform (filter_field,
+// src/subpatch_data.cpp:30-44, src/runtime.cpp:403-421: rows then columns of
+// rho, rho u, rho v, theta, then E rebuilt), the PassFR / PassFC pair of
+// step_kernels.cu restated per warp. Rows: one row per warp, the conserved
+// state -> (rho, rho u) | (rho v, theta) -> filter -> tF. Columns: one
+// column quad per CTA, tF -> filter -> e, E = rho theta / (gamma - 1) +
+// |m|^2 / (2 rho).
+
+template <int NL>
+FCSG_HD void wfilter_x_body(int lane, int line, double2* buf, const double2* mult, const EngineDev& E,
+                            const double* blend, const unsigned short* st) {
+    using namespace w280;
+    constexpr int PPL = kN / NL;
+    constexpr int KL = PPL >= 4 ? 4 : 1;
+    const int ni = E.ni, nj = E.nj;
+    const int sub = line / nj, row = line - sub * nj;
+    const long rb = static_cast<long>(sub) * ni * nj + static_cast<long>(row) * ni;
+    double2* bA = buf;
+    double2* bB = buf + kBP;
+#pragma unroll 1
+    for (int m0 = 0; m0 < PPL; m0 += KL) {
+        double v[KL][4];
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const long p = rb + lane + NL * (m0 + k);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[k][c] = ldg1(E.e[c] + p);
+        }
+#pragma unroll
+        for (int k = 0; k < KL; ++k) {
+            const double rho = v[k][0], mx = v[k][1], my = v[k][2], En = v[k][3];
+            const int s = st[lane + NL * (m0 + k)];
+            bA[s] = mk2(rho, mx);
+            bB[s] = mk2(my, kGm1 * (En - 0.5 * (mx * mx + my * my) / rho) / rho);
+        }
+    }
+    FCSG_SYNCWARP();
+    transform<NL, 2>(lane, buf, kBP, mult, blend);
+#pragma unroll 4
+    for (int m = 0; m < PPL; ++m) {
+        const int i = lane + NL * m;
+        const long p = rb + i;
+        const int s = st[i];
+        const double2 a = bA[s], b = bB[s];
+        E.tF[0][p] = a.x;
+        E.tF[1][p] = a.y;
+        E.tF[2][p] = b.x;
+        E.tF[3][p] = b.y;
+    }
+}
+
+template <int NT>
+FCSG_HD void wfilter_y_quad(int tid, int quad, double2* bufs, const double2* mult, const EngineDev& E,
+                            const double* blend, const unsigned short* st) {
+    using namespace w280;
+    constexpr int PPT = kQuad * kN / NT;
+    const int ni = E.ni, nj = E.nj;
+    const int qps = (ni + kQuad - 1) / kQuad;
+    const int sub = quad / qps, c0 = (quad - sub * qps) * kQuad;
+    const long gb = static_cast<long>(sub) * ni * nj + c0;
+    const int ncol = ni - c0 < kQuad ? ni - c0 : kQuad;
+    auto col = [&](int k) { return (tid + NT * k) & (kQuad - 1); };
+    auto row = [&](int k) { return (tid + NT * k) >> 2; };
+    auto pt = [&](int k) { return gb + static_cast<long>(row(k)) * ni + col(k); };
+    auto bA = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + st[row(k)]]; };
+    auto bB = [&](int k) -> double2& { return bufs[col(k) * 2 * kBP + kBP + st[row(k)]]; };
+#pragma unroll 4
+    for (int k = 0; k < PPT; ++k) {
+        const bool ok = col(k) < ncol;
+        const long p = ok ? pt(k) : gb;
+        bA(k) = ok ? mk2(ldg1(E.tF[0] + p), ldg1(E.tF[1] + p)) : mk2(1.0, 0.0);
+        bB(k) = ok ? mk2(ldg1(E.tF[2] + p), ldg1(E.tF[3] + p)) : mk2(0.0, 1.0);
+    }
+    FCSG_SYNC();
+#if FCSG_CUDA
+    const int warp = tid >> 5;
+    if (warp < kQuad) transform<32, 2>(tid & 31, bufs + warp * 2 * kBP, kBP, mult, blend);
+#else
+    for (int c = 0; c < kQuad; ++c) transform<1, 2>(0, bufs + c * 2 * kBP, kBP, mult, blend);
+#endif
+    FCSG_SYNC();
+#pragma unroll 4
+    for (int k = 0; k < PPT; ++k) {
+        if (col(k) >= ncol) continue;
+        const long p = pt(k);
+        const double2 a = bA(k), b = bB(k);
+        const double rho = a.x, mx = a.y, my = b.x;
+        E.e[0][p] = rho;
+        E.e[1][p] = mx;
+        E.e[2][p] = my;
+        E.e[3][p] = rho * b.y / kGm1 + 0.5 * (mx * mx + my * my) / rho;
+    }
+}
+
 #if FCSG_CUDA
 // pass X: CTA of kXWarps independent warps, each with two line buffers
 constexpr int kXWarps = 4;
@@ -528,6 +627,35 @@ __global__ void __launch_bounds__(kYThreads, 5) wpass_y_kernel(const __grid_cons
     }
 }
 
+__global__ void __launch_bounds__(kXThreads, 5) wfilter_x_kernel(const __grid_constant__ EngineDev E,
+                                                                 const double2* __restrict__ mult_src,
+                                                                 const double* __restrict__ blend_src) {
+    extern __shared__ double2 wsm[];
+    double2* mult = wsm;
+    double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
+    stage_w280_tables(threadIdx.x, kXThreads, mult_src, blend_src, mult, blend);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* buf = wsm + kTabSlots + warp * 2 * kBP;
+    const int nlines = E.S * E.nj;
+    for (int line = blockIdx.x * kXWarps + warp; line < nlines; line += gridDim.x * kXWarps)
+        wfilter_x_body<32>(lane, line, buf, mult, E, blend, slot_table(mult));
+}
+
+__global__ void __launch_bounds__(kYThreads, 5) wfilter_y_kernel(const __grid_constant__ EngineDev E,
+                                                                 const double2* __restrict__ mult_src,
+                                                                 const double* __restrict__ blend_src) {
+    extern __shared__ double2 wsm[];
+    double2* mult = wsm;
+    double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
+    stage_w280_tables(threadIdx.x, kYThreads, mult_src, blend_src, mult, blend);
+    const int nquads = E.S * ((E.ni + kQuad - 1) / kQuad);
+    for (int quad = blockIdx.x; quad < nquads; quad += gridDim.x) {
+        __syncthreads();
+        wfilter_y_quad<kYThreads>(threadIdx.x, quad, wsm + kTabSlots, mult, E, blend, slot_table(mult));
+    }
+}
+
 // resident CTAs of a kernel (grid of the persistent launches), per device
 template <class K>
 int resident_ctas(K kernel, int threads, size_t smem, unsigned long long* done, int* cache) {
@@ -537,6 +665,7 @@ int resident_ctas(K kernel, int threads, size_t smem, unsigned long long* done, 
         int sms = 0, per = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+        if (const char* v = std::getenv("FCSG_WPASS_MAX_CTAS")) per = std::min(per, std::atoi(v));  // experiments
         cache[d & 63] = sms * (per > 0 ? per : 1);
     }
     return cache[d & 63];
@@ -578,6 +707,40 @@ void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage,
     } else {
         std::vector<double2> bufs(kQuad * 2 * kBP);
         for (int q = 0; q < nquads; ++q) wpass_y_quad<1>(0, q, bufs.data(), mult, E, pl.blend, host_slot_table());
+    }
+#endif
+}
+
+void launch_wfilter(const EngineDev& E, const FcPlanDev& pl, bool rows, void* stream) {
+    const int nlines = E.S * (rows ? E.nj : E.ni);
+    if (nlines == 0) return;
+    const double2* mult = pl.mult_pfa + 2 * w280::kNE;  // mode 3: the per-step filter
+    const int nquads = E.S * ((E.ni + kQuad - 1) / kQuad);
+#if FCSG_CUDA
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static unsigned long long done = 0, occ_x = 0, occ_y = 0;
+    static int res_x[64], res_y[64];
+    if (dev::first_on_device(&done)) {
+        cudaFuncSetAttribute(wfilter_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kXSmem));
+        cudaFuncSetAttribute(wfilter_y_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kYSmem));
+    }
+    if (rows) {
+        const int need = (nlines + kXWarps - 1) / kXWarps;
+        const int grid = std::min(need, resident_ctas(wfilter_x_kernel, kXThreads, kXSmem, &occ_x, res_x));
+        wfilter_x_kernel<<<grid, kXThreads, kXSmem, s>>>(E, mult, pl.blend);
+    } else {
+        const int grid = std::min(nquads, resident_ctas(wfilter_y_kernel, kYThreads, kYSmem, &occ_y, res_y));
+        wfilter_y_kernel<<<grid, kYThreads, kYSmem, s>>>(E, mult, pl.blend);
+    }
+#else
+    (void)stream;
+    if (rows) {
+        std::vector<double2> buf(2 * kBP);
+        for (int line = 0; line < nlines; ++line)
+            wfilter_x_body<1>(0, line, buf.data(), mult, E, pl.blend, host_slot_table());
+    } else {
+        std::vector<double2> bufs(kQuad * 2 * kBP);
+        for (int q = 0; q < nquads; ++q) wfilter_y_quad<1>(0, q, bufs.data(), mult, E, pl.blend, host_slot_table());
     }
 #endif
 }
