@@ -289,8 +289,8 @@ int fcsg_engine_copy_dtmin(fcsg_engine* eng, void* d_buf, int to_engine);
  * (src/runtime.cpp:352-371, 433-454, 482-512).
  * fcsg_comm_unique_id: a rendezvous id (ncclUniqueId, 128 bytes) made on rank
  * 0 and broadcast by the caller. fcsg_engine_attach_comm (collective, after
- * finalize and the halo lists): peers = the other ranks this one exchanges
- * with, ascending; per peer the number of values (points) in the packed send
+ * finalize and the halo lists): peers = the ranks this one exchanges with,
+ * ascending (itself allowed: a send to self); per peer the number of values (points) in the packed send
  * and receive buffers of the state and mu_hat halos, in that peer order (the
  * sums equal fcsg_engine_halo_size 0..3). */
 int fcsg_comm_unique_id(char* id);

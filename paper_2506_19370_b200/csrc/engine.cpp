@@ -121,10 +121,21 @@ void Engine::layout() {
         size_t g = 0;
         while (g < groups_.size() && !(groups_[g].ni == sp.ni && groups_[g].nj == sp.nj)) ++g;
         if (g == groups_.size()) {
-            groups_.push_back(Group{sp.ni, sp.nj, 0, 0, 0});
+            groups_.push_back(Group{sp.ni, sp.nj, 0, 0, 0, 0});
             members.emplace_back();
         }
         members[g].push_back(id);
+    }
+    // multi-rank: inside each group the subpatches owning donors of the state
+    // halo come first, so a stage's edge run can be passed, packed and sent
+    // while the interior run is still being passed (enqueue_step)
+    std::vector<char> edge(subs_.size(), 0);
+    for (const auto& h : halo_e_src_)
+        if (h.first >= 0 && h.first < static_cast<int>(subs_.size())) edge[h.first] = 1;
+    for (size_t g = 0; g < groups_.size(); ++g) {
+        auto& m = members[g];
+        std::stable_partition(m.begin(), m.end(), [&](int id) { return edge[id] != 0; });
+        groups_[g].n_edge = static_cast<int>(std::count_if(m.begin(), m.end(), [&](int id) { return edge[id] != 0; }));
     }
     slot_of_.assign(subs_.size(), -1);
     id_of_slot_.clear();
@@ -253,8 +264,7 @@ void Engine::set_plan_interps(int which, std::vector<int> dst_sub, std::vector<i
 void Engine::set_halo(std::vector<int> e_sub, std::vector<int> e_loc, long n_recv_e, std::vector<int> mu_sub,
                       std::vector<int> mu_loc, long n_recv_mu) {
     if (finalized_) throw Error(kUsage, "engine already finalized");
-    layout();
-    if (have_plan_) throw Error(kUsage, "set the halo before the plan");
+    if (laid_out_) throw Error(kUsage, "set the halo before the plan");  // the layout orders edge subpatches first
     if (e_sub.size() != e_loc.size() || mu_sub.size() != mu_loc.size() || n_recv_e < 0 || n_recv_mu < 0)
         throw Error(kUsage, "bad halo lists");
     halo_e_src_.clear();
@@ -311,8 +321,10 @@ void Engine::attach_comm(std::unique_ptr<Comm> comm, std::vector<int> peers, std
     if (e_send.size() != np || e_recv.size() != np || mu_send.size() != np || mu_recv.size() != np)
         throw Error(kUsage, "per-peer count lists must match the peer list");
     for (size_t k = 0; k < np; ++k) {
-        if (peers[k] < 0 || peers[k] >= comm->size() || peers[k] == comm->rank() || (k && peers[k] <= peers[k - 1]))
-            throw Error(kUsage, "peers must be distinct other ranks in ascending order");
+        // (a rank may list itself: NCCL sends to self, which the self-exchange
+        // GPU test uses to drive the transport on one device)
+        if (peers[k] < 0 || peers[k] >= comm->size() || (k && peers[k] <= peers[k - 1]))
+            throw Error(kUsage, "peers must be distinct ranks in ascending order");
         if (e_send[k] < 0 || e_recv[k] < 0 || mu_send[k] < 0 || mu_recv[k] < 0) throw Error(kUsage, "negative count");
     }
     const long want[4] = {static_cast<long>(halo_e_.size()), n_recv_e_, static_cast<long>(halo_mu_.size()),
@@ -717,6 +729,7 @@ void Engine::finalize() {
     // line; line sets per orientation and length
     G_.clear();
     chunks_.clear();
+    chunk_edge_.clear();
     bool all_cart = true;
     // view of slots [g.slot0 + k0, g.slot0 + k0 + n) of group g
     auto make_view = [&](const Group& g, int k0, int n) {
@@ -857,16 +870,27 @@ void Engine::finalize() {
         // (a chunk keeps >= kChunkPoints points: smaller kernels lose more to
         // launch gaps than they gain from the overlap)
         const long by_size = static_cast<long>(g.n) * g.ni * g.nj / kChunkPoints;
-        const int nch = any_l ? 1 : static_cast<int>(std::max(1L, std::min<long>({by_size, cfg_.stage_chunks, g.n})));
+        std::vector<int> cuts;  // chunk boundaries in the group's slots
+        if (!halo_e_src_.empty()) {
+            // multi-rank: the edge run, then the interior run (L-shaped
+            // groups, whose line runs are not split, stay whole)
+            cuts = {0};
+            if (!any_l && g.n_edge > 0 && g.n_edge < g.n) cuts.push_back(g.n_edge);
+            cuts.push_back(g.n);
+        } else {
+            const int nch = any_l ? 1 : static_cast<int>(std::max(1L, std::min<long>({by_size, cfg_.stage_chunks, g.n})));
+            for (int c = 0; c <= nch; ++c) cuts.push_back(static_cast<int>(static_cast<long>(g.n) * c / nch));
+        }
+        const int nch = static_cast<int>(cuts.size()) - 1;
         for (int c = 0; c < nch; ++c) {
-            const int k0 = static_cast<int>(static_cast<long>(g.n) * c / nch);
-            const int k1 = static_cast<int>(static_cast<long>(g.n) * (c + 1) / nch);
+            const int k0 = cuts[c], k1 = cuts[c + 1];
             GroupLaunch cl = gl;
             if (nch > 1) {
                 cl.E = make_view(g, k0, k1 - k0);
                 cl.E.cartesian = V.cartesian;
             }
             chunks_.push_back({cl});
+            chunk_edge_.push_back(k0 < g.n_edge ? 1 : 0);
         }
         G_.push_back(std::move(gl));
     }
@@ -1233,8 +1257,32 @@ void Engine::enqueue_step(bool step0) {
     // and fills each kernel's last wave with the next kernel's blocks.
     const bool chunked = dev::is_cuda() && chunks_.size() > 1;
     if (chunked) ensure_streams();
+    bool edge_first = false;  // multi-rank with an edge / interior split
+    for (size_t c = 0; c < chunk_edge_.size(); ++c) edge_first = edge_first || (comm_ && !chunk_edge_[c]);
+    edge_first = edge_first && chunked;
     for (int st = 0; st < 5; ++st) {
         const Range stage_range(kStageRange[st]);
+        if (edge_first) {
+            // the edge runs' passes and BCs, then their halo (pack, grouped
+            // ncclSend/Recv, unpack) on stream 0; the interior runs' passes on
+            // the other streams meanwhile; the exchange after both
+            const int ns = static_cast<int>(cstreams_.size());
+            dev::record(ev_stage_, s);
+            for (int k = 0; k < ns; ++k) dev::wait(cstreams_[k], ev_stage_);
+            int next = 1;
+            for (size_t c = 0; c < chunks_.size(); ++c) {
+                void* cs = chunk_edge_[c] ? cstreams_[0] : cstreams_[1 + (next++ - 1) % (ns - 1)];
+                launch_stage(chunks_[c], st, cs);
+                launch_bc(chunks_[c], cs);
+            }
+            halo(0, cstreams_[0]);
+            for (int k = 0; k < ns; ++k) {
+                dev::record(cevents_[k], cstreams_[k]);
+                dev::wait(s, cevents_[k]);
+            }
+            launch_exchange(E_, s);
+            continue;
+        }
         if (chunked) {
             const int ns = std::min(static_cast<int>(cstreams_.size()), static_cast<int>(chunks_.size()));
             dev::record(ev_stage_, s);

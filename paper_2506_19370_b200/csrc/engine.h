@@ -167,6 +167,7 @@ class Engine {
     struct Group {
         int ni, nj, slot0, n;
         long p0;
+        int n_edge;  // multi-rank: the first n_edge slots own donors other ranks read (edge-first order)
     };
     std::vector<Group> groups_;
     std::vector<int> slot_of_, id_of_slot_;
@@ -174,6 +175,7 @@ class Engine {
     EngineDev E_{};                         // global view
     std::vector<GroupLaunch> G_;            // group views + line sets
     std::vector<std::vector<GroupLaunch>> chunks_;  // stage chunks (one view each)
+    std::vector<char> chunk_edge_;                  // multi-rank: the chunk holds donors of the state halo
     std::vector<void*> allocs_;
     double* pool_ = nullptr;
     std::vector<double> mlp_;
