@@ -35,6 +35,22 @@ constexpr int kWThreads = kWarps * 32;
 // conservative -> primitive as prim_of (src/euler.cpp:29-41) with one
 // reciprocal of the density instead of four divisions per point (the
 // products differ from the quotients by an ulp, far inside the parity gates)
+// 1/x without the IEEE division's special-case branch: the SFU's approximate
+// reciprocal (rcp.approx.ftz.f64, ~2^-23 relative) refined by three Newton
+// steps (~2^-52: an ulp). x is a positive, finite density here (a
+// nonpositive or non-finite one is reported by the positivity check
+// regardless of its reciprocal).
+FCSG_HD double recip(double x) {
+#if FCSG_CUDA && !defined(FCSG_EXACT_DIV)
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return fma(r, fma(-x, r, 1.0), r);
+#else
+    return 1.0 / x;
+#endif
+}
 struct PrimR {
     double rho, mx, my, E, ir, theta, p;
 };
@@ -44,7 +60,7 @@ FCSG_HD PrimR prim_r(double rho, double mx, double my, double E) {
     q.mx = mx;
     q.my = my;
     q.E = E;
-    q.ir = 1.0 / ((rho != 0.0) ? rho : 1e-300);
+    q.ir = recip((rho != 0.0) ? rho : 1e-300);
     const double pr = kGm1 * (E - 0.5 * (mx * mx + my * my) * q.ir);
     q.theta = pr * q.ir;
     q.p = rho * q.theta;
@@ -255,7 +271,7 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
                           const double* blend, const unsigned short* st, int stage) {
     using namespace w280;
     constexpr int PPL = kN / NL;
-    constexpr int KC = PPL >= 2 ? 2 : 1;  // points per load chunk of the update epilogue (12 loads each)
+    constexpr int KC = 1;  // points per load chunk of the update epilogue (13 loads: one point; 2 and 4 measured slower)
     constexpr int KL = PPL >= 4 ? 4 : 1;  // points per load chunk of the other phases
     const int ni = E.ni, nj = E.nj;
     const int sub = line / nj, row = line - sub * nj;
