@@ -149,15 +149,20 @@ inline const unsigned short* host_slot_table() {
 // One complex line (two real lines) per warp, one pass over the batch: a
 // single wave for config 1 (2048 pairs). The kernel is latency-bound (16 MB
 // moved in a few microseconds), so every lane issues all 16 of its loads at
-// once, before the CTA stages the operator tables, and CTAs are two warps so
-// the 2048 warps spread evenly (14 per SM).
+// once, before the CTA stages the operator tables. Measured (graph-timed,
+// config 1): 2 lines per warp in 4-warp CTAs 9.9 us, 2-warp CTAs 10.1,
+// 1-warp 11.1; one real line per warp (twice the warps, the imaginary half
+// idle) 14.5-16.3.
 
-template <int NL>
-FCSG_HD void w280_load(int lane, long pair, const FcLinesArgs& a, double* v0, double* v1) {
+// RPW real lines per warp: 2 (one complex transform carries two lines, the
+// default) or 1 (the imaginary half idle: twice the warps for the same lines,
+// more latency hiding for the same single wave -- an A/B variant)
+template <int NL, int RPW>
+FCSG_HD void w280_load(int lane, long unit, const FcLinesArgs& a, double* v0, double* v1) {
     using namespace w280;
-    const long l = 2 * pair;
+    const long l = RPW * unit;
     const long ls = a.line_stride, st = a.stride;
-    const bool have1 = l + 1 < a.n_lines;
+    const bool have1 = RPW == 2 && l + 1 < a.n_lines;
     constexpr int PPL = kN / NL;
 #pragma unroll
     for (int m = 0; m < PPL; ++m) {
@@ -167,13 +172,13 @@ FCSG_HD void w280_load(int lane, long pair, const FcLinesArgs& a, double* v0, do
     }
 }
 
-template <int NL>
-FCSG_HD void w280_finish(int lane, long pair, double2* buf, const double2* mult, const double* blend,
+template <int NL, int RPW>
+FCSG_HD void w280_finish(int lane, long unit, double2* buf, const double2* mult, const double* blend,
                          const unsigned short* st, const FcLinesArgs& a, const double* v0, const double* v1) {
     using namespace w280;
-    const long l = 2 * pair;
+    const long l = RPW * unit;
     const long ols = a.out_line_stride, ost = a.out_stride;
-    const bool have1 = l + 1 < a.n_lines;
+    const bool have1 = RPW == 2 && l + 1 < a.n_lines;
     constexpr int PPL = kN / NL;
 #pragma unroll
     for (int m = 0; m < PPL; ++m) buf[st[lane + NL * m]] = mk2(v0[m], v1[m]);
@@ -189,27 +194,36 @@ FCSG_HD void w280_finish(int lane, long pair, double2* buf, const double2* mult,
 }
 
 #if FCSG_CUDA
-constexpr int kLWarps = 2;  // warps per CTA of the line batch
-__global__ void __launch_bounds__(kLWarps * 32) w280_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+template <int RPW, int WPC>
+__global__ void __launch_bounds__(WPC * 32) w280_lines_kernel(const __grid_constant__ FcLinesArgs a) {
     extern __shared__ double2 wsm[];
     double2* mult = wsm;
     double* blend = reinterpret_cast<double*>(wsm + w280::kNE);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double2* buf = wsm + kTabSlots + warp * w280::kSlots;
-    const long npairs = (a.n_lines + 1) / 2;
-    long pair = static_cast<long>(blockIdx.x) * kLWarps + warp;
+    const long nunits = (a.n_lines + RPW - 1) / RPW;
+    long unit = static_cast<long>(blockIdx.x) * WPC + warp;
     double v0[w280::kN / 32], v1[w280::kN / 32];
-    if (pair < npairs) w280_load<32>(lane, pair, a, v0, v1);  // in flight while the tables are staged
-    stage_w280_tables(threadIdx.x, kLWarps * 32, a.pl.mult_pfa + (a.mode - 1) * w280::kNE, a.pl.blend, mult, blend);
+    if (unit < nunits) w280_load<32, RPW>(lane, unit, a, v0, v1);  // in flight while the tables are staged
+    stage_w280_tables(threadIdx.x, WPC * 32, a.pl.mult_pfa + (a.mode - 1) * w280::kNE, a.pl.blend, mult, blend);
     __syncthreads();
-    for (; pair < npairs; pair += static_cast<long>(gridDim.x) * kLWarps) {
-        w280_finish<32>(lane, pair, buf, mult, blend, slot_table(mult), a, v0, v1);
-        const long nxt = pair + static_cast<long>(gridDim.x) * kLWarps;
-        if (nxt < npairs) {
+    for (; unit < nunits; unit += static_cast<long>(gridDim.x) * WPC) {
+        w280_finish<32, RPW>(lane, unit, buf, mult, blend, slot_table(mult), a, v0, v1);
+        const long nxt = unit + static_cast<long>(gridDim.x) * WPC;
+        if (nxt < nunits) {
             FCSG_SYNCWARP();
-            w280_load<32>(lane, nxt, a, v0, v1);
+            w280_load<32, RPW>(lane, nxt, a, v0, v1);
         }
     }
+}
+
+template <int RPW, int WPC>
+void launch_w280_variant(const FcLinesArgs& a, cudaStream_t s) {
+    const long nunits = (a.n_lines + RPW - 1) / RPW;
+    const size_t smem = (kTabSlots + WPC * w280::kSlots) * sizeof(double2);
+    const long nblk = (nunits + WPC - 1) / WPC;
+    const int grid = static_cast<int>(std::min<long>(nblk, 148L * 64));
+    w280_lines_kernel<RPW, WPC><<<grid, WPC * 32, smem, s>>>(a);
 }
 #endif
 
@@ -218,21 +232,30 @@ bool w280_lines_applies(const FcPlanDev& pl) {
 }
 
 void launch_w280_lines(const FcLinesArgs& a, void* stream) {
-    const long npairs = (a.n_lines + 1) / 2;
-    if (npairs == 0) return;
+    if (a.n_lines == 0) return;
 #if FCSG_CUDA
-    const size_t smem = (kTabSlots + kLWarps * w280::kSlots) * sizeof(double2);
-    const long nblk = (npairs + kLWarps - 1) / kLWarps;
-    const int grid = static_cast<int>(std::min<long>(nblk, 148L * 64));
-    w280_lines_kernel<<<grid, kLWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(a);
+    static const int variant = [] {  // A/B experiments: FCSG_W280_VARIANT = RPW * 10 + WPC
+        const char* v = std::getenv("FCSG_W280_VARIANT");
+        return v ? std::atoi(v) : 24;  // 2 lines per warp, 4-warp CTAs (measured best of 11..24)
+    }();
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (variant) {
+        case 11: launch_w280_variant<1, 1>(a, s); break;
+        case 12: launch_w280_variant<1, 2>(a, s); break;
+        case 14: launch_w280_variant<1, 4>(a, s); break;
+        case 21: launch_w280_variant<2, 1>(a, s); break;
+        case 22: launch_w280_variant<2, 2>(a, s); break;
+        default: launch_w280_variant<2, 4>(a, s); break;
+    }
 #else
     (void)stream;
+    const long npairs = (a.n_lines + 1) / 2;
     std::vector<double2> buf(w280::kSlots);
     const double2* mult = a.pl.mult_pfa + (a.mode - 1) * w280::kNE;
     double v0[w280::kN], v1[w280::kN];
     for (long pair = 0; pair < npairs; ++pair) {
-        w280_load<1>(0, pair, a, v0, v1);
-        w280_finish<1>(0, pair, buf.data(), mult, a.pl.blend, host_slot_table(), a, v0, v1);
+        w280_load<1, 2>(0, pair, a, v0, v1);
+        w280_finish<1, 2>(0, pair, buf.data(), mult, a.pl.blend, host_slot_table(), a, v0, v1);
     }
 #endif
 }

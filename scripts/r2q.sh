@@ -1,4 +1,4 @@
-for rep in 1 2; do
-for v in best xkl2 ykc2 ykc8; do
-  echo "== $v"; FCSG_LIB=paper_2506_19370_b200/lib/ab_$v.so timeout 600 python scripts/time_groups.py 2>&1 | grep -E "config5|pass_"
-done; done
+timeout 300 python -m pytest tests/test_kernels.py -m gpu -q -x -k "fc or line or deriv" 2>&1 | tail -1
+for v in 22 21 24 11 12 14; do
+  echo "== variant $v"; FCSG_W280_VARIANT=$v timeout 300 python scripts/fc_timing.py 2>&1 | tail -1
+done
