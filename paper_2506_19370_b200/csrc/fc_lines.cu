@@ -92,6 +92,10 @@ int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {
 }
 
 void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
+    if (wct_lines_applies(a) && !std::getenv("FCSG_NO_WCT_LINES") && !std::getenv("FCSG_NO_WARP_LINES")) {
+        launch_wct_lines(a, stream);
+        return;
+    }
     if (w280_lines_applies(a.pl) && !std::getenv("FCSG_NO_WARP_LINES")) {
         launch_w280_lines(a, stream);
         return;

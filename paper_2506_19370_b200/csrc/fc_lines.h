@@ -29,5 +29,9 @@ void launch_fc_lines(FcLinesArgs a, int LB, void* stream);
 // operator (n_ext = 280); launch_fc_lines takes it when it applies
 bool w280_lines_applies(const FcPlanDev& pl);
 void launch_w280_lines(const FcLinesArgs& a, void* stream);
+// the register-resident 8 x 35 kernel (wct280.h) for rows (stride 1) of the
+// same operator; launch_fc_lines prefers it
+bool wct_lines_applies(const FcLinesArgs& a);
+void launch_wct_lines(const FcLinesArgs& a, void* stream);
 
 }  // namespace fcsg

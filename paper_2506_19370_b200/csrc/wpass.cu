@@ -23,6 +23,7 @@
 #include "fc_lines.h"
 #include "pass_common.h"
 #include "step_kernels.h"
+#include "wct280.h"
 #include "wline.h"
 
 namespace fcsg {
@@ -226,6 +227,181 @@ void launch_w280_variant(const FcLinesArgs& a, cudaStream_t s) {
     w280_lines_kernel<RPW, WPC><<<grid, WPC * 32, smem, s>>>(a);
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// FC line batch, register-resident 8 x 35 transform (wct280.h): eight real
+// lines (four complex) per warp, rows only (stride 1 in and out: lane (c, r)
+// reads and writes positions r + 8 t of its lines straight from and to
+// global memory). Three warp phases separated by __syncwarp: P1 loads,
+// continuation, DFT-35 -> shared memory; P2 the 140 DFT-8 groups with the
+// multiplier; P3 shared memory -> inverse DFT-35 -> stores.
+
+FCSG_HD void wct_load(int lane, long unit, const FcLinesArgs& a, double2 (&z)[wct::kT]) {
+    using namespace wct;
+    const int c = lane >> 3, r = lane & 7;
+    const long l0 = 8 * unit + 2 * c;
+    const bool h0 = l0 < a.n_lines, h1 = l0 + 1 < a.n_lines;
+    const double* p0 = a.in + l0 * a.line_stride + r;
+    const double* p1 = p0 + a.line_stride;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) z[t] = mk2(h0 ? ldg1(p0 + 8 * t) : 0.0, h1 ? ldg1(p1 + 8 * t) : 0.0);
+}
+
+FCSG_HD void wct_p1(int lane, long unit, const FcLinesArgs& a, double2 (&z)[wct::kT], double2* buf,
+                    const double* blend) {
+    using namespace wct;
+    const int c = lane >> 3, r = lane & 7;
+    double2 fr[kD1], fl[kD1];
+#if FCSG_CUDA
+    (void)unit;
+    (void)a;
+    // f[253 + i] sits in lane 5 + i of the line's lane group (t = 31),
+    // f[2 - i] in lane 2 - i (t = 0)
+    const int g = lane & ~7;
+#pragma unroll
+    for (int i = 0; i < kD1; ++i) {
+        fr[i] = mk2(__shfl_sync(0xffffffffu, z[31].x, g + 5 + i), __shfl_sync(0xffffffffu, z[31].y, g + 5 + i));
+        fl[i] = mk2(__shfl_sync(0xffffffffu, z[0].x, g + 2 - i), __shfl_sync(0xffffffffu, z[0].y, g + 2 - i));
+    }
+#else
+    const long l0 = 8 * unit + 2 * c;
+    const bool h0 = l0 < a.n_lines, h1 = l0 + 1 < a.n_lines;
+    const double* q0 = a.in + l0 * a.line_stride;
+    const double* q1 = q0 + a.line_stride;
+    for (int i = 0; i < kD1; ++i) {
+        fr[i] = mk2(h0 ? q0[kN - kD1 + i] : 0.0, h1 ? q1[kN - kD1 + i] : 0.0);
+        fl[i] = mk2(h0 ? q0[kD1 - 1 - i] : 0.0, h1 ? q1[kD1 - 1 - i] : 0.0);
+    }
+#endif
+    continuation(r, z, fr, fl, blend);
+    dft35<false>(z);
+    put35(buf, c, r, z);
+}
+
+FCSG_HD void wct_p3(int lane, long unit, const FcLinesArgs& a, const double2* buf) {
+    using namespace wct;
+    const int c = lane >> 3, r = lane & 7;
+    const long l0 = 8 * unit + 2 * c;
+    const bool h0 = l0 < a.n_lines, h1 = l0 + 1 < a.n_lines;
+    double2 z[kT];
+    get35(buf, c, r, z);
+    dft35<true>(z);
+    double* q0 = a.out + l0 * a.out_line_stride + r;
+    double* q1 = q0 + a.out_line_stride;
+    const double s = a.scale;
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+        if (h0) q0[8 * t] = z[t].x * s;
+        if (h1) q1[8 * t] = z[t].y * s;
+    }
+}
+
+#if FCSG_CUDA
+// programmatic dependent launch: the kernel is launched with the
+// programmatic-stream-serialization attribute, so its CTAs may start while
+// the previous kernel of the stream finishes; everything before
+// griddepcontrol.wait reads only the operator tables (written once at
+// operator creation, never by a kernel), everything after it sees the
+// previous kernel's results
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32) wct_lines_kernel(const __grid_constant__ FcLinesArgs a) {
+    extern __shared__ double2 wsm[];
+    double2* tabs = wsm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* buf = wsm + wct::kTabSlots + warp * wct::kBufSlots;
+    const long nunits = (a.n_lines + 7) / 8;
+    const double* blend = reinterpret_cast<const double*>(tabs + wct::kNE + wct::kTwSlots);
+    const long stride = static_cast<long>(gridDim.x) * WPC;
+    long unit = static_cast<long>(blockIdx.x) * WPC + warp;
+    double2 z[wct::kT];
+    {
+        wct::TableRegs<WPC * 32> tr;
+        tr.load(threadIdx.x, a.pl.mult_pfa + (a.mode - 1) * wct::kNE, a.pl.tw, a.pl.blend);
+        griddep_wait();
+        if (unit < nunits) wct_load(lane, unit, a, z);
+        griddep_launch_dependents();
+        tr.store(threadIdx.x, tabs);
+    }
+    __syncthreads();
+    // the first unit peeled (its loads were issued above, before the table
+    // stores); later units (batches beyond one wave) load at the top
+    auto body = [&](long u) {
+        wct_p1(lane, u, a, z, buf, blend);
+        __syncwarp();
+        wct::middle<32>(lane, buf, tabs + wct::kNE, tabs);
+        __syncwarp();
+        wct_p3(lane, u, a, buf);
+        __syncwarp();
+    };
+    if (unit < nunits) body(unit);
+    for (unit += stride; unit < nunits; unit += stride) {
+        wct_load(lane, unit, a, z);
+        body(unit);
+    }
+}
+
+template <int WPC>
+void launch_wct_variant(const FcLinesArgs& a, cudaStream_t s, bool pdl) {
+    static unsigned long long done = 0;
+    constexpr size_t smem = (wct::kTabSlots + WPC * wct::kBufSlots) * sizeof(double2);
+    if (dev::first_on_device(&done))
+        cudaFuncSetAttribute(wct_lines_kernel<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const long nunits = (a.n_lines + 7) / 8;
+    const long nblk = (nunits + WPC - 1) / WPC;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<long>(nblk, 148L * 16)));
+    cfg.blockDim = dim3(WPC * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, wct_lines_kernel<WPC>, a);
+}
+#endif
+
+bool wct_lines_applies(const FcLinesArgs& a) {
+    return w280_lines_applies(a.pl) && a.stride == 1 && a.out_stride == 1;
+}
+
+void launch_wct_lines(const FcLinesArgs& a, void* stream) {
+    if (a.n_lines == 0) return;
+#if FCSG_CUDA
+    static const int wpc = [] {  // A/B experiments: FCSG_WCT_WPC = warps per CTA
+        const char* v = std::getenv("FCSG_WCT_WPC");
+        return v ? std::atoi(v) : 4;
+    }();
+    static const bool pdl = !std::getenv("FCSG_NO_PDL");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    switch (wpc) {
+        case 2: launch_wct_variant<2>(a, s, pdl); break;
+        case 8: launch_wct_variant<8>(a, s, pdl); break;
+        default: launch_wct_variant<4>(a, s, pdl); break;
+    }
+#else
+    (void)stream;
+    std::vector<double2> tabs(wct::kTabSlots), buf(wct::kBufSlots);
+    wct::stage_tables(0, 1, a.pl.mult_pfa + (a.mode - 1) * wct::kNE, a.pl.tw, a.pl.blend, tabs.data());
+    const double* blend = reinterpret_cast<const double*>(tabs.data() + wct::kNE + wct::kTwSlots);
+    const long nunits = (a.n_lines + 7) / 8;
+    double2 z[wct::kT];
+    for (long unit = 0; unit < nunits; ++unit) {
+        for (int lane = 0; lane < 32; ++lane) {
+            wct_load(lane, unit, a, z);
+            wct_p1(lane, unit, a, z, buf.data(), blend);
+        }
+        for (int lane = 0; lane < 32; ++lane) wct::middle<32>(lane, buf.data(), tabs.data() + wct::kNE, tabs.data());
+        for (int lane = 0; lane < 32; ++lane) wct_p3(lane, unit, a, buf.data());
+    }
+#endif
+}
 
 bool w280_lines_applies(const FcPlanDev& pl) {
     return pl.n_ext == 280 && pl.n == 256 && pl.n_gap == 24 && pl.dp1 == 3 && pl.mult_pfa != nullptr;

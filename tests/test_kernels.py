@@ -72,6 +72,22 @@ def test_fc_config1_full_size(backend):
         assert line_rel_l2(gotc, ref).max() < 1e-11
 
 
+@pytest.mark.parametrize("n_lines", [1, 7, 13, 4093])
+def test_fc_ragged_batches(backend, n_lines):
+    """line counts that leave a warp's line group partly empty (the row
+    kernels take 8 lines per warp, the column kernel 2): rows and columns
+    against the oracle"""
+    kind, ctx = backend
+    if kind == "emu" and n_lines > 100:
+        n_lines = 29
+    _, f, _ = P.fc_lines_config1(n_lines=n_lines, n=256, seed=n_lines)
+    op = fc.FcOperator(ctx, 256)
+    ref = O.get_op(256).derivative(f)
+    assert line_rel_l2(_apply(op, f, 1, device=(kind == "gpu")), ref).max() < 1e-11
+    gotc = _apply(op, np.ascontiguousarray(f.T), 1, axis=0, device=(kind == "gpu")).T
+    assert line_rel_l2(gotc, ref).max() < 1e-11
+
+
 @pytest.mark.parametrize("n_cont,degree,n_ext", [(28, 4, 283), (27, 4, 282)])
 def test_fc_degree4_config1_operator(backend, n_cont, degree, n_ext):
     """config 1's 5-point / C=27 operator (prime and 2*3*47 FFT lengths): oracle
