@@ -338,6 +338,35 @@ def fc_derivative_gbs(ctx, n_cont=25, degree=2):
     return 16.0 * f.size / (ms * 1e-3) / 1e9, ms
 
 
+def fc_derivative_batch_gbs(ctx, copies=64):
+    """The same operator on `copies` config-1 batches in ONE call (262144
+    lines, 512 MiB in and out: beyond L2 by itself): the line kernel in its
+    throughput regime -- config 1 alone is a single wave of 512 warps and is
+    bound by one warp's latency chain, not by HBM. Device time, CUDA events,
+    two rotating buffer pairs."""
+    import torch
+
+    from paper_2506_19370_b200 import fc, problems as P
+
+    op = fc.FcOperator(ctx, 256)
+    _, f, _ = P.fc_lines_config1(n_lines=4096, n=256, seed=1)
+    src = torch.from_numpy(f).cuda().repeat(copies, 1).contiguous()
+    ins = [src, src.clone()]
+    outs = [torch.empty_like(src) for _ in range(2)]
+    for k in range(2):
+        op.apply(ins[k], 1, out=outs[k])
+    torch.cuda.synchronize()
+    reps = 8
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()  # op.apply launches on torch's current stream, where these events are recorded
+    for k in range(reps):
+        op.apply(ins[k % 2], 1, out=outs[k % 2])
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    return 16.0 * src.numel() / (ms * 1e-3) / 1e9, ms, src.shape[0]
+
+
 def config2_rate(ctx, steps=10):
     """BASELINE config 2 (one 512x512 subpatch, seeded quadrants, CFL 0.5) on
     this GPU: device time per superstep (CUDA graph, after warm-up)."""
@@ -563,6 +592,7 @@ def run_fcsg(args):
     traffic, traffic_src = ncu_traffic(dom, npts) if world == 1 else (None, None)
     fc_gbs, fc_ms = fc_derivative_gbs(ctx)
     fc4_gbs, fc4_ms = fc_derivative_gbs(ctx, n_cont=27, degree=4)
+    fcb_gbs, fcb_ms, fcb_lines = fc_derivative_batch_gbs(ctx)
     cfg2 = config2_rate(ctx) if world == 1 else None
     cfg3 = config3_rate(ctx) if world == 1 else None
     cfg4 = config4_rate(ctx) if world == 1 else None
@@ -625,6 +655,10 @@ def run_fcsg(args):
         "fc_derivative": {"config": "config1: 4096 lines x N=256, reference operator (degree 2, n_cont=25, "
                                     "n_ext=280), d/dx, HBM->HBM",
                           "gbs": fc_gbs, "us_per_call": fc_ms * 1e3, "frac_of_hbm": fc_gbs / hbm},
+        "fc_derivative_batch": {"config": f"{fcb_lines} lines x N=256 in one call (64 config-1 batches, 512 MiB in + "
+                                          "512 MiB out), reference operator, d/dx, HBM->HBM: the line kernel's "
+                                          "throughput regime",
+                                "gbs": fcb_gbs, "us_per_call": fcb_ms * 1e3, "frac_of_hbm": fcb_gbs / hbm},
         "fc_derivative_config1_operator": {"config": "config1 as BASELINE states it: 4096 lines x N=256, Gram degree "
                                                      "4, d=5, C=27 (n_ext=282=2x3x47), d/dx, HBM->HBM",
                                            "gbs": fc4_gbs, "us_per_call": fc4_ms * 1e3, "frac_of_hbm": fc4_gbs / hbm},

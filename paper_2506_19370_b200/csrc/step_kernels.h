@@ -186,6 +186,10 @@ int step_scr_cap(const FcPlanDev& pl);
 // transform (wpass.cu): rows = pass X, else pass Y (stage = RK stage)
 bool wpass_applies(const EngineDev& E, const FcPlanDev& pl, bool rows);
 void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage, void* stream);
+// the same passes on the register-resident 8 x 35 transform (wctpass.cu;
+// FCSG_WPASS_CT=1 -- an A/B variant, measured slower than the prime-factor
+// kernels of wpass.cu, which stay the default)
+void launch_wctpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage, void* stream);
 // the phase-2 per-step filter (steady steps) on the same transform: rows
 // (e -> tF) or columns (tF -> e)
 void launch_wfilter(const EngineDev& E, const FcPlanDev& pl, bool rows, void* stream);

@@ -25,6 +25,7 @@
 #include "step_kernels.h"
 #include "wct280.h"
 #include "wline.h"
+#include "wpass_common.h"
 
 namespace fcsg {
 
@@ -33,86 +34,6 @@ constexpr int kWarps = 8;  // warps per CTA
 constexpr int kWThreads = kWarps * 32;
 }  // namespace
 
-// conservative -> primitive as prim_of (src/euler.cpp:29-41) with one
-// reciprocal of the density instead of four divisions per point (the
-// products differ from the quotients by an ulp, far inside the parity gates)
-// 1/x without the IEEE division's special-case branch: the SFU's approximate
-// reciprocal (rcp.approx.ftz.f64, ~2^-23 relative) refined by three Newton
-// steps (~2^-52: an ulp). x is a positive, finite density here (a
-// nonpositive or non-finite one is reported by the positivity check
-// regardless of its reciprocal).
-FCSG_HD double recip(double x) {
-#if FCSG_CUDA && !defined(FCSG_EXACT_DIV)
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    r = fma(r, fma(-x, r, 1.0), r);
-    r = fma(r, fma(-x, r, 1.0), r);
-    return fma(r, fma(-x, r, 1.0), r);
-#else
-    return 1.0 / x;
-#endif
-}
-struct PrimR {
-    double rho, mx, my, E, ir, theta, p;
-};
-FCSG_HD PrimR prim_r(double rho, double mx, double my, double E) {
-    PrimR q;
-    q.rho = rho;
-    q.mx = mx;
-    q.my = my;
-    q.E = E;
-    q.ir = recip((rho != 0.0) ? rho : 1e-300);
-    const double pr = kGm1 * (E - 0.5 * (mx * mx + my * my) * q.ir);
-    q.theta = pr * q.ir;
-    q.p = rho * q.theta;
-    return q;
-}
-// x-flux F_c and y-flux G_c (src/euler.cpp:44-55, 64-75)
-FCSG_HD double flux_x(const PrimR& q, int c) {
-    const double u = q.mx * q.ir;
-    switch (c) {
-        case 0: return q.mx;
-        case 1: return q.mx * u + q.p;
-        case 2: return q.my * u;
-        default: return u * (q.E + q.p);
-    }
-}
-FCSG_HD double flux_y(const PrimR& q, int c) {
-    const double v = q.my * q.ir;
-    switch (c) {
-        case 0: return q.my;
-        case 1: return q.mx * v;
-        case 2: return q.my * v + q.p;
-        default: return v * (q.E + q.p);
-    }
-}
-
-// L2 prefetch of one 32-byte sector (the epilogue inputs of the next round,
-// issued before the transform so their DRAM latency hides behind it)
-FCSG_HD void pf_l2(const double* p) {
-#if FCSG_CUDA
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-#else
-    (void)p;
-#endif
-}
-// L2 prefetch of a contiguous range (bytes a multiple of 16). The bulk
-// prefetch needs a 16-byte aligned start; a group view's fields start at the
-// group's first point, which is only 8-byte aligned after a group with an odd
-// number of points -- then the range is prefetched from its first aligned byte.
-FCSG_HD void pf_l2_bulk(const double* p, unsigned bytes) {
-#if FCSG_CUDA
-    const unsigned long long a = reinterpret_cast<unsigned long long>(p);
-    if (a & 15) {
-        p += 1;
-        bytes -= 16;
-    }
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-#else
-    (void)p;
-    (void)bytes;
-#endif
-}
 
 // the operator tables a CTA keeps in shared memory: the multiplier (280
 // double2, prime-factor order), the 24 x 3 blend matrix and the slot of each
@@ -452,13 +373,6 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream) {
 // buffers over the banks (309 and 311, which would fit a fifth CTA per SM,
 // measured 5-9% slower passes at either 4 or 5 CTAs)
 constexpr int kBP = w280::kSlots + 1;
-
-// interior positivity diagnostic of euler_rhs (src/euler.cpp:37-39)
-FCSG_HD void w_check_positive(const EngineDev& E, double rho, double theta, long p, int sub, int i, int j) {
-    const double pr = theta * ((rho != 0.0) ? rho : 1e-300);
-    if ((!(rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) && E.mask[p] == 1)
-        raise_error(E.sc, 1, E.sub_base + sub, i, j);
-}
 
 // Pass X (rows, second pass of the stage): D1 (rho, rho u) and D1 (rho v,
 // theta) -> Phi_x = mu iq1x D1 w - F_c -> D1 Phi_x -> rhs_c = tA_c + iq1x
@@ -895,6 +809,19 @@ bool wpass_applies(const EngineDev& E, const FcPlanDev& pl, bool rows) {
 void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage, void* stream) {
     const int nlines = E.S * (rows ? E.nj : E.ni);
     if (nlines == 0) return;
+    // A/B: FCSG_WPASS_CT=1 runs the passes on the register-resident 8 x 35
+    // transform (wctpass.cu). Measured slower on the B200 (config 5: pass Y
+    // 0.38 ms, pass X 0.39 ms against 0.22 / 0.21 ms here): 35 complex values
+    // per lane leave 8 warps per SM, too few to cover the FP64 dependency
+    // chains -- so the prime-factor kernels stay the default.
+    static const bool ct = [] {
+        const char* v = std::getenv("FCSG_WPASS_CT");
+        return v && v[0] == '1';
+    }();
+    if (ct) {
+        launch_wctpass(E, pl, rows, stage, stream);
+        return;
+    }
     const double2* mult = pl.mult_pfa;  // mode 1: d/dq
     const int nquads = E.S * ((E.ni + kQuad - 1) / kQuad);
 #if FCSG_CUDA

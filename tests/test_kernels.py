@@ -355,3 +355,43 @@ def test_superstep_small_compile_time_plans(backend, n0, n_ext, general):
     OE.step()
     assert E.run(2) == 2
     _compare_engines(E, OE, 1)
+
+
+_CT_SCRIPT = """
+import os, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from paper_2506_19370_b200 import _native as N, engine as EN, problems as P
+ctx = N.Context(emulate=True) if {emu} else N.Context(0)
+dec, ic, _ = P.vortex_tiles(r=2, s=1)
+E = EN.Engine(ctx, dec, ic, EN.EngineConfig(cfl=0.5))
+assert E.run(2, use_graph=False) == 2
+np.savez({out!r}, *[E.get_state(k) for k in range(len(dec.subs))])
+"""
+
+
+@pytest.mark.parametrize("kind", [pytest.param("emu", id="emu"), pytest.param("gpu", id="gpu", marks=pytest.mark.gpu)])
+def test_register_resident_passes_match_default(kind, tmp_path):
+    """The Cartesian flux passes on the register-resident 8 x 35 transform
+    (wctpass.cu, FCSG_WPASS_CT=1: an A/B variant read once per process, hence
+    the subprocesses) against the default prime-factor passes: two 256 x 256
+    vortex tiles, 2 supersteps (all five stage classes of the update)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if kind == "emu":
+        from paper_2506_19370_b200 import build
+        build.build(emulate=True)
+    states = {}
+    for ct in ("0", "1"):
+        out = str(tmp_path / f"ct{ct}.npz")
+        env = dict(os.environ, FCSG_WPASS_CT=ct)
+        r = subprocess.run([sys.executable, "-c", _CT_SCRIPT.format(root=root, emu=(kind == "emu"), out=out)],
+                           env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        z = np.load(out)
+        states[ct] = [z[k] for k in z.files]
+    for a, b in zip(states["0"], states["1"]):
+        assert rel_err(b, a) < 1e-13
