@@ -34,6 +34,23 @@ constexpr int kWarps = 8;  // warps per CTA
 constexpr int kWThreads = kWarps * 32;
 }  // namespace
 
+// tuning knobs of the passes (A/B variant builds: scripts/build_variant.sh)
+#ifndef FCSG_X_MINB
+#define FCSG_X_MINB 5  // pass X: CTAs per SM the register budget is sized for
+#endif
+#ifndef FCSG_Y_MINB
+#define FCSG_Y_MINB 5
+#endif
+#ifndef FCSG_X_KC
+#define FCSG_X_KC 1  // pass X update epilogue: points per load chunk
+#endif
+#ifndef FCSG_X_KL
+#define FCSG_X_KL 4  // pass X other phases: points per load chunk
+#endif
+#ifndef FCSG_Y_KC
+#define FCSG_Y_KC 4  // pass Y: points per load chunk
+#endif
+
 
 // the operator tables a CTA keeps in shared memory: the multiplier (280
 // double2, prime-factor order), the 24 x 3 blend matrix and the slot of each
@@ -259,9 +276,24 @@ __global__ void __launch_bounds__(WPC * 32) wct_lines_kernel(const __grid_consta
         wct_p3(lane, u, a, buf);
         __syncwarp();
     };
-    if (unit < nunits) body(unit);
+    // batches beyond one wave: the next unit's eight rows into L2 (one bulk
+    // prefetch of 2 KB per real line, by the line pair's first lane) while
+    // this unit is transformed
+    auto prefetch_next = [&](long u) {
+        const long nxt = u + stride;
+        if (nxt < nunits && (lane & 7) == 0) {
+            const long l0 = 8 * nxt + 2 * (lane >> 3);
+            if (l0 < a.n_lines) pf_l2_bulk(a.in + l0 * a.line_stride, wct::kN * sizeof(double));
+            if (l0 + 1 < a.n_lines) pf_l2_bulk(a.in + (l0 + 1) * a.line_stride, wct::kN * sizeof(double));
+        }
+    };
+    if (unit < nunits) {
+        prefetch_next(unit);
+        body(unit);
+    }
     for (unit += stride; unit < nunits; unit += stride) {
         wct_load(lane, unit, a, z);
+        prefetch_next(unit);
         body(unit);
     }
 }
@@ -384,8 +416,8 @@ FCSG_HD void wpass_x_body(int lane, int line, double2* buf, const double2* mult,
                           const double* blend, const unsigned short* st, int stage) {
     using namespace w280;
     constexpr int PPL = kN / NL;
-    constexpr int KC = 1;  // points per load chunk of the update epilogue (13 loads: one point; 2 and 4 measured slower)
-    constexpr int KL = PPL >= 4 ? 4 : 1;  // points per load chunk of the other phases
+    constexpr int KC = PPL >= FCSG_X_KC ? FCSG_X_KC : 1;  // points per load chunk of the update epilogue (13 loads per point)
+    constexpr int KL = PPL >= FCSG_X_KL ? FCSG_X_KL : 1;  // points per load chunk of the other phases
     const int ni = E.ni, nj = E.nj;
     const int sub = line / nj, row = line - sub * nj;
     const long rb = static_cast<long>(sub) * ni * nj + static_cast<long>(row) * ni;
@@ -507,7 +539,7 @@ FCSG_HD void wpass_y_quad(int tid, int quad, double2* bufs, const double2* mult,
                           const double* blend, const unsigned short* st) {
     using namespace w280;
     constexpr int PPT = kQuad * kN / NT;  // points per thread
-    constexpr int KC = PPT >= 4 ? 4 : 1;  // points per load chunk
+    constexpr int KC = PPT >= FCSG_Y_KC ? FCSG_Y_KC : 1;  // points per load chunk
     const int ni = E.ni, nj = E.nj;
     const int qps = (ni + kQuad - 1) / kQuad;
     const int sub = quad / qps, c0 = (quad - sub * qps) * kQuad;
@@ -711,7 +743,7 @@ constexpr size_t kYSmem = (kTabSlots + kQuad * 2 * kBP) * sizeof(double2);
 // Both kernels are persistent (grid = resident CTAs): a CTA stages the
 // operator tables once and walks its work items, prefetching the next
 // item's state into L2 before it starts on the current one.
-__global__ void __launch_bounds__(kXThreads, 5) wpass_x_kernel(const __grid_constant__ EngineDev E,
+__global__ void __launch_bounds__(kXThreads, FCSG_X_MINB) wpass_x_kernel(const __grid_constant__ EngineDev E,
                                                                const double2* __restrict__ mult_src,
                                                                const double* __restrict__ blend_src, int stage) {
     extern __shared__ double2 wsm[];
@@ -734,7 +766,7 @@ __global__ void __launch_bounds__(kXThreads, 5) wpass_x_kernel(const __grid_cons
     }
 }
 
-__global__ void __launch_bounds__(kYThreads, 5) wpass_y_kernel(const __grid_constant__ EngineDev E,
+__global__ void __launch_bounds__(kYThreads, FCSG_Y_MINB) wpass_y_kernel(const __grid_constant__ EngineDev E,
                                                                const double2* __restrict__ mult_src,
                                                                const double* __restrict__ blend_src) {
     extern __shared__ double2 wsm[];
