@@ -636,7 +636,13 @@ def run_fcsg(args):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "alg_bytes_per_launch": alg, "peak_kind": peak_kind,
-                     "alg_bytes_per_point": ALG_BYTES.get(dom), "ms_per_launch": groups[dom]},
+                     "alg_bytes_per_point": ALG_BYTES.get(dom), "ms_per_launch": groups[dom],
+                     # the other kernel groups of the step against the same peak (pass Y and pass X take the
+                     # same time, so which of the two is "dominant" flips with the noise)
+                     "all_groups": {g: {"alg_bytes_per_point": ALG_BYTES[g], "ms_per_launch": groups[g],
+                                        "achieved": ALG_BYTES[g] * npts / (groups[g] * 1e-3) / 1e9,
+                                        "frac": ALG_BYTES[g] * npts / (groups[g] * 1e-3) / 1e9 / hbm}
+                                    for g in ALG_BYTES if ALG_BYTES[g] and groups.get(g, 0) > 1e-3}},
         "roofline_fp64": {
             "note": "the line passes and the classifier are bound by the FP64 pipe and instruction issue, not HBM "
                     "(ncu: FP64 pipe 33-38%, DRAM 11-28% of peak, profiles/README.md); algorithmic flops by "

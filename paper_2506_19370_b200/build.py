@@ -24,7 +24,7 @@ CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 
-CU_SOURCES = ["dev.cu", "fc_lines.cu", "step_kernels.cu", "wpass.cu", "wctpass.cu", "classify_f32.cu"]
+CU_SOURCES = ["dev.cu", "fc_lines.cu", "step_kernels.cu", "wpass.cu", "wctpass.cu", "w20lines.cu", "classify_f32.cu"]
 CPP_SOURCES = ["fc_tables.cpp", "capi.cpp", "engine.cpp", "comm.cpp"]
 
 

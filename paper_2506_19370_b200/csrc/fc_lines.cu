@@ -91,9 +91,21 @@ int fc_lines_scr_cap(const FcPlanDev& pl, int LB) {
     return cap;
 }
 
+constexpr long kW20MaxLines = 0;
+
 void launch_fc_lines(FcLinesArgs a, int LB, void* stream) {
     if (wct_lines_applies(a) && !std::getenv("FCSG_NO_WCT_LINES") && !std::getenv("FCSG_NO_WARP_LINES")) {
-        launch_wct_lines(a, stream);
+        // register-resident transforms: 8 x 35 (eight lines per warp), or
+        // 14 x 20 (four lines per warp, half the registers) with
+        // FCSG_LINES_KERNEL=20 -- an A/B variant, measured slower at every
+        // batch size (config 1: 10.4 against 8.3 us per call; 262144 lines:
+        // 3785 against 4299 GB/s), so kW20MaxLines = 0
+        static const int pick = [] {
+            const char* v = std::getenv("FCSG_LINES_KERNEL");
+            return v ? std::atoi(v) : 0;
+        }();
+        if (pick == 20 || (pick == 0 && a.n_lines <= kW20MaxLines)) launch_w20_lines(a, stream);
+        else launch_wct_lines(a, stream);
         return;
     }
     if (w280_lines_applies(a.pl) && !std::getenv("FCSG_NO_WARP_LINES")) {

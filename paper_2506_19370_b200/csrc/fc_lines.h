@@ -33,5 +33,9 @@ void launch_w280_lines(const FcLinesArgs& a, void* stream);
 // same operator; launch_fc_lines prefers it
 bool wct_lines_applies(const FcLinesArgs& a);
 void launch_wct_lines(const FcLinesArgs& a, void* stream);
+// the same batches on the register-resident 14 x 20 transform (w20lines.cu:
+// four real lines per warp, half the registers): FCSG_LINES_KERNEL=20, an A/B
+// variant (measured slower than the 8 x 35 kernel at every batch size)
+void launch_w20_lines(const FcLinesArgs& a, void* stream);
 
 }  // namespace fcsg

@@ -395,3 +395,43 @@ def test_register_resident_passes_match_default(kind, tmp_path):
         states[ct] = [z[k] for k in z.files]
     for a, b in zip(states["0"], states["1"]):
         assert rel_err(b, a) < 1e-13
+
+
+_W20_SCRIPT = """
+import os, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+from paper_2506_19370_b200 import _native as N, fc, problems as P
+ctx = N.Context(emulate=True) if {emu} else N.Context(0)
+op = fc.FcOperator(ctx, 256)
+_, f, _ = P.fc_lines_config1(n_lines=37, n=256, seed=5)
+np.savez({out!r}, *[op.apply(f, mode) for mode in (1, 2, 3, 4)])
+"""
+
+
+@pytest.mark.parametrize("kind", [pytest.param("emu", id="emu"), pytest.param("gpu", id="gpu", marks=pytest.mark.gpu)])
+def test_line_kernel_variants_agree(kind, tmp_path):
+    """The FC line batch on the 14 x 20 register-resident transform
+    (w20lines.cu, FCSG_LINES_KERNEL=20: an A/B variant read once per process,
+    hence the subprocesses) against the default 8 x 35 kernel: a ragged batch
+    of 37 lines, all four multiplier modes."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if kind == "emu":
+        from paper_2506_19370_b200 import build
+        build.build(emulate=True)
+    res = {}
+    for k in ("35", "20"):
+        out = str(tmp_path / f"k{k}.npz")
+        env = dict(os.environ, FCSG_LINES_KERNEL=k)
+        r = subprocess.run([sys.executable, "-c", _W20_SCRIPT.format(root=root, emu=(kind == "emu"), out=out)],
+                           env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        z = np.load(out)
+        res[k] = [z[n] for n in z.files]
+    # two factorisations of the same DFT: round-off apart (the derivative amplifies it by ~N)
+    for a, b in zip(res["35"], res["20"]):
+        assert rel_err(b, a) < 1e-11
