@@ -298,6 +298,155 @@ __global__ void __launch_bounds__(WPC * 32) wct_lines_kernel(const __grid_consta
     }
 }
 
+// ---------------------------------------------------------------------------
+// The same kernel with the rows staged by the TMA unit (FCSG_LINES_TMA=1, an
+// A/B variant): one lane arms the warp's mbarrier with the byte count and
+// issues one 2 KB bulk copy per real line (cp.async.bulk global -> shared,
+// SASS UBLKCP) into the warp's transform buffer -- which is free until the
+// DFT-35 results are stored -- in natural order with a row pitch of 2080 bytes
+// (lane groups of consecutive complex lines land on the two halves of the
+// bank row); the lanes read their positions r + 8 t from shared memory. The
+// results go back the same way: registers -> rows in shared memory ->
+// fence.proxy.async -> one bulk store per line. 64 LDG + 64 STG per lane
+// become 16 bulk copies per warp and 64 LDS + 64 STS per lane. Needs 16-byte
+// aligned rows (base pointers and even line strides), else the direct kernel.
+constexpr int kTmaRowPitch = 2080;  // bytes
+static_assert(8 * kTmaRowPitch <= wct::kBufSlots * 16, "the staged rows fit the transform buffer");
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32) wct_lines_tma_kernel(const __grid_constant__ FcLinesArgs a) {
+    extern __shared__ double2 wsm[];
+    double2* tabs = wsm;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* buf = wsm + wct::kTabSlots + warp * wct::kBufSlots;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + wct::kTabSlots + WPC * wct::kBufSlots) + warp;
+    char* rows = reinterpret_cast<char*>(buf);
+    const long nunits = (a.n_lines + 7) / 8;
+    const double* blend = reinterpret_cast<const double*>(tabs + wct::kNE + wct::kTwSlots);
+    const long stride = static_cast<long>(gridDim.x) * WPC;
+    const int c = lane >> 3, r = lane & 7;
+    constexpr unsigned kRowBytes = wct::kN * sizeof(double);
+    if (lane == 0) mbar_init(bar, 1);
+    __syncwarp();
+    // lane 0: arm the barrier and request the unit's rows
+    auto request = [&](long u) {
+        if (lane == 0) {
+            const long l0 = 8 * u;
+            const int nrows = static_cast<int>(a.n_lines - l0 < 8 ? a.n_lines - l0 : 8);
+            mbar_expect_tx(bar, nrows * kRowBytes);
+            for (int k = 0; k < nrows; ++k)
+                bulk_load(rows + k * kTmaRowPitch, a.in + (l0 + k) * a.line_stride, kRowBytes, bar);
+        }
+    };
+    long unit = static_cast<long>(blockIdx.x) * WPC + warp;
+    {
+        wct::TableRegs<WPC * 32> tr;
+        tr.load(threadIdx.x, a.pl.mult_pfa + (a.mode - 1) * wct::kNE, a.pl.tw, a.pl.blend);
+        griddep_wait();
+        if (unit < nunits) request(unit);
+        griddep_launch_dependents();
+        tr.store(threadIdx.x, tabs);
+    }
+    __syncthreads();
+    unsigned parity = 0;
+    for (; unit < nunits; unit += stride) {
+        const long l0 = 8 * unit + 2 * c;
+        const bool h0 = l0 < a.n_lines, h1 = l0 + 1 < a.n_lines;
+        mbar_wait(bar, parity);
+        parity ^= 1;
+        double2 z[wct::kT];
+        {
+            const double* x0 = reinterpret_cast<const double*>(rows + (2 * c) * kTmaRowPitch) + r;
+            const double* x1 = reinterpret_cast<const double*>(rows + (2 * c + 1) * kTmaRowPitch) + r;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) z[t] = mk2(h0 ? x0[8 * t] : 0.0, h1 ? x1[8 * t] : 0.0);
+        }
+        __syncwarp();  // every lane has read its rows: the buffer may take the DFT-35 results
+        wct_p1(lane, unit, a, z, buf, blend);
+        __syncwarp();
+        wct::middle<32>(lane, buf, tabs + wct::kNE, tabs);
+        __syncwarp();
+        wct::get35(buf, c, r, z);
+        wct::dft35<true>(z);
+        __syncwarp();  // every lane has read the buffer: it may take the result rows
+        {
+            double* y0 = reinterpret_cast<double*>(rows + (2 * c) * kTmaRowPitch) + r;
+            double* y1 = reinterpret_cast<double*>(rows + (2 * c + 1) * kTmaRowPitch) + r;
+            const double sc = a.scale;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) {
+                y0[8 * t] = z[t].x * sc;
+                y1[8 * t] = z[t].y * sc;
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> the bulk store's reads
+        __syncwarp();
+        if (lane == 0) {
+            const long b0 = 8 * unit;
+            const int nrows = static_cast<int>(a.n_lines - b0 < 8 ? a.n_lines - b0 : 8);
+            for (int k = 0; k < nrows; ++k)
+                bulk_store(a.out + (b0 + k) * a.out_line_stride, rows + k * kTmaRowPitch, kRowBytes);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the rows have been read out
+        }
+        __syncwarp();
+        if (unit + stride < nunits) request(unit + stride);
+    }
+}
+
+template <int WPC>
+void launch_wct_tma_variant(const FcLinesArgs& a, cudaStream_t s, bool pdl) {
+    static unsigned long long done = 0;
+    constexpr size_t smem = (wct::kTabSlots + WPC * wct::kBufSlots) * sizeof(double2) + WPC * sizeof(unsigned long long);
+    if (dev::first_on_device(&done))
+        cudaFuncSetAttribute(wct_lines_tma_kernel<WPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const long nunits = (a.n_lines + 7) / 8;
+    const long nblk = (nunits + WPC - 1) / WPC;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<long>(nblk, 148L * 16)));
+    cfg.blockDim = dim3(WPC * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, wct_lines_tma_kernel<WPC>, a);
+}
+
 template <int WPC>
 void launch_wct_variant(const FcLinesArgs& a, cudaStream_t s, bool pdl) {
     static unsigned long long done = 0;
@@ -333,6 +482,22 @@ void launch_wct_lines(const FcLinesArgs& a, void* stream) {
     }();
     static const bool pdl = !std::getenv("FCSG_NO_PDL");
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // A/B: FCSG_LINES_TMA=1 stages the rows with TMA bulk copies (needs 16-byte aligned rows)
+    static const bool tma = [] {
+        const char* v = std::getenv("FCSG_LINES_TMA");
+        return v && v[0] == '1';
+    }();
+    const bool aligned = reinterpret_cast<unsigned long long>(a.in) % 16 == 0 &&
+                         reinterpret_cast<unsigned long long>(a.out) % 16 == 0 && a.line_stride % 2 == 0 &&
+                         a.out_line_stride % 2 == 0;
+    if (tma && aligned) {
+        switch (wpc) {
+            case 2: launch_wct_tma_variant<2>(a, s, pdl); break;
+            case 8: launch_wct_tma_variant<8>(a, s, pdl); break;
+            default: launch_wct_tma_variant<4>(a, s, pdl); break;
+        }
+        return;
+    }
     switch (wpc) {
         case 2: launch_wct_variant<2>(a, s, pdl); break;
         case 8: launch_wct_variant<8>(a, s, pdl); break;

@@ -435,3 +435,28 @@ def test_line_kernel_variants_agree(kind, tmp_path):
     # two factorisations of the same DFT: round-off apart (the derivative amplifies it by ~N)
     for a, b in zip(res["35"], res["20"]):
         assert rel_err(b, a) < 1e-11
+
+
+@pytest.mark.gpu
+def test_line_kernel_tma_staging_bitwise(tmp_path):
+    """The 8 x 35 line kernel with its rows staged by TMA bulk copies
+    (FCSG_LINES_TMA=1, an A/B variant): the same arithmetic on the same
+    values, so bitwise equal to the direct-load kernel (ragged batch of 37
+    lines, all four multiplier modes)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for tma in ("0", "1"):
+        out = str(tmp_path / f"tma{tma}.npz")
+        env = dict(os.environ, FCSG_LINES_TMA=tma)
+        env.pop("FCSG_LINES_KERNEL", None)
+        r = subprocess.run([sys.executable, "-c", _W20_SCRIPT.format(root=root, emu=False, out=out)],
+                           env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        z = np.load(out)
+        res[tma] = [z[n] for n in z.files]
+    for a, b in zip(res["0"], res["1"]):
+        assert np.array_equal(a, b)
