@@ -219,6 +219,11 @@ FCSG_HD void ct_point_prologue(const CtLane& L) {
 #pragma unroll
     for (int t = 0; t < kPtDepth; ++t) ct_point_issue<ROWS>(L, t);
 }
+// points consumed per wait: their dependent chains (reciprocal + Newton steps
+// -> pressure -> fluxes, ~25 FP64 operations deep) interleave; one point at a
+// time left the chain's latency exposed at two warps per scheduler
+constexpr int kPtChunk = 4;
+static_assert(kPtChunk <= kPtDepth && 32 % kPtChunk == 0, "chunk within the ring");
 template <bool ROWS>
 FCSG_HD void ct_point_main(const EngineDev& E, const CtLane& L, int round, double2 (&z)[wct::kT]) {
     const CtLine& g = L.g;
@@ -226,37 +231,50 @@ FCSG_HD void ct_point_main(const EngineDev& E, const CtLane& L, int round, doubl
     const bool uq = E.uniform_q != 0;
     const double* metric = (ROWS ? E.iq1x : E.iq2y) + g.base + L.r * (ROWS ? 1 : g.step);
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-        cp_wait<kPtDepth - 1>();
-        const double* s = L.ring + (t % kPtDepth) * kPtVals * 32;
-        const double v0 = s[0], v1 = s[32], v2 = s[64], v3 = s[96], mu = s[128];
-        const PrimR q = prim_r(v0, v1, v2, v3);
-        double ms, f0, f1;
-        if (round == 0) {
-            if (ROWS && half == 0 && g.ok) {
-                const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
-                if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr)) ct_positivity_fail(E.mask, E.sc, g.base + L.r + 8 * t, E.sub_base + g.sub, L.r + 8 * t, g.idx);
-            }
-            ms = 0.0;
-            f0 = half ? -q.my : -q.rho;
-            f1 = half ? -q.theta : -q.mx;
-        } else {
-            const double a = uq ? g.qc : ldg1(metric + (ROWS ? 8 * t : t * L.step8));
-            ms = mu * (a * g.inv_len);
-            if (ROWS) {  // F = (mx, mx u + p | my u, u (E + p)): the half selects operands, not results
-                const double u = q.mx * q.ir;
-                const double my_u = q.my * u;
-                f0 = half ? my_u : q.mx;
-                f1 = fma(half ? q.E + q.p : q.mx, u, half ? 0.0 : q.p);
-            } else {  // G = (my, mx v | my v + p, v (E + p))
-                const double vv = q.my * q.ir;
-                f0 = half ? fma(q.my, vv, q.p) : q.my;
-                f1 = (half ? q.E + q.p : q.mx) * vv;
-            }
+    for (int t0 = 0; t0 < 32; t0 += kPtChunk) {
+        cp_wait<kPtDepth - kPtChunk>();  // all but the newest D - C groups: points t0 .. t0 + C - 1 have landed
+        double v[kPtChunk][kPtVals], a[kPtChunk];
+#pragma unroll
+        for (int k = 0; k < kPtChunk; ++k) {
+            const double* s = L.ring + ((t0 + k) % kPtDepth) * kPtVals * 32;
+#pragma unroll
+            for (int q = 0; q < kPtVals; ++q) v[k][q] = s[32 * q];
+            a[k] = (uq || round == 0) ? g.qc : ldg1(metric + (ROWS ? 8 * (t0 + k) : (t0 + k) * L.step8));
         }
-        z[t] = mk2(fma(ms, z[t].x, -f0), fma(ms, z[t].y, -f1));
-        if (t + kPtDepth < 32) ct_point_issue<ROWS>(L, t + kPtDepth);
-        else cp_commit();
+#pragma unroll
+        for (int k = 0; k < kPtChunk; ++k) {
+            const int t = t0 + k;
+            const PrimR q = prim_r(v[k][0], v[k][1], v[k][2], v[k][3]);
+            double ms, f0, f1;
+            if (round == 0) {
+                if (ROWS && half == 0 && g.ok) {
+                    const double pr = q.theta * ((q.rho != 0.0) ? q.rho : 1e-300);
+                    if (!(q.rho > 0.0) || !(pr > 0.0) || !finite_d(pr))
+                        ct_positivity_fail(E.mask, E.sc, g.base + L.r + 8 * t, E.sub_base + g.sub, L.r + 8 * t, g.idx);
+                }
+                ms = 0.0;
+                f0 = half ? -q.my : -q.rho;
+                f1 = half ? -q.theta : -q.mx;
+            } else {
+                ms = v[k][4] * (a[k] * g.inv_len);
+                if (ROWS) {  // F = (mx, mx u + p | my u, u (E + p)): the half selects operands, not results
+                    const double u = q.mx * q.ir;
+                    const double my_u = q.my * u;
+                    f0 = half ? my_u : q.mx;
+                    f1 = fma(half ? q.E + q.p : q.mx, u, half ? 0.0 : q.p);
+                } else {  // G = (my, mx v | my v + p, v (E + p))
+                    const double vv = q.my * q.ir;
+                    f0 = half ? fma(q.my, vv, q.p) : q.my;
+                    f1 = (half ? q.E + q.p : q.mx) * vv;
+                }
+            }
+            z[t] = mk2(fma(ms, z[t].x, -f0), fma(ms, z[t].y, -f1));
+        }
+#pragma unroll
+        for (int k = 0; k < kPtChunk; ++k) {
+            if (t0 + k + kPtDepth < 32) ct_point_issue<ROWS>(L, t0 + k + kPtDepth);
+            else cp_commit();
+        }
     }
     cp_wait<0>();
 }
@@ -320,6 +338,7 @@ template <int SC>
 FCSG_HD void ct_update_main(const EngineDev& E, const CtLane& L, const UpdSrc& U, int stage,
                             const double2 (&z)[wct::kT]) {
     constexpr int NV = UpdVals<SC>::kVals, D = UpdVals<SC>::kDepth, PC = UpdVals<SC>::kPerComp;
+    constexpr int C = D >= 8 ? 4 : (D >= 4 ? 2 : 1);  // points per wait (their loads and chains interleave)
     const CtLine& g = L.g;
     const bool uq = E.uniform_q != 0;
     const double dt = E.sc->dt;
@@ -327,26 +346,39 @@ FCSG_HD void ct_update_main(const EngineDev& E, const CtLane& L, const UpdSrc& U
     const double cU = stage == 1 ? SA21 : stage == 2 ? SA32 : stage == 3 ? SA43 : 1.0;
     const double cR = dt * (stage == 0 ? SB0 : stage == 1 ? SB1 : stage == 2 ? SB2 : SB3);
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-        cp_wait<D - 1>();
-        const double* s = L.ring + (t % D) * NV * 32;
-        const double sa = (uq ? g.qc : ldg1(E.iq1x + g.base + L.r + 8 * t)) * g.inv_len;
+    for (int t0 = 0; t0 < 32; t0 += C) {
+        cp_wait<D - C>();
+        double v[C][NV], sa[C];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const double* sk = s + k * PC * 32;
-            const double u = sk[0];
-            const double r = fma(sa, k ? z[t].y : z[t].x, sk[32]);
-            double nu;
-            if (SC == 2) nu = SC2 * sk[64] + SC3 * sk[96] + dt * SD3 * sk[128] + SC4 * u + dt * SD4 * r;
-            else nu = cA * (SC == 1 ? sk[64] : 0.0) + cU * u + cR * r;
-            if (g.ok) {
-                if (U.rhs[k]) U.rhs[k][8 * t] = r;
-                U.e[k][8 * t] = nu;
-                if (SC != 2) U.aux[k][8 * t] = stage == 0 ? u : (stage == 3 ? r : nu);
+        for (int k = 0; k < C; ++k) {
+            const double* s = L.ring + ((t0 + k) % D) * NV * 32;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) v[k][q] = s[32 * q];
+            sa[k] = (uq ? g.qc : ldg1(E.iq1x + g.base + L.r + 8 * (t0 + k))) * g.inv_len;
+        }
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            const int t = t0 + k;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double* sk = v[k] + h * PC;
+                const double u = sk[0];
+                const double r = fma(sa[k], h ? z[t].y : z[t].x, sk[1]);
+                double nu;
+                if (SC == 2) nu = SC2 * sk[2 % PC] + SC3 * sk[3 % PC] + dt * SD3 * sk[4 % PC] + SC4 * u + dt * SD4 * r;
+                else nu = cA * (SC == 1 ? sk[2 % PC] : 0.0) + cU * u + cR * r;
+                if (g.ok) {
+                    if (U.rhs[h]) U.rhs[h][8 * t] = r;
+                    U.e[h][8 * t] = nu;
+                    if (SC != 2) U.aux[h][8 * t] = stage == 0 ? u : (stage == 3 ? r : nu);
+                }
             }
         }
-        if (t + D < 32) ct_update_issue<SC>(L, U, t + D);
-        else cp_commit();
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+            if (t0 + k + D < 32) ct_update_issue<SC>(L, U, t0 + k + D);
+            else cp_commit();
+        }
     }
     cp_wait<0>();
 }

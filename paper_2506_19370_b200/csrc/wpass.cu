@@ -1010,7 +1010,7 @@ void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage,
     if (nlines == 0) return;
     // A/B: FCSG_WPASS_CT=1 runs the passes on the register-resident 8 x 35
     // transform (wctpass.cu). Measured slower on the B200 (config 5: pass Y
-    // 0.38 ms, pass X 0.39 ms against 0.22 / 0.21 ms here): 35 complex values
+    // 0.36 ms, pass X 0.32 ms against 0.22 / 0.21 ms here): 35 complex values
     // per lane leave 8 warps per SM, too few to cover the FP64 dependency
     // chains -- so the prime-factor kernels stay the default.
     static const bool ct = [] {
