@@ -456,7 +456,7 @@ def config4_rate(ctx, steps=20):
     return {"config": "config4: Mach 3 forward-facing step in [0,3]x[0,1] (step 0.2 high at x = 0.6); convex C1 "
                       "corner patch at the step top (L-shaped subpatches), concave C2 corner patch at its foot, an "
                       "S patch along the step top, 2 Cartesian I patches of 256x256 subpatches; inflow rho 1.4, "
-                      "p 1, u 3; CFL 0.5",
+                      f"p 1, u 3; CFL {meta['cfl']} (the reference's value for problems with C1 patches)",
             "points": npts, "subpatches": len(dec.subs), "build_s": build_s, "ms_per_step": ms,
             "value": 5.0 * npts / (ms * 1e-3), "unit": UNIT}
 
