@@ -657,12 +657,16 @@ struct PassXc {
 // (rho v, E) from the first load for the first update, then (rho, rho u)
 // from the last load for the second.
 // slots: 0 iq2y, 1 mu | 1, 2 tA pair (update rounds), 3-4 stash
+#ifndef FCSG_YC_LB
+#define FCSG_YC_LB 4  // lines per CTA of the block-transform pass Y (A/B knob; 2 runs 128-thread CTAs: measured slower)
+#endif
 struct PassYc {
     static constexpr bool kRows = false;
     static constexpr int kRounds = 4;
     static constexpr int kStage = 3;
     static constexpr int kStash = 2;
-    static constexpr int kLB = 4;
+    static constexpr int kLB = FCSG_YC_LB;
+    static constexpr int kNT = FCSG_YC_LB == 2 ? 128 : 256;
     static constexpr bool kScaled = true;
     const EngineDev& E;
     int stage;
@@ -859,6 +863,13 @@ struct PassGB {
     FCSG_HD void finish(Thr, const LineCtx&, int) const {}
 };
 
+// lines per CTA of the phase-2 filter passes (A/B knob): 4 gives a single
+// 512 x 512 subpatch 128 CTAs instead of 64 (config 2: filter 0.175 -> 0.088 ms,
+// superstep 1.17 -> 1.08 ms; 2 lines per CTA the same; configs 3 and 4 unchanged)
+#ifndef FCSG_FILTER_LB
+#define FCSG_FILTER_LB 4
+#endif
+
 // Phase 2 rows: filter (or, at t=0, smear) rho, rho u, rho v, theta
 // (src/runtime.cpp:375-411, subpatch_data.cpp:30-67). Writes tF only.
 struct PassFR {
@@ -866,7 +877,7 @@ struct PassFR {
     static constexpr int kRounds = 2;
     static constexpr int kStage = 0;
     static constexpr int kStash = 0;
-    static constexpr int kLB = 8;
+    static constexpr int kLB = FCSG_FILTER_LB;
     static constexpr bool kScaled = false;
     const EngineDev& E;
     bool smear;
@@ -913,7 +924,7 @@ struct PassFC {
     static constexpr int kRounds = 2;
     static constexpr int kStage = 0;
     static constexpr int kStash = 0;
-    static constexpr int kLB = 8;
+    static constexpr int kLB = FCSG_FILTER_LB;
     static constexpr bool kScaled = false;
     const EngineDev& E;
     bool smear;
