@@ -895,6 +895,14 @@ void Engine::finalize() {
         G_.push_back(std::move(gl));
     }
     E.cartesian = all_cart ? 1 : 0;
+    // several shape groups run their stage passes side by side on the stream
+    // pool: a persistent warp-pass grid that fills every SM would hold the
+    // other groups' CTAs back until it ends (config 4: 4.47 -> 3.99 ms per
+    // superstep with 3 of 4 CTAs per SM; config 3 unchanged; 2 costs config 3 7%)
+    const int cap = groups_.size() > 1 ? kMultiGroupWpassCap : 0;
+    for (GroupLaunch& g : G_) g.E.wpass_cap = cap;
+    for (auto& c : chunks_)
+        for (GroupLaunch& g : c) g.E.wpass_cap = cap;
     finalized_ = true;
 }
 

@@ -224,6 +224,7 @@ class Engine {
     // streams of the RK-stage chunks (enqueue_step)
     static constexpr int kStageStreams = 8;
     static constexpr long kChunkPoints = 1L << 21;
+    static constexpr int kMultiGroupWpassCap = 3;  // CTAs per SM of the persistent warp passes when several shape groups run side by side
     std::vector<void*> cstreams_, cevents_;
     void ensure_streams();
     std::vector<char> wq_set_;

@@ -65,6 +65,8 @@ struct EngineDev {
     int S, ni, nj;
     int sub_base;   // storage slot of the view's first subpatch (error reports)
     int cartesian;  // 1: iq2x == iq1y == 0 at every point of the view
+    int wpass_cap;  // persistent warp passes: CTAs per SM at most (0 = all that fit); engines with several
+                    // shape groups leave room for the other groups' CTAs, which a full persistent grid starves
     int reference_order;  // 1: euler_rhs's own accumulation order (3 passes); 0: flux form
     long npts;      // points of the view (< 2^31)
     FastDiv div_ni, div_sz;  // by ni and by ni * nj (group views)

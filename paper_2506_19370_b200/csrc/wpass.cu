@@ -998,6 +998,14 @@ int resident_ctas(K kernel, int threads, size_t smem, unsigned long long* done, 
     }
     return cache[d & 63];
 }
+// the persistent grid under a view's cap of CTAs per SM
+inline int capped_grid(int resident, int cap) {
+    if (cap <= 0) return resident;
+    int d = 0, sms = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    return std::min(resident, cap * sms);
+}
 #endif
 
 bool wpass_applies(const EngineDev& E, const FcPlanDev& pl, bool rows) {
@@ -1033,10 +1041,10 @@ void launch_wpass(const EngineDev& E, const FcPlanDev& pl, bool rows, int stage,
     }
     if (rows) {
         const int need = (nlines + kXWarps - 1) / kXWarps;
-        const int grid = std::min(need, resident_ctas(wpass_x_kernel, kXThreads, kXSmem, &occ_x, res_x));
+        const int grid = std::min(need, capped_grid(resident_ctas(wpass_x_kernel, kXThreads, kXSmem, &occ_x, res_x), E.wpass_cap));
         wpass_x_kernel<<<grid, kXThreads, kXSmem, s>>>(E, mult, pl.blend, stage);
     } else {
-        const int grid = std::min(nquads, resident_ctas(wpass_y_kernel, kYThreads, kYSmem, &occ_y, res_y));
+        const int grid = std::min(nquads, capped_grid(resident_ctas(wpass_y_kernel, kYThreads, kYSmem, &occ_y, res_y), E.wpass_cap));
         wpass_y_kernel<<<grid, kYThreads, kYSmem, s>>>(E, mult, pl.blend);
     }
 #else
@@ -1067,10 +1075,10 @@ void launch_wfilter(const EngineDev& E, const FcPlanDev& pl, bool rows, void* st
     }
     if (rows) {
         const int need = (nlines + kXWarps - 1) / kXWarps;
-        const int grid = std::min(need, resident_ctas(wfilter_x_kernel, kXThreads, kXSmem, &occ_x, res_x));
+        const int grid = std::min(need, capped_grid(resident_ctas(wfilter_x_kernel, kXThreads, kXSmem, &occ_x, res_x), E.wpass_cap));
         wfilter_x_kernel<<<grid, kXThreads, kXSmem, s>>>(E, mult, pl.blend);
     } else {
-        const int grid = std::min(nquads, resident_ctas(wfilter_y_kernel, kYThreads, kYSmem, &occ_y, res_y));
+        const int grid = std::min(nquads, capped_grid(resident_ctas(wfilter_y_kernel, kYThreads, kYSmem, &occ_y, res_y), E.wpass_cap));
         wfilter_y_kernel<<<grid, kYThreads, kYSmem, s>>>(E, mult, pl.blend);
     }
 #else
