@@ -722,7 +722,12 @@ __device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const d
     for (int ph = 0; ph < 2; ++ph) {
         const double2* src = ph == 0 ? buf : scr;
         double2* dst = ph == 0 ? scr : buf;
-        for (int nt = warp; nt < NTILE; nt += NW) {
+        // work items = (tile of 4 block-lines, chunk of MC m-tiles) over the
+        // warps: with few block-lines (one 139-point line set: a single tile)
+        // the m-tiles are what spreads the product over the CTA
+        constexpr int NMC = (MT + MC - 1) / MC;
+        for (int item = warp; item < NTILE * NMC; item += NW) {
+            const int nt = item / NMC, mt_begin = (item - nt * NMC) * MC;
             const int blB = nt * 4 + (g >> 1);  // B column n = g: block-line, real/imaginary part
             const bool vB = blB < NBL;
             const double* colB =
@@ -735,7 +740,8 @@ __device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const d
             const double2* mb = mult + blk * P;
             // m-tiles in chunks of MC (all at once for P = 47; one at a time
             // for P = 67, whose 5 x 4 accumulators would not fit 80 registers)
-            for (int mt0 = 0; mt0 < MT; mt0 += MC) {
+            {
+                const int mt0 = mt_begin;
                 double aA[MC][2], aB[MC][2];
 #pragma unroll
                 for (int m = 0; m < MC; ++m) aA[m][0] = aA[m][1] = aB[m][0] = aB[m][1] = 0.0;
