@@ -10,3 +10,4 @@ python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; tail -1 gpuru
 python scripts/fc_batch_timing.py > gpurun_out/fc_batch.log 2>&1; cat gpurun_out/fc_batch.log
 bash scripts/prof_r02.sh > gpurun_out/prof_r02.log 2>&1; tail -3 gpurun_out/prof_r02.log
 rm -f gpurun_out/r02_all_details.csv
+timeout 1500 python scripts/config_scale.py gpurun_out/config_scale.json > gpurun_out/config_scale.log 2>&1; cut -c1-200 gpurun_out/config_scale.log | tail -3
