@@ -46,12 +46,27 @@ FCSG_HD double2 ldg2(const double2* p) {
 #endif
 }
 
-// shared-memory slots (double2) for the staged tables of one operator
-FCSG_HD int table_slots(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
+// shared-memory slots (double2) for the staged tables of one operator:
+// twiddles (n_ext), multiplier (n_ext), blend matrix, and -- when the last
+// radix P is a large prime (a direct DFT, on the tensor cores in the
+// compile-time plans) -- the P-th roots of unity packed contiguously: in the
+// n_ext-entry twiddle table they sit n_ext / P entries apart, i.e. a multiple
+// of 128 bytes whenever n_ext / P is a multiple of 8 (536 = 8 x 67): every
+// lane of a fragment load on the same banks
+FCSG_HD int large_prime_radix(const FcPlanDev& pl) {
+    const int p = pl.nstages > 0 ? pl.radix[pl.nstages - 1] : 0;
+    return p >= 17 && p < pl.n_ext ? p : 0;  // a prime n_ext: the twiddle table is the packed table
+}
+FCSG_HD int table_slots(const FcPlanDev& pl) {
+    return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2 + large_prime_radix(pl);
+}
 #if FCSG_CUDA
 __host__
 #endif
-inline int table_slots_host(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
+inline int table_slots_host(const FcPlanDev& pl) {
+    const int p = pl.nstages > 0 ? pl.radix[pl.nstages - 1] : 0;
+    return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2 + (p >= 17 && p < pl.n_ext ? p : 0);
+}
 
 // Copy the twiddles, the multiplier table of `mode` and the blend matrix into
 // shared memory (tab, table_slots() slots) once per CTA, so no stage waits on
@@ -67,6 +82,11 @@ FCSG_HD FcPlanDev stage_tables(Thr t, const FcPlanDev& pl, int mode, double2* ta
     }
     double* sb = reinterpret_cast<double*>(tab + 2 * n);
     for (int k = t.tid; k < pl.n_gap * pl.dp1; k += t.nthr) sb[k] = pl.blend[k];
+    if (const int P = large_prime_radix(pl)) {  // the packed P-th roots (middle_dmma_ct)
+        double2* roots = tab + 2 * n + (pl.n_gap * pl.dp1 + 1) / 2;
+        const int step = n / P;
+        for (int k = t.tid; k < P; k += t.nthr) roots[k] = pl.tw[k * step];
+    }
     FcPlanDev q = pl;
     q.tw = tab;
     q.mult = tab + n - (mode - 1) * n;
@@ -707,9 +727,13 @@ __device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const d
     }
     __syncthreads();
     // cos / sin (2 pi q r / P) of this lane's A fragment (row q = 8 mt + g, column r)
+    // the staged tables' packed P-th roots (stage_tables), not the n_ext-entry
+    // twiddle table: there the roots are pstep entries apart, and pstep = 8
+    // (n_ext = 536) puts every lane's load on one bank group
+    const double2* roots = P < NE ? tw + 2 * NE + (ct_gap(NE) * ct_dp1(NE) + 1) / 2 : tw;
     auto cs = [&](int q, int r, double& c, double& sn) {
         if (q <= H && r <= H) {
-            const double2 w = tw[((q * r) % P) * pstep];  // (cos, -sin)
+            const double2 w = roots[(q * r) % P];  // (cos, -sin)
             c = w.x;
             sn = -w.y;
         } else {
