@@ -45,6 +45,12 @@ int Ctx::get_op(int n, int n_cont, int degree, FilterSpec f) {
         dev::h2d(op->d_mult_pfa, t.mult_pfa.data(), t.mult_pfa.size() * sizeof(double2), stream);
         p.mult_pfa = op->d_mult_pfa;
     }
+    p.prime_frag = nullptr;
+    if (!t.prime_frag.empty()) {
+        op->d_prime_frag = dev::alloc_n<double2>(t.prime_frag.size());
+        dev::h2d(op->d_prime_frag, t.prime_frag.data(), t.prime_frag.size() * sizeof(double2), stream);
+        p.prime_frag = op->d_prime_frag;
+    }
     const int id = static_cast<int>(ops.size());
     ops.push_back(std::move(op));
     op_index[key] = id;

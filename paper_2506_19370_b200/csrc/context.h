@@ -22,7 +22,9 @@ struct DevOp {
     double* d_blend = nullptr;
     double2* d_mult = nullptr;
     double2* d_mult_pfa = nullptr;
+    double2* d_prime_frag = nullptr;
     ~DevOp() {
+        dev::free(d_prime_frag);
         dev::free(d_mult_pfa);
         dev::free(d_tw);
         dev::free(d_blend);

@@ -234,6 +234,24 @@ FcTables build_fc_tables(int n_points, int n_cont, int degree, FilterSpec f) {
                     for (int m = 0; m < 4; ++m) t.mult_pfa[m * n + idx] = t.mult[m * n + pos];
                 }
     }
+    // operand fragments of the tensor-core prime DFT (fft_line.h
+    // middle_dmma_ct): lane (g, t) = (lane / 4, lane % 4) of m-tile mt and
+    // k-step ks holds (cos, sin)(2 pi q r / P), q = 8 mt + g, r = 1 + 4 ks + t,
+    // zero outside q, r <= (P - 1) / 2 -- the values of the twiddle table, so
+    // that the kernel neither reduces q r mod P nor gathers from it
+    if (!t.radix.empty() && t.radix.back() >= 17) {
+        const int P = t.radix.back(), H = (P - 1) / 2, pstep = n / P;
+        const int MT = (H + 1 + 7) / 8, KS = (H + 3) / 4;
+        t.prime_frag.assign(static_cast<size_t>(MT) * KS * 32, double2{0.0, 0.0});
+        for (int mt = 0; mt < MT; ++mt)
+            for (int ks = 0; ks < KS; ++ks)
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int q = 8 * mt + (lane >> 2), r = 1 + 4 * ks + (lane & 3);
+                    if (q > H || r > H) continue;
+                    const double2 w = t.tw[static_cast<size_t>((q * r) % P) * pstep];  // (cos, -sin)
+                    t.prime_frag[(static_cast<size_t>(mt) * KS + ks) * 32 + lane] = double2{w.x, -w.y};
+                }
+    }
     return t;
 }
 

@@ -35,6 +35,8 @@ struct FcTables {
     std::vector<double2> tw;             // n_ext
     std::vector<double2> mult;           // 4 x n_ext (d1, d2, filter, smear) in position order
     std::vector<double2> mult_pfa;       // n_ext = 280: 4 x 280 in the (k1, k2, k3) order of wline.h
+    std::vector<double2> prime_frag;     // last radix P >= 17: (cos, sin)(2 pi q r / P) per lane of the DMMA A
+                                         // fragments, [m-tile][k-step][lane] (fft_line.h middle_dmma_ct)
 };
 
 // Blend-to-zero matrix for Gram degree d (d = 2 is the reference's

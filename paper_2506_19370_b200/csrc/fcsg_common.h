@@ -134,6 +134,8 @@ struct FcPlanDev {
     const double2* mult;    // 4 x n_ext multipliers in DIF output order: d1, d2, filter, smear
     const double2* mult_pfa;  // n_ext = 280 only (else null): the same 4 tables in the prime-factor
                               // order (k1, k2, k3) of wline.h, k3 fastest
+    const double2* prime_frag;  // last radix P a large prime (else null): the (cos, sin)(2 pi q r / P) operand
+                                // fragments of the tensor-core DFT, [m-tile][k-step][lane] (fc_tables.cpp)
 };
 
 }  // namespace fcsg

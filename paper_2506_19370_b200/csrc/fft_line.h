@@ -46,27 +46,12 @@ FCSG_HD double2 ldg2(const double2* p) {
 #endif
 }
 
-// shared-memory slots (double2) for the staged tables of one operator:
-// twiddles (n_ext), multiplier (n_ext), blend matrix, and -- when the last
-// radix P is a large prime (a direct DFT, on the tensor cores in the
-// compile-time plans) -- the P-th roots of unity packed contiguously: in the
-// n_ext-entry twiddle table they sit n_ext / P entries apart, i.e. a multiple
-// of 128 bytes whenever n_ext / P is a multiple of 8 (536 = 8 x 67): every
-// lane of a fragment load on the same banks
-FCSG_HD int large_prime_radix(const FcPlanDev& pl) {
-    const int p = pl.nstages > 0 ? pl.radix[pl.nstages - 1] : 0;
-    return p >= 17 && p < pl.n_ext ? p : 0;  // a prime n_ext: the twiddle table is the packed table
-}
-FCSG_HD int table_slots(const FcPlanDev& pl) {
-    return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2 + large_prime_radix(pl);
-}
+// shared-memory slots (double2) for the staged tables of one operator
+FCSG_HD int table_slots(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
 #if FCSG_CUDA
 __host__
 #endif
-inline int table_slots_host(const FcPlanDev& pl) {
-    const int p = pl.nstages > 0 ? pl.radix[pl.nstages - 1] : 0;
-    return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2 + (p >= 17 && p < pl.n_ext ? p : 0);
-}
+inline int table_slots_host(const FcPlanDev& pl) { return 2 * pl.n_ext + (pl.n_gap * pl.dp1 + 1) / 2; }
 
 // Copy the twiddles, the multiplier table of `mode` and the blend matrix into
 // shared memory (tab, table_slots() slots) once per CTA, so no stage waits on
@@ -82,11 +67,6 @@ FCSG_HD FcPlanDev stage_tables(Thr t, const FcPlanDev& pl, int mode, double2* ta
     }
     double* sb = reinterpret_cast<double*>(tab + 2 * n);
     for (int k = t.tid; k < pl.n_gap * pl.dp1; k += t.nthr) sb[k] = pl.blend[k];
-    if (const int P = large_prime_radix(pl)) {  // the packed P-th roots (middle_dmma_ct)
-        double2* roots = tab + 2 * n + (pl.n_gap * pl.dp1 + 1) / 2;
-        const int step = n / P;
-        for (int k = t.tid; k < P; k += t.nthr) roots[k] = pl.tw[k * step];
-    }
     FcPlanDev q = pl;
     q.tw = tab;
     q.mult = tab + n - (mode - 1) * n;
@@ -700,7 +680,8 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // are formed in registers. The inverse is the same product over the sums /
 // differences of the multiplied outputs.
 template <int NE, int LB, int NTHR>
-__device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const double2* mult, double2* scr) {
+__device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const double2* mult, double2* scr,
+                               const double2* frag) {
     constexpr Factors F = factor_stages(NE);
     constexpr int P = F.r[F.n - 1];
     constexpr int H = (P - 1) / 2;
@@ -726,20 +707,16 @@ __device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const d
         xb[(P - r) * LB] = csub(a, b);
     }
     __syncthreads();
-    // cos / sin (2 pi q r / P) of this lane's A fragment (row q = 8 mt + g, column r)
-    // the staged tables' packed P-th roots (stage_tables), not the n_ext-entry
-    // twiddle table: there the roots are pstep entries apart, and pstep = 8
-    // (n_ext = 536) puts every lane's load on one bank group
-    const double2* roots = P < NE ? tw + 2 * NE + (ct_gap(NE) * ct_dp1(NE) + 1) / 2 : tw;
-    auto cs = [&](int q, int r, double& c, double& sn) {
-        if (q <= H && r <= H) {
-            const double2 w = roots[(q * r) % P];  // (cos, -sin)
-            c = w.x;
-            sn = -w.y;
-        } else {
-            c = 0.0;
-            sn = 0.0;
-        }
+    // cos / sin (2 pi q r / P) of this lane's A fragment (row q = 8 mt + g,
+    // column r = 1 + 4 ks + t): one 16-byte load per (m-tile, k-step) from the
+    // plan's fragment table (FcPlanDev::prime_frag, L1 / L2 resident; zero
+    // outside q, r <= H) -- reducing q r mod P and gathering the root from the
+    // staged twiddles cost a quarter of the pass's issue slots and most of
+    // its shared-memory bank conflicts
+    auto cs = [&](int mt, int ks, double& c, double& sn) {
+        const double2 w = ldg2(frag + (mt * KS + ks) * 32 + lane);
+        c = w.x;
+        sn = w.y;
     };
     // 2: forward DFT + multiplier; src = buf (s at r, d at P - r), dst = scr
     // 3: inverse; src = scr (S at q, D at P - q), dst = buf
@@ -778,7 +755,7 @@ __device__ void middle_dmma_ct(int tid, double2* buf, const double2* tw, const d
 #pragma unroll
                     for (int m = 0; m < MC; ++m) {
                         double c, sn;
-                        cs(8 * (mt0 + m) + g, r, c, sn);
+                        cs(mt0 + m, ks, c, sn);
                         dmma884(aA[m][0], aA[m][1], c, sv);
                         dmma884(aB[m][0], aB[m][1], sn, dv);
                     }
@@ -823,7 +800,7 @@ FCSG_HD void fc_transform_ct(int tid, double2* buf, const FcPlanDev& pl, int mod
         middle_fused_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE);
     } else {
 #if FCSG_CUDA
-        middle_dmma_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
+        middle_dmma_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr, pl.prime_frag);
 #else
         middle_sym_ct<NE, LB, NTHR>(tid, buf, pl.tw, pl.mult + (mode - 1) * NE, scr);
 #endif
