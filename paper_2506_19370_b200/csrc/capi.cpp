@@ -1,5 +1,6 @@
 // extern "C" boundary (include/fcsg.h). Every entry point catches and maps
 // exceptions to the reference's error kinds; nothing throws across the ABI.
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -94,6 +95,11 @@ int guard(Ctx* c, F&& f) {
 }
 
 int pick_lb(long n_lines, int n_ext) {
+    static const int forced = [] {  // A/B runs: FCSG_FC_LB = complex lines per CTA (4, 5, 6, 8, 16)
+        const char* v = std::getenv("FCSG_FC_LB");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (forced == 4 || forced == 5 || forced == 6 || forced == 8 || forced == 16) return forced;
     // Complex lines per CTA. The compile-time plans (n_ext 280, 536) run three
     // 256-thread CTAs per SM: pick the LB whose grid fills its last wave of
     // 3 x 148 CTAs best (a 1.15-wave grid costs two CTA lifetimes), the

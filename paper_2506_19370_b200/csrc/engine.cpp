@@ -899,7 +899,11 @@ void Engine::finalize() {
     // pool: a persistent warp-pass grid that fills every SM would hold the
     // other groups' CTAs back until it ends (config 4: 4.47 -> 3.99 ms per
     // superstep with 3 of 4 CTAs per SM; config 3 unchanged; 2 costs config 3 7%)
-    const int cap = groups_.size() > 1 ? kMultiGroupWpassCap : 0;
+    static const int cap_env = [] {  // A/B runs: FCSG_WPASS_CAP = CTAs per SM (0 = no cap)
+        const char* v = std::getenv("FCSG_WPASS_CAP");
+        return v ? std::atoi(v) : -1;
+    }();
+    const int cap = groups_.size() > 1 ? (cap_env >= 0 ? cap_env : kMultiGroupWpassCap) : 0;
     for (GroupLaunch& g : G_) g.E.wpass_cap = cap;
     for (auto& c : chunks_)
         for (GroupLaunch& g : c) g.E.wpass_cap = cap;
