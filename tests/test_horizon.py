@@ -150,3 +150,40 @@ def test_config3_positivity_loss_matches_reference(gpu_ctx):
     assert f"patch {ours[1]} subpatch {ours[2]} ({ours[3]},{ours[4]})" in msg, (msg, ours)
     print(f"config3 layout: positivity lost at step {ours[0]}, patch {ours[1]} subpatch {ours[2]} "
           f"({ours[3]},{ours[4]}) in both; reference: {msg}")
+
+
+@pytest.mark.gpu
+def test_config2_200_steps_against_reference(gpu_ctx):
+    """BASELINE config 2's horizon (200 supersteps of the seeded Riemann
+    quadrants, ANN classifier, CFL 0.5) on a 128 x 128 subpatch against the
+    reference's own Engine::run: states within 1e-10 relative L2 per field and
+    tau equal wherever the reference's logit margin exceeds 1e-9, at steps 100
+    and 200. The full 512 x 512 case is scripts/config2_horizon.py (minutes of
+    reference CPU time; profiles/r02_config2_200_steps.log: <= 1e-13, tau
+    identical at every point)."""
+    n = 128
+    dec, ic, meta = PR.riemann_quadrants(n=n, seed=2)
+    p = dec.patches[0]
+    R = ref.RefEngine(p.origin[0], p.origin[1], p.e1[0], p.e2[1], 1, 1, n - 2 * p.nv, p.nv, [5, 5, 5, 5],
+                      cfl=meta["cfl"], workers=THREADS, weight_path=EN.DEFAULT_WEIGHTS)
+    e0 = PR.initial_state(dec, ic, 0)
+    R.set_state(0, e0)
+    R.finish_ic()
+    E = EN.Engine(gpu_ctx, dec, cfg=EN.EngineConfig(cfl=meta["cfl"]), initial_states=[e0])
+    mlp = O.Mlp.load(EN.DEFAULT_WEIGHTS)
+    done = 0
+    for mark in (100, 200):
+        R.run(mark - 1)
+        assert E.run(mark - 1 - done) == mark - 1 - done
+        margin = tau_margins(mlp, R.get_state(0))[1]
+        R.run(mark)
+        assert E.run(1) == 1
+        done = mark
+        assert E.time()[0] == pytest.approx(R.time()[0], rel=1e-12)
+        g, w = E.get_state(0), R.get_state(0)
+        for c in range(4):
+            assert rel_l2(g[c], w[c]) < 1e-10, (mark, c)
+        sure = margin > 1e-9
+        assert sure.mean() > 0.999
+        assert np.array_equal(E.get(0, "tau")[sure], R.get(0, "tau")[sure])
+        assert (R.get(0, "tau") < 4).any()  # the classifier is active: the run is not a smooth one
