@@ -116,6 +116,10 @@ class ClockSampler:
             pynvml.nvmlInit()
             self.nvml = pynvml
             self.h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            # NVML's first queries can take tens of milliseconds -- as long as the
+            # whole timed region: make them here, before the poll thread starts
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
             self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
             return self
@@ -135,12 +139,12 @@ class ClockSampler:
         N = self.nvml
         get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
             N.nvmlDeviceGetCurrentClocksThrottleReasons
-        mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        self._sample = lambda: self.rows.append(
+            (float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)), self.mx,
+             [k for k, b in self.BITS.items() if get_reasons(self.h) & b]))
         while not self.stop.is_set():
             try:
-                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
-                bits = get_reasons(self.h)
-                self.rows.append((float(sm), float(mx), [k for k, b in self.BITS.items() if bits & b]))
+                self._sample()
             except Exception:
                 pass
             self.stop.wait(0.002)
@@ -157,6 +161,11 @@ class ClockSampler:
         self.stop.set()
         if self.nvml is not None:
             self.t.join(timeout=2)
+            if not self.rows:  # the poll thread never ran inside a very short region: one sample at its end
+                try:
+                    self._sample()
+                except Exception:
+                    pass
             try:
                 self.nvml.nvmlShutdown()
             except Exception:
